@@ -1,0 +1,179 @@
+/*
+ * superpipe.h — C ABI of the B200 Superpipeline layer-streaming executor.
+ *
+ * This is the drop-in boundary for the reference's layer-scheduling path. The reference
+ * (pipesim, /root/reference/proj) exposes it as a C++ API; each entry point below names
+ * the reference interface it replaces. The C++ mirror of that API (include/pipesim_b200/,
+ * namespace pipesim) is a thin shim over these calls, so reference callers recompile
+ * unchanged. Plain pointers and sizes only; no CUDA or torch types cross the boundary.
+ *
+ * Conventions
+ *  - Every call returns an sp_status; sp_last_error() gives the message of the last failure
+ *    on that executor. Codes mirror the reference exit taxonomy (experiment.hpp:60-64;
+ *    main.cpp:155-178): 2 = invalid argument (std::invalid_argument), 3 = OOM
+ *    (OomDeadlockError, engine.hpp:27-29), 1 = internal invariant (std::logic_error).
+ *  - One executor per device per thread; calls are synchronous. The executor owns all
+ *    device memory and the pinned host copy of the weights.
+ *  - Tensors are row-major fp32: inputs [n_items][rows][d], weights W[in][out] (d*d) and
+ *    bias b[d] exactly as LayerBlock (model.hpp:14-26).
+ *  - Numerics: SP_NUMERICS_EXACT reproduces the reference bit-for-bit (fp32 SIMT kernels,
+ *    reference summation order). SP_NUMERICS_BF16 runs the layer GEMMs on tcgen05 tensor
+ *    cores (bf16 operands, fp32 accumulate/master weights); results are bit-identical across
+ *    every (k, k') setting and within the documented tolerance of the reference.
+ *  - There is no CPU path: without a CUDA device every compute call fails with
+ *    SP_ERR_CUDA. CpuOnly (strategy.hpp:13) is rejected with SP_ERR_INVALID.
+ */
+#ifndef SUPERPIPE_H
+#define SUPERPIPE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SP_ABI_VERSION 1
+
+typedef struct sp_exec sp_exec;
+
+typedef enum {
+    SP_OK = 0,
+    SP_ERR_INTERNAL = 1, /* std::logic_error in the reference */
+    SP_ERR_INVALID = 2,  /* std::invalid_argument (shapes, knobs, lr, ...) */
+    SP_ERR_OOM = 3,      /* OomDeadlockError: the plan cannot fit capacity_bytes */
+    SP_ERR_FIDELITY = 4, /* digest mismatch (reserved; mirrors exit code 4) */
+    SP_ERR_CUDA = 5,     /* CUDA runtime/driver failure or no device */
+    SP_ERR_NCCL = 6,     /* NCCL failure (data-parallel gradient reduction) */
+    SP_ERR_STATE = 7     /* call out of order (e.g. layer not registered) */
+} sp_status;
+
+/* StrategyKind (strategy.hpp:13) — same order. */
+typedef enum { SP_STANDARD = 0, SP_CPU_ONLY = 1, SP_NAIVE = 2, SP_SUPERPIPELINE = 3 } sp_strategy;
+/* TransferMode (sim.hpp:15) — same order. */
+typedef enum { SP_SEQUENTIAL = 0, SP_BATCH = 1 } sp_transfer_mode;
+/* Activation (model.hpp:11) — same order. */
+typedef enum { SP_RELU = 0, SP_IDENTITY = 1 } sp_activation;
+typedef enum { SP_NUMERICS_EXACT = 0, SP_NUMERICS_BF16 = 1 } sp_numerics;
+
+/* Executor configuration: LayeredModel shape (model.hpp:28-37) + StrategyConfig
+ * (strategy.hpp:17-25) + ArenaConfig::capacity_bytes (arena.hpp:14-30) +
+ * TrainConfig::checkpointing (engine.hpp:15-24). The arena's bandwidth/latency/rate
+ * fields are simulator inputs and have no GPU counterpart. */
+typedef struct {
+    int32_t n_layers;
+    int32_t d;
+    int32_t strategy;       /* sp_strategy */
+    int32_t k;              /* resident window (Naive, Superpipeline) */
+    int32_t k_prime;        /* prefetch / eviction group (Superpipeline) */
+    int32_t transfer_mode;  /* sp_transfer_mode */
+    int32_t numerics;       /* sp_numerics */
+    int32_t checkpointing;  /* training: offload saved activations with their layer */
+    int32_t device;         /* CUDA ordinal */
+    int32_t trace;          /* 1: record per-op CUDA-event timeline (sp_get_trace) */
+    uint64_t capacity_bytes; /* ledger budget in reference bytes; 0 = unlimited */
+} sp_config;
+
+/* RunSummary (trace.hpp:52-71) + measured device figures. Ledger fields follow the
+ * reference's byte accounting (DeviceArena, arena.hpp:38-111); *_ms fields are measured
+ * with CUDA events on the executor's streams for the last forward/train call. */
+typedef struct {
+    uint64_t peak_bytes;            /* ledger: max weight+activation+gradient bytes */
+    uint64_t peak_weight_bytes;
+    uint64_t peak_activation_bytes;
+    uint64_t peak_gradient_bytes;
+    uint64_t total_gradient_bytes;
+    uint64_t n_transfers_h2d;       /* H2D channel jobs (batch: one per group) */
+    uint64_t n_transfers_d2h;       /* D2H jobs with real bytes (writebacks, offloads) */
+    uint64_t n_evictions;           /* slot releases (the reference counts these as D2H) */
+    uint64_t h2d_bytes;             /* bytes actually copied host->device (weights+acts) */
+    uint64_t d2h_bytes;             /* bytes actually copied device->host */
+    uint64_t hbm_reserved_bytes;    /* measured: device memory held by the executor */
+    uint64_t kernels_launched;      /* executor kernels launched in the last call */
+    double per_item_ms;             /* (last compute end - first compute start) / n_items */
+    double makespan_ms;             /* first op start -> last op end */
+    double stall_ms;                /* compute-stream idle time waiting for residency */
+    double compute_ms;              /* sum of compute-op durations */
+    float loss;                     /* training: MSE loss of the last step */
+    int32_t n_slots;                /* HBM ring slots S = min(k+k', n) for Superpipeline */
+    char digest[17];                /* digest_tensors / digest_train of the last call */
+    char _pad[3];
+} sp_stats;
+
+/* One timeline row (TraceEvent, trace.hpp:20-50); times in ms from the call's start. */
+typedef struct {
+    double t_start, t_end;
+    int32_t kind;      /* 0 Compute, 1 H2D, 2 D2H, 3 Stall (TraceEvent::Kind order) */
+    int32_t item, layer, backward;
+    int32_t first_layer, n_layers_moved;
+    uint64_t weight_bytes, activation_bytes;
+} sp_trace_event;
+
+/* ---- lifecycle --------------------------------------------------------------------- */
+/* Replaces Engine::Engine (engine.cpp:35-49): validates StrategyConfig (strategy.cpp:19-36),
+ * allocates the pinned host weight pool and the HBM slot ring. */
+int sp_create(const sp_config* cfg, sp_exec** out);
+/* Replaces LayerBlock registration (model.hpp:14-26 / build_model, model.cpp:23-52):
+ * copies W[d*d] ([in][out]) and b[d] into executor-owned pinned host memory. */
+int sp_register_layer(sp_exec* ex, int32_t index, const float* W, const float* b,
+                      int32_t activation, int32_t frozen);
+int sp_destroy(sp_exec* ex);
+const char* sp_last_error(const sp_exec* ex);
+int sp_abi_version(void);
+
+/* ---- hot path ---------------------------------------------------------------------- */
+/* Replaces run_inference (engine.hpp:42-43, engine.cpp:552-556): streams the item-major
+ * (item, layer) sequence (strategy.cpp:38-46) through the ring. x, y: host fp32
+ * [n_items][rows][d] (pinned buffers from sp_host_alloc avoid a staging copy). */
+int sp_forward(sp_exec* ex, const float* x, int64_t rows, int32_t n_items, float* y);
+/* Same, with x/y already resident in device memory (fp32). */
+int sp_forward_device(sp_exec* ex, const void* x_dev, int64_t rows, int32_t n_items,
+                      void* y_dev);
+/* Replaces run_train_step (engine.hpp:48-50, engine.cpp:558-563): forward, MSE loss,
+ * reverse backward with SGD (model.cpp:157-184) through the ring; the updated weights are
+ * written back into the pinned host copy. x, target: host fp32 [rows][d]. */
+int sp_train_step(sp_exec* ex, const float* x, const float* target, int64_t rows, float lr,
+                  float* loss);
+int sp_train_step_device(sp_exec* ex, const void* x_dev, const void* target_dev, int64_t rows,
+                         float lr, float* loss);
+/* Reads back a layer's current weights (RunResult::model, engine.hpp:33). */
+int sp_read_layer(sp_exec* ex, int32_t index, float* W, float* b);
+
+/* ---- metrics ----------------------------------------------------------------------- */
+int sp_get_stats(const sp_exec* ex, sp_stats* out);
+/* Copies up to cap events of the last call's measured timeline; *count = total rows. */
+int sp_get_trace(const sp_exec* ex, sp_trace_event* events, int32_t cap, int32_t* count);
+
+/* ---- data parallel ----------------------------------------------------------------- */
+/* Per-layer NCCL all-reduce of dW/db as each layer's backward completes. */
+int sp_nccl_unique_id(uint8_t id[128]);
+int sp_dp_init(sp_exec* ex, const uint8_t id[128], int32_t rank, int32_t world);
+
+/* ---- host utilities ---------------------------------------------------------------- */
+/* Pinned (page-locked, portable) host buffers for callers' inputs/outputs. */
+void* sp_host_alloc(uint64_t bytes);
+void sp_host_free(void* p);
+/* peak_weight_residency (strategy.cpp:48-60) and StrategyConfig::validate
+ * (strategy.cpp:19-36); pure host functions. validate returns SP_OK or SP_ERR_INVALID. */
+uint64_t sp_peak_weight_residency(int32_t strategy, int32_t k, int32_t k_prime,
+                                  int32_t n_layers, uint64_t layer_bytes);
+int sp_validate_strategy(int32_t strategy, int32_t k, int32_t k_prime, int32_t n_layers);
+/* Describes the static op plan the executor would run (policy_step, scheduler.cpp:53-141,
+ * resolved ahead of time) as text, one op per line; returns the needed length. Host-only. */
+int64_t sp_describe_plan(const sp_config* cfg, int32_t n_items, int32_t train, char* buf,
+                         int64_t cap);
+/* Deterministic layer / input generators of the reference (host-only), so callers can
+ * register synthetic models without a second copy: build_model's per-layer splitmix64 stream
+ * (model.cpp:23-52, W[fan_in][fan_out] then b[fan_out], U(+-1/sqrt(fan_in)); fan_in = fan_out
+ * = d for the reference's square block, 0 = d) and make_input (model.cpp:186-191). */
+int sp_build_layer(uint64_t seed, int32_t index, int32_t d, int32_t fan_in, int32_t fan_out,
+                   float* W, float* b);
+void sp_make_input(uint64_t seed, uint64_t tag, int64_t rows, int32_t d, float* out);
+/* digest helpers (engine.cpp:565-581): FNV-1a-64 digests as 16 hex chars + NUL. */
+void sp_digest_tensors(const float* values, int32_t n_items, int64_t rows, int32_t d,
+                       char out[17]);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SUPERPIPE_H */

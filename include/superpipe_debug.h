@@ -1,0 +1,30 @@
+/*
+ * superpipe_debug.h — kernel-level entry points of libsuperpipe.so used by the GPU unit
+ * tests to check the tcgen05 GEMM in isolation against a torch fp32 reference. Not part of
+ * the reference-facing boundary (superpipe.h). Pointers are device pointers; the call is
+ * synchronous on the legacy default stream.
+ */
+#ifndef SUPERPIPE_DEBUG_H
+#define SUPERPIPE_DEBUG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* C[M,N] = A[M,K] B[K,N] with bf16 A/B. a_mn: A stored [K][lda] (M contiguous) instead of
+ * [M][lda]; b_mn: B stored [K][ldb] (N contiguous) instead of [N][ldb]. epilogue: 0 bf16
+ * act(acc+bias), 1 fp32 act(acc+bias), 2 bf16 ReLU-gated by `gate`, 3 fp32 split-K partials
+ * (split s at out + s*M*ldo). Returns 0 or a cudaError_t value. */
+int sp_debug_gemm_bf16(int32_t M, int32_t N, int32_t K, const void* A, int32_t lda, int32_t a_mn,
+                       const void* B, int32_t ldb, int32_t b_mn, int32_t epilogue, void* out,
+                       int32_t ldo, const float* bias, int32_t relu, const void* gate,
+                       int32_t ldg, int32_t splits, int32_t block_n);
+/* Split count the GEMM will use for a given K and requested splits. */
+int32_t sp_debug_effective_splits(int32_t K, int32_t splits);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,254 @@
+// capi.cpp — extern "C" boundary (include/superpipe.h) over the ring executor.
+// Exceptions never cross the ABI: every entry point maps them onto sp_status codes that
+// mirror the reference's exception taxonomy (invalid_argument -> 2, OomDeadlockError -> 3,
+// logic_error -> 1).
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "executor.hpp"
+#include "nccl_dyn.hpp"
+#include "plan.hpp"
+
+struct sp_exec {
+    sp::Executor* impl = nullptr;
+    std::string error;
+};
+
+namespace {
+
+template <typename F>
+int guarded(sp_exec* ex, F&& f) {
+    try {
+        f();
+        if (ex) ex->error.clear();
+        return SP_OK;
+    } catch (const sp::Error& e) {
+        if (ex) ex->error = e.what();
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        if (ex) ex->error = "host allocation failed";
+        return SP_ERR_OOM;
+    } catch (const std::exception& e) {
+        if (ex) ex->error = e.what();
+        return SP_ERR_INTERNAL;
+    }
+}
+
+thread_local std::string g_create_error;
+
+}  // namespace
+
+extern "C" {
+
+int sp_abi_version(void) { return SP_ABI_VERSION; }
+
+int sp_create(const sp_config* cfg, sp_exec** out) {
+    if (!cfg || !out) return SP_ERR_INVALID;
+    *out = nullptr;
+    auto* ex = new (std::nothrow) sp_exec;
+    if (!ex) return SP_ERR_OOM;
+    const int rc = guarded(ex, [&] { ex->impl = new sp::Executor(*cfg); });
+    if (rc != SP_OK) {
+        g_create_error = ex->error;
+        delete ex;
+        return rc;
+    }
+    *out = ex;
+    return SP_OK;
+}
+
+int sp_register_layer(sp_exec* ex, int32_t index, const float* W, const float* b,
+                      int32_t activation, int32_t frozen) {
+    if (!ex) return SP_ERR_INVALID;
+    return guarded(ex, [&] { ex->impl->register_layer(index, W, b, activation, frozen); });
+}
+
+int sp_destroy(sp_exec* ex) {
+    if (!ex) return SP_OK;
+    delete ex->impl;
+    delete ex;
+    return SP_OK;
+}
+
+const char* sp_last_error(const sp_exec* ex) {
+    return ex ? ex->error.c_str() : g_create_error.c_str();
+}
+
+int sp_forward(sp_exec* ex, const float* x, int64_t rows, int32_t n_items, float* y) {
+    if (!ex) return SP_ERR_INVALID;
+    return guarded(ex, [&] { ex->impl->forward(x, rows, n_items, y, false); });
+}
+
+int sp_forward_device(sp_exec* ex, const void* x_dev, int64_t rows, int32_t n_items,
+                      void* y_dev) {
+    if (!ex) return SP_ERR_INVALID;
+    return guarded(ex, [&] {
+        ex->impl->forward(static_cast<const float*>(x_dev), rows, n_items,
+                          static_cast<float*>(y_dev), true);
+    });
+}
+
+int sp_train_step(sp_exec* ex, const float* x, const float* target, int64_t rows, float lr,
+                  float* loss) {
+    if (!ex) return SP_ERR_INVALID;
+    return guarded(ex, [&] {
+        const float l = ex->impl->train_step(x, target, rows, lr, false);
+        if (loss) *loss = l;
+    });
+}
+
+int sp_train_step_device(sp_exec* ex, const void* x_dev, const void* target_dev, int64_t rows,
+                         float lr, float* loss) {
+    if (!ex) return SP_ERR_INVALID;
+    return guarded(ex, [&] {
+        const float l = ex->impl->train_step(static_cast<const float*>(x_dev),
+                                             static_cast<const float*>(target_dev), rows, lr, true);
+        if (loss) *loss = l;
+    });
+}
+
+int sp_read_layer(sp_exec* ex, int32_t index, float* W, float* b) {
+    if (!ex) return SP_ERR_INVALID;
+    return guarded(ex, [&] { ex->impl->read_layer(index, W, b); });
+}
+
+int sp_get_stats(const sp_exec* ex, sp_stats* out) {
+    if (!ex || !out) return SP_ERR_INVALID;
+    *out = ex->impl->stats();
+    return SP_OK;
+}
+
+int sp_get_trace(const sp_exec* ex, sp_trace_event* events, int32_t cap, int32_t* count) {
+    if (!ex || !count) return SP_ERR_INVALID;
+    const auto& tr = ex->impl->trace();
+    *count = static_cast<int32_t>(tr.size());
+    if (events)
+        for (int32_t i = 0; i < cap && i < static_cast<int32_t>(tr.size()); ++i) events[i] = tr[i];
+    return SP_OK;
+}
+
+int sp_nccl_unique_id(uint8_t id[128]) {
+    if (!id) return SP_ERR_INVALID;
+    ncclUniqueId uid;
+    if (!sp::nccl().ok() || sp::nccl().GetUniqueId(&uid) != ncclSuccess) return SP_ERR_NCCL;
+    std::memcpy(id, uid.internal, sizeof(uid.internal));
+    return SP_OK;
+}
+
+int sp_dp_init(sp_exec* ex, const uint8_t id[128], int32_t rank, int32_t world) {
+    if (!ex || !id) return SP_ERR_INVALID;
+    return guarded(ex, [&] { ex->impl->dp_init(id, rank, world); });
+}
+
+void* sp_host_alloc(uint64_t bytes) {
+    void* p = nullptr;
+    if (cudaHostAlloc(&p, bytes ? bytes : 1, cudaHostAllocPortable) != cudaSuccess) return nullptr;
+    return p;
+}
+
+void sp_host_free(void* p) {
+    if (p) cudaFreeHost(p);
+}
+
+uint64_t sp_peak_weight_residency(int32_t strategy, int32_t k, int32_t k_prime,
+                                  int32_t n_layers, uint64_t layer_bytes) {
+    if (!sp::validate_strategy(strategy, k, k_prime, n_layers).empty()) return 0;
+    return sp::peak_weight_residency(strategy, k, k_prime, n_layers, layer_bytes);
+}
+
+int sp_validate_strategy(int32_t strategy, int32_t k, int32_t k_prime, int32_t n_layers) {
+    return sp::validate_strategy(strategy, k, k_prime, n_layers).empty() ? SP_OK : SP_ERR_INVALID;
+}
+
+int64_t sp_describe_plan(const sp_config* cfg, int32_t n_items, int32_t train, char* buf,
+                         int64_t cap) {
+    if (!cfg) return -1;
+    sp::PlanInput in;
+    in.n_layers = cfg->n_layers;
+    in.strategy = cfg->strategy;
+    in.k = cfg->k;
+    in.k_prime = cfg->k_prime;
+    in.transfer_mode = cfg->transfer_mode;
+    in.train = train != 0;
+    in.n_items = n_items;
+    in.checkpointing = cfg->checkpointing != 0;
+    in.layer_bytes = (static_cast<uint64_t>(cfg->d) * cfg->d + cfg->d) * 4;
+    in.act_bytes = static_cast<uint64_t>(cfg->d) * 4;  // one row per item
+    in.capacity = cfg->capacity_bytes;
+    sp::Plan plan = sp::build_plan(in, {});
+    std::string text = plan.error.empty() ? sp::describe_plan(plan) : ("ERROR " + plan.error + "\n");
+    if (buf && cap > 0) {
+        const int64_t n = std::min<int64_t>(cap - 1, static_cast<int64_t>(text.size()));
+        std::memcpy(buf, text.data(), static_cast<size_t>(n));
+        buf[n] = '\0';
+    }
+    return static_cast<int64_t>(text.size()) + 1;
+}
+
+void sp_digest_tensors(const float* values, int32_t n_items, int64_t rows, int32_t d,
+                       char out[17]) {
+    uint64_t h = 0xCBF29CE484222325ull;
+    auto fnv = [&](const void* p, size_t n) {
+        const unsigned char* c = static_cast<const unsigned char*>(p);
+        for (size_t i = 0; i < n; ++i) {
+            h ^= c[i];
+            h *= 0x100000001B3ull;
+        }
+    };
+    const int64_t shape[2] = {rows, d};
+    const size_t count = static_cast<size_t>(rows) * d;
+    for (int32_t t = 0; t < n_items; ++t) {
+        fnv(shape, sizeof(shape));
+        fnv(values + t * count, count * 4);
+    }
+    static const char digits[] = "0123456789abcdef";
+    for (int i = 15; i >= 0; --i) {
+        out[i] = digits[h & 0xF];
+        h >>= 4;
+    }
+    out[16] = '\0';
+}
+
+}  // extern "C"
+
+// ---- kernel-level debug entry points (include/superpipe_debug.h) ----------------------
+#include "../../include/superpipe_debug.h"
+#include "kernels.hpp"
+
+extern "C" int sp_debug_gemm_bf16(int32_t M, int32_t N, int32_t K, const void* A, int32_t lda,
+                                  int32_t a_mn, const void* B, int32_t ldb, int32_t b_mn,
+                                  int32_t epilogue, void* out, int32_t ldo, const float* bias,
+                                  int32_t relu, const void* gate, int32_t ldg, int32_t splits,
+                                  int32_t block_n) {
+    sp::GemmProblem g;
+    g.M = M;
+    g.N = N;
+    g.K = K;
+    g.A = A;
+    g.lda = lda;
+    g.a_mn = a_mn != 0;
+    g.B = B;
+    g.ldb = ldb;
+    g.b_mn = b_mn != 0;
+    g.epilogue = epilogue;
+    g.out = out;
+    g.ldo = ldo;
+    g.bias = bias;
+    g.relu = relu;
+    g.gate = gate;
+    g.ldg = ldg;
+    g.splits = splits;
+    g.split_stride = static_cast<int64_t>(M) * ldo;
+    g.block_n = block_n;
+    cudaError_t e = sp::gemm_bf16(g, 0);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    return static_cast<int>(e);
+}
+
+extern "C" int32_t sp_debug_effective_splits(int32_t K, int32_t splits) {
+    return sp::effective_splits(K, splits);
+}

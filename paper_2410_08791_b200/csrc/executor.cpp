@@ -1,0 +1,731 @@
+// executor.cpp — the B200 layer-streaming ring executor.
+//
+// Replaces the reference Engine (engine.cpp:33-548): instead of a virtual event loop, the
+// static plan (plan.cpp) is enqueued once onto four CUDA streams —
+//   h2d  : pinned host -> HBM slot copies (copy engine 0)
+//   comp : the layer kernels (tcgen05 GEMMs or the exact SIMT kernels), loss
+//   d2h  : updated-weight writeback / activation offload (copy engine 1)
+//   upd  : gradient all-reduce (NCCL, data parallel) + SGD update
+// joined only by CUDA events at the plan's dependency edges, so the copy engines stream
+// layers i+1..i+k over the host link while layer i computes. The DeviceArena ledger is
+// replayed by the planner (reference byte semantics); real HBM use is reported separately.
+#include "executor.hpp"
+
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <thread>
+
+#include "kernels.hpp"
+#include "nccl_dyn.hpp"
+
+namespace sp {
+
+#define CUDA_OK(expr)                                                                      \
+    do {                                                                                   \
+        cudaError_t e_ = (expr);                                                           \
+        if (e_ != cudaSuccess)                                                             \
+            throw Error(SP_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+#define NCCL_OK(expr)                                                                      \
+    do {                                                                                   \
+        ncclResult_t r_ = (expr);                                                          \
+        if (r_ != ncclSuccess)                                                             \
+            throw Error(SP_ERR_NCCL, std::string(#expr) + ": " + nccl().GetErrorString(r_)); \
+    } while (0)
+
+namespace {
+
+size_t round_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+uint16_t bf16_rne(float f) {  // matches __float2bfloat16_rn for all inputs
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    if ((u & 0x7fffffffu) > 0x7f800000u) return static_cast<uint16_t>((u >> 16) | 0x40u);
+    u += 0x7fffu + ((u >> 16) & 1u);
+    return static_cast<uint16_t>(u >> 16);
+}
+
+template <typename F>
+void parallel_for(int n, F&& f) {
+    const int hw = std::max(1u, std::thread::hardware_concurrency());
+    const int nt = std::min(n, std::min(hw, 16));
+    if (nt <= 1) {
+        for (int i = 0; i < n; ++i) f(i);
+        return;
+    }
+    std::vector<std::thread> th;
+    for (int t = 0; t < nt; ++t)
+        th.emplace_back([&, t] {
+            for (int i = t; i < n; i += nt) f(i);
+        });
+    for (auto& x : th) x.join();
+}
+
+}  // namespace
+
+Executor::Executor(const sp_config& cfg) : cfg_(cfg) {
+    n_ = cfg.n_layers;
+    d_ = cfg.d;
+    if (n_ < 1) throw Error(SP_ERR_INVALID, "build_model: n_layers must be >= 1");
+    if (d_ < 1) throw Error(SP_ERR_INVALID, "build_model: d must be >= 1");
+    const std::string v = validate_strategy(cfg.strategy, cfg.k, cfg.k_prime, n_);
+    if (!v.empty()) throw Error(SP_ERR_INVALID, v);
+    if (cfg.strategy == static_cast<int>(Strategy::CpuOnly))
+        throw Error(SP_ERR_INVALID,
+                    "strategy: cpu_only is the reference's host path; the GPU executor has no CPU "
+                    "fallback");
+    if (cfg.numerics != SP_NUMERICS_EXACT && cfg.numerics != SP_NUMERICS_BF16)
+        throw Error(SP_ERR_INVALID, "numerics: unknown mode");
+    if (cfg.transfer_mode != SP_SEQUENTIAL && cfg.transfer_mode != SP_BATCH)
+        throw Error(SP_ERR_INVALID, "transfer_mode: unknown mode");
+    bf16_ = cfg.numerics == SP_NUMERICS_BF16;
+    if (bf16_ && d_ % 64 != 0)
+        throw Error(SP_ERR_INVALID, "bf16 numerics requires d % 64 == 0 (128-byte TMA rows)");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        throw Error(SP_ERR_CUDA, "no CUDA device visible: the executor has no CPU fallback");
+    if (cfg.device < 0 || cfg.device >= ndev) throw Error(SP_ERR_INVALID, "device ordinal out of range");
+    CUDA_OK(cudaSetDevice(cfg.device));
+
+    const size_t dd = static_cast<size_t>(d_) * d_;
+    CUDA_OK(cudaHostAlloc(&host32_, static_cast<size_t>(n_) * (dd + d_) * 4, cudaHostAllocPortable));
+    std::memset(host32_, 0, static_cast<size_t>(n_) * (dd + d_) * 4);
+    if (bf16_) CUDA_OK(cudaHostAlloc(&host16_, static_cast<size_t>(n_) * wire16_bytes(), cudaHostAllocPortable));
+
+    n_slots_ = ring_slots(cfg.strategy, cfg.k, cfg.k_prime, n_);
+    const size_t a_region = round_up(layer_bytes(), 1024);
+    off_w16_ = a_region;
+    slot_bytes_ = bf16_ ? round_up(a_region + wire16_bytes(), 1024) : a_region;
+    CUDA_OK(cudaMalloc(&slots_dev_, static_cast<size_t>(n_slots_) * slot_bytes_));
+    cache_.assign(static_cast<size_t>(n_slots_), SlotCache{});
+    w16_layer_.assign(static_cast<size_t>(n_slots_), -1);
+
+    CUDA_OK(cudaStreamCreateWithFlags(&s_h2d_, cudaStreamNonBlocking));
+    CUDA_OK(cudaStreamCreateWithFlags(&s_comp_, cudaStreamNonBlocking));
+    CUDA_OK(cudaStreamCreateWithFlags(&s_d2h_, cudaStreamNonBlocking));
+    CUDA_OK(cudaStreamCreateWithFlags(&s_upd_, cudaStreamNonBlocking));
+    CUDA_OK(cudaEventCreate(&ev_call0_));
+    CUDA_OK(cudaEventCreateWithFlags(&ev_io_in_, cudaEventDisableTiming));
+    CUDA_OK(cudaEventCreateWithFlags(&ev_io_out_, cudaEventDisableTiming));
+    CUDA_OK(cudaHostAlloc(&loss_host_, 16, cudaHostAllocPortable));
+
+    relu_.assign(static_cast<size_t>(n_), 1);
+    frozen_.assign(static_cast<size_t>(n_), 0);
+    registered_.assign(static_cast<size_t>(n_), 0);
+    host16_stale_.assign(static_cast<size_t>(n_), 1);
+}
+
+Executor::~Executor() {
+    if (s_h2d_) cudaStreamSynchronize(s_h2d_);
+    if (s_comp_) cudaStreamSynchronize(s_comp_);
+    if (s_d2h_) cudaStreamSynchronize(s_d2h_);
+    if (s_upd_) cudaStreamSynchronize(s_upd_);
+    if (comm_ && nccl().ok()) nccl().CommDestroy(comm_);
+    for (void* p : dev_allocs_) cudaFree(p);
+    if (slots_dev_) cudaFree(slots_dev_);
+    for (auto e : ev_done_) cudaEventDestroy(e);
+    for (auto e : ev_start_) cudaEventDestroy(e);
+    if (ev_call0_) cudaEventDestroy(ev_call0_);
+    if (ev_io_in_) cudaEventDestroy(ev_io_in_);
+    if (ev_io_out_) cudaEventDestroy(ev_io_out_);
+    if (host32_) cudaFreeHost(host32_);
+    if (host16_) cudaFreeHost(host16_);
+    if (host_act_) cudaFreeHost(host_act_);
+    if (loss_host_) cudaFreeHost(loss_host_);
+    for (auto s : {s_h2d_, s_comp_, s_d2h_, s_upd_})
+        if (s) cudaStreamDestroy(s);
+}
+
+void Executor::register_layer(int index, const float* W, const float* b, int activation,
+                              int frozen) {
+    if (index < 0 || index >= n_) throw Error(SP_ERR_INVALID, "register_layer: index out of range");
+    if (!W || !b) throw Error(SP_ERR_INVALID, "register_layer: null weight or bias");
+    if (activation != SP_RELU && activation != SP_IDENTITY)
+        throw Error(SP_ERR_INVALID, "register_layer: unknown activation");
+    const size_t dd = static_cast<size_t>(d_) * d_;
+    float* dst = host32_ + static_cast<size_t>(index) * (dd + d_);
+    std::memcpy(dst, W, dd * 4);
+    std::memcpy(dst + dd, b, static_cast<size_t>(d_) * 4);
+    relu_[index] = activation == SP_RELU;
+    frozen_[index] = frozen != 0;
+    registered_[index] = 1;
+    host16_stale_[index] = 1;
+    for (auto& c : cache_)
+        if (c.layer == index) c.valid = false;
+}
+
+void Executor::check_ready() const {
+    for (int i = 0; i < n_; ++i)
+        if (!registered_[i])
+            throw Error(SP_ERR_STATE, "layer " + std::to_string(i) + " was never registered");
+}
+
+void Executor::refresh_host16() {
+    if (!bf16_) return;
+    std::vector<int> todo;
+    for (int i = 0; i < n_; ++i)
+        if (host16_stale_[i]) todo.push_back(i);
+    if (todo.empty()) return;
+    const size_t dd = static_cast<size_t>(d_) * d_;
+    parallel_for(static_cast<int>(todo.size()), [&](int t) {
+        const int L = todo[t];
+        const float* src = host32_ + static_cast<size_t>(L) * (dd + d_);
+        uint8_t* dst = host16_ + static_cast<size_t>(L) * wire16_bytes();
+        uint16_t* w16 = reinterpret_cast<uint16_t*>(dst);
+        for (size_t e = 0; e < dd; ++e) w16[e] = bf16_rne(src[e]);
+        std::memcpy(dst + dd * 2, src + dd, static_cast<size_t>(d_) * 4);
+    });
+    for (int L : todo) host16_stale_[L] = 0;
+}
+
+void Executor::ensure_buffers(int64_t rows, int n_items, bool train, bool device_io) {
+    const bool ckpt = train && cfg_.checkpointing && cfg_.strategy != SP_STANDARD;
+    const bool fits = rows <= cap_rows_ && n_items <= cap_items_ && (!train || cap_train_);
+    if (fits && (!ckpt || host_act_)) return;
+    CUDA_OK(cudaDeviceSynchronize());
+    for (void* p : dev_allocs_) cudaFree(p);
+    dev_allocs_.clear();
+    dev_bytes_ = 0;
+    if (host_act_) {
+        cudaFreeHost(host_act_);
+        host_act_ = nullptr;
+    }
+    const int64_t R = std::max<int64_t>(rows, cap_rows_);
+    const int items = std::max(n_items, cap_items_);
+    const bool tr = train || cap_train_;
+    auto alloc = [&](size_t bytes) -> void* {
+        void* p = nullptr;
+        bytes = round_up(std::max<size_t>(bytes, 256), 1024);
+        CUDA_OK(cudaMalloc(&p, bytes));
+        dev_allocs_.push_back(p);
+        dev_bytes_ += bytes;
+        return p;
+    };
+    const size_t elt = bf16_ ? 2 : 4;
+    const size_t act = static_cast<size_t>(R) * d_;
+    const size_t dd = static_cast<size_t>(d_) * d_;
+    xin_ = static_cast<float*>(alloc(std::max<size_t>(static_cast<size_t>(items), 1) * act * 4));
+    yout_ = static_cast<float*>(alloc(std::max<size_t>(static_cast<size_t>(items), 1) * act * 4));
+    for (auto& p : pp_) p = alloc(act * elt);
+    xconv_ = alloc(act * 2);
+    act_.clear();
+    ba_.clear();
+    if (tr) {
+        tgt_ = static_cast<float*>(alloc(act * 4));
+        for (int l = 0; l < n_; ++l) act_.push_back(alloc(act * elt));
+        for (auto& g : gbuf_) g = alloc(act * elt);
+        dw_bn_ = bf16_ ? choose_block_n(d_) : 0;
+        splits_cap_ = bf16_ ? choose_splits(d_, d_, static_cast<int>(R), dw_bn_) : 1;
+        col_chunks_cap_ = bf16_ ? colsum_chunks(R) : 1;
+        const size_t ws = bf16_ ? static_cast<size_t>(splits_cap_) * dd + static_cast<size_t>(col_chunks_cap_) * d_
+                                : dd + d_;
+        for (auto& g : gws_) g = static_cast<float*>(alloc(ws * 4));
+        grad_red_ = static_cast<float*>(alloc((dd + d_) * 4));
+        loss_parts_ = static_cast<float*>(alloc(4096 * 4));
+        loss_dev_ = static_cast<float*>(alloc(16));
+        if (cfg_.checkpointing && cfg_.strategy != SP_STANDARD) {
+            for (auto& f : fa_) f = alloc(act * elt);
+            for (int s = 0; s < n_slots_; ++s) ba_.push_back(alloc(act * elt));
+            host_act_bytes_ = static_cast<size_t>(n_) * act * elt;
+            CUDA_OK(cudaHostAlloc(&host_act_, host_act_bytes_, cudaHostAllocPortable));
+        }
+    }
+    cap_rows_ = R;
+    cap_items_ = items;
+    cap_train_ = tr;
+    (void)device_io;
+}
+
+Plan Executor::make_plan(bool train, int n_items, int64_t rows, int fmt) {
+    PlanInput in;
+    in.n_layers = n_;
+    in.strategy = cfg_.strategy;
+    in.k = cfg_.k;
+    in.k_prime = cfg_.k_prime;
+    in.transfer_mode = cfg_.transfer_mode;
+    in.train = train;
+    in.n_items = n_items;
+    in.checkpointing = cfg_.checkpointing != 0;
+    in.frozen.assign(frozen_.begin(), frozen_.end());
+    in.layer_bytes = layer_bytes();
+    in.act_bytes = static_cast<uint64_t>(rows) * d_ * 4;
+    in.capacity = cfg_.capacity_bytes;
+    const std::vector<SlotCache> none;
+    Plan plan = build_plan(in, fmt == cache_fmt_ ? cache_ : none);
+    if (!plan.error.empty()) throw Error(plan.oom ? SP_ERR_OOM : SP_ERR_INVALID, plan.error);
+    return plan;
+}
+
+cudaStream_t Executor::stream_of(OpKind k) const {
+    switch (k) {
+        case OpKind::H2D: return s_h2d_;
+        case OpKind::D2H:
+        case OpKind::ActSave: return s_d2h_;
+        case OpKind::Update: return s_upd_;
+        default: return s_comp_;
+    }
+}
+
+void Executor::gemm(const GemmProblem& g, cudaStream_t st) {
+    const cudaError_t e = gemm_bf16(g, st);
+    if (e != cudaSuccess) throw Error(SP_ERR_CUDA, std::string("tcgen05 gemm: ") + cudaGetErrorString(e));
+    ++kernels_;
+}
+
+void Executor::compute_op(const Op& op, bool train, int64_t rows, int fmt) {
+    (void)fmt;
+    const int L = op.layer, s = op.slot;
+    const size_t act = static_cast<size_t>(rows) * d_;
+    const bool ckpt = train && cfg_.checkpointing && cfg_.strategy != SP_STANDARD;
+    cudaStream_t st = s_comp_;
+    auto ensure_w16 = [&] {
+        if (w16_layer_[s] == L) return;
+        convert_f32_to_bf16(slot_w32(s), slot_w16(s), static_cast<int64_t>(d_) * d_, st);
+        ++kernels_;
+        w16_layer_[s] = L;
+    };
+    if (!train) {
+        const float* x_item = cur_x_ + static_cast<size_t>(op.item) * act;
+        float* y_item = cur_y_ + static_cast<size_t>(op.item) * act;
+        const bool last = L == n_ - 1;
+        if (!bf16_) {
+            const float* in = L == 0 ? x_item : static_cast<const float*>(pp_[(L - 1) % 2]);
+            float* out = last ? y_item : static_cast<float*>(pp_[L % 2]);
+            exact_forward(in, slot_w32(s), slot_b32(s), relu_[L], out, rows, d_, st);
+            ++kernels_;
+            return;
+        }
+        if (L == 0) {
+            convert_f32_to_bf16(x_item, xconv_, static_cast<int64_t>(act), st);
+            ++kernels_;
+        }
+        GemmProblem g;
+        g.M = static_cast<int>(rows);
+        g.N = d_;
+        g.K = d_;
+        g.A = L == 0 ? xconv_ : pp_[(L - 1) % 2];
+        g.lda = d_;
+        g.B = slot_w16(s);
+        g.ldb = d_;
+        g.b_mn = true;
+        g.epilogue = last ? EPI_BIAS_ACT_F32 : EPI_BIAS_ACT_BF16;
+        g.out = last ? static_cast<void*>(y_item) : pp_[L % 2];
+        g.ldo = d_;
+        g.bias = slot_b16(s);
+        g.relu = relu_[L];
+        gemm(g, st);
+        return;
+    }
+    if (op.pass == 0) {  // training forward: save x_L, produce x_{L+1}
+        void* xL = ckpt ? fa_[L % 3] : act_[L];
+        const bool last = L == n_ - 1;
+        void* out = last ? static_cast<void*>(yout_) : (ckpt ? fa_[(L + 1) % 3] : act_[L + 1]);
+        if (L == 0) {
+            if (bf16_) {
+                convert_f32_to_bf16(cur_x_, xL, static_cast<int64_t>(act), st);
+                ++kernels_;
+            } else {
+                CUDA_OK(cudaMemcpyAsync(xL, cur_x_, act * 4, cudaMemcpyDeviceToDevice, st));
+            }
+        }
+        if (!bf16_) {
+            exact_forward(static_cast<const float*>(xL), slot_w32(s), slot_b32(s), relu_[L],
+                          static_cast<float*>(out), rows, d_, st);
+            ++kernels_;
+            return;
+        }
+        ensure_w16();
+        GemmProblem g;
+        g.M = static_cast<int>(rows);
+        g.N = d_;
+        g.K = d_;
+        g.A = xL;
+        g.lda = d_;
+        g.B = slot_w16(s);
+        g.ldb = d_;
+        g.b_mn = true;
+        g.epilogue = last ? EPI_BIAS_ACT_F32 : EPI_BIAS_ACT_BF16;
+        g.out = out;
+        g.ldo = d_;
+        g.bias = slot_b32(s);
+        g.relu = relu_[L];
+        gemm(g, st);
+        return;
+    }
+    // backward of layer L: dz_L (gbuf[L%2]) -> dz_{L-1} (gated by layer L-1's ReLU) + dW/db
+    void* dz = gbuf_[L % 2];
+    void* xL = ckpt ? ba_[s] : act_[L];
+    const bool trainable = !frozen_[L];
+    if (L > 0) {
+        void* out = gbuf_[(L - 1) % 2];
+        const bool gate = relu_[L - 1] != 0;
+        if (!bf16_) {
+            exact_backward_dx(static_cast<const float*>(dz), slot_w32(s),
+                              gate ? static_cast<const float*>(xL) : nullptr,
+                              static_cast<float*>(out), rows, d_, st);
+            ++kernels_;
+        } else {
+            ensure_w16();
+            GemmProblem g;
+            g.M = static_cast<int>(rows);
+            g.N = d_;
+            g.K = d_;
+            g.A = dz;
+            g.lda = d_;
+            g.B = slot_w16(s);  // W[i][j] is the K-major B of dx = dz W^T
+            g.ldb = d_;
+            g.epilogue = EPI_GATE_BF16;
+            g.out = out;
+            g.ldo = d_;
+            g.gate = xL;
+            g.ldg = d_;
+            g.relu = gate ? 1 : 0;
+            gemm(g, st);
+        }
+    }
+    if (!trainable) return;
+    float* ws = gws_[L % 2];
+    const size_t dd = static_cast<size_t>(d_) * d_;
+    if (!bf16_) {
+        exact_backward_dw(static_cast<const float*>(xL), static_cast<const float*>(dz), ws,
+                          ws + dd, rows, d_, st);
+        ++kernels_;
+        return;
+    }
+    GemmProblem g;
+    g.M = d_;
+    g.N = d_;
+    g.K = static_cast<int>(rows);
+    g.A = xL;  // x_L [r][i]: the M-major A of dW = x^T dz
+    g.lda = d_;
+    g.a_mn = true;
+    g.B = dz;  // dz [r][j]: N-major B
+    g.ldb = d_;
+    g.b_mn = true;
+    g.epilogue = EPI_F32;
+    g.out = ws;
+    g.ldo = d_;
+    g.splits = splits_;
+    g.split_stride = static_cast<int64_t>(dd);
+    g.block_n = dw_bn_;
+    gemm(g, st);
+    colsum_bf16(dz, rows, d_, ws + static_cast<size_t>(splits_) * dd, st);
+    ++kernels_;
+}
+
+void Executor::loss_op(int64_t rows) {
+    const int64_t count = rows * d_;
+    const float inv_n = 1.0f / static_cast<float>(count * world_);
+    const int last = n_ - 1;
+    void* g = gbuf_[last % 2];
+    if (!bf16_) {
+        exact_loss_grad(yout_, cur_t_, count, inv_n, relu_[last], static_cast<float*>(g), loss_dev_, s_comp_);
+        kernels_ += 2;
+    } else {
+        loss_blocks_ = loss_grad_bf16(yout_, cur_t_, count, inv_n, relu_[last], g, loss_parts_, s_comp_);
+        loss_finalize(loss_parts_, loss_blocks_, loss_dev_, s_comp_);
+        kernels_ += 2;
+    }
+    if (comm_) NCCL_OK(nccl().AllReduce(loss_dev_, loss_dev_, 1, ncclFloat, ncclSum, comm_, s_comp_));
+    CUDA_OK(cudaMemcpyAsync(loss_host_, loss_dev_, 4, cudaMemcpyDeviceToHost, s_comp_));
+}
+
+void Executor::update_op(const Op& op, float lr) {
+    const int L = op.layer, s = op.slot;
+    const size_t dd = static_cast<size_t>(d_) * d_;
+    cudaStream_t st = s_upd_;
+    float* ws = gws_[L % 2];
+    if (!bf16_) {
+        if (comm_) NCCL_OK(nccl().AllReduce(ws, ws, dd + d_, ncclFloat, ncclSum, comm_, st));
+        exact_sgd(slot_w32(s), ws, static_cast<int64_t>(dd + d_), lr, st);  // [W|b] contiguous
+        ++kernels_;
+    } else if (!comm_) {
+        sgd_reduce(slot_w32(s), ws, splits_, static_cast<int64_t>(dd), static_cast<int64_t>(dd), lr, st);
+        sgd_reduce(slot_b32(s), ws + splits_ * dd, col_chunks_, d_, d_, lr, st);
+        kernels_ += 2;
+    } else {
+        reduce_partials(ws, splits_, static_cast<int64_t>(dd), static_cast<int64_t>(dd), grad_red_, st);
+        reduce_partials(ws + splits_ * dd, col_chunks_, d_, d_, grad_red_ + dd, st);
+        NCCL_OK(nccl().AllReduce(grad_red_, grad_red_, dd + d_, ncclFloat, ncclSum, comm_, st));
+        exact_sgd(slot_w32(s), grad_red_, static_cast<int64_t>(dd + d_), lr, st);
+        kernels_ += 3;
+    }
+    w16_layer_[s] = -1;  // the bf16 copy is now stale
+}
+
+void Executor::enqueue_op(const Plan& plan, int i, bool train, int n_items, int64_t rows,
+                          float lr, int fmt) {
+    (void)n_items;
+    const Op& op = plan.ops[static_cast<size_t>(i)];
+    cudaStream_t st = stream_of(op.kind);
+    for (int dep : op.deps) {
+        if (stream_of(plan.ops[static_cast<size_t>(dep)].kind) != st)
+            CUDA_OK(cudaStreamWaitEvent(st, ev_done_[static_cast<size_t>(dep)], 0));
+    }
+    CUDA_OK(cudaEventRecord(ev_start_[static_cast<size_t>(i)], st));
+    const size_t dd = static_cast<size_t>(d_) * d_;
+    const size_t act_b = static_cast<size_t>(rows) * d_ * (bf16_ ? 2 : 4);
+    switch (op.kind) {
+        case OpKind::H2D:
+            for (size_t j = 0; j < op.layers.size(); ++j) {
+                const int L = op.layers[j], s = op.slots[j];
+                if (op.weights[j]) {
+                    if (fmt == kFmtBf16Infer) {
+                        CUDA_OK(cudaMemcpyAsync(slot_ptr(s) + off_w16_,
+                                                host16_ + static_cast<size_t>(L) * wire16_bytes(),
+                                                wire16_bytes(), cudaMemcpyHostToDevice, st));
+                        h2d_bytes_ += wire16_bytes();
+                    } else {
+                        CUDA_OK(cudaMemcpyAsync(slot_ptr(s), host32_ + static_cast<size_t>(L) * (dd + d_),
+                                                layer_bytes(), cudaMemcpyHostToDevice, st));
+                        h2d_bytes_ += layer_bytes();
+                        w16_layer_[s] = -1;
+                    }
+                }
+                if (op.acts[j]) {
+                    CUDA_OK(cudaMemcpyAsync(ba_[s], host_act_ + static_cast<size_t>(L) * act_b, act_b,
+                                            cudaMemcpyHostToDevice, st));
+                    h2d_bytes_ += act_b;
+                }
+            }
+            break;
+        case OpKind::Compute:
+            compute_op(op, train, rows, fmt);
+            break;
+        case OpKind::Loss:
+            loss_op(rows);
+            break;
+        case OpKind::Update:
+            update_op(op, lr);
+            break;
+        case OpKind::D2H: {
+            const int L = op.layers[0], s = op.slots[0];
+            CUDA_OK(cudaMemcpyAsync(host32_ + static_cast<size_t>(L) * (dd + d_), slot_ptr(s),
+                                    layer_bytes(), cudaMemcpyDeviceToHost, st));
+            d2h_bytes_ += layer_bytes();
+            host16_stale_[L] = 1;
+            break;
+        }
+        case OpKind::ActSave:
+            CUDA_OK(cudaMemcpyAsync(host_act_ + static_cast<size_t>(op.layer) * act_b, fa_[op.layer % 3],
+                                    act_b, cudaMemcpyDeviceToHost, st));
+            d2h_bytes_ += act_b;
+            break;
+    }
+    CUDA_OK(cudaEventRecord(ev_done_[static_cast<size_t>(i)], st));
+}
+
+void Executor::run_plan(const Plan& plan, bool train, int n_items, int64_t rows, float lr,
+                        int fmt) {
+    while (ev_done_.size() < plan.ops.size()) {
+        cudaEvent_t a, b;
+        CUDA_OK(cudaEventCreate(&a));
+        CUDA_OK(cudaEventCreate(&b));
+        ev_done_.push_back(a);
+        ev_start_.push_back(b);
+    }
+    int first_compute = -1;
+    for (size_t i = 0; i < plan.ops.size(); ++i)
+        if (plan.ops[i].kind == OpKind::Compute) {
+            first_compute = static_cast<int>(i);
+            break;
+        }
+    (void)first_compute;
+    for (size_t i = 0; i < plan.ops.size(); ++i)
+        enqueue_op(plan, static_cast<int>(i), train, n_items, rows, lr, fmt);
+    cache_ = plan.final_slots;
+    cache_fmt_ = fmt;
+}
+
+void Executor::collect_stats(const Plan& plan, int n_items, bool train) {
+    trace_.clear();
+    double first_c = -1, last_c = 0, makespan = 0, stall = 0, comp = 0, prev_end = -1;
+    for (size_t i = 0; i < plan.ops.size(); ++i) {
+        const Op& op = plan.ops[i];
+        float t0 = 0, t1 = 0;
+        CUDA_OK(cudaEventElapsedTime(&t0, ev_call0_, ev_start_[i]));
+        CUDA_OK(cudaEventElapsedTime(&t1, ev_call0_, ev_done_[i]));
+        makespan = std::max(makespan, static_cast<double>(t1));
+        sp_trace_event ev{};
+        ev.t_start = t0;
+        ev.t_end = t1;
+        ev.item = op.item;
+        ev.layer = op.layer;
+        ev.backward = op.pass == 1;
+        if (op.kind == OpKind::Compute || op.kind == OpKind::Loss) {
+            if (op.kind == OpKind::Compute) {
+                if (first_c < 0) first_c = t0;
+                last_c = std::max(last_c, static_cast<double>(t1));
+                comp += t1 - t0;
+            }
+            if (prev_end >= 0 && t0 > prev_end) {
+                sp_trace_event s{};
+                s.t_start = prev_end;
+                s.t_end = t0;
+                s.kind = 3;
+                s.layer = op.layer;
+                s.backward = op.pass == 1;
+                stall += t0 - prev_end;
+                trace_.push_back(s);
+            }
+            prev_end = t1;
+            if (op.kind == OpKind::Loss) continue;
+            ev.kind = 0;
+        } else if (op.kind == OpKind::H2D || op.kind == OpKind::D2H || op.kind == OpKind::ActSave) {
+            ev.kind = op.kind == OpKind::H2D ? 1 : 2;
+            if (!op.layers.empty()) {
+                ev.first_layer = op.layers[0];
+                ev.n_layers_moved = static_cast<int>(op.layers.size());
+                for (size_t j = 0; j < op.layers.size(); ++j) {
+                    if (op.weights[j]) ev.weight_bytes += layer_bytes();
+                    if (op.acts[j]) ev.activation_bytes += static_cast<uint64_t>(cap_rows_) * d_ * 4;
+                }
+            } else {
+                ev.first_layer = op.layer;
+                ev.n_layers_moved = 0;
+            }
+        } else {
+            continue;
+        }
+        trace_.push_back(ev);
+    }
+    stats_.peak_bytes = plan.ledger.peak_bytes;
+    stats_.peak_weight_bytes = plan.ledger.peak_weight;
+    stats_.peak_activation_bytes = plan.ledger.peak_activation;
+    stats_.peak_gradient_bytes = plan.ledger.peak_gradient;
+    stats_.total_gradient_bytes = plan.ledger.total_gradient;
+    stats_.n_transfers_h2d = plan.n_h2d_jobs;
+    stats_.n_transfers_d2h = plan.n_d2h_jobs + plan.d2h_act_layers;
+    stats_.n_evictions = plan.n_evictions;
+    stats_.h2d_bytes = h2d_bytes_;
+    stats_.d2h_bytes = d2h_bytes_;
+    stats_.hbm_reserved_bytes = static_cast<uint64_t>(n_slots_) * slot_bytes_ + dev_bytes_;
+    stats_.kernels_launched = kernels_;
+    stats_.per_item_ms = first_c >= 0 ? (last_c - first_c) / std::max(1, train ? 1 : n_items) : 0.0;
+    stats_.makespan_ms = makespan;
+    stats_.stall_ms = stall;
+    stats_.compute_ms = comp;
+    stats_.n_slots = plan.n_slots;
+}
+
+void Executor::forward(const float* x, int64_t rows, int n_items, float* y, bool device_io) {
+    if (!x || !y) throw Error(SP_ERR_INVALID, "run_inference: null input or output");
+    if (rows < 1 || n_items < 1) throw Error(SP_ERR_INVALID, "run_inference: no inputs");
+    if (rows > (1ll << 31) - 1) throw Error(SP_ERR_INVALID, "run_inference: too many rows");
+    check_ready();
+    const int fmt = bf16_ ? kFmtBf16Infer : kFmtExactF32;
+    Plan plan = make_plan(false, n_items, rows, fmt);
+    refresh_host16();
+    ensure_buffers(rows, n_items, false, device_io);
+    CUDA_OK(cudaSetDevice(cfg_.device));
+    kernels_ = 0;
+    h2d_bytes_ = d2h_bytes_ = 0;
+    const size_t bytes = static_cast<size_t>(n_items) * rows * d_ * 4;
+    CUDA_OK(cudaEventRecord(ev_call0_, s_h2d_));
+    for (auto s : {s_comp_, s_d2h_, s_upd_}) CUDA_OK(cudaStreamWaitEvent(s, ev_call0_, 0));
+    if (device_io) {
+        cur_x_ = x;
+        cur_y_ = y;
+    } else {
+        CUDA_OK(cudaMemcpyAsync(xin_, x, bytes, cudaMemcpyHostToDevice, s_comp_));
+        cur_x_ = xin_;
+        cur_y_ = yout_;
+    }
+    run_plan(plan, false, n_items, rows, 0.0f, fmt);
+    if (!device_io) {
+        CUDA_OK(cudaEventRecord(ev_io_out_, s_comp_));
+        CUDA_OK(cudaStreamWaitEvent(s_d2h_, ev_io_out_, 0));
+        CUDA_OK(cudaMemcpyAsync(y, yout_, bytes, cudaMemcpyDeviceToHost, s_d2h_));
+    }
+    for (auto s : {s_h2d_, s_comp_, s_d2h_, s_upd_}) CUDA_OK(cudaStreamSynchronize(s));
+    CUDA_OK(cudaGetLastError());
+    collect_stats(plan, n_items, false);
+    stats_.loss = 0.0f;
+    if (!device_io) sp_digest_tensors(y, n_items, rows, d_, stats_.digest);
+    else std::memset(stats_.digest, 0, sizeof(stats_.digest));
+}
+
+float Executor::train_step(const float* x, const float* target, int64_t rows, float lr,
+                           bool device_io) {
+    if (!x || !target) throw Error(SP_ERR_INVALID, "run_train_step: null input or target");
+    if (!(lr > 0.0f)) throw Error(SP_ERR_INVALID, "train: lr must be > 0");
+    if (rows < 1) throw Error(SP_ERR_INVALID, "train: batch_size must be >= 1");
+    check_ready();
+    const int fmt = bf16_ ? kFmtBf16Train : kFmtExactF32;
+    Plan plan = make_plan(true, 1, rows, fmt);
+    ensure_buffers(rows, 1, true, device_io);
+    CUDA_OK(cudaSetDevice(cfg_.device));
+    if (bf16_) {  // split-K depends only on (d, rows): identical for every window setting
+        const int want = choose_splits(d_, d_, static_cast<int>(rows), dw_bn_);
+        splits_ = effective_splits(static_cast<int>(rows), std::min(want, splits_cap_));
+        col_chunks_ = colsum_chunks(rows);
+    }
+    kernels_ = 0;
+    h2d_bytes_ = d2h_bytes_ = 0;
+    const size_t bytes = static_cast<size_t>(rows) * d_ * 4;
+    CUDA_OK(cudaEventRecord(ev_call0_, s_h2d_));
+    for (auto s : {s_comp_, s_d2h_, s_upd_}) CUDA_OK(cudaStreamWaitEvent(s, ev_call0_, 0));
+    if (device_io) {
+        cur_x_ = x;
+        cur_t_ = target;
+    } else {
+        CUDA_OK(cudaMemcpyAsync(xin_, x, bytes, cudaMemcpyHostToDevice, s_comp_));
+        CUDA_OK(cudaMemcpyAsync(tgt_, target, bytes, cudaMemcpyHostToDevice, s_comp_));
+        cur_x_ = xin_;
+        cur_t_ = tgt_;
+    }
+    if (cache_fmt_ != fmt) std::fill(w16_layer_.begin(), w16_layer_.end(), -1);
+    run_plan(plan, true, 1, rows, lr, fmt);
+    for (auto s : {s_h2d_, s_comp_, s_d2h_, s_upd_}) CUDA_OK(cudaStreamSynchronize(s));
+    CUDA_OK(cudaGetLastError());
+    collect_stats(plan, 1, true);
+    const float loss = loss_host_[0] / static_cast<float>(rows * d_ * world_);
+    stats_.loss = loss;
+    // digest_train (engine.cpp:574-581): loss bytes, then each block's W and b.
+    {
+        uint64_t h = 0xCBF29CE484222325ull;
+        auto fnv = [&](const void* p, size_t n) {
+            const unsigned char* c = static_cast<const unsigned char*>(p);
+            for (size_t i = 0; i < n; ++i) {
+                h ^= c[i];
+                h *= 0x100000001B3ull;
+            }
+        };
+        fnv(&loss, 4);
+        const size_t dd = static_cast<size_t>(d_) * d_;
+        fnv(host32_, static_cast<size_t>(n_) * (dd + d_) * 4);  // W_0 b_0 W_1 b_1 ... contiguous
+        static const char digits[] = "0123456789abcdef";
+        for (int i = 15; i >= 0; --i) {
+            stats_.digest[i] = digits[h & 0xF];
+            h >>= 4;
+        }
+        stats_.digest[16] = '\0';
+    }
+    return loss;
+}
+
+void Executor::read_layer(int index, float* W, float* b) {
+    if (index < 0 || index >= n_) throw Error(SP_ERR_INVALID, "read_layer: index out of range");
+    const size_t dd = static_cast<size_t>(d_) * d_;
+    const float* src = host32_ + static_cast<size_t>(index) * (dd + d_);
+    if (W) std::memcpy(W, src, dd * 4);
+    if (b) std::memcpy(b, src + dd, static_cast<size_t>(d_) * 4);
+}
+
+void Executor::dp_init(const uint8_t id[128], int rank, int world) {
+    if (world < 1 || rank < 0 || rank >= world) throw Error(SP_ERR_INVALID, "dp_init: bad rank/world");
+    if (world == 1) return;
+    if (!nccl().ok()) throw Error(SP_ERR_NCCL, nccl().error);
+    CUDA_OK(cudaSetDevice(cfg_.device));
+    ncclUniqueId uid;
+    std::memcpy(uid.internal, id, sizeof(uid.internal));
+    NCCL_OK(nccl().CommInitRank(&comm_, world, uid, rank));
+    rank_ = rank;
+    world_ = world;
+}
+
+}  // namespace sp

@@ -1,0 +1,126 @@
+// executor.hpp — the B200 ring executor behind the C ABI (include/superpipe.h).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/superpipe.h"
+#include "plan.hpp"
+
+namespace sp {
+
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+// Content format of the HBM ring slots (cached slot contents are only reusable within a
+// format): exact fp32, bf16 training (fp32 master + derived bf16), bf16 inference wire.
+enum SlotFormat : int { kFmtExactF32 = 0, kFmtBf16Train = 1, kFmtBf16Infer = 2 };
+
+class Executor {
+public:
+    explicit Executor(const sp_config& cfg);
+    ~Executor();
+
+    void register_layer(int index, const float* W, const float* b, int activation, int frozen);
+    void forward(const float* x, int64_t rows, int n_items, float* y, bool device_io);
+    float train_step(const float* x, const float* target, int64_t rows, float lr,
+                     bool device_io);
+    void read_layer(int index, float* W, float* b);
+    void dp_init(const uint8_t id[128], int rank, int world);
+
+    const sp_stats& stats() const { return stats_; }
+    const std::vector<sp_trace_event>& trace() const { return trace_; }
+    std::string error;
+
+private:
+    // layout helpers
+    uint64_t layer_bytes() const { return (static_cast<uint64_t>(d_) * d_ + d_) * 4; }
+    uint64_t wire16_bytes() const { return static_cast<uint64_t>(d_) * d_ * 2 + d_ * 4ull; }
+    uint8_t* slot_ptr(int s) const { return slots_dev_ + static_cast<size_t>(s) * slot_bytes_; }
+    float* slot_w32(int s) const { return reinterpret_cast<float*>(slot_ptr(s)); }
+    float* slot_b32(int s) const { return slot_w32(s) + static_cast<size_t>(d_) * d_; }
+    void* slot_w16(int s) const { return slot_ptr(s) + off_w16_; }
+    float* slot_b16(int s) const {  // bias of the bf16 inference wire image
+        return reinterpret_cast<float*>(slot_ptr(s) + off_w16_ + static_cast<size_t>(d_) * d_ * 2);
+    }
+
+    void check_ready() const;
+    void ensure_buffers(int64_t rows, int n_items, bool train, bool device_io);
+    void refresh_host16();
+    Plan make_plan(bool train, int n_items, int64_t rows, int fmt);
+    void run_plan(const Plan& plan, bool train, int n_items, int64_t rows, float lr, int fmt);
+    void enqueue_op(const Plan& plan, int i, bool train, int n_items, int64_t rows, float lr,
+                    int fmt);
+    void compute_op(const Op& op, bool train, int64_t rows, int fmt);
+    void loss_op(int64_t rows);
+    void update_op(const Op& op, float lr);
+    void collect_stats(const Plan& plan, int n_items, bool train);
+    void gemm(const struct GemmProblem& g, cudaStream_t st);
+    cudaStream_t stream_of(OpKind k) const;
+
+    sp_config cfg_;
+    int n_ = 0, d_ = 0;
+    bool bf16_ = false;
+    // pinned host copies
+    float* host32_ = nullptr;  // [n][d*d + d] fp32 master (W then b)
+    uint8_t* host16_ = nullptr;  // [n][wire16] bf16 W + fp32 b (bf16 inference wire)
+    std::vector<uint8_t> host16_stale_;
+    std::vector<int> relu_, frozen_;
+    std::vector<uint8_t> registered_;
+    // HBM ring
+    int n_slots_ = 0;
+    size_t slot_bytes_ = 0, off_w16_ = 0;
+    uint8_t* slots_dev_ = nullptr;
+    std::vector<SlotCache> cache_;
+    int cache_fmt_ = -1;
+    std::vector<int> w16_layer_;  // bf16 training: layer whose bf16 copy is current per slot
+    // streams / events
+    cudaStream_t s_h2d_ = nullptr, s_comp_ = nullptr, s_d2h_ = nullptr, s_upd_ = nullptr;
+    std::vector<cudaEvent_t> ev_done_, ev_start_;
+    cudaEvent_t ev_call0_ = nullptr, ev_io_in_ = nullptr, ev_io_out_ = nullptr;
+    // activations / workspaces (device)
+    int64_t cap_rows_ = 0;
+    int cap_items_ = 0;
+    bool cap_train_ = false;
+    std::vector<void*> dev_allocs_;
+    uint64_t dev_bytes_ = 0;
+    float* xin_ = nullptr;   // staging for host-side inputs [items][rows][d] fp32
+    float* yout_ = nullptr;  // staging for host-side outputs / training output y (fp32)
+    float* tgt_ = nullptr;   // training target staging (fp32)
+    void* pp_[2] = {nullptr, nullptr};  // inference ping-pong activations
+    void* xconv_ = nullptr;             // bf16 converted input
+    std::vector<void*> act_;            // training saved inputs x_0..x_{n-1}
+    void* gbuf_[2] = {nullptr, nullptr};  // dz ping-pong
+    float* gws_[2] = {nullptr, nullptr};  // per-layer gradient workspaces (dW [+db] partials)
+    float* grad_red_ = nullptr;           // reduced gradient (DP path)
+    float* loss_parts_ = nullptr;
+    float* loss_dev_ = nullptr;
+    float* loss_host_ = nullptr;  // pinned
+    void* fa_[3] = {nullptr, nullptr, nullptr};  // checkpointing: forward activation ring
+    std::vector<void*> ba_;                      // checkpointing: backward act per slot
+    uint8_t* host_act_ = nullptr;                // checkpointing: pinned activation store
+    size_t host_act_bytes_ = 0;
+    // current call pointers
+    const float* cur_x_ = nullptr;
+    float* cur_y_ = nullptr;
+    const float* cur_t_ = nullptr;
+    int splits_ = 1, dw_bn_ = 256, col_chunks_ = 1, splits_cap_ = 1, col_chunks_cap_ = 1;
+    int loss_blocks_ = 0;
+    // data parallel
+    ncclComm_t comm_ = nullptr;
+    int rank_ = 0, world_ = 1;
+    // metrics
+    sp_stats stats_{};
+    std::vector<sp_trace_event> trace_;
+    uint64_t kernels_ = 0;
+    uint64_t h2d_bytes_ = 0, d2h_bytes_ = 0;
+};
+
+}  // namespace sp

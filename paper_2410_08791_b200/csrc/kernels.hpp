@@ -1,0 +1,85 @@
+// kernels.hpp — host-side launchers for the executor's sm_100a kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace sp {
+
+// ---- exact (bit-identical to the reference CPU math, model.cpp:54-155) -------------
+// y = act(x W + b), i-ascending fp32, separately rounded mul/add, bias last.
+void exact_forward(const float* x, const float* W, const float* b, int relu, float* y,
+                   int64_t rows, int d, cudaStream_t st);
+// dz_out[r,i] = sum_j dz[r,j] W[i,j] (j ascending); then, if gate != nullptr, the ReLU
+// derivative of the layer below: dz_out = gate[r,i] <= 0 ? 0 : dz_out (model.cpp:91-96 with
+// z recomputation replaced by the stored activation, which has the same sign).
+void exact_backward_dx(const float* dz, const float* W, const float* gate, float* dz_out,
+                       int64_t rows, int d, cudaStream_t st);
+// dW[i,j] = sum_r x[r,i] dz[r,j]; db[j] = sum_r dz[r,j] (r ascending), model.cpp:108-121.
+void exact_backward_dw(const float* x, const float* dz, float* dW, float* db, int64_t rows,
+                       int d, cudaStream_t st);
+// loss = (sum e^2)/N sequential (model.cpp:131-140) into *loss_dev; g = 2 e (1/N) gated by
+// the last layer's ReLU (y <= 0 -> 0). partial != nullptr: write the raw sum instead (DP).
+void exact_loss_grad(const float* y, const float* t, int64_t count, float inv_n, int relu,
+                     float* g, float* loss_sum_dev, cudaStream_t st);
+// w -= lr * g  (model.cpp:150-155), no FMA.
+void exact_sgd(float* w, const float* g, int64_t count, float lr, cudaStream_t st);
+
+// ---- bf16 tensor-core path -----------------------------------------------------------
+enum GemmEpilogue : int {
+    EPI_BIAS_ACT_BF16 = 0,  // out(bf16) = act(acc + bias)
+    EPI_BIAS_ACT_F32 = 1,   // out(f32)  = act(acc + bias)
+    EPI_GATE_BF16 = 2,      // out(bf16) = (relu && gate <= 0) ? 0 : acc
+    EPI_F32 = 3             // out(f32)  = acc  (split-K partial at out + split*split_stride)
+};
+
+struct GemmProblem {
+    // C[M,N] = A[M,K] * B[K,N]; A given K-major ([M][lda]) or M-major ([K][lda]);
+    // B given K-major ([N][ldb]) or N-major ([K][ldb]). Leading dims in elements.
+    int M = 0, N = 0, K = 0;
+    const void* A = nullptr;
+    int lda = 0;
+    bool a_mn = false;
+    const void* B = nullptr;
+    int ldb = 0;
+    bool b_mn = false;
+    int epilogue = EPI_F32;
+    void* out = nullptr;
+    int ldo = 0;
+    const float* bias = nullptr;
+    int relu = 0;
+    const void* gate = nullptr;  // bf16 [M][ldg]
+    int ldg = 0;
+    int splits = 1;
+    int64_t split_stride = 0;
+    int block_n = 0;  // 0 = choose
+};
+
+// Launches the warp-specialized tcgen05/TMEM/TMA GEMM. Returns cudaSuccess or an error.
+cudaError_t gemm_bf16(const GemmProblem& p, cudaStream_t st);
+// Picks the split-K factor that best fills the 148 SMs for an M x N x K problem.
+int choose_splits(int M, int N, int K, int block_n);
+int choose_block_n(int N);
+// Split count actually used for K (no empty split): what gemm_bf16 will launch.
+int effective_splits(int K, int splits);
+int num_sms();
+
+void convert_f32_to_bf16(const float* src, void* dst, int64_t count, cudaStream_t st);
+// Fused MSE: partial sums of e^2 per block into partials[nblk] (fixed grid, deterministic),
+// g(bf16) = 2 e inv_n gated by the last layer's ReLU. Then loss_finalize sums partials in a
+// fixed order into *out (raw sum; caller divides by N).
+int loss_grad_bf16(const float* y, const float* t, int64_t count, float inv_n, int relu,
+                   void* g, float* partials, cudaStream_t st);
+void loss_finalize(const float* partials, int n, float* out, cudaStream_t st);
+// Column sums of a bf16 [rows][d] matrix into partials[chunks][d] (fixed chunking).
+int colsum_bf16(const void* x, int64_t rows, int d, float* partials, cudaStream_t st);
+int colsum_chunks(int64_t rows);
+// grad[i] = sum_s parts[s*stride + i] (fixed order).
+void reduce_partials(const float* parts, int nparts, int64_t stride, int64_t count,
+                     float* grad, cudaStream_t st);
+// w[i] -= lr * sum_s parts[s*stride + i]  (reduction fused into the SGD update).
+void sgd_reduce(float* w, const float* parts, int nparts, int64_t stride, int64_t count,
+                float lr, cudaStream_t st);
+void scale_inplace(float* x, int64_t count, float s, cudaStream_t st);
+
+}  // namespace sp

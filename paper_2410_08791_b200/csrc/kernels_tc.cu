@@ -1,0 +1,511 @@
+// kernels_tc.cu — warp-specialized tcgen05 GEMM for the streamed dense layers (sm_100a).
+//
+// One persistent CTA per SM (grid = min(tiles, #SMs)), 256 threads:
+//   warp 0      TMA producer: 2D tensor-map loads (128B swizzle) into a STAGES-deep smem ring
+//   warp 1      MMA issuer:   one elected thread issues tcgen05.mma.cta_group::1.kind::f16
+//               (bf16 x bf16 -> fp32) into a double-buffered TMEM accumulator
+//   warp 2      TMEM allocator (512 columns = 2 accumulator stages)
+//   warps 4..7  epilogue: tcgen05.ld 32x32b -> fused bias/ReLU, ReLU-gate or fp32 store
+// Synchronisation is mbarrier-only: smem full/empty (TMA <-> MMA, tcgen05.commit frees a
+// stage) and TMEM full/empty (MMA <-> epilogue), so tile t's epilogue overlaps tile t+1's
+// MMAs. Operands may be K-major or MN-major (the layer's forward uses W as an N-major B, the
+// dX GEMM the same W as a K-major B, the dW GEMM x^T / dz as MN-major A / B), so no
+// transposes are ever materialised. Each output tile is produced by exactly one CTA with a
+// fixed K order and split-K partials are reduced in a fixed order, so results depend only on
+// the problem shape: bit-identical for every (k, k') window and every ring slot address.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cudaTypedefs.h>
+
+#include <cstdio>
+#include <mutex>
+
+#include "kernels.hpp"
+
+namespace sp {
+namespace tc {
+
+constexpr int BM = 128;
+constexpr int BK = 64;  // bf16 elements per 128-byte swizzle row
+constexpr int kThreads = 256;
+constexpr int A_BYTES = BM * BK * 2;  // 16 KB
+constexpr int ACC_STRIDE = 256;       // TMEM columns between the two accumulator stages
+constexpr int TMEM_COLS = 512;
+
+template <int BN, bool B_MN>
+struct Cfg {
+    static constexpr int B_ROWS = B_MN ? ((BN + 63) / 64) * 64 : BN;
+    static constexpr int B_BYTES = B_ROWS * BK * 2;
+    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+    static constexpr int STAGES = (200 * 1024) / STAGE_BYTES < 8 ? (200 * 1024) / STAGE_BYTES : 8;
+    static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+};
+
+struct Params {
+    int M, N, K;
+    int m_tiles, n_tiles, k_blocks, kb_per_split, splits;
+    void* out;
+    int ldo;
+    const float* bias;
+    int relu;
+    const __nv_bfloat16* gate;
+    int ldg;
+    long long split_stride;
+};
+
+// ---------------------------------------------------------------------------------------
+// PTX wrappers
+// ---------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    const uint32_t addr = smem_u32(bar);
+    uint32_t done = 0;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(addr), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst,
+                                            int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes "
+        "[%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+__device__ __forceinline__ void fence_before() {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void fence_after() {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+// Shared-memory matrix descriptor (tcgen05 "smem descriptor"): start, LBO, SBO in 16-byte
+// units, version 1 (sm_100), layout SWIZZLE_128B (2). Tiles are 1024-byte aligned so the
+// base-offset field stays 0.
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
+    d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16;
+    d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32;
+    d |= static_cast<uint64_t>(1) << 46;
+    d |= static_cast<uint64_t>(2) << 61;
+    return d;
+}
+// Instruction descriptor, kind::f16: D fp32, A/B bf16, majors, N>>3, M>>4.
+__host__ __device__ constexpr uint32_t make_idesc(int M, int N, bool a_mn, bool b_mn) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | ((a_mn ? 1u : 0u) << 15) |
+           ((b_mn ? 1u : 0u) << 16) | (static_cast<uint32_t>(N >> 3) << 17) |
+           (static_cast<uint32_t>(M >> 4) << 24);
+}
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                          uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+            smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+          "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+          "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+          "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+          "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+    __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&v);
+}
+
+// ---------------------------------------------------------------------------------------
+// the kernel
+// ---------------------------------------------------------------------------------------
+template <int BN, bool A_MN, bool B_MN, int EPI>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                const Params p) {
+    using C = Cfg<BN, B_MN>;
+    constexpr int STAGES = C::STAGES;
+    constexpr uint32_t IDESC = make_idesc(BM, BN, A_MN, B_MN);
+    constexpr uint32_t TX = C::STAGE_BYTES;
+
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + STAGES * A_BYTES;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * C::B_BYTES);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+
+    if (warp == 0 && lane == 0) {
+        prefetch_tmap(&tmA);
+        prefetch_tmap(&tmB);
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&tfull[s], 1);
+            mbar_init(&tempty[s], 128);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_slot)),
+                     "r"(TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    const int tiles_mn = p.m_tiles * p.n_tiles;
+    const int total = tiles_mn * p.splits;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ===== TMA producer =====
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = blockIdx.x; t < total; t += gridDim.x) {
+                const int m0 = (t % p.m_tiles) * BM;
+                const int n0 = ((t / p.m_tiles) % p.n_tiles) * BN;
+                const int split = t / tiles_mn;
+                const int kb0 = split * p.kb_per_split;
+                const int kb1 = min(kb0 + p.kb_per_split, p.k_blocks);
+                for (int kb = kb0; kb < kb1; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    mbar_expect_tx(&full[stage], TX);
+                    const int k0 = kb * BK;
+                    uint8_t* a = sA + stage * A_BYTES;
+                    uint8_t* b = sB + stage * C::B_BYTES;
+                    if (A_MN) {
+                        tma_load_2d(&tmA, &full[stage], a, m0, k0);
+                        tma_load_2d(&tmA, &full[stage], a + 8192, m0 + 64, k0);
+                    } else {
+                        tma_load_2d(&tmA, &full[stage], a, k0, m0);
+                    }
+                    if (B_MN) {
+#pragma unroll
+                        for (int j = 0; j < C::B_ROWS / 64; ++j)
+                            tma_load_2d(&tmB, &full[stage], b + j * 8192, n0 + 64 * j, k0);
+                    } else {
+                        tma_load_2d(&tmB, &full[stage], b, k0, n0);
+                    }
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // ===== MMA issuer (single thread) =====
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int t = blockIdx.x; t < total; t += gridDim.x) {
+                const int split = t / tiles_mn;
+                const int kb0 = split * p.kb_per_split;
+                const int kb1 = min(kb0 + p.kb_per_split, p.k_blocks);
+                mbar_wait(&tempty[acc], acc_phase ^ 1);
+                fence_after();
+                const uint32_t d_tmem = tmem_base + acc * ACC_STRIDE;
+                for (int kb = kb0; kb < kb1; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    fence_after();
+                    const uint32_t a_base = smem_u32(sA + stage * A_BYTES);
+                    const uint32_t b_base = smem_u32(sB + stage * C::B_BYTES);
+#pragma unroll
+                    for (int kk = 0; kk < BK / 16; ++kk) {
+                        const uint64_t ad = A_MN ? make_desc(a_base + kk * 2048, 8192, 1024)
+                                                 : make_desc(a_base + kk * 32, 16, 1024);
+                        const uint64_t bd = B_MN ? make_desc(b_base + kk * 2048, 8192, 1024)
+                                                 : make_desc(b_base + kk * 32, 16, 1024);
+                        umma_bf16(d_tmem, ad, bd, IDESC, (kb > kb0 || kk > 0) ? 1u : 0u);
+                    }
+                    umma_commit(&empty[stage]);  // frees the smem stage when these MMAs finish
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                umma_commit(&tfull[acc]);  // accumulator ready for the epilogue
+                acc ^= 1;
+                if (acc == 0) acc_phase ^= 1;
+            }
+        }
+    } else if (warp >= 4) {
+        // ===== epilogue: TMEM -> registers -> fused op -> global =====
+        const int q = warp & 3;  // TMEM lanes [32q, 32q+32)
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int t = blockIdx.x; t < total; t += gridDim.x) {
+            const int m0 = (t % p.m_tiles) * BM;
+            const int n0 = ((t / p.m_tiles) % p.n_tiles) * BN;
+            const int split = t / tiles_mn;
+            mbar_wait(&tfull[acc], acc_phase);
+            fence_after();
+            const int row = m0 + q * 32 + lane;
+            const bool row_ok = row < p.M;
+#pragma unroll 1
+            for (int c = 0; c < BN / 32; ++c) {
+                uint32_t r[32];
+                tmem_ld32(tmem_base + acc * ACC_STRIDE + c * 32 + (static_cast<uint32_t>(q * 32) << 16), r);
+                const int col0 = n0 + c * 32;
+                if (!row_ok || col0 >= p.N) continue;
+                float v[32];
+#pragma unroll
+                for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+                if (EPI == EPI_BIAS_ACT_BF16 || EPI == EPI_BIAS_ACT_F32) {
+                    const float4* bp = reinterpret_cast<const float4*>(p.bias + col0);
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const float4 bv = __ldg(bp + i);
+                        v[4 * i + 0] += bv.x;
+                        v[4 * i + 1] += bv.y;
+                        v[4 * i + 2] += bv.z;
+                        v[4 * i + 3] += bv.w;
+                    }
+                    if (p.relu) {
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) v[i] = v[i] < 0.0f ? 0.0f : v[i];
+                    }
+                }
+                if (EPI == EPI_GATE_BF16 && p.relu) {
+                    const uint4* gp = reinterpret_cast<const uint4*>(
+                        p.gate + static_cast<long long>(row) * p.ldg + col0);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const uint4 g = __ldg(gp + i);
+                        const uint32_t gw[4] = {g.x, g.y, g.z, g.w};
+#pragma unroll
+                        for (int h = 0; h < 4; ++h) {
+                            const float2 gf = __bfloat1622float2(
+                                *reinterpret_cast<const __nv_bfloat162*>(&gw[h]));
+                            if (gf.x <= 0.0f) v[8 * i + 2 * h] = 0.0f;
+                            if (gf.y <= 0.0f) v[8 * i + 2 * h + 1] = 0.0f;
+                        }
+                    }
+                }
+                if (EPI == EPI_BIAS_ACT_BF16 || EPI == EPI_GATE_BF16) {
+                    uint4* op = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.out) +
+                                                         static_cast<long long>(row) * p.ldo + col0);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+                        op[i] = make_uint4(pack_bf16(v[8 * i + 0], v[8 * i + 1]),
+                                           pack_bf16(v[8 * i + 2], v[8 * i + 3]),
+                                           pack_bf16(v[8 * i + 4], v[8 * i + 5]),
+                                           pack_bf16(v[8 * i + 6], v[8 * i + 7]));
+                } else {
+                    float* base = static_cast<float*>(p.out) +
+                                  (EPI == EPI_F32 ? split * p.split_stride : 0LL) +
+                                  static_cast<long long>(row) * p.ldo + col0;
+                    float4* op = reinterpret_cast<float4*>(base);
+#pragma unroll
+                    for (int i = 0; i < 8; ++i)
+                        op[i] = make_float4(v[4 * i + 0], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+                }
+            }
+            fence_before();
+            mbar_arrive(&tempty[acc]);
+            acc ^= 1;
+            if (acc == 0) acc_phase ^= 1;
+        }
+    }
+    __syncwarp();
+    fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                     "r"(TMEM_COLS));
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------------------
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaDriverEntryPointQueryResult q;
+        void* f = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    });
+    return fn;
+}
+
+bool make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint64_t ld,
+              uint32_t box_inner, uint32_t box_outer) {
+    auto fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[2] = {inner, outer};
+    cuuint64_t strides[1] = {ld * 2};
+    cuuint32_t box[2] = {box_inner, box_outer};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+template <int BN, bool A_MN, bool B_MN, int EPI>
+cudaError_t launch(const GemmProblem& g, cudaStream_t st) {
+    using C = Cfg<BN, B_MN>;
+    auto kern = gemm_kernel<BN, A_MN, B_MN, EPI>;
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    CUtensorMap ta, tb;
+    bool ok = A_MN ? make_map(&ta, g.A, g.M, g.K, g.lda, 64, 64)
+                   : make_map(&ta, g.A, g.K, g.M, g.lda, 64, BM);
+    ok = ok && (B_MN ? make_map(&tb, g.B, g.N, g.K, g.ldb, 64, 64)
+                     : make_map(&tb, g.B, g.K, g.N, g.ldb, 64, BN));
+    if (!ok) return cudaErrorInvalidValue;
+    Params p;
+    p.M = g.M;
+    p.N = g.N;
+    p.K = g.K;
+    p.m_tiles = (g.M + BM - 1) / BM;
+    p.n_tiles = (g.N + BN - 1) / BN;
+    p.k_blocks = (g.K + BK - 1) / BK;
+    p.splits = g.splits < 1 ? 1 : g.splits;
+    if (p.splits > p.k_blocks) p.splits = p.k_blocks;
+    p.kb_per_split = (p.k_blocks + p.splits - 1) / p.splits;
+    p.splits = (p.k_blocks + p.kb_per_split - 1) / p.kb_per_split;  // no empty split
+    p.out = g.out;
+    p.ldo = g.ldo;
+    p.bias = g.bias;
+    p.relu = g.relu;
+    p.gate = static_cast<const __nv_bfloat16*>(g.gate);
+    p.ldg = g.ldg;
+    p.split_stride = g.split_stride;
+    const int total = p.m_tiles * p.n_tiles * p.splits;
+    const int grid = total < num_sms() ? total : num_sms();
+    kern<<<grid, kThreads, C::SMEM, st>>>(ta, tb, p);
+    return cudaGetLastError();
+}
+
+template <int BN>
+cudaError_t dispatch_bn(const GemmProblem& g, cudaStream_t st) {
+    if (!g.a_mn && g.b_mn && g.epilogue == EPI_BIAS_ACT_BF16) return launch<BN, false, true, EPI_BIAS_ACT_BF16>(g, st);
+    if (!g.a_mn && g.b_mn && g.epilogue == EPI_BIAS_ACT_F32) return launch<BN, false, true, EPI_BIAS_ACT_F32>(g, st);
+    if (!g.a_mn && !g.b_mn && g.epilogue == EPI_GATE_BF16) return launch<BN, false, false, EPI_GATE_BF16>(g, st);
+    if (g.a_mn && g.b_mn && g.epilogue == EPI_F32) return launch<BN, true, true, EPI_F32>(g, st);
+    if (!g.a_mn && !g.b_mn && g.epilogue == EPI_F32) return launch<BN, false, false, EPI_F32>(g, st);
+    if (!g.a_mn && g.b_mn && g.epilogue == EPI_F32) return launch<BN, false, true, EPI_F32>(g, st);
+    return cudaErrorNotSupported;
+}
+
+}  // namespace tc
+
+int choose_block_n(int N) {
+    // Minimise padded columns; prefer wide tiles (fewer smem bytes per MMA).
+    const int cands[3] = {256, 192, 128};
+    int best = 256;
+    long best_pad = -1;
+    for (int bn : cands) {
+        const long pad = static_cast<long>((N + bn - 1) / bn) * bn - N;
+        if (best_pad < 0 || pad < best_pad) {
+            best = bn;
+            best_pad = pad;
+        }
+    }
+    return best;
+}
+
+int choose_splits(int M, int N, int K, int block_n) {
+    const int tiles = ((M + tc::BM - 1) / tc::BM) * ((N + block_n - 1) / block_n);
+    const int kblocks = (K + tc::BK - 1) / tc::BK;
+    const int sms = num_sms();
+    int best = 1;
+    double best_eff = 0.0;
+    for (int s = 1; s <= 16 && s <= kblocks; ++s) {
+        if (s > 1 && kblocks / s < 8) break;  // keep >= 512 of K per split
+        const int work = tiles * s;
+        const int waves = (work + sms - 1) / sms;
+        // useful work per (wave x SM), discounted by the split-K reduction traffic
+        const double eff = static_cast<double>(work) / (static_cast<double>(waves) * sms) *
+                           (1.0 - 0.02 * (s - 1));
+        if (eff > best_eff + 1e-9) {
+            best_eff = eff;
+            best = s;
+        }
+    }
+    return best;
+}
+
+int effective_splits(int K, int splits) {
+    const int kb = (K + tc::BK - 1) / tc::BK;
+    int s = splits < 1 ? 1 : (splits > kb ? kb : splits);
+    const int per = (kb + s - 1) / s;
+    return (kb + per - 1) / per;
+}
+
+cudaError_t gemm_bf16(const GemmProblem& g, cudaStream_t st) {
+    if (g.M <= 0 || g.N <= 0 || g.K <= 0) return cudaErrorInvalidValue;
+    if (g.N % 32 != 0 || g.lda % 8 != 0 || g.ldb % 8 != 0) return cudaErrorInvalidValue;
+    const int bn = g.block_n ? g.block_n : choose_block_n(g.N);
+    switch (bn) {
+        case 128: return tc::dispatch_bn<128>(g, st);
+        case 192: return tc::dispatch_bn<192>(g, st);
+        case 256: return tc::dispatch_bn<256>(g, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace sp

@@ -1,0 +1,508 @@
+// plan.cpp — builds the static Superpipeline op DAG (see plan.hpp).
+//
+// Policy semantics follow the reference scheduler exactly:
+//   * Superpipeline (scheduler.cpp:105-136): prologue loads positions [0, k); every time k'
+//     computed positions are awaiting eviction, those k' are evicted and the next k'
+//     positions are prefetched (trigger = the compute that completed the group); the final
+//     partial group is evicted at stream end.
+//   * Naive (scheduler.cpp:85-104): load a group of k, compute it, evict it, next group.
+//   * Standard (scheduler.cpp:71-80): everything loaded once and kept across passes.
+//   * Training (engine.cpp:84-114,184-194): a forward pass, the loss, then a reversed pass.
+// GPU-specific refinements that do not change the math:
+//   * an evicted slot keeps its (still valid) weights until it is overwritten, so a later
+//     request for the same layer claims it without a copy (this is how the last forward
+//     layers are reused by the backward prologue instead of the reference's D2H + H2D
+//     round trip, engine.cpp:368-369);
+//   * forward evictions of unmodified weights move no bytes; backward evictions of trained
+//     layers write the updated fp32 weights back to the pinned host copy;
+//   * the prefetch H2D of group g targets the slots released one trigger earlier, so it
+//     waits only for their last reader (compute, or the writeback D2H in training).
+#include "plan.hpp"
+
+#include <algorithm>
+#include <deque>
+#include <limits>
+#include <sstream>
+
+namespace sp {
+
+std::string validate_strategy(int strategy, int k, int k_prime, int n_layers) {
+    if (n_layers < 1) return "strategy: n_layers must be >= 1";
+    switch (strategy) {
+        case 0:
+        case 1:
+            return "";
+        case 2:
+            if (k <= 0 || k > n_layers) return "strategy: naive requires 0 < k <= n_layers";
+            return "";
+        case 3:
+            if (k <= 0 || k > n_layers)
+                return "strategy: superpipeline requires 0 < k <= n_layers";
+            if (k_prime <= 0 || k_prime >= k) return "strategy: superpipeline requires 0 < k' < k";
+            return "";
+        default:
+            return "strategy: unknown kind";
+    }
+}
+
+uint64_t peak_weight_residency(int strategy, int k, int k_prime, int n_layers,
+                               uint64_t layer_bytes) {
+    switch (strategy) {
+        case 0: return static_cast<uint64_t>(n_layers) * layer_bytes;
+        case 1: return 0;
+        case 2: return static_cast<uint64_t>(k) * layer_bytes;
+        case 3: return static_cast<uint64_t>(std::min(k + k_prime, n_layers)) * layer_bytes;
+        default: return 0;
+    }
+}
+
+int ring_slots(int strategy, int k, int k_prime, int n_layers) {
+    switch (strategy) {
+        case 0: return n_layers;
+        case 2: return k;
+        case 3: return std::min(k + k_prime, n_layers);
+        default: return 0;
+    }
+}
+
+namespace {
+
+constexpr int kInf = std::numeric_limits<int>::max();
+
+struct SlotState {
+    int layer = -1;
+    bool valid = false;
+    int refs = 0;        // claimed positions not yet released
+    int fill_op = -1;    // op that last wrote the weights
+    int busy_op = -1;    // last op touching the slot's memory (overwrite must wait)
+    uint64_t stamp = 0;  // release order (FIFO tie-break)
+};
+
+enum Tag { kWeight = 0, kActivation = 1, kGradient = 2 };
+
+class Builder {
+public:
+    Builder(const PlanInput& in, const std::vector<SlotCache>& initial, int n_slots)
+        : in_(in), n_(in.n_layers) {
+        // Standard never evicts, so its activations are never offloaded (the reference's
+        // checkpointing rides eviction D2H / prefetch H2D jobs, engine.cpp:247-252).
+        ckpt_ = in.train && in.checkpointing &&
+                in.strategy != static_cast<int>(Strategy::Standard);
+        plan_.n_slots = n_slots;
+        slots_.resize(static_cast<std::size_t>(n_slots));
+        for (int s = 0; s < n_slots && s < static_cast<int>(initial.size()); ++s) {
+            slots_[s].layer = initial[s].layer;
+            slots_[s].valid = initial[s].valid && initial[s].layer >= 0 &&
+                              initial[s].layer < n_;
+        }
+        ba_busy_.assign(static_cast<std::size_t>(n_slots), -1);
+        if (in_.train) {
+            std::vector<int> fwd(n_), bwd(n_);
+            for (int i = 0; i < n_; ++i) fwd[i] = i, bwd[i] = n_ - 1 - i;
+            seqs_ = {fwd, bwd};
+        } else {
+            std::vector<int> seq(static_cast<std::size_t>(n_) * in_.n_items);
+            for (std::size_t p = 0; p < seq.size(); ++p) seq[p] = static_cast<int>(p) % n_;
+            seqs_ = {seq};
+        }
+    }
+
+    Plan run() {
+        if (!in_.train) {
+            // The reference holds one io activation buffer for inference (engine.cpp:60-64).
+            if (in_.capacity && in_.act_bytes > in_.capacity) {
+                plan_.oom = true;
+                plan_.error = "activation buffer alone exceeds device capacity";
+                return plan_;
+            }
+            ledger_add(kActivation, in_.act_bytes);
+        }
+        for (pass_ = 0; pass_ < static_cast<int>(seqs_.size()); ++pass_) {
+            run_pass();
+            if (in_.train && pass_ == 0) {
+                Op loss;
+                loss.kind = OpKind::Loss;
+                loss.pass = 0;
+                loss_op_ = push(std::move(loss));
+            }
+        }
+        flush_deferred();
+        for (auto& s : slots_) {  // end of call: every claim is dropped (release_remaining)
+            if (s.refs > 0) ledger_sub(kWeight, in_.layer_bytes);
+            s.refs = 0;
+        }
+        plan_.final_slots.resize(slots_.size());
+        for (std::size_t s = 0; s < slots_.size(); ++s)
+            plan_.final_slots[s] = SlotCache{slots_[s].layer, slots_[s].valid};
+        return plan_;
+    }
+
+private:
+    const std::vector<int>& seq() const { return seqs_[static_cast<std::size_t>(pass_)]; }
+    int len() const { return static_cast<int>(seq().size()); }
+    bool backward() const { return in_.train && pass_ == 1; }
+    bool trainable(int layer) const {
+        return !(layer < static_cast<int>(in_.frozen.size()) && in_.frozen[layer]);
+    }
+
+    int push(Op op) {
+        plan_.ops.push_back(std::move(op));
+        return static_cast<int>(plan_.ops.size()) - 1;
+    }
+
+    // ---- ledger (DeviceArena semantics, arena.hpp:45-67) -----------------------------
+    void ledger_add(int tag, uint64_t bytes) {
+        tag_[tag] += bytes;
+        auto& pk = tag == kWeight ? plan_.ledger.peak_weight
+                   : tag == kActivation ? plan_.ledger.peak_activation
+                                        : plan_.ledger.peak_gradient;
+        pk = std::max(pk, tag_[tag]);
+        const uint64_t total = tag_[0] + tag_[1] + tag_[2];
+        plan_.ledger.peak_bytes = std::max(plan_.ledger.peak_bytes, total);
+        if (in_.capacity && total > in_.capacity && !plan_.oom) {
+            plan_.oom = true;
+            plan_.error = "no runnable event: required working set cannot fit in " +
+                          std::to_string(in_.capacity) + " bytes";
+        }
+    }
+    void ledger_sub(int tag, uint64_t bytes) { tag_[tag] -= std::min(tag_[tag], bytes); }
+    // Evictions free their bytes when the D2H completes in the reference
+    // (engine.cpp:390-405), i.e. while the next compute is already running.
+    void defer_free(int tag, uint64_t bytes) { deferred_.push_back({tag, bytes}); }
+    void flush_deferred() {
+        for (auto [tag, bytes] : deferred_) ledger_sub(tag, bytes);
+        deferred_.clear();
+    }
+
+    // ---- slot choice -------------------------------------------------------------------
+    int next_use(int layer, int after_pos) const {
+        int base = 0;
+        for (int ps = 0; ps < static_cast<int>(seqs_.size()); ++ps) {
+            const auto& s = seqs_[ps];
+            const int start = ps < pass_ ? static_cast<int>(s.size()) : ps == pass_ ? after_pos + 1 : 0;
+            for (int q = start; q < static_cast<int>(s.size()); ++q)
+                if (s[q] == layer) return base + q;
+            base += static_cast<int>(s.size());
+        }
+        return kInf;
+    }
+    int active_slot(int layer) const {
+        for (int s = 0; s < static_cast<int>(slots_.size()); ++s)
+            if (slots_[s].refs > 0 && slots_[s].layer == layer) return s;
+        return -1;
+    }
+    int cached_free_slot(int layer) const {
+        for (int s = 0; s < static_cast<int>(slots_.size()); ++s)
+            if (slots_[s].refs == 0 && slots_[s].valid && slots_[s].layer == layer) return s;
+        return -1;
+    }
+    // Belady among free slots: evict the cached layer whose next use is farthest away;
+    // ties go to the earliest-released slot, then the lowest index.
+    int victim_slot(int pos) const {
+        int best = -1, best_use = -1;
+        uint64_t best_stamp = 0;
+        for (int s = 0; s < static_cast<int>(slots_.size()); ++s) {
+            if (slots_[s].refs != 0) continue;
+            const int use = slots_[s].valid ? next_use(slots_[s].layer, pos) : kInf;
+            if (best < 0 || use > best_use || (use == best_use && slots_[s].stamp < best_stamp)) {
+                best = s;
+                best_use = use;
+                best_stamp = slots_[s].stamp;
+            }
+        }
+        return best;
+    }
+    int free_slots() const {
+        int c = 0;
+        for (const auto& s : slots_) c += s.refs == 0;
+        return c;
+    }
+    int misses_in(int b, int e) const {
+        int m = 0;
+        std::vector<int> seen;
+        for (int q = b; q < e; ++q) {
+            const int L = seq()[q];
+            if (std::find(seen.begin(), seen.end(), L) != seen.end()) continue;
+            seen.push_back(L);
+            if (active_slot(L) < 0) ++m;  // cached free slots are consumed as well
+        }
+        return m;
+    }
+
+    // ---- policy actions ----------------------------------------------------------------
+    void claim_positions(int b, int e, int trigger) {
+        struct Move { int pos, slot; bool weights, act; };
+        std::vector<Move> moves;
+        for (int q = b; q < e; ++q) {
+            const int L = seq()[q];
+            int s = active_slot(L);
+            if (s >= 0) {
+                slots_[s].refs += 1;
+                pos_slot_[q] = s;
+                pos_load_[q] = slots_[s].fill_op;
+                continue;
+            }
+            bool miss = false;
+            s = cached_free_slot(L);
+            if (s < 0) {
+                s = victim_slot(q);
+                if (s < 0) {
+                    plan_.error = "plan: no free ring slot (internal)";
+                    plan_.oom = true;
+                    return;
+                }
+                miss = true;
+                slots_[s].layer = L;
+                slots_[s].valid = true;
+            }
+            slots_[s].refs = 1;
+            pos_slot_[q] = s;
+            pos_load_[q] = slots_[s].fill_op;
+            ledger_add(kWeight, in_.layer_bytes);
+            const bool act = backward() && ckpt_;
+            if (act) ledger_add(kActivation, in_.act_bytes);
+            if (miss || act) moves.push_back({q, s, miss, act});
+        }
+        if (moves.empty()) return;
+        auto emit = [&](const std::vector<Move>& group) {
+            Op op;
+            op.kind = OpKind::H2D;
+            op.pass = pass_;
+            if (trigger >= 0) op.deps.push_back(trigger);
+            for (const auto& m : group) {
+                op.layers.push_back(seq()[m.pos]);
+                op.slots.push_back(m.slot);
+                op.weights.push_back(m.weights);
+                op.acts.push_back(m.act);
+                if (m.weights && slots_[m.slot].busy_op >= 0) op.deps.push_back(slots_[m.slot].busy_op);
+                if (m.act && ba_busy_[m.slot] >= 0) op.deps.push_back(ba_busy_[m.slot]);
+                plan_.h2d_weight_layers += m.weights;
+                plan_.h2d_act_layers += m.act;
+            }
+            const int id = push(std::move(op));
+            for (const auto& m : group) {
+                if (m.weights) {
+                    slots_[m.slot].fill_op = id;
+                    slots_[m.slot].busy_op = id;
+                }
+                pos_load_[m.pos] = id;
+                if (m.act) pos_act_[m.pos] = id;
+            }
+            plan_.n_h2d_jobs += 1;
+        };
+        if (in_.transfer_mode == 0) {
+            for (const auto& m : moves) emit({m});
+        } else {
+            emit(moves);
+        }
+    }
+
+    void release_positions(const std::vector<int>& positions) {
+        for (int q : positions) {
+            const int s = pos_slot_[q];
+            plan_.n_evictions += 1;
+            if (--slots_[s].refs == 0) {
+                slots_[s].stamp = ++stamp_;
+                defer_free(kWeight, in_.layer_bytes);
+                if (!backward() && in_.train && ckpt_)
+                    defer_free(kActivation, in_.act_bytes);  // offloaded with the layer
+            }
+        }
+    }
+
+    int emit_compute(int p) {
+        const int L = seq()[p];
+        const int s = pos_slot_[p];
+        Op op;
+        op.kind = OpKind::Compute;
+        op.pass = pass_;
+        op.position = p;
+        op.item = in_.train ? 0 : p / n_;
+        op.layer = L;
+        op.slot = s;
+        if (pos_load_[p] >= 0) op.deps.push_back(pos_load_[p]);
+        if (backward() && ckpt_ && pos_act_[p] >= 0) op.deps.push_back(pos_act_[p]);
+        if (!backward() && in_.train && ckpt_) {
+            const int buf = (L + 1) % 3;  // forward act ring: x_{L+1} overwrites x_{L-2}
+            if (fa_busy_[buf] >= 0) op.deps.push_back(fa_busy_[buf]);
+        }
+        if (backward() && trainable(L) && gws_busy_[L % 2] >= 0)
+            op.deps.push_back(gws_busy_[L % 2]);  // dW workspace double buffer
+        // Ledger at compute begin (engine.cpp:271-282).
+        if (in_.train && !backward()) ledger_add(kActivation, in_.act_bytes);
+        const bool grad = backward() && trainable(L);
+        if (grad) {
+            ledger_add(kGradient, in_.layer_bytes);
+            plan_.ledger.total_gradient += in_.layer_bytes;
+        }
+        flush_deferred();
+        const int id = push(std::move(op));
+        slots_[s].busy_op = id;
+        if (grad) ledger_sub(kGradient, in_.layer_bytes);  // freed at compute end
+        if (backward() && ckpt_) {
+            ba_busy_[s] = id;
+            ledger_sub(kActivation, in_.act_bytes);  // engine.cpp:438-441
+        }
+        if (!backward() && in_.train && ckpt_) {
+            Op save;  // offload x_L to the pinned host activation store
+            save.kind = OpKind::ActSave;
+            save.pass = 0;
+            save.layer = L;
+            save.deps.push_back(id);
+            fa_busy_[L % 3] = push(std::move(save));
+            plan_.d2h_act_layers += 1;
+        }
+        if (grad) {
+            Op upd;  // gradient all-reduce (DP) + SGD on the update stream
+            upd.kind = OpKind::Update;
+            upd.pass = 1;
+            upd.layer = L;
+            upd.slot = s;
+            upd.deps.push_back(id);
+            const int uid = push(std::move(upd));
+            gws_busy_[L % 2] = uid;
+            Op wb;  // write the updated fp32 weights back to the host master copy
+            wb.kind = OpKind::D2H;
+            wb.pass = 1;
+            wb.layers = {L};
+            wb.slots = {s};
+            wb.weights = {1};
+            wb.acts = {0};
+            wb.deps.push_back(uid);
+            const int wid = push(std::move(wb));
+            slots_[s].busy_op = wid;
+            plan_.n_d2h_jobs += 1;
+            plan_.d2h_weight_layers += 1;
+        }
+        return id;
+    }
+
+    void run_pass() {
+        const int n = len();
+        pos_slot_.assign(static_cast<std::size_t>(n), -1);
+        pos_load_.assign(static_cast<std::size_t>(n), -1);
+        pos_act_.assign(static_cast<std::size_t>(n), -1);
+        const int trigger0 = pass_ == 0 ? -1 : loss_op_;
+        const auto kind = static_cast<Strategy>(in_.strategy);
+        if (kind == Strategy::Standard) {
+            claim_positions(0, n, trigger0);
+            for (int p = 0; p < n && !plan_.oom; ++p) emit_compute(p);
+            return;
+        }
+        if (kind == Strategy::Naive) {
+            int trigger = trigger0;
+            for (int gb = 0; gb < n && !plan_.oom; gb += in_.k) {
+                const int ge = std::min(gb + in_.k, n);
+                claim_positions(gb, ge, trigger);
+                std::vector<int> group;
+                for (int p = gb; p < ge && !plan_.oom; ++p) {
+                    trigger = emit_compute(p);
+                    group.push_back(p);
+                }
+                release_positions(group);
+            }
+            return;
+        }
+        // Superpipeline.
+        const int k = in_.k, kp = in_.k_prime;
+        claim_positions(0, std::min(k, n), trigger0);
+        int next_load = std::min(k, n);
+        std::deque<int> ready;
+        for (int p = 0; p < n && !plan_.oom; ++p) {
+            const int c = emit_compute(p);
+            ready.push_back(p);
+            if (static_cast<int>(ready.size()) >= kp) {
+                std::vector<int> evict(ready.begin(), ready.begin() + kp);
+                ready.erase(ready.begin(), ready.begin() + kp);
+                const int nb = next_load, ne = std::min(next_load + kp, n);
+                if (nb < ne && misses_in(nb, ne) <= free_slots()) {
+                    claim_positions(nb, ne, c);  // prefetch into slots freed one group earlier
+                    release_positions(evict);
+                } else {
+                    release_positions(evict);
+                    if (nb < ne) claim_positions(nb, ne, c);
+                }
+                next_load = ne;
+            }
+        }
+        release_positions(std::vector<int>(ready.begin(), ready.end()));
+    }
+
+    const PlanInput& in_;
+    int n_;
+    Plan plan_;
+    std::vector<SlotState> slots_;
+    std::vector<std::vector<int>> seqs_;
+    std::vector<int> pos_slot_, pos_load_, pos_act_;
+    std::vector<int> ba_busy_;
+    int fa_busy_[3] = {-1, -1, -1};
+    int gws_busy_[2] = {-1, -1};
+    int pass_ = 0;
+    int loss_op_ = -1;
+    bool ckpt_ = false;
+    uint64_t stamp_ = 0;
+    uint64_t tag_[3] = {0, 0, 0};
+    std::vector<std::pair<int, uint64_t>> deferred_;
+};
+
+}  // namespace
+
+Plan build_plan(const PlanInput& in, const std::vector<SlotCache>& initial) {
+    Plan bad;
+    bad.error = validate_strategy(in.strategy, in.k, in.k_prime, in.n_layers);
+    if (!bad.error.empty()) return bad;
+    if (in.strategy == static_cast<int>(Strategy::CpuOnly)) {
+        bad.error = "strategy: cpu_only is the reference's host path; the GPU executor has no "
+                    "CPU fallback";
+        return bad;
+    }
+    if (in.n_items < 1) {
+        bad.error = "execution_stream: counts must be >= 1";
+        return bad;
+    }
+    // The reference admits a prefetch only when it fits (engine.cpp:366-378), so a tight
+    // capacity shrinks the effective ring instead of failing; below the minimum working
+    // set (k slots, or n for Standard) it deadlocks -> OOM.
+    int S = ring_slots(in.strategy, in.k, in.k_prime, in.n_layers);
+    const int smin = in.strategy == static_cast<int>(Strategy::Standard) ? in.n_layers : in.k;
+    for (;;) {
+        Builder b(in, initial, S);
+        Plan p = b.run();
+        if (!p.oom || S <= smin) return p;
+        --S;
+    }
+}
+
+std::string describe_plan(const Plan& plan) {
+    static const char* names[] = {"H2D", "COMPUTE", "D2H", "LOSS", "UPDATE", "ACTSAVE"};
+    std::ostringstream os;
+    os << "slots=" << plan.n_slots << " ops=" << plan.ops.size()
+       << " h2d_jobs=" << plan.n_h2d_jobs << " d2h_jobs=" << plan.n_d2h_jobs
+       << " evictions=" << plan.n_evictions << " peak=" << plan.ledger.peak_bytes
+       << " peak_w=" << plan.ledger.peak_weight << " peak_a=" << plan.ledger.peak_activation
+       << " peak_g=" << plan.ledger.peak_gradient << " total_g=" << plan.ledger.total_gradient
+       << (plan.oom ? " OOM" : "") << "\n";
+    auto list = [&](const std::vector<int>& v) {
+        std::ostringstream s;
+        for (std::size_t i = 0; i < v.size(); ++i) s << (i ? "," : "") << v[i];
+        return s.str();
+    };
+    for (std::size_t i = 0; i < plan.ops.size(); ++i) {
+        const Op& op = plan.ops[i];
+        os << i << " " << names[static_cast<int>(op.kind)] << " pass=" << op.pass;
+        if (op.kind == OpKind::Compute)
+            os << " pos=" << op.position << " item=" << op.item << " layer=" << op.layer
+               << " slot=" << op.slot;
+        if (op.kind == OpKind::Update || op.kind == OpKind::ActSave) os << " layer=" << op.layer;
+        if (op.kind == OpKind::H2D || op.kind == OpKind::D2H) {
+            std::vector<int> w(op.weights.begin(), op.weights.end()),
+                a(op.acts.begin(), op.acts.end());
+            os << " layers=" << list(op.layers) << " slots=" << list(op.slots)
+               << " w=" << list(w) << " a=" << list(a);
+        }
+        os << " deps=" << list(op.deps) << "\n";
+    }
+    return os.str();
+}
+
+}  // namespace sp

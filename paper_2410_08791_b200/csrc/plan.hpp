@@ -1,0 +1,89 @@
+// plan.hpp — static Superpipeline op plan (host-only, no CUDA).
+//
+// The reference drives its policy online from a virtual event loop: policy_step
+// (scheduler.cpp:53-141) is re-evaluated after every completion (engine.cpp:172-182) and
+// transfers are admitted against a byte ledger (engine.cpp:366-378). Because compute is
+// strictly sequential in stream order, the Superpipeline policy is a pure function of
+// (n, n_items, k, k', mode, pass structure), so on the GPU it is resolved ONCE into a DAG of
+// ops on three CUDA streams (H2D copy engine, compute, D2H copy engine, + an update stream
+// for SGD / gradient all-reduce) joined by events. This file builds that DAG, assigns the
+// fixed HBM ring slots, and replays the reference's DeviceArena ledger (arena.hpp:38-111)
+// along it for peak / OOM accounting.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace sp {
+
+enum class Strategy : int { Standard = 0, CpuOnly = 1, Naive = 2, Superpipeline = 3 };
+enum class OpKind : int { H2D = 0, Compute = 1, D2H = 2, Loss = 3, Update = 4, ActSave = 5 };
+
+// StrategyConfig::validate (strategy.cpp:19-36). Returns an empty string when valid.
+std::string validate_strategy(int strategy, int k, int k_prime, int n_layers);
+// peak_weight_residency (strategy.cpp:48-60).
+uint64_t peak_weight_residency(int strategy, int k, int k_prime, int n_layers,
+                               uint64_t layer_bytes);
+// Number of HBM weight slots the ring needs (S = min(k+k', n) for Superpipeline).
+int ring_slots(int strategy, int k, int k_prime, int n_layers);
+
+struct PlanInput {
+    int n_layers = 1;
+    int strategy = 3;
+    int k = 0, k_prime = 0;
+    int transfer_mode = 1;  // 0 sequential, 1 batch
+    bool train = false;
+    int n_items = 1;
+    bool checkpointing = false;
+    std::vector<uint8_t> frozen;  // per layer
+    uint64_t layer_bytes = 0;     // reference ledger units: (d*d + d) * 4
+    uint64_t act_bytes = 0;       // rows * d * 4
+    uint64_t capacity = 0;        // 0 = unlimited
+};
+
+// Persistent content of one HBM slot across calls (weights valid == equal to host copy).
+struct SlotCache {
+    int layer = -1;
+    bool valid = false;
+};
+
+struct Op {
+    OpKind kind = OpKind::Compute;
+    int pass = 0;       // 0 forward / inference, 1 backward
+    int position = -1;  // compute position in the pass sequence
+    int item = 0;       // inference item
+    int layer = -1;     // Compute / Update / ActSave
+    int slot = -1;      // Compute / Update: the weight slot
+    std::vector<int> layers;       // H2D / D2H: moved layers (in order)
+    std::vector<int> slots;        // H2D / D2H: their slots
+    std::vector<uint8_t> weights;  // per moved layer: weight bytes move
+    std::vector<uint8_t> acts;     // per moved layer: the saved activation rides along
+    std::vector<int> deps;         // op indices that must complete first (any stream)
+};
+
+struct LedgerPeaks {
+    uint64_t peak_bytes = 0, peak_weight = 0, peak_activation = 0, peak_gradient = 0;
+    uint64_t total_gradient = 0;
+};
+
+struct Plan {
+    int n_slots = 0;
+    std::vector<Op> ops;
+    LedgerPeaks ledger;
+    std::vector<SlotCache> final_slots;
+    uint64_t n_h2d_jobs = 0, n_d2h_jobs = 0, n_evictions = 0;
+    uint64_t h2d_weight_layers = 0, h2d_act_layers = 0, d2h_weight_layers = 0,
+             d2h_act_layers = 0;
+    bool oom = false;
+    std::string error;  // invalid configuration or OOM reason
+};
+
+// Builds the op DAG for one call. `initial` is the slot content left by the previous call
+// (empty = cold ring).
+Plan build_plan(const PlanInput& in, const std::vector<SlotCache>& initial);
+
+// Human-readable one-op-per-line listing (used by sp_describe_plan and the CPU tests).
+std::string describe_plan(const Plan& plan);
+
+}  // namespace sp

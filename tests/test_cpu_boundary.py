@@ -1,0 +1,175 @@
+"""CPU-only tests: the C-ABI library loads and exports every declared symbol, and the
+host-side logic (model generation, strategy validation, ledger/plan semantics) matches the
+reference. No CUDA device is touched here."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2410_08791_b200 as sp
+from paper_2410_08791_b200 import _capi
+from pyoracle import BATCH, NAIVE, SEQUENTIAL, STANDARD, SUPERPIPELINE, Oracle, Reference
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ORC = Oracle()
+
+
+def declared_functions():
+    names = set()
+    for h in ("superpipe.h", "superpipe_debug.h"):
+        text = open(os.path.join(ROOT, "include", h)).read()
+        text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+        names |= set(re.findall(r"\b(sp_[a-z0-9_]+)\s*\(", text))
+    return names
+
+
+def test_library_exports_every_declared_symbol():
+    names = declared_functions()
+    assert len(names) >= 20
+    for n in sorted(names):
+        assert hasattr(_capi.LIB, n), f"{n} declared in include/ but not exported"
+    assert set(_capi.EXPORTS) == names
+    assert _capi.LIB.sp_abi_version() == 1
+
+
+def test_no_device_means_loud_failure_not_fallback():
+    # Without a GPU the executor must refuse (SP_ERR_CUDA); there is no CPU path.
+    try:
+        import torch
+        if torch.cuda.is_available():
+            pytest.skip("a GPU is visible")
+    except ImportError:
+        pass
+    with pytest.raises(sp.SpError) as e:
+        sp.Executor(4, 16, sp.StrategyConfig(sp.SUPERPIPELINE, 2, 1))
+    assert e.value.code == _capi.SP_ERR_CUDA
+
+
+@pytest.mark.parametrize("seed,n,d", [(7, 8, 16), (1, 4, 3), (11, 12, 16), (42, 3, 97)])
+def test_build_model_matches_reference_bitwise(seed, n, d):
+    m = sp.build_model(seed, n, d, frozen_prefix=n // 2)
+    W, b = ORC.build_model(seed, n, d)
+    assert np.array_equal(m.W, W) and np.array_equal(m.b, b)
+    assert list(m.frozen) == [1 if i < n // 2 else 0 for i in range(n)]
+    assert m.layer_bytes() == (d * d + d) * 4
+
+
+def test_make_input_matches_reference_bitwise():
+    for seed, tag, rows, d in [(7, 0, 1, 16), (11, 1, 4, 16), (3, 1001, 5, 7)]:
+        assert np.array_equal(sp.make_input(seed, tag, rows, d), ORC.make_input(seed, tag, rows, d))
+
+
+def test_build_model_rejects_bad_parameters():
+    # test_model.cpp:210-215
+    for args in [(1, 0, 4, 0), (1, 4, 0, 0), (1, 4, 4, 5), (1, 4, 4, -1)]:
+        with pytest.raises(sp.InvalidArgument):
+            sp.build_model(*args)
+
+
+def test_strategy_validation_matches_reference():
+    # strategy.cpp:19-36, test_scheduler.cpp:48-61
+    ok = [(STANDARD, 0, 0, 3), (NAIVE, 1, 0, 3), (NAIVE, 3, 0, 3), (SUPERPIPELINE, 2, 1, 2),
+          (SUPERPIPELINE, 4, 3, 8)]
+    bad = [(NAIVE, 0, 0, 3), (NAIVE, 4, 0, 3), (SUPERPIPELINE, 1, 0, 4), (SUPERPIPELINE, 2, 2, 4),
+           (SUPERPIPELINE, 5, 1, 4), (SUPERPIPELINE, 3, 0, 4)]
+    for kind, k, kp, n in ok:
+        sp.StrategyConfig(kind, k, kp).validate(n)
+    for kind, k, kp, n in bad:
+        with pytest.raises(sp.InvalidArgument):
+            sp.StrategyConfig(kind, k, kp).validate(n)
+
+
+def test_peak_weight_residency_formula():
+    # strategy.cpp:48-60, test_scheduler.cpp:63-71
+    s = 1088
+    assert sp.peak_weight_residency(sp.StrategyConfig(STANDARD), 8, s) == 8 * s
+    assert sp.peak_weight_residency(sp.StrategyConfig(NAIVE, 3), 8, s) == 3 * s
+    assert sp.peak_weight_residency(sp.StrategyConfig(SUPERPIPELINE, 4, 2), 8, s) == 6 * s
+    assert sp.peak_weight_residency(sp.StrategyConfig(SUPERPIPELINE, 7, 3), 8, s) == 8 * s
+
+
+def parse_plan(text):
+    lines = text.strip().splitlines()
+    head = dict(kv.split("=") for kv in lines[0].split() if "=" in kv)
+    ops = []
+    for ln in lines[1:]:
+        parts = ln.split()
+        op = {"kind": parts[1]}
+        for kv in parts[2:]:
+            k, v = kv.split("=")
+            op[k] = [int(t) for t in v.split(",")] if v and k in ("layers", "slots", "w", "a", "deps") else (int(v) if v else [])
+        ops.append(op)
+    return head, ops
+
+
+def test_plan_superpipeline_pairs_eviction_with_prefetch():
+    # test_scheduler.cpp:163-194: SP(4,2) on 8 layers loads {0,1,2,3}, and after computes 0,1
+    # issues the prefetch of {4,5}; compute of position 2 follows.
+    head, ops = parse_plan(sp.describe_plan(8, 16, sp.StrategyConfig(SUPERPIPELINE, 4, 2)))
+    assert ops[0]["kind"] == "H2D" and ops[0]["layers"] == [0, 1, 2, 3]
+    assert [o["kind"] for o in ops[1:4]] == ["COMPUTE", "COMPUTE", "H2D"]
+    assert ops[3]["layers"] == [4, 5] and 2 in ops[3]["deps"]  # trigger = compute of pos 1
+    assert ops[4]["kind"] == "COMPUTE" and ops[4]["pos"] == 2
+    assert int(head["slots"]) == 6
+
+
+def test_plan_ledger_matches_reference_goldens():
+    ref = Reference()
+    # configs/default.json: peak 6592 and 15 H2D jobs; oom_train.json: 13952 / OOM.
+    head, _ = parse_plan(sp.describe_plan(8, 16, sp.StrategyConfig(SUPERPIPELINE, 4, 2), n_items=4))
+    assert int(head["peak"]) == 6592 and int(head["h2d_jobs"]) == 15
+    W, b, fz = ref.build_model(7, 8, 16)
+    xs = np.stack([ref.make_input(7, i, 1, 16) for i in range(4)])
+    rc, _, s = ref.run_inference(W, b, xs, SUPERPIPELINE, 4, 2, BATCH, 1 << 30)
+    assert s.peak_bytes == 6592 and s.n_transfers_h2d == 15
+    txt = sp.describe_plan(12, 16, sp.StrategyConfig(SUPERPIPELINE, 6, 3), train=True,
+                           capacity_bytes=15000)
+    # describe_plan sizes activations for one row; oom_train uses b=4 -> check via executor
+    # semantics in the GPU suite. Standard never fits 15000 B at b=1 either way:
+    assert "OOM" not in txt
+    txt = sp.describe_plan(12, 16, sp.StrategyConfig(STANDARD), train=True, capacity_bytes=13000)
+    assert txt.startswith("ERROR")
+
+
+@pytest.mark.parametrize("n,k,kp,items", [(8, 4, 2, 1), (8, 4, 2, 3), (12, 6, 3, 1), (5, 2, 1, 2),
+                                          (6, 5, 3, 2), (16, 8, 3, 1), (3, 2, 1, 4)])
+def test_plan_is_well_formed(n, k, kp, items):
+    """Every compute is preceded by the load of its layer; at most S slots are ever in use;
+    weights bytes peak equals the analytic bound when the window fits the model."""
+    for mode in (BATCH, SEQUENTIAL):
+        head, ops = parse_plan(sp.describe_plan(n, 8, sp.StrategyConfig(SUPERPIPELINE, k, kp, mode),
+                                                n_items=items))
+        S = int(head["slots"])
+        assert S == min(k + kp, n)
+        slot_layer = {}
+        for i, op in enumerate(ops):
+            for d in op.get("deps", []):
+                assert d < i
+            if op["kind"] == "H2D":
+                for L, s in zip(op["layers"], op["slots"]):
+                    assert 0 <= s < S
+                    slot_layer[s] = L
+            if op["kind"] == "COMPUTE":
+                assert slot_layer.get(op["slot"]) == op["layer"], (i, op)
+        computes = [o for o in ops if o["kind"] == "COMPUTE"]
+        assert [o["layer"] for o in computes] == [p % n for p in range(n * items)]
+        if items == 1 and k + kp <= n:
+            assert int(head["peak_w"]) == (k + kp) * (8 * 8 + 8) * 4
+
+
+def test_plan_training_reuses_forward_tail_without_reload():
+    head, ops = parse_plan(sp.describe_plan(8, 8, sp.StrategyConfig(SUPERPIPELINE, 4, 2), train=True))
+    loss_at = [i for i, o in enumerate(ops) if o["kind"] == "LOSS"][0]
+    after = ops[loss_at + 1:]
+    # The first k + k' backward layers are still in the ring: no H2D before their computes.
+    first_h2d = next(i for i, o in enumerate(after) if o["kind"] == "H2D")
+    computed = [o["layer"] for o in after[:first_h2d] if o["kind"] == "COMPUTE"]
+    assert computed[:2] == [7, 6]
+    # Each trainable layer gets an UPDATE then a writeback D2H.
+    assert sum(o["kind"] == "UPDATE" for o in after) == 8
+    assert sum(o["kind"] == "D2H" for o in after) == 8
+
+
+def test_cpu_only_is_rejected_not_emulated():
+    assert sp.describe_plan(4, 8, sp.StrategyConfig(sp.CPU_ONLY)).startswith("ERROR")
