@@ -1,0 +1,351 @@
+#!/usr/bin/env python
+"""bench.py — Superpipeline layer-streaming training step on B200 (driver contract).
+
+Workload (BASELINE.json configs[1]): a GPT-2 XL-shape stack — 48 of the reference's dense
+blocks at d=1600 (LayerBlock y = relu(xW+b), model.hpp:14-26) — one bf16 training step
+(forward, MSE, reverse backward + SGD, reference_train_step semantics) streamed through a
+Superpipeline ring (k=4, k'=2) from pinned host memory. A "step" = one train step over a
+batch of ROWS synthetic rows (make_input, seed 7). Weights: build_model(7, 48, 1600).
+
+value: samples (rows) per second with x/target already in HBM (sp_train_step_device);
+e2e:   the same through the host-buffer C-ABI call (sp_train_step): x/target H2D from pinned
+       host memory and the loss D2H inside the timed region.
+Weights always stream from pinned host memory — that is the path being measured.
+
+--impl reference: the reference's own CPU implementation (oracle/_ref, built from the
+reference sources) on the host cores, same metric.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "samples/sec vs peak HBM GB at window k; % of max(FLOP, host-link bytes) roofline"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--layers", type=int, default=48)
+    p.add_argument("--d", type=int, default=1600)
+    p.add_argument("--rows", type=int, default=16384, help="batch rows per GPU per step")
+    p.add_argument("--k", type=int, default=4)
+    p.add_argument("--kp", type=int, default=2)
+    p.add_argument("--strategy", default="superpipeline",
+                   choices=["superpipeline", "standard", "naive"])
+    p.add_argument("--lr", type=float, default=0.01)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--sweep", default="", help="comma list of k:kp to report extra lines")
+    return p.parse_args()
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampler for the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm = [float(r[0]) for r in self.rows if len(r) >= 8 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 8 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            if len(r) >= 8:
+                for n, v in zip(names, r[4:8]):
+                    if "Active" in v and "Not" not in v:
+                        reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measure_link(torch, mb=256):
+    n = mb << 20
+    ha = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    hb = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    da = torch.empty(n, dtype=torch.uint8, device="cuda")
+    db = torch.empty(n, dtype=torch.uint8, device="cuda")
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+
+    def run(h2d, d2h, reps=6):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s1)
+        s2.wait_event(e0)
+        for _ in range(reps):
+            if h2d:
+                with torch.cuda.stream(s1):
+                    da.copy_(ha, non_blocking=True)
+            if d2h:
+                with torch.cuda.stream(s2):
+                    hb.copy_(db, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(s2)
+        s1.wait_event(ev)
+        e1.record(s1)
+        e1.synchronize()
+        return n * reps / (e0.elapsed_time(e1) * 1e-3) / 1e9
+
+    run(True, True, 2)
+    return {"h2d_gbs": run(True, False), "d2h_gbs": run(False, True),
+            "duplex_gbs_per_dir": run(True, True)}
+
+
+def layer_roofline(a, link, pk, rows_per_gpu):
+    """Per-layer max(FLOP at tensor peak, host-link bytes / measured pinned bandwidth), summed
+    over the step (forward: H2D fp32 layer; backward: H2D + D2H concurrently)."""
+    d, L = a.d, a.layers
+    lb = (d * d + d) * 4
+    peak = pk["bf16_tflops_sustained"] * 1e12
+    fwd = max(2.0 * rows_per_gpu * d * d / peak, lb / (link["h2d_gbs"] * 1e9))
+    bwd = max(4.0 * rows_per_gpu * d * d / peak, lb / (link["duplex_gbs_per_dir"] * 1e9))
+    first = 2.0 * rows_per_gpu * d * d / peak  # layer 0 needs no dX
+    bwd0 = max(first, lb / (link["duplex_gbs_per_dir"] * 1e9))
+    return L * fwd + (L - 1) * bwd + bwd0
+
+
+def cpu_baseline_ref(a, threads, rows_per_thread=2, layers_sample=6):
+    """The reference's reference_train_step (oracle/_ref = the reference compiled from its own
+    sources) on host cores: `threads` concurrent single-threaded replicas, each training a
+    layers_sample-layer slice of the d-wide model on rows_per_thread rows; scaled linearly in
+    layers (every block costs the same) to the full model."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from pyoracle import Reference
+    ref = Reference()
+    W, b, _ = ref.build_model(7, layers_sample, a.d)
+    xs = [ref.make_input(7, 100 + t, rows_per_thread, a.d) for t in range(threads)]
+    ts = [ref.make_input(7, 200 + t, rows_per_thread, a.d) for t in range(threads)]
+    out = [None] * threads
+
+    def work(t):
+        out[t] = ref.train_step(W, b, xs[t], ts[t], a.lr)
+
+    t0 = time.perf_counter()
+    th = [threading.Thread(target=work, args=(t,)) for t in range(threads)]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join()
+    dt = time.perf_counter() - t0
+    full = dt * a.layers / layers_sample
+    return threads * rows_per_thread / full, dt
+
+
+def run_reference(a, rank, world):
+    if rank != 0:
+        return
+    threads = max(1, min(os.cpu_count() or 1, 64))
+    rates = []
+    for i in range(a.warmup + a.steps):
+        v, dt = cpu_baseline_ref(a, threads)
+        if i >= a.warmup:
+            rates.append(v)
+    value = statistics.mean(rates)
+    sample = (f"{threads} concurrent reference_train_step replicas x 2 rows x 6 of {a.layers} "
+              f"layers (d={a.d}), time scaled x{a.layers / 6:g} to the full model")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "samples/s",
+            "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
+            "ms_per_step": 1e3 * (2 * threads) / value, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": config_of(a, world),
+            "cpu_baseline": {"value": value, "unit": "samples/s", "cores": threads,
+                             "kind": "reference", "sample": sample},
+            "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def config_of(a, world):
+    return {"workload": f"GPT-2 XL-shape layer stack: {a.layers} x d={a.d} dense ReLU blocks "
+                        f"(reference LayerBlock), bf16 train step (fwd+MSE+bwd+SGD)",
+            "layers": a.layers, "d": a.d, "rows_per_gpu": a.rows, "global_batch": a.rows * world,
+            "strategy": a.strategy, "k": a.k, "k_prime": a.kp, "transfer_mode": "batch",
+            "weights": "pinned host DRAM (fp32 master), streamed per step",
+            "parallelism": f"dp{world}", "l2": "working set (weights+activations) >> 126 MB L2"}
+
+
+def main():
+    a = parse()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    if a.impl == "reference":
+        run_reference(a, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("gloo")
+    import paper_2410_08791_b200 as sp
+    from paper_2410_08791_b200 import _capi
+
+    pk, pk_src = peaks()
+    strategy = {"superpipeline": sp.StrategyConfig(sp.SUPERPIPELINE, a.k, a.kp),
+                "standard": sp.StrategyConfig(sp.STANDARD),
+                "naive": sp.StrategyConfig(sp.NAIVE, a.k)}[a.strategy]
+    ex = sp.Executor(a.layers, a.d, strategy, numerics=sp.BF16, device=local, trace=True)
+    Wl = np.empty((a.d, a.d), np.float32)
+    bl = np.empty((a.d,), np.float32)
+    for i in range(a.layers):
+        _capi.LIB.sp_build_layer(7, i, a.d, 0, 0, Wl.ctypes.data, bl.ctypes.data)
+        ex.register_layer(i, Wl, bl)
+    if world > 1:
+        uid = [ex.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        ex.dp_init(uid[0], rank, world)
+
+    x = sp.make_input(7, 2 * rank, a.rows, a.d)
+    t = sp.make_input(7, 2 * rank + 1, a.rows, a.d)
+    x_dev = torch.from_numpy(x).cuda()
+    t_dev = torch.from_numpy(t).cuda()
+    hx = sp.HostBuffer(x.shape)
+    ht = sp.HostBuffer(t.shape)
+    hx.array[...] = x
+    ht.array[...] = t
+    link = measure_link(torch)
+    torch.cuda.synchronize()
+
+    def step_dev():
+        return ex.train_step_ptr(x_dev.data_ptr(), t_dev.data_ptr(), a.rows, a.lr, device=True)
+
+    def step_e2e():
+        return ex.train_step_ptr(hx.ptr, ht.ptr, a.rows, a.lr, device=False)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def timed(fn, collect):
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        losses = []
+        for _ in range(a.steps):
+            losses.append(fn())
+            if collect is not None:
+                collect.append(ex.stats())
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        barrier()
+        if world > 1:
+            tt = torch.tensor([ms], dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ms = float(tt.item())
+        return ms, losses
+
+    for _ in range(a.warmup):
+        step_dev()
+    step_e2e()
+    stats = []
+    with Clocks(local) as clk:
+        ms, losses = timed(step_dev, stats)
+    ms_e2e, _ = timed(step_e2e, None)
+    last = stats[-1]
+    gemm_ms = sum(s["gemm_ms"] for s in stats)
+    gemm_fl = sum(s["gemm_flops"] for s in stats)
+    gemm_n = sum(s["gemm_launches"] for s in stats)
+    achieved = gemm_fl / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else None
+    peak_tf = pk["bf16_tflops_sustained"]
+    traffic = None
+    tr_path = os.path.join(ROOT, "profiles", "gemm_traffic.json")
+    if os.path.exists(tr_path):
+        try:
+            traffic = json.load(open(tr_path)).get("bytes_per_launch")
+        except Exception:
+            traffic = None
+    step_s = ms * 1e-3 / a.steps
+    roof_s = layer_roofline(a, link, pk, a.rows)
+    value = world * a.rows * a.steps / (ms * 1e-3)
+    e2e = world * a.rows * a.steps / (ms_e2e * 1e-3)
+
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        v, dt = cpu_baseline_ref(a, 1, rows_per_thread=4, layers_sample=6)
+        cpu = {"value": v, "unit": "samples/s", "cores": 1, "kind": "reference",
+               "sample": f"reference_train_step (oracle/_ref), 4 rows x 6 of {a.layers} layers "
+                         f"d={a.d}, {dt:.1f}s, scaled x{a.layers / 6:g} in layers"}
+
+    line = {"metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms / a.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (build_model/make_input seed 7)", "config": config_of(a, world),
+            "peak_hbm_gb": {"ledger": last["peak_bytes"] / 1e9,
+                            "ledger_weights": last["peak_weight_bytes"] / 1e9,
+                            "measured_reserved": last["hbm_reserved_bytes"] / 1e9,
+                            "full_residency_weights": a.layers * (a.d * a.d + a.d) * 4 / 1e9},
+            "north_star": {"layer_roofline_ms": roof_s * 1e3, "measured_ms": step_s * 1e3,
+                           "frac_of_layer_roofline": roof_s / step_s, "link": link,
+                           "stall_ms": last["stall_ms"], "loss": losses[-1]},
+            "roofline": {"bound": "tensor", "kernel": "tcgen05 bf16 GEMM (fwd / dX / dW)",
+                         "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
+                         "frac": achieved / peak_tf if achieved else None, "traffic": traffic,
+                         "peak_source": f"{pk_src} bf16_tflops_sustained",
+                         "launches_timed": gemm_n, "gemm_share_of_step": gemm_ms / ms},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e, "unit": "samples/s",
+                    "h2d_bytes_per_step": 2 * a.rows * a.d * 4, "d2h_bytes_per_step": 4},
+            "gpu_launches": int(sum(s["kernels_launched"] for s in stats)),
+            "clocks": clk.summary()}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    ex.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

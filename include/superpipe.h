@@ -98,6 +98,11 @@ typedef struct {
     int32_t n_slots;                /* HBM ring slots S = min(k+k', n) for Superpipeline */
     char digest[17];                /* digest_tensors / digest_train of the last call */
     char _pad[3];
+    /* tcgen05 GEMM launches of the last call, each bracketed by CUDA events on the compute
+     * stream (cfg.trace = 1): count, summed device time and algorithmic FLOPs (2*M*N*K). */
+    uint64_t gemm_launches;
+    double gemm_ms;
+    double gemm_flops;
 } sp_stats;
 
 /* One timeline row (TraceEvent, trace.hpp:20-50); times in ms from the call's start. */

@@ -33,7 +33,8 @@ class SpStats(C.Structure):
         "h2d_bytes", "d2h_bytes", "hbm_reserved_bytes", "kernels_launched")] + [
         (n, C.c_double) for n in ("per_item_ms", "makespan_ms", "stall_ms", "compute_ms")] + [
         ("loss", C.c_float), ("n_slots", C.c_int32), ("digest", C.c_char * 17),
-        ("_pad", C.c_char * 3)]
+        ("_pad", C.c_char * 3), ("gemm_launches", C.c_uint64), ("gemm_ms", C.c_double),
+        ("gemm_flops", C.c_double)]
 
     def as_dict(self):
         out = {}

@@ -129,6 +129,7 @@ Executor::~Executor() {
     if (slots_dev_) cudaFree(slots_dev_);
     for (auto e : ev_done_) cudaEventDestroy(e);
     for (auto e : ev_start_) cudaEventDestroy(e);
+    for (auto e : gemm_ev_) cudaEventDestroy(e);
     if (ev_call0_) cudaEventDestroy(ev_call0_);
     if (ev_io_in_) cudaEventDestroy(ev_io_in_);
     if (ev_io_out_) cudaEventDestroy(ev_io_out_);
@@ -271,8 +272,20 @@ cudaStream_t Executor::stream_of(OpKind k) const {
 }
 
 void Executor::gemm(const GemmProblem& g, cudaStream_t st) {
+    const bool timed = cfg_.trace != 0;
+    if (timed) {
+        while (gemm_ev_.size() < 2 * (gemm_count_ + 1)) {
+            cudaEvent_t e;
+            CUDA_OK(cudaEventCreate(&e));
+            gemm_ev_.push_back(e);
+        }
+        CUDA_OK(cudaEventRecord(gemm_ev_[2 * gemm_count_], st));
+    }
     const cudaError_t e = gemm_bf16(g, st);
     if (e != cudaSuccess) throw Error(SP_ERR_CUDA, std::string("tcgen05 gemm: ") + cudaGetErrorString(e));
+    if (timed) CUDA_OK(cudaEventRecord(gemm_ev_[2 * gemm_count_ + 1], st));
+    ++gemm_count_;
+    gemm_flops_ += 2.0 * g.M * static_cast<double>(g.N) * g.K;
     ++kernels_;
 }
 
@@ -610,6 +623,15 @@ void Executor::collect_stats(const Plan& plan, int n_items, bool train) {
     stats_.stall_ms = stall;
     stats_.compute_ms = comp;
     stats_.n_slots = plan.n_slots;
+    stats_.gemm_launches = gemm_count_;
+    stats_.gemm_flops = gemm_flops_;
+    stats_.gemm_ms = 0.0;
+    if (cfg_.trace)
+        for (size_t g = 0; g < gemm_count_; ++g) {
+            float ms = 0;
+            CUDA_OK(cudaEventElapsedTime(&ms, gemm_ev_[2 * g], gemm_ev_[2 * g + 1]));
+            stats_.gemm_ms += ms;
+        }
 }
 
 void Executor::forward(const float* x, int64_t rows, int n_items, float* y, bool device_io) {
@@ -622,8 +644,7 @@ void Executor::forward(const float* x, int64_t rows, int n_items, float* y, bool
     refresh_host16();
     ensure_buffers(rows, n_items, false, device_io);
     CUDA_OK(cudaSetDevice(cfg_.device));
-    kernels_ = 0;
-    h2d_bytes_ = d2h_bytes_ = 0;
+    reset_call_counters();
     const size_t bytes = static_cast<size_t>(n_items) * rows * d_ * 4;
     CUDA_OK(cudaEventRecord(ev_call0_, s_h2d_));
     for (auto s : {s_comp_, s_d2h_, s_upd_}) CUDA_OK(cudaStreamWaitEvent(s, ev_call0_, 0));
@@ -664,8 +685,7 @@ float Executor::train_step(const float* x, const float* target, int64_t rows, fl
         splits_ = effective_splits(static_cast<int>(rows), std::min(want, splits_cap_));
         col_chunks_ = colsum_chunks(rows);
     }
-    kernels_ = 0;
-    h2d_bytes_ = d2h_bytes_ = 0;
+    reset_call_counters();
     const size_t bytes = static_cast<size_t>(rows) * d_ * 4;
     CUDA_OK(cudaEventRecord(ev_call0_, s_h2d_));
     for (auto s : {s_comp_, s_d2h_, s_upd_}) CUDA_OK(cudaStreamWaitEvent(s, ev_call0_, 0));

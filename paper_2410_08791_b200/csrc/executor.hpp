@@ -121,6 +121,15 @@ private:
     std::vector<sp_trace_event> trace_;
     uint64_t kernels_ = 0;
     uint64_t h2d_bytes_ = 0, d2h_bytes_ = 0;
+    std::vector<cudaEvent_t> gemm_ev_;  // start/end pairs around each tcgen05 GEMM launch
+    size_t gemm_count_ = 0;
+    double gemm_flops_ = 0.0;
+    void reset_call_counters() {
+        kernels_ = 0;
+        h2d_bytes_ = d2h_bytes_ = 0;
+        gemm_count_ = 0;
+        gemm_flops_ = 0.0;
+    }
 };
 
 }  // namespace sp

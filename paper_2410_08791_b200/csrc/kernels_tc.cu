@@ -397,6 +397,10 @@ bool make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, 
     CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        fprintf(stderr, "superpipe: cuTensorMapEncodeTiled failed (%d): base=%p dims={%llu,%llu} ld=%llu box={%u,%u}\n",
+                static_cast<int>(r), base, (unsigned long long)inner, (unsigned long long)outer,
+                (unsigned long long)ld, box_inner, box_outer);
     return r == CUDA_SUCCESS;
 }
 

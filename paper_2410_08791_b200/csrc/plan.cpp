@@ -400,6 +400,7 @@ private:
                     group.push_back(p);
                 }
                 release_positions(group);
+                flush_deferred();  // the next group is admitted only once this one drained
             }
             return;
         }
@@ -418,8 +419,9 @@ private:
                 if (nb < ne && misses_in(nb, ne) <= free_slots()) {
                     claim_positions(nb, ne, c);  // prefetch into slots freed one group earlier
                     release_positions(evict);
-                } else {
+                } else {  // capacity-bound: the prefetch waits for the eviction to drain
                     release_positions(evict);
+                    flush_deferred();
                     if (nb < ne) claim_positions(nb, ne, c);
                 }
                 next_load = ne;
