@@ -174,7 +174,10 @@ int64_t sp_describe_plan(const sp_config* cfg, int32_t n_items, int32_t train, c
 int sp_build_layer(uint64_t seed, int32_t index, int32_t d, int32_t fan_in, int32_t fan_out,
                    float* W, float* b);
 void sp_make_input(uint64_t seed, uint64_t tag, int64_t rows, int32_t d, float* out);
-/* digest helpers (engine.cpp:565-581): FNV-1a-64 digests as 16 hex chars + NUL. */
+/* digest helpers (engine.cpp:565-581): FNV-1a-64 digests as 16 hex chars + NUL. They are
+ * computed on demand (never inside the hot path): sp_digest_tensors over a caller's outputs,
+ * sp_digest_train over (loss, the executor's current weights) = digest_train(loss, model). */
+int sp_digest_train(const sp_exec* ex, float loss, char out[17]);
 void sp_digest_tensors(const float* values, int32_t n_items, int64_t rows, int32_t d,
                        char out[17]);
 

@@ -61,6 +61,7 @@ EXPORTS = [
     "sp_read_layer", "sp_get_stats", "sp_get_trace", "sp_nccl_unique_id", "sp_dp_init",
     "sp_host_alloc", "sp_host_free", "sp_peak_weight_residency", "sp_validate_strategy",
     "sp_describe_plan", "sp_build_layer", "sp_make_input", "sp_digest_tensors",
+    "sp_digest_train",
     "sp_debug_gemm_bf16", "sp_debug_effective_splits",
 ]
 
@@ -94,6 +95,7 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "sp_build_layer": ([u64, i32, i32, i32, i32, vp, vp], C.c_int),
         "sp_make_input": ([u64, u64, i64, i32, vp], None),
         "sp_digest_tensors": ([vp, i32, i64, i32, C.c_char_p], None),
+        "sp_digest_train": ([ex, C.c_float, C.c_char_p], C.c_int),
         "sp_debug_gemm_bf16": ([i32, i32, i32, vp, i32, i32, vp, i32, i32, i32, vp, i32, vp,
                                 i32, vp, i32, i32, i32], C.c_int),
         "sp_debug_effective_splits": ([i32, i32], i32),

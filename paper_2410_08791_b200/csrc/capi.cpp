@@ -116,6 +116,12 @@ int sp_read_layer(sp_exec* ex, int32_t index, float* W, float* b) {
     return guarded(ex, [&] { ex->impl->read_layer(index, W, b); });
 }
 
+int sp_digest_train(const sp_exec* ex, float loss, char out[17]) {
+    if (!ex || !out) return SP_ERR_INVALID;
+    ex->impl->digest_train(loss, out);
+    return SP_OK;
+}
+
 int sp_get_stats(const sp_exec* ex, sp_stats* out) {
     if (!ex || !out) return SP_ERR_INVALID;
     *out = ex->impl->stats();

@@ -666,8 +666,7 @@ void Executor::forward(const float* x, int64_t rows, int n_items, float* y, bool
     CUDA_OK(cudaGetLastError());
     collect_stats(plan, n_items, false);
     stats_.loss = 0.0f;
-    if (!device_io) sp_digest_tensors(y, n_items, rows, d_, stats_.digest);
-    else std::memset(stats_.digest, 0, sizeof(stats_.digest));
+    std::memset(stats_.digest, 0, sizeof(stats_.digest));  // on demand: sp_digest_tensors(y)
 }
 
 float Executor::train_step(const float* x, const float* target, int64_t rows, float lr,
@@ -705,27 +704,30 @@ float Executor::train_step(const float* x, const float* target, int64_t rows, fl
     collect_stats(plan, 1, true);
     const float loss = loss_host_[0] / static_cast<float>(rows * d_ * world_);
     stats_.loss = loss;
-    // digest_train (engine.cpp:574-581): loss bytes, then each block's W and b.
-    {
-        uint64_t h = 0xCBF29CE484222325ull;
-        auto fnv = [&](const void* p, size_t n) {
-            const unsigned char* c = static_cast<const unsigned char*>(p);
-            for (size_t i = 0; i < n; ++i) {
-                h ^= c[i];
-                h *= 0x100000001B3ull;
-            }
-        };
-        fnv(&loss, 4);
-        const size_t dd = static_cast<size_t>(d_) * d_;
-        fnv(host32_, static_cast<size_t>(n_) * (dd + d_) * 4);  // W_0 b_0 W_1 b_1 ... contiguous
-        static const char digits[] = "0123456789abcdef";
-        for (int i = 15; i >= 0; --i) {
-            stats_.digest[i] = digits[h & 0xF];
-            h >>= 4;
-        }
-        stats_.digest[16] = '\0';
-    }
+    std::memset(stats_.digest, 0, sizeof(stats_.digest));  // on demand: digest_train()
     return loss;
+}
+
+void Executor::digest_train(float loss, char out[17]) const {
+    // digest_train (engine.cpp:574-581): loss bytes, then each block's W and b — the host
+    // master copy is [W_0 b_0 W_1 b_1 ...] contiguous, exactly the reference's byte order.
+    uint64_t h = 0xCBF29CE484222325ull;
+    auto fnv = [&](const void* p, size_t n) {
+        const unsigned char* c = static_cast<const unsigned char*>(p);
+        for (size_t i = 0; i < n; ++i) {
+            h ^= c[i];
+            h *= 0x100000001B3ull;
+        }
+    };
+    fnv(&loss, 4);
+    const size_t dd = static_cast<size_t>(d_) * d_;
+    fnv(host32_, static_cast<size_t>(n_) * (dd + d_) * 4);
+    static const char digits[] = "0123456789abcdef";
+    for (int i = 15; i >= 0; --i) {
+        out[i] = digits[h & 0xF];
+        h >>= 4;
+    }
+    out[16] = '\0';
 }
 
 void Executor::read_layer(int index, float* W, float* b) {

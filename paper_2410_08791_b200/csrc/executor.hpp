@@ -33,6 +33,7 @@ public:
     float train_step(const float* x, const float* target, int64_t rows, float lr,
                      bool device_io);
     void read_layer(int index, float* W, float* b);
+    void digest_train(float loss, char out[17]) const;
     void dp_init(const uint8_t id[128], int rank, int world);
 
     const sp_stats& stats() const { return stats_; }

@@ -92,22 +92,57 @@ __global__ void finalize_kernel(const float* __restrict__ partials, int n, float
     if (threadIdx.x == 0) *out = s;
 }
 
-constexpr int kColRows = 256;  // rows per column-sum chunk (fixed => deterministic)
+// Column sums (db = sum_r dz[r, :]) of a bf16 [rows][d] matrix. Block = 32 column-groups of
+// 8 columns (one 16-byte load each) x 8 row-lanes; a block owns kColRows consecutive rows,
+// each row-lane sums kColRows/8 rows with independent unrolled loads, then the 8 lanes are
+// combined in a fixed order in shared memory -> partials[chunk][d]. Deterministic.
+constexpr int kColRows = 128;
+constexpr int kColLanes = 8;
 
-__global__ void colsum_kernel(const __nv_bfloat16* __restrict__ x, int64_t rows, int d,
-                              float* __restrict__ partials) {
-    const int c2 = blockIdx.x * blockDim.x + threadIdx.x;  // column pair
-    if (2 * c2 >= d) return;
+__global__ void __launch_bounds__(256) colsum_kernel(const __nv_bfloat16* __restrict__ x,
+                                                     int64_t rows, int d,
+                                                     float* __restrict__ partials) {
+    __shared__ float red[kColLanes][32][9];
+    const int g = blockIdx.x * 32 + threadIdx.x;  // 8-column group
+    const int lane_r = threadIdx.y;
     const int64_t r0 = static_cast<int64_t>(blockIdx.y) * kColRows;
-    const int64_t r1 = (r0 + kColRows) < rows ? (r0 + kColRows) : rows;
-    float a = 0.0f, b = 0.0f;
-    for (int64_t r = r0; r < r1; ++r) {
-        const float2 v = __bfloat1622float2(reinterpret_cast<const __nv_bfloat162*>(x + r * d)[c2]);
-        a += v.x;
-        b += v.y;
+    float acc[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
+    if (8 * g < d) {
+        constexpr int per = kColRows / kColLanes;
+        uint4 v[per];
+#pragma unroll
+        for (int i = 0; i < per; ++i) {
+            const int64_t r = r0 + lane_r + static_cast<int64_t>(i) * kColLanes;
+            v[i] = r < rows ? __ldg(reinterpret_cast<const uint4*>(x + r * d) + g) : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int i = 0; i < per; ++i) {
+            const uint32_t w[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[h]));
+                acc[2 * h] += f.x;
+                acc[2 * h + 1] += f.y;
+            }
+        }
     }
-    partials[static_cast<int64_t>(blockIdx.y) * d + 2 * c2] = a;
-    partials[static_cast<int64_t>(blockIdx.y) * d + 2 * c2 + 1] = b;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) red[lane_r][threadIdx.x][i] = acc[i];
+    __syncthreads();
+    if (lane_r == 0 && 8 * g < d) {
+        float out[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            float s = red[0][threadIdx.x][i];
+            for (int l = 1; l < kColLanes; ++l) s += red[l][threadIdx.x][i];
+            out[i] = s;
+        }
+        float4* dst = reinterpret_cast<float4*>(partials + static_cast<int64_t>(blockIdx.y) * d + 8 * g);
+        dst[0] = make_float4(out[0], out[1], out[2], out[3]);
+        dst[1] = make_float4(out[4], out[5], out[6], out[7]);
+    }
 }
 
 __global__ void reduce_kernel(const float* __restrict__ parts, int nparts, int64_t stride,
@@ -190,9 +225,10 @@ void loss_finalize(const float* partials, int n, float* out, cudaStream_t st) {
 int colsum_chunks(int64_t rows) { return static_cast<int>((rows + kColRows - 1) / kColRows); }
 
 int colsum_bf16(const void* x, int64_t rows, int d, float* partials, cudaStream_t st) {
-    const int chunks = colsum_chunks(rows);
-    dim3 grid((d / 2 + 127) / 128, chunks);
-    colsum_kernel<<<grid, 128, 0, st>>>(static_cast<const __nv_bfloat16*>(x), rows, d, partials);
+    const int chunks = colsum_chunks(rows);  // requires d % 8 == 0 (bf16 path: d % 64 == 0)
+    dim3 grid((d / 8 + 31) / 32, chunks);
+    colsum_kernel<<<grid, dim3(32, kColLanes), 0, st>>>(static_cast<const __nv_bfloat16*>(x),
+                                                       rows, d, partials);
     return chunks;
 }
 
