@@ -141,6 +141,47 @@ def measure_link(torch, mb=256):
             "duplex_gbs_per_dir": run(True, True)}
 
 
+def gemm_kernel_timing(torch, capi, a, reps=20):
+    """Average device time per launch of the step's three tcgen05 GEMM shapes (forward
+    y = relu(xW + b), dX = (dz W^T) . [x > 0], dW with fused SGD), launched back to back on
+    the current stream between two CUDA events, with operands of the step's exact shape."""
+    rows, d = a.rows, a.d
+    x = torch.randn(rows, d, device="cuda").to(torch.bfloat16)
+    dz = torch.randn(rows, d, device="cuda").to(torch.bfloat16) * 1e-3
+    W = torch.randn(d, d, device="cuda").to(torch.bfloat16)
+    W32 = torch.randn(d, d, device="cuda")
+    bias = torch.randn(d, device="cuda")
+    out = torch.empty(rows, d, device="cuda", dtype=torch.bfloat16)
+    st = torch.cuda.current_stream().cuda_stream
+    L = capi.LIB
+    shapes = {
+        "fwd": (lambda: L.sp_debug_gemm_bf16_async(rows, d, d, x.data_ptr(), d, 0, W.data_ptr(), d,
+                                                   1, 0, out.data_ptr(), d, bias.data_ptr(), 1,
+                                                   None, 0, 1, 0, st), a.layers),
+        "dx": (lambda: L.sp_debug_gemm_bf16_async(rows, d, d, dz.data_ptr(), d, 0, W.data_ptr(), d,
+                                                  0, 2, out.data_ptr(), d, None, 1, x.data_ptr(),
+                                                  d, 1, 0, st), a.layers - 1),
+        "dw_sgd": (lambda: L.sp_debug_gemm_bf16_async(d, d, rows, x.data_ptr(), d, 1,
+                                                      dz.data_ptr(), d, 1, 4, W32.data_ptr(), d,
+                                                      None, 0, None, 0, 1, 0, st), a.layers),
+    }
+    res = {}
+    for name, (fn, per_step) in shapes.items():
+        for _ in range(3):
+            assert fn() == 0
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        e1.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        fl = 2.0 * rows * d * d
+        res[name] = {"ms": ms, "flops": fl, "tflops": fl / ms / 1e9, "per_step": per_step}
+    return res
+
+
 def layer_roofline(a, link, pk, rows_per_gpu):
     """Per-layer max(FLOP at tensor peak, host-link bytes / measured pinned bandwidth), summed
     over the step (forward: H2D fp32 layer; backward: H2D + D2H concurrently)."""
@@ -235,7 +276,7 @@ def main():
     strategy = {"superpipeline": sp.StrategyConfig(sp.SUPERPIPELINE, a.k, a.kp),
                 "standard": sp.StrategyConfig(sp.STANDARD),
                 "naive": sp.StrategyConfig(sp.NAIVE, a.k)}[a.strategy]
-    ex = sp.Executor(a.layers, a.d, strategy, numerics=sp.BF16, device=local, trace=True)
+    ex = sp.Executor(a.layers, a.d, strategy, numerics=sp.BF16, device=local, trace=0)
     Wl = np.empty((a.d, a.d), np.float32)
     bl = np.empty((a.d,), np.float32)
     for i in range(a.layers):
@@ -295,10 +336,16 @@ def main():
         ms, losses = timed(step_dev, stats)
     ms_e2e, _ = timed(step_e2e, None)
     last = stats[-1]
-    gemm_ms = sum(s["gemm_ms"] for s in stats)
-    gemm_fl = sum(s["gemm_flops"] for s in stats)
-    gemm_n = sum(s["gemm_launches"] for s in stats)
-    achieved = gemm_fl / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else None
+    # One extra step with the per-op CUDA-event timeline (not timed): stall / compute split.
+    ex.set_trace(1)
+    step_dev()
+    traced = ex.stats()
+    ex.set_trace(0)
+    gemm = gemm_kernel_timing(torch, _capi, a)
+    gemm_fl = sum(g["flops"] * g["per_step"] for g in gemm.values())
+    gemm_s = sum(g["ms"] * 1e-3 * g["per_step"] for g in gemm.values())
+    achieved = gemm_fl / gemm_s / 1e12
+    gemm_n = sum(g["per_step"] for g in gemm.values())
     peak_tf = pk["bf16_tflops_sustained"]
     traffic = None
     tr_path = os.path.join(ROOT, "profiles", "gemm_traffic.json")
@@ -329,12 +376,18 @@ def main():
                             "full_residency_weights": a.layers * (a.d * a.d + a.d) * 4 / 1e9},
             "north_star": {"layer_roofline_ms": roof_s * 1e3, "measured_ms": step_s * 1e3,
                            "frac_of_layer_roofline": roof_s / step_s, "link": link,
-                           "stall_ms": last["stall_ms"], "loss": losses[-1]},
+                           "traced_step": {k: traced[k] for k in (
+                               "makespan_ms", "compute_ms", "stall_ms", "per_item_ms",
+                               "h2d_bytes", "d2h_bytes", "n_slots", "graph_replays")},
+                           "loss": losses[-1]},
             "roofline": {"bound": "tensor", "kernel": "tcgen05 bf16 GEMM (fwd / dX / dW)",
                          "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
-                         "frac": achieved / peak_tf if achieved else None, "traffic": traffic,
+                         "frac": achieved / peak_tf, "traffic": traffic,
                          "peak_source": f"{pk_src} bf16_tflops_sustained",
-                         "launches_timed": gemm_n, "gemm_share_of_step": gemm_ms / ms},
+                         "per_shape": gemm, "launches_per_step": gemm_n,
+                         "gemm_share_of_step": gemm_s / step_s,
+                         "method": "CUDA events around 20 back-to-back launches per shape on the "
+                                   "launching stream, step-weighted by launches per step"},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e, "unit": "samples/s",
                     "h2d_bytes_per_step": 2 * a.rows * a.d * 4, "d2h_bytes_per_step": 4},

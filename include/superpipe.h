@@ -70,7 +70,9 @@ typedef struct {
     int32_t numerics;       /* sp_numerics */
     int32_t checkpointing;  /* training: offload saved activations with their layer */
     int32_t device;         /* CUDA ordinal */
-    int32_t trace;          /* 1: record per-op CUDA-event timeline (sp_get_trace) */
+    int32_t trace;          /* 0: call makespan only; 1: + per-op CUDA-event timeline
+                               (sp_get_trace, stall/per-item figures); 2: + per-GEMM events
+                               (each event record costs device time between kernels) */
     uint64_t capacity_bytes; /* ledger budget in reference bytes; 0 = unlimited */
 } sp_config;
 
@@ -103,6 +105,10 @@ typedef struct {
     uint64_t gemm_launches;
     double gemm_ms;
     double gemm_flops;
+    /* host time to enqueue (or replay) the call, and how many calls so far were replayed from
+     * a captured CUDA graph (the plan is static, so repeated steps are one graph launch). */
+    double host_enqueue_ms;
+    uint64_t graph_replays;
 } sp_stats;
 
 /* One timeline row (TraceEvent, trace.hpp:20-50); times in ms from the call's start. */
@@ -146,6 +152,8 @@ int sp_read_layer(sp_exec* ex, int32_t index, float* W, float* b);
 
 /* ---- metrics ----------------------------------------------------------------------- */
 int sp_get_stats(const sp_exec* ex, sp_stats* out);
+/* Changes the trace level (sp_config.trace) for subsequent calls. */
+int sp_set_trace(sp_exec* ex, int32_t level);
 /* Copies up to cap events of the last call's measured timeline; *count = total rows. */
 int sp_get_trace(const sp_exec* ex, sp_trace_event* events, int32_t cap, int32_t* count);
 

@@ -21,6 +21,13 @@ int sp_debug_gemm_bf16(int32_t M, int32_t N, int32_t K, const void* A, int32_t l
                        const void* B, int32_t ldb, int32_t b_mn, int32_t epilogue, void* out,
                        int32_t ldo, const float* bias, int32_t relu, const void* gate,
                        int32_t ldg, int32_t splits, int32_t block_n);
+/* Same, launched asynchronously on `stream` (a cudaStream_t) without synchronising, for
+ * back-to-back timing of the kernel between two CUDA events. */
+int sp_debug_gemm_bf16_async(int32_t M, int32_t N, int32_t K, const void* A, int32_t lda,
+                             int32_t a_mn, const void* B, int32_t ldb, int32_t b_mn,
+                             int32_t epilogue, void* out, int32_t ldo, const float* bias,
+                             int32_t relu, const void* gate, int32_t ldg, int32_t splits,
+                             int32_t block_n, void* stream);
 /* Split count the GEMM will use for a given K and requested splits. */
 int32_t sp_debug_effective_splits(int32_t K, int32_t splits);
 

@@ -34,7 +34,8 @@ class SpStats(C.Structure):
         (n, C.c_double) for n in ("per_item_ms", "makespan_ms", "stall_ms", "compute_ms")] + [
         ("loss", C.c_float), ("n_slots", C.c_int32), ("digest", C.c_char * 17),
         ("_pad", C.c_char * 3), ("gemm_launches", C.c_uint64), ("gemm_ms", C.c_double),
-        ("gemm_flops", C.c_double)]
+        ("gemm_flops", C.c_double), ("host_enqueue_ms", C.c_double),
+        ("graph_replays", C.c_uint64)]
 
     def as_dict(self):
         out = {}
@@ -58,11 +59,12 @@ class SpTraceEvent(C.Structure):
 EXPORTS = [
     "sp_create", "sp_register_layer", "sp_destroy", "sp_last_error", "sp_abi_version",
     "sp_forward", "sp_forward_device", "sp_train_step", "sp_train_step_device",
-    "sp_read_layer", "sp_get_stats", "sp_get_trace", "sp_nccl_unique_id", "sp_dp_init",
+    "sp_read_layer", "sp_get_stats", "sp_get_trace", "sp_set_trace", "sp_nccl_unique_id",
+    "sp_dp_init",
     "sp_host_alloc", "sp_host_free", "sp_peak_weight_residency", "sp_validate_strategy",
     "sp_describe_plan", "sp_build_layer", "sp_make_input", "sp_digest_tensors",
     "sp_digest_train",
-    "sp_debug_gemm_bf16", "sp_debug_effective_splits",
+    "sp_debug_gemm_bf16", "sp_debug_gemm_bf16_async", "sp_debug_effective_splits",
 ]
 
 
@@ -85,6 +87,7 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "sp_read_layer": ([ex, i32, vp, vp], C.c_int),
         "sp_get_stats": ([ex, C.POINTER(SpStats)], C.c_int),
         "sp_get_trace": ([ex, C.POINTER(SpTraceEvent), i32, C.POINTER(i32)], C.c_int),
+        "sp_set_trace": ([ex, i32], C.c_int),
         "sp_nccl_unique_id": ([C.c_char_p], C.c_int),
         "sp_dp_init": ([ex, C.c_char_p, i32, i32], C.c_int),
         "sp_host_alloc": ([u64], vp),
@@ -98,6 +101,8 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "sp_digest_train": ([ex, C.c_float, C.c_char_p], C.c_int),
         "sp_debug_gemm_bf16": ([i32, i32, i32, vp, i32, i32, vp, i32, i32, i32, vp, i32, vp,
                                 i32, vp, i32, i32, i32], C.c_int),
+        "sp_debug_gemm_bf16_async": ([i32, i32, i32, vp, i32, i32, vp, i32, i32, i32, vp, i32,
+                                      vp, i32, vp, i32, i32, i32, vp], C.c_int),
         "sp_debug_effective_splits": ([i32, i32], i32),
     }
     for name, (args, res) in sig.items():

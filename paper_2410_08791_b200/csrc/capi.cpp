@@ -116,6 +116,12 @@ int sp_read_layer(sp_exec* ex, int32_t index, float* W, float* b) {
     return guarded(ex, [&] { ex->impl->read_layer(index, W, b); });
 }
 
+int sp_set_trace(sp_exec* ex, int32_t level) {
+    if (!ex || level < 0 || level > 2) return SP_ERR_INVALID;
+    ex->impl->set_trace(level);
+    return SP_OK;
+}
+
 int sp_digest_train(const sp_exec* ex, float loss, char out[17]) {
     if (!ex || !out) return SP_ERR_INVALID;
     ex->impl->digest_train(loss, out);
@@ -224,6 +230,35 @@ void sp_digest_tensors(const float* values, int32_t n_items, int64_t rows, int32
 // ---- kernel-level debug entry points (include/superpipe_debug.h) ----------------------
 #include "../../include/superpipe_debug.h"
 #include "kernels.hpp"
+
+extern "C" int sp_debug_gemm_bf16_async(int32_t M, int32_t N, int32_t K, const void* A,
+                                        int32_t lda, int32_t a_mn, const void* B, int32_t ldb,
+                                        int32_t b_mn, int32_t epilogue, void* out, int32_t ldo,
+                                        const float* bias, int32_t relu, const void* gate,
+                                        int32_t ldg, int32_t splits, int32_t block_n,
+                                        void* stream) {
+    sp::GemmProblem g;
+    g.M = M;
+    g.N = N;
+    g.K = K;
+    g.A = A;
+    g.lda = lda;
+    g.a_mn = a_mn != 0;
+    g.B = B;
+    g.ldb = ldb;
+    g.b_mn = b_mn != 0;
+    g.epilogue = epilogue;
+    g.out = out;
+    g.ldo = ldo;
+    g.bias = bias;
+    g.relu = relu;
+    g.gate = gate;
+    g.ldg = ldg;
+    g.splits = splits;
+    g.split_stride = static_cast<int64_t>(M) * ldo;
+    g.block_n = block_n;
+    return static_cast<int>(sp::gemm_bf16(g, static_cast<cudaStream_t>(stream)));
+}
 
 extern "C" int sp_debug_gemm_bf16(int32_t M, int32_t N, int32_t K, const void* A, int32_t lda,
                                   int32_t a_mn, const void* B, int32_t ldb, int32_t b_mn,

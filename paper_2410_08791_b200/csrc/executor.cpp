@@ -14,7 +14,9 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <thread>
 
@@ -109,8 +111,12 @@ Executor::Executor(const sp_config& cfg) : cfg_(cfg) {
     CUDA_OK(cudaStreamCreateWithFlags(&s_d2h_, cudaStreamNonBlocking));
     CUDA_OK(cudaStreamCreateWithFlags(&s_upd_, cudaStreamNonBlocking));
     CUDA_OK(cudaEventCreate(&ev_call0_));
+    CUDA_OK(cudaEventCreate(&ev_call1_));
     CUDA_OK(cudaEventCreateWithFlags(&ev_io_in_, cudaEventDisableTiming));
     CUDA_OK(cudaEventCreateWithFlags(&ev_io_out_, cudaEventDisableTiming));
+    CUDA_OK(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
+    for (auto& e : ev_join_) CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    if (const char* g = std::getenv("SUPERPIPE_GRAPHS")) use_graphs_ = std::atoi(g) != 0;
     CUDA_OK(cudaHostAlloc(&loss_host_, 16, cudaHostAllocPortable));
 
     relu_.assign(static_cast<size_t>(n_), 1);
@@ -130,7 +136,13 @@ Executor::~Executor() {
     for (auto e : ev_done_) cudaEventDestroy(e);
     for (auto e : ev_start_) cudaEventDestroy(e);
     for (auto e : gemm_ev_) cudaEventDestroy(e);
+    for (auto e : ev_dep_) cudaEventDestroy(e);
+    for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second.exec);
+    if (ev_fork_) cudaEventDestroy(ev_fork_);
+    for (auto e : ev_join_)
+        if (e) cudaEventDestroy(e);
     if (ev_call0_) cudaEventDestroy(ev_call0_);
+    if (ev_call1_) cudaEventDestroy(ev_call1_);
     if (ev_io_in_) cudaEventDestroy(ev_io_in_);
     if (ev_io_out_) cudaEventDestroy(ev_io_out_);
     if (host32_) cudaFreeHost(host32_);
@@ -188,6 +200,7 @@ void Executor::ensure_buffers(int64_t rows, int n_items, bool train, bool device
     const bool fits = rows <= cap_rows_ && n_items <= cap_items_ && (!train || cap_train_);
     if (fits && (!ckpt || host_act_)) return;
     CUDA_OK(cudaDeviceSynchronize());
+    ++alloc_gen_;  // captured graphs refer to the old buffers
     for (void* p : dev_allocs_) cudaFree(p);
     dev_allocs_.clear();
     dev_bytes_ = 0;
@@ -261,6 +274,11 @@ Plan Executor::make_plan(bool train, int n_items, int64_t rows, int fmt) {
     return plan;
 }
 
+void Executor::record_timing(cudaEvent_t ev, cudaStream_t st) {
+    if (capturing_) CUDA_OK(cudaEventRecordWithFlags(ev, st, cudaEventRecordExternal));
+    else CUDA_OK(cudaEventRecord(ev, st));
+}
+
 cudaStream_t Executor::stream_of(OpKind k) const {
     switch (k) {
         case OpKind::H2D: return s_h2d_;
@@ -272,18 +290,19 @@ cudaStream_t Executor::stream_of(OpKind k) const {
 }
 
 void Executor::gemm(const GemmProblem& g, cudaStream_t st) {
-    const bool timed = cfg_.trace != 0;
+    const bool timed = cfg_.trace >= 2;  // per-GEMM events perturb the stream: opt-in only
     if (timed) {
         while (gemm_ev_.size() < 2 * (gemm_count_ + 1)) {
             cudaEvent_t e;
             CUDA_OK(cudaEventCreate(&e));
             gemm_ev_.push_back(e);
         }
-        CUDA_OK(cudaEventRecord(gemm_ev_[2 * gemm_count_], st));
+        record_timing(gemm_ev_[2 * gemm_count_], st);
     }
     const cudaError_t e = gemm_bf16(g, st);
     if (e != cudaSuccess) throw Error(SP_ERR_CUDA, std::string("tcgen05 gemm: ") + cudaGetErrorString(e));
-    if (timed) CUDA_OK(cudaEventRecord(gemm_ev_[2 * gemm_count_ + 1], st));
+    if (timed)
+        record_timing(gemm_ev_[2 * gemm_count_ + 1], st);
     ++gemm_count_;
     gemm_flops_ += 2.0 * g.M * static_cast<double>(g.N) * g.K;
     ++kernels_;
@@ -419,14 +438,20 @@ void Executor::compute_op(const Op& op, bool train, int64_t rows, int fmt) {
     g.B = dz;  // dz [r][j]: N-major B
     g.ldb = d_;
     g.b_mn = true;
-    g.epilogue = EPI_F32;
-    g.out = ws;
+    // One GPU: no gradient exchange, so SGD is fused into the dW epilogue (W -= lr*acc on the
+    // slot's fp32 master; splits = 1 keeps each element owned by one CTA). Data parallel: raw
+    // split-K partials, reduced + all-reduced + applied on the update stream.
+    const bool fused = comm_ == nullptr;
+    g.epilogue = fused ? EPI_SGD_F32 : EPI_F32;
+    g.out = fused ? static_cast<void*>(slot_w32(s)) : static_cast<void*>(ws);
     g.ldo = d_;
-    g.splits = splits_;
+    g.splits = fused ? 1 : splits_;
     g.split_stride = static_cast<int64_t>(dd);
     g.block_n = dw_bn_;
+    g.lr = cur_lr_;
     gemm(g, st);
-    colsum_bf16(dz, rows, d_, ws + static_cast<size_t>(splits_) * dd, st);
+    if (fused) w16_layer_[s] = -1;
+    colsum_bf16(dz, rows, d_, ws + (fused ? 0 : static_cast<size_t>(splits_) * dd), st);
     ++kernels_;
 }
 
@@ -456,10 +481,9 @@ void Executor::update_op(const Op& op, float lr) {
         if (comm_) NCCL_OK(nccl().AllReduce(ws, ws, dd + d_, ncclFloat, ncclSum, comm_, st));
         exact_sgd(slot_w32(s), ws, static_cast<int64_t>(dd + d_), lr, st);  // [W|b] contiguous
         ++kernels_;
-    } else if (!comm_) {
-        sgd_reduce(slot_w32(s), ws, splits_, static_cast<int64_t>(dd), static_cast<int64_t>(dd), lr, st);
-        sgd_reduce(slot_b32(s), ws + splits_ * dd, col_chunks_, d_, d_, lr, st);
-        kernels_ += 2;
+    } else if (!comm_) {  // W already updated in the dW epilogue; bias from the db partials
+        sgd_reduce(slot_b32(s), ws, col_chunks_, d_, d_, lr, st);
+        kernels_ += 1;
     } else {
         reduce_partials(ws, splits_, static_cast<int64_t>(dd), static_cast<int64_t>(dd), grad_red_, st);
         reduce_partials(ws + splits_ * dd, col_chunks_, d_, d_, grad_red_ + dd, st);
@@ -477,9 +501,11 @@ void Executor::enqueue_op(const Plan& plan, int i, bool train, int n_items, int6
     cudaStream_t st = stream_of(op.kind);
     for (int dep : op.deps) {
         if (stream_of(plan.ops[static_cast<size_t>(dep)].kind) != st)
-            CUDA_OK(cudaStreamWaitEvent(st, ev_done_[static_cast<size_t>(dep)], 0));
+            CUDA_OK(cudaStreamWaitEvent(st, ev_dep_[static_cast<size_t>(dep)], 0));
     }
-    CUDA_OK(cudaEventRecord(ev_start_[static_cast<size_t>(i)], st));
+    // Timing events are "external" so that, under graph capture, they become event-record
+    // nodes; the dependency events (ev_dep_) become graph edges.
+    if (cfg_.trace >= 1) record_timing(ev_start_[static_cast<size_t>(i)], st);
     const size_t dd = static_cast<size_t>(d_) * d_;
     const size_t act_b = static_cast<size_t>(rows) * d_ * (bf16_ ? 2 : 4);
     switch (op.kind) {
@@ -529,40 +555,178 @@ void Executor::enqueue_op(const Plan& plan, int i, bool train, int n_items, int6
             d2h_bytes_ += act_b;
             break;
     }
-    CUDA_OK(cudaEventRecord(ev_done_[static_cast<size_t>(i)], st));
+    if (cfg_.trace >= 1) record_timing(ev_done_[static_cast<size_t>(i)], st);
+    if (cross_dep_[static_cast<size_t>(i)]) CUDA_OK(cudaEventRecord(ev_dep_[static_cast<size_t>(i)], st));
 }
 
-void Executor::run_plan(const Plan& plan, bool train, int n_items, int64_t rows, float lr,
-                        int fmt) {
-    while (ev_done_.size() < plan.ops.size()) {
-        cudaEvent_t a, b;
+// Everything one call puts on the device, from the timing base to the final join: the input
+// copies, every op of the plan, the output copy. Enqueued eagerly or captured into a graph.
+void Executor::enqueue_call(const Plan& plan, const CallIO& io) {
+    // Dependency events only where another stream waits on the op (every event record on
+    // the compute stream costs device time between kernels).
+    cross_dep_.assign(plan.ops.size(), 0);
+    for (size_t j = 0; j < plan.ops.size(); ++j)
+        for (int dep : plan.ops[j].deps)
+            if (stream_of(plan.ops[static_cast<size_t>(dep)].kind) != stream_of(plan.ops[j].kind))
+                cross_dep_[static_cast<size_t>(dep)] = 1;
+    record_timing(ev_call0_, s_h2d_);
+    CUDA_OK(cudaEventRecord(ev_fork_, s_h2d_));
+    for (auto s : {s_comp_, s_d2h_, s_upd_}) CUDA_OK(cudaStreamWaitEvent(s, ev_fork_, 0));
+    const size_t act = static_cast<size_t>(io.rows) * d_ * 4;
+    if (!io.device_io) {
+        CUDA_OK(cudaMemcpyAsync(xin_, io.x, act * (io.train ? 1 : io.n_items), cudaMemcpyHostToDevice, s_comp_));
+        if (io.train) CUDA_OK(cudaMemcpyAsync(tgt_, io.t, act, cudaMemcpyHostToDevice, s_comp_));
+    }
+    for (size_t i = 0; i < plan.ops.size(); ++i)
+        enqueue_op(plan, static_cast<int>(i), io.train, io.n_items, io.rows, io.lr, io.fmt);
+    if (!io.device_io && !io.train) {
+        CUDA_OK(cudaEventRecord(ev_io_out_, s_comp_));
+        CUDA_OK(cudaStreamWaitEvent(s_d2h_, ev_io_out_, 0));
+        CUDA_OK(cudaMemcpyAsync(io.y, yout_, act * io.n_items, cudaMemcpyDeviceToHost, s_d2h_));
+    }
+    int k = 0;
+    for (auto s : {s_comp_, s_d2h_, s_upd_}) {
+        CUDA_OK(cudaEventRecord(ev_join_[k], s));
+        CUDA_OK(cudaStreamWaitEvent(s_h2d_, ev_join_[k], 0));
+        ++k;
+    }
+    record_timing(ev_call1_, s_h2d_);  // all streams joined: the call's device makespan
+}
+
+namespace {
+bool pinned_or_null(const void* p) {
+    if (!p) return true;
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeDevice ||
+           a.type == cudaMemoryTypeManaged;
+}
+}  // namespace
+
+uint64_t Executor::call_signature(const Plan& plan, const CallIO& io) const {
+    uint64_t h = 0xCBF29CE484222325ull;
+    auto mix = [&](uint64_t v) {
+        for (int b = 0; b < 8; ++b) {
+            h ^= (v >> (8 * b)) & 0xFF;
+            h *= 0x100000001B3ull;
+        }
+    };
+    for (const Op& op : plan.ops) {
+        mix(static_cast<uint64_t>(op.kind) | static_cast<uint64_t>(op.pass) << 8 |
+            static_cast<uint64_t>(static_cast<uint32_t>(op.layer)) << 16 |
+            static_cast<uint64_t>(static_cast<uint32_t>(op.slot)) << 40);
+        mix(static_cast<uint64_t>(static_cast<uint32_t>(op.item)));
+        for (size_t j = 0; j < op.layers.size(); ++j)
+            mix(static_cast<uint64_t>(op.layers[j]) << 32 | static_cast<uint32_t>(op.slots[j]) |
+                static_cast<uint64_t>(op.weights[j]) << 62 | static_cast<uint64_t>(op.acts[j]) << 63);
+        for (int dep : op.deps) mix(static_cast<uint64_t>(dep) | 1ull << 60);
+    }
+    uint32_t lr_bits;
+    std::memcpy(&lr_bits, &io.lr, 4);
+    mix(static_cast<uint64_t>(io.train) | static_cast<uint64_t>(io.device_io) << 1 |
+        static_cast<uint64_t>(io.fmt) << 2 | static_cast<uint64_t>(lr_bits) << 32);
+    mix(static_cast<uint64_t>(io.rows));
+    mix(static_cast<uint64_t>(io.n_items));
+    mix(reinterpret_cast<uintptr_t>(io.x));
+    mix(reinterpret_cast<uintptr_t>(io.t));
+    mix(reinterpret_cast<uintptr_t>(io.y));
+    for (int v : w16_layer_) mix(static_cast<uint64_t>(static_cast<uint32_t>(v)));
+    mix(static_cast<uint64_t>(splits_) | static_cast<uint64_t>(col_chunks_) << 32);
+    mix(reinterpret_cast<uintptr_t>(comm_));
+    mix(alloc_gen_);
+    mix(static_cast<uint64_t>(cfg_.trace));
+    return h;
+}
+
+void Executor::run_call(const Plan& plan, const CallIO& io) {
+    const size_t need = plan.ops.size();
+    while (ev_done_.size() < need) {
+        cudaEvent_t a, b, c;
         CUDA_OK(cudaEventCreate(&a));
         CUDA_OK(cudaEventCreate(&b));
+        CUDA_OK(cudaEventCreateWithFlags(&c, cudaEventDisableTiming));
         ev_done_.push_back(a);
         ev_start_.push_back(b);
+        ev_dep_.push_back(c);
     }
-    int first_compute = -1;
-    for (size_t i = 0; i < plan.ops.size(); ++i)
-        if (plan.ops[i].kind == OpKind::Compute) {
-            first_compute = static_cast<int>(i);
-            break;
+    const bool graphable = use_graphs_ && (io.device_io || (pinned_or_null(io.x) &&
+                                                            pinned_or_null(io.t) &&
+                                                            pinned_or_null(io.y)));
+    if (!graphable) {
+        enqueue_call(plan, io);
+    } else {
+        const uint64_t sig = call_signature(plan, io);
+        auto it = graphs_.find(sig);
+        if (it != graphs_.end()) {
+            // Replay: one launch for the whole step; re-apply the host-side effects the
+            // captured enqueue had (bf16-copy tracking, stale inference wire, counters).
+            const GraphEntry& g = it->second;
+            CUDA_OK(cudaGraphLaunch(g.exec, s_h2d_));
+            w16_layer_ = g.w16_after;
+            for (int L : g.stale_layers) host16_stale_[static_cast<size_t>(L)] = 1;
+            kernels_ = g.kernels;
+            h2d_bytes_ = g.h2d_bytes;
+            d2h_bytes_ = g.d2h_bytes;
+            gemm_count_ = g.gemm_count;
+            gemm_flops_ = g.gemm_flops;
+            ++graph_replays_;
+        } else {
+            if (graphs_.size() >= 16) {
+                for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second.exec);
+                graphs_.clear();
+            }
+            CUDA_OK(cudaStreamBeginCapture(s_h2d_, cudaStreamCaptureModeThreadLocal));
+            capturing_ = true;
+            try {
+                enqueue_call(plan, io);
+            } catch (...) {
+                capturing_ = false;
+                cudaGraph_t broken = nullptr;
+                cudaStreamEndCapture(s_h2d_, &broken);
+                if (broken) cudaGraphDestroy(broken);
+                cudaGetLastError();
+                throw;
+            }
+            capturing_ = false;
+            cudaGraph_t graph = nullptr;
+            CUDA_OK(cudaStreamEndCapture(s_h2d_, &graph));
+            GraphEntry g;
+            const cudaError_t ie = cudaGraphInstantiate(&g.exec, graph, 0);
+            cudaGraphDestroy(graph);
+            CUDA_OK(ie);
+            g.w16_after = w16_layer_;
+            for (const Op& op : plan.ops)
+                if (op.kind == OpKind::D2H) g.stale_layers.push_back(op.layers[0]);
+            g.kernels = kernels_;
+            g.h2d_bytes = h2d_bytes_;
+            g.d2h_bytes = d2h_bytes_;
+            g.gemm_count = gemm_count_;
+            g.gemm_flops = gemm_flops_;
+            CUDA_OK(cudaGraphLaunch(g.exec, s_h2d_));
+            graphs_.emplace(sig, std::move(g));
         }
-    (void)first_compute;
-    for (size_t i = 0; i < plan.ops.size(); ++i)
-        enqueue_op(plan, static_cast<int>(i), train, n_items, rows, lr, fmt);
+    }
     cache_ = plan.final_slots;
-    cache_fmt_ = fmt;
+    cache_fmt_ = io.fmt;
 }
 
 void Executor::collect_stats(const Plan& plan, int n_items, bool train) {
     trace_.clear();
     double first_c = -1, last_c = 0, makespan = 0, stall = 0, comp = 0, prev_end = -1;
-    for (size_t i = 0; i < plan.ops.size(); ++i) {
+    {
+        float call = 0;
+        CUDA_OK(cudaEventElapsedTime(&call, ev_call0_, ev_call1_));
+        makespan = call;
+    }
+    const size_t timed_ops = cfg_.trace >= 1 ? plan.ops.size() : 0;
+    for (size_t i = 0; i < timed_ops; ++i) {
         const Op& op = plan.ops[i];
         float t0 = 0, t1 = 0;
         CUDA_OK(cudaEventElapsedTime(&t0, ev_call0_, ev_start_[i]));
         CUDA_OK(cudaEventElapsedTime(&t1, ev_call0_, ev_done_[i]));
-        makespan = std::max(makespan, static_cast<double>(t1));
         sp_trace_event ev{};
         ev.t_start = t0;
         ev.t_end = t1;
@@ -623,10 +787,12 @@ void Executor::collect_stats(const Plan& plan, int n_items, bool train) {
     stats_.stall_ms = stall;
     stats_.compute_ms = comp;
     stats_.n_slots = plan.n_slots;
+    stats_.host_enqueue_ms = host_enqueue_ms_;
+    stats_.graph_replays = graph_replays_;
     stats_.gemm_launches = gemm_count_;
     stats_.gemm_flops = gemm_flops_;
     stats_.gemm_ms = 0.0;
-    if (cfg_.trace)
+    if (cfg_.trace >= 2)
         for (size_t g = 0; g < gemm_count_; ++g) {
             float ms = 0;
             CUDA_OK(cudaEventElapsedTime(&ms, gemm_ev_[2 * g], gemm_ev_[2 * g + 1]));
@@ -645,23 +811,12 @@ void Executor::forward(const float* x, int64_t rows, int n_items, float* y, bool
     ensure_buffers(rows, n_items, false, device_io);
     CUDA_OK(cudaSetDevice(cfg_.device));
     reset_call_counters();
-    const size_t bytes = static_cast<size_t>(n_items) * rows * d_ * 4;
-    CUDA_OK(cudaEventRecord(ev_call0_, s_h2d_));
-    for (auto s : {s_comp_, s_d2h_, s_upd_}) CUDA_OK(cudaStreamWaitEvent(s, ev_call0_, 0));
-    if (device_io) {
-        cur_x_ = x;
-        cur_y_ = y;
-    } else {
-        CUDA_OK(cudaMemcpyAsync(xin_, x, bytes, cudaMemcpyHostToDevice, s_comp_));
-        cur_x_ = xin_;
-        cur_y_ = yout_;
-    }
-    run_plan(plan, false, n_items, rows, 0.0f, fmt);
-    if (!device_io) {
-        CUDA_OK(cudaEventRecord(ev_io_out_, s_comp_));
-        CUDA_OK(cudaStreamWaitEvent(s_d2h_, ev_io_out_, 0));
-        CUDA_OK(cudaMemcpyAsync(y, yout_, bytes, cudaMemcpyDeviceToHost, s_d2h_));
-    }
+    cur_x_ = device_io ? x : xin_;
+    cur_y_ = device_io ? y : yout_;
+    CallIO io{false, n_items, rows, 0.0f, fmt, device_io, x, nullptr, y};
+    const auto t0 = std::chrono::steady_clock::now();
+    run_call(plan, io);
+    host_enqueue_ms_ = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     for (auto s : {s_h2d_, s_comp_, s_d2h_, s_upd_}) CUDA_OK(cudaStreamSynchronize(s));
     CUDA_OK(cudaGetLastError());
     collect_stats(plan, n_items, false);
@@ -685,20 +840,14 @@ float Executor::train_step(const float* x, const float* target, int64_t rows, fl
         col_chunks_ = colsum_chunks(rows);
     }
     reset_call_counters();
-    const size_t bytes = static_cast<size_t>(rows) * d_ * 4;
-    CUDA_OK(cudaEventRecord(ev_call0_, s_h2d_));
-    for (auto s : {s_comp_, s_d2h_, s_upd_}) CUDA_OK(cudaStreamWaitEvent(s, ev_call0_, 0));
-    if (device_io) {
-        cur_x_ = x;
-        cur_t_ = target;
-    } else {
-        CUDA_OK(cudaMemcpyAsync(xin_, x, bytes, cudaMemcpyHostToDevice, s_comp_));
-        CUDA_OK(cudaMemcpyAsync(tgt_, target, bytes, cudaMemcpyHostToDevice, s_comp_));
-        cur_x_ = xin_;
-        cur_t_ = tgt_;
-    }
+    cur_x_ = device_io ? x : xin_;
+    cur_t_ = device_io ? target : tgt_;
     if (cache_fmt_ != fmt) std::fill(w16_layer_.begin(), w16_layer_.end(), -1);
-    run_plan(plan, true, 1, rows, lr, fmt);
+    cur_lr_ = lr;
+    CallIO io{true, 1, rows, lr, fmt, device_io, x, target, nullptr};
+    const auto t0 = std::chrono::steady_clock::now();
+    run_call(plan, io);
+    host_enqueue_ms_ = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     for (auto s : {s_h2d_, s_comp_, s_d2h_, s_upd_}) CUDA_OK(cudaStreamSynchronize(s));
     CUDA_OK(cudaGetLastError());
     collect_stats(plan, 1, true);

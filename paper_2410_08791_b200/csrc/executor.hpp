@@ -7,6 +7,7 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/superpipe.h"
@@ -34,6 +35,7 @@ public:
                      bool device_io);
     void read_layer(int index, float* W, float* b);
     void digest_train(float loss, char out[17]) const;
+    void set_trace(int level) { cfg_.trace = level; }
     void dp_init(const uint8_t id[128], int rank, int world);
 
     const sp_stats& stats() const { return stats_; }
@@ -52,11 +54,36 @@ private:
         return reinterpret_cast<float*>(slot_ptr(s) + off_w16_ + static_cast<size_t>(d_) * d_ * 2);
     }
 
+    // What one call moves across the host boundary (user pointers; device or host).
+    struct CallIO {
+        bool train;
+        int n_items;
+        int64_t rows;
+        float lr;
+        int fmt;
+        bool device_io;
+        const float* x;
+        const float* t;
+        float* y;
+    };
+    // A captured step: replayed with one cudaGraphLaunch while the call signature (plan,
+    // pointers, lr, bf16-copy state, buffers) is unchanged.
+    struct GraphEntry {
+        cudaGraphExec_t exec = nullptr;
+        std::vector<int> w16_after;
+        std::vector<int> stale_layers;
+        uint64_t kernels = 0, h2d_bytes = 0, d2h_bytes = 0;
+        size_t gemm_count = 0;
+        double gemm_flops = 0.0;
+    };
+
     void check_ready() const;
     void ensure_buffers(int64_t rows, int n_items, bool train, bool device_io);
     void refresh_host16();
     Plan make_plan(bool train, int n_items, int64_t rows, int fmt);
-    void run_plan(const Plan& plan, bool train, int n_items, int64_t rows, float lr, int fmt);
+    void enqueue_call(const Plan& plan, const CallIO& io);
+    void run_call(const Plan& plan, const CallIO& io);
+    uint64_t call_signature(const Plan& plan, const CallIO& io) const;
     void enqueue_op(const Plan& plan, int i, bool train, int n_items, int64_t rows, float lr,
                     int fmt);
     void compute_op(const Op& op, bool train, int64_t rows, int fmt);
@@ -84,8 +111,20 @@ private:
     std::vector<int> w16_layer_;  // bf16 training: layer whose bf16 copy is current per slot
     // streams / events
     cudaStream_t s_h2d_ = nullptr, s_comp_ = nullptr, s_d2h_ = nullptr, s_upd_ = nullptr;
-    std::vector<cudaEvent_t> ev_done_, ev_start_;
+    std::vector<cudaEvent_t> ev_done_, ev_start_;  // per-op timing (external records)
+    std::vector<cudaEvent_t> ev_dep_;              // per-op dependency edges
     cudaEvent_t ev_call0_ = nullptr, ev_io_in_ = nullptr, ev_io_out_ = nullptr;
+    cudaEvent_t ev_fork_ = nullptr, ev_join_[3] = {nullptr, nullptr, nullptr};
+    cudaEvent_t ev_call1_ = nullptr;
+    std::vector<uint8_t> cross_dep_;  // op has a dependent on another stream
+    bool use_graphs_ = true;
+    bool capturing_ = false;
+    // Timing events: plain records when eager; "external" event-record nodes under capture
+    // (cudaEventRecordExternal is only valid while capturing).
+    void record_timing(cudaEvent_t ev, cudaStream_t st);
+    std::unordered_map<uint64_t, GraphEntry> graphs_;
+    uint64_t alloc_gen_ = 0;
+    uint64_t graph_replays_ = 0;
     // activations / workspaces (device)
     int64_t cap_rows_ = 0;
     int cap_items_ = 0;
@@ -112,6 +151,8 @@ private:
     const float* cur_x_ = nullptr;
     float* cur_y_ = nullptr;
     const float* cur_t_ = nullptr;
+    float cur_lr_ = 0.0f;
+    double host_enqueue_ms_ = 0.0;
     int splits_ = 1, dw_bn_ = 256, col_chunks_ = 1, splits_cap_ = 1, col_chunks_cap_ = 1;
     int loss_blocks_ = 0;
     // data parallel

@@ -30,7 +30,8 @@ enum GemmEpilogue : int {
     EPI_BIAS_ACT_BF16 = 0,  // out(bf16) = act(acc + bias)
     EPI_BIAS_ACT_F32 = 1,   // out(f32)  = act(acc + bias)
     EPI_GATE_BF16 = 2,      // out(bf16) = (relu && gate <= 0) ? 0 : acc
-    EPI_F32 = 3             // out(f32)  = acc  (split-K partial at out + split*split_stride)
+    EPI_F32 = 3,            // out(f32)  = acc  (split-K partial at out + split*split_stride)
+    EPI_SGD_F32 = 4         // out(f32) -= lr * acc  (fused SGD on the fp32 master; splits == 1)
 };
 
 struct GemmProblem {
@@ -53,6 +54,7 @@ struct GemmProblem {
     int splits = 1;
     int64_t split_stride = 0;
     int block_n = 0;  // 0 = choose
+    float lr = 0.0f;  // EPI_SGD_F32
 };
 
 // Launches the warp-specialized tcgen05/TMEM/TMA GEMM. Returns cudaSuccess or an error.

@@ -19,6 +19,7 @@
 
 #include <cstdio>
 #include <mutex>
+#include <unordered_map>
 
 #include "kernels.hpp"
 
@@ -51,6 +52,7 @@ struct Params {
     const __nv_bfloat16* gate;
     int ldg;
     long long split_stride;
+    float lr;
 };
 
 // ---------------------------------------------------------------------------------------
@@ -343,6 +345,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                                            pack_bf16(v[8 * i + 2], v[8 * i + 3]),
                                            pack_bf16(v[8 * i + 4], v[8 * i + 5]),
                                            pack_bf16(v[8 * i + 6], v[8 * i + 7]));
+                } else if (EPI == EPI_SGD_F32) {
+                    // fused SGD (apply_sgd, model.cpp:150-155): w -= lr * dW, no FMA, in place
+                    // on the slot's fp32 master weights; the tile is owned by this CTA alone.
+                    float4* wp = reinterpret_cast<float4*>(static_cast<float*>(p.out) +
+                                                           static_cast<long long>(row) * p.ldo + col0);
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        float4 w = wp[i];
+                        w.x = __fsub_rn(w.x, __fmul_rn(p.lr, v[4 * i + 0]));
+                        w.y = __fsub_rn(w.y, __fmul_rn(p.lr, v[4 * i + 1]));
+                        w.z = __fsub_rn(w.z, __fmul_rn(p.lr, v[4 * i + 2]));
+                        w.w = __fsub_rn(w.w, __fmul_rn(p.lr, v[4 * i + 3]));
+                        wp[i] = w;
+                    }
                 } else {
                     float* base = static_cast<float*>(p.out) +
                                   (EPI == EPI_F32 ? split * p.split_stride : 0LL) +
@@ -386,8 +402,50 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
+bool encode_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint64_t ld,
+                uint32_t box_inner, uint32_t box_outer);
+
+// Tensor maps depend only on (address, shape, box): the ring slots, activation buffers and
+// workspaces have fixed addresses, so each map is encoded once and reused by every step.
 bool make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint64_t ld,
               uint32_t box_inner, uint32_t box_outer) {
+    struct Key {
+        const void* base;
+        uint64_t inner, outer, ld;
+        uint32_t bi, bo;
+        bool operator==(const Key& o) const {
+            return base == o.base && inner == o.inner && outer == o.outer && ld == o.ld &&
+                   bi == o.bi && bo == o.bo;
+        }
+    };
+    struct Hash {
+        size_t operator()(const Key& k) const {
+            size_t h = reinterpret_cast<size_t>(k.base);
+            for (uint64_t v : {k.inner, k.outer, k.ld, static_cast<uint64_t>(k.bi) << 32 | k.bo})
+                h = h * 1000003u ^ static_cast<size_t>(v);
+            return h;
+        }
+    };
+    static std::mutex mu;
+    static std::unordered_map<Key, CUtensorMap, Hash> cache;
+    const Key key{base, inner, outer, ld, box_inner, box_outer};
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        auto it = cache.find(key);
+        if (it != cache.end()) {
+            *m = it->second;
+            return true;
+        }
+    }
+    if (!encode_map(m, base, inner, outer, ld, box_inner, box_outer)) return false;
+    std::lock_guard<std::mutex> lock(mu);
+    if (cache.size() > 8192) cache.clear();
+    cache.emplace(key, *m);
+    return true;
+}
+
+bool encode_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint64_t ld,
+                uint32_t box_inner, uint32_t box_outer) {
     auto fn = encode_fn();
     if (!fn) return false;
     cuuint64_t dims[2] = {inner, outer};
@@ -438,6 +496,8 @@ cudaError_t launch(const GemmProblem& g, cudaStream_t st) {
     p.gate = static_cast<const __nv_bfloat16*>(g.gate);
     p.ldg = g.ldg;
     p.split_stride = g.split_stride;
+    p.lr = g.lr;
+    if (EPI == EPI_SGD_F32 && p.splits != 1) return cudaErrorInvalidValue;
     const int total = p.m_tiles * p.n_tiles * p.splits;
     const int grid = total < num_sms() ? total : num_sms();
     kern<<<grid, kThreads, C::SMEM, st>>>(ta, tb, p);
@@ -450,6 +510,7 @@ cudaError_t dispatch_bn(const GemmProblem& g, cudaStream_t st) {
     if (!g.a_mn && g.b_mn && g.epilogue == EPI_BIAS_ACT_F32) return launch<BN, false, true, EPI_BIAS_ACT_F32>(g, st);
     if (!g.a_mn && !g.b_mn && g.epilogue == EPI_GATE_BF16) return launch<BN, false, false, EPI_GATE_BF16>(g, st);
     if (g.a_mn && g.b_mn && g.epilogue == EPI_F32) return launch<BN, true, true, EPI_F32>(g, st);
+    if (g.a_mn && g.b_mn && g.epilogue == EPI_SGD_F32) return launch<BN, true, true, EPI_SGD_F32>(g, st);
     if (!g.a_mn && !g.b_mn && g.epilogue == EPI_F32) return launch<BN, false, false, EPI_F32>(g, st);
     if (!g.a_mn && g.b_mn && g.epilogue == EPI_F32) return launch<BN, false, true, EPI_F32>(g, st);
     return cudaErrorNotSupported;

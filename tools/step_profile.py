@@ -15,7 +15,8 @@ import paper_2410_08791_b200 as sp  # noqa: E402
 from paper_2410_08791_b200 import _capi  # noqa: E402
 
 L, d, rows, k, kp = (int(v) for v in (sys.argv[1:6] if len(sys.argv) > 5 else (48, 1600, 16384, 4, 2)))
-ex = sp.Executor(L, d, sp.StrategyConfig(sp.SUPERPIPELINE, k, kp), numerics=sp.BF16, trace=True)
+ex = sp.Executor(L, d, sp.StrategyConfig(sp.SUPERPIPELINE, k, kp), numerics=sp.BF16,
+                 trace=os.environ.get("TRACE", "1") != "0")
 W = np.empty((d, d), np.float32)
 b = np.empty((d,), np.float32)
 for i in range(L):
@@ -30,7 +31,7 @@ for i in range(3):
     st = ex.stats()
     print(json.dumps({"step": i, "host_s": host, "loss": loss, "makespan_ms": st["makespan_ms"],
                       "compute_ms": st["compute_ms"], "stall_ms": st["stall_ms"],
-                      "gemm_ms": st["gemm_ms"], "kernels": st["kernels_launched"],
+                      "gemm_ms": st["gemm_ms"], "kernels": st["kernels_launched"], "enqueue_ms": st["host_enqueue_ms"], "replays": st["graph_replays"],
                       "h2d_bytes": st["h2d_bytes"], "d2h_bytes": st["d2h_bytes"]}))
 tr = ex.trace()
 agg = defaultdict(lambda: [0, 0.0, 0.0])
