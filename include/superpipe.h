@@ -173,8 +173,8 @@ uint64_t sp_peak_weight_residency(int32_t strategy, int32_t k, int32_t k_prime,
 int sp_validate_strategy(int32_t strategy, int32_t k, int32_t k_prime, int32_t n_layers);
 /* Describes the static op plan the executor would run (policy_step, scheduler.cpp:53-141,
  * resolved ahead of time) as text, one op per line; returns the needed length. Host-only. */
-int64_t sp_describe_plan(const sp_config* cfg, int32_t n_items, int32_t train, char* buf,
-                         int64_t cap);
+int64_t sp_describe_plan(const sp_config* cfg, int32_t n_items, int32_t train,
+                         const int32_t* frozen, char* buf, int64_t cap);
 /* Deterministic layer / input generators of the reference (host-only), so callers can
  * register synthetic models without a second copy: build_model's per-layer splitmix64 stream
  * (model.cpp:23-52, W[fan_in][fan_out] then b[fan_out], U(+-1/sqrt(fan_in)); fan_in = fan_out

@@ -94,7 +94,7 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "sp_host_free": ([vp], None),
         "sp_peak_weight_residency": ([i32, i32, i32, i32, u64], u64),
         "sp_validate_strategy": ([i32, i32, i32, i32], C.c_int),
-        "sp_describe_plan": ([C.POINTER(SpConfig), i32, i32, C.c_char_p, i64], i64),
+        "sp_describe_plan": ([C.POINTER(SpConfig), i32, i32, vp, C.c_char_p, i64], i64),
         "sp_build_layer": ([u64, i32, i32, i32, i32, vp, vp], C.c_int),
         "sp_make_input": ([u64, u64, i64, i32, vp], None),
         "sp_digest_tensors": ([vp, i32, i64, i32, C.c_char_p], None),

@@ -176,8 +176,8 @@ int sp_validate_strategy(int32_t strategy, int32_t k, int32_t k_prime, int32_t n
     return sp::validate_strategy(strategy, k, k_prime, n_layers).empty() ? SP_OK : SP_ERR_INVALID;
 }
 
-int64_t sp_describe_plan(const sp_config* cfg, int32_t n_items, int32_t train, char* buf,
-                         int64_t cap) {
+int64_t sp_describe_plan(const sp_config* cfg, int32_t n_items, int32_t train,
+                         const int32_t* frozen, char* buf, int64_t cap) {
     if (!cfg) return -1;
     sp::PlanInput in;
     in.n_layers = cfg->n_layers;
@@ -191,6 +191,8 @@ int64_t sp_describe_plan(const sp_config* cfg, int32_t n_items, int32_t train, c
     in.layer_bytes = (static_cast<uint64_t>(cfg->d) * cfg->d + cfg->d) * 4;
     in.act_bytes = static_cast<uint64_t>(cfg->d) * 4;  // one row per item
     in.capacity = cfg->capacity_bytes;
+    if (frozen)
+        for (int32_t l = 0; l < cfg->n_layers; ++l) in.frozen.push_back(frozen[l] != 0);
     sp::Plan plan = sp::build_plan(in, {});
     std::string text = plan.error.empty() ? sp::describe_plan(plan) : ("ERROR " + plan.error + "\n");
     if (buf && cap > 0) {

@@ -179,6 +179,27 @@ __global__ void sgd_reduce_kernel(float* __restrict__ w, const float* __restrict
     }
 }
 
+// w[j] -= lr * sum_p parts[p*stride + j] for a short vector (the bias) with many partials:
+// 32 columns x 8 lanes per block, each lane sums every 8th partial, lanes combined in a fixed
+// order. Deterministic and latency-tolerant (independent loads per lane).
+__global__ void __launch_bounds__(256) sgd_reduce_narrow_kernel(float* __restrict__ w,
+                                                                const float* __restrict__ parts,
+                                                                int nparts, int64_t stride,
+                                                                int64_t count, float lr) {
+    __shared__ float red[8][33];
+    const int64_t j = static_cast<int64_t>(blockIdx.x) * 32 + threadIdx.x;
+    float s = 0.0f;
+    if (j < count)
+        for (int p = threadIdx.y; p < nparts; p += 8) s += parts[p * stride + j];
+    red[threadIdx.y][threadIdx.x] = s;
+    __syncthreads();
+    if (threadIdx.y == 0 && j < count) {
+        float t = red[0][threadIdx.x];
+        for (int l = 1; l < 8; ++l) t += red[l][threadIdx.x];
+        w[j] = __fsub_rn(w[j], __fmul_rn(lr, t));
+    }
+}
+
 __global__ void scale_kernel(float* __restrict__ x, int64_t count, float s) {
     const int64_t gs = static_cast<int64_t>(gridDim.x) * blockDim.x;
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += gs)
@@ -239,6 +260,11 @@ void reduce_partials(const float* parts, int nparts, int64_t stride, int64_t cou
 
 void sgd_reduce(float* w, const float* parts, int nparts, int64_t stride, int64_t count,
                 float lr, cudaStream_t st) {
+    if (count <= 65536 && nparts > 8) {  // short vector, many partials (bias from colsum)
+        sgd_reduce_narrow_kernel<<<static_cast<unsigned>((count + 31) / 32), dim3(32, 8), 0, st>>>(
+            w, parts, nparts, stride, count, lr);
+        return;
+    }
     sgd_reduce_kernel<<<grid_for(count / 4 + 1), kThreads, 0, st>>>(w, parts, nparts, stride,
                                                                      count, lr);
 }

@@ -96,6 +96,7 @@ public:
                               initial[s].layer < n_;
         }
         ba_busy_.assign(static_cast<std::size_t>(n_slots), -1);
+        act_save_op_.assign(static_cast<std::size_t>(n_), -1);
         if (in_.train) {
             std::vector<int> fwd(n_), bwd(n_);
             for (int i = 0; i < n_; ++i) fwd[i] = i, bwd[i] = n_ - 1 - i;
@@ -276,6 +277,10 @@ private:
                 op.acts.push_back(m.act);
                 if (m.weights && slots_[m.slot].busy_op >= 0) op.deps.push_back(slots_[m.slot].busy_op);
                 if (m.act && ba_busy_[m.slot] >= 0) op.deps.push_back(ba_busy_[m.slot]);
+                // The reload reads the pinned copy written by this layer's forward offload
+                // (the reference only reloads once act_on_host_ is set, engine.cpp:397-402).
+                const int saved = act_save_op_[static_cast<size_t>(seq()[m.pos])];
+                if (m.act && saved >= 0) op.deps.push_back(saved);
                 plan_.h2d_weight_layers += m.weights;
                 plan_.h2d_act_layers += m.act;
             }
@@ -350,6 +355,7 @@ private:
             save.layer = L;
             save.deps.push_back(id);
             fa_busy_[L % 3] = push(std::move(save));
+            act_save_op_[static_cast<size_t>(L)] = fa_busy_[L % 3];
             plan_.d2h_act_layers += 1;
         }
         if (grad) {
@@ -437,6 +443,7 @@ private:
     std::vector<std::vector<int>> seqs_;
     std::vector<int> pos_slot_, pos_load_, pos_act_;
     std::vector<int> ba_busy_;
+    std::vector<int> act_save_op_;  // per layer: the forward ActSave op (offload to host)
     int fa_busy_[3] = {-1, -1, -1};
     int gws_busy_[2] = {-1, -1};
     int pass_ = 0;
@@ -495,7 +502,8 @@ std::string describe_plan(const Plan& plan) {
         if (op.kind == OpKind::Compute)
             os << " pos=" << op.position << " item=" << op.item << " layer=" << op.layer
                << " slot=" << op.slot;
-        if (op.kind == OpKind::Update || op.kind == OpKind::ActSave) os << " layer=" << op.layer;
+        if (op.kind == OpKind::Update) os << " layer=" << op.layer << " slot=" << op.slot;
+        if (op.kind == OpKind::ActSave) os << " layer=" << op.layer;
         if (op.kind == OpKind::H2D || op.kind == OpKind::D2H) {
             std::vector<int> w(op.weights.begin(), op.weights.end()),
                 a(op.acts.begin(), op.acts.end());
