@@ -282,10 +282,9 @@ def main():
     for i in range(a.layers):
         _capi.LIB.sp_build_layer(7, i, a.d, 0, 0, Wl.ctypes.data, bl.ctypes.data)
         ex.register_layer(i, Wl, bl)
+    from paper_2410_08791_b200 import dp
     if world > 1:
-        uid = [ex.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        ex.dp_init(uid[0], rank, world)
+        dp.init_executor_dp(ex, dist, rank, world)  # per-layer NCCL all-reduce of dW/db
 
     x = sp.make_input(7, 2 * rank, a.rows, a.d)
     t = sp.make_input(7, 2 * rank + 1, a.rows, a.d)
@@ -323,9 +322,7 @@ def main():
         ms = e0.elapsed_time(e1)
         barrier()
         if world > 1:
-            tt = torch.tensor([ms], dtype=torch.float64)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            ms = float(tt.item())
+            ms = dp.max_over_ranks(dist, torch, ms)
         return ms, losses
 
     for _ in range(a.warmup):
