@@ -276,12 +276,20 @@ def main():
     strategy = {"superpipeline": sp.StrategyConfig(sp.SUPERPIPELINE, a.k, a.kp),
                 "standard": sp.StrategyConfig(sp.STANDARD),
                 "naive": sp.StrategyConfig(sp.NAIVE, a.k)}[a.strategy]
-    ex = sp.Executor(a.layers, a.d, strategy, numerics=sp.BF16, device=local, trace=0)
-    Wl = np.empty((a.d, a.d), np.float32)
-    bl = np.empty((a.d,), np.float32)
+    weights = []  # build_model(7, layers, d) — generated once, registered per executor
     for i in range(a.layers):
+        Wl = np.empty((a.d, a.d), np.float32)
+        bl = np.empty((a.d,), np.float32)
         _capi.LIB.sp_build_layer(7, i, a.d, 0, 0, Wl.ctypes.data, bl.ctypes.data)
-        ex.register_layer(i, Wl, bl)
+        weights.append((Wl, bl))
+
+    def make_executor(strat):
+        e = sp.Executor(a.layers, a.d, strat, numerics=sp.BF16, device=local, trace=0)
+        for i, (Wl, bl) in enumerate(weights):
+            e.register_layer(i, Wl, bl)
+        return e
+
+    ex = make_executor(strategy)
     from paper_2410_08791_b200 import dp
     if world > 1:
         dp.init_executor_dp(ex, dist, rank, world)  # per-layer NCCL all-reduce of dW/db
@@ -393,6 +401,45 @@ def main():
     if rank == 0:
         print(json.dumps(line), flush=True)
     ex.close()
+
+    # Optional window sweep (BASELINE configs[1]: "window sweep k=1..8"): extra lines, each a
+    # separately timed run of the same step; k=1 is the reference's Naive(1) (Superpipeline
+    # needs 0 < k' < k, strategy.cpp:29-33).
+    for spec in [s for s in a.sweep.split(",") if s]:
+        if spec == "standard":
+            strat, k, kp = sp.StrategyConfig(sp.STANDARD), a.layers, 0
+        else:
+            k, kp = (int(v) for v in spec.split(":"))
+            strat = (sp.StrategyConfig(sp.NAIVE, k) if kp == 0
+                     else sp.StrategyConfig(sp.SUPERPIPELINE, k, kp))
+        e = make_executor(strat)
+        if world > 1:
+            dp.init_executor_dp(e, dist, rank, world)
+        for _ in range(a.warmup):
+            e.train_step_ptr(x_dev.data_ptr(), t_dev.data_ptr(), a.rows, a.lr, device=True)
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(a.steps):
+            e.train_step_ptr(x_dev.data_ptr(), t_dev.data_ptr(), a.rows, a.lr, device=True)
+        e1.record()
+        torch.cuda.synchronize()
+        sms = e0.elapsed_time(e1)
+        if world > 1:
+            sms = dp.max_over_ranks(dist, torch, sms)
+        st = e.stats()
+        if rank == 0:
+            print(json.dumps({
+                "sweep": spec, "strategy": ["standard", "cpu_only", "naive", "superpipeline"][strat.kind],
+                "k": k, "k_prime": kp, "value": world * a.rows * a.steps / (sms * 1e-3),
+                "unit": "samples/s", "ms_per_step": sms / a.steps, "n_slots": st["n_slots"],
+                "peak_hbm_gb": {"ledger_weights": st["peak_weight_bytes"] / 1e9,
+                                "ledger": st["peak_bytes"] / 1e9,
+                                "measured_reserved": st["hbm_reserved_bytes"] / 1e9},
+                "h2d_gb_per_step": st["h2d_bytes"] / 1e9, "d2h_gb_per_step": st["d2h_bytes"] / 1e9,
+                "layer_roofline_ms": roof_s * 1e3}), flush=True)
+        e.close()
     if world > 1:
         dist.destroy_process_group()
 

@@ -1,0 +1,93 @@
+"""Superpipeline inference (run_inference path, bf16 tcgen05) on the BASELINE inference
+configs with the reference's square dense blocks:
+  c1   12 x d=768,  4 items x 1 row,  SP(2,1)         (configs[0] shape, latency-bound)
+  c1b  12 x d=768,  1 item x 4096 rows, SP(2,1)
+  c3   32 x d=4096, 1 item x 65536 rows (32 x 2048), SP(4,2)   (Llama-3-8B depth/width)
+  c5   80 x d=8192, 1 item x 8192 rows, SP(8,k') sweep, capacity 40 GB (Llama-3-70B depth/width)
+Weights: build_model(7, n, d) (splitmix64, generated in parallel threads); bf16 on the wire.
+Prints one JSON line per run: samples/s (rows/s), ms/call, per-layer roofline, HBM."""
+import argparse
+import json
+import os
+import sys
+import threading
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch  # noqa: E402
+
+import paper_2410_08791_b200 as sp  # noqa: E402
+from paper_2410_08791_b200 import _capi  # noqa: E402
+
+CONFIGS = {
+    "c1": dict(n=12, d=768, items=4, rows=1, windows=[(2, 1)]),
+    "c1b": dict(n=12, d=768, items=1, rows=4096, windows=[(2, 1), (4, 2)]),
+    "c3": dict(n=32, d=4096, items=1, rows=65536, windows=[(4, 2)]),
+    "c5": dict(n=80, d=8192, items=1, rows=8192, windows=[(8, 1), (8, 2), (8, 4), (12, 6)],
+               capacity=40 << 30),
+}
+
+
+def build_weights(n, d, threads=16):
+    out = [None] * n
+
+    def work(lo):
+        for i in range(lo, n, threads):
+            W = np.empty((d, d), np.float32)
+            b = np.empty((d,), np.float32)
+            _capi.LIB.sp_build_layer(7, i, d, 0, 0, W.ctypes.data, b.ctypes.data)
+            out[i] = (W, b)
+
+    th = [threading.Thread(target=work, args=(t,)) for t in range(threads)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    return out
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("configs", nargs="*", default=["c1", "c1b", "c3"])
+    p.add_argument("--steps", type=int, default=5)
+    a = p.parse_args()
+    peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["bf16_tflops_sustained"] * 1e12
+    for name in a.configs:
+        c = CONFIGS[name]
+        n, d, items, rows = c["n"], c["d"], c["items"], c["rows"]
+        weights = build_weights(n, d)
+        x = torch.from_numpy(np.stack([sp.make_input(7, i, rows, d) for i in range(items)])).cuda()
+        y = torch.empty_like(x)
+        for k, kp in c["windows"]:
+            ex = sp.Executor(n, d, sp.StrategyConfig(sp.SUPERPIPELINE, k, kp), numerics=sp.BF16,
+                             trace=0, capacity_bytes=c.get("capacity", 0))
+            for i, (W, b) in enumerate(weights):
+                ex.register_layer(i, W, b)
+            for _ in range(2):
+                ex.forward_ptr(x.data_ptr(), rows, items, y.data_ptr(), device=True)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(a.steps):
+                ex.forward_ptr(x.data_ptr(), rows, items, y.data_ptr(), device=True)
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / a.steps
+            st = ex.stats()
+            wire = d * d * 2 + d * 4
+            roof = items * n * max(2.0 * rows * d * d / peak, wire / 55.5e9) * 1e3
+            print(json.dumps({
+                "config": name, "layers": n, "d": d, "items": items, "rows": rows, "k": k,
+                "k_prime": kp, "ms_per_call": ms, "samples_per_s": items * rows / (ms * 1e-3),
+                "layer_roofline_ms": roof, "frac_of_roofline": roof / ms,
+                "n_slots": st["n_slots"], "peak_weight_gb": st["peak_weight_bytes"] / 1e9,
+                "hbm_reserved_gb": st["hbm_reserved_bytes"] / 1e9,
+                "full_residency_bf16_gb": n * wire / 1e9,
+                "h2d_gb_per_call": st["h2d_bytes"] / 1e9}), flush=True)
+            ex.close()
+
+
+if __name__ == "__main__":
+    main()
