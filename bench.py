@@ -157,13 +157,13 @@ def gemm_kernel_timing(torch, capi, a, reps=20):
     shapes = {
         "fwd": (lambda: L.sp_debug_gemm_bf16_async(rows, d, d, x.data_ptr(), d, 0, W.data_ptr(), d,
                                                    1, 0, out.data_ptr(), d, bias.data_ptr(), 1,
-                                                   None, 0, 1, 0, st), a.layers),
+                                                   None, 0, 1, 0, 0, st), a.layers),
         "dx": (lambda: L.sp_debug_gemm_bf16_async(rows, d, d, dz.data_ptr(), d, 0, W.data_ptr(), d,
                                                   0, 2, out.data_ptr(), d, None, 1, x.data_ptr(),
-                                                  d, 1, 0, st), a.layers - 1),
+                                                  d, 1, 0, 0, st), a.layers - 1),
         "dw_sgd": (lambda: L.sp_debug_gemm_bf16_async(d, d, rows, x.data_ptr(), d, 1,
                                                       dz.data_ptr(), d, 1, 4, W32.data_ptr(), d,
-                                                      None, 0, None, 0, 1, 0, st), a.layers),
+                                                      None, 0, None, 0, 1, 0, 0, st), a.layers),
     }
     res = {}
     for name, (fn, per_step) in shapes.items():

@@ -16,18 +16,20 @@ extern "C" {
 /* C[M,N] = A[M,K] B[K,N] with bf16 A/B. a_mn: A stored [K][lda] (M contiguous) instead of
  * [M][lda]; b_mn: B stored [K][ldb] (N contiguous) instead of [N][ldb]. epilogue: 0 bf16
  * act(acc+bias), 1 fp32 act(acc+bias), 2 bf16 ReLU-gated by `gate`, 3 fp32 split-K partials
- * (split s at out + s*M*ldo). Returns 0 or a cudaError_t value. */
+ * (split s at out + s*M*ldo), 4 fp32 out -= lr*acc with lr = 1 (fused SGD). block_n: tile N
+ * (0 = choose); cta: 1 = one CTA per 128-row tile, 2 = CTA pair per 256-row tile (cta_group::2),
+ * 0 = choose. Returns 0 or a cudaError_t value. */
 int sp_debug_gemm_bf16(int32_t M, int32_t N, int32_t K, const void* A, int32_t lda, int32_t a_mn,
                        const void* B, int32_t ldb, int32_t b_mn, int32_t epilogue, void* out,
                        int32_t ldo, const float* bias, int32_t relu, const void* gate,
-                       int32_t ldg, int32_t splits, int32_t block_n);
+                       int32_t ldg, int32_t splits, int32_t block_n, int32_t cta);
 /* Same, launched asynchronously on `stream` (a cudaStream_t) without synchronising, for
  * back-to-back timing of the kernel between two CUDA events. */
 int sp_debug_gemm_bf16_async(int32_t M, int32_t N, int32_t K, const void* A, int32_t lda,
                              int32_t a_mn, const void* B, int32_t ldb, int32_t b_mn,
                              int32_t epilogue, void* out, int32_t ldo, const float* bias,
                              int32_t relu, const void* gate, int32_t ldg, int32_t splits,
-                             int32_t block_n, void* stream);
+                             int32_t block_n, int32_t cta, void* stream);
 /* Split count the GEMM will use for a given K and requested splits. */
 int32_t sp_debug_effective_splits(int32_t K, int32_t splits);
 

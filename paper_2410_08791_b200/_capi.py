@@ -100,9 +100,9 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "sp_digest_tensors": ([vp, i32, i64, i32, C.c_char_p], None),
         "sp_digest_train": ([ex, C.c_float, C.c_char_p], C.c_int),
         "sp_debug_gemm_bf16": ([i32, i32, i32, vp, i32, i32, vp, i32, i32, i32, vp, i32, vp,
-                                i32, vp, i32, i32, i32], C.c_int),
+                                i32, vp, i32, i32, i32, i32], C.c_int),
         "sp_debug_gemm_bf16_async": ([i32, i32, i32, vp, i32, i32, vp, i32, i32, i32, vp, i32,
-                                      vp, i32, vp, i32, i32, i32, vp], C.c_int),
+                                      vp, i32, vp, i32, i32, i32, i32, vp], C.c_int),
         "sp_debug_effective_splits": ([i32, i32], i32),
     }
     for name, (args, res) in sig.items():

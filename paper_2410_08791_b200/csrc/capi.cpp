@@ -238,7 +238,7 @@ extern "C" int sp_debug_gemm_bf16_async(int32_t M, int32_t N, int32_t K, const v
                                         int32_t b_mn, int32_t epilogue, void* out, int32_t ldo,
                                         const float* bias, int32_t relu, const void* gate,
                                         int32_t ldg, int32_t splits, int32_t block_n,
-                                        void* stream) {
+                                        int32_t cta, void* stream) {
     sp::GemmProblem g;
     g.M = M;
     g.N = N;
@@ -259,6 +259,8 @@ extern "C" int sp_debug_gemm_bf16_async(int32_t M, int32_t N, int32_t K, const v
     g.splits = splits;
     g.split_stride = static_cast<int64_t>(M) * ldo;
     g.block_n = block_n;
+    g.cta = cta;
+    g.lr = 1.0f;
     return static_cast<int>(sp::gemm_bf16(g, static_cast<cudaStream_t>(stream)));
 }
 
@@ -266,7 +268,7 @@ extern "C" int sp_debug_gemm_bf16(int32_t M, int32_t N, int32_t K, const void* A
                                   int32_t a_mn, const void* B, int32_t ldb, int32_t b_mn,
                                   int32_t epilogue, void* out, int32_t ldo, const float* bias,
                                   int32_t relu, const void* gate, int32_t ldg, int32_t splits,
-                                  int32_t block_n) {
+                                  int32_t block_n, int32_t cta) {
     sp::GemmProblem g;
     g.M = M;
     g.N = N;
@@ -287,6 +289,8 @@ extern "C" int sp_debug_gemm_bf16(int32_t M, int32_t N, int32_t K, const void* A
     g.splits = splits;
     g.split_stride = static_cast<int64_t>(M) * ldo;
     g.block_n = block_n;
+    g.cta = cta;
+    g.lr = 1.0f;
     cudaError_t e = sp::gemm_bf16(g, 0);
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     return static_cast<int>(e);

@@ -53,9 +53,18 @@ struct GemmProblem {
     int ldg = 0;
     int splits = 1;
     int64_t split_stride = 0;
-    int block_n = 0;  // 0 = choose
+    int block_n = 0;  // 0 = choose (1-CTA: N per CTA; 2-CTA: N per CTA pair)
     float lr = 0.0f;  // EPI_SGD_F32
+    int cta = 0;      // 0 = choose, 1 = one CTA per tile (M=128), 2 = CTA pair (M=256)
 };
+
+struct GemmChoice {
+    int cta;
+    int block_n;
+};
+// The kernel variant gemm_bf16 picks when cta/block_n are 0 (depends on the shape only, so
+// results are identical for every window setting).
+GemmChoice choose_gemm(int M, int N, int K, int splits);
 
 // Launches the warp-specialized tcgen05/TMEM/TMA GEMM. Returns cudaSuccess or an error.
 cudaError_t gemm_bf16(const GemmProblem& p, cudaStream_t st);

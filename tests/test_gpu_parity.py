@@ -253,7 +253,7 @@ def test_bf16_train_window_invariant_and_close():
 torch = pytest.importorskip("torch")
 
 
-def _gemm(M, N, K, a_mn, b_mn, epi, bn, splits=1, relu=1, seed=0):
+def _gemm(M, N, K, a_mn, b_mn, epi, bn, splits=1, relu=1, seed=0, cta=1):
     g = torch.Generator(device="cpu").manual_seed(seed)
     A = (torch.randn((K, M) if a_mn else (M, K), generator=g) * 0.5).to(torch.bfloat16).cuda()
     B = (torch.randn((K, N) if b_mn else (N, K), generator=g) * 0.5).to(torch.bfloat16).cuda()
@@ -271,10 +271,14 @@ def _gemm(M, N, K, a_mn, b_mn, epi, bn, splits=1, relu=1, seed=0):
     eff = sp._capi.LIB.sp_debug_effective_splits(K, splits) if epi == 3 else 1
     out = torch.empty((eff * M, N) if epi == 3 else (M, N),
                       dtype=torch.bfloat16 if epi in (0, 2) else torch.float32, device="cuda")
+    if epi == 4:  # fused SGD: out (= W) -= 1.0 * acc
+        w0 = torch.randn((M, N), generator=g).float()
+        out.copy_(w0)
+        ref = w0.cuda() - ref
     rc = sp._capi.LIB.sp_debug_gemm_bf16(M, N, K, A.data_ptr(), M if a_mn else K, int(a_mn),
                                          B.data_ptr(), N if b_mn else K, int(b_mn), epi,
                                          out.data_ptr(), N, bias.data_ptr(), relu, gate.data_ptr(),
-                                         N, splits, bn)
+                                         N, splits, bn, cta)
     assert rc == 0, f"gemm rc={rc}"
     got = out.float()
     if epi == 3:
@@ -282,20 +286,21 @@ def _gemm(M, N, K, a_mn, b_mn, epi, bn, splits=1, relu=1, seed=0):
     return got.cpu().numpy(), ref.cpu().numpy()
 
 
-@pytest.mark.parametrize("bn", [128, 192, 256])
+@pytest.mark.parametrize("cta,bn", [(1, 128), (1, 192), (1, 256), (2, 128), (2, 256)])
 @pytest.mark.parametrize("layout,epi", [((False, True), 0), ((False, True), 1), ((False, False), 2),
-                                        ((True, True), 3), ((False, False), 3)])
-def test_tcgen05_gemm_matches_torch(bn, layout, epi):
+                                        ((True, True), 3), ((False, False), 3), ((True, True), 4)])
+def test_tcgen05_gemm_matches_torch(cta, bn, layout, epi):
     a_mn, b_mn = layout
     # M-major A needs a 16-byte aligned leading dim (M % 8 == 0); partial tiles still covered
-    for (M, N, K) in [(128, bn, 64), (304, 2 * bn, 320), (1000, 3 * bn - 64, 1600)]:
-        got, ref = _gemm(M, N, K, a_mn, b_mn, epi, bn)
+    for (M, N, K) in [(128, bn, 64), (304, 2 * bn, 320), (1000, 3 * bn - 64, 1600), (520, bn, 192)]:
+        got, ref = _gemm(M, N, K, a_mn, b_mn, epi, bn, cta=cta)
         tol = 1e-2 if epi in (0, 2) else 2e-4  # bf16 output rounding vs fp32 accumulation order
-        assert rel_err(got, ref) <= tol, (M, N, K, bn, layout, epi, rel_err(got, ref))
+        assert rel_err(got, ref) <= tol, (M, N, K, cta, bn, layout, epi, rel_err(got, ref))
 
 
-def test_tcgen05_gemm_split_k_deterministic():
-    a, ref = _gemm(256, 256, 4096, True, True, 3, 256, splits=4)
-    b, _ = _gemm(256, 256, 4096, True, True, 3, 256, splits=4)
+@pytest.mark.parametrize("cta", [1, 2])
+def test_tcgen05_gemm_split_k_deterministic(cta):
+    a, ref = _gemm(256, 256, 4096, True, True, 3, 256, splits=4, cta=cta)
+    b, _ = _gemm(256, 256, 4096, True, True, 3, 256, splits=4, cta=cta)
     assert np.array_equal(a, b)
     assert rel_err(a, ref) <= 2e-4

@@ -1,6 +1,6 @@
-"""Times the tcgen05 GEMM (sp_debug_gemm_bf16) on the three per-layer shapes of a square
-block training step (forward, dX, dW) for each tile width, against torch.matmul (cuBLAS)
-as a yardstick. CUDA events on the default stream; L2 flushed between launches.
+"""Times the tcgen05 GEMM variants (1-CTA M=128 tiles, 2-CTA cta_group::2 M=256 tiles, tile N)
+on the three per-layer shapes of a square-block training step (forward, dX, dW-with-SGD) via
+back-to-back launches between CUDA events, against torch.matmul (cuBLAS) as a yardstick.
 Usage: python tools/gemm_bench.py [rows d]"""
 import json
 import os
@@ -13,49 +13,55 @@ from paper_2410_08791_b200 import _capi  # noqa: E402
 
 rows, d = (int(v) for v in (sys.argv[1:3] if len(sys.argv) > 2 else (16384, 1600)))
 LIB = _capi.LIB
-flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 x = torch.randn(rows, d, device="cuda").to(torch.bfloat16)
-dz = torch.randn(rows, d, device="cuda").to(torch.bfloat16)
+dz = (torch.randn(rows, d, device="cuda") * 1e-3).to(torch.bfloat16)
 W = torch.randn(d, d, device="cuda").to(torch.bfloat16)
+W32 = torch.randn(d, d, device="cuda")
 bias = torch.randn(d, device="cuda")
 out16 = torch.empty(rows, d, device="cuda", dtype=torch.bfloat16)
-out32 = torch.empty(16 * d * d, device="cuda", dtype=torch.float32)
+st = torch.cuda.current_stream().cuda_stream
 
 
-def timeit(fn, reps=10):
-    fn()
+def timeit(fn, reps=20):
+    for _ in range(3):
+        assert fn() == 0
     torch.cuda.synchronize()
-    tot = 0.0
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
     for _ in range(reps):
-        flush.zero_()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
         fn()
-        e1.record()
-        e1.synchronize()
-        tot += e0.elapsed_time(e1)
-    return tot / reps
+    e1.record()
+    e1.synchronize()
+    return e0.elapsed_time(e1) / reps
 
 
-res = []
-for bn in (128, 192, 256):
+fl = 2.0 * rows * d * d
+for cta, bn in [(1, 128), (1, 192), (1, 256), (2, 128), (2, 256), (0, 0)]:
     shapes = {
-        "fwd": lambda: LIB.sp_debug_gemm_bf16(rows, d, d, x.data_ptr(), d, 0, W.data_ptr(), d, 1, 0,
-                                              out16.data_ptr(), d, bias.data_ptr(), 1, None, 0, 1, bn),
-        "dx": lambda: LIB.sp_debug_gemm_bf16(rows, d, d, dz.data_ptr(), d, 0, W.data_ptr(), d, 0, 2,
-                                             out16.data_ptr(), d, None, 1, x.data_ptr(), d, 1, bn),
+        "fwd": lambda: LIB.sp_debug_gemm_bf16_async(rows, d, d, x.data_ptr(), d, 0, W.data_ptr(), d, 1, 0,
+                                                    out16.data_ptr(), d, bias.data_ptr(), 1, None, 0, 1,
+                                                    bn, cta, st),
+        "dx": lambda: LIB.sp_debug_gemm_bf16_async(rows, d, d, dz.data_ptr(), d, 0, W.data_ptr(), d, 0, 2,
+                                                   out16.data_ptr(), d, None, 1, x.data_ptr(), d, 1, bn,
+                                                   cta, st),
+        "dw_sgd": lambda: LIB.sp_debug_gemm_bf16_async(d, d, rows, x.data_ptr(), d, 1, dz.data_ptr(), d, 1,
+                                                       4, W32.data_ptr(), d, None, 0, None, 0, 1, bn, cta,
+                                                       st),
     }
-    for s in (1, 2, 4, 6, 8):
-        shapes[f"dw_s{s}"] = (lambda s=s: LIB.sp_debug_gemm_bf16(
-            d, d, rows, x.data_ptr(), d, 1, dz.data_ptr(), d, 1, 3, out32.data_ptr(), d, None, 0,
-            None, 0, s, bn))
     for name, fn in shapes.items():
         ms = timeit(fn)
-        fl = 2.0 * rows * d * d
-        res.append({"bn": bn, "gemm": name, "ms": ms, "tflops": fl / ms / 1e9})
-        print(json.dumps(res[-1]), flush=True)
+        print(json.dumps({"cta": cta or "auto", "bn": bn or "auto", "gemm": name, "ms": round(ms, 4),
+                          "tflops": round(fl / ms / 1e9, 1)}), flush=True)
 for name, fn in {"torch_fwd": lambda: torch.matmul(x, W),
                  "torch_dx": lambda: torch.matmul(dz, W.t()),
                  "torch_dw": lambda: torch.matmul(x.t(), dz)}.items():
-    ms = timeit(fn)
-    print(json.dumps({"gemm": name, "ms": ms, "tflops": 2.0 * rows * d * d / ms / 1e9}), flush=True)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    fn()
+    e0.record()
+    for _ in range(20):
+        fn()
+    e1.record()
+    e1.synchronize()
+    ms = e0.elapsed_time(e1) / 20
+    print(json.dumps({"gemm": name, "ms": round(ms, 4), "tflops": round(fl / ms / 1e9, 1)}), flush=True)
