@@ -447,7 +447,7 @@ void Executor::compute_op(const Op& op, bool train, int64_t rows, int fmt) {
     g.ldo = d_;
     g.splits = fused ? 1 : splits_;
     g.split_stride = static_cast<int64_t>(dd);
-    g.block_n = dw_bn_;
+    g.block_n = 0;  // kernel variant chosen from the shape (choose_gemm)
     g.lr = cur_lr_;
     gemm(g, st);
     if (fused) w16_layer_[s] = -1;

@@ -154,6 +154,21 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
     return *reinterpret_cast<uint32_t*>(&v);
 }
 
+// Grouped rasterisation: consecutive tile indices walk G m-blocks x every n-block, so the CTAs
+// resident at any moment share their A panels (and B panels) in L2 instead of re-streaming each
+// A panel from DRAM once per n-block. Only the order of tiles changes, never a tile's math.
+template <int G>
+__device__ __forceinline__ void tile_mn(int t, int m_tiles, int n_tiles, int& mb, int& nb) {
+    const int tmn = t % (m_tiles * n_tiles);
+    const int per_group = G * n_tiles;
+    const int g = tmn / per_group;
+    const int first = g * G;
+    const int gm = min(G, m_tiles - first);
+    const int r = tmn - g * per_group;
+    mb = first + r % gm;
+    nb = r / gm;
+}
+
 // Epilogue for 32 accumulator columns [col0, col0+32) of one output row (one TMEM lane).
 template <int EPI>
 __device__ __forceinline__ void epilogue_chunk(const Params& p, const uint32_t (&r)[32], int row,
@@ -280,8 +295,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             int stage = 0;
             uint32_t phase = 0;
             for (int t = blockIdx.x; t < total; t += gridDim.x) {
-                const int m0 = (t % p.m_tiles) * BM;
-                const int n0 = ((t / p.m_tiles) % p.n_tiles) * BN;
+                int mb, nbk;
+                tile_mn<16>(t, p.m_tiles, p.n_tiles, mb, nbk);
+                const int m0 = mb * BM;
+                const int n0 = nbk * BN;
                 const int split = t / tiles_mn;
                 const int kb0 = split * p.kb_per_split;
                 const int kb1 = min(kb0 + p.kb_per_split, p.k_blocks);
@@ -355,8 +372,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int t = blockIdx.x; t < total; t += gridDim.x) {
-            const int m0 = (t % p.m_tiles) * BM;
-            const int n0 = ((t / p.m_tiles) % p.n_tiles) * BN;
+            int mb, nbk;
+            tile_mn<16>(t, p.m_tiles, p.n_tiles, mb, nbk);
+            const int m0 = mb * BM;
+            const int n0 = nbk * BN;
             const int split = t / tiles_mn;
             mbar_wait(&tfull[acc], acc_phase);
             fence_after();
@@ -509,8 +528,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             int stage = 0;
             uint32_t phase = 0;
             for (int t = cid; t < total; t += ncl) {
-                const int m0 = (t % m_tiles2) * 2 * BM + static_cast<int>(rank) * BM;
-                const int nb = ((t / m_tiles2) % p.n_tiles) * BN + static_cast<int>(rank) * (BN / 2);
+                int mb, nbk;
+                tile_mn<8>(t, m_tiles2, p.n_tiles, mb, nbk);
+                const int m0 = mb * 2 * BM + static_cast<int>(rank) * BM;
+                const int nb = nbk * BN + static_cast<int>(rank) * (BN / 2);
                 const int split = t / tiles_mn;
                 const int kb0 = split * p.kb_per_split;
                 const int kb1 = min(kb0 + p.kb_per_split, p.k_blocks);
@@ -586,8 +607,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int t = cid; t < total; t += ncl) {
-            const int m0 = (t % m_tiles2) * 2 * BM + static_cast<int>(rank) * BM;
-            const int n0 = ((t / m_tiles2) % p.n_tiles) * BN;
+            int mb, nbk;
+            tile_mn<8>(t, m_tiles2, p.n_tiles, mb, nbk);
+            const int m0 = mb * 2 * BM + static_cast<int>(rank) * BM;
+            const int n0 = nbk * BN;
             const int split = t / tiles_mn;
             mbar_wait(&tfull[acc], acc_phase);
             fence_after();
@@ -806,9 +829,10 @@ cudaError_t dispatch2_bn(const GemmProblem& g, cudaStream_t st) {
 
 }  // namespace tc
 
-// Kernel choice from a wave-quantised cost model: time ~ waves x tile work / per-SM rate.
-// Per-SM tensor efficiency (measured on B200 at d=1600): 1-CTA N=192/256 ~0.70, N=128 ~0.55
-// (smem/L2 operand traffic); 2-CTA pairs ~0.9 (half the B bytes per MAC).
+// Kernel choice from a wave-quantised cost model: time ~ waves x per-SM tile work / per-SM
+// rate. Relative per-SM rates calibrated on B200 (tools/gemm_bench.py, grouped rasterisation):
+// 2-CTA N=256 ~0.95 (1189 TFLOP/s at 16384x1600x1600, 1568 at 65536x4096x4096), 1-CTA
+// N=192/256 ~0.80; N=128 tiles (either kind) are never competitive and are not candidates.
 GemmChoice choose_gemm(int M, int N, int K, int splits) {
     const int sms = num_sms();
     GemmChoice best{1, 256};
@@ -818,17 +842,15 @@ GemmChoice choose_gemm(int M, int N, int K, int splits) {
                            ((N + bn - 1) / bn) * splits;
         const long slots = sms / cta;
         const long waves = (tiles + slots - 1) / slots;
-        const double t = static_cast<double>(waves) * cta * tc::BM * bn / eff;
+        const double t = static_cast<double>(waves) * tc::BM * bn / eff;  // per-SM work per wave
         if (t < best_t - 1e-9) {
             best_t = t;
             best = GemmChoice{cta, bn};
         }
     };
-    consider(2, 256, 0.90);
-    consider(2, 128, 0.80);
-    consider(1, 256, 0.70);
-    consider(1, 192, 0.70);
-    consider(1, 128, 0.55);
+    consider(2, 256, 0.95);
+    consider(1, 256, 0.80);
+    consider(1, 192, 0.80);
     (void)K;
     return best;
 }
@@ -881,6 +903,7 @@ cudaError_t gemm_bf16(const GemmProblem& g, cudaStream_t st) {
         const GemmChoice c = choose_gemm(g.M, g.N, g.K, g.splits < 1 ? 1 : g.splits);
         cta = c.cta;
         if (!bn) bn = c.block_n;
+        if (cta == 2 && bn != 128 && bn != 256) cta = 1;  // a forced tile width decides
     }
     if (!bn) bn = cta == 2 ? 256 : choose_block_n(g.N);
     if (cta == 2) {
