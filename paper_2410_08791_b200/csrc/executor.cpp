@@ -889,9 +889,16 @@ void Executor::read_layer(int index, float* W, float* b) {
 
 void Executor::dp_init(const uint8_t id[128], int rank, int world) {
     if (world < 1 || rank < 0 || rank >= world) throw Error(SP_ERR_INVALID, "dp_init: bad rank/world");
-    if (world == 1) return;
+    // world == 1 still builds a (1-rank) communicator: the data-parallel code path (split-K
+    // partials, fixed-order reduce, NCCL all-reduce inside the captured graph, SGD on the
+    // update stream) then runs end to end on a single GPU.
     if (!nccl().ok()) throw Error(SP_ERR_NCCL, nccl().error);
     CUDA_OK(cudaSetDevice(cfg_.device));
+    for (auto s : {s_h2d_, s_comp_, s_d2h_, s_upd_}) CUDA_OK(cudaStreamSynchronize(s));
+    if (comm_) {
+        nccl().CommDestroy(comm_);
+        comm_ = nullptr;
+    }
     ncclUniqueId uid;
     std::memcpy(uid.internal, id, sizeof(uid.internal));
     NCCL_OK(nccl().CommInitRank(&comm_, world, uid, rank));

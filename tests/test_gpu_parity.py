@@ -304,3 +304,63 @@ def test_tcgen05_gemm_split_k_deterministic(cta):
     b, _ = _gemm(256, 256, 4096, True, True, 3, 256, splits=4, cta=cta)
     assert np.array_equal(a, b)
     assert rel_err(a, ref) <= 2e-4
+
+
+# --------------------------------------------------------------------------------------
+# data-parallel code path on one GPU (1-rank NCCL communicator)
+# --------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("numerics", [sp.EXACT, sp.BF16])
+def test_dp_code_path_single_rank(numerics):
+    """sp_dp_init(world=1) routes training through the DP path: raw dW/db (split-K partials in
+    bf16), fixed-order reduce, ncclAllReduce on the update stream (inside the captured CUDA
+    graph), SGD. With one rank the all-reduce is the identity, so the result must equal the
+    non-DP path (exact: bitwise; bf16: up to the split-K summation order) and be identical
+    across windows."""
+    d = 16 if numerics == sp.EXACT else 128
+    model = sp.build_model(21, 6, d, 1)
+    rows = 5 if numerics == sp.EXACT else 640
+    x, t = sp.make_input(21, 0, rows, d), sp.make_input(21, 1, rows, d)
+    outs = []
+    for s in [S(sp.SUPERPIPELINE, 2, 1), S(sp.SUPERPIPELINE, 4, 2), S(sp.STANDARD)]:
+        for dp in (False, True):
+            with sp.Executor(6, d, s, numerics=numerics) as ex:
+                ex.register_model(model)
+                if dp:
+                    ex.dp_init(sp.Executor.nccl_unique_id(), 0, 1)
+                losses = [ex.train_step(x, t, 0.05) for _ in range(2)]  # 2nd step: graph replay
+                outs.append((s, dp, losses, ex.read_model(model)))
+    base = outs[0]
+    for s, dp, losses, m in outs:
+        if numerics == sp.EXACT or dp == base[1]:
+            assert losses == base[2], (s, dp)
+        if numerics == sp.EXACT:
+            assert np.array_equal(m.W, base[3].W) and np.array_equal(m.b, base[3].b), (s, dp)
+        else:
+            assert norm_err(m.W - model.W, base[3].W - model.W) <= 1e-3, (s, dp)
+    dps = [o for o in outs if o[1]]
+    for s, dp, losses, m in dps[1:]:  # DP path itself is window-invariant, bitwise
+        assert losses == dps[0][2] and np.array_equal(m.W, dps[0][3].W)
+    if numerics == sp.EXACT:  # and matches the CPU oracle bitwise
+        W, b = model.W.copy(), model.b.copy()
+        for _ in range(2):
+            loss, W, b = ORC.train_step(W, b, x, t, 0.05, frozen=model.frozen)
+        assert np.array_equal(dps[0][3].W, W) and np.array_equal(dps[0][3].b, b)
+
+
+def test_bf16_full_size_window_invariance():
+    """Size-independent property at the bench's full size (48 x 1600, 16384 rows): one bf16
+    train step gives bit-identical weights and loss for different windows."""
+    n, d, rows = 48, 1600, 16384
+    Wl = np.empty((d, d), np.float32)
+    bl = np.empty((d,), np.float32)
+    x, t = sp.make_input(7, 0, rows, d), sp.make_input(7, 1, rows, d)
+    digests = []
+    for s in [S(sp.SUPERPIPELINE, 4, 2), S(sp.SUPERPIPELINE, 6, 3, sp.SEQUENTIAL), S(sp.NAIVE, 3)]:
+        with sp.Executor(n, d, s, numerics=sp.BF16, trace=0) as ex:
+            for i in range(n):
+                sp._capi.LIB.sp_build_layer(7, i, d, 0, 0, Wl.ctypes.data, bl.ctypes.data)
+                ex.register_layer(i, Wl, bl)
+            loss = ex.train_step(x, t, 0.01)
+            digests.append((loss, ex.digest_train(loss)))
+    assert len(set(digests)) == 1, digests
