@@ -118,6 +118,8 @@ typedef struct {
     int32_t item, layer, backward;
     int32_t first_layer, n_layers_moved;
     uint64_t weight_bytes, activation_bytes;
+    int32_t op_index;  /* index of the op in sp_last_plan's listing (-1 for Stall rows) */
+    int32_t reserved;
 } sp_trace_event;
 
 /* ---- lifecycle --------------------------------------------------------------------- */
@@ -152,6 +154,10 @@ int sp_read_layer(sp_exec* ex, int32_t index, float* W, float* b);
 
 /* ---- metrics ----------------------------------------------------------------------- */
 int sp_get_stats(const sp_exec* ex, sp_stats* out);
+/* The op plan of the last forward/train call, in sp_describe_plan's format (one op per line,
+ * with the reference-semantics ledger snapshot "led=weight,activation,gradient"); returns the
+ * needed length. Joined with sp_get_trace rows (op_index) it yields the reference's trace CSV. */
+int64_t sp_last_plan(const sp_exec* ex, char* buf, int64_t cap);
 /* Changes the trace level (sp_config.trace) for subsequent calls. */
 int sp_set_trace(sp_exec* ex, int32_t level);
 /* Copies up to cap events of the last call's measured timeline; *count = total rows. */

@@ -51,7 +51,8 @@ class SpTraceEvent(C.Structure):
     _fields_ = [("t_start", C.c_double), ("t_end", C.c_double)] + [
         (n, C.c_int32) for n in ("kind", "item", "layer", "backward", "first_layer",
                                  "n_layers_moved")] + [
-        ("weight_bytes", C.c_uint64), ("activation_bytes", C.c_uint64)]
+        ("weight_bytes", C.c_uint64), ("activation_bytes", C.c_uint64),
+        ("op_index", C.c_int32), ("reserved", C.c_int32)]
 
 
 # Every symbol include/superpipe.h and include/superpipe_debug.h declare (checked by the
@@ -59,7 +60,8 @@ class SpTraceEvent(C.Structure):
 EXPORTS = [
     "sp_create", "sp_register_layer", "sp_destroy", "sp_last_error", "sp_abi_version",
     "sp_forward", "sp_forward_device", "sp_train_step", "sp_train_step_device",
-    "sp_read_layer", "sp_get_stats", "sp_get_trace", "sp_set_trace", "sp_nccl_unique_id",
+    "sp_read_layer", "sp_get_stats", "sp_get_trace", "sp_set_trace", "sp_last_plan",
+    "sp_nccl_unique_id",
     "sp_dp_init",
     "sp_host_alloc", "sp_host_free", "sp_peak_weight_residency", "sp_validate_strategy",
     "sp_describe_plan", "sp_build_layer", "sp_make_input", "sp_digest_tensors",
@@ -88,6 +90,7 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "sp_get_stats": ([ex, C.POINTER(SpStats)], C.c_int),
         "sp_get_trace": ([ex, C.POINTER(SpTraceEvent), i32, C.POINTER(i32)], C.c_int),
         "sp_set_trace": ([ex, i32], C.c_int),
+        "sp_last_plan": ([ex, C.c_char_p, i64], i64),
         "sp_nccl_unique_id": ([C.c_char_p], C.c_int),
         "sp_dp_init": ([ex, C.c_char_p, i32, i32], C.c_int),
         "sp_host_alloc": ([u64], vp),

@@ -116,6 +116,17 @@ int sp_read_layer(sp_exec* ex, int32_t index, float* W, float* b) {
     return guarded(ex, [&] { ex->impl->read_layer(index, W, b); });
 }
 
+int64_t sp_last_plan(const sp_exec* ex, char* buf, int64_t cap) {
+    if (!ex) return -1;
+    const std::string text = ex->impl->last_plan_text();
+    if (buf && cap > 0) {
+        const int64_t n = std::min<int64_t>(cap - 1, static_cast<int64_t>(text.size()));
+        std::memcpy(buf, text.data(), static_cast<size_t>(n));
+        buf[n] = '\0';
+    }
+    return static_cast<int64_t>(text.size()) + 1;
+}
+
 int sp_set_trace(sp_exec* ex, int32_t level) {
     if (!ex || level < 0 || level > 2) return SP_ERR_INVALID;
     ex->impl->set_trace(level);

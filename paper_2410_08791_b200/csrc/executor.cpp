@@ -728,6 +728,7 @@ void Executor::collect_stats(const Plan& plan, int n_items, bool train) {
         CUDA_OK(cudaEventElapsedTime(&t0, ev_call0_, ev_start_[i]));
         CUDA_OK(cudaEventElapsedTime(&t1, ev_call0_, ev_done_[i]));
         sp_trace_event ev{};
+        ev.op_index = static_cast<int32_t>(i);
         ev.t_start = t0;
         ev.t_end = t1;
         ev.item = op.item;
@@ -741,6 +742,7 @@ void Executor::collect_stats(const Plan& plan, int n_items, bool train) {
             }
             if (prev_end >= 0 && t0 > prev_end) {
                 sp_trace_event s{};
+                s.op_index = -1;
                 s.t_start = prev_end;
                 s.t_end = t0;
                 s.kind = 3;
@@ -770,6 +772,7 @@ void Executor::collect_stats(const Plan& plan, int n_items, bool train) {
         }
         trace_.push_back(ev);
     }
+    last_plan_ = plan;
     stats_.peak_bytes = plan.ledger.peak_bytes;
     stats_.peak_weight_bytes = plan.ledger.peak_weight;
     stats_.peak_activation_bytes = plan.ledger.peak_activation;

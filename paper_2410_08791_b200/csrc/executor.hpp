@@ -36,6 +36,7 @@ public:
     void read_layer(int index, float* W, float* b);
     void digest_train(float loss, char out[17]) const;
     void set_trace(int level) { cfg_.trace = level; }
+    std::string last_plan_text() const { return describe_plan(last_plan_); }
     void dp_init(const uint8_t id[128], int rank, int world);
 
     const sp_stats& stats() const { return stats_; }
@@ -161,6 +162,7 @@ private:
     // metrics
     sp_stats stats_{};
     std::vector<sp_trace_event> trace_;
+    Plan last_plan_;
     uint64_t kernels_ = 0;
     uint64_t h2d_bytes_ = 0, d2h_bytes_ = 0;
     std::vector<cudaEvent_t> gemm_ev_;  // start/end pairs around each tcgen05 GEMM launch

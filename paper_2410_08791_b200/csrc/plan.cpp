@@ -147,6 +147,10 @@ private:
     }
 
     int push(Op op) {
+        // ledger snapshot at this point of the plan (TraceEvent::footprint_after, trace.hpp:44-46)
+        op.led_w = tag_[kWeight];
+        op.led_a = tag_[kActivation];
+        op.led_g = tag_[kGradient];
         plan_.ops.push_back(std::move(op));
         return static_cast<int>(plan_.ops.size()) - 1;
     }
@@ -510,7 +514,8 @@ std::string describe_plan(const Plan& plan) {
             os << " layers=" << list(op.layers) << " slots=" << list(op.slots)
                << " w=" << list(w) << " a=" << list(a);
         }
-        os << " deps=" << list(op.deps) << "\n";
+        os << " deps=" << list(op.deps) << " led=" << op.led_w << "," << op.led_a << ","
+           << op.led_g << "\n";
     }
     return os.str();
 }

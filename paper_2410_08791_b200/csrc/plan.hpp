@@ -60,6 +60,7 @@ struct Op {
     std::vector<uint8_t> weights;  // per moved layer: weight bytes move
     std::vector<uint8_t> acts;     // per moved layer: the saved activation rides along
     std::vector<int> deps;         // op indices that must complete first (any stream)
+    uint64_t led_w = 0, led_a = 0, led_g = 0;  // ledger (weight/act/grad bytes) at this op
 };
 
 struct LedgerPeaks {

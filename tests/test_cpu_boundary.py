@@ -90,17 +90,8 @@ def test_peak_weight_residency_formula():
 
 
 def parse_plan(text):
-    lines = text.strip().splitlines()
-    head = dict(kv.split("=") for kv in lines[0].split() if "=" in kv)
-    ops = []
-    for ln in lines[1:]:
-        parts = ln.split()
-        op = {"kind": parts[1]}
-        for kv in parts[2:]:
-            k, v = kv.split("=")
-            op[k] = [int(t) for t in v.split(",")] if v and k in ("layers", "slots", "w", "a", "deps") else (int(v) if v else [])
-        ops.append(op)
-    return head, ops
+    from paper_2410_08791_b200.trace_io import plan_ops
+    return plan_ops(text)
 
 
 def test_plan_superpipeline_pairs_eviction_with_prefetch():
