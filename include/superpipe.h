@@ -167,6 +167,14 @@ int sp_get_trace(const sp_exec* ex, sp_trace_event* events, int32_t cap, int32_t
 /* Per-layer NCCL all-reduce of dW/db as each layer's backward completes. */
 int sp_nccl_unique_id(uint8_t id[128]);
 int sp_dp_init(sp_exec* ex, const uint8_t id[128], int32_t rank, int32_t world);
+/* Same, choosing the weight-streaming mode explicitly. shard_weights = 1: each rank copies only
+ * 1/world of every layer over its own host link and an NCCL all-gather over NVLink completes the
+ * slot; in training the gradient is reduce-scattered, each rank updates and writes back only its
+ * shard (its pinned copy stays authoritative for exactly the shard it streams). shard_weights = 0:
+ * every rank streams whole layers and all-reduces dW/db. sp_dp_init uses shard_weights =
+ * (world > 1). world = 1 builds a 1-rank communicator (exercises the same code path). */
+int sp_dp_init2(sp_exec* ex, const uint8_t id[128], int32_t rank, int32_t world,
+                int32_t shard_weights);
 
 /* ---- host utilities ---------------------------------------------------------------- */
 /* Pinned (page-locked, portable) host buffers for callers' inputs/outputs. */
@@ -180,7 +188,7 @@ int sp_validate_strategy(int32_t strategy, int32_t k, int32_t k_prime, int32_t n
 /* Describes the static op plan the executor would run (policy_step, scheduler.cpp:53-141,
  * resolved ahead of time) as text, one op per line; returns the needed length. Host-only. */
 int64_t sp_describe_plan(const sp_config* cfg, int32_t n_items, int32_t train,
-                         const int32_t* frozen, char* buf, int64_t cap);
+                         const int32_t* frozen, int32_t sharded, char* buf, int64_t cap);
 /* Deterministic layer / input generators of the reference (host-only), so callers can
  * register synthetic models without a second copy: build_model's per-layer splitmix64 stream
  * (model.cpp:23-52, W[fan_in][fan_out] then b[fan_out], U(+-1/sqrt(fan_in)); fan_in = fan_out

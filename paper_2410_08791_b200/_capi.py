@@ -62,7 +62,7 @@ EXPORTS = [
     "sp_forward", "sp_forward_device", "sp_train_step", "sp_train_step_device",
     "sp_read_layer", "sp_get_stats", "sp_get_trace", "sp_set_trace", "sp_last_plan",
     "sp_nccl_unique_id",
-    "sp_dp_init",
+    "sp_dp_init", "sp_dp_init2",
     "sp_host_alloc", "sp_host_free", "sp_peak_weight_residency", "sp_validate_strategy",
     "sp_describe_plan", "sp_build_layer", "sp_make_input", "sp_digest_tensors",
     "sp_digest_train",
@@ -93,11 +93,12 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "sp_last_plan": ([ex, C.c_char_p, i64], i64),
         "sp_nccl_unique_id": ([C.c_char_p], C.c_int),
         "sp_dp_init": ([ex, C.c_char_p, i32, i32], C.c_int),
+        "sp_dp_init2": ([ex, C.c_char_p, i32, i32, i32], C.c_int),
         "sp_host_alloc": ([u64], vp),
         "sp_host_free": ([vp], None),
         "sp_peak_weight_residency": ([i32, i32, i32, i32, u64], u64),
         "sp_validate_strategy": ([i32, i32, i32, i32], C.c_int),
-        "sp_describe_plan": ([C.POINTER(SpConfig), i32, i32, vp, C.c_char_p, i64], i64),
+        "sp_describe_plan": ([C.POINTER(SpConfig), i32, i32, vp, i32, C.c_char_p, i64], i64),
         "sp_build_layer": ([u64, i32, i32, i32, i32, vp, vp], C.c_int),
         "sp_make_input": ([u64, u64, i64, i32, vp], None),
         "sp_digest_tensors": ([vp, i32, i64, i32, C.c_char_p], None),

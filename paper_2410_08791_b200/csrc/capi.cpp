@@ -163,8 +163,13 @@ int sp_nccl_unique_id(uint8_t id[128]) {
 }
 
 int sp_dp_init(sp_exec* ex, const uint8_t id[128], int32_t rank, int32_t world) {
+    return sp_dp_init2(ex, id, rank, world, world > 1 ? 1 : 0);
+}
+
+int sp_dp_init2(sp_exec* ex, const uint8_t id[128], int32_t rank, int32_t world,
+                int32_t shard_weights) {
     if (!ex || !id) return SP_ERR_INVALID;
-    return guarded(ex, [&] { ex->impl->dp_init(id, rank, world); });
+    return guarded(ex, [&] { ex->impl->dp_init(id, rank, world, shard_weights != 0); });
 }
 
 void* sp_host_alloc(uint64_t bytes) {
@@ -188,7 +193,7 @@ int sp_validate_strategy(int32_t strategy, int32_t k, int32_t k_prime, int32_t n
 }
 
 int64_t sp_describe_plan(const sp_config* cfg, int32_t n_items, int32_t train,
-                         const int32_t* frozen, char* buf, int64_t cap) {
+                         const int32_t* frozen, int32_t sharded, char* buf, int64_t cap) {
     if (!cfg) return -1;
     sp::PlanInput in;
     in.n_layers = cfg->n_layers;
@@ -204,6 +209,7 @@ int64_t sp_describe_plan(const sp_config* cfg, int32_t n_items, int32_t train,
     in.capacity = cfg->capacity_bytes;
     if (frozen)
         for (int32_t l = 0; l < cfg->n_layers; ++l) in.frozen.push_back(frozen[l] != 0);
+    in.sharded = sharded != 0;
     sp::Plan plan = sp::build_plan(in, {});
     std::string text = plan.error.empty() ? sp::describe_plan(plan) : ("ERROR " + plan.error + "\n");
     if (buf && cap > 0) {

@@ -99,12 +99,7 @@ Executor::Executor(const sp_config& cfg) : cfg_(cfg) {
     if (bf16_) CUDA_OK(cudaHostAlloc(&host16_, static_cast<size_t>(n_) * wire16_bytes(), cudaHostAllocPortable));
 
     n_slots_ = ring_slots(cfg.strategy, cfg.k, cfg.k_prime, n_);
-    const size_t a_region = round_up(layer_bytes(), 1024);
-    off_w16_ = a_region;
-    slot_bytes_ = bf16_ ? round_up(a_region + wire16_bytes(), 1024) : a_region;
-    CUDA_OK(cudaMalloc(&slots_dev_, static_cast<size_t>(n_slots_) * slot_bytes_));
-    cache_.assign(static_cast<size_t>(n_slots_), SlotCache{});
-    w16_layer_.assign(static_cast<size_t>(n_slots_), -1);
+    layout_slots(1);
 
     CUDA_OK(cudaStreamCreateWithFlags(&s_h2d_, cudaStreamNonBlocking));
     CUDA_OK(cudaStreamCreateWithFlags(&s_comp_, cudaStreamNonBlocking));
@@ -115,6 +110,7 @@ Executor::Executor(const sp_config& cfg) : cfg_(cfg) {
     CUDA_OK(cudaEventCreateWithFlags(&ev_io_in_, cudaEventDisableTiming));
     CUDA_OK(cudaEventCreateWithFlags(&ev_io_out_, cudaEventDisableTiming));
     CUDA_OK(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
+    CUDA_OK(cudaEventCreateWithFlags(&ev_loss_, cudaEventDisableTiming));
     for (auto& e : ev_join_) CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     if (const char* g = std::getenv("SUPERPIPE_GRAPHS")) use_graphs_ = std::atoi(g) != 0;
     CUDA_OK(cudaHostAlloc(&loss_host_, 16, cudaHostAllocPortable));
@@ -139,6 +135,7 @@ Executor::~Executor() {
     for (auto e : ev_dep_) cudaEventDestroy(e);
     for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second.exec);
     if (ev_fork_) cudaEventDestroy(ev_fork_);
+    if (ev_loss_) cudaEventDestroy(ev_loss_);
     for (auto e : ev_join_)
         if (e) cudaEventDestroy(e);
     if (ev_call0_) cudaEventDestroy(ev_call0_);
@@ -151,6 +148,29 @@ Executor::~Executor() {
     if (loss_host_) cudaFreeHost(loss_host_);
     for (auto s : {s_h2d_, s_comp_, s_d2h_, s_upd_})
         if (s) cudaStreamDestroy(s);
+}
+
+// Slot = [A: fp32 W|b image, world shards] [B: bf16 W + fp32 b wire image, world shards].
+// Each region is cut into `world` equal shards (256-byte aligned) so a rank can H2D / D2H its
+// own shard and NCCL all-gather / reduce-scatter the rest in place.
+void Executor::layout_slots(int world) {
+    shardA_ = round_up((layer_bytes() + world - 1) / world, 256);
+    shardB_ = round_up((wire16_bytes() + world - 1) / world, 256);
+    const size_t a_region = round_up(shardA_ * world, 1024);
+    off_w16_ = a_region;
+    slot_bytes_ = bf16_ ? round_up(a_region + shardB_ * world, 1024) : a_region;
+    if (slots_dev_) {
+        CUDA_OK(cudaDeviceSynchronize());
+        cudaFree(slots_dev_);
+        slots_dev_ = nullptr;
+    }
+    CUDA_OK(cudaMalloc(&slots_dev_, static_cast<size_t>(n_slots_) * slot_bytes_));
+    cache_.assign(static_cast<size_t>(n_slots_), SlotCache{});
+    cache_fmt_ = -1;
+    w16_layer_.assign(static_cast<size_t>(n_slots_), -1);
+    for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second.exec);
+    graphs_.clear();
+    ++alloc_gen_;
 }
 
 void Executor::register_layer(int index, const float* W, const float* b, int activation,
@@ -235,10 +255,12 @@ void Executor::ensure_buffers(int64_t rows, int n_items, bool train, bool device
         dw_bn_ = bf16_ ? choose_block_n(d_) : 0;
         splits_cap_ = bf16_ ? choose_splits(d_, d_, static_cast<int>(R), dw_bn_) : 1;
         col_chunks_cap_ = bf16_ ? colsum_chunks(R) : 1;
+        // gradient buffers hold world equal shards when reduce-scattered (sharded streaming)
+        const size_t grad_f = std::max(dd + d_, shardA_ / 4 * static_cast<size_t>(world_));
         const size_t ws = bf16_ ? static_cast<size_t>(splits_cap_) * dd + static_cast<size_t>(col_chunks_cap_) * d_
-                                : dd + d_;
+                                : grad_f;
         for (auto& g : gws_) g = static_cast<float*>(alloc(ws * 4));
-        grad_red_ = static_cast<float*>(alloc((dd + d_) * 4));
+        grad_red_ = static_cast<float*>(alloc(grad_f * 4));
         loss_parts_ = static_cast<float*>(alloc(4096 * 4));
         loss_dev_ = static_cast<float*>(alloc(16));
         if (cfg_.checkpointing && cfg_.strategy != SP_STANDARD) {
@@ -268,6 +290,7 @@ Plan Executor::make_plan(bool train, int n_items, int64_t rows, int fmt) {
     in.layer_bytes = layer_bytes();
     in.act_bytes = static_cast<uint64_t>(rows) * d_ * 4;
     in.capacity = cfg_.capacity_bytes;
+    in.sharded = sharded_;
     const std::vector<SlotCache> none;
     Plan plan = build_plan(in, fmt == cache_fmt_ ? cache_ : none);
     if (!plan.error.empty()) throw Error(plan.oom ? SP_ERR_OOM : SP_ERR_INVALID, plan.error);
@@ -284,7 +307,8 @@ cudaStream_t Executor::stream_of(OpKind k) const {
         case OpKind::H2D: return s_h2d_;
         case OpKind::D2H:
         case OpKind::ActSave: return s_d2h_;
-        case OpKind::Update: return s_upd_;
+        case OpKind::Update:
+        case OpKind::AllGather: return s_upd_;  // every NCCL call on one stream, plan order
         default: return s_comp_;
     }
 }
@@ -468,8 +492,17 @@ void Executor::loss_op(int64_t rows) {
         loss_finalize(loss_parts_, loss_blocks_, loss_dev_, s_comp_);
         kernels_ += 2;
     }
-    if (comm_) NCCL_OK(nccl().AllReduce(loss_dev_, loss_dev_, 1, ncclFloat, ncclSum, comm_, s_comp_));
-    CUDA_OK(cudaMemcpyAsync(loss_host_, loss_dev_, 4, cudaMemcpyDeviceToHost, s_comp_));
+    if (comm_) {
+        // The loss value is only reported (the gradient above already uses the global count),
+        // so its all-reduce joins the other NCCL calls on the update stream, off the critical
+        // path; one stream keeps every rank's collectives in the same order.
+        CUDA_OK(cudaEventRecord(ev_loss_, s_comp_));
+        CUDA_OK(cudaStreamWaitEvent(s_upd_, ev_loss_, 0));
+        NCCL_OK(nccl().AllReduce(loss_dev_, loss_dev_, 1, ncclFloat, ncclSum, comm_, s_upd_));
+        CUDA_OK(cudaMemcpyAsync(loss_host_, loss_dev_, 4, cudaMemcpyDeviceToHost, s_upd_));
+    } else {
+        CUDA_OK(cudaMemcpyAsync(loss_host_, loss_dev_, 4, cudaMemcpyDeviceToHost, s_comp_));
+    }
 }
 
 void Executor::update_op(const Op& op, float lr) {
@@ -477,19 +510,36 @@ void Executor::update_op(const Op& op, float lr) {
     const size_t dd = static_cast<size_t>(d_) * d_;
     cudaStream_t st = s_upd_;
     float* ws = gws_[L % 2];
-    if (!bf16_) {
-        if (comm_) NCCL_OK(nccl().AllReduce(ws, ws, dd + d_, ncclFloat, ncclSum, comm_, st));
-        exact_sgd(slot_w32(s), ws, static_cast<int64_t>(dd + d_), lr, st);  // [W|b] contiguous
-        ++kernels_;
-    } else if (!comm_) {  // W already updated in the dW epilogue; bias from the db partials
+    if (bf16_ && !comm_) {  // W already updated in the dW epilogue; bias from the db partials
         sgd_reduce(slot_b32(s), ws, col_chunks_, d_, d_, lr, st);
         kernels_ += 1;
-    } else {
+        w16_layer_[s] = -1;
+        return;
+    }
+    // The full-batch gradient [dW | db] (fp32, the slot's [W | b] layout) in `g`.
+    float* g = ws;
+    if (bf16_) {
         reduce_partials(ws, splits_, static_cast<int64_t>(dd), static_cast<int64_t>(dd), grad_red_, st);
         reduce_partials(ws + splits_ * dd, col_chunks_, d_, d_, grad_red_ + dd, st);
-        NCCL_OK(nccl().AllReduce(grad_red_, grad_red_, dd + d_, ncclFloat, ncclSum, comm_, st));
-        exact_sgd(slot_w32(s), grad_red_, static_cast<int64_t>(dd + d_), lr, st);
-        kernels_ += 3;
+        kernels_ += 2;
+        g = grad_red_;
+    }
+    if (comm_ && sharded_) {
+        // Reduce-scatter: this rank receives the summed gradient of its shard only, applies
+        // SGD to that shard of the slot, and (D2H op) writes back just that shard.
+        const size_t shard_f = shardA_ / 4;
+        float* mine = g + shard_f * static_cast<size_t>(rank_);
+        NCCL_OK(nccl().ReduceScatter(g, mine, shard_f, ncclFloat, ncclSum, comm_, st));
+        size_t lo = 0, hi = 0;
+        shard_range(shardA_, layer_bytes(), lo, hi);
+        if (hi > lo) {
+            exact_sgd(slot_w32(s) + lo / 4, mine, static_cast<int64_t>((hi - lo) / 4), lr, st);
+            ++kernels_;
+        }
+    } else {
+        if (comm_) NCCL_OK(nccl().AllReduce(g, g, dd + d_, ncclFloat, ncclSum, comm_, st));
+        exact_sgd(slot_w32(s), g, static_cast<int64_t>(dd + d_), lr, st);  // [W|b] contiguous
+        ++kernels_;
     }
     w16_layer_[s] = -1;  // the bf16 copy is now stale
 }
@@ -513,17 +563,19 @@ void Executor::enqueue_op(const Plan& plan, int i, bool train, int n_items, int6
             for (size_t j = 0; j < op.layers.size(); ++j) {
                 const int L = op.layers[j], s = op.slots[j];
                 if (op.weights[j]) {
-                    if (fmt == kFmtBf16Infer) {
-                        CUDA_OK(cudaMemcpyAsync(slot_ptr(s) + off_w16_,
-                                                host16_ + static_cast<size_t>(L) * wire16_bytes(),
-                                                wire16_bytes(), cudaMemcpyHostToDevice, st));
-                        h2d_bytes_ += wire16_bytes();
-                    } else {
-                        CUDA_OK(cudaMemcpyAsync(slot_ptr(s), host32_ + static_cast<size_t>(L) * (dd + d_),
-                                                layer_bytes(), cudaMemcpyHostToDevice, st));
-                        h2d_bytes_ += layer_bytes();
-                        w16_layer_[s] = -1;
-                    }
+                    // Whole image, or (sharded) only this rank's [lo, hi) byte range of it.
+                    const bool wire = fmt == kFmtBf16Infer;
+                    const size_t img = wire ? wire16_bytes() : layer_bytes();
+                    size_t lo = 0, hi = img;
+                    if (sharded_) shard_range(wire ? shardB_ : shardA_, img, lo, hi);
+                    const uint8_t* src = wire ? host16_ + static_cast<size_t>(L) * wire16_bytes()
+                                              : reinterpret_cast<const uint8_t*>(
+                                                    host32_ + static_cast<size_t>(L) * (dd + d_));
+                    uint8_t* dst = wire ? slot_ptr(s) + off_w16_ : slot_ptr(s);
+                    if (hi > lo)
+                        CUDA_OK(cudaMemcpyAsync(dst + lo, src + lo, hi - lo, cudaMemcpyHostToDevice, st));
+                    h2d_bytes_ += hi - lo;
+                    if (!wire) w16_layer_[s] = -1;
                 }
                 if (op.acts[j]) {
                     CUDA_OK(cudaMemcpyAsync(ba_[s], host_act_ + static_cast<size_t>(L) * act_b, act_b,
@@ -542,13 +594,30 @@ void Executor::enqueue_op(const Plan& plan, int i, bool train, int n_items, int6
             update_op(op, lr);
             break;
         case OpKind::D2H: {
+            // Updated fp32 master back to the pinned host copy (sharded: this rank's shard only;
+            // every rank streams exactly that shard in later calls, so its copy stays
+            // authoritative for it).
             const int L = op.layers[0], s = op.slots[0];
-            CUDA_OK(cudaMemcpyAsync(host32_ + static_cast<size_t>(L) * (dd + d_), slot_ptr(s),
-                                    layer_bytes(), cudaMemcpyDeviceToHost, st));
-            d2h_bytes_ += layer_bytes();
+            size_t lo = 0, hi = layer_bytes();
+            if (sharded_) shard_range(shardA_, layer_bytes(), lo, hi);
+            if (hi > lo)
+                CUDA_OK(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(host32_ + static_cast<size_t>(L) * (dd + d_)) + lo,
+                                        slot_ptr(s) + lo, hi - lo, cudaMemcpyDeviceToHost, st));
+            d2h_bytes_ += hi - lo;
             host16_stale_[L] = 1;
             break;
         }
+        case OpKind::AllGather:
+            for (size_t j = 0; j < op.layers.size(); ++j) {
+                const int s = op.slots[j];
+                const bool wire = fmt == kFmtBf16Infer;
+                uint8_t* base = wire ? slot_ptr(s) + off_w16_ : slot_ptr(s);
+                const size_t shard = wire ? shardB_ : shardA_;
+                NCCL_OK(nccl().AllGather(base + shard * static_cast<size_t>(rank_), base, shard,
+                                         ncclUint8, comm_, st));
+                if (!wire) w16_layer_[s] = -1;
+            }
+            break;
         case OpKind::ActSave:
             CUDA_OK(cudaMemcpyAsync(host_act_ + static_cast<size_t>(op.layer) * act_b, fa_[op.layer % 3],
                                     act_b, cudaMemcpyDeviceToHost, st));
@@ -890,7 +959,7 @@ void Executor::read_layer(int index, float* W, float* b) {
     if (b) std::memcpy(b, src + dd, static_cast<size_t>(d_) * 4);
 }
 
-void Executor::dp_init(const uint8_t id[128], int rank, int world) {
+void Executor::dp_init(const uint8_t id[128], int rank, int world, bool shard_weights) {
     if (world < 1 || rank < 0 || rank >= world) throw Error(SP_ERR_INVALID, "dp_init: bad rank/world");
     // world == 1 still builds a (1-rank) communicator: the data-parallel code path (split-K
     // partials, fixed-order reduce, NCCL all-reduce inside the captured graph, SGD on the
@@ -907,6 +976,9 @@ void Executor::dp_init(const uint8_t id[128], int rank, int world) {
     NCCL_OK(nccl().CommInitRank(&comm_, world, uid, rank));
     rank_ = rank;
     world_ = world;
+    sharded_ = shard_weights;
+    layout_slots(shard_weights ? world : 1);  // shard-aligned slot regions
+    cap_rows_ = 0;                            // gradient buffers re-sized for world shards
 }
 
 }  // namespace sp

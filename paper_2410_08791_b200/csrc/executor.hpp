@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -37,7 +38,7 @@ public:
     void digest_train(float loss, char out[17]) const;
     void set_trace(int level) { cfg_.trace = level; }
     std::string last_plan_text() const { return describe_plan(last_plan_); }
-    void dp_init(const uint8_t id[128], int rank, int world);
+    void dp_init(const uint8_t id[128], int rank, int world, bool shard_weights);
 
     const sp_stats& stats() const { return stats_; }
     const std::vector<sp_trace_event>& trace() const { return trace_; }
@@ -78,6 +79,7 @@ private:
         double gemm_flops = 0.0;
     };
 
+    void layout_slots(int world);
     void check_ready() const;
     void ensure_buffers(int64_t rows, int n_items, bool train, bool device_io);
     void refresh_host16();
@@ -116,7 +118,7 @@ private:
     std::vector<cudaEvent_t> ev_dep_;              // per-op dependency edges
     cudaEvent_t ev_call0_ = nullptr, ev_io_in_ = nullptr, ev_io_out_ = nullptr;
     cudaEvent_t ev_fork_ = nullptr, ev_join_[3] = {nullptr, nullptr, nullptr};
-    cudaEvent_t ev_call1_ = nullptr;
+    cudaEvent_t ev_call1_ = nullptr, ev_loss_ = nullptr;
     std::vector<uint8_t> cross_dep_;  // op has a dependent on another stream
     bool use_graphs_ = true;
     bool capturing_ = false;
@@ -159,6 +161,13 @@ private:
     // data parallel
     ncclComm_t comm_ = nullptr;
     int rank_ = 0, world_ = 1;
+    bool sharded_ = false;          // each rank streams 1/world of every layer (+ NCCL)
+    size_t shardA_ = 0, shardB_ = 0;  // shard bytes of the fp32 / bf16-wire slot images
+    // byte range [lo, hi) of this rank's shard within an image of `img` bytes
+    void shard_range(size_t shard, size_t img, size_t& lo, size_t& hi) const {
+        lo = std::min(img, shard * static_cast<size_t>(rank_));
+        hi = std::min(img, lo + shard);
+    }
     // metrics
     sp_stats stats_{};
     std::vector<sp_trace_event> trace_;

@@ -289,12 +289,29 @@ private:
                 plan_.h2d_act_layers += m.act;
             }
             const int id = push(std::move(op));
+            // Sharded streaming (data parallel): the H2D brought only this rank's 1/world of
+            // each layer; an NCCL all-gather over NVLink completes the slot before any use.
+            int fill = id;
+            if (in_.sharded) {
+                Op ag;
+                ag.kind = OpKind::AllGather;
+                ag.pass = pass_;
+                ag.deps.push_back(id);
+                for (const auto& m : group)
+                    if (m.weights) {
+                        ag.layers.push_back(seq()[m.pos]);
+                        ag.slots.push_back(m.slot);
+                        ag.weights.push_back(1);
+                        ag.acts.push_back(0);
+                    }
+                if (!ag.layers.empty()) fill = push(std::move(ag));
+            }
             for (const auto& m : group) {
                 if (m.weights) {
-                    slots_[m.slot].fill_op = id;
-                    slots_[m.slot].busy_op = id;
+                    slots_[m.slot].fill_op = fill;
+                    slots_[m.slot].busy_op = fill;
                 }
-                pos_load_[m.pos] = id;
+                pos_load_[m.pos] = m.weights ? fill : id;
                 if (m.act) pos_act_[m.pos] = id;
             }
             plan_.n_h2d_jobs += 1;
@@ -383,6 +400,9 @@ private:
             slots_[s].busy_op = wid;
             plan_.n_d2h_jobs += 1;
             plan_.d2h_weight_layers += 1;
+            // Sharded: only this rank's shard of the slot was updated (and written back), so
+            // the slot no longer holds a valid full copy of the layer.
+            if (in_.sharded) slots_[s].valid = false;
         }
         return id;
     }
@@ -487,7 +507,7 @@ Plan build_plan(const PlanInput& in, const std::vector<SlotCache>& initial) {
 }
 
 std::string describe_plan(const Plan& plan) {
-    static const char* names[] = {"H2D", "COMPUTE", "D2H", "LOSS", "UPDATE", "ACTSAVE"};
+    static const char* names[] = {"H2D", "COMPUTE", "D2H", "LOSS", "UPDATE", "ACTSAVE", "ALLGATHER"};
     std::ostringstream os;
     os << "slots=" << plan.n_slots << " ops=" << plan.ops.size()
        << " h2d_jobs=" << plan.n_h2d_jobs << " d2h_jobs=" << plan.n_d2h_jobs
@@ -508,7 +528,7 @@ std::string describe_plan(const Plan& plan) {
                << " slot=" << op.slot;
         if (op.kind == OpKind::Update) os << " layer=" << op.layer << " slot=" << op.slot;
         if (op.kind == OpKind::ActSave) os << " layer=" << op.layer;
-        if (op.kind == OpKind::H2D || op.kind == OpKind::D2H) {
+        if (op.kind == OpKind::H2D || op.kind == OpKind::D2H || op.kind == OpKind::AllGather) {
             std::vector<int> w(op.weights.begin(), op.weights.end()),
                 a(op.acts.begin(), op.acts.end());
             os << " layers=" << list(op.layers) << " slots=" << list(op.slots)

@@ -18,7 +18,10 @@
 namespace sp {
 
 enum class Strategy : int { Standard = 0, CpuOnly = 1, Naive = 2, Superpipeline = 3 };
-enum class OpKind : int { H2D = 0, Compute = 1, D2H = 2, Loss = 3, Update = 4, ActSave = 5 };
+enum class OpKind : int {
+    H2D = 0, Compute = 1, D2H = 2, Loss = 3, Update = 4, ActSave = 5,
+    AllGather = 6  // sharded streaming: NCCL all-gather completing a slot (update stream)
+};
 
 // StrategyConfig::validate (strategy.cpp:19-36). Returns an empty string when valid.
 std::string validate_strategy(int strategy, int k, int k_prime, int n_layers);
@@ -36,6 +39,7 @@ struct PlanInput {
     bool train = false;
     int n_items = 1;
     bool checkpointing = false;
+    bool sharded = false;         // data parallel: H2D 1/world of each layer + all-gather
     std::vector<uint8_t> frozen;  // per layer
     uint64_t layer_bytes = 0;     // reference ledger units: (d*d + d) * 4
     uint64_t act_bytes = 0;       // rows * d * 4

@@ -323,11 +323,13 @@ def test_dp_code_path_single_rank(numerics):
     x, t = sp.make_input(21, 0, rows, d), sp.make_input(21, 1, rows, d)
     outs = []
     for s in [S(sp.SUPERPIPELINE, 2, 1), S(sp.SUPERPIPELINE, 4, 2), S(sp.STANDARD)]:
-        for dp in (False, True):
+        # None: single-GPU path; "allreduce": replicated streaming + all-reduce; "sharded":
+        # 1/world H2D + NCCL all-gather, reduce-scatter + shard SGD + shard writeback.
+        for dp in (None, "allreduce", "sharded"):
             with sp.Executor(6, d, s, numerics=numerics) as ex:
                 ex.register_model(model)
                 if dp:
-                    ex.dp_init(sp.Executor.nccl_unique_id(), 0, 1)
+                    ex.dp_init(sp.Executor.nccl_unique_id(), 0, 1, shard_weights=dp == "sharded")
                 losses = [ex.train_step(x, t, 0.05) for _ in range(2)]  # 2nd step: graph replay
                 outs.append((s, dp, losses, ex.read_model(model)))
     base = outs[0]
@@ -338,9 +340,14 @@ def test_dp_code_path_single_rank(numerics):
             assert np.array_equal(m.W, base[3].W) and np.array_equal(m.b, base[3].b), (s, dp)
         else:
             assert norm_err(m.W - model.W, base[3].W - model.W) <= 1e-3, (s, dp)
-    dps = [o for o in outs if o[1]]
-    for s, dp, losses, m in dps[1:]:  # DP path itself is window-invariant, bitwise
-        assert losses == dps[0][2] and np.array_equal(m.W, dps[0][3].W)
+    for mode in ("allreduce", "sharded"):  # each DP mode is itself window-invariant, bitwise
+        dps = [o for o in outs if o[1] == mode]
+        for s, dp, losses, m in dps[1:]:
+            assert losses == dps[0][2] and np.array_equal(m.W, dps[0][3].W), (s, dp)
+    ar = [o for o in outs if o[1] == "allreduce"][0]
+    sh = [o for o in outs if o[1] == "sharded"][0]
+    assert np.array_equal(ar[3].W, sh[3].W) and ar[2] == sh[2]  # 1 rank: identical math
+    dps = [o for o in outs if o[1] == "sharded"]
     if numerics == sp.EXACT:  # and matches the CPU oracle bitwise
         W, b = model.W.copy(), model.b.copy()
         for _ in range(2):

@@ -22,7 +22,7 @@ import paper_2410_08791_b200 as sp
 from test_cpu_boundary import parse_plan
 
 STREAM = {"H2D": "h2d", "COMPUTE": "comp", "LOSS": "comp", "D2H": "d2h", "ACTSAVE": "d2h",
-          "UPDATE": "upd"}
+          "UPDATE": "upd", "ALLGATHER": "upd"}
 
 
 def accesses(ops, ckpt, frozen):
@@ -51,6 +51,9 @@ def accesses(ops, ckpt, frozen):
         elif k == "UPDATE":
             acc.append((i, ("g", op["layer"] % 2), False))
             acc.append((i, ("W", op["slot"]), True))
+        elif k == "ALLGATHER":  # sharded streaming: completes the slot over NVLink
+            for s in op["slots"]:
+                acc.append((i, ("W", s), True))
         elif k == "D2H":
             for L, s in zip(op["layers"], op["slots"]):
                 acc.append((i, ("W", s), False))
@@ -80,10 +83,10 @@ def happens_before(ops):
     return lambda a, b: bool(reach[b] >> a & 1)
 
 
-def check(n, strategy, train, ckpt, items=1, frozen=None):
+def check(n, strategy, train, ckpt, items=1, frozen=None, sharded=False):
     frozen = frozen or [0] * n
     txt = sp.describe_plan(n, 8, strategy, n_items=items, train=train, checkpointing=ckpt,
-                           frozen=frozen)
+                           frozen=frozen, sharded=sharded)
     assert not txt.startswith("ERROR"), txt
     head, ops = parse_plan(txt)
     ck = ckpt and train and strategy.kind != sp.STANDARD
@@ -122,6 +125,36 @@ def test_inference_plan_has_no_cross_stream_races(n, items):
     for s in STRATS:
         if s.k <= n:
             check(n, s, False, False, items=items)
+            check(n, s, False, False, items=items, sharded=True)
+
+
+@pytest.mark.parametrize("n", [2, 5, 8])
+@pytest.mark.parametrize("ckpt", [False, True])
+def test_sharded_training_plan_has_no_cross_stream_races(n, ckpt):
+    for s in STRATS:
+        if s.k <= n:
+            for frozen in ([0] * n, [1] + [0] * (n - 1)):
+                check(n, s, True, ckpt, frozen=frozen, sharded=True)
+
+
+def test_sharded_plan_gathers_every_loaded_layer_and_never_reuses_updated_slots():
+    head, ops = parse_plan(sp.describe_plan(8, 8, sp.StrategyConfig(sp.SUPERPIPELINE, 4, 2),
+                                            train=True, sharded=True))
+    h2d = [o for o in ops if o["kind"] == "H2D"]
+    ag = [o for o in ops if o["kind"] == "ALLGATHER"]
+    assert len(ag) == len(h2d)
+    for o in ag:  # each all-gather directly follows (and depends on) its H2D
+        assert ops[o["index"] - 1]["kind"] == "H2D" and o["index"] - 1 in o["deps"]
+    # every compute depends on the all-gather that last completed its slot (not the raw H2D)
+    fill = {}
+    for o in ops:
+        if o["kind"] == "ALLGATHER":
+            for s in o["slots"]:
+                fill[s] = o["index"]
+        if o["kind"] == "COMPUTE":
+            assert fill[o["slot"]] in o["deps"], o
+    # after its backward update a slot holds only this rank's fresh shard: the next step must
+    # reload it (final slot cache invalid), checked through the executor on GPU
 
 
 def test_checker_detects_a_missing_edge():
