@@ -175,6 +175,12 @@ int sp_dp_init(sp_exec* ex, const uint8_t id[128], int32_t rank, int32_t world);
  * (world > 1). world = 1 builds a 1-rank communicator (exercises the same code path). */
 int sp_dp_init2(sp_exec* ex, const uint8_t id[128], int32_t rank, int32_t world,
                 int32_t shard_weights);
+/* Collective, every rank in the same order. After sharded training each rank's pinned host
+ * master holds only its own shard of every trained layer; sp_dp_sync all-gathers those shards
+ * (NCCL over NVLink) so the host copy is whole again. Until then sp_read_layer,
+ * sp_digest_train, bf16 sp_forward and sp_dp_init fail with SP_ERR_STATE instead of returning
+ * a mix of current and stale shards. No-op when nothing is partial. */
+int sp_dp_sync(sp_exec* ex);
 
 /* ---- host utilities ---------------------------------------------------------------- */
 /* Pinned (page-locked, portable) host buffers for callers' inputs/outputs. */

@@ -30,6 +30,10 @@ int sp_debug_gemm_bf16_async(int32_t M, int32_t N, int32_t K, const void* A, int
                              int32_t epilogue, void* out, int32_t ldo, const float* bias,
                              int32_t relu, const void* gate, int32_t ldg, int32_t splits,
                              int32_t block_n, int32_t cta, void* stream);
+/* Sharded streaming geometry (the executor's own functions): shard size for an image of
+ * img bytes over world ranks, and rank's byte range [lo, hi). */
+uint64_t sp_debug_shard_range(uint64_t img, int32_t world, int32_t rank, uint64_t* lo,
+                              uint64_t* hi);
 /* Split count the GEMM will use for a given K and requested splits. */
 int32_t sp_debug_effective_splits(int32_t K, int32_t splits);
 

@@ -62,11 +62,12 @@ EXPORTS = [
     "sp_forward", "sp_forward_device", "sp_train_step", "sp_train_step_device",
     "sp_read_layer", "sp_get_stats", "sp_get_trace", "sp_set_trace", "sp_last_plan",
     "sp_nccl_unique_id",
-    "sp_dp_init", "sp_dp_init2",
+    "sp_dp_init", "sp_dp_init2", "sp_dp_sync",
     "sp_host_alloc", "sp_host_free", "sp_peak_weight_residency", "sp_validate_strategy",
     "sp_describe_plan", "sp_build_layer", "sp_make_input", "sp_digest_tensors",
     "sp_digest_train",
     "sp_debug_gemm_bf16", "sp_debug_gemm_bf16_async", "sp_debug_effective_splits",
+    "sp_debug_shard_range",
 ]
 
 
@@ -94,6 +95,7 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "sp_nccl_unique_id": ([C.c_char_p], C.c_int),
         "sp_dp_init": ([ex, C.c_char_p, i32, i32], C.c_int),
         "sp_dp_init2": ([ex, C.c_char_p, i32, i32, i32], C.c_int),
+        "sp_dp_sync": ([ex], C.c_int),
         "sp_host_alloc": ([u64], vp),
         "sp_host_free": ([vp], None),
         "sp_peak_weight_residency": ([i32, i32, i32, i32, u64], u64),
@@ -108,6 +110,7 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "sp_debug_gemm_bf16_async": ([i32, i32, i32, vp, i32, i32, vp, i32, i32, i32, vp, i32,
                                       vp, i32, vp, i32, i32, i32, i32, vp], C.c_int),
         "sp_debug_effective_splits": ([i32, i32], i32),
+        "sp_debug_shard_range": ([u64, i32, i32, C.POINTER(u64), C.POINTER(u64)], u64),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

@@ -172,6 +172,11 @@ int sp_dp_init2(sp_exec* ex, const uint8_t id[128], int32_t rank, int32_t world,
     return guarded(ex, [&] { ex->impl->dp_init(id, rank, world, shard_weights != 0); });
 }
 
+int sp_dp_sync(sp_exec* ex) {
+    if (!ex) return SP_ERR_INVALID;
+    return guarded(ex, [&] { ex->impl->dp_sync(); });
+}
+
 void* sp_host_alloc(uint64_t bytes) {
     void* p = nullptr;
     if (cudaHostAlloc(&p, bytes ? bytes : 1, cudaHostAllocPortable) != cudaSuccess) return nullptr;
@@ -311,6 +316,13 @@ extern "C" int sp_debug_gemm_bf16(int32_t M, int32_t N, int32_t K, const void* A
     cudaError_t e = sp::gemm_bf16(g, 0);
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     return static_cast<int>(e);
+}
+
+extern "C" uint64_t sp_debug_shard_range(uint64_t img, int32_t world, int32_t rank, uint64_t* lo,
+                                         uint64_t* hi) {
+    const uint64_t shard = sp::shard_bytes(img, world);
+    sp::shard_range(shard, img, rank, *lo, *hi);
+    return shard;
 }
 
 extern "C" int32_t sp_debug_effective_splits(int32_t K, int32_t splits) {

@@ -119,6 +119,7 @@ Executor::Executor(const sp_config& cfg) : cfg_(cfg) {
     frozen_.assign(static_cast<size_t>(n_), 0);
     registered_.assign(static_cast<size_t>(n_), 0);
     host16_stale_.assign(static_cast<size_t>(n_), 1);
+    host_partial_.assign(static_cast<size_t>(n_), 0);
 }
 
 Executor::~Executor() {
@@ -154,8 +155,8 @@ Executor::~Executor() {
 // Each region is cut into `world` equal shards (256-byte aligned) so a rank can H2D / D2H its
 // own shard and NCCL all-gather / reduce-scatter the rest in place.
 void Executor::layout_slots(int world) {
-    shardA_ = round_up((layer_bytes() + world - 1) / world, 256);
-    shardB_ = round_up((wire16_bytes() + world - 1) / world, 256);
+    shardA_ = shard_bytes(layer_bytes(), world);
+    shardB_ = shard_bytes(wire16_bytes(), world);
     const size_t a_region = round_up(shardA_ * world, 1024);
     off_w16_ = a_region;
     slot_bytes_ = bf16_ ? round_up(a_region + shardB_ * world, 1024) : a_region;
@@ -187,8 +188,17 @@ void Executor::register_layer(int index, const float* W, const float* b, int act
     frozen_[index] = frozen != 0;
     registered_[index] = 1;
     host16_stale_[index] = 1;
+    host_partial_[index] = 0;
     for (auto& c : cache_)
         if (c.layer == index) c.valid = false;
+}
+
+void Executor::require_full_host(int layer, const char* what) const {
+    for (int i = 0; i < n_; ++i)
+        if ((layer < 0 || i == layer) && host_partial_[static_cast<size_t>(i)])
+            throw Error(SP_ERR_STATE, std::string(what) + ": layer " + std::to_string(i) +
+                                          " holds only this rank's shard after sharded training; "
+                                          "call sp_dp_sync() on every rank first");
 }
 
 void Executor::check_ready() const {
@@ -878,6 +888,9 @@ void Executor::forward(const float* x, int64_t rows, int n_items, float* y, bool
     if (rows > (1ll << 31) - 1) throw Error(SP_ERR_INVALID, "run_inference: too many rows");
     check_ready();
     const int fmt = bf16_ ? kFmtBf16Infer : kFmtExactF32;
+    // The bf16 wire image is derived from the whole fp32 master; its shards do not line up
+    // with the fp32 shards, so it needs every element current on this rank.
+    if (bf16_) require_full_host(-1, "run_inference");
     Plan plan = make_plan(false, n_items, rows, fmt);
     refresh_host16();
     ensure_buffers(rows, n_items, false, device_io);
@@ -923,6 +936,9 @@ float Executor::train_step(const float* x, const float* target, int64_t rows, fl
     for (auto s : {s_h2d_, s_comp_, s_d2h_, s_upd_}) CUDA_OK(cudaStreamSynchronize(s));
     CUDA_OK(cudaGetLastError());
     collect_stats(plan, 1, true);
+    if (sharded_)
+        for (int L = 0; L < n_; ++L)
+            if (!frozen_[static_cast<size_t>(L)]) host_partial_[static_cast<size_t>(L)] = 1;
     const float loss = loss_host_[0] / static_cast<float>(rows * d_ * world_);
     stats_.loss = loss;
     std::memset(stats_.digest, 0, sizeof(stats_.digest));  // on demand: digest_train()
@@ -930,6 +946,7 @@ float Executor::train_step(const float* x, const float* target, int64_t rows, fl
 }
 
 void Executor::digest_train(float loss, char out[17]) const {
+    require_full_host(-1, "digest_train");
     // digest_train (engine.cpp:574-581): loss bytes, then each block's W and b — the host
     // master copy is [W_0 b_0 W_1 b_1 ...] contiguous, exactly the reference's byte order.
     uint64_t h = 0xCBF29CE484222325ull;
@@ -953,6 +970,7 @@ void Executor::digest_train(float loss, char out[17]) const {
 
 void Executor::read_layer(int index, float* W, float* b) {
     if (index < 0 || index >= n_) throw Error(SP_ERR_INVALID, "read_layer: index out of range");
+    require_full_host(index, "read_layer");
     const size_t dd = static_cast<size_t>(d_) * d_;
     const float* src = host32_ + static_cast<size_t>(index) * (dd + d_);
     if (W) std::memcpy(W, src, dd * 4);
@@ -961,6 +979,7 @@ void Executor::read_layer(int index, float* W, float* b) {
 
 void Executor::dp_init(const uint8_t id[128], int rank, int world, bool shard_weights) {
     if (world < 1 || rank < 0 || rank >= world) throw Error(SP_ERR_INVALID, "dp_init: bad rank/world");
+    require_full_host(-1, "dp_init");
     // world == 1 still builds a (1-rank) communicator: the data-parallel code path (split-K
     // partials, fixed-order reduce, NCCL all-reduce inside the captured graph, SGD on the
     // update stream) then runs end to end on a single GPU.
@@ -979,6 +998,35 @@ void Executor::dp_init(const uint8_t id[128], int rank, int world, bool shard_we
     sharded_ = shard_weights;
     layout_slots(shard_weights ? world : 1);  // shard-aligned slot regions
     cap_rows_ = 0;                            // gradient buffers re-sized for world shards
+}
+
+void Executor::dp_sync() {
+    // Collective (every rank, same order): for each layer whose host master is shard-only,
+    // stream this rank's shard into slot 0, all-gather the image over NCCL, and copy the
+    // whole image back to the pinned host master.
+    bool any = false;
+    for (uint8_t p : host_partial_) any = any || p;
+    if (!any) return;
+    if (!comm_) throw Error(SP_ERR_STATE, "dp_sync: no communicator");
+    CUDA_OK(cudaSetDevice(cfg_.device));
+    for (auto s : {s_h2d_, s_comp_, s_d2h_, s_upd_}) CUDA_OK(cudaStreamSynchronize(s));
+    const size_t img = layer_bytes(), dd = static_cast<size_t>(d_) * d_;
+    size_t lo = 0, hi = 0;
+    shard_range(shardA_, img, lo, hi);
+    uint8_t* stage = slot_ptr(0);
+    for (int L = 0; L < n_; ++L) {
+        if (!host_partial_[static_cast<size_t>(L)]) continue;
+        uint8_t* host = reinterpret_cast<uint8_t*>(host32_ + static_cast<size_t>(L) * (dd + d_));
+        if (hi > lo) CUDA_OK(cudaMemcpyAsync(stage + lo, host + lo, hi - lo, cudaMemcpyHostToDevice, s_upd_));
+        NCCL_OK(nccl().AllGather(stage + shardA_ * static_cast<size_t>(rank_), stage, shardA_,
+                                 ncclUint8, comm_, s_upd_));
+        CUDA_OK(cudaMemcpyAsync(host, stage, img, cudaMemcpyDeviceToHost, s_upd_));
+        CUDA_OK(cudaStreamSynchronize(s_upd_));  // stage is reused by the next layer
+        host_partial_[static_cast<size_t>(L)] = 0;
+        host16_stale_[static_cast<size_t>(L)] = 1;
+    }
+    for (auto& c : cache_) c.valid = false;  // slot 0 was overwritten
+    std::fill(w16_layer_.begin(), w16_layer_.end(), -1);
 }
 
 }  // namespace sp

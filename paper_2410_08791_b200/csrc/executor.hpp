@@ -39,6 +39,7 @@ public:
     void set_trace(int level) { cfg_.trace = level; }
     std::string last_plan_text() const { return describe_plan(last_plan_); }
     void dp_init(const uint8_t id[128], int rank, int world, bool shard_weights);
+    void dp_sync();
 
     const sp_stats& stats() const { return stats_; }
     const std::vector<sp_trace_event>& trace() const { return trace_; }
@@ -163,10 +164,16 @@ private:
     int rank_ = 0, world_ = 1;
     bool sharded_ = false;          // each rank streams 1/world of every layer (+ NCCL)
     size_t shardA_ = 0, shardB_ = 0;  // shard bytes of the fp32 / bf16-wire slot images
-    // byte range [lo, hi) of this rank's shard within an image of `img` bytes
+    // Sharded training writes back only this rank's shard: such a layer's pinned host master
+    // is authoritative for that shard alone until dp_sync() all-gathers it.
+    std::vector<uint8_t> host_partial_;
+    void require_full_host(int layer, const char* what) const;
+    // byte range [lo, hi) of this rank's shard within an image of `img` bytes (plan.hpp)
     void shard_range(size_t shard, size_t img, size_t& lo, size_t& hi) const {
-        lo = std::min(img, shard * static_cast<size_t>(rank_));
-        hi = std::min(img, lo + shard);
+        uint64_t l = 0, h = 0;
+        sp::shard_range(shard, img, rank_, l, h);
+        lo = static_cast<size_t>(l);
+        hi = static_cast<size_t>(h);
     }
     // metrics
     sp_stats stats_{};

@@ -31,6 +31,19 @@ uint64_t peak_weight_residency(int strategy, int k, int k_prime, int n_layers,
 // Number of HBM weight slots the ring needs (S = min(k+k', n) for Superpipeline).
 int ring_slots(int strategy, int k, int k_prime, int n_layers);
 
+// Sharded streaming: an image of `img` bytes is cut into `world` equal shards of
+// shard_bytes(img, world) bytes (256-byte aligned, so world*shard >= img); rank r owns the
+// byte range [lo, hi) = [min(img, r*shard), min(img, (r+1)*shard)).
+inline uint64_t shard_bytes(uint64_t img, int world) {
+    const uint64_t per = (img + static_cast<uint64_t>(world) - 1) / static_cast<uint64_t>(world);
+    return (per + 255) / 256 * 256;
+}
+inline void shard_range(uint64_t shard, uint64_t img, int rank, uint64_t& lo, uint64_t& hi) {
+    const uint64_t start = shard * static_cast<uint64_t>(rank);
+    lo = start < img ? start : img;
+    hi = lo + shard < img ? lo + shard : img;
+}
+
 struct PlanInput {
     int n_layers = 1;
     int strategy = 3;

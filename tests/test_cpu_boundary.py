@@ -164,3 +164,23 @@ def test_plan_training_reuses_forward_tail_without_reload():
 
 def test_cpu_only_is_rejected_not_emulated():
     assert sp.describe_plan(4, 8, sp.StrategyConfig(sp.CPU_ONLY)).startswith("ERROR")
+
+
+@pytest.mark.parametrize("d", [1, 7, 64, 300, 1600])
+@pytest.mark.parametrize("world", [1, 2, 3, 4, 8])
+def test_shard_ranges_tile_every_slot_image(d, world):
+    """Sharded streaming (executor.cpp layout_slots / enqueue_op): the ranks' byte ranges of
+    a slot image are 256-aligned, disjoint, cover the image exactly once, and fit in
+    world*shard bytes so NCCL all-gather / reduce-scatter (equal counts per rank) are valid."""
+    import ctypes as C
+    for img in ((d * d + d) * 4, d * d * 2 + d * 4):  # fp32 W|b image, bf16 wire image
+        covered = 0
+        for r in range(world):
+            lo, hi = C.c_uint64(), C.c_uint64()
+            shard = _capi.LIB.sp_debug_shard_range(img, world, r, C.byref(lo), C.byref(hi))
+            assert shard % 256 == 0 and shard * world >= img
+            assert lo.value == min(img, r * shard)
+            assert lo.value <= hi.value <= lo.value + shard
+            assert lo.value == covered or hi.value == lo.value
+            covered = max(covered, hi.value)
+        assert covered == img

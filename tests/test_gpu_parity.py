@@ -331,19 +331,29 @@ def test_dp_code_path_single_rank(numerics):
                 if dp:
                     ex.dp_init(sp.Executor.nccl_unique_id(), 0, 1, shard_weights=dp == "sharded")
                 losses = [ex.train_step(x, t, 0.05) for _ in range(2)]  # 2nd step: graph replay
+                if dp == "sharded":
+                    # host master is shard-only until the collective sync: loud, not stale
+                    with pytest.raises(sp.SpError, match="sp_dp_sync"):
+                        ex.read_model(model)
+                    ex.dp_sync()
                 outs.append((s, dp, losses, ex.read_model(model)))
+                # inference after training (bf16: wire image rebuilt from the synced master)
+                y = ex.forward([x[:4]])
+                outs[-1] = outs[-1] + (y,)
     base = outs[0]
-    for s, dp, losses, m in outs:
+    for s, dp, losses, m, y in outs:
         if numerics == sp.EXACT or dp == base[1]:
             assert losses == base[2], (s, dp)
+            assert np.array_equal(y, base[4]), (s, dp)
         if numerics == sp.EXACT:
             assert np.array_equal(m.W, base[3].W) and np.array_equal(m.b, base[3].b), (s, dp)
         else:
             assert norm_err(m.W - model.W, base[3].W - model.W) <= 1e-3, (s, dp)
     for mode in ("allreduce", "sharded"):  # each DP mode is itself window-invariant, bitwise
         dps = [o for o in outs if o[1] == mode]
-        for s, dp, losses, m in dps[1:]:
+        for s, dp, losses, m, y in dps[1:]:
             assert losses == dps[0][2] and np.array_equal(m.W, dps[0][3].W), (s, dp)
+            assert np.array_equal(y[0], dps[0][4][0]), (s, dp)
     ar = [o for o in outs if o[1] == "allreduce"][0]
     sh = [o for o in outs if o[1] == "sharded"][0]
     assert np.array_equal(ar[3].W, sh[3].W) and ar[2] == sh[2]  # 1 rank: identical math
