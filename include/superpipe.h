@@ -160,6 +160,13 @@ int sp_get_stats(const sp_exec* ex, sp_stats* out);
 int64_t sp_last_plan(const sp_exec* ex, char* buf, int64_t cap);
 /* Changes the trace level (sp_config.trace) for subsequent calls. */
 int sp_set_trace(sp_exec* ex, int32_t level);
+/* Item batching for sp_forward (layer-major streaming). 0 (default): the
+ * reference's item-major execution_stream (strategy.cpp:38-46), every item streams the whole
+ * layer stack. 1: the n_items inputs are stacked into one [n_items*rows, d] pass, so each
+ * layer crosses the host link once per call instead of once per item. Rows are independent
+ * in the layer math, so outputs are bitwise identical; only the transfer count, the ledger
+ * and the time change. */
+int sp_set_item_batching(sp_exec* ex, int32_t on);
 /* Copies up to cap events of the last call's measured timeline; *count = total rows. */
 int sp_get_trace(const sp_exec* ex, sp_trace_event* events, int32_t cap, int32_t* count);
 

@@ -133,6 +133,12 @@ int sp_set_trace(sp_exec* ex, int32_t level) {
     return SP_OK;
 }
 
+int sp_set_item_batching(sp_exec* ex, int32_t on) {
+    if (!ex || on < 0 || on > 1) return SP_ERR_INVALID;
+    ex->impl->set_item_batching(on != 0);
+    return SP_OK;
+}
+
 int sp_digest_train(const sp_exec* ex, float loss, char out[17]) {
     if (!ex || !out) return SP_ERR_INVALID;
     ex->impl->digest_train(loss, out);

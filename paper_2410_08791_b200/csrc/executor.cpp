@@ -472,10 +472,11 @@ void Executor::compute_op(const Op& op, bool train, int64_t rows, int fmt) {
     g.B = dz;  // dz [r][j]: N-major B
     g.ldb = d_;
     g.b_mn = true;
-    // One GPU: no gradient exchange, so SGD is fused into the dW epilogue (W -= lr*acc on the
-    // slot's fp32 master; splits = 1 keeps each element owned by one CTA). Data parallel: raw
-    // split-K partials, reduced + all-reduced + applied on the update stream.
-    const bool fused = comm_ == nullptr;
+    // One GPU and enough output tiles to fill the SMs: SGD is fused into the dW epilogue
+    // (W -= lr*acc on the slot's fp32 master; splits = 1 keeps each element owned by one CTA).
+    // Otherwise (too few d x d tiles for the SMs, or data parallel): raw split-K partials,
+    // reduced in a fixed order [+ all-reduced] and applied on the update stream.
+    const bool fused = dw_fused_;
     g.epilogue = fused ? EPI_SGD_F32 : EPI_F32;
     g.out = fused ? static_cast<void*>(slot_w32(s)) : static_cast<void*>(ws);
     g.ldo = d_;
@@ -520,8 +521,15 @@ void Executor::update_op(const Op& op, float lr) {
     const size_t dd = static_cast<size_t>(d_) * d_;
     cudaStream_t st = s_upd_;
     float* ws = gws_[L % 2];
-    if (bf16_ && !comm_) {  // W already updated in the dW epilogue; bias from the db partials
-        sgd_reduce(slot_b32(s), ws, col_chunks_, d_, d_, lr, st);
+    if (bf16_ && !comm_) {
+        // W: updated in the dW epilogue (fused), or here from the split-K partials in a fixed
+        // order; bias from the db column-sum partials.
+        const size_t db_off = dw_fused_ ? 0 : static_cast<size_t>(splits_) * dd;
+        if (!dw_fused_) {
+            sgd_reduce(slot_w32(s), ws, splits_, static_cast<int64_t>(dd), static_cast<int64_t>(dd), lr, st);
+            kernels_ += 1;
+        }
+        sgd_reduce(slot_b32(s), ws + db_off, col_chunks_, d_, d_, lr, st);
         kernels_ += 1;
         w16_layer_[s] = -1;
         return;
@@ -887,6 +895,12 @@ void Executor::forward(const float* x, int64_t rows, int n_items, float* y, bool
     if (rows < 1 || n_items < 1) throw Error(SP_ERR_INVALID, "run_inference: no inputs");
     if (rows > (1ll << 31) - 1) throw Error(SP_ERR_INVALID, "run_inference: too many rows");
     check_ready();
+    if (item_batching_ && n_items > 1 && rows * n_items <= (1ll << 31) - 1) {
+        // [items][rows][d] is contiguous, i.e. one [items*rows][d] input: one pass over the
+        // ring serves every item (row-independent math, so outputs are unchanged).
+        rows *= n_items;
+        n_items = 1;
+    }
     const int fmt = bf16_ ? kFmtBf16Infer : kFmtExactF32;
     // The bf16 wire image is derived from the whole fp32 master; its shards do not line up
     // with the fp32 shards, so it needs every element current on this rank.
@@ -923,6 +937,7 @@ float Executor::train_step(const float* x, const float* target, int64_t rows, fl
         const int want = choose_splits(d_, d_, static_cast<int>(rows), dw_bn_);
         splits_ = effective_splits(static_cast<int>(rows), std::min(want, splits_cap_));
         col_chunks_ = colsum_chunks(rows);
+        dw_fused_ = comm_ == nullptr && splits_ == 1;
     }
     reset_call_counters();
     cur_x_ = device_io ? x : xin_;

@@ -37,6 +37,7 @@ public:
     void read_layer(int index, float* W, float* b);
     void digest_train(float loss, char out[17]) const;
     void set_trace(int level) { cfg_.trace = level; }
+    void set_item_batching(bool on) { item_batching_ = on; }
     std::string last_plan_text() const { return describe_plan(last_plan_); }
     void dp_init(const uint8_t id[128], int rank, int world, bool shard_weights);
     void dp_sync();
@@ -122,6 +123,7 @@ private:
     cudaEvent_t ev_call1_ = nullptr, ev_loss_ = nullptr;
     std::vector<uint8_t> cross_dep_;  // op has a dependent on another stream
     bool use_graphs_ = true;
+    bool item_batching_ = false;  // forward: n_items x rows as one layer-major pass
     bool capturing_ = false;
     // Timing events: plain records when eager; "external" event-record nodes under capture
     // (cudaEventRecordExternal is only valid while capturing).
@@ -159,6 +161,7 @@ private:
     double host_enqueue_ms_ = 0.0;
     int splits_ = 1, dw_bn_ = 256, col_chunks_ = 1, splits_cap_ = 1, col_chunks_cap_ = 1;
     int loss_blocks_ = 0;
+    bool dw_fused_ = true;  // bf16 dW: SGD fused into the GEMM epilogue (else split-K partials)
     // data parallel
     ncclComm_t comm_ = nullptr;
     int rank_ = 0, world_ = 1;

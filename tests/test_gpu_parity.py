@@ -219,14 +219,17 @@ def test_bf16_inference_window_invariant_and_close():
     assert rel_err(outs[0], ref) <= BF16_FWD_TOL
 
 
-def test_bf16_train_window_invariant_and_close():
-    model = sp.build_model(13, 8, 192, 1)
-    x, t = sp.make_input(13, 0, 640, 192), sp.make_input(13, 1, 640, 192)
+@pytest.mark.parametrize("d,rows", [(192, 640), (256, 2048)])
+def test_bf16_train_window_invariant_and_close(d, rows):
+    # (192, 640): 10 K-blocks, one split -> SGD fused into the dW epilogue;
+    # (256, 2048): 2 output tiles for 148 SMs -> split-K partials + fixed-order SGD reduce.
+    model = sp.build_model(13, 8, d, 1)
+    x, t = sp.make_input(13, 0, rows, d), sp.make_input(13, 1, rows, d)
     loss, Wn, bn = ORC.train_step(model.W, model.b, x, t, 0.05, frozen=model.frozen)
     results = []
     for s in [S(sp.STANDARD), S(sp.SUPERPIPELINE, 2, 1), S(sp.SUPERPIPELINE, 5, 2)]:
         for ckpt in (False, True):
-            r = sp.run_train_step(model, x, t, s, sp.ArenaConfig(), sp.TrainConfig(0.05, ckpt, 640),
+            r = sp.run_train_step(model, x, t, s, sp.ArenaConfig(), sp.TrainConfig(0.05, ckpt, rows),
                                   numerics=sp.BF16)
             results.append(r)
     for r in results[1:]:
@@ -381,3 +384,23 @@ def test_bf16_full_size_window_invariance():
             loss = ex.train_step(x, t, 0.01)
             digests.append((loss, ex.digest_train(loss)))
     assert len(set(digests)) == 1, digests
+
+
+@pytest.mark.parametrize("numerics", [sp.EXACT, sp.BF16])
+def test_item_batching_is_bitwise_and_streams_once(numerics):
+    """sp_set_item_batching (SURVEY 8f layer-major streaming): the items are stacked into one
+    pass, so every layer crosses the link once per call instead of once per item, and the
+    outputs are bitwise those of the reference's item-major stream."""
+    n, d, items, rows = 6, 64 if numerics == sp.EXACT else 256, 4, 3
+    model = sp.build_model(17, n, d)
+    xs = np.stack(inputs(17, items, rows, d))
+    out = {}
+    for batching in (False, True):
+        with sp.Executor(n, d, S(sp.SUPERPIPELINE, 2, 1), numerics=numerics) as ex:
+            ex.register_model(model)
+            ex.set_item_batching(batching)
+            out[batching] = (ex.forward(xs), ex.stats())
+    assert np.array_equal(out[False][0], out[True][0])
+    assert out[False][1]["h2d_bytes"] == items * out[True][1]["h2d_bytes"]  # no cross-item reuse at S=3 < n
+    if numerics == sp.EXACT:
+        assert np.array_equal(out[True][0], oracle_outputs(model, list(xs)))

@@ -1,0 +1,91 @@
+"""Superpipeline training step (run_train_step path, bf16 tcgen05) on the BASELINE training
+configs with the reference's square dense blocks:
+  c2   48 x d=1600, 16384 rows, SP(4,2)             (GPT-2 XL depth/width; the bench.py headline)
+  c4   32 x d=1280, 65792 rows (256 x 257), SP(4,2)  (ViT-H/14 depth/width), activations saved
+       on device (ckpt off) and offloaded to pinned host memory (ckpt on)
+Inputs are device-resident (train_step_device); weights stream from the executor's pinned host
+master every step. Prints one JSON line per run: samples/s, ms/step, per-layer roofline
+(max of FLOPs at the measured bf16 peak and host-link bytes at the measured pinned bandwidth;
+activation offload adds its D2H in the forward and its H2D in the backward), HBM peaks."""
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tools"))
+import bench  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2410_08791_b200 as sp  # noqa: E402
+from infer_bench import build_weights  # noqa: E402
+
+CONFIGS = {
+    "c2": dict(n=48, d=1600, rows=16384, windows=[(4, 2)], ckpt=[False, True]),
+    "c4": dict(n=32, d=1280, rows=65792, windows=[(4, 2)], ckpt=[False, True]),
+}
+
+
+def roofline_ms(n, d, rows, ckpt, link, peak):
+    lb = (d * d + d) * 4           # fp32 master per layer, each direction
+    act = rows * d * 2             # bf16 saved activation per layer
+    h2d, dup = link["h2d_gbs"] * 1e9, link["duplex_gbs_per_dir"] * 1e9
+    fwd_flop, bwd_flop = 2.0 * rows * d * d / peak, 4.0 * rows * d * d / peak
+    if ckpt:  # forward: weight H2D || activation D2H; backward: weight+act H2D || weight D2H
+        fwd = max(fwd_flop, lb / dup, act / dup)
+        bwd = max(bwd_flop, (lb + act) / dup)
+    else:
+        fwd = max(fwd_flop, lb / h2d)
+        bwd = max(bwd_flop, lb / dup)
+    return 1e3 * n * (fwd + bwd)
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("configs", nargs="*", default=["c4"])
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--lr", type=float, default=0.01)
+    a = p.parse_args()
+    peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["bf16_tflops_sustained"] * 1e12
+    link = bench.measure_link(torch)
+    print(json.dumps({"link": link}), flush=True)
+    for name in a.configs:
+        c = CONFIGS[name]
+        n, d, rows = c["n"], c["d"], c["rows"]
+        weights = build_weights(n, d)
+        x = torch.from_numpy(sp.make_input(7, 0, rows, d)).cuda()
+        t = torch.from_numpy(sp.make_input(7, 1, rows, d)).cuda()
+        for k, kp in c["windows"]:
+            for ckpt in c["ckpt"]:
+                ex = sp.Executor(n, d, sp.StrategyConfig(sp.SUPERPIPELINE, k, kp),
+                                 numerics=sp.BF16, checkpointing=ckpt, trace=0)
+                for i, (W, b) in enumerate(weights):
+                    ex.register_layer(i, W, b)
+                for _ in range(3):
+                    ex.train_step_ptr(x.data_ptr(), t.data_ptr(), rows, a.lr, device=True)
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                for _ in range(a.steps):
+                    loss = ex.train_step_ptr(x.data_ptr(), t.data_ptr(), rows, a.lr, device=True)
+                e1.record()
+                torch.cuda.synchronize()
+                ms = e0.elapsed_time(e1) / a.steps
+                st = ex.stats()
+                roof = roofline_ms(n, d, rows, ckpt, link, peak)
+                print(json.dumps({
+                    "config": name, "layers": n, "d": d, "rows": rows, "k": k, "k_prime": kp,
+                    "checkpointing": ckpt, "ms_per_step": ms, "samples_per_s": rows / ms * 1e3,
+                    "roofline_ms": roof, "frac_of_roofline": roof / ms, "loss": loss,
+                    "h2d_gb": st["h2d_bytes"] / 1e9, "d2h_gb": st["d2h_bytes"] / 1e9,
+                    "ledger_peak_gb": st["peak_bytes"] / 1e9,
+                    "ledger_weights_gb": st["peak_weight_bytes"] / 1e9,
+                    "ledger_acts_gb": st["peak_activation_bytes"] / 1e9,
+                    "hbm_reserved_gb": st["hbm_reserved_bytes"] / 1e9,
+                    "graph_replays": st["graph_replays"]}), flush=True)
+                ex.close()
+
+
+if __name__ == "__main__":
+    main()
