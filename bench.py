@@ -143,13 +143,17 @@ def measure_link(torch, mb=256):
 
 def gemm_kernel_timing(torch, capi, a, reps=20):
     """Average device time per launch of the step's three tcgen05 GEMM shapes (forward
-    y = relu(xW + b), dX = (dz W^T) . [x > 0], dW with fused SGD), launched back to back on
-    the current stream between two CUDA events, with operands of the step's exact shape."""
+    y = relu(xW + b), dX = (dz W^T) . [x > 0], dW exactly as the executor runs it: SGD fused
+    into the epilogue when one split fills the SMs, else split-K fp32 partials), launched back
+    to back on the current stream between two CUDA events, with operands of the step's exact
+    shape."""
     rows, d = a.rows, a.d
     x = torch.randn(rows, d, device="cuda").to(torch.bfloat16)
     dz = torch.randn(rows, d, device="cuda").to(torch.bfloat16) * 1e-3
     W = torch.randn(d, d, device="cuda").to(torch.bfloat16)
     W32 = torch.randn(d, d, device="cuda")
+    dw_splits = int(capi.LIB.sp_debug_dw_splits(d, rows))
+    parts = torch.empty(max(dw_splits, 1) * d * d, device="cuda") if dw_splits > 1 else W32
     bias = torch.randn(d, device="cuda")
     out = torch.empty(rows, d, device="cuda", dtype=torch.bfloat16)
     st = torch.cuda.current_stream().cuda_stream
@@ -161,9 +165,10 @@ def gemm_kernel_timing(torch, capi, a, reps=20):
         "dx": (lambda: L.sp_debug_gemm_bf16_async(rows, d, d, dz.data_ptr(), d, 0, W.data_ptr(), d,
                                                   0, 2, out.data_ptr(), d, None, 1, x.data_ptr(),
                                                   d, 1, 0, 0, st), a.layers - 1),
-        "dw_sgd": (lambda: L.sp_debug_gemm_bf16_async(d, d, rows, x.data_ptr(), d, 1,
-                                                      dz.data_ptr(), d, 1, 4, W32.data_ptr(), d,
-                                                      None, 0, None, 0, 1, 0, 0, st), a.layers),
+        "dw": (lambda: L.sp_debug_gemm_bf16_async(d, d, rows, x.data_ptr(), d, 1,
+                                                  dz.data_ptr(), d, 1, 4 if dw_splits == 1 else 3,
+                                                  parts.data_ptr(), d, None, 0, None, 0,
+                                                  dw_splits, 0, 0, st), a.layers),
     }
     res = {}
     for name, (fn, per_step) in shapes.items():

@@ -34,6 +34,9 @@ int sp_debug_gemm_bf16_async(int32_t M, int32_t N, int32_t K, const void* A, int
  * img bytes over world ranks, and rank's byte range [lo, hi). */
 uint64_t sp_debug_shard_range(uint64_t img, int32_t world, int32_t rank, uint64_t* lo,
                               uint64_t* hi);
+/* Split-K count the executor's bf16 dW GEMM uses for a d x d layer at `rows` rows (1 = SGD
+ * fused into the GEMM epilogue; > 1 = fp32 partials reduced by the update op). */
+int32_t sp_debug_dw_splits(int32_t d, int64_t rows);
 /* Split count the GEMM will use for a given K and requested splits. */
 int32_t sp_debug_effective_splits(int32_t K, int32_t splits);
 

@@ -331,6 +331,12 @@ extern "C" uint64_t sp_debug_shard_range(uint64_t img, int32_t world, int32_t ra
     return shard;
 }
 
+extern "C" int32_t sp_debug_dw_splits(int32_t d, int64_t rows) {
+    if (d < 1 || rows < 1 || rows > (1ll << 31) - 1) return 0;
+    const int r = static_cast<int>(rows);
+    return sp::effective_splits(r, sp::choose_splits(d, d, r, sp::choose_block_n(d)));
+}
+
 extern "C" int32_t sp_debug_effective_splits(int32_t K, int32_t splits) {
     return sp::effective_splits(K, splits);
 }

@@ -27,17 +27,21 @@ CONFIGS = {
 }
 
 
+def link_ms(a, b, link):
+    """Time to move a bytes H2D and b bytes D2H concurrently: each direction at its simplex
+    rate, and both together at most 2 x the measured per-direction duplex rate."""
+    h2d, d2h, dup = (link[k] * 1e9 for k in ("h2d_gbs", "d2h_gbs", "duplex_gbs_per_dir"))
+    return max(a / h2d, b / d2h, (a + b) / (2 * dup))
+
+
 def roofline_ms(n, d, rows, ckpt, link, peak):
     lb = (d * d + d) * 4           # fp32 master per layer, each direction
     act = rows * d * 2             # bf16 saved activation per layer
-    h2d, dup = link["h2d_gbs"] * 1e9, link["duplex_gbs_per_dir"] * 1e9
     fwd_flop, bwd_flop = 2.0 * rows * d * d / peak, 4.0 * rows * d * d / peak
-    if ckpt:  # forward: weight H2D || activation D2H; backward: weight+act H2D || weight D2H
-        fwd = max(fwd_flop, lb / dup, act / dup)
-        bwd = max(bwd_flop, (lb + act) / dup)
-    else:
-        fwd = max(fwd_flop, lb / h2d)
-        bwd = max(bwd_flop, lb / dup)
+    # forward: weight H2D (|| activation D2H when offloading); backward: weight (+ activation)
+    # H2D || updated-weight D2H
+    fwd = max(fwd_flop, link_ms(lb, act if ckpt else 0, link))
+    bwd = max(bwd_flop, link_ms(lb + (act if ckpt else 0), lb, link))
     return 1e3 * n * (fwd + bwd)
 
 
