@@ -827,6 +827,15 @@ cudaError_t dispatch2_bn(const GemmProblem& g, cudaStream_t st) {
     return cudaErrorNotSupported;
 }
 
+// 2-CTA tiles whose per-CTA half of N is not a whole 64-column swizzle atom (N = 192 -> 96
+// per CTA) exist only for K-major B, where a CTA's B half is a plain [rows][64] TMA box.
+template <int BN>
+cudaError_t dispatch2_bn_kmajor(const GemmProblem& g, cudaStream_t st) {
+    if (!g.a_mn && !g.b_mn && g.epilogue == EPI_GATE_BF16) return launch2<BN, false, false, EPI_GATE_BF16>(g, st);
+    if (!g.a_mn && !g.b_mn && g.epilogue == EPI_F32) return launch2<BN, false, false, EPI_F32>(g, st);
+    return cudaErrorNotSupported;
+}
+
 }  // namespace tc
 
 // Kernel choice from a wave-quantised cost model: time ~ waves x per-SM tile work / per-SM
@@ -903,13 +912,14 @@ cudaError_t gemm_bf16(const GemmProblem& g, cudaStream_t st) {
         const GemmChoice c = choose_gemm(g.M, g.N, g.K, g.splits < 1 ? 1 : g.splits);
         cta = c.cta;
         if (!bn) bn = c.block_n;
-        if (cta == 2 && bn != 128 && bn != 256) cta = 1;  // a forced tile width decides
+        if (cta == 2 && bn != 128 && bn != 256 && !(bn == 192 && !g.b_mn)) cta = 1;  // a forced tile width decides
     }
     if (!bn) bn = cta == 2 ? 256 : choose_block_n(g.N);
     if (cta == 2) {
         switch (bn) {
             case 128: return tc::dispatch2_bn<128>(g, st);
             case 256: return tc::dispatch2_bn<256>(g, st);
+            case 192: return tc::dispatch2_bn_kmajor<192>(g, st);
             default: return cudaErrorInvalidValue;
         }
     }

@@ -19,6 +19,8 @@ W = torch.randn(d, d, device="cuda").to(torch.bfloat16)
 W32 = torch.randn(d, d, device="cuda")
 bias = torch.randn(d, device="cuda")
 out16 = torch.empty(rows, d, device="cuda", dtype=torch.bfloat16)
+SPLITS = int(LIB.sp_debug_dw_splits(d, rows))
+parts = torch.empty(max(SPLITS, 1) * d * d, device="cuda")
 st = torch.cuda.current_stream().cuda_stream
 
 
@@ -36,7 +38,7 @@ def timeit(fn, reps=20):
 
 
 fl = 2.0 * rows * d * d
-for cta, bn in [(1, 128), (1, 192), (1, 256), (2, 128), (2, 256), (0, 0)]:
+for cta, bn in [(1, 192), (1, 256), (2, 128), (2, 192), (2, 256), (0, 0)]:
     shapes = {
         "fwd": lambda: LIB.sp_debug_gemm_bf16_async(rows, d, d, x.data_ptr(), d, 0, W.data_ptr(), d, 1, 0,
                                                     out16.data_ptr(), d, bias.data_ptr(), 1, None, 0, 1,
@@ -47,8 +49,14 @@ for cta, bn in [(1, 128), (1, 192), (1, 256), (2, 128), (2, 256), (0, 0)]:
         "dw_sgd": lambda: LIB.sp_debug_gemm_bf16_async(d, d, rows, x.data_ptr(), d, 1, dz.data_ptr(), d, 1,
                                                        4, W32.data_ptr(), d, None, 0, None, 0, 1, bn, cta,
                                                        st),
+        # dW as the executor runs it when one split underfills the SMs: split-K fp32 partials
+        "dw_split": lambda: LIB.sp_debug_gemm_bf16_async(d, d, rows, x.data_ptr(), d, 1, dz.data_ptr(), d,
+                                                         1, 3, parts.data_ptr(), d, None, 0, None, 0,
+                                                         SPLITS, bn, cta, st),
     }
     for name, fn in shapes.items():
+        if cta == 2 and bn == 192 and name != "dx":
+            continue  # 2-CTA N=192 exists for K-major B only
         ms = timeit(fn)
         print(json.dumps({"cta": cta or "auto", "bn": bn or "auto", "gemm": name, "ms": round(ms, 4),
                           "tflops": round(fl / ms / 1e9, 1)}), flush=True)
