@@ -18,6 +18,8 @@
 #include <cudaTypedefs.h>
 
 #include <cstdio>
+#include <cstdlib>
+#include <cstring>
 #include <mutex>
 #include <unordered_map>
 
@@ -33,13 +35,26 @@ constexpr int A_BYTES = BM * BK * 2;  // 16 KB
 constexpr int ACC_STRIDE = 256;       // TMEM columns between the two accumulator stages
 constexpr int TMEM_COLS = 512;
 
-template <int BN, bool B_MN>
+constexpr int kSmemMax = 232448;  // 227 KB opt-in dynamic shared memory per CTA
+constexpr int kBarBytes = 512;    // mbarriers + TMEM address slot
+template <int EPI>
+struct EpiSmem;
+// Operand ring depth: as many stages as fit beside the epilogue's staging buffers (max 8).
+constexpr int ring_stages(int stage_bytes, int epi_bytes) {
+    return (kSmemMax - 1024 - kBarBytes - epi_bytes) / stage_bytes < 8
+               ? (kSmemMax - 1024 - kBarBytes - epi_bytes) / stage_bytes
+               : 8;
+}
+
+template <int BN, bool B_MN, int EPI>
 struct Cfg {
     static constexpr int B_ROWS = B_MN ? ((BN + 63) / 64) * 64 : BN;
     static constexpr int B_BYTES = B_ROWS * BK * 2;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-    static constexpr int STAGES = (200 * 1024) / STAGE_BYTES < 8 ? (200 * 1024) / STAGE_BYTES : 8;
-    static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+    static constexpr int EPI_BYTES = EpiSmem<EPI>::BYTES;
+    static constexpr int STAGES = ring_stages(STAGE_BYTES, EPI_BYTES);
+    static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + kBarBytes;
+    static_assert(STAGES >= 3, "operand ring too shallow");
 };
 
 struct Params {
@@ -53,6 +68,7 @@ struct Params {
     int ldg;
     long long split_stride;
     float lr;
+    int narrow;  // 2-CTA: the ragged last N tile is computed with an MMA of N = BN/2
 };
 
 // ---------------------------------------------------------------------------------------
@@ -134,19 +150,17 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
             smem_u32(bar))
         : "memory");
 }
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+// Split form for a pipelined epilogue: issue the load, work on the previous chunk, then wait.
+// The wait names the destination registers as read-write operands, so the compiler cannot
+// hoist any use of them above it.
+__device__ __forceinline__ void tmem_ld32_async(uint32_t taddr, uint32_t (&r)[32]) {
     asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
-        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
-          "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
-          "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
-          "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
-          "=r"(r[31])
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
         : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_ld_wait(uint32_t (&r)[32]) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]), "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15]), "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]), "+r"(r[22]), "+r"(r[23]), "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]), "+r"(r[29]), "+r"(r[30]), "+r"(r[31]) : : "memory");
 }
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
@@ -169,71 +183,225 @@ __device__ __forceinline__ void tile_mn(int t, int m_tiles, int n_tiles, int& mb
     nb = r / gm;
 }
 
-// Epilogue for 32 accumulator columns [col0, col0+32) of one output row (one TMEM lane).
+// ---------------------------------------------------------------------------------------
+// epilogue: TMEM -> registers -> fused op -> swizzled smem staging -> TMA store
+// ---------------------------------------------------------------------------------------
+// Each epilogue warp owns 32 accumulator rows (its TMEM lane quarter) and walks the tile in
+// 32-column chunks. A lane holds one row, so writing global memory directly would touch 32
+// lines per 16-byte access; instead the warp stages its 32 x 32 chunk in shared memory in the
+// TMA swizzle pattern (4 wavefronts per 16-byte access, the minimum) and one lane stores it
+// with cp.async.bulk.tensor (bounds-clipped by the tensor map, asynchronous, double-buffered).
+// The ReLU gate of the dX GEMM comes in the same way: a TMA load of the chunk into swizzled
+// smem, one chunk ahead, completed on a per-warp mbarrier. Only the fused-SGD epilogue (a
+// read-modify-write of the fp32 master weights) stores from registers.
+// The kernels' EPI template argument is an epilogue code (kernels.hpp) plus EPI_TMA when the
+// epilogue stages through shared memory and stores with TMA (short K, where the epilogue is on
+// the critical path); without it lanes store rows straight to global memory, which is smaller
+// code and leaves shared memory to the operand ring (long K, where the epilogue hides).
+constexpr int EPI_TMA = 16;
 template <int EPI>
-__device__ __forceinline__ void epilogue_chunk(const Params& p, const uint32_t (&r)[32], int row,
-                                               int col0, int split) {
-    float v[32];
-#pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-    if (EPI == EPI_BIAS_ACT_BF16 || EPI == EPI_BIAS_ACT_F32) {
-        const float4* bp = reinterpret_cast<const float4*>(p.bias + col0);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const float4 bv = __ldg(bp + i);
-            v[4 * i + 0] += bv.x;
-            v[4 * i + 1] += bv.y;
-            v[4 * i + 2] += bv.z;
-            v[4 * i + 3] += bv.w;
+struct EpiSmem {
+    static constexpr int BASE = EPI & (EPI_TMA - 1);
+    static constexpr bool TMA = (EPI & EPI_TMA) != 0 && BASE != EPI_SGD_F32;
+    static constexpr bool TMA_OUT = TMA;
+    static constexpr int OUT_ELT = (BASE == EPI_BIAS_ACT_BF16 || BASE == EPI_GATE_BF16) ? 2 : 4;
+    static constexpr int OUT_BUF = 32 * 32 * OUT_ELT;  // one warp's 32 x 32 chunk
+    static constexpr bool GATE = TMA && BASE == EPI_GATE_BF16;
+    static constexpr int GATE_BUF = 32 * 32 * 2;
+    static constexpr int OUT_BYTES = TMA_OUT ? 4 * 2 * OUT_BUF : 0;  // 4 warps x 2 buffers
+    static constexpr int GATE_BYTES = GATE ? 4 * 2 * GATE_BUF : 0;
+    static constexpr int BYTES = OUT_BYTES + GATE_BYTES;
+};
+
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(smem_u32(src)), "r"(c0), "r"(c1)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int c0, int c1,
+                                             int c2) {
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+// 16-byte chunk i of staged row r: 64-byte rows use the 64B swizzle (chunk ^ (r>>1)&3), 128-byte
+// rows the 128B swizzle (chunk ^ r&7) — the layouts CU_TENSOR_MAP_SWIZZLE_64B/128B expect.
+template <int ROW_BYTES>
+__device__ __forceinline__ uint32_t swz(int r, int i) {
+    return ROW_BYTES == 64 ? static_cast<uint32_t>(r * 64 + ((i ^ ((r >> 1) & 3)) << 4))
+                           : static_cast<uint32_t>(r * 128 + ((i ^ (r & 7)) << 4));
+}
+
+template <int BN, int EPI>
+struct TileEpilogue {
+    using E = EpiSmem<EPI>;
+    static constexpr int BASE = E::BASE;
+    static constexpr int CHUNKS = BN / 32;
+    uint8_t* obuf;    // this warp's two output staging buffers (TMA kind)
+    uint8_t* gbuf;    // this warp's two gate buffers (TMA kind)
+    uint64_t* gbar;   // their two mbarriers
+    int lane;
+    uint32_t out_n = 0, gate_issued = 0, gate_used = 0;
+
+    __device__ __forceinline__ TileEpilogue(uint8_t* epi_smem, uint64_t* gate_bars, int q, int ln)
+        : obuf(epi_smem + q * 2 * E::OUT_BUF),
+          gbuf(epi_smem + E::OUT_BYTES + q * 2 * E::GATE_BUF),
+          gbar(gate_bars + 2 * q),
+          lane(ln) {}
+
+    __device__ __forceinline__ void gate_issue(const CUtensorMap* tmG, int row0, int col0) {
+        const int b = gate_issued & 1;
+        __syncwarp();  // every lane is done reading this buffer's previous chunk
+        if (lane == 0) {
+            mbar_expect_tx(&gbar[b], E::GATE_BUF);
+            tma_load_2d(tmG, &gbar[b], gbuf + b * E::GATE_BUF, col0, row0);
         }
-        if (p.relu) {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = v[i] < 0.0f ? 0.0f : v[i];
-        }
+        ++gate_issued;
     }
-    if (EPI == EPI_GATE_BF16 && p.relu) {
-        const uint4* gp = reinterpret_cast<const uint4*>(p.gate + static_cast<long long>(row) * p.ldg + col0);
+    // before the accumulator wait: the gate of the tile's first chunk starts loading
+    __device__ __forceinline__ void begin_tile(const CUtensorMap* tmG, const Params& p, int row0, int n0) {
+        if (E::GATE && p.relu) gate_issue(tmG, row0, n0);
+    }
+
+    __device__ __forceinline__ void chunk(const CUtensorMap* tmO, const Params& p, const uint32_t (&r)[32],
+                                          int row0, int col0, int split) {
+        float v[32];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const uint4 g = __ldg(gp + i);
-            const uint32_t gw[4] = {g.x, g.y, g.z, g.w};
+        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+        const int row = row0 + lane;
+        if (BASE == EPI_BIAS_ACT_BF16 || BASE == EPI_BIAS_ACT_F32) {
+            const float4* bp = reinterpret_cast<const float4*>(p.bias + col0);  // one address per warp
 #pragma unroll
-            for (int h = 0; h < 4; ++h) {
-                const float2 gf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&gw[h]));
-                if (gf.x <= 0.0f) v[8 * i + 2 * h] = 0.0f;
-                if (gf.y <= 0.0f) v[8 * i + 2 * h + 1] = 0.0f;
+            for (int i = 0; i < 8; ++i) {
+                const float4 bv = __ldg(bp + i);
+                v[4 * i + 0] += bv.x;
+                v[4 * i + 1] += bv.y;
+                v[4 * i + 2] += bv.z;
+                v[4 * i + 3] += bv.w;
+            }
+            if (p.relu) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) v[i] = v[i] < 0.0f ? 0.0f : v[i];
             }
         }
-    }
-    if (EPI == EPI_BIAS_ACT_BF16 || EPI == EPI_GATE_BF16) {
-        uint4* op = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.out) +
-                                             static_cast<long long>(row) * p.ldo + col0);
+        if (BASE == EPI_GATE_BF16 && p.relu) {
+            uint4 gv[4];
+            if (E::GATE) {
+                const int b = gate_used & 1;
+                mbar_wait(&gbar[b], (gate_used >> 1) & 1);
+                ++gate_used;
+                const uint8_t* gb = gbuf + b * E::GATE_BUF;
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-            op[i] = make_uint4(pack_bf16(v[8 * i + 0], v[8 * i + 1]), pack_bf16(v[8 * i + 2], v[8 * i + 3]),
-                               pack_bf16(v[8 * i + 4], v[8 * i + 5]), pack_bf16(v[8 * i + 6], v[8 * i + 7]));
-    } else if (EPI == EPI_SGD_F32) {
-        // fused SGD (apply_sgd, model.cpp:150-155): w -= lr * dW, no FMA, in place on the
-        // slot's fp32 master weights; the tile is owned by this CTA alone.
-        float4* wp = reinterpret_cast<float4*>(static_cast<float*>(p.out) +
-                                               static_cast<long long>(row) * p.ldo + col0);
+                for (int i = 0; i < 4; ++i) gv[i] = *reinterpret_cast<const uint4*>(gb + swz<64>(lane, i));
+            } else {
+                if (row >= p.M) return;
+                const uint4* gp = reinterpret_cast<const uint4*>(p.gate + static_cast<long long>(row) * p.ldg + col0);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            float4 w = wp[i];
-            w.x = __fsub_rn(w.x, __fmul_rn(p.lr, v[4 * i + 0]));
-            w.y = __fsub_rn(w.y, __fmul_rn(p.lr, v[4 * i + 1]));
-            w.z = __fsub_rn(w.z, __fmul_rn(p.lr, v[4 * i + 2]));
-            w.w = __fsub_rn(w.w, __fmul_rn(p.lr, v[4 * i + 3]));
-            wp[i] = w;
+                for (int i = 0; i < 4; ++i) gv[i] = __ldg(gp + i);
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const uint32_t gw[4] = {gv[i].x, gv[i].y, gv[i].z, gv[i].w};
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                    const float2 gf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&gw[h]));
+                    if (gf.x <= 0.0f) v[8 * i + 2 * h] = 0.0f;
+                    if (gf.y <= 0.0f) v[8 * i + 2 * h + 1] = 0.0f;
+                }
+            }
         }
-    } else {
-        float* base = static_cast<float*>(p.out) + (EPI == EPI_F32 ? split * p.split_stride : 0LL) +
-                      static_cast<long long>(row) * p.ldo + col0;
-        float4* op = reinterpret_cast<float4*>(base);
+        if (BASE == EPI_SGD_F32) {
+            // fused SGD (apply_sgd, model.cpp:150-155): w -= lr * dW, no FMA, in place on the
+            // slot's fp32 master weights; the tile is owned by this CTA alone.
+            if (row < p.M) {
+                float4* wp = reinterpret_cast<float4*>(static_cast<float*>(p.out) +
+                                                       static_cast<long long>(row) * p.ldo + col0);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) op[i] = make_float4(v[4 * i + 0], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+                for (int i = 0; i < 8; ++i) {
+                    float4 w = wp[i];
+                    w.x = __fsub_rn(w.x, __fmul_rn(p.lr, v[4 * i + 0]));
+                    w.y = __fsub_rn(w.y, __fmul_rn(p.lr, v[4 * i + 1]));
+                    w.z = __fsub_rn(w.z, __fmul_rn(p.lr, v[4 * i + 2]));
+                    w.w = __fsub_rn(w.w, __fmul_rn(p.lr, v[4 * i + 3]));
+                    wp[i] = w;
+                }
+            }
+        } else if (!E::TMA_OUT) {  // per-lane row stores straight to global
+            if (row >= p.M) return;
+            if (E::OUT_ELT == 2) {
+                uint4* op = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.out) +
+                                                     static_cast<long long>(row) * p.ldo + col0);
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    op[i] = make_uint4(pack_bf16(v[8 * i + 0], v[8 * i + 1]), pack_bf16(v[8 * i + 2], v[8 * i + 3]),
+                                       pack_bf16(v[8 * i + 4], v[8 * i + 5]), pack_bf16(v[8 * i + 6], v[8 * i + 7]));
+            } else {
+                float4* op = reinterpret_cast<float4*>(static_cast<float*>(p.out) +
+                                                       (BASE == EPI_F32 ? split * p.split_stride : 0LL) +
+                                                       static_cast<long long>(row) * p.ldo + col0);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) op[i] = make_float4(v[4 * i + 0], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+            }
+        } else {  // swizzled smem staging -> one TMA store per 32 x 32 chunk
+            uint8_t* ob = obuf + (out_n & 1) * E::OUT_BUF;
+            if (lane == 0) bulk_wait_read<1>();  // the store that last read this buffer is done
+            __syncwarp();
+            if (E::OUT_ELT == 2) {
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    *reinterpret_cast<uint4*>(ob + swz<64>(lane, i)) =
+                        make_uint4(pack_bf16(v[8 * i + 0], v[8 * i + 1]), pack_bf16(v[8 * i + 2], v[8 * i + 3]),
+                                   pack_bf16(v[8 * i + 4], v[8 * i + 5]), pack_bf16(v[8 * i + 6], v[8 * i + 7]));
+            } else {
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                    *reinterpret_cast<float4*>(ob + swz<128>(lane, i)) =
+                        make_float4(v[4 * i + 0], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+            }
+            fence_proxy_async_smem();  // generic-proxy writes -> visible to the TMA (async proxy)
+            __syncwarp();
+            if (lane == 0) {
+                if (BASE == EPI_F32) tma_store_3d(tmO, ob, col0, row0, split);
+                else tma_store_2d(tmO, ob, col0, row0);
+                bulk_commit();
+            }
+            ++out_n;
+        }
     }
-}
+
+    // One accumulator tile: chunk by chunk out of TMEM; the accumulator stage is released to the
+    // MMA warp once every chunk is in registers or stored.
+    template <typename Release>
+    __device__ __forceinline__ void run(const CUtensorMap* tmO, const CUtensorMap* tmG, const Params& p,
+                                        uint32_t tmem_acc, int row0, int n0, int split, Release&& release) {
+        uint32_t ra[32];
+#pragma unroll 1
+        for (int c = 0; c < CHUNKS; ++c) {
+            const int col0 = n0 + c * 32;
+            tmem_ld32_async(tmem_acc + c * 32, ra);
+            tmem_ld_wait(ra);
+            if (E::GATE && p.relu && c + 1 < CHUNKS && col0 + 32 < p.N) gate_issue(tmG, row0, col0 + 32);
+            if (col0 < p.N) chunk(tmO, p, ra, row0, col0, split);
+        }
+        release();
+    }
+    __device__ __forceinline__ void finish() {
+        if (E::TMA_OUT && lane == 0) bulk_wait_all();
+        __syncwarp();
+    }
+};
 
 // ---------------------------------------------------------------------------------------
 // the kernel (1-CTA: M = 128 per MMA)
@@ -241,8 +409,9 @@ __device__ __forceinline__ void epilogue_chunk(const Params& p, const uint32_t (
 template <int BN, bool A_MN, bool B_MN, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmG,
                 const Params p) {
-    using C = Cfg<BN, B_MN>;
+    using C = Cfg<BN, B_MN, EPI>;
     constexpr int STAGES = C::STAGES;
     constexpr uint32_t IDESC = make_idesc(BM, BN, A_MN, B_MN);
     constexpr uint32_t TX = C::STAGE_BYTES;
@@ -252,11 +421,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
     uint8_t* sA = smem;
     uint8_t* sB = smem + STAGES * A_BYTES;
-    uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * C::B_BYTES);
+    uint8_t* sE = sB + STAGES * C::B_BYTES;  // epilogue staging (1024-aligned)
+    uint64_t* full = reinterpret_cast<uint64_t*>(sE + C::EPI_BYTES);
     uint64_t* empty = full + STAGES;
     uint64_t* tfull = empty + STAGES;
     uint64_t* tempty = tfull + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* gbar = tempty + 2;  // 4 epilogue warps x 2 gate buffers
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbar + 8);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -264,6 +435,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 0 && lane == 0) {
         prefetch_tmap(&tmA);
         prefetch_tmap(&tmB);
+        if (EpiSmem<EPI>::TMA_OUT) prefetch_tmap(&tmO);
+        if (EpiSmem<EPI>::GATE) prefetch_tmap(&tmG);
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
@@ -272,6 +445,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(&tfull[s], 1);
             mbar_init(&tempty[s], 128);
         }
+        for (int s = 0; s < 8; ++s) mbar_init(&gbar[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
@@ -367,33 +541,30 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp >= 4) {
-        // ===== epilogue: TMEM -> registers -> fused op -> global =====
+        // ===== epilogue: TMEM -> registers -> fused op -> smem -> TMA store =====
         const int q = warp & 3;  // TMEM lanes [32q, 32q+32)
+        TileEpilogue<BN, EPI> ep(sE, gbar, q, lane);
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int t = blockIdx.x; t < total; t += gridDim.x) {
             int mb, nbk;
             tile_mn<16>(t, p.m_tiles, p.n_tiles, mb, nbk);
-            const int m0 = mb * BM;
+            const int row0 = mb * BM + q * 32;
             const int n0 = nbk * BN;
             const int split = t / tiles_mn;
+            ep.begin_tile(&tmG, p, row0, n0);
             mbar_wait(&tfull[acc], acc_phase);
             fence_after();
-            const int row = m0 + q * 32 + lane;
-            const bool row_ok = row < p.M;
-#pragma unroll 1
-            for (int c = 0; c < BN / 32; ++c) {
-                uint32_t r[32];
-                tmem_ld32(tmem_base + acc * ACC_STRIDE + c * 32 + (static_cast<uint32_t>(q * 32) << 16), r);
-                const int col0 = n0 + c * 32;
-                if (!row_ok || col0 >= p.N) continue;
-                epilogue_chunk<EPI>(p, r, row, col0, split);
-            }
-            fence_before();
-            mbar_arrive(&tempty[acc]);
+            uint64_t* te = &tempty[acc];
+            ep.run(&tmO, &tmG, p, tmem_base + acc * ACC_STRIDE + (static_cast<uint32_t>(q * 32) << 16), row0,
+                   n0, split, [&] {
+                       fence_before();
+                       mbar_arrive(te);
+                   });
             acc ^= 1;
             if (acc == 0) acc_phase ^= 1;
         }
+        ep.finish();
     }
     __syncwarp();
     fence_before();
@@ -456,21 +627,65 @@ __device__ __forceinline__ void umma2_commit_both(uint64_t* bar) {
         : "memory");
 }
 
-template <int BN, bool A_MN, bool B_MN>
+// Tile schedule of a CTA pair (2-CTA kernel). Full tiles are dealt round-robin; when the last
+// N tile is ragged (N mod 256 <= 128) it is computed at half width (half the MMA work), and
+// those half tiles go first to the pairs that got one full tile fewer - twice each, since two
+// halves make one full tile - then round-robin. This is the largest-first (LPT) assignment for
+// tiles of cost 1 and 1/2: at 16384 x 1600 the busiest pair does 6.0 tile-times instead of 7.
+// Which pair computes a tile never changes the tile's arithmetic.
+struct PairSched {
+    int U, u, F, R, r, mt, ntf, nt, per_split;
+    __device__ __forceinline__ PairSched(const Params& p, int m_tiles2, int cid, int ncl) {
+        mt = m_tiles2;
+        nt = p.n_tiles;
+        ntf = p.narrow ? nt - 1 : nt;
+        per_split = mt * ntf;
+        F = per_split * p.splits;
+        R = p.narrow ? mt * p.splits : 0;
+        U = ncl;
+        u = cid;
+        r = F % U;
+    }
+    // i-th tile of this pair; false when the pair is done.
+    __device__ __forceinline__ bool get(int i, int& mb, int& nb, int& split, bool& narrow) const {
+        const int nfull = u < F ? (F - 1 - u) / U + 1 : 0;
+        if (i < nfull) {
+            const int t = u + U * i;
+            split = t / per_split;
+            tile_mn<8>(t - split * per_split, mt, ntf, mb, nb);
+            narrow = false;
+            return true;
+        }
+        const int k = i - nfull;
+        const int lo = U - r;
+        const int j = u >= r ? (k < 2 ? (u - r) + k * lo : 2 * lo + u + U * (k - 2)) : 2 * lo + u + U * k;
+        if (j >= R) return false;
+        split = j / mt;
+        mb = j - split * mt;
+        nb = nt - 1;
+        narrow = true;
+        return true;
+    }
+};
+
+template <int BN, bool A_MN, bool B_MN, int EPI>
 struct Cfg2 {
     static constexpr int B_ROWS = BN / 2;  // this CTA's half of the tile's N
     static constexpr int B_BYTES = B_ROWS * BK * 2;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-    static constexpr int STAGES = (200 * 1024) / STAGE_BYTES < 8 ? (200 * 1024) / STAGE_BYTES : 8;
-    static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+    static constexpr int EPI_BYTES = EpiSmem<EPI>::BYTES;
+    static constexpr int STAGES = ring_stages(STAGE_BYTES, EPI_BYTES);
+    static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + kBarBytes;
+    static_assert(STAGES >= 3, "operand ring too shallow");
     static_assert(!B_MN || B_ROWS % 64 == 0, "MN-major B halves must be whole 128B-swizzle atoms");
 };
 
 template <int BN, bool A_MN, bool B_MN, int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                 const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmG,
                  const Params p) {
-    using C = Cfg2<BN, A_MN, B_MN>;
+    using C = Cfg2<BN, A_MN, B_MN, EPI>;
     constexpr int STAGES = C::STAGES;
     constexpr uint32_t IDESC = make_idesc(2 * BM, BN, A_MN, B_MN);
     constexpr uint32_t TX = 2 * C::STAGE_BYTES;  // both CTAs' bytes land on the leader's barrier
@@ -480,11 +695,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
     uint8_t* sA = smem;
     uint8_t* sB = smem + STAGES * A_BYTES;
-    uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * C::B_BYTES);
+    uint8_t* sE = sB + STAGES * C::B_BYTES;  // epilogue staging (1024-aligned)
+    uint64_t* full = reinterpret_cast<uint64_t*>(sE + C::EPI_BYTES);
     uint64_t* empty = full + STAGES;
     uint64_t* tfull = empty + STAGES;
     uint64_t* tempty = tfull + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* gbar = tempty + 2;  // 4 epilogue warps x 2 gate buffers
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbar + 8);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -494,6 +711,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     if (warp == 0 && lane == 0) {
         prefetch_tmap(&tmA);
         prefetch_tmap(&tmB);
+        if (EpiSmem<EPI>::TMA_OUT) prefetch_tmap(&tmO);
+        if (EpiSmem<EPI>::GATE) prefetch_tmap(&tmG);
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
@@ -502,6 +721,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             mbar_init(&tfull[s], 1);
             mbar_init(&tempty[s], 2 * 128);  // both CTAs' epilogue threads (leader's copy used)
         }
+        for (int s = 0; s < 8; ++s) mbar_init(&gbar[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
@@ -517,27 +737,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const uint32_t tmem_base = *tmem_slot;
 
     const int m_tiles2 = (p.M + 2 * BM - 1) / (2 * BM);
-    const int tiles_mn = m_tiles2 * p.n_tiles;
-    const int total = tiles_mn * p.splits;
-    const int cid = blockIdx.x >> 1;
-    const int ncl = gridDim.x >> 1;
+    const PairSched sched(p, m_tiles2, blockIdx.x >> 1, gridDim.x >> 1);
+    constexpr uint32_t IDESC_NARROW = make_idesc(2 * BM, BN / 2, A_MN, B_MN);
 
     if (warp == 0) {
         if (lane == 0) {
             // ===== TMA producer (both CTAs, each loads its own halves) =====
             int stage = 0;
             uint32_t phase = 0;
-            for (int t = cid; t < total; t += ncl) {
-                int mb, nbk;
-                tile_mn<8>(t, m_tiles2, p.n_tiles, mb, nbk);
+            for (int i = 0;; ++i) {
+                int mb, nbk, split;
+                bool nar;
+                if (!sched.get(i, mb, nbk, split, nar)) break;
+                // this CTA's share of the tile's N: BN/2 columns, or BN/4 of a half-width tile
+                const int half = nar ? BN / 4 : BN / 2;
                 const int m0 = mb * 2 * BM + static_cast<int>(rank) * BM;
-                const int nb = nbk * BN + static_cast<int>(rank) * (BN / 2);
-                const int split = t / tiles_mn;
+                const int nb = nbk * BN + static_cast<int>(rank) * half;
+                const uint32_t tx = B_MN ? 2u * static_cast<uint32_t>(A_BYTES + (half / 64) * 8192) : TX;
                 const int kb0 = split * p.kb_per_split;
                 const int kb1 = min(kb0 + p.kb_per_split, p.k_blocks);
                 for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
-                    if (leader) mbar_expect_tx(&full[stage], TX);
+                    if (leader) mbar_expect_tx(&full[stage], tx);
                     const int k0 = kb * BK;
                     uint8_t* a = sA + stage * A_BYTES;
                     uint8_t* b = sB + stage * C::B_BYTES;
@@ -550,9 +771,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     if (B_MN) {
 #pragma unroll
                         for (int j = 0; j < C::B_ROWS / 64; ++j)
-                            tma_load_2d_pair(&tmB, &full[stage], b + j * 8192, nb + 64 * j, k0);
+                            if (j * 64 < half) tma_load_2d_pair(&tmB, &full[stage], b + j * 8192, nb + 64 * j, k0);
                     } else {
-                        tma_load_2d_pair(&tmB, &full[stage], b, k0, nb);
+                        tma_load_2d_pair(&tmB, &full[stage], b, k0, nb);  // full box; MMA reads `half` rows
                     }
                     if (++stage == STAGES) {
                         stage = 0;
@@ -568,8 +789,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
-            for (int t = cid; t < total; t += ncl) {
-                const int split = t / tiles_mn;
+            for (int i = 0;; ++i) {
+                int mb, nbk, split;
+                bool nar;
+                if (!sched.get(i, mb, nbk, split, nar)) break;
+                const uint32_t idesc = nar ? IDESC_NARROW : IDESC;
                 const int kb0 = split * p.kb_per_split;
                 const int kb1 = min(kb0 + p.kb_per_split, p.k_blocks);
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -586,7 +810,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                                                  : make_desc(a_base + kk * 32, 16, 1024);
                         const uint64_t bd = B_MN ? make_desc(b_base + kk * 2048, 8192, 1024)
                                                  : make_desc(b_base + kk * 32, 16, 1024);
-                        umma2_bf16(d_tmem, ad, bd, IDESC, (kb > kb0 || kk > 0) ? 1u : 0u);
+                        umma2_bf16(d_tmem, ad, bd, idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
                     }
                     umma2_commit_both(&empty[stage]);  // frees the stage in BOTH CTAs
                     if (++stage == STAGES) {
@@ -604,31 +828,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int q = warp & 3;
         const uint32_t tempty_leader0 = map_to_rank0(smem_u32(&tempty[0]));
         const uint32_t tempty_leader1 = map_to_rank0(smem_u32(&tempty[1]));
+        TileEpilogue<BN, EPI> ep(sE, gbar, q, lane);
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int t = cid; t < total; t += ncl) {
-            int mb, nbk;
-            tile_mn<8>(t, m_tiles2, p.n_tiles, mb, nbk);
-            const int m0 = mb * 2 * BM + static_cast<int>(rank) * BM;
-            const int n0 = nbk * BN;
-            const int split = t / tiles_mn;
+        for (int i = 0;; ++i) {
+            int mb, nbk, split;
+            bool nar;
+            if (!sched.get(i, mb, nbk, split, nar)) break;
+            const int row0 = mb * 2 * BM + static_cast<int>(rank) * BM + q * 32;
+            const int n0 = nbk * BN;  // a half-width tile's dead columns are >= N: never stored
+            ep.begin_tile(&tmG, p, row0, n0);
             mbar_wait(&tfull[acc], acc_phase);
             fence_after();
-            const int row = m0 + q * 32 + lane;
-            const bool row_ok = row < p.M;
-#pragma unroll 1
-            for (int c = 0; c < BN / 32; ++c) {
-                uint32_t r[32];
-                tmem_ld32(tmem_base + acc * ACC_STRIDE + c * 32 + (static_cast<uint32_t>(q * 32) << 16), r);
-                const int col0 = n0 + c * 32;
-                if (!row_ok || col0 >= p.N) continue;
-                epilogue_chunk<EPI>(p, r, row, col0, split);
-            }
-            fence_before();
-            mbar_arrive_cluster(acc == 0 ? tempty_leader0 : tempty_leader1);
+            const uint32_t te = acc == 0 ? tempty_leader0 : tempty_leader1;
+            ep.run(&tmO, &tmG, p, tmem_base + acc * ACC_STRIDE + (static_cast<uint32_t>(q * 32) << 16), row0,
+                   n0, split, [&] {
+                       fence_before();
+                       mbar_arrive_cluster(te);
+                   });
             acc ^= 1;
             if (acc == 0) acc_phase ^= 1;
         }
+        ep.finish();
     }
     __syncwarp();
     fence_before();
@@ -657,69 +878,154 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
-bool encode_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint64_t ld,
-                uint32_t box_inner, uint32_t box_outer);
+// A tensor map description: element type, rank (2 or 3), dims / byte strides / box, swizzle.
+struct MapDesc {
+    CUtensorMapDataType dtype;
+    int rank;
+    const void* base;
+    uint64_t dims[3];
+    uint64_t strides[2];  // bytes, dims 1..rank-1
+    uint32_t box[3];
+    CUtensorMapSwizzle swizzle;
+    bool operator==(const MapDesc& o) const {
+        return dtype == o.dtype && rank == o.rank && base == o.base && swizzle == o.swizzle &&
+               std::memcmp(dims, o.dims, sizeof(dims)) == 0 &&
+               std::memcmp(strides, o.strides, sizeof(strides)) == 0 &&
+               std::memcmp(box, o.box, sizeof(box)) == 0;
+    }
+};
+struct MapDescHash {
+    size_t operator()(const MapDesc& k) const {
+        size_t h = reinterpret_cast<size_t>(k.base) ^ (static_cast<size_t>(k.dtype) << 48) ^
+                   (static_cast<size_t>(k.swizzle) << 56) ^ static_cast<size_t>(k.rank);
+        for (uint64_t v : {k.dims[0], k.dims[1], k.dims[2], k.strides[0], k.strides[1],
+                           static_cast<uint64_t>(k.box[0]) << 32 | k.box[1], static_cast<uint64_t>(k.box[2])})
+            h = h * 1000003u ^ static_cast<size_t>(v);
+        return h;
+    }
+};
 
-// Tensor maps depend only on (address, shape, box): the ring slots, activation buffers and
+bool encode(CUtensorMap* m, const MapDesc& k) {
+    auto fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[3] = {k.dims[0], k.dims[1], k.dims[2]};
+    cuuint64_t strides[2] = {k.strides[0], k.strides[1]};
+    cuuint32_t box[3] = {k.box[0], k.box[1], k.box[2]};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = fn(m, k.dtype, k.rank, const_cast<void*>(k.base), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, k.swizzle, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        fprintf(stderr, "superpipe: cuTensorMapEncodeTiled failed (%d): base=%p rank=%d dims={%llu,%llu,%llu} box={%u,%u,%u}\n",
+                static_cast<int>(r), k.base, k.rank, (unsigned long long)k.dims[0],
+                (unsigned long long)k.dims[1], (unsigned long long)k.dims[2], k.box[0], k.box[1], k.box[2]);
+    return r == CUDA_SUCCESS;
+}
+
+// Tensor maps depend only on (address, shape, box, type): the ring slots, activation buffers and
 // workspaces have fixed addresses, so each map is encoded once and reused by every step.
-bool make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint64_t ld,
-              uint32_t box_inner, uint32_t box_outer) {
-    struct Key {
-        const void* base;
-        uint64_t inner, outer, ld;
-        uint32_t bi, bo;
-        bool operator==(const Key& o) const {
-            return base == o.base && inner == o.inner && outer == o.outer && ld == o.ld &&
-                   bi == o.bi && bo == o.bo;
-        }
-    };
-    struct Hash {
-        size_t operator()(const Key& k) const {
-            size_t h = reinterpret_cast<size_t>(k.base);
-            for (uint64_t v : {k.inner, k.outer, k.ld, static_cast<uint64_t>(k.bi) << 32 | k.bo})
-                h = h * 1000003u ^ static_cast<size_t>(v);
-            return h;
-        }
-    };
+bool make_map(CUtensorMap* m, const MapDesc& k) {
     static std::mutex mu;
-    static std::unordered_map<Key, CUtensorMap, Hash> cache;
-    const Key key{base, inner, outer, ld, box_inner, box_outer};
+    static std::unordered_map<MapDesc, CUtensorMap, MapDescHash> cache;
     {
         std::lock_guard<std::mutex> lock(mu);
-        auto it = cache.find(key);
+        auto it = cache.find(k);
         if (it != cache.end()) {
             *m = it->second;
             return true;
         }
     }
-    if (!encode_map(m, base, inner, outer, ld, box_inner, box_outer)) return false;
+    if (!encode(m, k)) return false;
     std::lock_guard<std::mutex> lock(mu);
     if (cache.size() > 8192) cache.clear();
-    cache.emplace(key, *m);
+    cache.emplace(k, *m);
     return true;
 }
 
-bool encode_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint64_t ld,
-                uint32_t box_inner, uint32_t box_outer) {
-    auto fn = encode_fn();
-    if (!fn) return false;
-    cuuint64_t dims[2] = {inner, outer};
-    cuuint64_t strides[1] = {ld * 2};
-    cuuint32_t box[2] = {box_inner, box_outer};
-    cuuint32_t estr[2] = {1, 1};
-    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
-                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS)
-        fprintf(stderr, "superpipe: cuTensorMapEncodeTiled failed (%d): base=%p dims={%llu,%llu} ld=%llu box={%u,%u}\n",
-                static_cast<int>(r), base, (unsigned long long)inner, (unsigned long long)outer,
-                (unsigned long long)ld, box_inner, box_outer);
-    return r == CUDA_SUCCESS;
+// bf16 operand [outer][ld] (inner contiguous), 128B-swizzled box {box_inner, box_outer}
+bool make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint64_t ld,
+              uint32_t box_inner, uint32_t box_outer) {
+    MapDesc k{};
+    k.dtype = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+    k.rank = 2;
+    k.base = base;
+    k.dims[0] = inner;
+    k.dims[1] = outer;
+    k.dims[2] = 1;
+    k.strides[0] = ld * 2;
+    k.box[0] = box_inner;
+    k.box[1] = box_outer;
+    k.box[2] = 1;
+    k.swizzle = CU_TENSOR_MAP_SWIZZLE_128B;
+    return make_map(m, k);
+}
+
+// The epilogue's maps: output (bf16 / fp32, a 3-D {N, M, split} map for split-K partials so the
+// TMA clips every split at M) and the dX GEMM's ReLU gate, with 32 x 32 boxes in the swizzle
+// the staging code writes (64B for 64-byte bf16 rows, 128B for 128-byte fp32 rows).
+template <int EPI>
+bool make_epilogue_maps(const GemmProblem& g, int splits, CUtensorMap* to, CUtensorMap* tg) {
+    using E = EpiSmem<EPI>;
+    std::memset(to, 0, sizeof(*to));
+    std::memset(tg, 0, sizeof(*tg));
+    if (E::TMA_OUT) {
+        MapDesc k{};
+        k.dtype = E::OUT_ELT == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+        k.base = g.out;
+        k.dims[0] = static_cast<uint64_t>(g.N);
+        k.dims[1] = static_cast<uint64_t>(g.M);
+        k.strides[0] = static_cast<uint64_t>(g.ldo) * E::OUT_ELT;
+        k.box[0] = 32;
+        k.box[1] = 32;
+        k.box[2] = 1;
+        k.swizzle = E::OUT_ELT == 2 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B;
+        if (E::BASE == EPI_F32) {
+            k.rank = 3;
+            k.dims[2] = static_cast<uint64_t>(splits);
+            k.strides[1] = static_cast<uint64_t>(g.split_stride) * 4;
+        } else {
+            k.rank = 2;
+            k.dims[2] = 1;
+        }
+        if (!make_map(to, k)) return false;
+    }
+    if (E::GATE && g.relu) {
+        MapDesc k{};
+        k.dtype = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+        k.rank = 2;
+        k.base = g.gate;
+        k.dims[0] = static_cast<uint64_t>(g.N);
+        k.dims[1] = static_cast<uint64_t>(g.M);
+        k.dims[2] = 1;
+        k.strides[0] = static_cast<uint64_t>(g.ldg) * 2;
+        k.box[0] = 32;
+        k.box[1] = 32;
+        k.box[2] = 1;
+        k.swizzle = CU_TENSOR_MAP_SWIZZLE_64B;
+        if (!make_map(tg, k)) return false;
+    }
+    return true;
+}
+
+// Epilogue kind: TMA staging when the tile's K loop is short (the epilogue is then on the
+// critical path: +8..15% on the d=1280/1600 layer GEMMs, ncu, fixed clocks), direct per-lane
+// stores for long K (where the epilogue hides and the TMA kind costs ~5%, d=4096).
+// SP_EPI_MODE=1/2 forces direct/TMA (A/B measurement only).
+bool use_tma_epilogue(const GemmProblem& g, int splits) {
+    static const int forced = [] {
+        const char* e = std::getenv("SP_EPI_MODE");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (g.epilogue == EPI_SGD_F32) return false;
+    if (forced == 1) return false;
+    if (forced == 2) return true;
+    const int k_per_tile = (g.K + splits - 1) / (splits < 1 ? 1 : splits);
+    return k_per_tile <= 2048;
 }
 
 template <int BN, bool A_MN, bool B_MN, int EPI>
 cudaError_t launch(const GemmProblem& g, cudaStream_t st) {
-    using C = Cfg<BN, B_MN>;
+    using C = Cfg<BN, B_MN, EPI>;
     auto kern = gemm_kernel<BN, A_MN, B_MN, EPI>;
     static bool configured = false;
     if (!configured) {
@@ -752,17 +1058,20 @@ cudaError_t launch(const GemmProblem& g, cudaStream_t st) {
     p.ldg = g.ldg;
     p.split_stride = g.split_stride;
     p.lr = g.lr;
-    if (EPI == EPI_SGD_F32 && p.splits != 1) return cudaErrorInvalidValue;
+    p.narrow = 0;
+    if ((EPI & (EPI_TMA - 1)) == EPI_SGD_F32 && p.splits != 1) return cudaErrorInvalidValue;
+    CUtensorMap to, tg;
+    if (!make_epilogue_maps<EPI>(g, p.splits, &to, &tg)) return cudaErrorInvalidValue;
     const int total = p.m_tiles * p.n_tiles * p.splits;
     const int grid = total < num_sms() ? total : num_sms();
-    kern<<<grid, kThreads, C::SMEM, st>>>(ta, tb, p);
+    kern<<<grid, kThreads, C::SMEM, st>>>(ta, tb, to, tg, p);
     return cudaGetLastError();
 }
 
 // 2-CTA launch: BN is the pair's N (each CTA stages BN/2 columns of B); grid = 2 x clusters.
 template <int BN, bool A_MN, bool B_MN, int EPI>
 cudaError_t launch2(const GemmProblem& g, cudaStream_t st) {
-    using C = Cfg2<BN, A_MN, B_MN>;
+    using C = Cfg2<BN, A_MN, B_MN, EPI>;
     auto kern = gemm2_kernel<BN, A_MN, B_MN, EPI>;
     static bool configured = false;
     if (!configured) {
@@ -795,35 +1104,57 @@ cudaError_t launch2(const GemmProblem& g, cudaStream_t st) {
     p.ldg = g.ldg;
     p.split_stride = g.split_stride;
     p.lr = g.lr;
-    if (EPI == EPI_SGD_F32 && p.splits != 1) return cudaErrorInvalidValue;
+    {
+        const int last = g.N - (p.n_tiles - 1) * BN;  // columns in the last N tile
+        static const int allow = [] {  // SP_NARROW=0 disables half-width tiles (A/B only)
+            const char* e = std::getenv("SP_NARROW");
+            return e ? std::atoi(e) : 1;
+        }();
+        p.narrow = (allow && BN == 256 && last <= 128) ? 1 : 0;
+    }
+    if ((EPI & (EPI_TMA - 1)) == EPI_SGD_F32 && p.splits != 1) return cudaErrorInvalidValue;
+    CUtensorMap to, tg;
+    if (!make_epilogue_maps<EPI>(g, p.splits, &to, &tg)) return cudaErrorInvalidValue;
     const int total = p.m_tiles * p.n_tiles * p.splits;
     const int pairs = num_sms() / 2;
     const int grid = 2 * (total < pairs ? total : pairs);
-    kern<<<grid, kThreads, C::SMEM, st>>>(ta, tb, p);
+    kern<<<grid, kThreads, C::SMEM, st>>>(ta, tb, to, tg, p);
     return cudaGetLastError();
+}
+
+// Picks the epilogue kind at run time; each kind is its own kernel instantiation.
+template <int BN, bool A_MN, bool B_MN, int EPI>
+cudaError_t launch_k(const GemmProblem& g, cudaStream_t st) {
+    return use_tma_epilogue(g, g.splits < 1 ? 1 : g.splits) ? launch<BN, A_MN, B_MN, EPI | EPI_TMA>(g, st)
+                                                             : launch<BN, A_MN, B_MN, EPI>(g, st);
+}
+template <int BN, bool A_MN, bool B_MN, int EPI>
+cudaError_t launch2_k(const GemmProblem& g, cudaStream_t st) {
+    return use_tma_epilogue(g, g.splits < 1 ? 1 : g.splits) ? launch2<BN, A_MN, B_MN, EPI | EPI_TMA>(g, st)
+                                                             : launch2<BN, A_MN, B_MN, EPI>(g, st);
 }
 
 template <int BN>
 cudaError_t dispatch_bn(const GemmProblem& g, cudaStream_t st) {
-    if (!g.a_mn && g.b_mn && g.epilogue == EPI_BIAS_ACT_BF16) return launch<BN, false, true, EPI_BIAS_ACT_BF16>(g, st);
-    if (!g.a_mn && g.b_mn && g.epilogue == EPI_BIAS_ACT_F32) return launch<BN, false, true, EPI_BIAS_ACT_F32>(g, st);
-    if (!g.a_mn && !g.b_mn && g.epilogue == EPI_GATE_BF16) return launch<BN, false, false, EPI_GATE_BF16>(g, st);
-    if (g.a_mn && g.b_mn && g.epilogue == EPI_F32) return launch<BN, true, true, EPI_F32>(g, st);
-    if (g.a_mn && g.b_mn && g.epilogue == EPI_SGD_F32) return launch<BN, true, true, EPI_SGD_F32>(g, st);
-    if (!g.a_mn && !g.b_mn && g.epilogue == EPI_F32) return launch<BN, false, false, EPI_F32>(g, st);
-    if (!g.a_mn && g.b_mn && g.epilogue == EPI_F32) return launch<BN, false, true, EPI_F32>(g, st);
+    if (!g.a_mn && g.b_mn && g.epilogue == EPI_BIAS_ACT_BF16) return launch_k<BN, false, true, EPI_BIAS_ACT_BF16>(g, st);
+    if (!g.a_mn && g.b_mn && g.epilogue == EPI_BIAS_ACT_F32) return launch_k<BN, false, true, EPI_BIAS_ACT_F32>(g, st);
+    if (!g.a_mn && !g.b_mn && g.epilogue == EPI_GATE_BF16) return launch_k<BN, false, false, EPI_GATE_BF16>(g, st);
+    if (g.a_mn && g.b_mn && g.epilogue == EPI_F32) return launch_k<BN, true, true, EPI_F32>(g, st);
+    if (g.a_mn && g.b_mn && g.epilogue == EPI_SGD_F32) return launch_k<BN, true, true, EPI_SGD_F32>(g, st);
+    if (!g.a_mn && !g.b_mn && g.epilogue == EPI_F32) return launch_k<BN, false, false, EPI_F32>(g, st);
+    if (!g.a_mn && g.b_mn && g.epilogue == EPI_F32) return launch_k<BN, false, true, EPI_F32>(g, st);
     return cudaErrorNotSupported;
 }
 
 template <int BN>
 cudaError_t dispatch2_bn(const GemmProblem& g, cudaStream_t st) {
-    if (!g.a_mn && g.b_mn && g.epilogue == EPI_BIAS_ACT_BF16) return launch2<BN, false, true, EPI_BIAS_ACT_BF16>(g, st);
-    if (!g.a_mn && g.b_mn && g.epilogue == EPI_BIAS_ACT_F32) return launch2<BN, false, true, EPI_BIAS_ACT_F32>(g, st);
-    if (!g.a_mn && !g.b_mn && g.epilogue == EPI_GATE_BF16) return launch2<BN, false, false, EPI_GATE_BF16>(g, st);
-    if (g.a_mn && g.b_mn && g.epilogue == EPI_F32) return launch2<BN, true, true, EPI_F32>(g, st);
-    if (g.a_mn && g.b_mn && g.epilogue == EPI_SGD_F32) return launch2<BN, true, true, EPI_SGD_F32>(g, st);
-    if (!g.a_mn && !g.b_mn && g.epilogue == EPI_F32) return launch2<BN, false, false, EPI_F32>(g, st);
-    if (!g.a_mn && g.b_mn && g.epilogue == EPI_F32) return launch2<BN, false, true, EPI_F32>(g, st);
+    if (!g.a_mn && g.b_mn && g.epilogue == EPI_BIAS_ACT_BF16) return launch2_k<BN, false, true, EPI_BIAS_ACT_BF16>(g, st);
+    if (!g.a_mn && g.b_mn && g.epilogue == EPI_BIAS_ACT_F32) return launch2_k<BN, false, true, EPI_BIAS_ACT_F32>(g, st);
+    if (!g.a_mn && !g.b_mn && g.epilogue == EPI_GATE_BF16) return launch2_k<BN, false, false, EPI_GATE_BF16>(g, st);
+    if (g.a_mn && g.b_mn && g.epilogue == EPI_F32) return launch2_k<BN, true, true, EPI_F32>(g, st);
+    if (g.a_mn && g.b_mn && g.epilogue == EPI_SGD_F32) return launch2_k<BN, true, true, EPI_SGD_F32>(g, st);
+    if (!g.a_mn && !g.b_mn && g.epilogue == EPI_F32) return launch2_k<BN, false, false, EPI_F32>(g, st);
+    if (!g.a_mn && g.b_mn && g.epilogue == EPI_F32) return launch2_k<BN, false, true, EPI_F32>(g, st);
     return cudaErrorNotSupported;
 }
 
@@ -831,8 +1162,8 @@ cudaError_t dispatch2_bn(const GemmProblem& g, cudaStream_t st) {
 // per CTA) exist only for K-major B, where a CTA's B half is a plain [rows][64] TMA box.
 template <int BN>
 cudaError_t dispatch2_bn_kmajor(const GemmProblem& g, cudaStream_t st) {
-    if (!g.a_mn && !g.b_mn && g.epilogue == EPI_GATE_BF16) return launch2<BN, false, false, EPI_GATE_BF16>(g, st);
-    if (!g.a_mn && !g.b_mn && g.epilogue == EPI_F32) return launch2<BN, false, false, EPI_F32>(g, st);
+    if (!g.a_mn && !g.b_mn && g.epilogue == EPI_GATE_BF16) return launch2_k<BN, false, false, EPI_GATE_BF16>(g, st);
+    if (!g.a_mn && !g.b_mn && g.epilogue == EPI_F32) return launch2_k<BN, false, false, EPI_F32>(g, st);
     return cudaErrorNotSupported;
 }
 
@@ -842,16 +1173,37 @@ cudaError_t dispatch2_bn_kmajor(const GemmProblem& g, cudaStream_t st) {
 // rate. Relative per-SM rates calibrated on B200 (tools/gemm_bench.py, grouped rasterisation):
 // 2-CTA N=256 ~0.95 (1189 TFLOP/s at 16384x1600x1600, 1568 at 65536x4096x4096), 1-CTA
 // N=192/256 ~0.80; N=128 tiles (either kind) are never competitive and are not candidates.
+// Busiest CTA pair's work, in full-tile units, under PairSched (kernels above): F full tiles
+// round-robin, R half-width tiles largest-first.
+double pair_max_load(long F, long R, long U) {
+    const long q = F / U, r = F % U, lo = U - r;
+    double worst = 0.0;
+    for (long u = 0; u < U; ++u) {
+        long halves = 0;
+        if (u >= r) halves += (u - r < R) + (u - r + lo < R);
+        const long first = 2 * lo + u;  // then every U-th half tile
+        if (first < R) halves += (R - 1 - first) / U + 1;
+        const double load = static_cast<double>(q + (u < r ? 1 : 0)) + 0.5 * static_cast<double>(halves);
+        worst = load > worst ? load : worst;
+    }
+    return worst;
+}
+
 GemmChoice choose_gemm(int M, int N, int K, int splits) {
     const int sms = num_sms();
     GemmChoice best{1, 256};
     double best_t = 1e300;
     auto consider = [&](int cta, int bn, double eff) {
-        const long tiles = static_cast<long>((M + cta * tc::BM - 1) / (cta * tc::BM)) *
-                           ((N + bn - 1) / bn) * splits;
+        const long mt = (M + cta * tc::BM - 1) / (cta * tc::BM);
+        const long nt = (N + bn - 1) / bn;
+        const long tiles = mt * nt * splits;
         const long slots = sms / cta;
-        const long waves = (tiles + slots - 1) / slots;
-        const double t = static_cast<double>(waves) * tc::BM * bn / eff;  // per-SM work per wave
+        double waves = static_cast<double>((tiles + slots - 1) / slots);
+        if (cta == 2 && bn == 256 && N - (nt - 1) * bn <= 128) {  // half-width last N tile
+            const long R = mt * splits, F = tiles - R;
+            waves = pair_max_load(F, R, tiles < slots ? tiles : slots);
+        }
+        const double t = waves * tc::BM * bn / eff;  // per-SM work of the busiest SM
         if (t < best_t - 1e-9) {
             best_t = t;
             best = GemmChoice{cta, bn};

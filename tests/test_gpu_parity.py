@@ -303,7 +303,11 @@ def test_tcgen05_gemm_matches_torch(cta, bn, layout, epi):
         assert rc != 0
         return
     # M-major A needs a 16-byte aligned leading dim (M % 8 == 0); partial tiles still covered
-    for (M, N, K) in [(128, bn, 64), (304, 2 * bn, 320), (1000, 3 * bn - 64, 1600), (520, bn, 192)]:
+    # (.., 2*bn + 64, ..): a 64-column last N tile -> the 2-CTA kernel's half-width tiles and
+    # largest-first pair schedule; (16384, 1600, ..) has enough tiles that full and half tiles
+    # share CTA pairs
+    for (M, N, K) in [(128, bn, 64), (304, 2 * bn, 320), (1000, 3 * bn - 64, 1600), (520, bn, 192),
+                      (1000, 2 * bn + 64, 640), (16384, 1600, 128)]:
         got, ref = _gemm(M, N, K, a_mn, b_mn, epi, bn, cta=cta)
         tol = 1e-2 if epi in (0, 2) else 2e-4  # bf16 output rounding vs fp32 accumulation order
         assert rel_err(got, ref) <= tol, (M, N, K, cta, bn, layout, epi, rel_err(got, ref))

@@ -38,8 +38,12 @@ def timeit(fn, reps=20):
 
 
 fl = 2.0 * rows * d * d
-for cta, bn in [(1, 192), (1, 256), (2, 128), (2, 192), (2, 256), (0, 0)]:
-    shapes = {
+VARIANTS = [(1, 192), (1, 256), (2, 128), (2, 192), (2, 256), (0, 0)]
+ROUNDS = int(os.environ.get("ROUNDS", "3"))
+
+
+def shapes_for(cta, bn):
+    return {
         "fwd": lambda: LIB.sp_debug_gemm_bf16_async(rows, d, d, x.data_ptr(), d, 0, W.data_ptr(), d, 1, 0,
                                                     out16.data_ptr(), d, bias.data_ptr(), 1, None, 0, 1,
                                                     bn, cta, st),
@@ -54,12 +58,22 @@ for cta, bn in [(1, 192), (1, 256), (2, 128), (2, 192), (2, 256), (0, 0)]:
                                                          1, 3, parts.data_ptr(), d, None, 0, None, 0,
                                                          SPLITS, bn, cta, st),
     }
-    for name, fn in shapes.items():
-        if cta == 2 and bn == 192 and name != "dx":
-            continue  # 2-CTA N=192 exists for K-major B only
-        ms = timeit(fn)
-        print(json.dumps({"cta": cta or "auto", "bn": bn or "auto", "gemm": name, "ms": round(ms, 4),
-                          "tflops": round(fl / ms / 1e9, 1)}), flush=True)
+
+
+# Variants are interleaved round-robin over ROUNDS rounds (clock / power drift hits every
+# variant alike); min and median per (variant, shape) are reported.
+times = {}
+for r in range(ROUNDS):
+    for cta, bn in VARIANTS:
+        for name, fn in shapes_for(cta, bn).items():
+            if cta == 2 and bn == 192 and name != "dx":
+                continue  # 2-CTA N=192 exists for K-major B only
+            times.setdefault((cta, bn, name), []).append(timeit(fn))
+for (cta, bn, name), ts in times.items():
+    ts = sorted(ts)
+    print(json.dumps({"cta": cta or "auto", "bn": bn or "auto", "gemm": name,
+                      "ms_min": round(ts[0], 4), "ms_med": round(ts[len(ts) // 2], 4),
+                      "tflops_best": round(fl / ts[0] / 1e9, 1)}), flush=True)
 for name, fn in {"torch_fwd": lambda: torch.matmul(x, W),
                  "torch_dx": lambda: torch.matmul(dz, W.t()),
                  "torch_dw": lambda: torch.matmul(x.t(), dz)}.items():
