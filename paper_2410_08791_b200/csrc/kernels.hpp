@@ -64,7 +64,7 @@ struct GemmChoice {
 };
 // The kernel variant gemm_bf16 picks when cta/block_n are 0 (depends on the shape only, so
 // results are identical for every window setting).
-GemmChoice choose_gemm(int M, int N, int K, int splits);
+GemmChoice choose_gemm(int M, int N, int K, int splits, int epilogue);
 
 // Launches the warp-specialized tcgen05/TMEM/TMA GEMM. Returns cudaSuccess or an error.
 cudaError_t gemm_bf16(const GemmProblem& p, cudaStream_t st);

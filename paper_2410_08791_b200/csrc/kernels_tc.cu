@@ -1023,6 +1023,13 @@ bool use_tma_epilogue(const GemmProblem& g, int splits) {
     return k_per_tile <= 2048;
 }
 
+// Half-width last N tiles (PairSched) pay only for the split-K fp32 partials of dW (+5%, ncu):
+// for the activation GEMMs they were neutral warm and, being scheduled last, re-read every A
+// panel after it has left L2 (82 vs 58 MB DRAM reads per forward launch at 16384 x 1600).
+bool narrow_tiles(int epi_base, int bn, int last_cols) {
+    return epi_base == EPI_F32 && bn == 256 && last_cols <= 128;
+}
+
 template <int BN, bool A_MN, bool B_MN, int EPI>
 cudaError_t launch(const GemmProblem& g, cudaStream_t st) {
     using C = Cfg<BN, B_MN, EPI>;
@@ -1106,11 +1113,7 @@ cudaError_t launch2(const GemmProblem& g, cudaStream_t st) {
     p.lr = g.lr;
     {
         const int last = g.N - (p.n_tiles - 1) * BN;  // columns in the last N tile
-        static const int allow = [] {  // SP_NARROW=0 disables half-width tiles (A/B only)
-            const char* e = std::getenv("SP_NARROW");
-            return e ? std::atoi(e) : 1;
-        }();
-        p.narrow = (allow && BN == 256 && last <= 128) ? 1 : 0;
+        p.narrow = narrow_tiles(EPI & (EPI_TMA - 1), BN, last) ? 1 : 0;
     }
     if ((EPI & (EPI_TMA - 1)) == EPI_SGD_F32 && p.splits != 1) return cudaErrorInvalidValue;
     CUtensorMap to, tg;
@@ -1189,7 +1192,7 @@ double pair_max_load(long F, long R, long U) {
     return worst;
 }
 
-GemmChoice choose_gemm(int M, int N, int K, int splits) {
+GemmChoice choose_gemm(int M, int N, int K, int splits, int epilogue) {
     const int sms = num_sms();
     GemmChoice best{1, 256};
     double best_t = 1e300;
@@ -1199,7 +1202,7 @@ GemmChoice choose_gemm(int M, int N, int K, int splits) {
         const long tiles = mt * nt * splits;
         const long slots = sms / cta;
         double waves = static_cast<double>((tiles + slots - 1) / slots);
-        if (cta == 2 && bn == 256 && N - (nt - 1) * bn <= 128) {  // half-width last N tile
+        if (cta == 2 && tc::narrow_tiles(epilogue, bn, N - (nt - 1) * bn)) {  // half-width last N tile
             const long R = mt * splits, F = tiles - R;
             waves = pair_max_load(F, R, tiles < slots ? tiles : slots);
         }
@@ -1261,7 +1264,7 @@ cudaError_t gemm_bf16(const GemmProblem& g, cudaStream_t st) {
     if (g.N % 32 != 0 || g.lda % 8 != 0 || g.ldb % 8 != 0) return cudaErrorInvalidValue;
     int cta = g.cta, bn = g.block_n;
     if (cta == 0) {  // auto
-        const GemmChoice c = choose_gemm(g.M, g.N, g.K, g.splits < 1 ? 1 : g.splits);
+        const GemmChoice c = choose_gemm(g.M, g.N, g.K, g.splits < 1 ? 1 : g.splits, g.epilogue);
         cta = c.cta;
         if (!bn) bn = c.block_n;
         if (cta == 2 && bn != 128 && bn != 256 && !(bn == 192 && !g.b_mn)) cta = 1;  // a forced tile width decides
