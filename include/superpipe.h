@@ -167,6 +167,13 @@ int sp_set_trace(sp_exec* ex, int32_t level);
  * in the layer math, so outputs are bitwise identical; only the transfer count, the ledger
  * and the time change. */
 int sp_set_item_batching(sp_exec* ex, int32_t on);
+/* Prefetch timing. 1 (default): a weight/activation H2D starts as soon as its ring slot is free
+ * (the compute that last read the slot has finished). 0: it also waits for the compute whose
+ * completion triggers it in the reference policy (policy_step, scheduler.cpp:105-136: after
+ * every k' computes). Both run the same op sequence in the same slots with the same ledger and
+ * bitwise-identical results; 1 keeps the link busier (copies are not held behind a
+ * copy -> compute -> copy round trip). */
+int sp_set_eager_prefetch(sp_exec* ex, int32_t on);
 /* Copies up to cap events of the last call's measured timeline; *count = total rows. */
 int sp_get_trace(const sp_exec* ex, sp_trace_event* events, int32_t cap, int32_t* count);
 
@@ -199,9 +206,13 @@ uint64_t sp_peak_weight_residency(int32_t strategy, int32_t k, int32_t k_prime,
                                   int32_t n_layers, uint64_t layer_bytes);
 int sp_validate_strategy(int32_t strategy, int32_t k, int32_t k_prime, int32_t n_layers);
 /* Describes the static op plan the executor would run (policy_step, scheduler.cpp:53-141,
- * resolved ahead of time) as text, one op per line; returns the needed length. Host-only. */
+ * resolved ahead of time) as text, one op per line; returns the needed length. Host-only.
+ * flags: SP_PLAN_SHARDED (data-parallel sharded streaming), SP_PLAN_EAGER (eager prefetch
+ * dependencies, see sp_set_eager_prefetch). */
+#define SP_PLAN_SHARDED 1
+#define SP_PLAN_EAGER 2
 int64_t sp_describe_plan(const sp_config* cfg, int32_t n_items, int32_t train,
-                         const int32_t* frozen, int32_t sharded, char* buf, int64_t cap);
+                         const int32_t* frozen, int32_t flags, char* buf, int64_t cap);
 /* Deterministic layer / input generators of the reference (host-only), so callers can
  * register synthetic models without a second copy: build_model's per-layer splitmix64 stream
  * (model.cpp:23-52, W[fan_in][fan_out] then b[fan_out], U(+-1/sqrt(fan_in)); fan_in = fan_out

@@ -133,6 +133,12 @@ int sp_set_trace(sp_exec* ex, int32_t level) {
     return SP_OK;
 }
 
+int sp_set_eager_prefetch(sp_exec* ex, int32_t on) {
+    if (!ex || on < 0 || on > 1) return SP_ERR_INVALID;
+    ex->impl->set_eager_prefetch(on != 0);
+    return SP_OK;
+}
+
 int sp_set_item_batching(sp_exec* ex, int32_t on) {
     if (!ex || on < 0 || on > 1) return SP_ERR_INVALID;
     ex->impl->set_item_batching(on != 0);
@@ -204,7 +210,7 @@ int sp_validate_strategy(int32_t strategy, int32_t k, int32_t k_prime, int32_t n
 }
 
 int64_t sp_describe_plan(const sp_config* cfg, int32_t n_items, int32_t train,
-                         const int32_t* frozen, int32_t sharded, char* buf, int64_t cap) {
+                         const int32_t* frozen, int32_t flags, char* buf, int64_t cap) {
     if (!cfg) return -1;
     sp::PlanInput in;
     in.n_layers = cfg->n_layers;
@@ -220,7 +226,8 @@ int64_t sp_describe_plan(const sp_config* cfg, int32_t n_items, int32_t train,
     in.capacity = cfg->capacity_bytes;
     if (frozen)
         for (int32_t l = 0; l < cfg->n_layers; ++l) in.frozen.push_back(frozen[l] != 0);
-    in.sharded = sharded != 0;
+    in.sharded = (flags & SP_PLAN_SHARDED) != 0;
+    in.eager = (flags & SP_PLAN_EAGER) != 0;
     sp::Plan plan = sp::build_plan(in, {});
     std::string text = plan.error.empty() ? sp::describe_plan(plan) : ("ERROR " + plan.error + "\n");
     if (buf && cap > 0) {

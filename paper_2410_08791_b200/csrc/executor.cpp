@@ -301,6 +301,7 @@ Plan Executor::make_plan(bool train, int n_items, int64_t rows, int fmt) {
     in.act_bytes = static_cast<uint64_t>(rows) * d_ * 4;
     in.capacity = cfg_.capacity_bytes;
     in.sharded = sharded_;
+    in.eager = eager_prefetch_;
     const std::vector<SlotCache> none;
     Plan plan = build_plan(in, fmt == cache_fmt_ ? cache_ : none);
     if (!plan.error.empty()) throw Error(plan.oom ? SP_ERR_OOM : SP_ERR_INVALID, plan.error);

@@ -38,6 +38,7 @@ public:
     void digest_train(float loss, char out[17]) const;
     void set_trace(int level) { cfg_.trace = level; }
     void set_item_batching(bool on) { item_batching_ = on; }
+    void set_eager_prefetch(bool on) { eager_prefetch_ = on; }
     std::string last_plan_text() const { return describe_plan(last_plan_); }
     void dp_init(const uint8_t id[128], int rank, int world, bool shard_weights);
     void dp_sync();
@@ -124,6 +125,7 @@ private:
     std::vector<uint8_t> cross_dep_;  // op has a dependent on another stream
     bool use_graphs_ = true;
     bool item_batching_ = false;  // forward: n_items x rows as one layer-major pass
+    bool eager_prefetch_ = true;  // H2D waits for its slot only, not the policy trigger
     bool capturing_ = false;
     // Timing events: plain records when eager; "external" event-record nodes under capture
     // (cudaEventRecordExternal is only valid while capturing).

@@ -273,7 +273,7 @@ private:
             Op op;
             op.kind = OpKind::H2D;
             op.pass = pass_;
-            if (trigger >= 0) op.deps.push_back(trigger);
+            if (trigger >= 0 && !in_.eager) op.deps.push_back(trigger);
             for (const auto& m : group) {
                 op.layers.push_back(seq()[m.pos]);
                 op.slots.push_back(m.slot);

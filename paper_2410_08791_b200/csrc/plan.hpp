@@ -53,6 +53,10 @@ struct PlanInput {
     int n_items = 1;
     bool checkpointing = false;
     bool sharded = false;         // data parallel: H2D 1/world of each layer + all-gather
+    // Eager prefetch: an H2D waits only for its slot to be free (and, for activation reloads,
+    // for the offload it reads) - not for the compute that triggers it in policy_step
+    // (scheduler.cpp:105-136). Same ops, order, slots and ledger; copies start earlier.
+    bool eager = false;
     std::vector<uint8_t> frozen;  // per layer
     uint64_t layer_bytes = 0;     // reference ledger units: (d*d + d) * 4
     uint64_t act_bytes = 0;       // rows * d * 4

@@ -416,3 +416,32 @@ def test_item_batching_is_bitwise_and_streams_once(numerics):
     assert out[False][1]["h2d_bytes"] == items * out[True][1]["h2d_bytes"]  # no cross-item reuse at S=3 < n
     if numerics == sp.EXACT:
         assert np.array_equal(out[True][0], oracle_outputs(model, list(xs)))
+
+
+@pytest.mark.parametrize("numerics", [sp.EXACT, sp.BF16])
+def test_eager_prefetch_is_bitwise_and_same_ledger(numerics):
+    """sp_set_eager_prefetch: copies start when their slot frees instead of at the reference
+    policy's trigger; results, transfer counts and ledger peaks are identical."""
+    n, d, rows = 7, 32 if numerics == sp.EXACT else 128, 6 if numerics == sp.EXACT else 256
+    model = sp.build_model(23, n, d, 1)
+    xs = np.stack(inputs(23, 2, rows, d))
+    x, t = sp.make_input(23, 0, rows, d), sp.make_input(23, 1, rows, d)
+    res = {}
+    for eager in (False, True):
+        for s in [S(sp.SUPERPIPELINE, 2, 1), S(sp.SUPERPIPELINE, 4, 3, sp.SEQUENTIAL)]:
+            for ckpt in (False, True):
+                with sp.Executor(n, d, s, numerics=numerics, checkpointing=ckpt) as ex:
+                    ex.register_model(model)
+                    ex.set_eager_prefetch(eager)
+                    y = ex.forward(xs)
+                    st_f = ex.stats()
+                    loss = ex.train_step(x, t, 0.05)
+                    st_t = ex.stats()
+                    m = ex.read_model(model)
+                keys = ("peak_bytes", "peak_weight_bytes", "n_transfers_h2d", "h2d_bytes", "d2h_bytes")
+                res[(eager, str(s), ckpt)] = (y, loss, m.W, m.b, [st_f[k] for k in keys], [st_t[k] for k in keys])
+    for key, (y, loss, W, b, sf, stt) in res.items():
+        ref = res[(False,) + key[1:]]
+        assert np.array_equal(y, ref[0]) and loss == ref[1], key
+        assert np.array_equal(W, ref[2]) and np.array_equal(b, ref[3]), key
+        assert sf == ref[4] and stt == ref[5], key

@@ -84,9 +84,16 @@ def happens_before(ops):
 
 
 def check(n, strategy, train, ckpt, items=1, frozen=None, sharded=False):
+    # both dependency modes: the reference policy's triggers, and eager prefetch (an H2D waits
+    # only for its slot) - the executor's default, which must be just as race-free
+    for eager in (False, True):
+        check_one(n, strategy, train, ckpt, items, frozen, sharded, eager)
+
+
+def check_one(n, strategy, train, ckpt, items, frozen, sharded, eager):
     frozen = frozen or [0] * n
     txt = sp.describe_plan(n, 8, strategy, n_items=items, train=train, checkpointing=ckpt,
-                           frozen=frozen, sharded=sharded)
+                           frozen=frozen, sharded=sharded, eager=eager)
     assert not txt.startswith("ERROR"), txt
     head, ops = parse_plan(txt)
     ck = ckpt and train and strategy.kind != sp.STANDARD
@@ -101,7 +108,8 @@ def check(n, strategy, train, ckpt, items=1, frozen=None, sharded=False):
             if STREAM[ops[a]["kind"]] == STREAM[ops[b]["kind"]]:
                 continue
             assert hb(a, b), (f"unordered {res}: op {a} {ops[a]['kind']} and op {b} "
-                              f"{ops[b]['kind']} (n={n} {strategy} train={train} ckpt={ckpt})")
+                              f"{ops[b]['kind']} (n={n} {strategy} train={train} ckpt={ckpt} "
+                              f"eager={eager})")
 
 
 STRATS = [sp.StrategyConfig(sp.STANDARD), sp.StrategyConfig(sp.NAIVE, 1),
@@ -174,3 +182,22 @@ def test_checker_detects_a_missing_edge():
             if (wa or wb) and STREAM[ops[a]["kind"]] != STREAM[ops[b]["kind"]] and not hb(a, b):
                 bad += 1
     assert bad > 0
+
+
+def test_eager_prefetch_changes_only_the_trigger_dependencies():
+    """Eager prefetch keeps the op sequence, slots and ledger of the reference policy; H2D ops
+    only lose the dependency on their trigger compute (so copies can run ahead into free
+    slots), and every other op's dependencies are unchanged."""
+    for train in (False, True):
+        a = parse_plan(sp.describe_plan(12, 8, sp.StrategyConfig(sp.SUPERPIPELINE, 2, 1), train=train))[1]
+        b = parse_plan(sp.describe_plan(12, 8, sp.StrategyConfig(sp.SUPERPIPELINE, 2, 1), train=train,
+                                        eager=True))[1]
+        assert len(a) == len(b)
+        relaxed = 0
+        for x, y in zip(a, b):
+            assert {k: v for k, v in x.items() if k != "deps"} == {k: v for k, v in y.items() if k != "deps"}
+            assert set(y["deps"]) <= set(x["deps"])
+            if x["kind"] != "H2D":
+                assert x["deps"] == y["deps"]
+            relaxed += len(set(x["deps"]) - set(y["deps"]))
+        assert relaxed > 0

@@ -23,6 +23,8 @@ from paper_2410_08791_b200 import _capi  # noqa: E402
 
 CONFIGS = {
     "c1": dict(n=12, d=768, items=4, rows=1, windows=[(2, 1)]),
+    # c1 with sp_set_item_batching: the 4 items stream the layer stack once (layer-major)
+    "c1x": dict(n=12, d=768, items=4, rows=1, windows=[(2, 1)], batching=True),
     "c1b": dict(n=12, d=768, items=1, rows=4096, windows=[(2, 1), (4, 2)]),
     "c3": dict(n=32, d=4096, items=1, rows=65536, windows=[(4, 2)]),
     "c5": dict(n=80, d=8192, items=1, rows=8192, windows=[(8, 1), (8, 2), (8, 4), (12, 6)],
@@ -52,6 +54,8 @@ def main():
     p = argparse.ArgumentParser()
     p.add_argument("configs", nargs="*", default=["c1", "c1b", "c3"])
     p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--reference-prefetch", action="store_true",
+                   help="copies wait for the reference policy's trigger compute (no eager prefetch)")
     a = p.parse_args()
     peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["bf16_tflops_sustained"] * 1e12
     for name in a.configs:
@@ -65,6 +69,8 @@ def main():
                              trace=0, capacity_bytes=c.get("capacity", 0))
             for i, (W, b) in enumerate(weights):
                 ex.register_layer(i, W, b)
+            ex.set_item_batching(c.get("batching", False))
+            ex.set_eager_prefetch(not a.reference_prefetch)
             for _ in range(2):
                 ex.forward_ptr(x.data_ptr(), rows, items, y.data_ptr(), device=True)
             torch.cuda.synchronize()
@@ -77,9 +83,11 @@ def main():
             ms = e0.elapsed_time(e1) / a.steps
             st = ex.stats()
             wire = d * d * 2 + d * 4
-            roof = items * n * max(2.0 * rows * d * d / peak, wire / 55.5e9) * 1e3
+            passes = 1 if c.get("batching") else items  # layer-stack passes over the link
+            roof = passes * n * max(2.0 * rows * d * d * items / passes / peak, wire / 55.5e9) * 1e3
             print(json.dumps({
                 "config": name, "layers": n, "d": d, "items": items, "rows": rows, "k": k,
+                "item_batching": bool(c.get("batching")), "eager_prefetch": not a.reference_prefetch,
                 "k_prime": kp, "ms_per_call": ms, "samples_per_s": items * rows / (ms * 1e-3),
                 "layer_roofline_ms": roof, "frac_of_roofline": roof / ms,
                 "n_slots": st["n_slots"], "peak_weight_gb": st["peak_weight_bytes"] / 1e9,
