@@ -6,3 +6,4 @@ reference's pipesim API over that ABI (see engine.py).
 """
 from .engine import *  # noqa: F401,F403
 from .engine import __all__  # noqa: F401
+from . import experiment, trace_io, tuner  # noqa: F401,E402  (caller-side harness, formats, tuner)

@@ -91,6 +91,16 @@ def main():
     with open(path, "w") as f:
         json.dump(out, f, indent=1)
     print(f"wrote {len(cases)} cases to {path}")
+    # The reference's shipped experiment configs (data), for the experiment-harness tests.
+    cfg_dir = os.path.join(ROOT, "tests", "golden", "configs")
+    os.makedirs(cfg_dir, exist_ok=True)
+    for name in ("default.json", "oom_train.json"):
+        with open(os.path.join("/root/reference/proj/configs", name)) as f:
+            cfg = json.load(f)
+        with open(os.path.join(cfg_dir, name), "w") as f:
+            json.dump(cfg, f, indent=2)
+            f.write("\n")
+    print(f"wrote reference configs to {cfg_dir}")
 
 
 if __name__ == "__main__":
