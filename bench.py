@@ -48,6 +48,8 @@ def parse():
     p.add_argument("--strategy", default="superpipeline",
                    choices=["superpipeline", "standard", "naive"])
     p.add_argument("--lr", type=float, default=0.01)
+    p.add_argument("--mode", default="batch", choices=["batch", "sequential"],
+                   help="TransferMode (sim.hpp:15): one H2D op per k' group, or per layer")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--sweep", default="", help="comma list of k:kp to report extra lines")
     return p.parse_args()
@@ -255,7 +257,7 @@ def config_of(a, world):
     return {"workload": f"GPT-2 XL-shape layer stack: {a.layers} x d={a.d} dense ReLU blocks "
                         f"(reference LayerBlock), bf16 train step (fwd+MSE+bwd+SGD)",
             "layers": a.layers, "d": a.d, "rows_per_gpu": a.rows, "global_batch": a.rows * world,
-            "strategy": a.strategy, "k": a.k, "k_prime": a.kp, "transfer_mode": "batch",
+            "strategy": a.strategy, "k": a.k, "k_prime": a.kp, "transfer_mode": a.mode,
             "weights": "pinned host DRAM (fp32 master), streamed per step",
             "parallelism": f"dp{world}", "l2": "working set (weights+activations) >> 126 MB L2"}
 
@@ -278,7 +280,8 @@ def main():
     from paper_2410_08791_b200 import _capi
 
     pk, pk_src = peaks()
-    strategy = {"superpipeline": sp.StrategyConfig(sp.SUPERPIPELINE, a.k, a.kp),
+    tmode = sp.BATCH if a.mode == "batch" else sp.SEQUENTIAL
+    strategy = {"superpipeline": sp.StrategyConfig(sp.SUPERPIPELINE, a.k, a.kp, tmode),
                 "standard": sp.StrategyConfig(sp.STANDARD),
                 "naive": sp.StrategyConfig(sp.NAIVE, a.k)}[a.strategy]
     weights = []  # build_model(7, layers, d) — generated once, registered per executor
@@ -416,7 +419,8 @@ def main():
         else:
             k, kp = (int(v) for v in spec.split(":"))
             strat = (sp.StrategyConfig(sp.NAIVE, k) if kp == 0
-                     else sp.StrategyConfig(sp.SUPERPIPELINE, k, kp))
+                     else sp.StrategyConfig(sp.SUPERPIPELINE, k, kp,
+                                            sp.BATCH if a.mode == "batch" else sp.SEQUENTIAL))
         e = make_executor(strat)
         if world > 1:
             dp.init_executor_dp(e, dist, rank, world)

@@ -54,6 +54,7 @@ def main():
     p = argparse.ArgumentParser()
     p.add_argument("configs", nargs="*", default=["c1", "c1b", "c3"])
     p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--mode", default="batch", choices=["batch", "sequential"])
     p.add_argument("--reference-prefetch", action="store_true",
                    help="copies wait for the reference policy's trigger compute (no eager prefetch)")
     a = p.parse_args()
@@ -65,7 +66,8 @@ def main():
         x = torch.from_numpy(np.stack([sp.make_input(7, i, rows, d) for i in range(items)])).cuda()
         y = torch.empty_like(x)
         for k, kp in c["windows"]:
-            ex = sp.Executor(n, d, sp.StrategyConfig(sp.SUPERPIPELINE, k, kp), numerics=sp.BF16,
+            tmode = sp.BATCH if a.mode == "batch" else sp.SEQUENTIAL
+            ex = sp.Executor(n, d, sp.StrategyConfig(sp.SUPERPIPELINE, k, kp, tmode), numerics=sp.BF16,
                              trace=0, capacity_bytes=c.get("capacity", 0))
             for i, (W, b) in enumerate(weights):
                 ex.register_layer(i, W, b)
@@ -88,6 +90,7 @@ def main():
             print(json.dumps({
                 "config": name, "layers": n, "d": d, "items": items, "rows": rows, "k": k,
                 "item_batching": bool(c.get("batching")), "eager_prefetch": not a.reference_prefetch,
+                "transfer_mode": a.mode,
                 "k_prime": kp, "ms_per_call": ms, "samples_per_s": items * rows / (ms * 1e-3),
                 "layer_roofline_ms": roof, "frac_of_roofline": roof / ms,
                 "n_slots": st["n_slots"], "peak_weight_gb": st["peak_weight_bytes"] / 1e9,
