@@ -86,3 +86,97 @@ def test_shard_rows_requires_equal_shards():
     assert dp.shard_rows(16, 1, 4) == (4, 4)
     with pytest.raises(ValueError):
         dp.shard_rows(10, 0, 4)
+
+
+def _sharded_worker(rank, world, port, out):
+    """Emulates the executor's sharded-streaming step (executor.cpp enqueue_op H2D/ALLGATHER/D2H,
+    update_op reduce-scatter + shard SGD, dp_sync) on CPU bytes with gloo collectives, using
+    the executor's own shard geometry (sp_debug_shard_range)."""
+    import ctypes as C
+    import sys
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2410_08791_b200 import _capi, dp
+    from pyoracle import Oracle
+    orc = Oracle()
+    n, d, global_rows, lr = 3, 12, 6 * world, 0.05
+    W, b = orc.build_model(9, n, d)
+    x = orc.make_input(9, 0, global_rows, d)
+    t = orc.make_input(9, 1, global_rows, d)
+    start, count = dp.shard_rows(global_rows, rank, world)
+    img = (d * d + d) * 4
+    lo, hi = C.c_uint64(), C.c_uint64()
+    shard = int(_capi.LIB.sp_debug_shard_range(img, world, rank, C.byref(lo), C.byref(hi)))
+    lo, hi = lo.value, hi.value
+    # pinned host master of every rank: [W_l | b_l] fp32 images, registered identically
+    host = [np.concatenate([W[l].ravel(), b[l]]).astype(np.float32).view(np.uint8).copy()
+            for l in range(n)]
+    # forward/backward need the full layers: H2D own shard + all-gather -> full slot image
+    slots = []
+    for l in range(n):
+        mine = np.zeros(shard, np.uint8)
+        mine[:hi - lo] = host[l][lo:hi]
+        gathered = [torch.zeros(shard, dtype=torch.uint8) for _ in range(world)]
+        dist.all_gather(gathered, torch.from_numpy(mine))
+        slots.append(torch.cat(gathered).numpy()[:img].view(np.float32).copy())
+    Ws = np.stack([s[:d * d].reshape(d, d) for s in slots])
+    bs = np.stack([s[d * d:] for s in slots])
+    assert np.array_equal(Ws, W) and np.array_equal(bs, b)  # the gather rebuilt every layer
+    _, _, _, dW, db, _ = orc.train_step(Ws, bs, x[start:start + count], t[start:start + count], lr,
+                                        want_grads=True)
+    scale = np.float32(count / global_rows)
+    for l in range(n):
+        # gradient image [dW | db] padded to world*shard bytes, reduce-scattered (sum)
+        gimg = np.zeros(world * shard // 4, np.float32)
+        gimg[:d * d] = dW[l].ravel() * scale
+        gimg[d * d:d * d + d] = db[l] * scale
+        full = torch.from_numpy(gimg)
+        dist.all_reduce(full)  # gloo: reduce-scatter = all-reduce then keep this rank's shard
+        gs = full.numpy()[rank * shard // 4:(rank + 1) * shard // 4]
+        # SGD on this rank's shard of the slot, written back to this rank's host master shard
+        w32 = slots[l].view(np.uint8)[lo:hi].view(np.float32)
+        upd = (w32 - np.float32(lr) * gs[:(hi - lo) // 4]).astype(np.float32)
+        host[l][lo:hi] = upd.view(np.uint8)
+    stale = [not np.array_equal(host[l], np.concatenate([W[l].ravel(), b[l]]).view(np.uint8))
+             for l in range(n)]
+    # dp_sync: all-gather the host shards so every rank's master is whole again
+    synced = []
+    for l in range(n):
+        mine = np.zeros(shard, np.uint8)
+        mine[:hi - lo] = host[l][lo:hi]
+        gathered = [torch.zeros(shard, dtype=torch.uint8) for _ in range(world)]
+        dist.all_gather(gathered, torch.from_numpy(mine))
+        synced.append(torch.cat(gathered).numpy()[:img].view(np.float32).copy())
+    out.put((rank, np.stack(synced), any(stale)))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_streaming_step_equals_full_batch_step(world):
+    import sys
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from pyoracle import Oracle
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_sharded_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=180) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    orc = Oracle()
+    n, d, rows = 3, 12, 6 * world
+    W, b = orc.build_model(9, n, d)
+    x, t = orc.make_input(9, 0, rows, d), orc.make_input(9, 1, rows, d)
+    _, Wn, bn = orc.train_step(W, b, x, t, 0.05)
+    want = np.stack([np.concatenate([Wn[l].ravel(), bn[l]]) for l in range(n)])
+    imgs = [r[1] for r in sorted(res, key=lambda r: r[0])]
+    for img in imgs:  # every rank ends with the same, full-batch-updated master
+        assert np.array_equal(img, imgs[0])
+        assert np.allclose(img, want, rtol=1e-5, atol=1e-6)
+    assert all(r[2] for r in res)  # the step did change the host masters
