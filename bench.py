@@ -154,7 +154,9 @@ def gemm_kernel_timing(torch, capi, a, reps=20):
     dz = torch.randn(rows, d, device="cuda").to(torch.bfloat16) * 1e-3
     W = torch.randn(d, d, device="cuda").to(torch.bfloat16)
     W32 = torch.randn(d, d, device="cuda")
-    dw_splits = int(capi.LIB.sp_debug_dw_splits(d, rows))
+    import ctypes
+    dw_cta, dw_bn = ctypes.c_int32(), ctypes.c_int32()
+    dw_splits = int(capi.LIB.sp_debug_dw_choice(d, rows, 1, ctypes.byref(dw_cta), ctypes.byref(dw_bn)))
     parts = torch.empty(max(dw_splits, 1) * d * d, device="cuda") if dw_splits > 1 else W32
     bias = torch.randn(d, device="cuda")
     out = torch.empty(rows, d, device="cuda", dtype=torch.bfloat16)
@@ -170,7 +172,7 @@ def gemm_kernel_timing(torch, capi, a, reps=20):
         "dw": (lambda: L.sp_debug_gemm_bf16_async(d, d, rows, x.data_ptr(), d, 1,
                                                   dz.data_ptr(), d, 1, 4 if dw_splits == 1 else 3,
                                                   parts.data_ptr(), d, None, 0, None, 0,
-                                                  dw_splits, 0, 0, st), a.layers),
+                                                  dw_splits, dw_bn.value, dw_cta.value, st), a.layers),
     }
     res = {}
     for name, (fn, per_step) in shapes.items():

@@ -37,6 +37,10 @@ uint64_t sp_debug_shard_range(uint64_t img, int32_t world, int32_t rank, uint64_
 /* Split-K count the executor's bf16 dW GEMM uses for a d x d layer at `rows` rows (1 = SGD
  * fused into the GEMM epilogue; > 1 = fp32 partials reduced by the update op). */
 int32_t sp_debug_dw_splits(int32_t d, int64_t rows);
+/* The executor's full dW choice (choose_dw): returns the split count and writes the kernel
+ * variant (cta 1|2, tile N). fused_ok = 1 for one GPU (splits = 1 means SGD fused). */
+int32_t sp_debug_dw_choice(int32_t d, int64_t rows, int32_t fused_ok, int32_t* cta,
+                           int32_t* block_n);
 /* Split count the GEMM will use for a given K and requested splits. */
 int32_t sp_debug_effective_splits(int32_t K, int32_t splits);
 

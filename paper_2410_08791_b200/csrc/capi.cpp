@@ -341,7 +341,16 @@ extern "C" uint64_t sp_debug_shard_range(uint64_t img, int32_t world, int32_t ra
 extern "C" int32_t sp_debug_dw_splits(int32_t d, int64_t rows) {
     if (d < 1 || rows < 1 || rows > (1ll << 31) - 1) return 0;
     const int r = static_cast<int>(rows);
-    return sp::effective_splits(r, sp::choose_splits(d, d, r, sp::choose_block_n(d)));
+    return sp::choose_dw(d, d, r, 16, true).splits;
+}
+
+extern "C" int32_t sp_debug_dw_choice(int32_t d, int64_t rows, int32_t fused_ok, int32_t* cta,
+                                      int32_t* block_n) {
+    if (d < 1 || rows < 1 || rows > (1ll << 31) - 1 || !cta || !block_n) return 0;
+    const sp::DwChoice c = sp::choose_dw(d, d, static_cast<int>(rows), 16, fused_ok != 0);
+    *cta = c.cta;
+    *block_n = c.block_n;
+    return c.splits;
 }
 
 extern "C" int32_t sp_debug_effective_splits(int32_t K, int32_t splits) {

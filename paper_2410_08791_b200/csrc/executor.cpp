@@ -262,8 +262,7 @@ void Executor::ensure_buffers(int64_t rows, int n_items, bool train, bool device
         tgt_ = static_cast<float*>(alloc(act * 4));
         for (int l = 0; l < n_; ++l) act_.push_back(alloc(act * elt));
         for (auto& g : gbuf_) g = alloc(act * elt);
-        dw_bn_ = bf16_ ? choose_block_n(d_) : 0;
-        splits_cap_ = bf16_ ? choose_splits(d_, d_, static_cast<int>(R), dw_bn_) : 1;
+        splits_cap_ = bf16_ ? choose_dw(d_, d_, static_cast<int>(R), 16, comm_ == nullptr).splits : 1;
         col_chunks_cap_ = bf16_ ? colsum_chunks(R) : 1;
         // gradient buffers hold world equal shards when reduce-scattered (sharded streaming)
         const size_t grad_f = std::max(dd + d_, shardA_ / 4 * static_cast<size_t>(world_));
@@ -483,7 +482,8 @@ void Executor::compute_op(const Op& op, bool train, int64_t rows, int fmt) {
     g.ldo = d_;
     g.splits = fused ? 1 : splits_;
     g.split_stride = static_cast<int64_t>(dd);
-    g.block_n = 0;  // kernel variant chosen from the shape (choose_gemm)
+    g.cta = dw_cta_;  // variant and splits chosen together from the shape (choose_dw)
+    g.block_n = dw_bn_;
     g.lr = cur_lr_;
     gemm(g, st);
     if (fused) w16_layer_[s] = -1;
@@ -935,8 +935,10 @@ float Executor::train_step(const float* x, const float* target, int64_t rows, fl
     ensure_buffers(rows, 1, true, device_io);
     CUDA_OK(cudaSetDevice(cfg_.device));
     if (bf16_) {  // split-K depends only on (d, rows): identical for every window setting
-        const int want = choose_splits(d_, d_, static_cast<int>(rows), dw_bn_);
-        splits_ = effective_splits(static_cast<int>(rows), std::min(want, splits_cap_));
+        const DwChoice c = choose_dw(d_, d_, static_cast<int>(rows), splits_cap_, comm_ == nullptr);
+        splits_ = c.splits;
+        dw_cta_ = c.cta;
+        dw_bn_ = c.block_n;
         col_chunks_ = colsum_chunks(rows);
         dw_fused_ = comm_ == nullptr && splits_ == 1;
     }

@@ -161,7 +161,7 @@ private:
     const float* cur_t_ = nullptr;
     float cur_lr_ = 0.0f;
     double host_enqueue_ms_ = 0.0;
-    int splits_ = 1, dw_bn_ = 256, col_chunks_ = 1, splits_cap_ = 1, col_chunks_cap_ = 1;
+    int splits_ = 1, dw_bn_ = 256, dw_cta_ = 2, col_chunks_ = 1, splits_cap_ = 1, col_chunks_cap_ = 1;
     int loss_blocks_ = 0;
     bool dw_fused_ = true;  // bf16 dW: SGD fused into the GEMM epilogue (else split-K partials)
     // data parallel

@@ -70,6 +70,11 @@ GemmChoice choose_gemm(int M, int N, int K, int splits, int epilogue);
 cudaError_t gemm_bf16(const GemmProblem& p, cudaStream_t st);
 // Picks the split-K factor that best fills the 148 SMs for an M x N x K problem.
 int choose_splits(int M, int N, int K, int block_n);
+// dW kernel choice: variant and split-K count together (splits = 1 and fused_ok: SGD fused).
+struct DwChoice {
+    int cta, block_n, splits;
+};
+DwChoice choose_dw(int M, int N, int K, int max_splits, bool fused_ok);
 int choose_block_n(int N);
 // Split count actually used for K (no empty split): what gemm_bf16 will launch.
 int effective_splits(int K, int splits);

@@ -1219,6 +1219,44 @@ GemmChoice choose_gemm(int M, int N, int K, int splits, int epilogue) {
     return best;
 }
 
+// dW = x^T dz kernel choice, jointly over the variant and the split-K count: the busiest SM's
+// work (LPT load in tiles x tile width x K blocks per split) / calibrated per-SM rate, plus 2.5%
+// per extra split for the fp32 partial traffic. Calibrated on B200 (tools/dw_split_probe.py):
+// 16384 rows x d=1600 -> CTA pair, N=256, 3 splits (72.9 us, 1150 TFLOP/s; was 1-CTA N=192 with
+// 5 splits, 82.6 us); 65792 x 1280 -> pair, 256, 5 splits (161 us, 1337 TFLOP/s).
+// splits = 1 with fused_ok means the SGD is fused into the epilogue (no partials).
+DwChoice choose_dw(int M, int N, int K, int max_splits, bool fused_ok) {
+    const int sms = num_sms();
+    const int kb = (K + tc::BK - 1) / tc::BK;
+    DwChoice best{2, 256, 1};
+    double best_t = 1e300;
+    struct Cand {
+        int cta, bn;
+        double eff;
+    };
+    for (const Cand c : {Cand{2, 256, 0.95}, Cand{1, 256, 0.80}, Cand{1, 192, 0.80}, Cand{1, 128, 0.62}}) {
+        for (int s = 1; s <= 16 && s <= max_splits && s <= kb; ++s) {
+            if (s > 1 && kb / s < 8) break;  // keep >= 512 of K per split
+            if (effective_splits(K, s) != s) continue;
+            const long mt = (M + c.cta * tc::BM - 1) / (c.cta * tc::BM);
+            const long nt = (N + c.bn - 1) / c.bn;
+            const long tiles = mt * nt * s, slots = sms / c.cta;
+            double load = static_cast<double>((tiles + slots - 1) / slots);
+            const bool partials = s > 1 || !fused_ok;
+            if (c.cta == 2 && partials && tc::narrow_tiles(EPI_F32, c.bn, N - static_cast<int>(nt - 1) * c.bn)) {
+                const long R = mt * s;
+                load = pair_max_load(tiles - R, R, tiles < slots ? tiles : slots);
+            }
+            const double t = load * c.bn * ((kb + s - 1) / s) / c.eff * (1.0 + 0.025 * (s - 1));
+            if (t < best_t - 1e-9) {
+                best_t = t;
+                best = DwChoice{c.cta, c.bn, s};
+            }
+        }
+    }
+    return best;
+}
+
 int choose_block_n(int N) {
     // Widest tile whose padding wastes <= 10% of the columns: a 1-CTA M=128 MMA needs N >= 192
     // to keep its smem operand traffic under the ~128 B/clk/SM crossbar (measured on B200:
