@@ -10,7 +10,9 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsuperpipe.so")
+# SUPERPIPE_LIB selects another libsuperpipe build (A/B measurement of two builds of the same
+# ABI); there is no non-CUDA implementation to select.
+LIB_PATH = os.environ.get("SUPERPIPE_LIB") or os.path.join(HERE, "libsuperpipe.so")
 
 SP_OK, SP_ERR_INTERNAL, SP_ERR_INVALID, SP_ERR_OOM, SP_ERR_FIDELITY, SP_ERR_CUDA, \
     SP_ERR_NCCL, SP_ERR_STATE = range(8)
@@ -117,6 +119,8 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "sp_debug_shard_range": ([u64, i32, i32, C.POINTER(u64), C.POINTER(u64)], u64),
     }
     for name, (args, res) in sig.items():
+        if os.environ.get("SUPERPIPE_LIB") and not hasattr(lib, name):
+            continue  # A/B against an older build: bind what it has
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = res
