@@ -165,16 +165,27 @@ unsigned blocks_for(int64_t count, int threads) {
 
 }  // namespace
 
+// Rows are independent, so a row range larger than one grid's y extent (65535 blocks of kRows)
+// is launched in consecutive slices; each row's arithmetic is unchanged.
+constexpr int64_t kMaxRowsPerLaunch = 65535LL * kRows;
+
 void exact_forward(const float* x, const float* W, const float* b, int relu, float* y,
                    int64_t rows, int d, cudaStream_t st) {
-    dim3 grid((d + kCols - 1) / kCols, static_cast<unsigned>((rows + kRows - 1) / kRows));
-    exact_forward_kernel<<<grid, kCols, 0, st>>>(x, W, b, relu, y, rows, d);
+    for (int64_t r = 0; r < rows; r += kMaxRowsPerLaunch) {
+        const int64_t n = rows - r < kMaxRowsPerLaunch ? rows - r : kMaxRowsPerLaunch;
+        dim3 grid((d + kCols - 1) / kCols, static_cast<unsigned>((n + kRows - 1) / kRows));
+        exact_forward_kernel<<<grid, kCols, 0, st>>>(x + r * d, W, b, relu, y + r * d, n, d);
+    }
 }
 
 void exact_backward_dx(const float* dz, const float* W, const float* gate, float* dz_out,
                        int64_t rows, int d, cudaStream_t st) {
-    dim3 grid((d + kCols - 1) / kCols, static_cast<unsigned>((rows + kRows - 1) / kRows));
-    exact_dx_kernel<<<grid, kCols, 0, st>>>(dz, W, gate, dz_out, rows, d);
+    for (int64_t r = 0; r < rows; r += kMaxRowsPerLaunch) {
+        const int64_t n = rows - r < kMaxRowsPerLaunch ? rows - r : kMaxRowsPerLaunch;
+        dim3 grid((d + kCols - 1) / kCols, static_cast<unsigned>((n + kRows - 1) / kRows));
+        exact_dx_kernel<<<grid, kCols, 0, st>>>(dz + r * d, W, gate ? gate + r * d : nullptr,
+                                                dz_out + r * d, n, d);
+    }
 }
 
 void exact_backward_dw(const float* x, const float* dz, float* dW, float* db, int64_t rows,

@@ -445,3 +445,35 @@ def test_eager_prefetch_is_bitwise_and_same_ledger(numerics):
         assert np.array_equal(y, ref[0]) and loss == ref[1], key
         assert np.array_equal(W, ref[2]) and np.array_equal(b, ref[3]), key
         assert sf == ref[4] and stt == ref[5], key
+
+
+def test_exact_rows_beyond_one_launch_are_bitwise():
+    """600000 rows > 65535 row blocks of the exact kernels' grid: sliced launches, same bits."""
+    model = sp.build_model(29, 2, 16)
+    x = sp.make_input(29, 0, 600_000, 16)
+    r = sp.run_inference(model, [x], S(sp.SUPERPIPELINE, 2, 1), sp.ArenaConfig())
+    assert np.array_equal(r.outputs[0], ORC.forward(model.W, model.b, x))
+
+
+@pytest.mark.parametrize("rows", [1, 37, 1000])
+def test_bf16_ragged_and_single_row_batches(rows):
+    """M = 1 / ragged M tiles in the forward and dX GEMMs, ragged K (rows % 64 != 0) in dW:
+    within tolerance of the oracle and bit-identical across windows."""
+    d = 128
+    model = sp.build_model(31, 5, d, 1)
+    x, t = sp.make_input(31, 0, rows, d), sp.make_input(31, 1, rows, d)
+    ref = ORC.forward(model.W, model.b, x)
+    outs, trained = [], []
+    for s in [S(sp.SUPERPIPELINE, 2, 1), S(sp.STANDARD)]:
+        r = sp.run_inference(model, [x], s, sp.ArenaConfig(), numerics=sp.BF16)
+        outs.append(r.outputs[0])
+        rt = sp.run_train_step(model, x, t, s, sp.ArenaConfig(), sp.TrainConfig(0.05, False, rows),
+                               numerics=sp.BF16)
+        trained.append((rt.loss, rt.model.W, rt.model.b))
+    assert np.array_equal(outs[0], outs[1])
+    assert rel_err(outs[0], ref) <= BF16_FWD_TOL
+    assert trained[0][0] == trained[1][0] and np.array_equal(trained[0][1], trained[1][1])
+    loss, Wn, bn = ORC.train_step(model.W, model.b, x, t, 0.05, frozen=model.frozen)
+    assert abs(trained[0][0] - float(loss)) <= 2e-2 * abs(float(loss))
+    assert norm_err(trained[0][1][1:] - model.W[1:], Wn[1:] - model.W[1:]) <= BF16_UPD_TOL
+    assert norm_err(trained[0][2][1:] - model.b[1:], bn[1:] - model.b[1:]) <= BF16_UPD_TOL
