@@ -730,6 +730,18 @@ uint64_t Executor::call_signature(const Plan& plan, const CallIO& io) const {
 }
 
 void Executor::run_call(const Plan& plan, const CallIO& io) {
+    try {
+        run_call_impl(plan, io);
+    } catch (...) {
+        // A failed call may have overwritten ring slots part-way: nothing cached on the device
+        // can be trusted by the next call (the host master copy is the source of truth).
+        for (auto& c : cache_) c.valid = false;
+        std::fill(w16_layer_.begin(), w16_layer_.end(), -1);
+        throw;
+    }
+}
+
+void Executor::run_call_impl(const Plan& plan, const CallIO& io) {
     const size_t need = plan.ops.size();
     while (ev_done_.size() < need) {
         cudaEvent_t a, b, c;

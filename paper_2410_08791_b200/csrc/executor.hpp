@@ -89,6 +89,7 @@ private:
     Plan make_plan(bool train, int n_items, int64_t rows, int fmt);
     void enqueue_call(const Plan& plan, const CallIO& io);
     void run_call(const Plan& plan, const CallIO& io);
+    void run_call_impl(const Plan& plan, const CallIO& io);
     uint64_t call_signature(const Plan& plan, const CallIO& io) const;
     void enqueue_op(const Plan& plan, int i, bool train, int n_items, int64_t rows, float lr,
                     int fmt);
