@@ -477,3 +477,29 @@ def test_bf16_ragged_and_single_row_batches(rows):
     assert abs(trained[0][0] - float(loss)) <= 2e-2 * abs(float(loss))
     assert norm_err(trained[0][1][1:] - model.W[1:], Wn[1:] - model.W[1:]) <= BF16_UPD_TOL
     assert norm_err(trained[0][2][1:] - model.b[1:], bn[1:] - model.b[1:]) <= BF16_UPD_TOL
+
+
+@pytest.mark.parametrize("numerics", [sp.EXACT, sp.BF16])
+def test_identity_activation_layers(numerics):
+    """Activation::Identity blocks (model.hpp:11) mixed with ReLU ones, including an identity
+    last layer (the loss gradient is then not gated): exact is bitwise, bf16 within tolerance."""
+    n, d, rows = 6, 16 if numerics == sp.EXACT else 128, 5 if numerics == sp.EXACT else 384
+    model = sp.build_model(37, n, d, 1)
+    model.activation = np.array([sp.RELU, sp.IDENTITY, sp.RELU, sp.IDENTITY, sp.RELU, sp.IDENTITY],
+                                np.int32)
+    relu = (model.activation == sp.RELU).astype(np.int32)
+    x, t = sp.make_input(37, 0, rows, d), sp.make_input(37, 1, rows, d)
+    ref_y = ORC.forward(model.W, model.b, x, relu=relu)
+    loss, Wn, bn = ORC.train_step(model.W, model.b, x, t, 0.05, frozen=model.frozen, relu=relu)
+    for s in [S(sp.SUPERPIPELINE, 2, 1), S(sp.STANDARD)]:
+        y = sp.run_inference(model, [x], s, sp.ArenaConfig(), numerics=numerics).outputs[0]
+        r = sp.run_train_step(model, x, t, s, sp.ArenaConfig(), sp.TrainConfig(0.05, False, rows),
+                              numerics=numerics)
+        if numerics == sp.EXACT:
+            assert np.array_equal(y, ref_y), s
+            assert np.float32(r.loss).tobytes() == np.float32(loss).tobytes(), s
+            assert np.array_equal(r.model.W, Wn) and np.array_equal(r.model.b, bn), s
+        else:
+            assert rel_err(y, ref_y) <= BF16_FWD_TOL, s
+            assert abs(r.loss - float(loss)) <= 2e-2 * abs(float(loss)), s
+            assert norm_err(r.model.W[1:] - model.W[1:], Wn[1:] - model.W[1:]) <= BF16_UPD_TOL, s
