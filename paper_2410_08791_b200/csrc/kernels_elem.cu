@@ -7,6 +7,7 @@
 #include <cuda_bf16.h>
 
 #include "kernels.hpp"
+#include "pdl.cuh"
 
 namespace sp {
 namespace {
@@ -15,6 +16,7 @@ constexpr int kThreads = 256;
 
 __global__ void convert_kernel(const float* __restrict__ src, __nv_bfloat16* __restrict__ dst,
                                int64_t count) {
+    pdl_wait_then_release();
     const int64_t n4 = count / 4;
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n4; i += stride) {
@@ -59,6 +61,7 @@ __device__ __forceinline__ float grad_elem(float y, float t, float inv_n, int re
 __global__ void loss_grad_kernel(const float* __restrict__ y, const float* __restrict__ t,
                                  int64_t count, float inv_n, int relu,
                                  __nv_bfloat16* __restrict__ g, float* __restrict__ partials) {
+    pdl_wait_then_release();
     const int64_t n4 = count / 4;
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
     float acc = 0.0f;
@@ -86,6 +89,7 @@ __global__ void loss_grad_kernel(const float* __restrict__ y, const float* __res
 }
 
 __global__ void finalize_kernel(const float* __restrict__ partials, int n, float* __restrict__ out) {
+    pdl_wait_then_release();
     float acc = 0.0f;
     for (int i = threadIdx.x; i < n; i += blockDim.x) acc += partials[i];
     const float s = block_sum(acc);
@@ -102,6 +106,7 @@ constexpr int kColLanes = 8;
 __global__ void __launch_bounds__(256) colsum_kernel(const __nv_bfloat16* __restrict__ x,
                                                      int64_t rows, int d,
                                                      float* __restrict__ partials) {
+    pdl_wait_then_release();
     __shared__ float red[kColLanes][32][9];
     const int g = blockIdx.x * 32 + threadIdx.x;  // 8-column group
     const int lane_r = threadIdx.y;
@@ -147,6 +152,7 @@ __global__ void __launch_bounds__(256) colsum_kernel(const __nv_bfloat16* __rest
 
 __global__ void reduce_kernel(const float* __restrict__ parts, int nparts, int64_t stride,
                               int64_t count, float* __restrict__ grad) {
+    pdl_wait_then_release();
     const int64_t gs = static_cast<int64_t>(gridDim.x) * blockDim.x;
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += gs) {
         float s = parts[i];
@@ -157,6 +163,7 @@ __global__ void reduce_kernel(const float* __restrict__ parts, int nparts, int64
 
 __global__ void sgd_reduce_kernel(float* __restrict__ w, const float* __restrict__ parts,
                                   int nparts, int64_t stride, int64_t count, float lr) {
+    pdl_wait_then_release();
     const int64_t n4 = (stride % 4 == 0) ? count / 4 : 0;
     const int64_t gs = static_cast<int64_t>(gridDim.x) * blockDim.x;
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n4; i += gs) {
@@ -186,6 +193,7 @@ __global__ void __launch_bounds__(256) sgd_reduce_narrow_kernel(float* __restric
                                                                 const float* __restrict__ parts,
                                                                 int nparts, int64_t stride,
                                                                 int64_t count, float lr) {
+    pdl_wait_then_release();
     __shared__ float red[8][33];
     const int64_t j = static_cast<int64_t>(blockIdx.x) * 32 + threadIdx.x;
     float s = 0.0f;
@@ -201,6 +209,7 @@ __global__ void __launch_bounds__(256) sgd_reduce_narrow_kernel(float* __restric
 }
 
 __global__ void scale_kernel(float* __restrict__ x, int64_t count, float s) {
+    pdl_wait_then_release();
     const int64_t gs = static_cast<int64_t>(gridDim.x) * blockDim.x;
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += gs)
         x[i] *= s;
@@ -225,8 +234,8 @@ int num_sms() {
 }
 
 void convert_f32_to_bf16(const float* src, void* dst, int64_t count, cudaStream_t st) {
-    convert_kernel<<<grid_for(count / 4 + 1), kThreads, 0, st>>>(
-        src, static_cast<__nv_bfloat16*>(dst), count);
+    launch_pdl(convert_kernel, dim3(grid_for(count / 4 + 1)), dim3(kThreads), 0, st, src,
+               static_cast<__nv_bfloat16*>(dst), count);
 }
 
 int loss_grad_bf16(const float* y, const float* t, int64_t count, float inv_n, int relu,
@@ -234,13 +243,13 @@ int loss_grad_bf16(const float* y, const float* t, int64_t count, float inv_n, i
     // Fixed grid (a function of count only) => a fixed summation tree.
     const int64_t need = (count / 4 + kThreads) / kThreads;
     const int blocks = static_cast<int>(need < 1 ? 1 : (need < 1184 ? need : 1184));
-    loss_grad_kernel<<<blocks, kThreads, 0, st>>>(y, t, count, inv_n, relu,
-                                                  static_cast<__nv_bfloat16*>(g), partials);
+    launch_pdl(loss_grad_kernel, dim3(blocks), dim3(kThreads), 0, st, y, t, count, inv_n, relu,
+               static_cast<__nv_bfloat16*>(g), partials);
     return blocks;
 }
 
 void loss_finalize(const float* partials, int n, float* out, cudaStream_t st) {
-    finalize_kernel<<<1, kThreads, 0, st>>>(partials, n, out);
+    launch_pdl(finalize_kernel, dim3(1), dim3(kThreads), 0, st, partials, n, out);
 }
 
 int colsum_chunks(int64_t rows) { return static_cast<int>((rows + kColRows - 1) / kColRows); }
@@ -248,29 +257,30 @@ int colsum_chunks(int64_t rows) { return static_cast<int>((rows + kColRows - 1) 
 int colsum_bf16(const void* x, int64_t rows, int d, float* partials, cudaStream_t st) {
     const int chunks = colsum_chunks(rows);  // requires d % 8 == 0 (bf16 path: d % 64 == 0)
     dim3 grid((d / 8 + 31) / 32, chunks);
-    colsum_kernel<<<grid, dim3(32, kColLanes), 0, st>>>(static_cast<const __nv_bfloat16*>(x),
-                                                       rows, d, partials);
+    launch_pdl(colsum_kernel, grid, dim3(32, kColLanes), 0, st,
+               static_cast<const __nv_bfloat16*>(x), rows, d, partials);
     return chunks;
 }
 
 void reduce_partials(const float* parts, int nparts, int64_t stride, int64_t count,
                      float* grad, cudaStream_t st) {
-    reduce_kernel<<<grid_for(count), kThreads, 0, st>>>(parts, nparts, stride, count, grad);
+    launch_pdl(reduce_kernel, dim3(grid_for(count)), dim3(kThreads), 0, st, parts, nparts, stride,
+               count, grad);
 }
 
 void sgd_reduce(float* w, const float* parts, int nparts, int64_t stride, int64_t count,
                 float lr, cudaStream_t st) {
     if (count <= 65536 && nparts > 8) {  // short vector, many partials (bias from colsum)
-        sgd_reduce_narrow_kernel<<<static_cast<unsigned>((count + 31) / 32), dim3(32, 8), 0, st>>>(
-            w, parts, nparts, stride, count, lr);
+        launch_pdl(sgd_reduce_narrow_kernel, dim3(static_cast<unsigned>((count + 31) / 32)),
+                   dim3(32, 8), 0, st, w, parts, nparts, stride, count, lr);
         return;
     }
-    sgd_reduce_kernel<<<grid_for(count / 4 + 1), kThreads, 0, st>>>(w, parts, nparts, stride,
-                                                                     count, lr);
+    launch_pdl(sgd_reduce_kernel, dim3(grid_for(count / 4 + 1)), dim3(kThreads), 0, st, w, parts,
+               nparts, stride, count, lr);
 }
 
 void scale_inplace(float* x, int64_t count, float s, cudaStream_t st) {
-    scale_kernel<<<grid_for(count), kThreads, 0, st>>>(x, count, s);
+    launch_pdl(scale_kernel, dim3(grid_for(count)), dim3(kThreads), 0, st, x, count, s);
 }
 
 }  // namespace sp

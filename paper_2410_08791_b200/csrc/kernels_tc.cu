@@ -24,6 +24,7 @@
 #include <unordered_map>
 
 #include "kernels.hpp"
+#include "pdl.cuh"
 
 namespace sp {
 namespace tc {
@@ -459,6 +460,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    pdl_wait_then_release();  // prologue above overlaps the previous kernel's tail (pdl.cuh)
 
     const int tiles_mn = p.m_tiles * p.n_tiles;
     const int total = tiles_mn * p.splits;
@@ -735,6 +737,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     cluster_sync();
     fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    pdl_wait_then_release();  // prologue above overlaps the previous kernel's tail (pdl.cuh)
 
     const int m_tiles2 = (p.M + 2 * BM - 1) / (2 * BM);
     const PairSched sched(p, m_tiles2, blockIdx.x >> 1, gridDim.x >> 1);
@@ -1071,8 +1074,7 @@ cudaError_t launch(const GemmProblem& g, cudaStream_t st) {
     if (!make_epilogue_maps<EPI>(g, p.splits, &to, &tg)) return cudaErrorInvalidValue;
     const int total = p.m_tiles * p.n_tiles * p.splits;
     const int grid = total < num_sms() ? total : num_sms();
-    kern<<<grid, kThreads, C::SMEM, st>>>(ta, tb, to, tg, p);
-    return cudaGetLastError();
+    return launch_pdl(kern, dim3(grid), dim3(kThreads), C::SMEM, st, ta, tb, to, tg, p);
 }
 
 // 2-CTA launch: BN is the pair's N (each CTA stages BN/2 columns of B); grid = 2 x clusters.
@@ -1121,8 +1123,7 @@ cudaError_t launch2(const GemmProblem& g, cudaStream_t st) {
     const int total = p.m_tiles * p.n_tiles * p.splits;
     const int pairs = num_sms() / 2;
     const int grid = 2 * (total < pairs ? total : pairs);
-    kern<<<grid, kThreads, C::SMEM, st>>>(ta, tb, to, tg, p);
-    return cudaGetLastError();
+    return launch_pdl(kern, dim3(grid), dim3(kThreads), C::SMEM, st, ta, tb, to, tg, p);
 }
 
 // Picks the epilogue kind at run time; each kind is its own kernel instantiation.
