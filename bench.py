@@ -144,8 +144,9 @@ def measure_link(torch, mb=256):
 
 
 def gemm_kernel_timing(torch, capi, a, reps=20):
-    """Average device time per launch of the step's three tcgen05 GEMM shapes (forward
-    y = relu(xW + b), dX = (dz W^T) . [x > 0], dW exactly as the executor runs it: SGD fused
+    """Average device time per launch of the step's three tcgen05 GEMM shapes, each exactly as
+    the executor's bf16 training runs it (forward y = relu(xW + b) also writing the ReLU bit
+    mask, dX = (dz W^T) . [x > 0] gated by that mask, dW with its chosen variant: SGD fused
     into the epilogue when one split fills the SMs, else split-K fp32 partials), launched back
     to back on the current stream between two CUDA events, with operands of the step's exact
     shape."""
@@ -160,15 +161,17 @@ def gemm_kernel_timing(torch, capi, a, reps=20):
     parts = torch.empty(max(dw_splits, 1) * d * d, device="cuda") if dw_splits > 1 else W32
     bias = torch.randn(d, device="cuda")
     out = torch.empty(rows, d, device="cuda", dtype=torch.bfloat16)
+    # the executor's bf16 training gates dX with the ReLU bit mask its forward epilogue wrote
+    mask = torch.zeros(rows * d // 32, device="cuda", dtype=torch.int32)
     st = torch.cuda.current_stream().cuda_stream
     L = capi.LIB
     shapes = {
-        "fwd": (lambda: L.sp_debug_gemm_bf16_async(rows, d, d, x.data_ptr(), d, 0, W.data_ptr(), d,
-                                                   1, 0, out.data_ptr(), d, bias.data_ptr(), 1,
-                                                   None, 0, 1, 0, 0, st), a.layers),
-        "dx": (lambda: L.sp_debug_gemm_bf16_async(rows, d, d, dz.data_ptr(), d, 0, W.data_ptr(), d,
-                                                  0, 2, out.data_ptr(), d, None, 1, x.data_ptr(),
-                                                  d, 1, 0, 0, st), a.layers - 1),
+        "fwd": (lambda: L.sp_debug_gemm_bf16_masked_async(
+            rows, d, d, x.data_ptr(), d, 0, W.data_ptr(), d, 1, 0, out.data_ptr(), d,
+            bias.data_ptr(), 1, None, 0, 1, 0, 0, st, mask.data_ptr(), None), a.layers),
+        "dx": (lambda: L.sp_debug_gemm_bf16_masked_async(
+            rows, d, d, dz.data_ptr(), d, 0, W.data_ptr(), d, 0, 2, out.data_ptr(), d, None, 1,
+            x.data_ptr(), d, 1, 0, 0, st, None, mask.data_ptr()), a.layers - 1),
         "dw": (lambda: L.sp_debug_gemm_bf16_async(d, d, rows, x.data_ptr(), d, 1,
                                                   dz.data_ptr(), d, 1, 4 if dw_splits == 1 else 3,
                                                   parts.data_ptr(), d, None, 0, None, 0,

@@ -268,6 +268,41 @@ void sp_digest_tensors(const float* values, int32_t n_items, int64_t rows, int32
 #include "../../include/superpipe_debug.h"
 #include "kernels.hpp"
 
+extern "C" int sp_debug_gemm_bf16_masked_async(int32_t M, int32_t N, int32_t K, const void* A,
+                                               int32_t lda, int32_t a_mn, const void* B,
+                                               int32_t ldb, int32_t b_mn, int32_t epilogue,
+                                               void* out, int32_t ldo, const float* bias,
+                                               int32_t relu, const void* gate, int32_t ldg,
+                                               int32_t splits, int32_t block_n, int32_t cta,
+                                               void* stream, void* mask_out,
+                                               const void* gate_mask) {
+    sp::GemmProblem g;
+    g.M = M;
+    g.N = N;
+    g.K = K;
+    g.A = A;
+    g.lda = lda;
+    g.a_mn = a_mn != 0;
+    g.B = B;
+    g.ldb = ldb;
+    g.b_mn = b_mn != 0;
+    g.epilogue = epilogue;
+    g.out = out;
+    g.ldo = ldo;
+    g.bias = bias;
+    g.relu = relu;
+    g.gate = gate;
+    g.ldg = ldg;
+    g.splits = splits;
+    g.split_stride = static_cast<int64_t>(M) * ldo;
+    g.block_n = block_n;
+    g.cta = cta;
+    g.lr = 1.0f;
+    g.mask_out = static_cast<uint32_t*>(mask_out);
+    g.gate_mask = static_cast<const uint32_t*>(gate_mask);
+    return static_cast<int>(sp::gemm_bf16(g, static_cast<cudaStream_t>(stream)));
+}
+
 extern "C" int sp_debug_gemm_bf16_async(int32_t M, int32_t N, int32_t K, const void* A,
                                         int32_t lda, int32_t a_mn, const void* B, int32_t ldb,
                                         int32_t b_mn, int32_t epilogue, void* out, int32_t ldo,

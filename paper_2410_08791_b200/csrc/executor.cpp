@@ -258,9 +258,14 @@ void Executor::ensure_buffers(int64_t rows, int n_items, bool train, bool device
     xconv_ = alloc(act * 2);
     act_.clear();
     ba_.clear();
+    masks_.clear();
     if (tr) {
         tgt_ = static_cast<float*>(alloc(act * 4));
         for (int l = 0; l < n_; ++l) act_.push_back(alloc(act * elt));
+        masks_.clear();
+        if (bf16_ && !(cfg_.checkpointing && cfg_.strategy != SP_STANDARD) && d_ % 32 == 0)
+            for (int l = 0; l < n_; ++l)
+                masks_.push_back(static_cast<uint32_t*>(alloc(static_cast<size_t>(R) * (d_ / 32) * 4)));
         for (auto& g : gbuf_) g = alloc(act * elt);
         splits_cap_ = bf16_ ? choose_dw(d_, d_, static_cast<int>(R), 16, comm_ == nullptr).splits : 1;
         col_chunks_cap_ = bf16_ ? colsum_chunks(R) : 1;
@@ -419,6 +424,9 @@ void Executor::compute_op(const Op& op, bool train, int64_t rows, int fmt) {
         g.ldo = d_;
         g.bias = slot_b32(s);
         g.relu = relu_[L];
+        // ReLU bit mask of x_{L+1}: the backward's dX of layer L+1 gates with it instead of
+        // re-reading x_{L+1} (activation offload keeps the tensor gate: no mask buffers then)
+        if (!last && relu_[L] && !masks_.empty()) g.mask_out = masks_[static_cast<size_t>(L + 1)];
         gemm(g, st);
         return;
     }
@@ -450,6 +458,7 @@ void Executor::compute_op(const Op& op, bool train, int64_t rows, int fmt) {
             g.gate = xL;
             g.ldg = d_;
             g.relu = gate ? 1 : 0;
+            if (gate && !masks_.empty()) g.gate_mask = masks_[static_cast<size_t>(L)];
             gemm(g, st);
         }
     }

@@ -146,6 +146,7 @@ private:
     void* pp_[2] = {nullptr, nullptr};  // inference ping-pong activations
     void* xconv_ = nullptr;             // bf16 converted input
     std::vector<void*> act_;            // training saved inputs x_0..x_{n-1}
+    std::vector<uint32_t*> masks_;      // bf16 training: ReLU bit masks of x_1..x_{n-1} (no ckpt)
     void* gbuf_[2] = {nullptr, nullptr};  // dz ping-pong
     float* gws_[2] = {nullptr, nullptr};  // per-layer gradient workspaces (dW [+db] partials)
     float* grad_red_ = nullptr;           // reduced gradient (DP path)

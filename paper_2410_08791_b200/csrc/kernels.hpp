@@ -56,6 +56,12 @@ struct GemmProblem {
     int block_n = 0;  // 0 = choose (1-CTA: N per CTA; 2-CTA: N per CTA pair)
     float lr = 0.0f;  // EPI_SGD_F32
     int cta = 0;      // 0 = choose, 1 = one CTA per tile (M=128), 2 = CTA pair (M=256)
+    // EPI_BIAS_ACT_BF16 with relu: also write the ReLU mask of the stored output, one bit per
+    // element, mask_out[(col/32) * M + row] bit (col % 32) = !(bf16(y) <= 0) (column-chunk
+    // major, so one warp's 32 rows of a chunk are one 128-byte store / load).
+    uint32_t* mask_out = nullptr;
+    // EPI_GATE_BF16: gate with such a mask instead of reading the bf16 gate tensor.
+    const uint32_t* gate_mask = nullptr;
 };
 
 struct GemmChoice {

@@ -70,6 +70,8 @@ struct Params {
     long long split_stride;
     float lr;
     int narrow;  // 2-CTA: the ragged last N tile is computed with an MMA of N = BN/2
+    uint32_t* mask_out;         // EPI_BIAS_ACT_BF16: ReLU bit mask of the output (or nullptr)
+    const uint32_t* gate_mask;  // EPI_GATE_BF16: gate from a bit mask (or nullptr: gate tensor)
 };
 
 // ---------------------------------------------------------------------------------------
@@ -273,7 +275,7 @@ struct TileEpilogue {
     }
     // before the accumulator wait: the gate of the tile's first chunk starts loading
     __device__ __forceinline__ void begin_tile(const CUtensorMap* tmG, const Params& p, int row0, int n0) {
-        if (E::GATE && p.relu) gate_issue(tmG, row0, n0);
+        if (E::GATE && p.relu && !p.gate_mask) gate_issue(tmG, row0, n0);
     }
 
     __device__ __forceinline__ void chunk(const CUtensorMap* tmO, const Params& p, const uint32_t (&r)[32],
@@ -296,8 +298,22 @@ struct TileEpilogue {
 #pragma unroll
                 for (int i = 0; i < 32; ++i) v[i] = v[i] < 0.0f ? 0.0f : v[i];
             }
+            if (BASE == EPI_BIAS_ACT_BF16 && p.mask_out != nullptr && row < p.M) {
+                // bit i = !(stored bf16 value <= 0): exactly the dX gate's keep test on it
+                uint32_t bits = 0;
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                    bits |= (__bfloat162float(__float2bfloat16_rn(v[i])) <= 0.0f ? 0u : 1u) << i;
+                p.mask_out[static_cast<long long>(col0 / 32) * p.M + row] = bits;  // a warp: 128 B
+            }
         }
-        if (BASE == EPI_GATE_BF16 && p.relu) {
+        if (BASE == EPI_GATE_BF16 && p.relu && p.gate_mask != nullptr) {
+            const uint32_t bits =
+                row < p.M ? __ldg(p.gate_mask + static_cast<long long>(col0 / 32) * p.M + row) : 0u;
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+                if (!((bits >> i) & 1u)) v[i] = 0.0f;
+        } else if (BASE == EPI_GATE_BF16 && p.relu) {
             uint4 gv[4];
             if (E::GATE) {
                 const int b = gate_used & 1;
@@ -393,7 +409,8 @@ struct TileEpilogue {
             const int col0 = n0 + c * 32;
             tmem_ld32_async(tmem_acc + c * 32, ra);
             tmem_ld_wait(ra);
-            if (E::GATE && p.relu && c + 1 < CHUNKS && col0 + 32 < p.N) gate_issue(tmG, row0, col0 + 32);
+            if (E::GATE && p.relu && !p.gate_mask && c + 1 < CHUNKS && col0 + 32 < p.N)
+                gate_issue(tmG, row0, col0 + 32);
             if (col0 < p.N) chunk(tmO, p, ra, row0, col0, split);
         }
         release();
@@ -992,7 +1009,7 @@ bool make_epilogue_maps(const GemmProblem& g, int splits, CUtensorMap* to, CUten
         }
         if (!make_map(to, k)) return false;
     }
-    if (E::GATE && g.relu) {
+    if (E::GATE && g.relu && !g.gate_mask) {
         MapDesc k{};
         k.dtype = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
         k.rank = 2;
@@ -1069,6 +1086,8 @@ cudaError_t launch(const GemmProblem& g, cudaStream_t st) {
     p.split_stride = g.split_stride;
     p.lr = g.lr;
     p.narrow = 0;
+    p.mask_out = g.mask_out;
+    p.gate_mask = g.gate_mask;
     if ((EPI & (EPI_TMA - 1)) == EPI_SGD_F32 && p.splits != 1) return cudaErrorInvalidValue;
     CUtensorMap to, tg;
     if (!make_epilogue_maps<EPI>(g, p.splits, &to, &tg)) return cudaErrorInvalidValue;
@@ -1113,6 +1132,8 @@ cudaError_t launch2(const GemmProblem& g, cudaStream_t st) {
     p.ldg = g.ldg;
     p.split_stride = g.split_stride;
     p.lr = g.lr;
+    p.mask_out = g.mask_out;
+    p.gate_mask = g.gate_mask;
     {
         const int last = g.N - (p.n_tiles - 1) * BN;  // columns in the last N tile
         p.narrow = narrow_tiles(EPI & (EPI_TMA - 1), BN, last) ? 1 : 0;

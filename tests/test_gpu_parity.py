@@ -503,3 +503,35 @@ def test_identity_activation_layers(numerics):
             assert rel_err(y, ref_y) <= BF16_FWD_TOL, s
             assert abs(r.loss - float(loss)) <= 2e-2 * abs(float(loss)), s
             assert norm_err(r.model.W[1:] - model.W[1:], Wn[1:] - model.W[1:]) <= BF16_UPD_TOL, s
+
+
+@pytest.mark.parametrize("M,N,K", [(16384, 1600, 1600), (1000, 320, 192), (37, 128, 128)])
+def test_relu_bitmask_write_and_gate_are_exact(M, N, K):
+    """The forward epilogue's ReLU bit mask equals !(stored bf16 <= 0) bit for bit, and the dX
+    epilogue gated by that mask is bitwise the dX gated by the bf16 tensor."""
+    g = torch.Generator(device="cpu").manual_seed(M + N)
+    A = (torch.randn((M, K), generator=g) * 0.5).to(torch.bfloat16).cuda()
+    B = (torch.randn((K, N), generator=g) * 0.5).to(torch.bfloat16).cuda()   # N-major W
+    Bk = (torch.randn((N, K), generator=g) * 0.5).to(torch.bfloat16).cuda()  # K-major W
+    bias = torch.randn(N, generator=g).float().cuda()
+    y = torch.empty((M, N), dtype=torch.bfloat16, device="cuda")
+    mask = torch.zeros((N // 32, M), dtype=torch.int32, device="cuda")  # [N/32][M]
+    L = sp._capi.LIB
+    st = torch.cuda.current_stream().cuda_stream
+    assert L.sp_debug_gemm_bf16_masked_async(M, N, K, A.data_ptr(), K, 0, B.data_ptr(), N, 1, 0,
+                                             y.data_ptr(), N, bias.data_ptr(), 1, None, 0, 1, 0, 0,
+                                             st, mask.data_ptr(), None) == 0
+    torch.cuda.synchronize()
+    keep = (~(y.float() <= 0)).cpu().numpy().reshape(M, N // 32, 32)
+    want = (keep.astype(np.uint64) << np.arange(32, dtype=np.uint64)).sum(-1).astype(np.uint32)
+    assert np.array_equal(mask.cpu().numpy().view(np.uint32), want.T)
+    dz = (torch.randn((M, N), generator=g) * 0.5).to(torch.bfloat16).cuda()
+    outs = []
+    for gm in (None, mask.data_ptr()):
+        o = torch.empty((M, N), dtype=torch.bfloat16, device="cuda")
+        assert L.sp_debug_gemm_bf16_masked_async(M, N, N, dz.data_ptr(), N, 0, Bk.data_ptr(), N, 0, 2,
+                                                 o.data_ptr(), N, None, 1, y.data_ptr(), N, 1, 0, 0,
+                                                 st, None, gm) == 0
+        torch.cuda.synchronize()
+        outs.append(o.cpu())
+    assert torch.equal(outs[0], outs[1])
