@@ -257,6 +257,7 @@ struct TileEpilogue {
     uint64_t* gbar;   // their two mbarriers
     int lane;
     uint32_t out_n = 0, gate_issued = 0, gate_used = 0;
+    uint32_t mask_next = 0;  // ReLU bit-mask word of the next chunk (loaded one chunk ahead)
 
     __device__ __forceinline__ TileEpilogue(uint8_t* epi_smem, uint64_t* gate_bars, int q, int ln)
         : obuf(epi_smem + q * 2 * E::OUT_BUF),
@@ -273,13 +274,18 @@ struct TileEpilogue {
         }
         ++gate_issued;
     }
+    static constexpr bool kMaskGate = BASE == EPI_GATE_BF16;
+    __device__ __forceinline__ uint32_t mask_word(const Params& p, int row, int col0) const {
+        return row < p.M && col0 < p.N ? __ldg(p.gate_mask + static_cast<long long>(col0 / 32) * p.M + row) : 0u;
+    }
     // before the accumulator wait: the gate of the tile's first chunk starts loading
     __device__ __forceinline__ void begin_tile(const CUtensorMap* tmG, const Params& p, int row0, int n0) {
         if (E::GATE && p.relu && !p.gate_mask) gate_issue(tmG, row0, n0);
+        if (kMaskGate && p.relu && p.gate_mask) mask_next = mask_word(p, row0 + lane, n0);
     }
 
     __device__ __forceinline__ void chunk(const CUtensorMap* tmO, const Params& p, const uint32_t (&r)[32],
-                                          int row0, int col0, int split) {
+                                          int row0, int col0, int split, uint32_t gate_bits) {
         float v[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
@@ -298,21 +304,11 @@ struct TileEpilogue {
 #pragma unroll
                 for (int i = 0; i < 32; ++i) v[i] = v[i] < 0.0f ? 0.0f : v[i];
             }
-            if (BASE == EPI_BIAS_ACT_BF16 && p.mask_out != nullptr && row < p.M) {
-                // bit i = !(stored bf16 value <= 0): exactly the dX gate's keep test on it
-                uint32_t bits = 0;
-#pragma unroll
-                for (int i = 0; i < 32; ++i)
-                    bits |= (__bfloat162float(__float2bfloat16_rn(v[i])) <= 0.0f ? 0u : 1u) << i;
-                p.mask_out[static_cast<long long>(col0 / 32) * p.M + row] = bits;  // a warp: 128 B
-            }
         }
         if (BASE == EPI_GATE_BF16 && p.relu && p.gate_mask != nullptr) {
-            const uint32_t bits =
-                row < p.M ? __ldg(p.gate_mask + static_cast<long long>(col0 / 32) * p.M + row) : 0u;
 #pragma unroll
             for (int i = 0; i < 32; ++i)
-                if (!((bits >> i) & 1u)) v[i] = 0.0f;
+                if (!((gate_bits >> i) & 1u)) v[i] = 0.0f;
         } else if (BASE == EPI_GATE_BF16 && p.relu) {
             uint4 gv[4];
             if (E::GATE) {
@@ -355,15 +351,29 @@ struct TileEpilogue {
                     wp[i] = w;
                 }
             }
-        } else if (!E::TMA_OUT) {  // per-lane row stores straight to global
+            return;
+        }
+        uint32_t pk[16];  // the stored bf16 values, two per word
+        if (E::OUT_ELT == 2) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) pk[i] = pack_bf16(v[2 * i], v[2 * i + 1]);
+            if (BASE == EPI_BIAS_ACT_BF16 && p.relu && p.mask_out != nullptr && row < p.M) {
+                // ReLU bit mask of the stored values: after ReLU a value is +-0, > 0 or NaN, so
+                // !(x <= 0) is exactly "magnitude bits nonzero" — the dX gate's keep test
+                uint32_t bits = 0;
+#pragma unroll
+                for (int i = 0; i < 16; ++i)
+                    bits |= ((pk[i] & 0x7FFFu) ? 1u : 0u) << (2 * i) | ((pk[i] & 0x7FFF0000u) ? 1u : 0u) << (2 * i + 1);
+                p.mask_out[static_cast<long long>(col0 / 32) * p.M + row] = bits;  // a warp: 128 B
+            }
+        }
+        if (!E::TMA_OUT) {  // per-lane row stores straight to global
             if (row >= p.M) return;
             if (E::OUT_ELT == 2) {
                 uint4* op = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.out) +
                                                      static_cast<long long>(row) * p.ldo + col0);
 #pragma unroll
-                for (int i = 0; i < 4; ++i)
-                    op[i] = make_uint4(pack_bf16(v[8 * i + 0], v[8 * i + 1]), pack_bf16(v[8 * i + 2], v[8 * i + 3]),
-                                       pack_bf16(v[8 * i + 4], v[8 * i + 5]), pack_bf16(v[8 * i + 6], v[8 * i + 7]));
+                for (int i = 0; i < 4; ++i) op[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
             } else {
                 float4* op = reinterpret_cast<float4*>(static_cast<float*>(p.out) +
                                                        (BASE == EPI_F32 ? split * p.split_stride : 0LL) +
@@ -379,8 +389,7 @@ struct TileEpilogue {
 #pragma unroll
                 for (int i = 0; i < 4; ++i)
                     *reinterpret_cast<uint4*>(ob + swz<64>(lane, i)) =
-                        make_uint4(pack_bf16(v[8 * i + 0], v[8 * i + 1]), pack_bf16(v[8 * i + 2], v[8 * i + 3]),
-                                   pack_bf16(v[8 * i + 4], v[8 * i + 5]), pack_bf16(v[8 * i + 6], v[8 * i + 7]));
+                        make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
             } else {
 #pragma unroll
                 for (int i = 0; i < 8; ++i)
@@ -411,7 +420,10 @@ struct TileEpilogue {
             tmem_ld_wait(ra);
             if (E::GATE && p.relu && !p.gate_mask && c + 1 < CHUNKS && col0 + 32 < p.N)
                 gate_issue(tmG, row0, col0 + 32);
-            if (col0 < p.N) chunk(tmO, p, ra, row0, col0, split);
+            const uint32_t mask_cur = mask_next;
+            if (kMaskGate && p.relu && p.gate_mask && c + 1 < CHUNKS)
+                mask_next = mask_word(p, row0 + lane, col0 + 32);
+            if (col0 < p.N) chunk(tmO, p, ra, row0, col0, split, mask_cur);
         }
         release();
     }
