@@ -184,3 +184,55 @@ def test_shard_ranges_tile_every_slot_image(d, world):
             assert lo.value == covered or hi.value == lo.value
             covered = max(covered, hi.value)
         assert covered == img
+
+
+def test_plan_standard_one_prologue_never_evicts():
+    # test_scheduler.cpp:73-107: one full prologue of every layer, no eviction, and a second
+    # pass (training backward) computes from the resident copies without a new prologue.
+    for train in (False, True):
+        head, ops = parse_plan(sp.describe_plan(3, 16, sp.StrategyConfig(STANDARD), train=train))
+        h2d = [o for o in ops if o["kind"] == "H2D"]
+        assert len(h2d) == 1 and h2d[0]["layers"] == [0, 1, 2] and ops[0] is h2d[0]
+        assert int(head["evictions"]) == 0 and int(head["slots"]) == 3
+
+
+def test_plan_naive_strict_load_compute_evict_phases():
+    # test_scheduler.cpp:122-161: Naive(2) on 4 layers loads {0,1}, computes both, then (and
+    # only then) loads {2,3} into the freed slots.
+    head, ops = parse_plan(sp.describe_plan(4, 16, sp.StrategyConfig(NAIVE, 2)))
+    assert [o["kind"] for o in ops] == ["H2D", "COMPUTE", "COMPUTE", "H2D", "COMPUTE", "COMPUTE"]
+    assert ops[0]["layers"] == [0, 1] and ops[3]["layers"] == [2, 3]
+    assert {1, 2} <= set(ops[3]["deps"])  # both computes of the first group precede the load
+    assert int(head["slots"]) == 2 and int(head["evictions"]) == 4
+
+
+def test_plan_superpipeline_evicts_final_partial_group():
+    # test_scheduler.cpp:196-217: SP(2,1) on 3 layers evicts every layer, the last one after the
+    # stream ends; the ring never holds more than k + k' = 3 layers. Every computed position is
+    # released once (the reference's evictions); real copies can be fewer, since a layer still
+    # valid in a released slot is claimed without one.
+    head, ops = parse_plan(sp.describe_plan(3, 16, sp.StrategyConfig(SUPERPIPELINE, 2, 1)))
+    assert int(head["evictions"]) == 3
+    for n, k, kp, items in [(8, 4, 2, 1), (12, 2, 1, 3), (9, 5, 3, 2)]:
+        head, ops = parse_plan(sp.describe_plan(n, 16, sp.StrategyConfig(SUPERPIPELINE, k, kp),
+                                                n_items=items))
+        assert int(head["evictions"]) == n * items
+        loaded = sum(len(o["layers"]) for o in ops if o["kind"] == "H2D")
+        assert loaded <= n * items
+        assert int(head["slots"]) == min(k + kp, n)
+
+
+@pytest.mark.parametrize("train,ckpt", [(False, False), (True, False), (True, True)])
+def test_plan_ledger_peaks_are_per_tag_maxima(train, ckpt):
+    # test_arena.cpp:57-118: per-tag peaks track each tag independently and agree with a shadow
+    # ledger — here the per-op ledger snapshots (led=w,a,g) of the plan.
+    for s in [sp.StrategyConfig(STANDARD), sp.StrategyConfig(NAIVE, 2),
+              sp.StrategyConfig(SUPERPIPELINE, 3, 1), sp.StrategyConfig(SUPERPIPELINE, 4, 2)]:
+        head, ops = parse_plan(sp.describe_plan(7, 16, s, n_items=1 if train else 2, train=train,
+                                                checkpointing=ckpt, frozen=[1, 0, 0, 0, 0, 0, 0]))
+        led = [o["led"] for o in ops if "led" in o]
+        assert int(head["peak_w"]) == max(w for w, a, g in led)
+        assert int(head["peak_a"]) == max(a for w, a, g in led)
+        assert int(head["peak_g"]) == max(g for w, a, g in led)
+        assert int(head["peak"]) >= max(w + a + g for w, a, g in led)
+        assert int(head["peak"]) <= int(head["peak_w"]) + int(head["peak_a"]) + int(head["peak_g"])
