@@ -236,3 +236,76 @@ def test_plan_ledger_peaks_are_per_tag_maxima(train, ckpt):
         assert int(head["peak_g"]) == max(g for w, a, g in led)
         assert int(head["peak"]) >= max(w + a + g for w, a, g in led)
         assert int(head["peak"]) <= int(head["peak_w"]) + int(head["peak_a"]) + int(head["peak_g"])
+
+
+def test_plan_summary_against_the_reference_library():
+    """The static plan's ledger against the reference engine itself (oracle/_ref) over random
+    inference configs: peaks equal whenever the window does not wrap (k + k' <= n); for
+    wrapping windows the reference's virtual-clock peak <= ours <= the analytic bound; and the
+    executor never copies more than the reference (slot reuse only removes transfers)."""
+    ref = Reference()
+    rng = np.random.default_rng(5)
+    checked = 0
+    for _ in range(200):
+        n, d, items = int(rng.integers(1, 10)), 8, int(rng.integers(1, 4))
+        kind = [STANDARD, NAIVE, SUPERPIPELINE][int(rng.integers(0, 3))]
+        if kind == SUPERPIPELINE:
+            if n < 2:
+                continue
+            k = int(rng.integers(2, n + 1))
+            kp = int(rng.integers(1, k))
+        elif kind == NAIVE:
+            k, kp = int(rng.integers(1, n + 1)), 0
+        else:
+            k = kp = 0
+        mode = [BATCH, SEQUENTIAL][int(rng.integers(0, 2))]
+        W, b, _ = ref.build_model(3, n, d)
+        xs = np.stack([ref.make_input(3, i, 1, d) for i in range(items)])
+        rc, _, s = ref.run_inference(W, b, xs, kind, k, kp, mode, 1 << 30)
+        head, _ = parse_plan(sp.describe_plan(n, d, sp.StrategyConfig(kind, k, kp, mode), n_items=items))
+        peak_w = int(head["peak_w"])
+        if kind == SUPERPIPELINE and k + kp > n:
+            bound = sp.peak_weight_residency(sp.StrategyConfig(kind, k, kp, mode), n, (d * d + d) * 4)
+            assert s.peak_weight_bytes <= peak_w <= bound
+        else:
+            assert peak_w == s.peak_weight_bytes and int(head["peak"]) == s.peak_bytes
+        assert int(head["h2d_jobs"]) <= s.n_transfers_h2d
+        checked += 1
+    assert checked > 150
+
+
+def test_training_plan_ledger_equals_the_reference_library():
+    """Training ledger against the reference engine (oracle/_ref), one row (describe_plan sizes
+    activations for one row): every peak and the gradient total are EQUAL for all strategies,
+    frozen prefixes and transfer modes whenever no activation is offloaded and the window does
+    not wrap (k + k' < n). Outside that region the reference's own peaks depend on its
+    simulated rates, so there is no timing-free value to match."""
+    ref = Reference()
+    rng = np.random.default_rng(11)
+    checked = 0
+    for _ in range(300):
+        n, d = int(rng.integers(1, 9)), 8
+        kind = [STANDARD, NAIVE, SUPERPIPELINE][int(rng.integers(0, 3))]
+        if kind == SUPERPIPELINE:
+            if n < 3:
+                continue
+            k = int(rng.integers(2, n))
+            kp = int(rng.integers(1, min(k, n - k + 1)))
+            if k + kp >= n:
+                continue
+        elif kind == NAIVE:
+            k, kp = int(rng.integers(1, n + 1)), 0
+        else:
+            k = kp = 0
+        mode = [BATCH, SEQUENTIAL][int(rng.integers(0, 2))]
+        fp = int(rng.integers(0, n + 1))
+        W, b, fz = ref.build_model(3, n, d, fp)
+        x, t = ref.make_input(3, 0, 1, d), ref.make_input(3, 1, 1, d)
+        rc, _, _, s = ref.run_train_step(W, b, x, t, 0.01, kind, k, kp, mode, 1 << 30, frozen=fz)
+        head, _ = parse_plan(sp.describe_plan(n, d, sp.StrategyConfig(kind, k, kp, mode), train=True,
+                                              frozen=list(fz)))
+        got = [int(head[key]) for key in ("peak", "peak_w", "peak_a", "peak_g", "total_g")]
+        assert got == [s.peak_bytes, s.peak_weight_bytes, s.peak_activation_bytes,
+                       s.peak_gradient_bytes, s.total_gradient_bytes], (kind, n, k, kp, mode, fp)
+        checked += 1
+    assert checked > 150
