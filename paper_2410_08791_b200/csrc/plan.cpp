@@ -173,10 +173,21 @@ private:
     void ledger_sub(int tag, uint64_t bytes) { tag_[tag] -= std::min(tag_[tag], bytes); }
     // Evictions free their bytes when the D2H completes in the reference
     // (engine.cpp:390-405), i.e. while the next compute is already running.
-    void defer_free(int tag, uint64_t bytes) { deferred_.push_back({tag, bytes}); }
+    void defer_free(int tag, uint64_t bytes, int slot = -1) { deferred_.push_back({tag, bytes, slot}); }
     void flush_deferred() {
-        for (auto [tag, bytes] : deferred_) ledger_sub(tag, bytes);
+        for (const auto& f : deferred_) ledger_sub(f.tag, f.bytes);
         deferred_.clear();
+    }
+    // A claim of a released slot whose eviction has not drained yet: in the reference the layer
+    // has a single placement, so it is never counted twice — the pending free is cancelled and
+    // the layer stays counted once (instead of being added again).
+    bool cancel_pending_free(int slot) {
+        for (auto it = deferred_.begin(); it != deferred_.end(); ++it)
+            if (it->tag == kWeight && it->slot == slot) {
+                deferred_.erase(it);
+                return true;
+            }
+        return false;
     }
 
     // ---- slot choice -------------------------------------------------------------------
@@ -263,7 +274,7 @@ private:
             slots_[s].refs = 1;
             pos_slot_[q] = s;
             pos_load_[q] = slots_[s].fill_op;
-            ledger_add(kWeight, in_.layer_bytes);
+            if (miss || !cancel_pending_free(s)) ledger_add(kWeight, in_.layer_bytes);
             const bool act = backward() && ckpt_;
             if (act) ledger_add(kActivation, in_.act_bytes);
             if (miss || act) moves.push_back({q, s, miss, act});
@@ -329,7 +340,7 @@ private:
             plan_.n_evictions += 1;
             if (--slots_[s].refs == 0) {
                 slots_[s].stamp = ++stamp_;
-                defer_free(kWeight, in_.layer_bytes);
+                defer_free(kWeight, in_.layer_bytes, s);
                 if (!backward() && in_.train && ckpt_)
                     defer_free(kActivation, in_.act_bytes);  // offloaded with the layer
             }
@@ -475,7 +486,12 @@ private:
     bool ckpt_ = false;
     uint64_t stamp_ = 0;
     uint64_t tag_[3] = {0, 0, 0};
-    std::vector<std::pair<int, uint64_t>> deferred_;
+    struct PendingFree {
+        int tag;
+        uint64_t bytes;
+        int slot;  // weight frees: the released slot
+    };
+    std::vector<PendingFree> deferred_;
 };
 
 }  // namespace
