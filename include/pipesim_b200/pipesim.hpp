@@ -381,4 +381,39 @@ inline RunResult run_train_step(const LayeredModel& model, const Tensor& x, cons
     return r;
 }
 
+// engine.hpp:55-62 (engine.cpp:583-592): recompute the reference forward of every input and
+// compare bitwise. The recomputation is the executor's exact numerics, which reproduce
+// reference_forward bit for bit on the GPU (a Superpipeline(2,1) ring, so any model fits).
+struct FidelityResult {
+    bool ok = false;
+    std::string digest;
+};
+
+inline FidelityResult verify_fidelity(const std::vector<Tensor>& outputs, const LayeredModel& model,
+                                      const std::vector<Tensor>& inputs) {
+    FidelityResult result;
+    result.digest = digest_tensors(outputs);
+    if (outputs.size() != inputs.size()) return result;
+    const Numerics saved = detail::numerics();
+    detail::numerics() = Numerics::Exact;
+    const StrategyConfig ring = model.n_layers >= 2
+                                    ? StrategyConfig{StrategyKind::Superpipeline, 2, 1, TransferMode::Batch}
+                                    : StrategyConfig{StrategyKind::Standard, 0, 0, TransferMode::Batch};
+    try {
+        for (std::size_t i = 0; i < inputs.size(); ++i) {
+            const RunResult ref = run_inference(model, {inputs[i]}, ring, ArenaConfig{});
+            if (!(ref.outputs[0] == outputs[i])) {
+                detail::numerics() = saved;
+                return result;
+            }
+        }
+    } catch (...) {
+        detail::numerics() = saved;
+        throw;
+    }
+    detail::numerics() = saved;
+    result.ok = true;
+    return result;
+}
+
 }  // namespace pipesim

@@ -144,6 +144,26 @@ TEST_CASE("all strategies produce bitwise-identical outputs and digests [gpu]") 
     }
 }
 
+TEST_CASE("verify_fidelity flags a single perturbed bit [gpu]") {
+    // test_engine.cpp:120-127
+    LayeredModel model = build_model(5, 2, 3, 0);
+    auto inputs = make_inputs(5, 1, 1, 3);
+    RunResult r = run_inference(model, inputs, strat(StrategyKind::Standard), roomy_arena());
+    CHECK(verify_fidelity(r.outputs, model, inputs).ok);
+    CHECK(verify_fidelity(r.outputs, model, inputs).digest == r.summary.output_digest);
+    r.outputs[0].values[0] = std::nextafter(r.outputs[0].values[0], 1e30f);
+    CHECK(!verify_fidelity(r.outputs, model, inputs).ok);
+    // a bf16 run is not bit-faithful to the reference: verify_fidelity says so
+    set_numerics(Numerics::Bf16);
+    LayeredModel wide = build_model(5, 3, 64, 0);
+    auto xs = make_inputs(5, 2, 16, 64);
+    RunResult rb = run_inference(wide, xs, strat(StrategyKind::Superpipeline, 2, 1), roomy_arena());
+    set_numerics(Numerics::Exact);
+    CHECK(!verify_fidelity(rb.outputs, wide, xs).ok);
+    CHECK(verify_fidelity(run_inference(wide, xs, strat(StrategyKind::Standard), roomy_arena()).outputs,
+                          wide, xs).ok);
+}
+
 TEST_CASE("train step is bitwise-faithful for every strategy and option [gpu]") {
     for (int frozen_prefix : {0, 2, 4}) {
         LayeredModel ref = build_model(7, 4, 5, frozen_prefix);

@@ -535,3 +535,20 @@ def test_relu_bitmask_write_and_gate_are_exact(M, N, K):
         torch.cuda.synchronize()
         outs.append(o.cpu())
     assert torch.equal(outs[0], outs[1])
+
+
+def test_verify_fidelity_flags_a_single_perturbed_bit():
+    # test_engine.cpp:120-127, on the Python mirror
+    model = sp.build_model(5, 2, 3)
+    xs = inputs(5, 1, 1, 3)
+    r = sp.run_inference(model, xs, S(sp.STANDARD), sp.ArenaConfig(1 << 30))
+    f = sp.verify_fidelity(r.outputs, model, xs)
+    assert f.ok and f.digest == r.summary["output_digest"]
+    bad = [o.copy() for o in r.outputs]
+    bad[0].flat[0] = np.nextafter(bad[0].flat[0], np.float32(1e30))
+    assert not sp.verify_fidelity(bad, model, xs).ok
+    assert not sp.verify_fidelity(r.outputs[:0], model, xs).ok  # count mismatch
+    wide = sp.build_model(5, 3, 64)
+    xw = inputs(5, 2, 16, 64)
+    rb = sp.run_inference(wide, xw, S(sp.SUPERPIPELINE, 2, 1), sp.ArenaConfig(), numerics=sp.BF16)
+    assert not sp.verify_fidelity(rb.outputs, wide, xw).ok  # bf16 is not bit-faithful
