@@ -552,3 +552,25 @@ def test_verify_fidelity_flags_a_single_perturbed_bit():
     xw = inputs(5, 2, 16, 64)
     rb = sp.run_inference(wide, xw, S(sp.SUPERPIPELINE, 2, 1), sp.ArenaConfig(), numerics=sp.BF16)
     assert not sp.verify_fidelity(rb.outputs, wide, xw).ok  # bf16 is not bit-faithful
+
+
+def test_repeated_runs_yield_identical_plans_traces_and_summaries():
+    """test_engine.cpp:331-339 on a real executor: everything but the measured times repeats
+    exactly — outputs, the op plan, the trace rows (kind, layers, bytes, op order; stall rows
+    are measured gaps) and every non-time summary field."""
+    model = sp.build_model(15, 6, 4)
+    xs = inputs(15, 2, 2, 4)
+    s = S(sp.SUPERPIPELINE, 3, 2)
+    runs = []
+    for _ in range(2):
+        with sp.Executor(6, 4, s) as ex:
+            ex.register_model(model)
+            y = ex.forward(np.stack(xs))
+            st = ex.stats()
+            tr = [{k: v for k, v in e.items() if k not in ("t_start", "t_end")} for e in ex.trace()
+                  if e["kind"] != "Stall"]  # stall rows are measured gaps
+            runs.append((y, ex.last_plan(), tr,
+                         {k: v for k, v in st.items()
+                          if not k.endswith("_ms") and k not in ("hbm_reserved_bytes", "graph_replays")}))
+    (ya, pa, ta, sa), (yb, pb, tb, sb) = runs
+    assert np.array_equal(ya, yb) and pa == pb and ta == tb and sa == sb
