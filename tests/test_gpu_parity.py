@@ -574,3 +574,17 @@ def test_repeated_runs_yield_identical_plans_traces_and_summaries():
                           if not k.endswith("_ms") and k not in ("hbm_reserved_bytes", "graph_replays")}))
     (ya, pa, ta, sa), (yb, pb, tb, sb) = runs
     assert np.array_equal(ya, yb) and pa == pb and ta == tb and sa == sb
+
+
+@pytest.mark.parametrize("numerics", [sp.EXACT, sp.BF16])
+def test_training_reduces_the_loss(numerics):
+    """test_model.cpp:178-185 through the executor: consecutive SGD steps on the same batch
+    lower the MSE loss (both numerics; the slot cache and graph replay carry the updated
+    weights from step to step)."""
+    d, rows = (16, 8) if numerics == sp.EXACT else (128, 512)
+    model = sp.build_model(41, 4, d)
+    x, t = sp.make_input(41, 0, rows, d), sp.make_input(41, 1, rows, d)
+    with sp.Executor(4, d, S(sp.SUPERPIPELINE, 2, 1), numerics=numerics) as ex:
+        ex.register_model(model)
+        losses = [ex.train_step(x, t, 0.5) for _ in range(4)]
+    assert all(b < a for a, b in zip(losses, losses[1:])), losses
