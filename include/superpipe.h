@@ -174,6 +174,24 @@ int sp_set_item_batching(sp_exec* ex, int32_t on);
  * bitwise-identical results; 1 keeps the link busier (copies are not held behind a
  * copy -> compute -> copy round trip). */
 int sp_set_eager_prefetch(sp_exec* ex, int32_t on);
+
+/* ---- optimizer ------------------------------------------------------------------------ */
+/* The reference trains with plain SGD (apply_sgd, model.cpp:150-155): SP_OPT_SGD, the default.
+ * SP_OPT_ADAMW is PyTorch's AdamW (decoupled weight decay) on the fp32 master weights. Its
+ * state m, v lives in pinned host memory next to the weights and streams with every
+ * trainable layer's backward: H2D with the layer (even when its weights are still resident),
+ * updated in place by one fused kernel (split-K gradient reduction + AdamW), written back
+ * with the weights. Each operation is separately rounded in a fixed order (oracle.h
+ * orc_adamw), so SP_NUMERICS_EXACT is bit-reproducible. Setting the optimizer zeroes the
+ * state and the step count. In sharded data parallel each rank streams and updates only
+ * its shard of m, v. */
+#define SP_OPT_SGD 0
+#define SP_OPT_ADAMW 1
+int sp_set_optimizer(sp_exec* ex, int32_t kind, float beta1, float beta2, float eps,
+                     float weight_decay);
+/* Current AdamW state of one layer (m and v of W[d*d] and b[d]); any pointer may be NULL. */
+int sp_read_optimizer_state(sp_exec* ex, int32_t index, float* mW, float* mb, float* vW,
+                            float* vb);
 /* Copies up to cap events of the last call's measured timeline; *count = total rows. */
 int sp_get_trace(const sp_exec* ex, sp_trace_event* events, int32_t cap, int32_t* count);
 
@@ -208,9 +226,11 @@ int sp_validate_strategy(int32_t strategy, int32_t k, int32_t k_prime, int32_t n
 /* Describes the static op plan the executor would run (policy_step, scheduler.cpp:53-141,
  * resolved ahead of time) as text, one op per line; returns the needed length. Host-only.
  * flags: SP_PLAN_SHARDED (data-parallel sharded streaming), SP_PLAN_EAGER (eager prefetch
- * dependencies, see sp_set_eager_prefetch). */
+ * dependencies, see sp_set_eager_prefetch), SP_PLAN_OPTSTATE (an optimizer with state, e.g.
+ * AdamW: its m, v stream with each trainable layer's backward). */
 #define SP_PLAN_SHARDED 1
 #define SP_PLAN_EAGER 2
+#define SP_PLAN_OPTSTATE 4
 int64_t sp_describe_plan(const sp_config* cfg, int32_t n_items, int32_t train,
                          const int32_t* frozen, int32_t flags, char* buf, int64_t cap);
 /* Deterministic layer / input generators of the reference (host-only), so callers can

@@ -124,6 +124,20 @@ void orc_apply_sgd(float* w, const float* g, int64_t count, float lr) {  /* :150
     for (int64_t i = 0; i < count; ++i) w[i] -= lr * g[i];
 }
 
+void orc_adamw(int64_t count, float* w, float* m, float* v, const float* g, float decay,
+               float omb1, float b2, float omb2, float bc2_sqrt, float eps, float neg_step) {
+    for (int64_t i = 0; i < count; ++i) {
+        const float gi = g[i];
+        const float wi = w[i] * decay;
+        const float mi = m[i] + omb1 * (gi - m[i]);
+        const float vi = v[i] * b2 + (omb2 * gi) * gi;
+        const float denom = sqrtf(vi) / bc2_sqrt + eps;
+        w[i] = wi + neg_step * (mi / denom);
+        m[i] = mi;
+        v[i] = vi;
+    }
+}
+
 void orc_forward(int n_layers, int d, const float* W, const float* b, const int* relu,
                  const float* x, int64_t rows, float* y) {  /* model.cpp:125-129 */
     const int64_t count = rows * (int64_t)d;

@@ -46,6 +46,17 @@ void orc_mse_grad(const float* y, const float* t, int64_t count, float* g);
 /* apply_sgd — model.cpp:150-155 (caller skips frozen blocks). */
 void orc_apply_sgd(float* w, const float* g, int64_t count, float lr);
 
+/* AdamW step (no reference counterpart: the reference trains with apply_sgd). Restates
+ * PyTorch's single-tensor AdamW (torch/optim/adamw.py, decoupled weight decay) with every
+ * operation separately rounded, in this order:
+ *   w *= decay;  m += omb1 * (g - m);  v = v * b2 + (omb2 * g) * g;
+ *   w += neg_step * (m / (sqrt(v) / bc2_sqrt + eps))
+ * with decay = 1 - lr*wd, omb1 = 1 - b1, omb2 = 1 - b2, neg_step = -lr / (1 - b1^t),
+ * bc2_sqrt = sqrt(1 - b2^t), each computed in double and rounded to float once (as PyTorch
+ * does with its Python-float scalars). Pinned against torch.optim.AdamW in tests/. */
+void orc_adamw(int64_t count, float* w, float* m, float* v, const float* g, float decay,
+               float omb1, float b2, float omb2, float bc2_sqrt, float eps, float neg_step);
+
 /* reference_forward — model.cpp:125-129. relu: per-layer flags (NULL = all ReLU). */
 void orc_forward(int n_layers, int d, const float* W, const float* b, const int* relu,
                  const float* x, int64_t rows, float* y);

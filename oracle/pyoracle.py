@@ -51,7 +51,26 @@ class Oracle:
         lib.orc_digest_tensors.restype = u64
         lib.orc_digest_train.argtypes = [C.c_float, C.c_int, C.c_int, _F32P, _F32P]
         lib.orc_digest_train.restype = u64
+        f = C.c_float
+        lib.orc_adamw.argtypes = [i64, _F32P, _F32P, _F32P, _F32P, f, f, f, f, f, f, f]
         self.lib = lib
+
+    @staticmethod
+    def adamw_scalars(lr, beta1, beta2, eps, weight_decay, step):
+        """The float scalars of step `step` (1-based), computed in double and rounded once."""
+        f = lambda v: float(np.float32(v))  # noqa: E731
+        return dict(decay=f(1.0 - lr * weight_decay), omb1=f(1.0 - beta1), b2=f(beta2),
+                    omb2=f(1.0 - beta2), bc2_sqrt=f(np.sqrt(1.0 - beta2 ** step)), eps=f(eps),
+                    neg_step=f(-lr / (1.0 - beta1 ** step)))
+
+    def adamw(self, w, m, v, g, lr, beta1, beta2, eps, weight_decay, step):
+        """One AdamW step in place on float32 arrays w, m, v (orc_adamw)."""
+        s = self.adamw_scalars(lr, beta1, beta2, eps, weight_decay, step)
+        for a in (w, m, v):
+            assert a.dtype == np.float32 and a.flags.c_contiguous
+        g = np.ascontiguousarray(g, np.float32)
+        self.lib.orc_adamw(w.size, w, m, v, g, s["decay"], s["omb1"], s["b2"], s["omb2"],
+                           s["bc2_sqrt"], s["eps"], s["neg_step"])
 
     def build_model(self, seed, n_layers, d):
         W = np.empty((n_layers, d, d), np.float32)

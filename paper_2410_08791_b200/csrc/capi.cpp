@@ -145,6 +145,16 @@ int sp_set_item_batching(sp_exec* ex, int32_t on) {
     return SP_OK;
 }
 
+int sp_set_optimizer(sp_exec* ex, int32_t kind, float beta1, float beta2, float eps, float weight_decay) {
+    if (!ex) return SP_ERR_INVALID;
+    return guarded(ex, [&] { ex->impl->set_optimizer(kind, beta1, beta2, eps, weight_decay); });
+}
+
+int sp_read_optimizer_state(sp_exec* ex, int32_t index, float* mW, float* mb, float* vW, float* vb) {
+    if (!ex) return SP_ERR_INVALID;
+    return guarded(ex, [&] { ex->impl->read_optimizer_state(index, mW, mb, vW, vb); });
+}
+
 int sp_digest_train(const sp_exec* ex, float loss, char out[17]) {
     if (!ex || !out) return SP_ERR_INVALID;
     ex->impl->digest_train(loss, out);
@@ -228,6 +238,7 @@ int64_t sp_describe_plan(const sp_config* cfg, int32_t n_items, int32_t train,
         for (int32_t l = 0; l < cfg->n_layers; ++l) in.frozen.push_back(frozen[l] != 0);
     in.sharded = (flags & SP_PLAN_SHARDED) != 0;
     in.eager = (flags & SP_PLAN_EAGER) != 0;
+    in.optimizer_state = (flags & SP_PLAN_OPTSTATE) != 0;
     sp::Plan plan = sp::build_plan(in, {});
     std::string text = plan.error.empty() ? sp::describe_plan(plan) : ("ERROR " + plan.error + "\n");
     if (buf && cap > 0) {

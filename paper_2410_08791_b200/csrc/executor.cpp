@@ -144,6 +144,10 @@ Executor::~Executor() {
     if (ev_io_in_) cudaEventDestroy(ev_io_in_);
     if (ev_io_out_) cudaEventDestroy(ev_io_out_);
     if (host32_) cudaFreeHost(host32_);
+    if (host_m_) cudaFreeHost(host_m_);
+    if (host_v_) cudaFreeHost(host_v_);
+    if (adamw_host_) cudaFreeHost(adamw_host_);
+    if (adamw_dev_) cudaFree(adamw_dev_);
     if (host16_) cudaFreeHost(host16_);
     if (host_act_) cudaFreeHost(host_act_);
     if (loss_host_) cudaFreeHost(loss_host_);
@@ -151,15 +155,17 @@ Executor::~Executor() {
         if (s) cudaStreamDestroy(s);
 }
 
-// Slot = [A: fp32 W|b image, world shards] [B: bf16 W + fp32 b wire image, world shards].
-// Each region is cut into `world` equal shards (256-byte aligned) so a rank can H2D / D2H its
-// own shard and NCCL all-gather / reduce-scatter the rest in place.
+// Slot = [A: fp32 W|b image] ([M][V]: AdamW state, same layout as A) [B: bf16 W + fp32 b
+// wire image]. Each region is cut into `world` equal shards (256-byte aligned) so a rank can
+// H2D / D2H its own shard and NCCL all-gather / reduce-scatter the rest in place.
 void Executor::layout_slots(int world) {
     shardA_ = shard_bytes(layer_bytes(), world);
     shardB_ = shard_bytes(wire16_bytes(), world);
     const size_t a_region = round_up(shardA_ * world, 1024);
-    off_w16_ = a_region;
-    slot_bytes_ = bf16_ ? round_up(a_region + shardB_ * world, 1024) : a_region;
+    off_m_ = adamw() ? a_region : 0;
+    off_v_ = adamw() ? 2 * a_region : 0;
+    off_w16_ = adamw() ? 3 * a_region : a_region;
+    slot_bytes_ = bf16_ ? round_up(off_w16_ + shardB_ * world, 1024) : off_w16_;
     if (slots_dev_) {
         CUDA_OK(cudaDeviceSynchronize());
         cudaFree(slots_dev_);
@@ -306,6 +312,7 @@ Plan Executor::make_plan(bool train, int n_items, int64_t rows, int fmt) {
     in.capacity = cfg_.capacity_bytes;
     in.sharded = sharded_;
     in.eager = eager_prefetch_;
+    in.optimizer_state = train && adamw();
     const std::vector<SlotCache> none;
     Plan plan = build_plan(in, fmt == cache_fmt_ ? cache_ : none);
     if (!plan.error.empty()) throw Error(plan.oom ? SP_ERR_OOM : SP_ERR_INVALID, plan.error);
@@ -531,6 +538,16 @@ void Executor::update_op(const Op& op, float lr) {
     const size_t dd = static_cast<size_t>(d_) * d_;
     cudaStream_t st = s_upd_;
     float* ws = gws_[L % 2];
+    if (adamw() && bf16_ && !comm_) {
+        // AdamW straight from the partials: dW split-K partials, db column-sum partials
+        adamw_reduce(slot_w32(s), slot_m32(s), slot_v32(s), ws, splits_, static_cast<int64_t>(dd),
+                     static_cast<int64_t>(dd), adamw_dev_, st);
+        adamw_reduce(slot_b32(s), slot_m32(s) + dd, slot_v32(s) + dd, ws + static_cast<size_t>(splits_) * dd,
+                     col_chunks_, d_, d_, adamw_dev_, st);
+        kernels_ += 2;
+        w16_layer_[s] = -1;
+        return;
+    }
     if (bf16_ && !comm_) {
         // W: updated in the dW epilogue (fused), or here from the split-K partials in a fixed
         // order; bias from the db column-sum partials.
@@ -561,12 +578,21 @@ void Executor::update_op(const Op& op, float lr) {
         size_t lo = 0, hi = 0;
         shard_range(shardA_, layer_bytes(), lo, hi);
         if (hi > lo) {
-            exact_sgd(slot_w32(s) + lo / 4, mine, static_cast<int64_t>((hi - lo) / 4), lr, st);
+            const int64_t count = static_cast<int64_t>((hi - lo) / 4);
+            if (adamw())
+                adamw_reduce(slot_w32(s) + lo / 4, slot_m32(s) + lo / 4, slot_v32(s) + lo / 4, mine, 1, 0,
+                             count, adamw_dev_, st);
+            else
+                exact_sgd(slot_w32(s) + lo / 4, mine, count, lr, st);
             ++kernels_;
         }
     } else {
         if (comm_) NCCL_OK(nccl().AllReduce(g, g, dd + d_, ncclFloat, ncclSum, comm_, st));
-        exact_sgd(slot_w32(s), g, static_cast<int64_t>(dd + d_), lr, st);  // [W|b] contiguous
+        if (adamw())  // [W|b], [mW|mb], [vW|vb] are each contiguous
+            adamw_reduce(slot_w32(s), slot_m32(s), slot_v32(s), g, 1, 0, static_cast<int64_t>(dd + d_),
+                         adamw_dev_, st);
+        else
+            exact_sgd(slot_w32(s), g, static_cast<int64_t>(dd + d_), lr, st);
         ++kernels_;
     }
     w16_layer_[s] = -1;  // the bf16 copy is now stale
@@ -610,6 +636,20 @@ void Executor::enqueue_op(const Plan& plan, int i, bool train, int n_items, int6
                                             cudaMemcpyHostToDevice, st));
                     h2d_bytes_ += act_b;
                 }
+                if (j < op.opts.size() && op.opts[j]) {  // AdamW m, v (sharded: this rank's shard)
+                    size_t lo = 0, hi = layer_bytes();
+                    if (sharded_) shard_range(shardA_, layer_bytes(), lo, hi);
+                    const size_t off = static_cast<size_t>(L) * (dd + d_);
+                    if (hi > lo) {
+                        CUDA_OK(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(slot_m32(s)) + lo,
+                                                reinterpret_cast<const uint8_t*>(host_m_ + off) + lo, hi - lo,
+                                                cudaMemcpyHostToDevice, st));
+                        CUDA_OK(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(slot_v32(s)) + lo,
+                                                reinterpret_cast<const uint8_t*>(host_v_ + off) + lo, hi - lo,
+                                                cudaMemcpyHostToDevice, st));
+                    }
+                    h2d_bytes_ += 2 * (hi - lo);
+                }
             }
             break;
         case OpKind::Compute:
@@ -632,6 +672,16 @@ void Executor::enqueue_op(const Plan& plan, int i, bool train, int n_items, int6
                 CUDA_OK(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(host32_ + static_cast<size_t>(L) * (dd + d_)) + lo,
                                         slot_ptr(s) + lo, hi - lo, cudaMemcpyDeviceToHost, st));
             d2h_bytes_ += hi - lo;
+            if (adamw() && hi > lo) {  // the optimizer state rides the write-back
+                const size_t off = static_cast<size_t>(L) * (dd + d_);
+                CUDA_OK(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(host_m_ + off) + lo,
+                                        reinterpret_cast<const uint8_t*>(slot_m32(s)) + lo, hi - lo,
+                                        cudaMemcpyDeviceToHost, st));
+                CUDA_OK(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(host_v_ + off) + lo,
+                                        reinterpret_cast<const uint8_t*>(slot_v32(s)) + lo, hi - lo,
+                                        cudaMemcpyDeviceToHost, st));
+                d2h_bytes_ += 2 * (hi - lo);
+            }
             host16_stale_[L] = 1;
             break;
         }
@@ -669,6 +719,8 @@ void Executor::enqueue_call(const Plan& plan, const CallIO& io) {
     record_timing(ev_call0_, s_h2d_);
     CUDA_OK(cudaEventRecord(ev_fork_, s_h2d_));
     for (auto s : {s_comp_, s_d2h_, s_upd_}) CUDA_OK(cudaStreamWaitEvent(s, ev_fork_, 0));
+    if (io.train && adamw())  // this step's AdamW scalars: read at execution, so replays stay valid
+        CUDA_OK(cudaMemcpyAsync(adamw_dev_, adamw_host_, sizeof(AdamwScalars), cudaMemcpyHostToDevice, s_upd_));
     const size_t act = static_cast<size_t>(io.rows) * d_ * 4;
     if (!io.device_io) {
         CUDA_OK(cudaMemcpyAsync(xin_, io.x, act * (io.train ? 1 : io.n_items), cudaMemcpyHostToDevice, s_comp_));
@@ -961,13 +1013,26 @@ float Executor::train_step(const float* x, const float* target, int64_t rows, fl
         dw_cta_ = c.cta;
         dw_bn_ = c.block_n;
         col_chunks_ = colsum_chunks(rows);
-        dw_fused_ = comm_ == nullptr && splits_ == 1;
+        dw_fused_ = comm_ == nullptr && splits_ == 1 && !adamw();
     }
     reset_call_counters();
     cur_x_ = device_io ? x : xin_;
     cur_t_ = device_io ? target : tgt_;
     if (cache_fmt_ != fmt) std::fill(w16_layer_.begin(), w16_layer_.end(), -1);
     cur_lr_ = lr;
+    if (adamw()) {  // PyTorch's scalars: computed in double, rounded to float once (orc_adamw)
+        ++step_t_;
+        const double t = static_cast<double>(step_t_);
+        AdamwScalars& a = *adamw_host_;
+        a.decay = static_cast<float>(1.0 - static_cast<double>(lr) * wd_);
+        a.omb1 = static_cast<float>(1.0 - beta1_);
+        a.b2 = static_cast<float>(beta2_);
+        a.omb2 = static_cast<float>(1.0 - beta2_);
+        a.bc2_sqrt = static_cast<float>(std::sqrt(1.0 - std::pow(beta2_, t)));
+        a.eps = static_cast<float>(eps_);
+        a.neg_step = static_cast<float>(-static_cast<double>(lr) / (1.0 - std::pow(beta1_, t)));
+        a.pad = 0.0f;
+    }
     CallIO io{true, 1, rows, lr, fmt, device_io, x, target, nullptr};
     const auto t0 = std::chrono::steady_clock::now();
     run_call(plan, io);
@@ -1039,6 +1104,43 @@ void Executor::dp_init(const uint8_t id[128], int rank, int world, bool shard_we
     cap_rows_ = 0;                            // gradient buffers re-sized for world shards
 }
 
+void Executor::set_optimizer(int kind, float beta1, float beta2, float eps, float weight_decay) {
+    if (kind != SP_OPT_SGD && kind != SP_OPT_ADAMW) throw Error(SP_ERR_INVALID, "optimizer: unknown kind");
+    if (kind == SP_OPT_ADAMW && (!(beta1 >= 0.0f && beta1 < 1.0f) || !(beta2 >= 0.0f && beta2 < 1.0f) ||
+                                 !(eps > 0.0f) || !(weight_decay >= 0.0f)))
+        throw Error(SP_ERR_INVALID, "optimizer: AdamW needs 0 <= beta < 1, eps > 0, weight_decay >= 0");
+    require_full_host(-1, "set_optimizer");
+    CUDA_OK(cudaSetDevice(cfg_.device));
+    for (auto s : {s_h2d_, s_comp_, s_d2h_, s_upd_}) CUDA_OK(cudaStreamSynchronize(s));
+    optimizer_ = kind;
+    beta1_ = beta1;
+    beta2_ = beta2;
+    eps_ = eps;
+    wd_ = weight_decay;
+    step_t_ = 0;
+    const size_t img = static_cast<size_t>(n_) * (static_cast<size_t>(d_) * d_ + d_) * 4;
+    if (kind == SP_OPT_ADAMW) {
+        if (!host_m_) CUDA_OK(cudaHostAlloc(&host_m_, img, cudaHostAllocPortable));
+        if (!host_v_) CUDA_OK(cudaHostAlloc(&host_v_, img, cudaHostAllocPortable));
+        if (!adamw_host_) CUDA_OK(cudaHostAlloc(&adamw_host_, sizeof(AdamwScalars), cudaHostAllocPortable));
+        if (!adamw_dev_) CUDA_OK(cudaMalloc(&adamw_dev_, sizeof(AdamwScalars)));
+        std::memset(host_m_, 0, img);
+        std::memset(host_v_, 0, img);
+    }
+    layout_slots(sharded_ ? world_ : 1);  // [A][M][V][B] slots for AdamW; drops caches and graphs
+}
+
+void Executor::read_optimizer_state(int index, float* mW, float* mb, float* vW, float* vb) {
+    if (index < 0 || index >= n_) throw Error(SP_ERR_INVALID, "read_optimizer_state: index out of range");
+    if (!adamw()) throw Error(SP_ERR_STATE, "read_optimizer_state: the optimizer has no state (SGD)");
+    require_full_host(index, "read_optimizer_state");
+    const size_t dd = static_cast<size_t>(d_) * d_, off = static_cast<size_t>(index) * (dd + d_);
+    if (mW) std::memcpy(mW, host_m_ + off, dd * 4);
+    if (mb) std::memcpy(mb, host_m_ + off + dd, static_cast<size_t>(d_) * 4);
+    if (vW) std::memcpy(vW, host_v_ + off, dd * 4);
+    if (vb) std::memcpy(vb, host_v_ + off + dd, static_cast<size_t>(d_) * 4);
+}
+
 void Executor::dp_sync() {
     // Collective (every rank, same order): for each layer whose host master is shard-only,
     // stream this rank's shard into slot 0, all-gather the image over NCCL, and copy the
@@ -1055,12 +1157,16 @@ void Executor::dp_sync() {
     uint8_t* stage = slot_ptr(0);
     for (int L = 0; L < n_; ++L) {
         if (!host_partial_[static_cast<size_t>(L)]) continue;
-        uint8_t* host = reinterpret_cast<uint8_t*>(host32_ + static_cast<size_t>(L) * (dd + d_));
-        if (hi > lo) CUDA_OK(cudaMemcpyAsync(stage + lo, host + lo, hi - lo, cudaMemcpyHostToDevice, s_upd_));
-        NCCL_OK(nccl().AllGather(stage + shardA_ * static_cast<size_t>(rank_), stage, shardA_,
-                                 ncclUint8, comm_, s_upd_));
-        CUDA_OK(cudaMemcpyAsync(host, stage, img, cudaMemcpyDeviceToHost, s_upd_));
-        CUDA_OK(cudaStreamSynchronize(s_upd_));  // stage is reused by the next layer
+        // The weights, then (AdamW) the moments: all three are written back shard-only.
+        for (float* base : {host32_, adamw() ? host_m_ : nullptr, adamw() ? host_v_ : nullptr}) {
+            if (!base) continue;
+            uint8_t* host = reinterpret_cast<uint8_t*>(base + static_cast<size_t>(L) * (dd + d_));
+            if (hi > lo) CUDA_OK(cudaMemcpyAsync(stage + lo, host + lo, hi - lo, cudaMemcpyHostToDevice, s_upd_));
+            NCCL_OK(nccl().AllGather(stage + shardA_ * static_cast<size_t>(rank_), stage, shardA_,
+                                     ncclUint8, comm_, s_upd_));
+            CUDA_OK(cudaMemcpyAsync(host, stage, img, cudaMemcpyDeviceToHost, s_upd_));
+            CUDA_OK(cudaStreamSynchronize(s_upd_));  // stage is reused by the next array
+        }
         host_partial_[static_cast<size_t>(L)] = 0;
         host16_stale_[static_cast<size_t>(L)] = 1;
     }

@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "../../include/superpipe.h"
+#include "kernels.hpp"
 #include "plan.hpp"
 
 namespace sp {
@@ -42,6 +43,10 @@ public:
     std::string last_plan_text() const { return describe_plan(last_plan_); }
     void dp_init(const uint8_t id[128], int rank, int world, bool shard_weights);
     void dp_sync();
+    // Optimizer: SP_OPT_SGD (apply_sgd, the reference) or SP_OPT_ADAMW (state m, v in pinned
+    // host memory, streamed with each trainable layer's backward). Resets the state and step.
+    void set_optimizer(int kind, float beta1, float beta2, float eps, float weight_decay);
+    void read_optimizer_state(int index, float* mW, float* mb, float* vW, float* vb);
 
     const sp_stats& stats() const { return stats_; }
     const std::vector<sp_trace_event>& trace() const { return trace_; }
@@ -53,6 +58,8 @@ private:
     uint64_t wire16_bytes() const { return static_cast<uint64_t>(d_) * d_ * 2 + d_ * 4ull; }
     uint8_t* slot_ptr(int s) const { return slots_dev_ + static_cast<size_t>(s) * slot_bytes_; }
     float* slot_w32(int s) const { return reinterpret_cast<float*>(slot_ptr(s)); }
+    float* slot_m32(int s) const { return reinterpret_cast<float*>(slot_ptr(s) + off_m_); }  // AdamW
+    float* slot_v32(int s) const { return reinterpret_cast<float*>(slot_ptr(s) + off_v_); }
     float* slot_b32(int s) const { return slot_w32(s) + static_cast<size_t>(d_) * d_; }
     void* slot_w16(int s) const { return slot_ptr(s) + off_w16_; }
     float* slot_b16(int s) const {  // bias of the bf16 inference wire image
@@ -111,7 +118,7 @@ private:
     std::vector<uint8_t> registered_;
     // HBM ring
     int n_slots_ = 0;
-    size_t slot_bytes_ = 0, off_w16_ = 0;
+    size_t slot_bytes_ = 0, off_w16_ = 0, off_m_ = 0, off_v_ = 0;
     uint8_t* slots_dev_ = nullptr;
     std::vector<SlotCache> cache_;
     int cache_fmt_ = -1;
@@ -166,6 +173,15 @@ private:
     int splits_ = 1, dw_bn_ = 256, dw_cta_ = 2, col_chunks_ = 1, splits_cap_ = 1, col_chunks_cap_ = 1;
     int loss_blocks_ = 0;
     bool dw_fused_ = true;  // bf16 dW: SGD fused into the GEMM epilogue (else split-K partials)
+    // optimizer (SGD = the reference's apply_sgd; AdamW with streamed state)
+    int optimizer_ = SP_OPT_SGD;
+    double beta1_ = 0.9, beta2_ = 0.999, eps_ = 1e-8, wd_ = 0.0;
+    int64_t step_t_ = 0;
+    float* host_m_ = nullptr;  // pinned [n][d*d + d] fp32, same layout as host32_
+    float* host_v_ = nullptr;
+    AdamwScalars* adamw_host_ = nullptr;  // pinned: this step's scalars, copied in by the graph
+    AdamwScalars* adamw_dev_ = nullptr;
+    bool adamw() const { return optimizer_ == SP_OPT_ADAMW; }
     // data parallel
     ncclComm_t comm_ = nullptr;
     int rank_ = 0, world_ = 1;

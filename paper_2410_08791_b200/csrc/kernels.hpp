@@ -104,4 +104,14 @@ void sgd_reduce(float* w, const float* parts, int nparts, int64_t stride, int64_
                 float lr, cudaStream_t st);
 void scale_inplace(float* x, int64_t count, float s, cudaStream_t st);
 
+// AdamW (PyTorch's decoupled weight decay) on fp32 master weights w with optimizer state m, v,
+// the gradient being sum_p parts[p*stride + i] (fixed order; nparts = 1 for a plain gradient).
+// The step's scalars are read from device memory (refreshed each call, so a captured CUDA graph
+// replays every step). Each operation separately rounded, in orc_adamw's order (oracle.h).
+struct AdamwScalars {
+    float decay, omb1, b2, omb2, bc2_sqrt, eps, neg_step, pad;
+};
+void adamw_reduce(float* w, float* m, float* v, const float* parts, int nparts, int64_t stride,
+                  int64_t count, const AdamwScalars* scalars, cudaStream_t st);
+
 }  // namespace sp

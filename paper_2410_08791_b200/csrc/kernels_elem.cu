@@ -186,6 +186,49 @@ __global__ void sgd_reduce_kernel(float* __restrict__ w, const float* __restrict
     }
 }
 
+__device__ __forceinline__ void adamw_elem(float& w, float& m, float& v, float g, const AdamwScalars& s) {
+    const float wi = __fmul_rn(w, s.decay);
+    const float mi = __fadd_rn(m, __fmul_rn(s.omb1, __fsub_rn(g, m)));
+    const float vi = __fadd_rn(__fmul_rn(v, s.b2), __fmul_rn(__fmul_rn(s.omb2, g), g));
+    const float denom = __fadd_rn(__fdiv_rn(__fsqrt_rn(vi), s.bc2_sqrt), s.eps);
+    w = __fadd_rn(wi, __fmul_rn(s.neg_step, __fdiv_rn(mi, denom)));
+    m = mi;
+    v = vi;
+}
+
+__global__ void adamw_reduce_kernel(float* __restrict__ w, float* __restrict__ m, float* __restrict__ v,
+                                    const float* __restrict__ parts, int nparts, int64_t stride,
+                                    int64_t count, const AdamwScalars* __restrict__ sc) {
+    pdl_wait_then_release();
+    const AdamwScalars s = *sc;
+    const int64_t n4 = (stride % 4 == 0) ? count / 4 : 0;
+    const int64_t gs = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n4; i += gs) {
+        float4 g = reinterpret_cast<const float4*>(parts)[i];
+        for (int p = 1; p < nparts; ++p) {
+            const float4 q = reinterpret_cast<const float4*>(parts + p * stride)[i];
+            g.x = __fadd_rn(g.x, q.x);
+            g.y = __fadd_rn(g.y, q.y);
+            g.z = __fadd_rn(g.z, q.z);
+            g.w = __fadd_rn(g.w, q.w);
+        }
+        float4 wv = reinterpret_cast<float4*>(w)[i], mv = reinterpret_cast<float4*>(m)[i],
+               vv = reinterpret_cast<float4*>(v)[i];
+        adamw_elem(wv.x, mv.x, vv.x, g.x, s);
+        adamw_elem(wv.y, mv.y, vv.y, g.y, s);
+        adamw_elem(wv.z, mv.z, vv.z, g.z, s);
+        adamw_elem(wv.w, mv.w, vv.w, g.w, s);
+        reinterpret_cast<float4*>(w)[i] = wv;
+        reinterpret_cast<float4*>(m)[i] = mv;
+        reinterpret_cast<float4*>(v)[i] = vv;
+    }
+    for (int64_t i = n4 * 4 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += gs) {
+        float g = parts[i];
+        for (int p = 1; p < nparts; ++p) g = __fadd_rn(g, parts[p * stride + i]);
+        adamw_elem(w[i], m[i], v[i], g, s);
+    }
+}
+
 // w[j] -= lr * sum_p parts[p*stride + j] for a short vector (the bias) with many partials:
 // 32 columns x 8 lanes per block, each lane sums every 8th partial, lanes combined in a fixed
 // order. Deterministic and latency-tolerant (independent loads per lane).
@@ -277,6 +320,12 @@ void sgd_reduce(float* w, const float* parts, int nparts, int64_t stride, int64_
     }
     launch_pdl(sgd_reduce_kernel, dim3(grid_for(count / 4 + 1)), dim3(kThreads), 0, st, w, parts,
                nparts, stride, count, lr);
+}
+
+void adamw_reduce(float* w, float* m, float* v, const float* parts, int nparts, int64_t stride,
+                  int64_t count, const AdamwScalars* scalars, cudaStream_t st) {
+    launch_pdl(adamw_reduce_kernel, dim3(grid_for(count / 4 + 1)), dim3(kThreads), 0, st, w, m, v,
+               parts, nparts, stride, count, scalars);
 }
 
 void scale_inplace(float* x, int64_t count, float s, cudaStream_t st) {

@@ -247,15 +247,18 @@ private:
 
     // ---- policy actions ----------------------------------------------------------------
     void claim_positions(int b, int e, int trigger) {
-        struct Move { int pos, slot; bool weights, act; };
+        struct Move { int pos, slot; bool weights, act, opt; };
         std::vector<Move> moves;
         for (int q = b; q < e; ++q) {
             const int L = seq()[q];
+            // AdamW moments travel with each trainable layer's backward claim, hit or miss
+            const bool opt = backward() && in_.optimizer_state && trainable(L);
             int s = active_slot(L);
             if (s >= 0) {
                 slots_[s].refs += 1;
                 pos_slot_[q] = s;
                 pos_load_[q] = slots_[s].fill_op;
+                if (opt) moves.push_back({q, s, false, false, true});  // Standard: still resident
                 continue;
             }
             bool miss = false;
@@ -277,7 +280,7 @@ private:
             if (miss || !cancel_pending_free(s)) ledger_add(kWeight, in_.layer_bytes);
             const bool act = backward() && ckpt_;
             if (act) ledger_add(kActivation, in_.act_bytes);
-            if (miss || act) moves.push_back({q, s, miss, act});
+            if (miss || act || opt) moves.push_back({q, s, miss, act, opt});
         }
         if (moves.empty()) return;
         auto emit = [&](const std::vector<Move>& group) {
@@ -290,7 +293,9 @@ private:
                 op.slots.push_back(m.slot);
                 op.weights.push_back(m.weights);
                 op.acts.push_back(m.act);
-                if (m.weights && slots_[m.slot].busy_op >= 0) op.deps.push_back(slots_[m.slot].busy_op);
+                op.opts.push_back(m.opt);
+                // weights or optimizer state overwrite the slot: after its last reader
+                if ((m.weights || m.opt) && slots_[m.slot].busy_op >= 0) op.deps.push_back(slots_[m.slot].busy_op);
                 if (m.act && ba_busy_[m.slot] >= 0) op.deps.push_back(ba_busy_[m.slot]);
                 // The reload reads the pinned copy written by this layer's forward offload
                 // (the reference only reloads once act_on_host_ is set, engine.cpp:397-402).
@@ -546,9 +551,10 @@ std::string describe_plan(const Plan& plan) {
         if (op.kind == OpKind::ActSave) os << " layer=" << op.layer;
         if (op.kind == OpKind::H2D || op.kind == OpKind::D2H || op.kind == OpKind::AllGather) {
             std::vector<int> w(op.weights.begin(), op.weights.end()),
-                a(op.acts.begin(), op.acts.end());
+                a(op.acts.begin(), op.acts.end()), o(op.opts.begin(), op.opts.end());
             os << " layers=" << list(op.layers) << " slots=" << list(op.slots)
                << " w=" << list(w) << " a=" << list(a);
+            if (!o.empty()) os << " o=" << list(o);
         }
         os << " deps=" << list(op.deps) << " led=" << op.led_w << "," << op.led_a << ","
            << op.led_g << "\n";

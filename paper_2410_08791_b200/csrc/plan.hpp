@@ -57,6 +57,9 @@ struct PlanInput {
     // for the offload it reads) - not for the compute that triggers it in policy_step
     // (scheduler.cpp:105-136). Same ops, order, slots and ledger; copies start earlier.
     bool eager = false;
+    // Optimizer state (AdamW m, v) streams with every trainable layer's backward: its H2D
+    // (even when the weights are a slot hit) and its write-back ride the layer's transfers.
+    bool optimizer_state = false;
     std::vector<uint8_t> frozen;  // per layer
     uint64_t layer_bytes = 0;     // reference ledger units: (d*d + d) * 4
     uint64_t act_bytes = 0;       // rows * d * 4
@@ -80,6 +83,7 @@ struct Op {
     std::vector<int> slots;        // H2D / D2H: their slots
     std::vector<uint8_t> weights;  // per moved layer: weight bytes move
     std::vector<uint8_t> acts;     // per moved layer: the saved activation rides along
+    std::vector<uint8_t> opts;     // per moved layer: optimizer state (m, v) rides along
     std::vector<int> deps;         // op indices that must complete first (any stream)
     uint64_t led_w = 0, led_a = 0, led_g = 0;  // ledger (weight/act/grad bytes) at this op
 };

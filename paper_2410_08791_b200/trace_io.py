@@ -15,7 +15,7 @@ from __future__ import annotations
 import json
 
 HEADER = "t_start,t_end,kind,detail,resident_bytes,weight_bytes,activation_bytes,gradient_bytes"
-_LIST_KEYS = ("layers", "slots", "w", "a", "deps", "led")
+_LIST_KEYS = ("layers", "slots", "w", "a", "o", "deps", "led")
 
 
 def plan_ops(text: str):

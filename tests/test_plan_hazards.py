@@ -13,6 +13,8 @@ its own offload). Buffers modelled:
   fwd act ring fa[i]  COMPUTE(fwd L) reads fa[L%3], writes fa[(L+1)%3]; ACTSAVE(L) reads fa[L%3]
   grad workspace g[i] COMPUTE(bwd L, trainable) writes g[L%2]; UPDATE(L) reads g[L%2]
   host master[L]      D2H(L) writes; H2D(w, L) reads
+  AdamW moments MV[s] H2D(o) writes; UPDATE reads+writes; D2H reads (optimizer_state plans)
+  host moments[L]     D2H(L) writes; H2D(o, L) reads
 """
 import itertools
 
@@ -25,18 +27,22 @@ STREAM = {"H2D": "h2d", "COMPUTE": "comp", "LOSS": "comp", "D2H": "d2h", "ACTSAV
           "UPDATE": "upd", "ALLGATHER": "upd"}
 
 
-def accesses(ops, ckpt, frozen):
+def accesses(ops, ckpt, frozen, opt=False):
     acc = []  # (op index, resource, is_write)
     for i, op in enumerate(ops):
         k = op["kind"]
         if k == "H2D":
-            for L, s, w, a in zip(op["layers"], op["slots"], op["w"], op["a"]):
+            o = op.get("o", [0] * len(op["layers"]))
+            for L, s, w, a, m in zip(op["layers"], op["slots"], op["w"], op["a"], o):
                 if w:
                     acc.append((i, ("W", s), True))
                     acc.append((i, ("host", L), False))
                 if a:
                     acc.append((i, ("ba", s), True))
                     acc.append((i, ("hact", L), False))
+                if m:
+                    acc.append((i, ("MV", s), True))
+                    acc.append((i, ("hostMV", L), False))
         elif k == "COMPUTE":
             L, s, bwd = op["layer"], op["slot"], op["pass"] == 1
             acc.append((i, ("W", s), False))
@@ -51,6 +57,8 @@ def accesses(ops, ckpt, frozen):
         elif k == "UPDATE":
             acc.append((i, ("g", op["layer"] % 2), False))
             acc.append((i, ("W", op["slot"]), True))
+            if opt:
+                acc.append((i, ("MV", op["slot"]), True))
         elif k == "ALLGATHER":  # sharded streaming: completes the slot over NVLink
             for s in op["slots"]:
                 acc.append((i, ("W", s), True))
@@ -58,6 +66,9 @@ def accesses(ops, ckpt, frozen):
             for L, s in zip(op["layers"], op["slots"]):
                 acc.append((i, ("W", s), False))
                 acc.append((i, ("host", L), True))
+                if opt:
+                    acc.append((i, ("MV", s), False))
+                    acc.append((i, ("hostMV", L), True))
         elif k == "ACTSAVE":
             L = op["layer"]
             acc.append((i, ("fa", L % 3), False))
@@ -83,23 +94,23 @@ def happens_before(ops):
     return lambda a, b: bool(reach[b] >> a & 1)
 
 
-def check(n, strategy, train, ckpt, items=1, frozen=None, sharded=False):
+def check(n, strategy, train, ckpt, items=1, frozen=None, sharded=False, opt=False):
     # both dependency modes: the reference policy's triggers, and eager prefetch (an H2D waits
     # only for its slot) - the executor's default, which must be just as race-free
     for eager in (False, True):
-        check_one(n, strategy, train, ckpt, items, frozen, sharded, eager)
+        check_one(n, strategy, train, ckpt, items, frozen, sharded, eager, opt)
 
 
-def check_one(n, strategy, train, ckpt, items, frozen, sharded, eager):
+def check_one(n, strategy, train, ckpt, items, frozen, sharded, eager, opt=False):
     frozen = frozen or [0] * n
     txt = sp.describe_plan(n, 8, strategy, n_items=items, train=train, checkpointing=ckpt,
-                           frozen=frozen, sharded=sharded, eager=eager)
+                           frozen=frozen, sharded=sharded, eager=eager, optimizer_state=opt)
     assert not txt.startswith("ERROR"), txt
     head, ops = parse_plan(txt)
     ck = ckpt and train and strategy.kind != sp.STANDARD
     hb = happens_before(ops)
     by_res = {}
-    for i, res, w in accesses(ops, ck, frozen):
+    for i, res, w in accesses(ops, ck, frozen, opt and train):
         by_res.setdefault(res, []).append((i, w))
     for res, lst in by_res.items():
         for (a, wa), (b, wb) in itertools.combinations(sorted(lst), 2):
@@ -143,6 +154,39 @@ def test_sharded_training_plan_has_no_cross_stream_races(n, ckpt):
         if s.k <= n:
             for frozen in ([0] * n, [1] + [0] * (n - 1)):
                 check(n, s, True, ckpt, frozen=frozen, sharded=True)
+
+
+@pytest.mark.parametrize("n", [2, 3, 5, 8])
+@pytest.mark.parametrize("ckpt", [False, True])
+def test_adamw_plan_orders_every_moment_transfer(n, ckpt):
+    # AdamW: the moments of every trainable layer ride the backward pass through the ring
+    # (H2D o=1 -> UPDATE -> D2H), so the MV region of a slot and the host moments are
+    # checked exactly like the weights, sharded and not.
+    for s in STRATS:
+        if s.k > n:
+            continue
+        for frozen in ([0] * n, [1] + [0] * (n - 1)):
+            check(n, s, True, ckpt, frozen=frozen, opt=True)
+            check(n, s, True, ckpt, frozen=frozen, sharded=True, opt=True)
+
+
+def test_adamw_plan_streams_moments_for_each_trainable_layer_once():
+    n = 8
+    frozen = [1, 0, 0, 1, 0, 0, 0, 0]
+    for s in STRATS:
+        head, ops = parse_plan(sp.describe_plan(n, 8, s, train=True, frozen=frozen,
+                                                optimizer_state=True))
+        moved = [L for o in ops if o["kind"] == "H2D" and o["pass"] == 1
+                 for L, m in zip(o["layers"], o["o"]) if m]
+        assert sorted(moved) == [L for L in range(n) if not frozen[L]], (s, moved)
+        assert not any(m for o in ops if o["kind"] == "H2D" and o["pass"] == 0 for m in o["o"])
+        # each moment load precedes (happens-before) the update of that layer
+        hb = happens_before(ops)
+        load = {L: o["index"] for o in ops if o["kind"] == "H2D"
+                for L, m in zip(o["layers"], o["o"]) if m}
+        for o in ops:
+            if o["kind"] == "UPDATE":
+                assert hb(load[o["layer"]], o["index"])
 
 
 def test_sharded_plan_gathers_every_loaded_layer_and_never_reuses_updated_slots():
