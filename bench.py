@@ -50,6 +50,9 @@ def parse():
     p.add_argument("--lr", type=float, default=0.01)
     p.add_argument("--mode", default="batch", choices=["batch", "sequential"],
                    help="TransferMode (sim.hpp:15): one H2D op per k' group, or per layer")
+    p.add_argument("--optimizer", default="sgd", choices=["sgd", "adamw"],
+                   help="sgd: the reference's update (default); adamw: fp32 m, v in pinned host "
+                        "memory streamed with each backward layer, fused AdamW update")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--sweep", default="", help="comma list of k:kp to report extra lines")
     return p.parse_args()
@@ -194,17 +197,31 @@ def gemm_kernel_timing(torch, capi, a, reps=20):
     return res
 
 
-def layer_roofline(a, link, pk, rows_per_gpu):
-    """Per-layer max(FLOP at tensor peak, host-link bytes / measured pinned bandwidth), summed
-    over the step (forward: H2D fp32 layer; backward: H2D + D2H concurrently)."""
+def layer_roofline(a, link, pk, rows_per_gpu, slots, shards=1):
+    """Lower bound on the step time of a k-window ring with `slots` HBM slots: per layer
+    max(FLOP at the sustained tensor peak, its host-link bytes at the measured pinned bandwidth),
+    summed over the step.
+
+    Bytes: a ring of S slots can carry at most S layers across each direction reversal (end of
+    forward, end of step), so forward must load >= L - S layers and backward >= L - S; every
+    trainable layer writes its fp32 image back (D2H). AdamW adds the fp32 moments m, v of every
+    layer in both directions. Backward H2D and D2H overlap at the measured duplex rate; a
+    backward layer with nothing to load is bound by its write-back alone (simplex D2H).
+    Sharded data parallel (shards = world): each rank moves 1/world of every image."""
     d, L = a.d, a.layers
-    lb = (d * d + d) * 4
+    S = min(slots, L)
+    lb = (d * d + d) * 4 / shards
+    opt = 2 * lb if a.optimizer == "adamw" else 0.0
     peak = pk["bf16_tflops_sustained"] * 1e12
-    fwd = max(2.0 * rows_per_gpu * d * d / peak, lb / (link["h2d_gbs"] * 1e9))
-    bwd = max(4.0 * rows_per_gpu * d * d / peak, lb / (link["duplex_gbs_per_dir"] * 1e9))
-    first = 2.0 * rows_per_gpu * d * d / peak  # layer 0 needs no dX
-    bwd0 = max(first, lb / (link["duplex_gbs_per_dir"] * 1e9))
-    return L * fwd + (L - 1) * bwd + bwd0
+    h2d, d2h, dup = link["h2d_gbs"] * 1e9, link["d2h_gbs"] * 1e9, link["duplex_gbs_per_dir"] * 1e9
+    fl_f = 2.0 * rows_per_gpu * d * d / peak
+    t = (L - S) * max(fl_f, lb / h2d) + S * fl_f  # forward: S layers still resident
+    for pos in range(L):                            # backward, layer L-1 first
+        fl = fl_f if pos == L - 1 else 2 * fl_f     # layer 0 needs no dX
+        load = (lb if pos >= S else 0.0) + opt      # the forward's last S layers are resident
+        out = lb + opt
+        t += max(fl, out / d2h) if load == 0 else max(fl, load / dup, out / dup)
+    return t
 
 
 def cpu_baseline_ref(a, threads, rows_per_thread=2, layers_sample=6):
@@ -260,10 +277,12 @@ def run_reference(a, rank, world):
 
 def config_of(a, world):
     return {"workload": f"GPT-2 XL-shape layer stack: {a.layers} x d={a.d} dense ReLU blocks "
-                        f"(reference LayerBlock), bf16 train step (fwd+MSE+bwd+SGD)",
+                        f"(reference LayerBlock), bf16 train step (fwd+MSE+bwd+{a.optimizer.upper()})",
             "layers": a.layers, "d": a.d, "rows_per_gpu": a.rows, "global_batch": a.rows * world,
             "strategy": a.strategy, "k": a.k, "k_prime": a.kp, "transfer_mode": a.mode,
             "weights": "pinned host DRAM (fp32 master), streamed per step",
+            "optimizer": a.optimizer if a.optimizer == "sgd" else
+            "adamw (fp32 m, v in pinned host DRAM, streamed per step)",
             "parallelism": f"dp{world}", "l2": "working set (weights+activations) >> 126 MB L2"}
 
 
@@ -300,6 +319,8 @@ def main():
         e = sp.Executor(a.layers, a.d, strat, numerics=sp.BF16, device=local, trace=0)
         for i, (Wl, bl) in enumerate(weights):
             e.register_layer(i, Wl, bl)
+        if a.optimizer == "adamw":
+            e.set_optimizer(sp.OPT_ADAMW, 0.9, 0.999, 1e-8, 0.01)
         return e
 
     ex = make_executor(strategy)
@@ -373,7 +394,8 @@ def main():
         except Exception:
             traffic = None
     step_s = ms * 1e-3 / a.steps
-    roof_s = layer_roofline(a, link, pk, a.rows)
+    shards = world if world > 1 else 1  # dp.init_executor_dp: sharded streaming for world > 1
+    roof_s = layer_roofline(a, link, pk, a.rows, traced["n_slots"], shards)
     value = world * a.rows * a.steps / (ms * 1e-3)
     e2e = world * a.rows * a.steps / (ms_e2e * 1e-3)
 
@@ -452,7 +474,8 @@ def main():
                                 "ledger": st["peak_bytes"] / 1e9,
                                 "measured_reserved": st["hbm_reserved_bytes"] / 1e9},
                 "h2d_gb_per_step": st["h2d_bytes"] / 1e9, "d2h_gb_per_step": st["d2h_bytes"] / 1e9,
-                "layer_roofline_ms": roof_s * 1e3}), flush=True)
+                "layer_roofline_ms": layer_roofline(a, link, pk, a.rows, st["n_slots"], shards) * 1e3}),
+                flush=True)
         e.close()
     if world > 1:
         dist.destroy_process_group()

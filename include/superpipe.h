@@ -227,10 +227,14 @@ int sp_validate_strategy(int32_t strategy, int32_t k, int32_t k_prime, int32_t n
  * resolved ahead of time) as text, one op per line; returns the needed length. Host-only.
  * flags: SP_PLAN_SHARDED (data-parallel sharded streaming), SP_PLAN_EAGER (eager prefetch
  * dependencies, see sp_set_eager_prefetch), SP_PLAN_OPTSTATE (an optimizer with state, e.g.
- * AdamW: its m, v stream with each trainable layer's backward). */
+ * AdamW: its m, v stream with each trainable layer's backward), SP_PLAN_WRITEBACK (training:
+ * the executor's write-back scheme - updates copy the slot to a staging buffer the D2H reads,
+ * and layers still resident at the end are written back at the start of the next call; the
+ * plan shown is the second of two consecutive calls, i.e. the steady state). */
 #define SP_PLAN_SHARDED 1
 #define SP_PLAN_EAGER 2
 #define SP_PLAN_OPTSTATE 4
+#define SP_PLAN_WRITEBACK 8
 int64_t sp_describe_plan(const sp_config* cfg, int32_t n_items, int32_t train,
                          const int32_t* frozen, int32_t flags, char* buf, int64_t cap);
 /* Deterministic layer / input generators of the reference (host-only), so callers can

@@ -240,6 +240,15 @@ int64_t sp_describe_plan(const sp_config* cfg, int32_t n_items, int32_t train,
     in.eager = (flags & SP_PLAN_EAGER) != 0;
     in.optimizer_state = (flags & SP_PLAN_OPTSTATE) != 0;
     sp::Plan plan = sp::build_plan(in, {});
+    if ((flags & SP_PLAN_WRITEBACK) && in.train && plan.error.empty()) {
+        // the executor's training write-back scheme, steady state: the second of two calls
+        in.wb_stages = std::max(1, std::min(plan.n_slots, 8));
+        in.defer_writeback = !in.checkpointing;
+        plan = sp::build_plan(in, {});
+        in.pending_wb_layers = plan.deferred_layers;
+        in.pending_wb_slots = plan.deferred_slots;
+        plan = sp::build_plan(in, plan.final_slots);
+    }
     std::string text = plan.error.empty() ? sp::describe_plan(plan) : ("ERROR " + plan.error + "\n");
     if (buf && cap > 0) {
         const int64_t n = std::min<int64_t>(cap - 1, static_cast<int64_t>(text.size()));

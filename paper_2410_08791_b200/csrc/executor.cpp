@@ -74,6 +74,7 @@ Executor::Executor(const sp_config& cfg) : cfg_(cfg) {
     d_ = cfg.d;
     if (n_ < 1) throw Error(SP_ERR_INVALID, "build_model: n_layers must be >= 1");
     if (d_ < 1) throw Error(SP_ERR_INVALID, "build_model: d must be >= 1");
+    if (const char* e = std::getenv("SP_WB")) staged_writeback_ = std::atoi(e) != 0;  // A/B only
     const std::string v = validate_strategy(cfg.strategy, cfg.k, cfg.k_prime, n_);
     if (!v.empty()) throw Error(SP_ERR_INVALID, v);
     if (cfg.strategy == static_cast<int>(Strategy::CpuOnly))
@@ -148,6 +149,7 @@ Executor::~Executor() {
     if (host_v_) cudaFreeHost(host_v_);
     if (adamw_host_) cudaFreeHost(adamw_host_);
     if (adamw_dev_) cudaFree(adamw_dev_);
+    if (stages_dev_) cudaFree(stages_dev_);
     if (host16_) cudaFreeHost(host16_);
     if (host_act_) cudaFreeHost(host_act_);
     if (loss_host_) cudaFreeHost(loss_host_);
@@ -172,6 +174,13 @@ void Executor::layout_slots(int world) {
         slots_dev_ = nullptr;
     }
     CUDA_OK(cudaMalloc(&slots_dev_, static_cast<size_t>(n_slots_) * slot_bytes_));
+    if (stages_dev_) {  // re-sized on the next training call
+        cudaFree(stages_dev_);
+        stages_dev_ = nullptr;
+        n_stages_ = 0;
+    }
+    pending_wb_layers_.clear();  // callers flush first; the old slots are gone
+    pending_wb_slots_.clear();
     cache_.assign(static_cast<size_t>(n_slots_), SlotCache{});
     cache_fmt_ = -1;
     w16_layer_.assign(static_cast<size_t>(n_slots_), -1);
@@ -180,10 +189,41 @@ void Executor::layout_slots(int world) {
     ++alloc_gen_;
 }
 
+// Write-back stages: min(S, 8) buffers of one slot's fp32 regions (weights [+ m, v]).
+void Executor::ensure_stages() {
+    if (stages_dev_ || !staged_writeback_) return;
+    n_stages_ = std::max(1, std::min(n_slots_, 8));
+    stage_bytes_ = off_w16_;  // [A] or [A][M][V]: the slot minus its bf16 wire region
+    CUDA_OK(cudaMalloc(&stages_dev_, static_cast<size_t>(n_stages_) * stage_bytes_));
+}
+
+// Completes the previous train step's deferred write-backs now (host readers, inference,
+// re-layout): each still-resident layer's updated image [+ m, v] to the pinned master.
+void Executor::flush_writebacks() {
+    if (pending_wb_layers_.empty()) return;
+    CUDA_OK(cudaSetDevice(cfg_.device));
+    for (auto s : {s_h2d_, s_comp_, s_d2h_, s_upd_}) CUDA_OK(cudaStreamSynchronize(s));
+    const size_t img = layer_bytes(), dd = static_cast<size_t>(d_) * d_;
+    for (size_t i = 0; i < pending_wb_layers_.size(); ++i) {
+        const int L = pending_wb_layers_[i], s = pending_wb_slots_[i];
+        const size_t off = static_cast<size_t>(L) * (dd + d_);
+        CUDA_OK(cudaMemcpyAsync(host32_ + off, slot_ptr(s), img, cudaMemcpyDeviceToHost, s_d2h_));
+        if (adamw()) {
+            CUDA_OK(cudaMemcpyAsync(host_m_ + off, slot_m32(s), img, cudaMemcpyDeviceToHost, s_d2h_));
+            CUDA_OK(cudaMemcpyAsync(host_v_ + off, slot_v32(s), img, cudaMemcpyDeviceToHost, s_d2h_));
+        }
+        host16_stale_[static_cast<size_t>(L)] = 1;
+    }
+    CUDA_OK(cudaStreamSynchronize(s_d2h_));
+    pending_wb_layers_.clear();
+    pending_wb_slots_.clear();
+}
+
 void Executor::register_layer(int index, const float* W, const float* b, int activation,
                               int frozen) {
     if (index < 0 || index >= n_) throw Error(SP_ERR_INVALID, "register_layer: index out of range");
     if (!W || !b) throw Error(SP_ERR_INVALID, "register_layer: null weight or bias");
+    flush_writebacks();  // a pending write-back must not land on top of the new weights
     if (activation != SP_RELU && activation != SP_IDENTITY)
         throw Error(SP_ERR_INVALID, "register_layer: unknown activation");
     const size_t dd = static_cast<size_t>(d_) * d_;
@@ -313,6 +353,15 @@ Plan Executor::make_plan(bool train, int n_items, int64_t rows, int fmt) {
     in.sharded = sharded_;
     in.eager = eager_prefetch_;
     in.optimizer_state = train && adamw();
+    in.wb_stages = train && stages_dev_ ? n_stages_ : 0;
+    // (checkpointing: the D2H engine carries the forward's activation offloads - no deferral)
+    in.defer_writeback = train && staged_writeback_ && !cfg_.checkpointing;
+    if (train && fmt == cache_fmt_) {
+        in.pending_wb_layers = pending_wb_layers_;
+        in.pending_wb_slots = pending_wb_slots_;
+    } else {
+        flush_writebacks();
+    }
     const std::vector<SlotCache> none;
     Plan plan = build_plan(in, fmt == cache_fmt_ ? cache_ : none);
     if (!plan.error.empty()) throw Error(plan.oom ? SP_ERR_OOM : SP_ERR_INVALID, plan.error);
@@ -603,10 +652,15 @@ void Executor::enqueue_op(const Plan& plan, int i, bool train, int n_items, int6
     (void)n_items;
     const Op& op = plan.ops[static_cast<size_t>(i)];
     cudaStream_t st = stream_of(op.kind);
-    for (int dep : op.deps) {
+    auto wait = [&](int dep) {
         if (stream_of(plan.ops[static_cast<size_t>(dep)].kind) != st)
             CUDA_OK(cudaStreamWaitEvent(st, ev_dep_[static_cast<size_t>(dep)], 0));
-    }
+    };
+    // Eager H2D: each moved layer waits for its own slot just before its copy (deps is then
+    // exactly the union of move_deps); otherwise everything up front (policy trigger).
+    const bool per_move = op.kind == OpKind::H2D && eager_prefetch_ && !op.move_deps.empty();
+    if (!per_move)
+        for (int dep : op.deps) wait(dep);
     // Timing events are "external" so that, under graph capture, they become event-record
     // nodes; the dependency events (ev_dep_) become graph edges.
     if (cfg_.trace >= 1) record_timing(ev_start_[static_cast<size_t>(i)], st);
@@ -616,6 +670,8 @@ void Executor::enqueue_op(const Plan& plan, int i, bool train, int n_items, int6
         case OpKind::H2D:
             for (size_t j = 0; j < op.layers.size(); ++j) {
                 const int L = op.layers[j], s = op.slots[j];
+                if (per_move)
+                    for (int dep : op.move_deps[j]) wait(dep);
                 if (op.weights[j]) {
                     // Whole image, or (sharded) only this rank's [lo, hi) byte range of it.
                     const bool wire = fmt == kFmtBf16Infer;
@@ -660,29 +716,46 @@ void Executor::enqueue_op(const Plan& plan, int i, bool train, int n_items, int6
             break;
         case OpKind::Update:
             update_op(op, lr);
+            if (op.stage >= 0) {  // copy the updated image [+ m, v] out: the slot is free now
+                size_t lo = 0, hi = layer_bytes();
+                if (sharded_) shard_range(shardA_, layer_bytes(), lo, hi);
+                uint8_t* stage = stage_ptr(op.stage);
+                const uint8_t* slot = slot_ptr(op.slot);
+                if (hi > lo) {
+                    CUDA_OK(cudaMemcpyAsync(stage + lo, slot + lo, hi - lo, cudaMemcpyDeviceToDevice, st));
+                    if (adamw()) {
+                        CUDA_OK(cudaMemcpyAsync(stage + off_m_ + lo, slot + off_m_ + lo, hi - lo,
+                                                cudaMemcpyDeviceToDevice, st));
+                        CUDA_OK(cudaMemcpyAsync(stage + off_v_ + lo, slot + off_v_ + lo, hi - lo,
+                                                cudaMemcpyDeviceToDevice, st));
+                    }
+                }
+            }
             break;
         case OpKind::D2H: {
             // Updated fp32 master back to the pinned host copy (sharded: this rank's shard only;
             // every rank streams exactly that shard in later calls, so its copy stays
             // authoritative for it).
+            // From the write-back stage the Update filled, or (deferred write-back of the
+            // previous call, unstaged plans) straight from the slot.
             const int L = op.layers[0], s = op.slots[0];
+            host16_stale_[L] = 1;
+            if (op.deferred) break;  // done at the start of the next call (or a flush)
             size_t lo = 0, hi = layer_bytes();
             if (sharded_) shard_range(shardA_, layer_bytes(), lo, hi);
+            const uint8_t* src = op.stage >= 0 ? stage_ptr(op.stage) : slot_ptr(s);
+            const size_t off = static_cast<size_t>(L) * (dd + d_);
             if (hi > lo)
-                CUDA_OK(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(host32_ + static_cast<size_t>(L) * (dd + d_)) + lo,
-                                        slot_ptr(s) + lo, hi - lo, cudaMemcpyDeviceToHost, st));
+                CUDA_OK(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(host32_ + off) + lo, src + lo, hi - lo,
+                                        cudaMemcpyDeviceToHost, st));
             d2h_bytes_ += hi - lo;
             if (adamw() && hi > lo) {  // the optimizer state rides the write-back
-                const size_t off = static_cast<size_t>(L) * (dd + d_);
-                CUDA_OK(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(host_m_ + off) + lo,
-                                        reinterpret_cast<const uint8_t*>(slot_m32(s)) + lo, hi - lo,
-                                        cudaMemcpyDeviceToHost, st));
-                CUDA_OK(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(host_v_ + off) + lo,
-                                        reinterpret_cast<const uint8_t*>(slot_v32(s)) + lo, hi - lo,
-                                        cudaMemcpyDeviceToHost, st));
+                CUDA_OK(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(host_m_ + off) + lo, src + off_m_ + lo,
+                                        hi - lo, cudaMemcpyDeviceToHost, st));
+                CUDA_OK(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(host_v_ + off) + lo, src + off_v_ + lo,
+                                        hi - lo, cudaMemcpyDeviceToHost, st));
                 d2h_bytes_ += 2 * (hi - lo);
             }
-            host16_stale_[L] = 1;
             break;
         }
         case OpKind::AllGather:
@@ -772,6 +845,7 @@ uint64_t Executor::call_signature(const Plan& plan, const CallIO& io) const {
             mix(static_cast<uint64_t>(op.layers[j]) << 32 | static_cast<uint32_t>(op.slots[j]) |
                 static_cast<uint64_t>(op.weights[j]) << 62 | static_cast<uint64_t>(op.acts[j]) << 63);
         for (int dep : op.deps) mix(static_cast<uint64_t>(dep) | 1ull << 60);
+        mix(static_cast<uint64_t>(static_cast<uint32_t>(op.stage)) | static_cast<uint64_t>(op.deferred) << 40);
     }
     uint32_t lr_bits;
     std::memcpy(&lr_bits, &io.lr, 4);
@@ -798,6 +872,8 @@ void Executor::run_call(const Plan& plan, const CallIO& io) {
         // can be trusted by the next call (the host master copy is the source of truth).
         for (auto& c : cache_) c.valid = false;
         std::fill(w16_layer_.begin(), w16_layer_.end(), -1);
+        pending_wb_layers_.clear();  // their slots may have been overwritten as well
+        pending_wb_slots_.clear();
         throw;
     }
 }
@@ -872,6 +948,9 @@ void Executor::run_call_impl(const Plan& plan, const CallIO& io) {
     }
     cache_ = plan.final_slots;
     cache_fmt_ = io.fmt;
+    // this call ran the previous call's deferred write-backs and leaves its own
+    pending_wb_layers_ = plan.deferred_layers;
+    pending_wb_slots_ = plan.deferred_slots;
 }
 
 void Executor::collect_stats(const Plan& plan, int n_items, bool train) {
@@ -969,6 +1048,7 @@ void Executor::forward(const float* x, int64_t rows, int n_items, float* y, bool
     if (rows < 1 || n_items < 1) throw Error(SP_ERR_INVALID, "run_inference: no inputs");
     if (rows > (1ll << 31) - 1) throw Error(SP_ERR_INVALID, "run_inference: too many rows");
     check_ready();
+    flush_writebacks();  // inference reads the host master (and re-streams every layer)
     if (item_batching_ && n_items > 1 && rows * n_items <= (1ll << 31) - 1) {
         // [items][rows][d] is contiguous, i.e. one [items*rows][d] input: one pass over the
         // ring serves every item (row-independent math, so outputs are unchanged).
@@ -1004,6 +1084,8 @@ float Executor::train_step(const float* x, const float* target, int64_t rows, fl
     if (rows < 1) throw Error(SP_ERR_INVALID, "train: batch_size must be >= 1");
     check_ready();
     const int fmt = bf16_ ? kFmtBf16Train : kFmtExactF32;
+    CUDA_OK(cudaSetDevice(cfg_.device));
+    ensure_stages();
     Plan plan = make_plan(true, 1, rows, fmt);
     ensure_buffers(rows, 1, true, device_io);
     CUDA_OK(cudaSetDevice(cfg_.device));
@@ -1049,7 +1131,8 @@ float Executor::train_step(const float* x, const float* target, int64_t rows, fl
     return loss;
 }
 
-void Executor::digest_train(float loss, char out[17]) const {
+void Executor::digest_train(float loss, char out[17]) {
+    flush_writebacks();
     require_full_host(-1, "digest_train");
     // digest_train (engine.cpp:574-581): loss bytes, then each block's W and b — the host
     // master copy is [W_0 b_0 W_1 b_1 ...] contiguous, exactly the reference's byte order.
@@ -1074,6 +1157,7 @@ void Executor::digest_train(float loss, char out[17]) const {
 
 void Executor::read_layer(int index, float* W, float* b) {
     if (index < 0 || index >= n_) throw Error(SP_ERR_INVALID, "read_layer: index out of range");
+    flush_writebacks();
     require_full_host(index, "read_layer");
     const size_t dd = static_cast<size_t>(d_) * d_;
     const float* src = host32_ + static_cast<size_t>(index) * (dd + d_);
@@ -1083,6 +1167,7 @@ void Executor::read_layer(int index, float* W, float* b) {
 
 void Executor::dp_init(const uint8_t id[128], int rank, int world, bool shard_weights) {
     if (world < 1 || rank < 0 || rank >= world) throw Error(SP_ERR_INVALID, "dp_init: bad rank/world");
+    flush_writebacks();
     require_full_host(-1, "dp_init");
     // world == 1 still builds a (1-rank) communicator: the data-parallel code path (split-K
     // partials, fixed-order reduce, NCCL all-reduce inside the captured graph, SGD on the
@@ -1109,6 +1194,7 @@ void Executor::set_optimizer(int kind, float beta1, float beta2, float eps, floa
     if (kind == SP_OPT_ADAMW && (!(beta1 >= 0.0f && beta1 < 1.0f) || !(beta2 >= 0.0f && beta2 < 1.0f) ||
                                  !(eps > 0.0f) || !(weight_decay >= 0.0f)))
         throw Error(SP_ERR_INVALID, "optimizer: AdamW needs 0 <= beta < 1, eps > 0, weight_decay >= 0");
+    flush_writebacks();
     require_full_host(-1, "set_optimizer");
     CUDA_OK(cudaSetDevice(cfg_.device));
     for (auto s : {s_h2d_, s_comp_, s_d2h_, s_upd_}) CUDA_OK(cudaStreamSynchronize(s));
@@ -1133,6 +1219,7 @@ void Executor::set_optimizer(int kind, float beta1, float beta2, float eps, floa
 void Executor::read_optimizer_state(int index, float* mW, float* mb, float* vW, float* vb) {
     if (index < 0 || index >= n_) throw Error(SP_ERR_INVALID, "read_optimizer_state: index out of range");
     if (!adamw()) throw Error(SP_ERR_STATE, "read_optimizer_state: the optimizer has no state (SGD)");
+    flush_writebacks();
     require_full_host(index, "read_optimizer_state");
     const size_t dd = static_cast<size_t>(d_) * d_, off = static_cast<size_t>(index) * (dd + d_);
     if (mW) std::memcpy(mW, host_m_ + off, dd * 4);
@@ -1145,6 +1232,7 @@ void Executor::dp_sync() {
     // Collective (every rank, same order): for each layer whose host master is shard-only,
     // stream this rank's shard into slot 0, all-gather the image over NCCL, and copy the
     // whole image back to the pinned host master.
+    flush_writebacks();
     bool any = false;
     for (uint8_t p : host_partial_) any = any || p;
     if (!any) return;

@@ -36,7 +36,7 @@ public:
     float train_step(const float* x, const float* target, int64_t rows, float lr,
                      bool device_io);
     void read_layer(int index, float* W, float* b);
-    void digest_train(float loss, char out[17]) const;
+    void digest_train(float loss, char out[17]);
     void set_trace(int level) { cfg_.trace = level; }
     void set_item_batching(bool on) { item_batching_ = on; }
     void set_eager_prefetch(bool on) { eager_prefetch_ = on; }
@@ -90,6 +90,9 @@ private:
     };
 
     void layout_slots(int world);
+    void ensure_stages();
+    void flush_writebacks();
+    uint8_t* stage_ptr(int i) const { return stages_dev_ + static_cast<size_t>(i) * stage_bytes_; }
     void check_ready() const;
     void ensure_buffers(int64_t rows, int n_items, bool train, bool device_io);
     void refresh_host16();
@@ -122,6 +125,14 @@ private:
     uint8_t* slots_dev_ = nullptr;
     std::vector<SlotCache> cache_;
     int cache_fmt_ = -1;
+    // Write-back staging buffers ([A] or [A][M][V] like a slot) and the previous train step's
+    // deferred write-backs (layers whose updated image lives only in its ring slot until the
+    // next call's first D2H, or until flush_writebacks() before any host read).
+    uint8_t* stages_dev_ = nullptr;
+    int n_stages_ = 0;
+    size_t stage_bytes_ = 0;
+    bool staged_writeback_ = true;
+    std::vector<int> pending_wb_layers_, pending_wb_slots_;
     std::vector<int> w16_layer_;  // bf16 training: layer whose bf16 copy is current per slot
     // streams / events
     cudaStream_t s_h2d_ = nullptr, s_comp_ = nullptr, s_d2h_ = nullptr, s_upd_ = nullptr;

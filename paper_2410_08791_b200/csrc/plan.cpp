@@ -75,6 +75,7 @@ struct SlotState {
     int refs = 0;        // claimed positions not yet released
     int fill_op = -1;    // op that last wrote the weights
     int busy_op = -1;    // last op touching the slot's memory (overwrite must wait)
+    int wb_op = -1;      // a pending write-back (previous call's layer) the first writer waits for
     uint64_t stamp = 0;  // release order (FIFO tie-break)
 };
 
@@ -96,6 +97,7 @@ public:
                               initial[s].layer < n_;
         }
         ba_busy_.assign(static_cast<std::size_t>(n_slots), -1);
+        stage_busy_.assign(static_cast<std::size_t>(std::max(in.wb_stages, 0)), -1);
         act_save_op_.assign(static_cast<std::size_t>(n_), -1);
         if (in_.train) {
             std::vector<int> fwd(n_), bwd(n_);
@@ -109,6 +111,24 @@ public:
     }
 
     Plan run() {
+        // The previous call's deferred write-backs: first on the D2H engine, reading slots
+        // that still hold those layers (only the writers of those slots wait for them), in
+        // layer order - the order in which the forward releases, and overwrites, their slots.
+        std::vector<std::pair<int, int>> pending;
+        for (std::size_t i = 0; i < in_.pending_wb_layers.size(); ++i)
+            pending.emplace_back(in_.pending_wb_layers[i], in_.pending_wb_slots[i]);
+        std::sort(pending.begin(), pending.end());
+        for (const auto& [L, s] : pending) {
+            if (s < 0 || s >= static_cast<int>(slots_.size())) continue;
+            Op wb;
+            wb.kind = OpKind::D2H;
+            wb.pass = 0;
+            wb.layers = {L};
+            wb.slots = {s};
+            wb.weights = {1};
+            wb.acts = {0};
+            slots_[s].wb_op = push(std::move(wb));  // counted in the call that deferred it
+        }
         if (!in_.train) {
             // The reference holds one io activation buffer for inference (engine.cpp:60-64).
             if (in_.capacity && in_.act_bytes > in_.capacity) {
@@ -135,7 +155,36 @@ public:
         plan_.final_slots.resize(slots_.size());
         for (std::size_t s = 0; s < slots_.size(); ++s)
             plan_.final_slots[s] = SlotCache{slots_[s].layer, slots_[s].valid};
+        if (in_.defer_writeback) defer_final_writebacks();
         return plan_;
+    }
+
+    // Write-backs of layers that end the call resident (and valid) in their slot move to the
+    // next call; their Update skips the staging copy.
+    void defer_final_writebacks() {
+        for (std::size_t i = 0; i < plan_.ops.size(); ++i) {
+            Op& op = plan_.ops[i];
+            if (op.kind != OpKind::D2H || op.pass != 1) continue;
+            const int L = op.layers[0], s = op.slots[0];
+            if (!plan_.final_slots[static_cast<std::size_t>(s)].valid ||
+                plan_.final_slots[static_cast<std::size_t>(s)].layer != L)
+                continue;
+            op.deferred = true;
+            for (int dep : op.deps)
+                if (plan_.ops[static_cast<std::size_t>(dep)].kind == OpKind::Update)
+                    plan_.ops[static_cast<std::size_t>(dep)].stage = -1;
+            op.stage = -1;
+            plan_.deferred_layers.push_back(L);
+            plan_.deferred_slots.push_back(s);
+        }
+    }
+
+    // The first op that overwrites slot s after a pending write-back of its old content waits
+    // for it; every later writer is ordered after that one through the slot's own chain.
+    void wait_writeback(std::vector<int>& deps, int s) {
+        if (slots_[s].wb_op < 0) return;
+        deps.push_back(slots_[s].wb_op);
+        slots_[s].wb_op = -1;
     }
 
 private:
@@ -294,13 +343,17 @@ private:
                 op.weights.push_back(m.weights);
                 op.acts.push_back(m.act);
                 op.opts.push_back(m.opt);
+                std::vector<int> md;
                 // weights or optimizer state overwrite the slot: after its last reader
-                if ((m.weights || m.opt) && slots_[m.slot].busy_op >= 0) op.deps.push_back(slots_[m.slot].busy_op);
-                if (m.act && ba_busy_[m.slot] >= 0) op.deps.push_back(ba_busy_[m.slot]);
+                if ((m.weights || m.opt) && slots_[m.slot].busy_op >= 0) md.push_back(slots_[m.slot].busy_op);
+                if (m.act && ba_busy_[m.slot] >= 0) md.push_back(ba_busy_[m.slot]);
                 // The reload reads the pinned copy written by this layer's forward offload
                 // (the reference only reloads once act_on_host_ is set, engine.cpp:397-402).
                 const int saved = act_save_op_[static_cast<size_t>(seq()[m.pos])];
-                if (m.act && saved >= 0) op.deps.push_back(saved);
+                if (m.act && saved >= 0) md.push_back(saved);
+                if (m.weights || m.opt) wait_writeback(md, m.slot);
+                op.deps.insert(op.deps.end(), md.begin(), md.end());
+                op.move_deps.push_back(std::move(md));
                 plan_.h2d_weight_layers += m.weights;
                 plan_.h2d_act_layers += m.act;
             }
@@ -370,6 +423,7 @@ private:
         }
         if (backward() && trainable(L) && gws_busy_[L % 2] >= 0)
             op.deps.push_back(gws_busy_[L % 2]);  // dW workspace double buffer
+        if (backward() && trainable(L)) wait_writeback(op.deps, s);  // may update W in its epilogue
         // Ledger at compute begin (engine.cpp:271-282).
         if (in_.train && !backward()) ledger_add(kActivation, in_.act_bytes);
         const bool grad = backward() && trainable(L);
@@ -402,6 +456,12 @@ private:
             upd.layer = L;
             upd.slot = s;
             upd.deps.push_back(id);
+            wait_writeback(upd.deps, s);
+            if (!stage_busy_.empty()) {  // staged: the update also copies the slot to a stage
+                upd.stage = static_cast<int>(n_staged_++ % stage_busy_.size());
+                if (stage_busy_[upd.stage] >= 0) upd.deps.push_back(stage_busy_[upd.stage]);
+            }
+            const int stage = upd.stage;
             const int uid = push(std::move(upd));
             gws_busy_[L % 2] = uid;
             Op wb;  // write the updated fp32 weights back to the host master copy
@@ -411,9 +471,12 @@ private:
             wb.slots = {s};
             wb.weights = {1};
             wb.acts = {0};
+            wb.stage = stage;
             wb.deps.push_back(uid);
             const int wid = push(std::move(wb));
-            slots_[s].busy_op = wid;
+            // staged: the slot is free once the update (and its copy) is done
+            slots_[s].busy_op = stage >= 0 ? uid : wid;
+            if (stage >= 0) stage_busy_[stage] = wid;
             plan_.n_d2h_jobs += 1;
             plan_.d2h_weight_layers += 1;
             // Sharded: only this rank's shard of the slot was updated (and written back), so
@@ -483,6 +546,8 @@ private:
     std::vector<std::vector<int>> seqs_;
     std::vector<int> pos_slot_, pos_load_, pos_act_;
     std::vector<int> ba_busy_;
+    std::vector<int> stage_busy_;  // per write-back stage: the D2H that last read it
+    uint64_t n_staged_ = 0;
     std::vector<int> act_save_op_;  // per layer: the forward ActSave op (offload to host)
     int fa_busy_[3] = {-1, -1, -1};
     int gws_busy_[2] = {-1, -1};
@@ -547,7 +612,10 @@ std::string describe_plan(const Plan& plan) {
         if (op.kind == OpKind::Compute)
             os << " pos=" << op.position << " item=" << op.item << " layer=" << op.layer
                << " slot=" << op.slot;
-        if (op.kind == OpKind::Update) os << " layer=" << op.layer << " slot=" << op.slot;
+        if (op.kind == OpKind::Update) {
+            os << " layer=" << op.layer << " slot=" << op.slot;
+            if (op.stage >= 0) os << " stage=" << op.stage;
+        }
         if (op.kind == OpKind::ActSave) os << " layer=" << op.layer;
         if (op.kind == OpKind::H2D || op.kind == OpKind::D2H || op.kind == OpKind::AllGather) {
             std::vector<int> w(op.weights.begin(), op.weights.end()),
@@ -555,6 +623,16 @@ std::string describe_plan(const Plan& plan) {
             os << " layers=" << list(op.layers) << " slots=" << list(op.slots)
                << " w=" << list(w) << " a=" << list(a);
             if (!o.empty()) os << " o=" << list(o);
+            if (op.kind == OpKind::D2H && op.stage >= 0) os << " stage=" << op.stage;
+            if (op.deferred) os << " deferred=1";
+            if (op.kind == OpKind::H2D) {  // per-move dependencies: md=a.b|c|...
+                os << " md=";
+                for (std::size_t j = 0; j < op.move_deps.size(); ++j) {
+                    if (j) os << "|";
+                    for (std::size_t t = 0; t < op.move_deps[j].size(); ++t)
+                        os << (t ? "." : "") << op.move_deps[j][t];
+                }
+            }
         }
         os << " deps=" << list(op.deps) << " led=" << op.led_w << "," << op.led_a << ","
            << op.led_g << "\n";

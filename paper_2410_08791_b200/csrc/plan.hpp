@@ -60,6 +60,19 @@ struct PlanInput {
     // Optimizer state (AdamW m, v) streams with every trainable layer's backward: its H2D
     // (even when the weights are a slot hit) and its write-back ride the layer's transfers.
     bool optimizer_state = false;
+    // Staged write-back: an Update copies the updated image of its slot (HBM -> HBM, a few
+    // microseconds) into one of `wb_stages` staging buffers and the write-back D2H reads the
+    // stage, so the slot is free for the next H2D as soon as the update is done instead of
+    // after the (link-bound) D2H. 0 = write back straight from the slot.
+    int wb_stages = 0;
+    // Deferred write-back: a trained layer still resident in the ring at the end of the call
+    // (final_slots) is written back at the start of the NEXT call, on the otherwise idle D2H
+    // engine during the forward, instead of on the critical tail of this backward. Such D2H
+    // ops are marked `deferred` and listed in Plan::deferred_*; the next call passes them in
+    // pending_wb_* and gets one D2H per layer at its start, which every later writer of that
+    // slot depends on. The caller flushes pending write-backs before the host copy is read.
+    bool defer_writeback = false;
+    std::vector<int> pending_wb_layers, pending_wb_slots;
     std::vector<uint8_t> frozen;  // per layer
     uint64_t layer_bytes = 0;     // reference ledger units: (d*d + d) * 4
     uint64_t act_bytes = 0;       // rows * d * 4
@@ -85,6 +98,12 @@ struct Op {
     std::vector<uint8_t> acts;     // per moved layer: the saved activation rides along
     std::vector<uint8_t> opts;     // per moved layer: optimizer state (m, v) rides along
     std::vector<int> deps;         // op indices that must complete first (any stream)
+    // H2D: the dependencies of each moved layer alone (its slot's last reader, the offload it
+    // reloads, a pending write-back); deps = their union + the policy trigger. The executor
+    // waits per layer, so one batched job's first copy does not wait for its last slot.
+    std::vector<std::vector<int>> move_deps;
+    int stage = -1;         // Update: copy the slot to this write-back stage; D2H: read it
+    bool deferred = false;  // D2H: skipped in this call, done at the start of the next
     uint64_t led_w = 0, led_a = 0, led_g = 0;  // ledger (weight/act/grad bytes) at this op
 };
 
@@ -98,6 +117,7 @@ struct Plan {
     std::vector<Op> ops;
     LedgerPeaks ledger;
     std::vector<SlotCache> final_slots;
+    std::vector<int> deferred_layers, deferred_slots;  // write-backs left for the next call
     uint64_t n_h2d_jobs = 0, n_d2h_jobs = 0, n_evictions = 0;
     uint64_t h2d_weight_layers = 0, h2d_act_layers = 0, d2h_weight_layers = 0,
              d2h_act_layers = 0;

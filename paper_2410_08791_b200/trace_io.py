@@ -28,7 +28,9 @@ def plan_ops(text: str):
         op = {"index": int(parts[0]), "kind": parts[1]}
         for kv in parts[2:]:
             k, v = kv.split("=")
-            if k in _LIST_KEYS:
+            if k == "md":  # per-move dependency lists: a.b|c|
+                op[k] = [[int(t) for t in g.split(".") if t] for g in v.split("|")] if v else []
+            elif k in _LIST_KEYS:
                 op[k] = [int(t) for t in v.split(",")] if v else []
             else:
                 op[k] = int(v) if v else None

@@ -321,3 +321,34 @@ def test_ledger_against_the_reference_library_training_and_inference():
             [s.peak_bytes, s.peak_weight_bytes, s.peak_activation_bytes, s.peak_gradient_bytes,
              s.total_gradient_bytes]
     assert total > 300 and equal >= 0.9 * total, (equal, total)
+
+
+def test_oracle_adamw_pinned_to_torch_optim_adamw():
+    """orc_adamw (the checker of the AdamW option) restates torch.optim.AdamW's single-tensor
+    update (decoupled weight decay, bias-corrected moments). Pin it against torch in float64 on
+    the same float32 inputs over several steps, and check the scalar rounding convention."""
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(3)
+    w0 = rng.standard_normal(4099).astype(np.float32)
+    lr, b1, b2, eps, wd = 1e-3, 0.9, 0.999, 1e-8, 0.01
+    w, m, v = w0.copy(), np.zeros_like(w0), np.zeros_like(w0)
+    p = torch.nn.Parameter(torch.from_numpy(w0.astype(np.float64)))
+    opt = torch.optim.AdamW([p], lr=lr, betas=(b1, b2), eps=eps, weight_decay=wd, foreach=False)
+    for t in range(1, 6):
+        g = rng.standard_normal(4099).astype(np.float32) * (10.0 ** -t)
+        ORC.adamw(w, m, v, g, lr, b1, b2, eps, wd, t)
+        p.grad = torch.from_numpy(g.astype(np.float64))
+        opt.step()
+        ref = p.detach().numpy()
+        assert np.abs(w - ref).max() <= 1e-6 * np.abs(ref).max()
+        st = opt.state[p]
+        assert np.abs(m - st["exp_avg"].numpy()).max() <= 1e-6 * np.abs(st["exp_avg"].numpy()).max()
+        assert np.abs(v - st["exp_avg_sq"].numpy()).max() <= 1e-5 * np.abs(st["exp_avg_sq"].numpy()).max()
+    s = Oracle.adamw_scalars(lr, b1, b2, eps, wd, 3)
+    assert s["neg_step"] == float(np.float32(-lr / (1 - b1 ** 3)))
+    assert s["bc2_sqrt"] == float(np.float32(np.sqrt(1 - b2 ** 3)))
+
+
+def test_adamw_abi_is_exported_and_validates_without_a_device():
+    assert hasattr(_capi.LIB, "sp_set_optimizer") and hasattr(_capi.LIB, "sp_read_optimizer_state")
+    assert sp.OPT_SGD == 0 and sp.OPT_ADAMW == 1

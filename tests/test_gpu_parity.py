@@ -588,3 +588,42 @@ def test_training_reduces_the_loss(numerics):
         ex.register_model(model)
         losses = [ex.train_step(x, t, 0.5) for _ in range(4)]
     assert all(b < a for a, b in zip(losses, losses[1:])), losses
+
+
+@pytest.mark.parametrize("numerics", [sp.EXACT, sp.BF16])
+def test_staged_and_deferred_writeback_is_bitwise_and_flushes_on_read(numerics, monkeypatch):
+    """The executor's write-back scheme (updates copied to staging buffers; the ring's final
+    residents written back by the next call, or by a flush before any host read) against the
+    plain one (SP_WB=0, A/B switch): identical weights / losses after every step, with reads,
+    an inference call and a re-registration interleaved, for every strategy."""
+    d = 16 if numerics == sp.EXACT else 128
+    rows = 5 if numerics == sp.EXACT else 256
+    model = sp.build_model(23, 7, d, 1)
+    x, t = sp.make_input(23, 0, rows, d), sp.make_input(23, 1, rows, d)
+
+    def run(wb, s):
+        monkeypatch.setenv("SP_WB", wb)
+        out = []
+        with sp.Executor(7, d, s, numerics=numerics) as ex:
+            ex.register_model(model)
+            for i in range(4):
+                out.append(ex.train_step(x, t, 0.02))
+                if i == 1:
+                    out.append(ex.read_model(model).W.copy())     # flush mid-sequence
+                if i == 2:
+                    out.append(ex.forward([x[:3]]))               # inference flushes too
+            out.append(ex.read_model(model).W.copy())
+            ex.register_layer(3, model.W[3], model.b[3])          # re-register after training
+            out.append(ex.train_step(x, t, 0.02))
+            out.append(ex.read_model(model).W.copy())
+        return out
+
+    for s in [S(sp.STANDARD), S(sp.NAIVE, 2), S(sp.SUPERPIPELINE, 2, 1), S(sp.SUPERPIPELINE, 4, 2)]:
+        a, b = run("0", s), run("1", s)
+        for u, v in zip(a, b):
+            assert np.array_equal(np.asarray(u), np.asarray(v)), s
+    if numerics == sp.EXACT:  # and the oracle, step by step
+        W, bb = model.W.copy(), model.b.copy()
+        for _ in range(4):
+            _, W, bb = ORC.train_step(W, bb, x, t, 0.02, frozen=model.frozen)
+        assert np.array_equal(b[4], W)

@@ -15,6 +15,11 @@ its own offload). Buffers modelled:
   host master[L]      D2H(L) writes; H2D(w, L) reads
   AdamW moments MV[s] H2D(o) writes; UPDATE reads+writes; D2H reads (optimizer_state plans)
   host moments[L]     D2H(L) writes; H2D(o, L) reads
+  write-back stage[i] UPDATE(stage=i) writes (copy of its slot); D2H(stage=i) reads it instead
+                      of the slot. A deferred D2H moves nothing in its call; the next call's
+                      plan starts with that write-back (SP_PLAN_WRITEBACK shows the steady state)
+Eager prefetch: the executor waits each moved layer's own dependencies (md=) right before its
+copy, so an H2D job is checked as one sub-op per moved layer in stream order.
 """
 import itertools
 
@@ -59,15 +64,21 @@ def accesses(ops, ckpt, frozen, opt=False):
             acc.append((i, ("W", op["slot"]), True))
             if opt:
                 acc.append((i, ("MV", op["slot"]), True))
+            if op.get("stage") is not None:
+                acc.append((i, ("stage", op["stage"]), True))
         elif k == "ALLGATHER":  # sharded streaming: completes the slot over NVLink
             for s in op["slots"]:
                 acc.append((i, ("W", s), True))
         elif k == "D2H":
+            if op.get("deferred"):
+                continue  # nothing moves in this call
             for L, s in zip(op["layers"], op["slots"]):
-                acc.append((i, ("W", s), False))
+                src = ("stage", op["stage"]) if op.get("stage") is not None else ("W", s)
+                acc.append((i, src, False))
                 acc.append((i, ("host", L), True))
                 if opt:
-                    acc.append((i, ("MV", s), False))
+                    if op.get("stage") is None:
+                        acc.append((i, ("MV", s), False))
                     acc.append((i, ("hostMV", L), True))
         elif k == "ACTSAVE":
             L = op["layer"]
@@ -94,19 +105,43 @@ def happens_before(ops):
     return lambda a, b: bool(reach[b] >> a & 1)
 
 
+def split_moves(ops):
+    """Eager mode: one sub-op per moved layer of each H2D job, waiting only its own md deps
+    (plus stream order); dependents of the job wait for its last sub-op."""
+    last, out = {}, []
+    for op in ops:
+        if op["kind"] == "H2D" and op.get("md") is not None and len(op["layers"]) > 0:
+            for j in range(len(op["layers"])):
+                sub = {k: ([v[j]] if k in ("layers", "slots", "w", "a", "o") and isinstance(v, list) else v)
+                       for k, v in op.items()}
+                sub["deps"] = [last[d] for d in (op["md"][j] if j < len(op["md"]) else [])]
+                sub["index"] = len(out)
+                out.append(sub)
+        else:
+            sub = dict(op, deps=[last[d] for d in op["deps"]], index=len(out))
+            out.append(sub)
+        last[op["index"]] = len(out) - 1
+    return out
+
+
 def check(n, strategy, train, ckpt, items=1, frozen=None, sharded=False, opt=False):
     # both dependency modes: the reference policy's triggers, and eager prefetch (an H2D waits
-    # only for its slot) - the executor's default, which must be just as race-free
+    # only for its slot) - the executor's default, which must be just as race-free; training
+    # also with the executor's write-back scheme (staged + deferred, steady state)
     for eager in (False, True):
-        check_one(n, strategy, train, ckpt, items, frozen, sharded, eager, opt)
+        for wb in ((False, True) if train else (False,)):
+            check_one(n, strategy, train, ckpt, items, frozen, sharded, eager, opt, wb)
 
 
-def check_one(n, strategy, train, ckpt, items, frozen, sharded, eager, opt=False):
+def check_one(n, strategy, train, ckpt, items, frozen, sharded, eager, opt=False, wb=False):
     frozen = frozen or [0] * n
     txt = sp.describe_plan(n, 8, strategy, n_items=items, train=train, checkpointing=ckpt,
-                           frozen=frozen, sharded=sharded, eager=eager, optimizer_state=opt)
+                           frozen=frozen, sharded=sharded, eager=eager, optimizer_state=opt,
+                           writeback=wb)
     assert not txt.startswith("ERROR"), txt
     head, ops = parse_plan(txt)
+    if eager:
+        ops = split_moves(ops)
     ck = ckpt and train and strategy.kind != sp.STANDARD
     hb = happens_before(ops)
     by_res = {}
@@ -120,7 +155,7 @@ def check_one(n, strategy, train, ckpt, items, frozen, sharded, eager, opt=False
                 continue
             assert hb(a, b), (f"unordered {res}: op {a} {ops[a]['kind']} and op {b} "
                               f"{ops[b]['kind']} (n={n} {strategy} train={train} ckpt={ckpt} "
-                              f"eager={eager})")
+                              f"eager={eager} writeback={wb} opt={opt})")
 
 
 STRATS = [sp.StrategyConfig(sp.STANDARD), sp.StrategyConfig(sp.NAIVE, 1),
@@ -245,3 +280,65 @@ def test_eager_prefetch_changes_only_the_trigger_dependencies():
                 assert x["deps"] == y["deps"]
             relaxed += len(set(x["deps"]) - set(y["deps"]))
         assert relaxed > 0
+
+
+def _violations(ops, ckpt, frozen, opt=False):
+    hb = happens_before(ops)
+    by_res, bad = {}, 0
+    for i, res, w in accesses(ops, ckpt, frozen, opt):
+        by_res.setdefault(res, []).append((i, w))
+    for res, lst in by_res.items():
+        for (a, wa), (b, wb) in itertools.combinations(sorted(lst), 2):
+            if (wa or wb) and a != b and STREAM[ops[a]["kind"]] != STREAM[ops[b]["kind"]] and not hb(a, b):
+                bad += 1
+    return bad
+
+
+@pytest.mark.parametrize("opt", [False, True])
+def test_writeback_scheme_edges_are_each_necessary(opt):
+    """The staged / deferred write-back plan is race-free (above) and each of its new edges is
+    load-bearing: dropping the waits on the previous call's write-backs, or on a stage's last
+    reader, or one moved layer's own md deps, makes the checker fire."""
+    n, s = 16, sp.StrategyConfig(sp.SUPERPIPELINE, 4, 2)  # 10 staged write-backs > 6 stages
+    txt = sp.describe_plan(n, 8, s, train=True, eager=True, writeback=True, optimizer_state=opt)
+    head, ops = parse_plan(txt)
+    pend = {o["index"] for o in ops if o["kind"] == "D2H" and o["pass"] == 0}
+    assert pend and any(o.get("deferred") for o in ops) and any(o.get("stage") is not None for o in ops)
+    base = split_moves(ops)
+    assert _violations(base, False, [0] * n, opt) == 0
+
+    def drop(pred):
+        cut = [dict(o) for o in ops]
+        for o in cut:
+            o["deps"] = [d for d in o["deps"] if not pred(o, d)]
+            if o.get("md") is not None:
+                o["md"] = [[d for d in md if not pred(o, d)] for md in o["md"]]
+        return split_moves(cut)
+
+    assert _violations(drop(lambda o, d: d in pend), False, [0] * n, opt) > 0
+    stage_readers = {o["index"] for o in ops if o["kind"] == "D2H" and o.get("stage") is not None}
+    assert _violations(drop(lambda o, d: o["kind"] == "UPDATE" and d in stage_readers),
+                       False, [0] * n, opt) > 0
+    # the per-move split itself: give every move the first move's deps only
+    cut = [dict(o) for o in ops]
+    for o in cut:
+        if o["kind"] == "H2D" and len(o.get("md") or []) > 1:
+            o["md"] = [o["md"][0]] + [[] for _ in o["md"][1:]]
+    assert _violations(split_moves(cut), False, [0] * n, opt) > 0
+
+
+def test_writeback_scheme_keeps_policy_ops_and_moves_tail_writebacks():
+    """Same backward compute / H2D sequence as the plain plan; the trained layers still
+    resident at the end (the ring's last S backward layers) are written back by the next call."""
+    n, s = 12, sp.StrategyConfig(sp.SUPERPIPELINE, 4, 2)
+    plain = parse_plan(sp.describe_plan(n, 8, s, train=True, eager=True))[1]
+    steady = parse_plan(sp.describe_plan(n, 8, s, train=True, eager=True, writeback=True))[1]
+    key = lambda o: (o["kind"], o.get("layer"), o.get("layers"), o.get("slots"))  # noqa: E731
+    # (the plain plan is a cold first call: compare the backward, which starts from the same
+    # ring state either way)
+    assert [key(o) for o in plain if o["kind"] in ("COMPUTE", "H2D") and o["pass"] == 1] == \
+        [key(o) for o in steady if o["kind"] in ("COMPUTE", "H2D") and o["pass"] == 1]
+    pending = [o["layers"][0] for o in steady if o["kind"] == "D2H" and o["pass"] == 0]
+    deferred = [o["layers"][0] for o in steady if o.get("deferred")]
+    assert sorted(pending) == sorted(deferred) == list(range(6))  # S = k + k' = 6
+    assert pending == sorted(pending)  # forward order: the first slot reused is freed first
