@@ -663,15 +663,18 @@ void Executor::enqueue_op(const Plan& plan, int i, bool train, int n_items, int6
         for (int dep : op.deps) wait(dep);
     // Timing events are "external" so that, under graph capture, they become event-record
     // nodes; the dependency events (ev_dep_) become graph edges.
-    if (cfg_.trace >= 1) record_timing(ev_start_[static_cast<size_t>(i)], st);
+    // (per-move H2D: the start is taken once the first copy's own waits are satisfied)
+    if (cfg_.trace >= 1 && !per_move) record_timing(ev_start_[static_cast<size_t>(i)], st);
     const size_t dd = static_cast<size_t>(d_) * d_;
     const size_t act_b = static_cast<size_t>(rows) * d_ * (bf16_ ? 2 : 4);
     switch (op.kind) {
         case OpKind::H2D:
             for (size_t j = 0; j < op.layers.size(); ++j) {
                 const int L = op.layers[j], s = op.slots[j];
-                if (per_move)
+                if (per_move) {
                     for (int dep : op.move_deps[j]) wait(dep);
+                    if (j == 0 && cfg_.trace >= 1) record_timing(ev_start_[static_cast<size_t>(i)], st);
+                }
                 if (op.weights[j]) {
                     // Whole image, or (sharded) only this rank's [lo, hi) byte range of it.
                     const bool wire = fmt == kFmtBf16Infer;
@@ -721,14 +724,11 @@ void Executor::enqueue_op(const Plan& plan, int i, bool train, int n_items, int6
                 if (sharded_) shard_range(shardA_, layer_bytes(), lo, hi);
                 uint8_t* stage = stage_ptr(op.stage);
                 const uint8_t* slot = slot_ptr(op.slot);
-                if (hi > lo) {
-                    CUDA_OK(cudaMemcpyAsync(stage + lo, slot + lo, hi - lo, cudaMemcpyDeviceToDevice, st));
-                    if (adamw()) {
-                        CUDA_OK(cudaMemcpyAsync(stage + off_m_ + lo, slot + off_m_ + lo, hi - lo,
-                                                cudaMemcpyDeviceToDevice, st));
-                        CUDA_OK(cudaMemcpyAsync(stage + off_v_ + lo, slot + off_v_ + lo, hi - lo,
-                                                cudaMemcpyDeviceToDevice, st));
-                    }
+                if (hi > lo) {  // an SM kernel: copy engines stay with the PCIe transfers
+                    void* dst[3] = {stage + lo, stage + off_m_ + lo, stage + off_v_ + lo};
+                    const void* src[3] = {slot + lo, slot + off_m_ + lo, slot + off_v_ + lo};
+                    copy_regions(dst, src, adamw() ? 3 : 1, static_cast<int64_t>(hi - lo), st);
+                    ++kernels_;
                 }
             }
             break;

@@ -111,6 +111,8 @@ void scale_inplace(float* x, int64_t count, float s, cudaStream_t st);
 struct AdamwScalars {
     float decay, omb1, b2, omb2, bc2_sqrt, eps, neg_step, pad;
 };
+// n (<= 3) device-to-device copies of `bytes` each (multiple of 4, 4-byte aligned) on the SMs.
+void copy_regions(void* const* dst, const void* const* src, int n, int64_t bytes, cudaStream_t st);
 void adamw_reduce(float* w, float* m, float* v, const float* parts, int nparts, int64_t stride,
                   int64_t count, const AdamwScalars* scalars, cudaStream_t st);
 

@@ -328,6 +328,39 @@ void adamw_reduce(float* w, float* m, float* v, const float* parts, int nparts, 
                parts, nparts, stride, count, scalars);
 }
 
+// Up to three equal-size device copies in one launch (blockIdx.y = region) on the SMs: the
+// write-back staging copy must not queue on a copy engine the PCIe transfers are using.
+struct CopyRegions {
+    void* dst[3];
+    const void* src[3];
+};
+
+__global__ void copy_regions_kernel(CopyRegions r, int64_t bytes) {
+    pdl_wait_then_release();
+    const int k = blockIdx.y;
+    const int64_t n16 = bytes / 16;
+    const int64_t gs = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    const int64_t t0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const uint4* s = static_cast<const uint4*>(r.src[k]);
+    uint4* d = static_cast<uint4*>(r.dst[k]);
+    for (int64_t i = t0; i < n16; i += gs) d[i] = s[i];
+    const uint32_t* s4 = static_cast<const uint32_t*>(r.src[k]);
+    uint32_t* d4 = static_cast<uint32_t*>(r.dst[k]);
+    for (int64_t i = n16 * 4 + t0; i < bytes / 4; i += gs) d4[i] = s4[i];
+}
+
+void copy_regions(void* const* dst, const void* const* src, int n, int64_t bytes, cudaStream_t st) {
+    if (n < 1 || bytes <= 0) return;
+    CopyRegions r{};
+    for (int k = 0; k < n && k < 3; ++k) {
+        r.dst[k] = dst[k];
+        r.src[k] = src[k];
+    }
+    const int64_t n16 = bytes / 16 + 1;
+    const int blocks = static_cast<int>(std::min<int64_t>((n16 + kThreads - 1) / kThreads, 296));
+    launch_pdl(copy_regions_kernel, dim3(blocks, std::min(n, 3)), dim3(kThreads), 0, st, r, bytes);
+}
+
 void scale_inplace(float* x, int64_t count, float s, cudaStream_t st) {
     launch_pdl(scale_kernel, dim3(grid_for(count)), dim3(kThreads), 0, st, x, count, s);
 }

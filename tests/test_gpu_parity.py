@@ -626,4 +626,4 @@ def test_staged_and_deferred_writeback_is_bitwise_and_flushes_on_read(numerics, 
         W, bb = model.W.copy(), model.b.copy()
         for _ in range(4):
             _, W, bb = ORC.train_step(W, bb, x, t, 0.02, frozen=model.frozen)
-        assert np.array_equal(b[4], W)
+        assert np.array_equal(b[6], W)

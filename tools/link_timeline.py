@@ -87,3 +87,10 @@ head = sorted(tr, key=lambda e: e["t_start"])[:10]
 print("head:")
 for e in head:
     print(f"  {e['kind']:8s} L={e['layer']:3d} bwd={int(e['backward'])} [{e['t_start']:8.3f} {e['t_end']:8.3f}]")
+if os.environ.get("SEGMENT"):
+    lo, hi = (float(v) for v in os.environ["SEGMENT"].split(","))
+    print("segment:")
+    for e in sorted(tr, key=lambda e: e["t_start"]):
+        if lo <= e["t_start"] <= hi and e["kind"] != "Stall":
+            print(f"  {e['kind']:8s} L={e['layer']:3d} bwd={int(e['backward'])} [{e['t_start']:8.3f} {e['t_end']:8.3f}] "
+                  f"dur={e['t_end'] - e['t_start']:.3f}")
