@@ -54,6 +54,8 @@ def parse():
                    help="sgd: the reference's update (default); adamw: fp32 m, v in pinned host "
                         "memory streamed with each backward layer, fused AdamW update")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-variants", action="store_true",
+                   help="skip the in-run AdamW variant of the same step (reported under 'variants')")
     p.add_argument("--sweep", default="", help="comma list of k:kp to report extra lines")
     return p.parse_args()
 
@@ -251,21 +253,24 @@ def cpu_baseline_ref(a, threads, rows_per_thread=2, layers_sample=6):
     return threads * rows_per_thread / full, dt
 
 
+REF_ROWS = 16  # rows per host thread per reference-arm step (~1 s of CPU work per step)
+
+
 def run_reference(a, rank, world):
     if rank != 0:
         return
     threads = max(1, min(os.cpu_count() or 1, 64))
     rates = []
     for i in range(a.warmup + a.steps):
-        v, dt = cpu_baseline_ref(a, threads)
+        v, dt = cpu_baseline_ref(a, threads, rows_per_thread=REF_ROWS)
         if i >= a.warmup:
             rates.append(v)
     value = statistics.mean(rates)
-    sample = (f"{threads} concurrent reference_train_step replicas x 2 rows x 6 of {a.layers} "
-              f"layers (d={a.d}), time scaled x{a.layers / 6:g} to the full model")
+    sample = (f"{threads} concurrent reference_train_step replicas x {REF_ROWS} rows x 6 of "
+              f"{a.layers} layers (d={a.d}), time scaled x{a.layers / 6:g} to the full model")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "samples/s",
             "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
-            "ms_per_step": 1e3 * (2 * threads) / value, "higher_is_better": True,
+            "ms_per_step": 1e3 * (REF_ROWS * threads) / value, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": config_of(a, world),
             "cpu_baseline": {"value": value, "unit": "samples/s", "cores": threads,
@@ -315,11 +320,11 @@ def main():
         _capi.LIB.sp_build_layer(7, i, a.d, 0, 0, Wl.ctypes.data, bl.ctypes.data)
         weights.append((Wl, bl))
 
-    def make_executor(strat):
+    def make_executor(strat, opt=a.optimizer):
         e = sp.Executor(a.layers, a.d, strat, numerics=sp.BF16, device=local, trace=0)
         for i, (Wl, bl) in enumerate(weights):
             e.register_layer(i, Wl, bl)
-        if a.optimizer == "adamw":
+        if opt == "adamw":
             e.set_optimizer(sp.OPT_ADAMW, 0.9, 0.999, 1e-8, 0.01)
         return e
 
@@ -375,6 +380,34 @@ def main():
         ms, losses = timed(step_dev, stats)
     ms_e2e, _ = timed(step_e2e, None)
     last = stats[-1]
+    variants = {}
+    if a.optimizer == "sgd" and not a.no_variants:
+        # The same step with AdamW (north_star: optimizer state in pinned host DRAM, fused
+        # update), timed the same way in the same run; the headline stays the reference's SGD.
+        ev = make_executor(strategy, "adamw")
+        if world > 1:
+            dp.init_executor_dp(ev, dist, rank, world)
+        for _ in range(a.warmup):
+            ev.train_step_ptr(x_dev.data_ptr(), t_dev.data_ptr(), a.rows, a.lr, device=True)
+        barrier()
+        torch.cuda.synchronize()
+        v0, v1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        v0.record()
+        for _ in range(a.steps):
+            ev.train_step_ptr(x_dev.data_ptr(), t_dev.data_ptr(), a.rows, a.lr, device=True)
+        v1.record()
+        torch.cuda.synchronize()
+        vms = v0.elapsed_time(v1)
+        if world > 1:
+            vms = dp.max_over_ranks(dist, torch, vms)
+        va = argparse.Namespace(**dict(vars(a), optimizer="adamw"))
+        vroof = layer_roofline(va, link, pk, a.rows, ev.stats()["n_slots"], world if world > 1 else 1)
+        variants["adamw"] = {"value": world * a.rows * a.steps / (vms * 1e-3), "unit": "samples/s",
+                             "ms_per_step": vms / a.steps, "ring_roofline_ms": vroof * 1e3,
+                             "frac_of_ring_roofline": vroof / (vms * 1e-3 / a.steps),
+                             "h2d_gb_per_step": ev.stats()["h2d_bytes"] / 1e9,
+                             "d2h_gb_per_step": ev.stats()["d2h_bytes"] / 1e9}
+        ev.close()
     # One extra step with the per-op CUDA-event timeline (not timed): stall / compute split.
     ex.set_trace(1)
     step_dev()
@@ -401,9 +434,9 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
-        v, dt = cpu_baseline_ref(a, 1, rows_per_thread=4, layers_sample=6)
+        v, dt = cpu_baseline_ref(a, 1, rows_per_thread=128, layers_sample=6)
         cpu = {"value": v, "unit": "samples/s", "cores": 1, "kind": "reference",
-               "sample": f"reference_train_step (oracle/_ref), 4 rows x 6 of {a.layers} layers "
+               "sample": f"reference_train_step (oracle/_ref), 128 rows x 6 of {a.layers} layers "
                          f"d={a.d}, {dt:.1f}s, scaled x{a.layers / 6:g} in layers"}
 
     line = {"metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
@@ -428,6 +461,7 @@ def main():
                          "gemm_share_of_step": gemm_s / step_s,
                          "method": "CUDA events around 20 back-to-back launches per shape on the "
                                    "launching stream, step-weighted by launches per step"},
+            "variants": variants,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e, "unit": "samples/s",
                     "h2d_bytes_per_step": 2 * a.rows * a.d * 4, "d2h_bytes_per_step": 4},

@@ -73,6 +73,8 @@ def trace_rows(executor, layer_bytes: int, act_bytes: int):
             pending_stall = ev
             continue
         op = ops[ev["op_index"]]
+        if op.get("deferred"):
+            continue  # this write-back runs at the start of the next call (its own row there)
         led = op.get("led", [0, 0, 0])
         row = {"t_start": ev["t_start"] * 1e-3, "t_end": ev["t_end"] * 1e-3,
                "weight_bytes": led[0], "activation_bytes": led[1], "gradient_bytes": led[2]}
