@@ -116,36 +116,51 @@ class Clocks:
                 "samples": len(sm)}
 
 
-def measure_link(torch, mb=256):
+def measure_link(torch, mb=256, chunk=10 << 20):
+    """Pinned host <-> HBM bandwidth per direction, alone and duplex (both at once). Two copy
+    shapes: one 256 MB copy per direction, and trains of `chunk`-byte copies (the ring's
+    layer-sized transfers). Each rate reported is the better of the two, so the roofline
+    that divides by it is a bound the executor cannot beat by copy shape."""
     n = mb << 20
     ha = torch.empty(n, dtype=torch.uint8, pin_memory=True)
     hb = torch.empty(n, dtype=torch.uint8, pin_memory=True)
     da = torch.empty(n, dtype=torch.uint8, device="cuda")
     db = torch.empty(n, dtype=torch.uint8, device="cuda")
     s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    nc = max(1, min(n // max(chunk, 1), 48))
 
-    def run(h2d, d2h, reps=6):
+    def run(h2d, d2h, reps=6, chunked=False):
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(s1)
         s2.wait_event(e0)
-        for _ in range(reps):
-            if h2d:
-                with torch.cuda.stream(s1):
-                    da.copy_(ha, non_blocking=True)
-            if d2h:
-                with torch.cuda.stream(s2):
-                    hb.copy_(db, non_blocking=True)
+        moved = 0
+        for _ in range(reps if not chunked else 2):
+            parts = [(i * chunk, (i + 1) * chunk) for i in range(nc)] if chunked else [(0, n)]
+            for lo, hi in parts:
+                if h2d:
+                    with torch.cuda.stream(s1):
+                        da[lo:hi].copy_(ha[lo:hi], non_blocking=True)
+                if d2h:
+                    with torch.cuda.stream(s2):
+                        hb[lo:hi].copy_(db[lo:hi], non_blocking=True)
+                moved += hi - lo
         ev = torch.cuda.Event()
         ev.record(s2)
         s1.wait_event(ev)
         e1.record(s1)
         e1.synchronize()
-        return n * reps / (e0.elapsed_time(e1) * 1e-3) / 1e9
+        return moved / (e0.elapsed_time(e1) * 1e-3) / 1e9
 
     run(True, True, 2)
-    return {"h2d_gbs": run(True, False), "d2h_gbs": run(False, True),
-            "duplex_gbs_per_dir": run(True, True)}
+    out = {}
+    for key, h, dn in (("h2d_gbs", True, False), ("d2h_gbs", False, True), ("duplex_gbs_per_dir", True, True)):
+        big, small = run(h, dn), run(h, dn, chunked=True)
+        out[key] = max(big, small)
+        out[key + "_256mb"] = big
+        out[key + "_chunked"] = small
+    out["chunk_bytes"] = chunk
+    return out
 
 
 def gemm_kernel_timing(torch, capi, a, reps=20):
@@ -341,7 +356,7 @@ def main():
     ht = sp.HostBuffer(t.shape)
     hx.array[...] = x
     ht.array[...] = t
-    link = measure_link(torch)
+    link = measure_link(torch, chunk=(a.d * a.d + a.d) * 4)
     torch.cuda.synchronize()
 
     def step_dev():

@@ -34,15 +34,22 @@ def link_ms(a, b, link):
     return max(a / h2d, b / d2h, (a + b) / (2 * dup))
 
 
-def roofline_ms(n, d, rows, ckpt, link, peak):
+def roofline_ms(n, d, rows, ckpt, link, peak, slots):
+    """Ring lower bound (bench.layer_roofline, plus activation offload): S slots carry at
+    most S layers across each direction reversal, so forward and backward each load >= n - S
+    layers; every layer writes back; with offload each forward layer's input goes D2H and
+    comes back H2D in the backward."""
+    S = min(slots, n)
     lb = (d * d + d) * 4           # fp32 master per layer, each direction
     act = rows * d * 2             # bf16 saved activation per layer
     fwd_flop, bwd_flop = 2.0 * rows * d * d / peak, 4.0 * rows * d * d / peak
-    # forward: weight H2D (|| activation D2H when offloading); backward: weight (+ activation)
-    # H2D || updated-weight D2H
-    fwd = max(fwd_flop, link_ms(lb, act if ckpt else 0, link))
-    bwd = max(bwd_flop, link_ms(lb + (act if ckpt else 0), lb, link))
-    return 1e3 * n * (fwd + bwd)
+    t = 0.0
+    for L in range(n):             # forward: the first S layers are still resident
+        t += max(fwd_flop, link_ms(lb if L >= S else 0, act if ckpt else 0, link))
+    for pos in range(n):           # backward, layer n-1 first (layer 0 needs no dX)
+        fl = fwd_flop if pos == n - 1 else bwd_flop
+        t += max(fl, link_ms((lb if pos >= S else 0) + (act if ckpt else 0), lb, link))
+    return 1e3 * t
 
 
 def main():
@@ -52,7 +59,7 @@ def main():
     p.add_argument("--lr", type=float, default=0.01)
     a = p.parse_args()
     peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["bf16_tflops_sustained"] * 1e12
-    link = bench.measure_link(torch)
+    link = bench.measure_link(torch, chunk=(1280 * 1280 + 1280) * 4)
     print(json.dumps({"link": link}), flush=True)
     for name in a.configs:
         c = CONFIGS[name]
@@ -77,7 +84,7 @@ def main():
                 torch.cuda.synchronize()
                 ms = e0.elapsed_time(e1) / a.steps
                 st = ex.stats()
-                roof = roofline_ms(n, d, rows, ckpt, link, peak)
+                roof = roofline_ms(n, d, rows, ckpt, link, peak, st["n_slots"])
                 print(json.dumps({
                     "config": name, "layers": n, "d": d, "rows": rows, "k": k, "k_prime": kp,
                     "checkpointing": ckpt, "ms_per_step": ms, "samples_per_s": rows / ms * 1e3,
