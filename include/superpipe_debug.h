@@ -39,6 +39,15 @@ int sp_debug_gemm_bf16_masked_async(int32_t M, int32_t N, int32_t K, const void*
                                     int32_t relu, const void* gate, int32_t ldg, int32_t splits,
                                     int32_t block_n, int32_t cta, void* stream, void* mask_out,
                                     const void* gate_mask);
+/* The tf32 GEMM (fp32 A/B multiplied with tcgen05 kind::tf32, SP_NUMERICS_TF32): arguments
+ * as sp_debug_gemm_bf16_masked_async with fp32 operands; epilogue 1 (fp32 act(acc+bias), with
+ * mask_out), 5 (fp32 ReLU-gated by an fp32 `gate` or by gate_mask), 3, 4. */
+int sp_debug_gemm_tf32_async(int32_t M, int32_t N, int32_t K, const void* A, int32_t lda,
+                             int32_t a_mn, const void* B, int32_t ldb, int32_t b_mn,
+                             int32_t epilogue, void* out, int32_t ldo, const float* bias,
+                             int32_t relu, const void* gate, int32_t ldg, int32_t splits,
+                             int32_t block_n, int32_t cta, void* stream, void* mask_out,
+                             const void* gate_mask);
 /* Sharded streaming geometry (the executor's own functions): shard size for an image of
  * img bytes over world ranks, and rank's byte range [lo, hi). */
 uint64_t sp_debug_shard_range(uint64_t img, int32_t world, int32_t rank, uint64_t* lo,

@@ -71,6 +71,7 @@ EXPORTS = [
     "sp_describe_plan", "sp_build_layer", "sp_make_input", "sp_digest_tensors",
     "sp_digest_train",
     "sp_debug_gemm_bf16", "sp_debug_gemm_bf16_async", "sp_debug_gemm_bf16_masked_async",
+    "sp_debug_gemm_tf32_async",
     "sp_debug_effective_splits",
     "sp_debug_shard_range", "sp_debug_dw_splits", "sp_debug_dw_choice",
 ]
@@ -121,6 +122,8 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "sp_debug_gemm_bf16_masked_async": ([i32, i32, i32, vp, i32, i32, vp, i32, i32, i32, vp,
                                              i32, vp, i32, vp, i32, i32, i32, i32, vp, vp, vp],
                                             C.c_int),
+        "sp_debug_gemm_tf32_async": ([i32, i32, i32, vp, i32, i32, vp, i32, i32, i32, vp,
+                                      i32, vp, i32, vp, i32, i32, i32, i32, vp, vp, vp], C.c_int),
         "sp_debug_effective_splits": ([i32, i32], i32),
         "sp_debug_dw_splits": ([i32, i64], i32),
         "sp_debug_dw_choice": ([i32, i64, i32, C.POINTER(i32), C.POINTER(i32)], i32),

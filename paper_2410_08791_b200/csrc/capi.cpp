@@ -288,6 +288,24 @@ void sp_digest_tensors(const float* values, int32_t n_items, int64_t rows, int32
 #include "../../include/superpipe_debug.h"
 #include "kernels.hpp"
 
+namespace {
+int debug_gemm(int32_t M, int32_t N, int32_t K, const void* A, int32_t lda, int32_t a_mn,
+               const void* B, int32_t ldb, int32_t b_mn, int32_t epilogue, void* out, int32_t ldo,
+               const float* bias, int32_t relu, const void* gate, int32_t ldg, int32_t splits,
+               int32_t block_n, int32_t cta, void* stream, void* mask_out, const void* gate_mask,
+               bool tf32);
+}  // namespace
+
+extern "C" int sp_debug_gemm_tf32_async(int32_t M, int32_t N, int32_t K, const void* A,
+                                        int32_t lda, int32_t a_mn, const void* B, int32_t ldb,
+                                        int32_t b_mn, int32_t epilogue, void* out, int32_t ldo,
+                                        const float* bias, int32_t relu, const void* gate,
+                                        int32_t ldg, int32_t splits, int32_t block_n, int32_t cta,
+                                        void* stream, void* mask_out, const void* gate_mask) {
+    return debug_gemm(M, N, K, A, lda, a_mn, B, ldb, b_mn, epilogue, out, ldo, bias, relu, gate, ldg,
+                      splits, block_n, cta, stream, mask_out, gate_mask, true);
+}
+
 extern "C" int sp_debug_gemm_bf16_masked_async(int32_t M, int32_t N, int32_t K, const void* A,
                                                int32_t lda, int32_t a_mn, const void* B,
                                                int32_t ldb, int32_t b_mn, int32_t epilogue,
@@ -296,7 +314,18 @@ extern "C" int sp_debug_gemm_bf16_masked_async(int32_t M, int32_t N, int32_t K, 
                                                int32_t splits, int32_t block_n, int32_t cta,
                                                void* stream, void* mask_out,
                                                const void* gate_mask) {
+    return debug_gemm(M, N, K, A, lda, a_mn, B, ldb, b_mn, epilogue, out, ldo, bias, relu, gate, ldg,
+                      splits, block_n, cta, stream, mask_out, gate_mask, false);
+}
+
+namespace {
+int debug_gemm(int32_t M, int32_t N, int32_t K, const void* A, int32_t lda, int32_t a_mn,
+               const void* B, int32_t ldb, int32_t b_mn, int32_t epilogue, void* out, int32_t ldo,
+               const float* bias, int32_t relu, const void* gate, int32_t ldg, int32_t splits,
+               int32_t block_n, int32_t cta, void* stream, void* mask_out, const void* gate_mask,
+               bool tf32) {
     sp::GemmProblem g;
+    g.tf32 = tf32;
     g.M = M;
     g.N = N;
     g.K = K;
@@ -322,6 +351,7 @@ extern "C" int sp_debug_gemm_bf16_masked_async(int32_t M, int32_t N, int32_t K, 
     g.gate_mask = static_cast<const uint32_t*>(gate_mask);
     return static_cast<int>(sp::gemm_bf16(g, static_cast<cudaStream_t>(stream)));
 }
+}  // namespace
 
 extern "C" int sp_debug_gemm_bf16_async(int32_t M, int32_t N, int32_t K, const void* A,
                                         int32_t lda, int32_t a_mn, const void* B, int32_t ldb,

@@ -31,7 +31,8 @@ enum GemmEpilogue : int {
     EPI_BIAS_ACT_F32 = 1,   // out(f32)  = act(acc + bias)
     EPI_GATE_BF16 = 2,      // out(bf16) = (relu && gate <= 0) ? 0 : acc
     EPI_F32 = 3,            // out(f32)  = acc  (split-K partial at out + split*split_stride)
-    EPI_SGD_F32 = 4         // out(f32) -= lr * acc  (fused SGD on the fp32 master; splits == 1)
+    EPI_SGD_F32 = 4,        // out(f32) -= lr * acc  (fused SGD on the fp32 master; splits == 1)
+    EPI_GATE_F32 = 5        // out(f32)  = (relu && gate <= 0) ? 0 : acc  (tf32 path; fp32 gate)
 };
 
 struct GemmProblem {
@@ -49,7 +50,7 @@ struct GemmProblem {
     int ldo = 0;
     const float* bias = nullptr;
     int relu = 0;
-    const void* gate = nullptr;  // bf16 [M][ldg]
+    const void* gate = nullptr;  // [M][ldg], bf16 (EPI_GATE_BF16) or fp32 (EPI_GATE_F32)
     int ldg = 0;
     int splits = 1;
     int64_t split_stride = 0;
@@ -62,6 +63,10 @@ struct GemmProblem {
     uint32_t* mask_out = nullptr;
     // EPI_GATE_BF16: gate with such a mask instead of reading the bf16 gate tensor.
     const uint32_t* gate_mask = nullptr;
+    // Operands A and B are fp32 and multiplied as tf32 (tcgen05 kind::tf32) instead of bf16
+    // (kind::f16). Epilogues: EPI_BIAS_ACT_F32 (with mask_out), EPI_GATE_F32 (gate: fp32
+    // tensor or gate_mask), EPI_F32, EPI_SGD_F32.
+    bool tf32 = false;
 };
 
 struct GemmChoice {
@@ -80,10 +85,10 @@ int choose_splits(int M, int N, int K, int block_n);
 struct DwChoice {
     int cta, block_n, splits;
 };
-DwChoice choose_dw(int M, int N, int K, int max_splits, bool fused_ok);
+DwChoice choose_dw(int M, int N, int K, int max_splits, bool fused_ok, bool tf32 = false);
 int choose_block_n(int N);
 // Split count actually used for K (no empty split): what gemm_bf16 will launch.
-int effective_splits(int K, int splits);
+int effective_splits(int K, int splits, bool tf32 = false);
 int num_sms();
 
 void convert_f32_to_bf16(const float* src, void* dst, int64_t count, cudaStream_t st);
@@ -92,10 +97,15 @@ void convert_f32_to_bf16(const float* src, void* dst, int64_t count, cudaStream_
 // fixed order into *out (raw sum; caller divides by N).
 int loss_grad_bf16(const float* y, const float* t, int64_t count, float inv_n, int relu,
                    void* g, float* partials, cudaStream_t st);
+// The same with an fp32 gradient (tf32 path).
+int loss_grad_f32(const float* y, const float* t, int64_t count, float inv_n, int relu,
+                  float* g, float* partials, cudaStream_t st);
 void loss_finalize(const float* partials, int n, float* out, cudaStream_t st);
 // Column sums of a bf16 [rows][d] matrix into partials[chunks][d] (fixed chunking).
 int colsum_bf16(const void* x, int64_t rows, int d, float* partials, cudaStream_t st);
 int colsum_chunks(int64_t rows);
+// Column sums of an fp32 [rows][d] matrix (d % 4 == 0), same chunking (tf32 path).
+int colsum_f32(const float* x, int64_t rows, int d, float* partials, cudaStream_t st);
 // grad[i] = sum_s parts[s*stride + i] (fixed order).
 void reduce_partials(const float* parts, int nparts, int64_t stride, int64_t count,
                      float* grad, cudaStream_t st);

@@ -58,9 +58,26 @@ __device__ __forceinline__ float grad_elem(float y, float t, float inv_n, int re
     return g;
 }
 
+__device__ __forceinline__ void store_grad4(__nv_bfloat16* g, int64_t i, float a, float b, float c, float d) {
+    __nv_bfloat162 lo = __floats2bfloat162_rn(a, b);
+    __nv_bfloat162 hi = __floats2bfloat162_rn(c, d);
+    uint2 packed;
+    packed.x = *reinterpret_cast<uint32_t*>(&lo);
+    packed.y = *reinterpret_cast<uint32_t*>(&hi);
+    reinterpret_cast<uint2*>(g)[i] = packed;
+}
+__device__ __forceinline__ void store_grad4(float* g, int64_t i, float a, float b, float c, float d) {
+    reinterpret_cast<float4*>(g)[i] = make_float4(a, b, c, d);
+}
+__device__ __forceinline__ void store_grad1(__nv_bfloat16* g, int64_t i, float a) { g[i] = __float2bfloat16_rn(a); }
+__device__ __forceinline__ void store_grad1(float* g, int64_t i, float a) { g[i] = a; }
+
+// Fused MSE: per-block partial sums of e^2 and g = 2 e / N gated by the last ReLU, stored as
+// T (bf16 for the bf16 path, fp32 for tf32).
+template <typename T>
 __global__ void loss_grad_kernel(const float* __restrict__ y, const float* __restrict__ t,
                                  int64_t count, float inv_n, int relu,
-                                 __nv_bfloat16* __restrict__ g, float* __restrict__ partials) {
+                                 T* __restrict__ g, float* __restrict__ partials) {
     pdl_wait_then_release();
     const int64_t n4 = count / 4;
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
@@ -70,19 +87,13 @@ __global__ void loss_grad_kernel(const float* __restrict__ y, const float* __res
         const float4 tv = reinterpret_cast<const float4*>(t)[i];
         const float e0 = yv.x - tv.x, e1 = yv.y - tv.y, e2 = yv.z - tv.z, e3 = yv.w - tv.w;
         acc += e0 * e0 + e1 * e1 + e2 * e2 + e3 * e3;
-        __nv_bfloat162 lo = __floats2bfloat162_rn(grad_elem(yv.x, tv.x, inv_n, relu),
-                                                  grad_elem(yv.y, tv.y, inv_n, relu));
-        __nv_bfloat162 hi = __floats2bfloat162_rn(grad_elem(yv.z, tv.z, inv_n, relu),
-                                                  grad_elem(yv.w, tv.w, inv_n, relu));
-        uint2 packed;
-        packed.x = *reinterpret_cast<uint32_t*>(&lo);
-        packed.y = *reinterpret_cast<uint32_t*>(&hi);
-        reinterpret_cast<uint2*>(g)[i] = packed;
+        store_grad4(g, i, grad_elem(yv.x, tv.x, inv_n, relu), grad_elem(yv.y, tv.y, inv_n, relu),
+                    grad_elem(yv.z, tv.z, inv_n, relu), grad_elem(yv.w, tv.w, inv_n, relu));
     }
     for (int64_t i = n4 * 4 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += stride) {
         const float e = y[i] - t[i];
         acc += e * e;
-        g[i] = __float2bfloat16_rn(grad_elem(y[i], t[i], inv_n, relu));
+        store_grad1(g, i, grad_elem(y[i], t[i], inv_n, relu));
     }
     const float s = block_sum(acc);
     if (threadIdx.x == 0) partials[blockIdx.x] = s;
@@ -147,6 +158,47 @@ __global__ void __launch_bounds__(256) colsum_kernel(const __nv_bfloat16* __rest
         float4* dst = reinterpret_cast<float4*>(partials + static_cast<int64_t>(blockIdx.y) * d + 8 * g);
         dst[0] = make_float4(out[0], out[1], out[2], out[3]);
         dst[1] = make_float4(out[4], out[5], out[6], out[7]);
+    }
+}
+
+// The same for an fp32 [rows][d] matrix (tf32 path): 32 groups of 4 columns x 8 row-lanes.
+__global__ void __launch_bounds__(256) colsum_f32_kernel(const float* __restrict__ x, int64_t rows,
+                                                         int d, float* __restrict__ partials) {
+    pdl_wait_then_release();
+    __shared__ float red[kColLanes][32][5];
+    const int g = blockIdx.x * 32 + threadIdx.x;  // 4-column group
+    const int lane_r = threadIdx.y;
+    const int64_t r0 = static_cast<int64_t>(blockIdx.y) * kColRows;
+    float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    if (4 * g < d) {
+        constexpr int per = kColRows / kColLanes;
+        float4 v[per];
+#pragma unroll
+        for (int i = 0; i < per; ++i) {
+            const int64_t r = r0 + lane_r + static_cast<int64_t>(i) * kColLanes;
+            v[i] = r < rows ? __ldg(reinterpret_cast<const float4*>(x + r * d) + g) : make_float4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int i = 0; i < per; ++i) {
+            acc[0] += v[i].x;
+            acc[1] += v[i].y;
+            acc[2] += v[i].z;
+            acc[3] += v[i].w;
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) red[lane_r][threadIdx.x][i] = acc[i];
+    __syncthreads();
+    if (lane_r == 0 && 4 * g < d) {
+        float out[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            float s = red[0][threadIdx.x][i];
+            for (int l = 1; l < kColLanes; ++l) s += red[l][threadIdx.x][i];
+            out[i] = s;
+        }
+        reinterpret_cast<float4*>(partials + static_cast<int64_t>(blockIdx.y) * d)[g] =
+            make_float4(out[0], out[1], out[2], out[3]);
     }
 }
 
@@ -286,8 +338,17 @@ int loss_grad_bf16(const float* y, const float* t, int64_t count, float inv_n, i
     // Fixed grid (a function of count only) => a fixed summation tree.
     const int64_t need = (count / 4 + kThreads) / kThreads;
     const int blocks = static_cast<int>(need < 1 ? 1 : (need < 1184 ? need : 1184));
-    launch_pdl(loss_grad_kernel, dim3(blocks), dim3(kThreads), 0, st, y, t, count, inv_n, relu,
-               static_cast<__nv_bfloat16*>(g), partials);
+    launch_pdl(loss_grad_kernel<__nv_bfloat16>, dim3(blocks), dim3(kThreads), 0, st, y, t, count, inv_n,
+               relu, static_cast<__nv_bfloat16*>(g), partials);
+    return blocks;
+}
+
+int loss_grad_f32(const float* y, const float* t, int64_t count, float inv_n, int relu,
+                  float* g, float* partials, cudaStream_t st) {
+    const int64_t need = (count / 4 + kThreads) / kThreads;
+    const int blocks = static_cast<int>(need < 1 ? 1 : (need < 1184 ? need : 1184));
+    launch_pdl(loss_grad_kernel<float>, dim3(blocks), dim3(kThreads), 0, st, y, t, count, inv_n, relu, g,
+               partials);
     return blocks;
 }
 
@@ -302,6 +363,13 @@ int colsum_bf16(const void* x, int64_t rows, int d, float* partials, cudaStream_
     dim3 grid((d / 8 + 31) / 32, chunks);
     launch_pdl(colsum_kernel, grid, dim3(32, kColLanes), 0, st,
                static_cast<const __nv_bfloat16*>(x), rows, d, partials);
+    return chunks;
+}
+
+int colsum_f32(const float* x, int64_t rows, int d, float* partials, cudaStream_t st) {
+    const int chunks = colsum_chunks(rows);  // requires d % 4 == 0
+    dim3 grid((d / 4 + 31) / 32, chunks);
+    launch_pdl(colsum_f32_kernel, grid, dim3(32, kColLanes), 0, st, x, rows, d, partials);
     return chunks;
 }
 

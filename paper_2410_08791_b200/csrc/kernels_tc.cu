@@ -32,7 +32,7 @@ namespace tc {
 constexpr int BM = 128;
 constexpr int BK = 64;  // bf16 elements per 128-byte swizzle row
 constexpr int kThreads = 256;
-constexpr int A_BYTES = BM * BK * 2;  // 16 KB
+constexpr int A_BYTES = BM * 128;  // 16 KB: BM rows of one 128-byte swizzle row of K
 constexpr int ACC_STRIDE = 256;       // TMEM columns between the two accumulator stages
 constexpr int TMEM_COLS = 512;
 
@@ -40,6 +40,29 @@ constexpr int kSmemMax = 232448;  // 227 KB opt-in dynamic shared memory per CTA
 constexpr int kBarBytes = 512;    // mbarriers + TMEM address slot
 template <int EPI>
 struct EpiSmem;
+// Kernel-kind bits on top of the epilogue code (GemmEpilogue, kernels.hpp): EPI_TMA = the
+// epilogue stages through shared memory and stores with TMA; EPI_TF32 = operands are fp32
+// and multiply as tf32 (kind::tf32) instead of bf16 (kind::f16).
+constexpr int EPI_TMA = 16;
+constexpr int EPI_TF32 = 32;
+// Operand geometry per element type. A stage holds one 128-byte swizzle row of K per tile row
+// for either type, so stage bytes, the MMA count per stage (4) and the K-major descriptor
+// steps (32 bytes per MMA) are the same; MN-major tiles are cut into 128-byte-wide atoms.
+template <int EPI>
+struct Opnd {
+    static constexpr bool TF32 = (EPI & EPI_TF32) != 0;
+    static constexpr int ELT = TF32 ? 4 : 2;
+    static constexpr int BKE = 128 / ELT;         // K elements per stage
+    static constexpr int ATOM = 128 / ELT;        // MN elements per MN-major swizzle atom
+    static constexpr int KSTEP = 32 / ELT;        // K elements per MMA
+    static constexpr int ATOM_BYTES = BKE * 128;  // one MN-major atom over the stage's K rows
+    static constexpr int MMAS = BKE / KSTEP;      // MMAs per stage (4)
+    // MN-major smem layout: bf16 uses the 128B swizzle (16-byte granules, 8-row groups); tf32
+    // must use 128B_BASE32B (32-byte granules XOR row mod 4, 4-row groups: TMA swizzle
+    // 128B_ATOM_32B), so the descriptor's layout field and K-group stride differ.
+    static constexpr uint32_t MN_LAYOUT = TF32 ? 1u : 2u;
+    static constexpr uint32_t MN_SBO = TF32 ? 512u : 1024u;
+};
 // Operand ring depth: as many stages as fit beside the epilogue's staging buffers (max 8).
 constexpr int ring_stages(int stage_bytes, int epi_bytes) {
     return (kSmemMax - 1024 - kBarBytes - epi_bytes) / stage_bytes < 8
@@ -49,8 +72,9 @@ constexpr int ring_stages(int stage_bytes, int epi_bytes) {
 
 template <int BN, bool B_MN, int EPI>
 struct Cfg {
-    static constexpr int B_ROWS = B_MN ? ((BN + 63) / 64) * 64 : BN;
-    static constexpr int B_BYTES = B_ROWS * BK * 2;
+    static constexpr int ATOM = Opnd<EPI>::ATOM;
+    static constexpr int B_ROWS = B_MN ? ((BN + ATOM - 1) / ATOM) * ATOM : BN;
+    static constexpr int B_BYTES = B_ROWS * 128;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
     static constexpr int EPI_BYTES = EpiSmem<EPI>::BYTES;
     static constexpr int STAGES = ring_stages(STAGE_BYTES, EPI_BYTES);
@@ -65,7 +89,7 @@ struct Params {
     int ldo;
     const float* bias;
     int relu;
-    const __nv_bfloat16* gate;
+    const void* gate;  // bf16 (EPI_GATE_BF16) or fp32 (EPI_GATE_F32)
     int ldg;
     long long split_stride;
     float lr;
@@ -124,28 +148,39 @@ __device__ __forceinline__ void fence_after() {
 // Shared-memory matrix descriptor (tcgen05 "smem descriptor"): start, LBO, SBO in 16-byte
 // units, version 1 (sm_100), layout SWIZZLE_128B (2). Tiles are 1024-byte aligned so the
 // base-offset field stays 0.
-__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+// layout 2 = SWIZZLE_128B; 1 = SWIZZLE_128B_BASE32B (32-byte swizzle granules: the only
+// MN-major layout tcgen05 accepts for tf32 operands).
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout = 2) {
     uint64_t d = 0;
     d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
     d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16;
     d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32;
     d |= static_cast<uint64_t>(1) << 46;
-    d |= static_cast<uint64_t>(2) << 61;
+    d |= static_cast<uint64_t>(layout) << 61;
     return d;
 }
-// Instruction descriptor, kind::f16: D fp32, A/B bf16, majors, N>>3, M>>4.
-__host__ __device__ constexpr uint32_t make_idesc(int M, int N, bool a_mn, bool b_mn) {
-    return (1u << 4) | (1u << 7) | (1u << 10) | ((a_mn ? 1u : 0u) << 15) |
+// Instruction descriptor: D fp32, A/B bf16 (kind::f16, format 1) or tf32 (kind::tf32, format
+// 2), majors, N>>3, M>>4.
+__host__ __device__ constexpr uint32_t make_idesc(int M, int N, bool a_mn, bool b_mn, bool tf32 = false) {
+    return (1u << 4) | ((tf32 ? 2u : 1u) << 7) | ((tf32 ? 2u : 1u) << 10) | ((a_mn ? 1u : 0u) << 15) |
            ((b_mn ? 1u : 0u) << 16) | (static_cast<uint32_t>(N >> 3) << 17) |
            (static_cast<uint32_t>(M >> 4) << 24);
 }
-__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
-                                          uint32_t idesc, uint32_t accumulate) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+template <bool TF32>
+__device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                     uint32_t idesc, uint32_t accumulate) {
+    if (TF32)
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "setp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+            "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+    else
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "setp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+            "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
     asm volatile(
@@ -201,7 +236,6 @@ __device__ __forceinline__ void tile_mn(int t, int m_tiles, int n_tiles, int& mb
 // epilogue stages through shared memory and stores with TMA (short K, where the epilogue is on
 // the critical path); without it lanes store rows straight to global memory, which is smaller
 // code and leaves shared memory to the operand ring (long K, where the epilogue hides).
-constexpr int EPI_TMA = 16;
 template <int EPI>
 struct EpiSmem {
     static constexpr int BASE = EPI & (EPI_TMA - 1);
@@ -209,8 +243,10 @@ struct EpiSmem {
     static constexpr bool TMA_OUT = TMA;
     static constexpr int OUT_ELT = (BASE == EPI_BIAS_ACT_BF16 || BASE == EPI_GATE_BF16) ? 2 : 4;
     static constexpr int OUT_BUF = 32 * 32 * OUT_ELT;  // one warp's 32 x 32 chunk
-    static constexpr bool GATE = TMA && BASE == EPI_GATE_BF16;
-    static constexpr int GATE_BUF = 32 * 32 * 2;
+    static constexpr bool IS_GATE = BASE == EPI_GATE_BF16 || BASE == EPI_GATE_F32;
+    static constexpr int GATE_ELT = BASE == EPI_GATE_F32 ? 4 : 2;
+    static constexpr bool GATE = TMA && IS_GATE;
+    static constexpr int GATE_BUF = 32 * 32 * GATE_ELT;
     static constexpr int OUT_BYTES = TMA_OUT ? 4 * 2 * OUT_BUF : 0;  // 4 warps x 2 buffers
     static constexpr int GATE_BYTES = GATE ? 4 * 2 * GATE_BUF : 0;
     static constexpr int BYTES = OUT_BYTES + GATE_BYTES;
@@ -274,7 +310,7 @@ struct TileEpilogue {
         }
         ++gate_issued;
     }
-    static constexpr bool kMaskGate = BASE == EPI_GATE_BF16;
+    static constexpr bool kMaskGate = E::IS_GATE;
     __device__ __forceinline__ uint32_t mask_word(const Params& p, int row, int col0) const {
         return row < p.M && col0 < p.N ? __ldg(p.gate_mask + static_cast<long long>(col0 / 32) * p.M + row) : 0u;
     }
@@ -305,10 +341,33 @@ struct TileEpilogue {
                 for (int i = 0; i < 32; ++i) v[i] = v[i] < 0.0f ? 0.0f : v[i];
             }
         }
-        if (BASE == EPI_GATE_BF16 && p.relu && p.gate_mask != nullptr) {
+        if (E::IS_GATE && p.relu && p.gate_mask != nullptr) {
 #pragma unroll
             for (int i = 0; i < 32; ++i)
                 if (!((gate_bits >> i) & 1u)) v[i] = 0.0f;
+        } else if (BASE == EPI_GATE_F32 && p.relu) {  // fp32 gate tensor (tf32 path)
+            float4 gv[8];
+            if (E::GATE) {
+                const int b = gate_used & 1;
+                mbar_wait(&gbar[b], (gate_used >> 1) & 1);
+                ++gate_used;
+                const uint8_t* gb = gbuf + b * E::GATE_BUF;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) gv[i] = *reinterpret_cast<const float4*>(gb + swz<128>(lane, i));
+            } else {
+                if (row >= p.M) return;
+                const float4* gp = reinterpret_cast<const float4*>(static_cast<const float*>(p.gate) +
+                                                                   static_cast<long long>(row) * p.ldg + col0);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) gv[i] = __ldg(gp + i);
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                if (gv[i].x <= 0.0f) v[4 * i + 0] = 0.0f;
+                if (gv[i].y <= 0.0f) v[4 * i + 1] = 0.0f;
+                if (gv[i].z <= 0.0f) v[4 * i + 2] = 0.0f;
+                if (gv[i].w <= 0.0f) v[4 * i + 3] = 0.0f;
+            }
         } else if (BASE == EPI_GATE_BF16 && p.relu) {
             uint4 gv[4];
             if (E::GATE) {
@@ -320,7 +379,8 @@ struct TileEpilogue {
                 for (int i = 0; i < 4; ++i) gv[i] = *reinterpret_cast<const uint4*>(gb + swz<64>(lane, i));
             } else {
                 if (row >= p.M) return;
-                const uint4* gp = reinterpret_cast<const uint4*>(p.gate + static_cast<long long>(row) * p.ldg + col0);
+                const uint4* gp = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(p.gate) +
+                                                                 static_cast<long long>(row) * p.ldg + col0);
 #pragma unroll
                 for (int i = 0; i < 4; ++i) gv[i] = __ldg(gp + i);
             }
@@ -366,6 +426,12 @@ struct TileEpilogue {
                     bits |= ((pk[i] & 0x7FFFu) ? 1u : 0u) << (2 * i) | ((pk[i] & 0x7FFF0000u) ? 1u : 0u) << (2 * i + 1);
                 p.mask_out[static_cast<long long>(col0 / 32) * p.M + row] = bits;  // a warp: 128 B
             }
+        } else if (BASE == EPI_BIAS_ACT_F32 && p.relu && p.mask_out != nullptr && row < p.M) {
+            // fp32 output (tf32 path): the same rule on the stored fp32 values
+            uint32_t bits = 0;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) bits |= ((__float_as_uint(v[i]) & 0x7FFFFFFFu) ? 1u : 0u) << i;
+            p.mask_out[static_cast<long long>(col0 / 32) * p.M + row] = bits;
         }
         if (!E::TMA_OUT) {  // per-lane row stores straight to global
             if (row >= p.M) return;
@@ -442,8 +508,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmG,
                 const Params p) {
     using C = Cfg<BN, B_MN, EPI>;
+    using O = Opnd<EPI>;
     constexpr int STAGES = C::STAGES;
-    constexpr uint32_t IDESC = make_idesc(BM, BN, A_MN, B_MN);
+    constexpr uint32_t IDESC = make_idesc(BM, BN, A_MN, B_MN, O::TF32);
     constexpr uint32_t TX = C::STAGE_BYTES;
 
     extern __shared__ uint8_t smem_raw[];
@@ -510,19 +577,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     mbar_expect_tx(&full[stage], TX);
-                    const int k0 = kb * BK;
+                    const int k0 = kb * O::BKE;
                     uint8_t* a = sA + stage * A_BYTES;
                     uint8_t* b = sB + stage * C::B_BYTES;
                     if (A_MN) {
-                        tma_load_2d(&tmA, &full[stage], a, m0, k0);
-                        tma_load_2d(&tmA, &full[stage], a + 8192, m0 + 64, k0);
+#pragma unroll
+                        for (int j = 0; j < BM / O::ATOM; ++j)
+                            tma_load_2d(&tmA, &full[stage], a + j * O::ATOM_BYTES, m0 + O::ATOM * j, k0);
                     } else {
                         tma_load_2d(&tmA, &full[stage], a, k0, m0);
                     }
                     if (B_MN) {
 #pragma unroll
-                        for (int j = 0; j < C::B_ROWS / 64; ++j)
-                            tma_load_2d(&tmB, &full[stage], b + j * 8192, n0 + 64 * j, k0);
+                        for (int j = 0; j < C::B_ROWS / O::ATOM; ++j)
+                            tma_load_2d(&tmB, &full[stage], b + j * O::ATOM_BYTES, n0 + O::ATOM * j, k0);
                     } else {
                         tma_load_2d(&tmB, &full[stage], b, k0, n0);
                     }
@@ -553,12 +621,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const uint32_t a_base = smem_u32(sA + stage * A_BYTES);
                     const uint32_t b_base = smem_u32(sB + stage * C::B_BYTES);
 #pragma unroll
-                    for (int kk = 0; kk < BK / 16; ++kk) {
-                        const uint64_t ad = A_MN ? make_desc(a_base + kk * 2048, 8192, 1024)
+                    for (int kk = 0; kk < O::MMAS; ++kk) {
+                        // MN-major: the next KSTEP rows of every 128-byte atom; K-major: the next
+                        // 32 bytes of each swizzled row
+                        const uint64_t ad = A_MN ? make_desc(a_base + kk * O::KSTEP * 128, O::ATOM_BYTES, O::MN_SBO, O::MN_LAYOUT)
                                                  : make_desc(a_base + kk * 32, 16, 1024);
-                        const uint64_t bd = B_MN ? make_desc(b_base + kk * 2048, 8192, 1024)
+                        const uint64_t bd = B_MN ? make_desc(b_base + kk * O::KSTEP * 128, O::ATOM_BYTES, O::MN_SBO, O::MN_LAYOUT)
                                                  : make_desc(b_base + kk * 32, 16, 1024);
-                        umma_bf16(d_tmem, ad, bd, IDESC, (kb > kb0 || kk > 0) ? 1u : 0u);
+                        umma<O::TF32>(d_tmem, ad, bd, IDESC, (kb > kb0 || kk > 0) ? 1u : 0u);
                     }
                     umma_commit(&empty[stage]);  // frees the smem stage when these MMAs finish
                     if (++stage == STAGES) {
@@ -641,13 +711,21 @@ __device__ __forceinline__ void tma_load_2d_pair(const CUtensorMap* map, uint64_
         "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_addr), "r"(c0), "r"(c1)
         : "memory");
 }
-__device__ __forceinline__ void umma2_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
-                                           uint32_t idesc, uint32_t accumulate) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+template <bool TF32>
+__device__ __forceinline__ void umma2(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                      uint32_t idesc, uint32_t accumulate) {
+    if (TF32)
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "setp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+            "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+    else
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "setp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+            "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 __device__ __forceinline__ void umma2_commit_both(uint64_t* bar) {
     const uint16_t mask = 0x3;
@@ -702,13 +780,13 @@ struct PairSched {
 template <int BN, bool A_MN, bool B_MN, int EPI>
 struct Cfg2 {
     static constexpr int B_ROWS = BN / 2;  // this CTA's half of the tile's N
-    static constexpr int B_BYTES = B_ROWS * BK * 2;
+    static constexpr int B_BYTES = B_ROWS * 128;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
     static constexpr int EPI_BYTES = EpiSmem<EPI>::BYTES;
     static constexpr int STAGES = ring_stages(STAGE_BYTES, EPI_BYTES);
     static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + kBarBytes;
     static_assert(STAGES >= 3, "operand ring too shallow");
-    static_assert(!B_MN || B_ROWS % 64 == 0, "MN-major B halves must be whole 128B-swizzle atoms");
+    static_assert(!B_MN || B_ROWS % Opnd<EPI>::ATOM == 0, "MN-major B halves must be whole 128B-swizzle atoms");
 };
 
 template <int BN, bool A_MN, bool B_MN, int EPI>
@@ -717,8 +795,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                  const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmG,
                  const Params p) {
     using C = Cfg2<BN, A_MN, B_MN, EPI>;
+    using O = Opnd<EPI>;
     constexpr int STAGES = C::STAGES;
-    constexpr uint32_t IDESC = make_idesc(2 * BM, BN, A_MN, B_MN);
+    constexpr uint32_t IDESC = make_idesc(2 * BM, BN, A_MN, B_MN, O::TF32);
     constexpr uint32_t TX = 2 * C::STAGE_BYTES;  // both CTAs' bytes land on the leader's barrier
 
     extern __shared__ uint8_t smem_raw[];
@@ -770,7 +849,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 
     const int m_tiles2 = (p.M + 2 * BM - 1) / (2 * BM);
     const PairSched sched(p, m_tiles2, blockIdx.x >> 1, gridDim.x >> 1);
-    constexpr uint32_t IDESC_NARROW = make_idesc(2 * BM, BN / 2, A_MN, B_MN);
+    constexpr uint32_t IDESC_NARROW = make_idesc(2 * BM, BN / 2, A_MN, B_MN, O::TF32);
 
     if (warp == 0) {
         if (lane == 0) {
@@ -785,25 +864,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 const int half = nar ? BN / 4 : BN / 2;
                 const int m0 = mb * 2 * BM + static_cast<int>(rank) * BM;
                 const int nb = nbk * BN + static_cast<int>(rank) * half;
-                const uint32_t tx = B_MN ? 2u * static_cast<uint32_t>(A_BYTES + (half / 64) * 8192) : TX;
+                const uint32_t tx =
+                    B_MN ? 2u * static_cast<uint32_t>(A_BYTES + (half / O::ATOM) * O::ATOM_BYTES) : TX;
                 const int kb0 = split * p.kb_per_split;
                 const int kb1 = min(kb0 + p.kb_per_split, p.k_blocks);
                 for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     if (leader) mbar_expect_tx(&full[stage], tx);
-                    const int k0 = kb * BK;
+                    const int k0 = kb * O::BKE;
                     uint8_t* a = sA + stage * A_BYTES;
                     uint8_t* b = sB + stage * C::B_BYTES;
                     if (A_MN) {
-                        tma_load_2d_pair(&tmA, &full[stage], a, m0, k0);
-                        tma_load_2d_pair(&tmA, &full[stage], a + 8192, m0 + 64, k0);
+#pragma unroll
+                        for (int j = 0; j < BM / O::ATOM; ++j)
+                            tma_load_2d_pair(&tmA, &full[stage], a + j * O::ATOM_BYTES, m0 + O::ATOM * j, k0);
                     } else {
                         tma_load_2d_pair(&tmA, &full[stage], a, k0, m0);
                     }
                     if (B_MN) {
 #pragma unroll
-                        for (int j = 0; j < C::B_ROWS / 64; ++j)
-                            if (j * 64 < half) tma_load_2d_pair(&tmB, &full[stage], b + j * 8192, nb + 64 * j, k0);
+                        for (int j = 0; j < C::B_ROWS / O::ATOM; ++j)
+                            if (j * O::ATOM < half)
+                                tma_load_2d_pair(&tmB, &full[stage], b + j * O::ATOM_BYTES, nb + O::ATOM * j, k0);
                     } else {
                         tma_load_2d_pair(&tmB, &full[stage], b, k0, nb);  // full box; MMA reads `half` rows
                     }
@@ -837,12 +919,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     const uint32_t a_base = smem_u32(sA + stage * A_BYTES);
                     const uint32_t b_base = smem_u32(sB + stage * C::B_BYTES);
 #pragma unroll
-                    for (int kk = 0; kk < BK / 16; ++kk) {
-                        const uint64_t ad = A_MN ? make_desc(a_base + kk * 2048, 8192, 1024)
+                    for (int kk = 0; kk < O::MMAS; ++kk) {
+                        const uint64_t ad = A_MN ? make_desc(a_base + kk * O::KSTEP * 128, O::ATOM_BYTES, O::MN_SBO, O::MN_LAYOUT)
                                                  : make_desc(a_base + kk * 32, 16, 1024);
-                        const uint64_t bd = B_MN ? make_desc(b_base + kk * 2048, 8192, 1024)
+                        const uint64_t bd = B_MN ? make_desc(b_base + kk * O::KSTEP * 128, O::ATOM_BYTES, O::MN_SBO, O::MN_LAYOUT)
                                                  : make_desc(b_base + kk * 32, 16, 1024);
-                        umma2_bf16(d_tmem, ad, bd, idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
+                        umma2<O::TF32>(d_tmem, ad, bd, idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
                     }
                     umma2_commit_both(&empty[stage]);  // frees the stage in BOTH CTAs
                     if (++stage == STAGES) {
@@ -974,21 +1056,22 @@ bool make_map(CUtensorMap* m, const MapDesc& k) {
     return true;
 }
 
-// bf16 operand [outer][ld] (inner contiguous), 128B-swizzled box {box_inner, box_outer}
+// Operand [outer][ld] (inner contiguous; bf16, or fp32 for tf32), 128B-swizzled box
+// {box_inner, box_outer}
 bool make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint64_t ld,
-              uint32_t box_inner, uint32_t box_outer) {
+              uint32_t box_inner, uint32_t box_outer, bool f32 = false, bool base32 = false) {
     MapDesc k{};
-    k.dtype = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+    k.dtype = f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
     k.rank = 2;
     k.base = base;
     k.dims[0] = inner;
     k.dims[1] = outer;
     k.dims[2] = 1;
-    k.strides[0] = ld * 2;
+    k.strides[0] = ld * (f32 ? 4 : 2);
     k.box[0] = box_inner;
     k.box[1] = box_outer;
     k.box[2] = 1;
-    k.swizzle = CU_TENSOR_MAP_SWIZZLE_128B;
+    k.swizzle = base32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B;
     return make_map(m, k);
 }
 
@@ -1023,17 +1106,17 @@ bool make_epilogue_maps(const GemmProblem& g, int splits, CUtensorMap* to, CUten
     }
     if (E::GATE && g.relu && !g.gate_mask) {
         MapDesc k{};
-        k.dtype = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+        k.dtype = E::GATE_ELT == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
         k.rank = 2;
         k.base = g.gate;
         k.dims[0] = static_cast<uint64_t>(g.N);
         k.dims[1] = static_cast<uint64_t>(g.M);
         k.dims[2] = 1;
-        k.strides[0] = static_cast<uint64_t>(g.ldg) * 2;
+        k.strides[0] = static_cast<uint64_t>(g.ldg) * E::GATE_ELT;
         k.box[0] = 32;
         k.box[1] = 32;
         k.box[2] = 1;
-        k.swizzle = CU_TENSOR_MAP_SWIZZLE_64B;
+        k.swizzle = E::GATE_ELT == 2 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B;
         if (!make_map(tg, k)) return false;
     }
     return true;
@@ -1072,11 +1155,12 @@ cudaError_t launch(const GemmProblem& g, cudaStream_t st) {
         if (e != cudaSuccess) return e;
         configured = true;
     }
+    using O = Opnd<EPI>;
     CUtensorMap ta, tb;
-    bool ok = A_MN ? make_map(&ta, g.A, g.M, g.K, g.lda, 64, 64)
-                   : make_map(&ta, g.A, g.K, g.M, g.lda, 64, BM);
-    ok = ok && (B_MN ? make_map(&tb, g.B, g.N, g.K, g.ldb, 64, 64)
-                     : make_map(&tb, g.B, g.K, g.N, g.ldb, 64, BN));
+    bool ok = A_MN ? make_map(&ta, g.A, g.M, g.K, g.lda, O::ATOM, O::BKE, O::TF32, O::TF32)
+                   : make_map(&ta, g.A, g.K, g.M, g.lda, O::BKE, BM, O::TF32);
+    ok = ok && (B_MN ? make_map(&tb, g.B, g.N, g.K, g.ldb, O::ATOM, O::BKE, O::TF32, O::TF32)
+                     : make_map(&tb, g.B, g.K, g.N, g.ldb, O::BKE, BN, O::TF32));
     if (!ok) return cudaErrorInvalidValue;
     Params p;
     p.M = g.M;
@@ -1084,7 +1168,7 @@ cudaError_t launch(const GemmProblem& g, cudaStream_t st) {
     p.K = g.K;
     p.m_tiles = (g.M + BM - 1) / BM;
     p.n_tiles = (g.N + BN - 1) / BN;
-    p.k_blocks = (g.K + BK - 1) / BK;
+    p.k_blocks = (g.K + O::BKE - 1) / O::BKE;
     p.splits = g.splits < 1 ? 1 : g.splits;
     if (p.splits > p.k_blocks) p.splits = p.k_blocks;
     p.kb_per_split = (p.k_blocks + p.splits - 1) / p.splits;
@@ -1093,7 +1177,7 @@ cudaError_t launch(const GemmProblem& g, cudaStream_t st) {
     p.ldo = g.ldo;
     p.bias = g.bias;
     p.relu = g.relu;
-    p.gate = static_cast<const __nv_bfloat16*>(g.gate);
+    p.gate = g.gate;
     p.ldg = g.ldg;
     p.split_stride = g.split_stride;
     p.lr = g.lr;
@@ -1119,11 +1203,12 @@ cudaError_t launch2(const GemmProblem& g, cudaStream_t st) {
         if (e != cudaSuccess) return e;
         configured = true;
     }
+    using O = Opnd<EPI>;
     CUtensorMap ta, tb;
-    bool ok = A_MN ? make_map(&ta, g.A, g.M, g.K, g.lda, 64, 64)
-                   : make_map(&ta, g.A, g.K, g.M, g.lda, 64, BM);
-    ok = ok && (B_MN ? make_map(&tb, g.B, g.N, g.K, g.ldb, 64, 64)
-                     : make_map(&tb, g.B, g.K, g.N, g.ldb, 64, BN / 2));
+    bool ok = A_MN ? make_map(&ta, g.A, g.M, g.K, g.lda, O::ATOM, O::BKE, O::TF32, O::TF32)
+                   : make_map(&ta, g.A, g.K, g.M, g.lda, O::BKE, BM, O::TF32);
+    ok = ok && (B_MN ? make_map(&tb, g.B, g.N, g.K, g.ldb, O::ATOM, O::BKE, O::TF32, O::TF32)
+                     : make_map(&tb, g.B, g.K, g.N, g.ldb, O::BKE, BN / 2, O::TF32));
     if (!ok) return cudaErrorInvalidValue;
     Params p;
     p.M = g.M;
@@ -1131,7 +1216,7 @@ cudaError_t launch2(const GemmProblem& g, cudaStream_t st) {
     p.K = g.K;
     p.m_tiles = (g.M + 2 * BM - 1) / (2 * BM);
     p.n_tiles = (g.N + BN - 1) / BN;
-    p.k_blocks = (g.K + BK - 1) / BK;
+    p.k_blocks = (g.K + O::BKE - 1) / O::BKE;
     p.splits = g.splits < 1 ? 1 : g.splits;
     if (p.splits > p.k_blocks) p.splits = p.k_blocks;
     p.kb_per_split = (p.k_blocks + p.splits - 1) / p.splits;
@@ -1140,7 +1225,7 @@ cudaError_t launch2(const GemmProblem& g, cudaStream_t st) {
     p.ldo = g.ldo;
     p.bias = g.bias;
     p.relu = g.relu;
-    p.gate = static_cast<const __nv_bfloat16*>(g.gate);
+    p.gate = g.gate;
     p.ldg = g.ldg;
     p.split_stride = g.split_stride;
     p.lr = g.lr;
@@ -1192,6 +1277,27 @@ cudaError_t dispatch2_bn(const GemmProblem& g, cudaStream_t st) {
     if (g.a_mn && g.b_mn && g.epilogue == EPI_SGD_F32) return launch2_k<BN, true, true, EPI_SGD_F32>(g, st);
     if (!g.a_mn && !g.b_mn && g.epilogue == EPI_F32) return launch2_k<BN, false, false, EPI_F32>(g, st);
     if (!g.a_mn && g.b_mn && g.epilogue == EPI_F32) return launch2_k<BN, false, true, EPI_F32>(g, st);
+    return cudaErrorNotSupported;
+}
+
+// tf32 instantiations (SP_NUMERICS_TF32): the layer GEMMs only - forward (fp32 out + mask),
+// dX (fp32 out, gated), dW (fp32 partials or fused SGD) - at N = 256 (pair) / 128, 256 (1-CTA).
+template <int BN>
+cudaError_t dispatch_bn_tf32(const GemmProblem& g, cudaStream_t st) {
+    constexpr int T = EPI_TF32;
+    if (!g.a_mn && g.b_mn && g.epilogue == EPI_BIAS_ACT_F32) return launch_k<BN, false, true, EPI_BIAS_ACT_F32 | T>(g, st);
+    if (!g.a_mn && !g.b_mn && g.epilogue == EPI_GATE_F32) return launch_k<BN, false, false, EPI_GATE_F32 | T>(g, st);
+    if (g.a_mn && g.b_mn && g.epilogue == EPI_F32) return launch_k<BN, true, true, EPI_F32 | T>(g, st);
+    if (g.a_mn && g.b_mn && g.epilogue == EPI_SGD_F32) return launch_k<BN, true, true, EPI_SGD_F32 | T>(g, st);
+    return cudaErrorNotSupported;
+}
+template <int BN>
+cudaError_t dispatch2_bn_tf32(const GemmProblem& g, cudaStream_t st) {
+    constexpr int T = EPI_TF32;
+    if (!g.a_mn && g.b_mn && g.epilogue == EPI_BIAS_ACT_F32) return launch2_k<BN, false, true, EPI_BIAS_ACT_F32 | T>(g, st);
+    if (!g.a_mn && !g.b_mn && g.epilogue == EPI_GATE_F32) return launch2_k<BN, false, false, EPI_GATE_F32 | T>(g, st);
+    if (g.a_mn && g.b_mn && g.epilogue == EPI_F32) return launch2_k<BN, true, true, EPI_F32 | T>(g, st);
+    if (g.a_mn && g.b_mn && g.epilogue == EPI_SGD_F32) return launch2_k<BN, true, true, EPI_SGD_F32 | T>(g, st);
     return cudaErrorNotSupported;
 }
 
@@ -1259,9 +1365,10 @@ GemmChoice choose_gemm(int M, int N, int K, int splits, int epilogue) {
 // 16384 rows x d=1600 -> CTA pair, N=256, 3 splits (72.9 us, 1150 TFLOP/s; was 1-CTA N=192 with
 // 5 splits, 82.6 us); 65792 x 1280 -> pair, 256, 5 splits (161 us, 1337 TFLOP/s).
 // splits = 1 with fused_ok means the SGD is fused into the epilogue (no partials).
-DwChoice choose_dw(int M, int N, int K, int max_splits, bool fused_ok) {
+DwChoice choose_dw(int M, int N, int K, int max_splits, bool fused_ok, bool tf32) {
     const int sms = num_sms();
-    const int kb = (K + tc::BK - 1) / tc::BK;
+    const int bke = tf32 ? tc::BK / 2 : tc::BK;  // K elements per k-block
+    const int kb = (K + bke - 1) / bke;
     DwChoice best{2, 256, 1};
     double best_t = 1e300;
     struct Cand {
@@ -1269,9 +1376,10 @@ DwChoice choose_dw(int M, int N, int K, int max_splits, bool fused_ok) {
         double eff;
     };
     for (const Cand c : {Cand{2, 256, 0.95}, Cand{1, 256, 0.80}, Cand{1, 192, 0.80}, Cand{1, 128, 0.62}}) {
+        if (tf32 && c.bn == 192) continue;  // not instantiated for tf32
         for (int s = 1; s <= 16 && s <= max_splits && s <= kb; ++s) {
-            if (s > 1 && kb / s < 8) break;  // keep >= 512 of K per split
-            if (effective_splits(K, s) != s) continue;
+            if (s > 1 && kb * bke / s < 512) break;  // keep >= 512 of K per split
+            if (effective_splits(K, s, tf32) != s) continue;
             const long mt = (M + c.cta * tc::BM - 1) / (c.cta * tc::BM);
             const long nt = (N + c.bn - 1) / c.bn;
             const long tiles = mt * nt * s, slots = sms / c.cta;
@@ -1324,8 +1432,9 @@ int choose_splits(int M, int N, int K, int block_n) {
     return best;
 }
 
-int effective_splits(int K, int splits) {
-    const int kb = (K + tc::BK - 1) / tc::BK;
+int effective_splits(int K, int splits, bool tf32) {
+    const int bke = tf32 ? tc::BK / 2 : tc::BK;
+    const int kb = (K + bke - 1) / bke;
     int s = splits < 1 ? 1 : (splits > kb ? kb : splits);
     const int per = (kb + s - 1) / s;
     return (kb + per - 1) / per;
@@ -1333,7 +1442,21 @@ int effective_splits(int K, int splits) {
 
 cudaError_t gemm_bf16(const GemmProblem& g, cudaStream_t st) {
     if (g.M <= 0 || g.N <= 0 || g.K <= 0) return cudaErrorInvalidValue;
-    if (g.N % 32 != 0 || g.lda % 8 != 0 || g.ldb % 8 != 0) return cudaErrorInvalidValue;
+    const int align = g.tf32 ? 4 : 8;  // 16-byte rows for TMA
+    if (g.N % 32 != 0 || g.lda % align != 0 || g.ldb % align != 0) return cudaErrorInvalidValue;
+    if (g.tf32) {
+        int cta = g.cta, bn = g.block_n;
+        if (cta == 0) {
+            const GemmChoice c = choose_gemm(g.M, g.N, g.K, g.splits < 1 ? 1 : g.splits, g.epilogue);
+            cta = c.cta;
+            if (!bn) bn = c.block_n == 192 ? 256 : c.block_n;
+        }
+        if (!bn) bn = 256;
+        if (cta == 2 && bn == 256) return tc::dispatch2_bn_tf32<256>(g, st);
+        if (cta == 1 && bn == 256) return tc::dispatch_bn_tf32<256>(g, st);
+        if (cta == 1 && bn == 128) return tc::dispatch_bn_tf32<128>(g, st);
+        return cudaErrorInvalidValue;
+    }
     int cta = g.cta, bn = g.block_n;
     if (cta == 0) {  // auto
         const GemmChoice c = choose_gemm(g.M, g.N, g.K, g.splits < 1 ? 1 : g.splits, g.epilogue);
