@@ -14,8 +14,8 @@
 //   * compute runs on the GPU; RunSummary times are measured milliseconds (CUDA events),
 //     not the simulator's virtual seconds, and the trace is the measured timeline;
 //   * StrategyKind::CpuOnly throws std::invalid_argument (there is no CPU path);
-//   * numerics: bit-exact fp32 by default (Numerics::Exact), Numerics::Bf16 selects the
-//     tcgen05 tensor-core path (set_numerics()).
+//   * numerics: bit-exact fp32 by default (Numerics::Exact), Numerics::Bf16 / Numerics::Tf32
+//     select the tcgen05 tensor-core paths (set_numerics()).
 #pragma once
 
 #include <cstdint>
@@ -203,7 +203,7 @@ struct RunResult {
     RunSummary summary;
 };
 
-enum class Numerics { Exact = SP_NUMERICS_EXACT, Bf16 = SP_NUMERICS_BF16 };
+enum class Numerics { Exact = SP_NUMERICS_EXACT, Bf16 = SP_NUMERICS_BF16, Tf32 = SP_NUMERICS_TF32 };
 
 namespace detail {
 inline Numerics& numerics() {

@@ -19,7 +19,7 @@ SP_OK, SP_ERR_INTERNAL, SP_ERR_INVALID, SP_ERR_OOM, SP_ERR_FIDELITY, SP_ERR_CUDA
 STANDARD, CPU_ONLY, NAIVE, SUPERPIPELINE = range(4)   # strategy.hpp:13
 SEQUENTIAL, BATCH = 0, 1                              # sim.hpp:15
 RELU, IDENTITY = 0, 1                                 # model.hpp:11
-EXACT, BF16 = 0, 1
+EXACT, BF16, TF32 = 0, 1, 2                          # sp_numerics
 OPT_SGD, OPT_ADAMW = 0, 1                             # superpipe.h SP_OPT_*
 
 

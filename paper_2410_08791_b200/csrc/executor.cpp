@@ -81,13 +81,16 @@ Executor::Executor(const sp_config& cfg) : cfg_(cfg) {
         throw Error(SP_ERR_INVALID,
                     "strategy: cpu_only is the reference's host path; the GPU executor has no CPU "
                     "fallback");
-    if (cfg.numerics != SP_NUMERICS_EXACT && cfg.numerics != SP_NUMERICS_BF16)
+    if (cfg.numerics != SP_NUMERICS_EXACT && cfg.numerics != SP_NUMERICS_BF16 &&
+        cfg.numerics != SP_NUMERICS_TF32)
         throw Error(SP_ERR_INVALID, "numerics: unknown mode");
     if (cfg.transfer_mode != SP_SEQUENTIAL && cfg.transfer_mode != SP_BATCH)
         throw Error(SP_ERR_INVALID, "transfer_mode: unknown mode");
     bf16_ = cfg.numerics == SP_NUMERICS_BF16;
-    if (bf16_ && d_ % 64 != 0)
-        throw Error(SP_ERR_INVALID, "bf16 numerics requires d % 64 == 0 (128-byte TMA rows)");
+    tf32_ = cfg.numerics == SP_NUMERICS_TF32;
+    tc_ = bf16_ || tf32_;
+    if (tc_ && d_ % 64 != 0)
+        throw Error(SP_ERR_INVALID, "bf16 / tf32 numerics require d % 64 == 0 (128-byte TMA rows)");
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
         throw Error(SP_ERR_CUDA, "no CUDA device visible: the executor has no CPU fallback");
@@ -309,16 +312,16 @@ void Executor::ensure_buffers(int64_t rows, int n_items, bool train, bool device
         tgt_ = static_cast<float*>(alloc(act * 4));
         for (int l = 0; l < n_; ++l) act_.push_back(alloc(act * elt));
         masks_.clear();
-        if (bf16_ && !(cfg_.checkpointing && cfg_.strategy != SP_STANDARD) && d_ % 32 == 0)
+        if (tc_ && !(cfg_.checkpointing && cfg_.strategy != SP_STANDARD) && d_ % 32 == 0)
             for (int l = 0; l < n_; ++l)
                 masks_.push_back(static_cast<uint32_t*>(alloc(static_cast<size_t>(R) * (d_ / 32) * 4)));
         for (auto& g : gbuf_) g = alloc(act * elt);
-        splits_cap_ = bf16_ ? choose_dw(d_, d_, static_cast<int>(R), 16, comm_ == nullptr).splits : 1;
-        col_chunks_cap_ = bf16_ ? colsum_chunks(R) : 1;
+        splits_cap_ = tc_ ? choose_dw(d_, d_, static_cast<int>(R), 16, comm_ == nullptr, tf32_).splits : 1;
+        col_chunks_cap_ = tc_ ? colsum_chunks(R) : 1;
         // gradient buffers hold world equal shards when reduce-scattered (sharded streaming)
         const size_t grad_f = std::max(dd + d_, shardA_ / 4 * static_cast<size_t>(world_));
-        const size_t ws = bf16_ ? static_cast<size_t>(splits_cap_) * dd + static_cast<size_t>(col_chunks_cap_) * d_
-                                : grad_f;
+        const size_t ws = tc_ ? static_cast<size_t>(splits_cap_) * dd + static_cast<size_t>(col_chunks_cap_) * d_
+                              : grad_f;
         for (auto& g : gws_) g = static_cast<float*>(alloc(ws * 4));
         grad_red_ = static_cast<float*>(alloc(grad_f * 4));
         loss_parts_ = static_cast<float*>(alloc(4096 * 4));
@@ -410,7 +413,7 @@ void Executor::compute_op(const Op& op, bool train, int64_t rows, int fmt) {
     const bool ckpt = train && cfg_.checkpointing && cfg_.strategy != SP_STANDARD;
     cudaStream_t st = s_comp_;
     auto ensure_w16 = [&] {
-        if (w16_layer_[s] == L) return;
+        if (tf32_ || w16_layer_[s] == L) return;  // tf32 multiplies the fp32 master directly
         convert_f32_to_bf16(slot_w32(s), slot_w16(s), static_cast<int64_t>(d_) * d_, st);
         ++kernels_;
         w16_layer_[s] = L;
@@ -419,14 +422,14 @@ void Executor::compute_op(const Op& op, bool train, int64_t rows, int fmt) {
         const float* x_item = cur_x_ + static_cast<size_t>(op.item) * act;
         float* y_item = cur_y_ + static_cast<size_t>(op.item) * act;
         const bool last = L == n_ - 1;
-        if (!bf16_) {
+        if (!tc_) {
             const float* in = L == 0 ? x_item : static_cast<const float*>(pp_[(L - 1) % 2]);
             float* out = last ? y_item : static_cast<float*>(pp_[L % 2]);
             exact_forward(in, slot_w32(s), slot_b32(s), relu_[L], out, rows, d_, st);
             ++kernels_;
             return;
         }
-        if (L == 0) {
+        if (L == 0 && bf16_) {
             convert_f32_to_bf16(x_item, xconv_, static_cast<int64_t>(act), st);
             ++kernels_;
         }
@@ -434,16 +437,17 @@ void Executor::compute_op(const Op& op, bool train, int64_t rows, int fmt) {
         g.M = static_cast<int>(rows);
         g.N = d_;
         g.K = d_;
-        g.A = L == 0 ? xconv_ : pp_[(L - 1) % 2];
+        g.A = L == 0 ? (tf32_ ? static_cast<const void*>(x_item) : xconv_) : pp_[(L - 1) % 2];
         g.lda = d_;
-        g.B = slot_w16(s);
+        g.B = tf32_ ? static_cast<void*>(slot_w32(s)) : slot_w16(s);
         g.ldb = d_;
         g.b_mn = true;
-        g.epilogue = last ? EPI_BIAS_ACT_F32 : EPI_BIAS_ACT_BF16;
+        g.epilogue = last || tf32_ ? EPI_BIAS_ACT_F32 : EPI_BIAS_ACT_BF16;
         g.out = last ? static_cast<void*>(y_item) : pp_[L % 2];
         g.ldo = d_;
-        g.bias = slot_b16(s);
+        g.bias = tf32_ ? slot_b32(s) : slot_b16(s);
         g.relu = relu_[L];
+        g.tf32 = tf32_;
         gemm(g, st);
         return;
     }
@@ -452,14 +456,14 @@ void Executor::compute_op(const Op& op, bool train, int64_t rows, int fmt) {
         const bool last = L == n_ - 1;
         void* out = last ? static_cast<void*>(yout_) : (ckpt ? fa_[(L + 1) % 3] : act_[L + 1]);
         if (L == 0) {
-            if (bf16_) {
+            if (bf16_) {  // (tf32: fp32 activations, copied like the exact path)
                 convert_f32_to_bf16(cur_x_, xL, static_cast<int64_t>(act), st);
                 ++kernels_;
             } else {
                 CUDA_OK(cudaMemcpyAsync(xL, cur_x_, act * 4, cudaMemcpyDeviceToDevice, st));
             }
         }
-        if (!bf16_) {
+        if (!tc_) {
             exact_forward(static_cast<const float*>(xL), slot_w32(s), slot_b32(s), relu_[L],
                           static_cast<float*>(out), rows, d_, st);
             ++kernels_;
@@ -472,10 +476,11 @@ void Executor::compute_op(const Op& op, bool train, int64_t rows, int fmt) {
         g.K = d_;
         g.A = xL;
         g.lda = d_;
-        g.B = slot_w16(s);
+        g.B = tf32_ ? static_cast<void*>(slot_w32(s)) : slot_w16(s);
         g.ldb = d_;
         g.b_mn = true;
-        g.epilogue = last ? EPI_BIAS_ACT_F32 : EPI_BIAS_ACT_BF16;
+        g.tf32 = tf32_;
+        g.epilogue = last || tf32_ ? EPI_BIAS_ACT_F32 : EPI_BIAS_ACT_BF16;
         g.out = out;
         g.ldo = d_;
         g.bias = slot_b32(s);
@@ -493,7 +498,7 @@ void Executor::compute_op(const Op& op, bool train, int64_t rows, int fmt) {
     if (L > 0) {
         void* out = gbuf_[(L - 1) % 2];
         const bool gate = relu_[L - 1] != 0;
-        if (!bf16_) {
+        if (!tc_) {
             exact_backward_dx(static_cast<const float*>(dz), slot_w32(s),
                               gate ? static_cast<const float*>(xL) : nullptr,
                               static_cast<float*>(out), rows, d_, st);
@@ -506,9 +511,10 @@ void Executor::compute_op(const Op& op, bool train, int64_t rows, int fmt) {
             g.K = d_;
             g.A = dz;
             g.lda = d_;
-            g.B = slot_w16(s);  // W[i][j] is the K-major B of dx = dz W^T
+            g.B = tf32_ ? static_cast<void*>(slot_w32(s)) : slot_w16(s);  // W[i][j]: K-major B of dx = dz W^T
             g.ldb = d_;
-            g.epilogue = EPI_GATE_BF16;
+            g.tf32 = tf32_;
+            g.epilogue = tf32_ ? EPI_GATE_F32 : EPI_GATE_BF16;
             g.out = out;
             g.ldo = d_;
             g.gate = xL;
@@ -521,7 +527,7 @@ void Executor::compute_op(const Op& op, bool train, int64_t rows, int fmt) {
     if (!trainable) return;
     float* ws = gws_[L % 2];
     const size_t dd = static_cast<size_t>(d_) * d_;
-    if (!bf16_) {
+    if (!tc_) {
         exact_backward_dw(static_cast<const float*>(xL), static_cast<const float*>(dz), ws,
                           ws + dd, rows, d_, st);
         ++kernels_;
@@ -537,6 +543,7 @@ void Executor::compute_op(const Op& op, bool train, int64_t rows, int fmt) {
     g.B = dz;  // dz [r][j]: N-major B
     g.ldb = d_;
     g.b_mn = true;
+    g.tf32 = tf32_;
     // One GPU and enough output tiles to fill the SMs: SGD is fused into the dW epilogue
     // (W -= lr*acc on the slot's fp32 master; splits = 1 keeps each element owned by one CTA).
     // Otherwise (too few d x d tiles for the SMs, or data parallel): raw split-K partials,
@@ -552,7 +559,9 @@ void Executor::compute_op(const Op& op, bool train, int64_t rows, int fmt) {
     g.lr = cur_lr_;
     gemm(g, st);
     if (fused) w16_layer_[s] = -1;
-    colsum_bf16(dz, rows, d_, ws + (fused ? 0 : static_cast<size_t>(splits_) * dd), st);
+    float* db_parts = ws + (fused ? 0 : static_cast<size_t>(splits_) * dd);
+    if (tf32_) colsum_f32(static_cast<const float*>(dz), rows, d_, db_parts, st);
+    else colsum_bf16(dz, rows, d_, db_parts, st);
     ++kernels_;
 }
 
@@ -561,11 +570,13 @@ void Executor::loss_op(int64_t rows) {
     const float inv_n = 1.0f / static_cast<float>(count * world_);
     const int last = n_ - 1;
     void* g = gbuf_[last % 2];
-    if (!bf16_) {
+    if (!tc_) {
         exact_loss_grad(yout_, cur_t_, count, inv_n, relu_[last], static_cast<float*>(g), loss_dev_, s_comp_);
         kernels_ += 2;
     } else {
-        loss_blocks_ = loss_grad_bf16(yout_, cur_t_, count, inv_n, relu_[last], g, loss_parts_, s_comp_);
+        loss_blocks_ = tf32_ ? loss_grad_f32(yout_, cur_t_, count, inv_n, relu_[last], static_cast<float*>(g),
+                                             loss_parts_, s_comp_)
+                             : loss_grad_bf16(yout_, cur_t_, count, inv_n, relu_[last], g, loss_parts_, s_comp_);
         loss_finalize(loss_parts_, loss_blocks_, loss_dev_, s_comp_);
         kernels_ += 2;
     }
@@ -587,7 +598,7 @@ void Executor::update_op(const Op& op, float lr) {
     const size_t dd = static_cast<size_t>(d_) * d_;
     cudaStream_t st = s_upd_;
     float* ws = gws_[L % 2];
-    if (adamw() && bf16_ && !comm_) {
+    if (adamw() && tc_ && !comm_) {
         // AdamW straight from the partials: dW split-K partials, db column-sum partials
         adamw_reduce(slot_w32(s), slot_m32(s), slot_v32(s), ws, splits_, static_cast<int64_t>(dd),
                      static_cast<int64_t>(dd), adamw_dev_, st);
@@ -597,7 +608,7 @@ void Executor::update_op(const Op& op, float lr) {
         w16_layer_[s] = -1;
         return;
     }
-    if (bf16_ && !comm_) {
+    if (tc_ && !comm_) {
         // W: updated in the dW epilogue (fused), or here from the split-K partials in a fixed
         // order; bias from the db column-sum partials.
         const size_t db_off = dw_fused_ ? 0 : static_cast<size_t>(splits_) * dd;
@@ -612,7 +623,7 @@ void Executor::update_op(const Op& op, float lr) {
     }
     // The full-batch gradient [dW | db] (fp32, the slot's [W | b] layout) in `g`.
     float* g = ws;
-    if (bf16_) {
+    if (tc_) {
         reduce_partials(ws, splits_, static_cast<int64_t>(dd), static_cast<int64_t>(dd), grad_red_, st);
         reduce_partials(ws + splits_ * dd, col_chunks_, d_, d_, grad_red_ + dd, st);
         kernels_ += 2;
@@ -1089,8 +1100,8 @@ float Executor::train_step(const float* x, const float* target, int64_t rows, fl
     Plan plan = make_plan(true, 1, rows, fmt);
     ensure_buffers(rows, 1, true, device_io);
     CUDA_OK(cudaSetDevice(cfg_.device));
-    if (bf16_) {  // split-K depends only on (d, rows): identical for every window setting
-        const DwChoice c = choose_dw(d_, d_, static_cast<int>(rows), splits_cap_, comm_ == nullptr);
+    if (tc_) {  // split-K depends only on (d, rows): identical for every window setting
+        const DwChoice c = choose_dw(d_, d_, static_cast<int>(rows), splits_cap_, comm_ == nullptr, tf32_);
         splits_ = c.splits;
         dw_cta_ = c.cta;
         dw_bn_ = c.block_n;

@@ -112,7 +112,9 @@ private:
 
     sp_config cfg_;
     int n_ = 0, d_ = 0;
-    bool bf16_ = false;
+    bool bf16_ = false;  // bf16 tensor-core path (bf16 operands / activations)
+    bool tf32_ = false;  // tf32 tensor-core path (fp32 operands / activations, kind::tf32)
+    bool tc_ = false;    // either tensor-core path (split-K partials, masks, fused loss)
     // pinned host copies
     float* host32_ = nullptr;  // [n][d*d + d] fp32 master (W then b)
     uint8_t* host16_ = nullptr;  // [n][wire16] bf16 W + fp32 b (bf16 inference wire)
