@@ -55,7 +55,7 @@ def parse():
                         "memory streamed with each backward layer, fused AdamW update")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-variants", action="store_true",
-                   help="skip the in-run AdamW variant of the same step (reported under 'variants')")
+                   help="skip the in-run AdamW and tf32 variants of the same step ('variants')")
     p.add_argument("--sweep", default="", help="comma list of k:kp to report extra lines")
     return p.parse_args()
 
@@ -335,8 +335,8 @@ def main():
         _capi.LIB.sp_build_layer(7, i, a.d, 0, 0, Wl.ctypes.data, bl.ctypes.data)
         weights.append((Wl, bl))
 
-    def make_executor(strat, opt=a.optimizer):
-        e = sp.Executor(a.layers, a.d, strat, numerics=sp.BF16, device=local, trace=0)
+    def make_executor(strat, opt=a.optimizer, numerics=sp.BF16):
+        e = sp.Executor(a.layers, a.d, strat, numerics=numerics, device=local, trace=0)
         for i, (Wl, bl) in enumerate(weights):
             e.register_layer(i, Wl, bl)
         if opt == "adamw":
@@ -396,10 +396,12 @@ def main():
     ms_e2e, _ = timed(step_e2e, None)
     last = stats[-1]
     variants = {}
-    if a.optimizer == "sgd" and not a.no_variants:
-        # The same step with AdamW (north_star: optimizer state in pinned host DRAM, fused
-        # update), timed the same way in the same run; the headline stays the reference's SGD.
-        ev = make_executor(strategy, "adamw")
+    # The same step with AdamW (north_star: optimizer state in pinned host DRAM, fused update)
+    # and in tf32 numerics (fp32 operands on the tensor cores), timed the same way in the same
+    # run; the headline stays the reference's SGD in bf16.
+    for vname in ([] if a.optimizer != "sgd" or a.no_variants else ["adamw", "tf32"]):
+        ev = make_executor(strategy, "adamw" if vname == "adamw" else "sgd",
+                           sp.TF32 if vname == "tf32" else sp.BF16)
         if world > 1:
             dp.init_executor_dp(ev, dist, rank, world)
         for _ in range(a.warmup):
@@ -415,13 +417,18 @@ def main():
         vms = v0.elapsed_time(v1)
         if world > 1:
             vms = dp.max_over_ranks(dist, torch, vms)
-        va = argparse.Namespace(**dict(vars(a), optimizer="adamw"))
-        vroof = layer_roofline(va, link, pk, a.rows, ev.stats()["n_slots"], world if world > 1 else 1)
-        variants["adamw"] = {"value": world * a.rows * a.steps / (vms * 1e-3), "unit": "samples/s",
-                             "ms_per_step": vms / a.steps, "ring_roofline_ms": vroof * 1e3,
-                             "frac_of_ring_roofline": vroof / (vms * 1e-3 / a.steps),
-                             "h2d_gb_per_step": ev.stats()["h2d_bytes"] / 1e9,
-                             "d2h_gb_per_step": ev.stats()["d2h_bytes"] / 1e9}
+        va = argparse.Namespace(**dict(vars(a), optimizer="adamw" if vname == "adamw" else "sgd"))
+        # tf32's dense tensor rate is half of bf16's (1.1 vs 2.25 PFLOP/s nominal): the
+        # measured sustained bf16 peak / 2 is its roofline denominator
+        vpk = dict(pk, bf16_tflops_sustained=pk["bf16_tflops_sustained"] / 2) if vname == "tf32" else pk
+        vroof = layer_roofline(va, link, vpk, a.rows, ev.stats()["n_slots"], world if world > 1 else 1)
+        variants[vname] = {"value": world * a.rows * a.steps / (vms * 1e-3), "unit": "samples/s",
+                           "ms_per_step": vms / a.steps, "ring_roofline_ms": vroof * 1e3,
+                           "frac_of_ring_roofline": vroof / (vms * 1e-3 / a.steps),
+                           "h2d_gb_per_step": ev.stats()["h2d_bytes"] / 1e9,
+                           "d2h_gb_per_step": ev.stats()["d2h_bytes"] / 1e9,
+                           "numerics": "tf32" if vname == "tf32" else "bf16",
+                           "optimizer": "adamw" if vname == "adamw" else "sgd"}
         ev.close()
     # One extra step with the per-op CUDA-event timeline (not timed): stall / compute split.
     ex.set_trace(1)
