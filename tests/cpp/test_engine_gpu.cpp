@@ -287,4 +287,90 @@ TEST_CASE("bf16 tensor-core path is window-invariant and close to the reference 
     set_numerics(Numerics::Exact);
 }
 
+TEST_CASE("tf32 tensor-core path is window-invariant and within 2e-3 of the reference [gpu]") {
+    set_numerics(Numerics::Tf32);
+    LayeredModel model = build_model(5, 8, 128, 0);
+    auto inputs = make_inputs(5, 1, 256, 128);
+    Tensor want = reference_forward(model, inputs[0]);
+    std::vector<float> first;
+    for (const auto& s : {strat(StrategyKind::Standard), strat(StrategyKind::Superpipeline, 2, 1),
+                          strat(StrategyKind::Naive, 3)}) {
+        RunResult r = run_inference(model, inputs, s, roomy_arena());
+        if (first.empty()) first = r.outputs[0].values;
+        else CHECK(r.outputs[0].values == first);
+    }
+    float err = 0.0f, ref = 0.0f;
+    for (std::size_t i = 0; i < want.values.size(); ++i) {
+        err = std::fmax(err, std::fabs(first[i] - want.values[i]));
+        ref = std::fmax(ref, std::fabs(want.values[i]));
+    }
+    CHECK(err / ref <= 2e-3f);
+    set_numerics(Numerics::Exact);
+}
+
+// The AdamW option through the C ABI a reference-side caller binds (superpipe.h), checked
+// bitwise against the oracle: the reference's gradients (orc_train_step on a scratch copy),
+// then orc_adamw with the scalars computed in double and rounded once.
+TEST_CASE("AdamW through the C ABI is bit-identical to the oracle over several steps [gpu]") {
+    const int n = 4, d = 8, rows = 4;
+    const float lr = 0.01f, b1 = 0.9f, b2 = 0.999f, eps = 1e-8f, wd = 0.01f;
+    LayeredModel model = build_model(3, n, d, 1);
+    Tensor x = make_input(3, 0, rows, d), t = make_input(3, 1, rows, d);
+    sp_config c{};
+    c.n_layers = n;
+    c.d = d;
+    c.strategy = SP_SUPERPIPELINE;
+    c.k = 2;
+    c.k_prime = 1;
+    c.transfer_mode = SP_BATCH;
+    c.numerics = SP_NUMERICS_EXACT;
+    sp_exec* ex = nullptr;
+    REQUIRE(sp_create(&c, &ex) == SP_OK);
+    for (int l = 0; l < n; ++l)
+        REQUIRE(sp_register_layer(ex, l, model.blocks[l].weight.data(), model.blocks[l].bias.data(), SP_RELU,
+                                  model.blocks[l].frozen ? 1 : 0) == SP_OK);
+    CHECK(sp_set_optimizer(ex, SP_OPT_ADAMW, b1, b2, eps, wd) == SP_OK);
+    CHECK(sp_set_optimizer(ex, SP_OPT_ADAMW, 1.5f, b2, eps, wd) == SP_ERR_INVALID);
+    CHECK(sp_set_optimizer(ex, SP_OPT_ADAMW, b1, b2, eps, wd) == SP_OK);
+
+    Flat f(model);
+    const std::size_t dd = static_cast<std::size_t>(d) * d, img = dd + d;
+    std::vector<float> m(n * img, 0.0f), v(n * img, 0.0f);
+    for (int step = 1; step <= 3; ++step) {
+        float loss = 0.0f;
+        REQUIRE(sp_train_step(ex, x.values.data(), t.values.data(), rows, lr, &loss) == SP_OK);
+        std::vector<float> W(f.W), b(f.b), dW(f.W.size()), db(f.b.size());
+        const float want_loss = orc_train_step(n, d, W.data(), b.data(), f.relu.data(), f.frozen.data(),
+                                               x.values.data(), t.values.data(), rows, lr, dW.data(),
+                                               db.data(), nullptr);
+        CHECK(std::memcmp(&loss, &want_loss, 4) == 0);
+        const double tt = step;
+        const float decay = static_cast<float>(1.0 - static_cast<double>(lr) * wd);
+        const float omb1 = static_cast<float>(1.0 - b1), bb2 = b2, omb2 = static_cast<float>(1.0 - b2);
+        const float bc2 = static_cast<float>(std::sqrt(1.0 - std::pow(static_cast<double>(b2), tt)));
+        const float neg = static_cast<float>(-static_cast<double>(lr) / (1.0 - std::pow(static_cast<double>(b1), tt)));
+        for (int l = 0; l < n; ++l) {
+            if (f.frozen[l]) continue;
+            float* ml = m.data() + l * img;
+            float* vl = v.data() + l * img;
+            orc_adamw(static_cast<int64_t>(dd), f.W.data() + l * dd, ml, vl, dW.data() + l * dd, decay, omb1, bb2,
+                      omb2, bc2, eps, neg);
+            orc_adamw(d, f.b.data() + l * d, ml + dd, vl + dd, db.data() + l * d, decay, omb1, bb2, omb2, bc2,
+                      eps, neg);
+        }
+    }
+    for (int l = 0; l < n; ++l) {
+        std::vector<float> W(dd), b(d), mW(dd), mb(d), vW(dd), vb(d);
+        REQUIRE(sp_read_layer(ex, l, W.data(), b.data()) == SP_OK);
+        REQUIRE(sp_read_optimizer_state(ex, l, mW.data(), mb.data(), vW.data(), vb.data()) == SP_OK);
+        CHECK(std::memcmp(W.data(), f.W.data() + l * dd, dd * 4) == 0);
+        CHECK(std::memcmp(b.data(), f.b.data() + l * d, d * 4) == 0);
+        CHECK(std::memcmp(mW.data(), m.data() + l * img, dd * 4) == 0);
+        CHECK(std::memcmp(mb.data(), m.data() + l * img + dd, d * 4) == 0);
+        CHECK(std::memcmp(vW.data(), v.data() + l * img, dd * 4) == 0);
+        CHECK(std::memcmp(vb.data(), v.data() + l * img + dd, d * 4) == 0);
+    }
+    sp_destroy(ex);
+}
+
 int main(int argc, char** argv) { return mini::run(argc, argv); }
