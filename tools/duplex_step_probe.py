@@ -52,3 +52,22 @@ out = {"h2d_alone": run(True, False, False), "d2h_alone": run(False, True, False
        "duplex": run(True, True, False), "h2d_with_gemm": run(True, False, True),
        "duplex_with_gemm": run(True, True, True)}
 print(json.dumps(out))
+
+# Same pattern with host buffers from the executor's own allocator (sp_host_alloc:
+# cudaHostAllocPortable, first touched by this thread), to separate allocation / NUMA
+# placement effects from the executor's scheduling.
+import os  # noqa: E402
+import sys  # noqa: E402
+
+import numpy as np  # noqa: E402
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2410_08791_b200 as sp  # noqa: E402
+
+hb_up = sp.HostBuffer((N * LB,), np.uint8)
+hb_dn = sp.HostBuffer((N * LB,), np.uint8)
+hb_up.array[:] = 1
+hb_dn.array[:] = 1
+h_up = torch.from_numpy(hb_up.array)
+h_dn = torch.from_numpy(hb_dn.array)
+print(json.dumps({"sp_host_alloc": {"h2d_alone": run(True, False, False), "duplex": run(True, True, False)}}))
