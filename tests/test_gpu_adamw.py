@@ -200,3 +200,29 @@ def test_adamw_trains_and_survives_graph_replay_over_many_steps():
     assert same(got[1:], ref[1:])
     assert [x.tobytes() for x in got[0]] == [x.tobytes() for x in ref[0]]
     assert got[0][-1] < got[0][0]
+
+
+@pytest.mark.parametrize("n,strats", [
+    (1, [S(sp.STANDARD), S(sp.NAIVE, 1)]),                                 # a single layer
+    (3, [S(sp.SUPERPIPELINE, 2, 1), S(sp.SUPERPIPELINE, 3, 2), S(sp.NAIVE, 3),
+         S(sp.SUPERPIPELINE, 2, 1, sp.SEQUENTIAL)]),                      # ring covers every layer
+])
+def test_adamw_edge_windows_and_digest_after_deferred_writeback(n, strats):
+    """Edge windows (one layer; a ring holding the whole model, so every write-back is deferred;
+    sequential transfers): AdamW stays bit-identical to the oracle, and digest_train over the
+    executor's host master (which must first complete the deferred write-backs) equals the
+    reference's digest of the oracle's weights."""
+    model = sp.build_model(9, n, 8, 0)
+    batches = [(sp.make_input(9, 0, 5, 8), sp.make_input(9, 1, 5, 8))]
+    lr = F(0.02)
+    ref = oracle_adamw(model, batches, lr, 3, **HP)
+    for s in strats:
+        with sp.Executor(n, 8, s) as ex:
+            ex.register_model(model)
+            ex.set_optimizer(sp.OPT_ADAMW, **HP)
+            losses = [np.float32(ex.train_step(batches[0][0], batches[0][1], lr)) for _ in range(3)]
+            digest = ex.digest_train(float(losses[-1]))  # no read before: flushes pending write-backs
+            m = ex.read_model(model)
+        assert [x.tobytes() for x in losses] == [x.tobytes() for x in ref[0]], s
+        assert np.array_equal(m.W, ref[1]) and np.array_equal(m.b, ref[2]), s
+        assert digest == ORC.digest_train(ref[0][-1], ref[1], ref[2]), s
