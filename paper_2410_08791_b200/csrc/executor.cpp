@@ -138,6 +138,7 @@ Executor::~Executor() {
     for (auto e : ev_start_) cudaEventDestroy(e);
     for (auto e : gemm_ev_) cudaEventDestroy(e);
     for (auto e : ev_dep_) cudaEventDestroy(e);
+    for (auto e : ev_move_) cudaEventDestroy(e);
     for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second.exec);
     if (ev_fork_) cudaEventDestroy(ev_fork_);
     if (ev_loss_) cudaEventDestroy(ev_loss_);
@@ -664,12 +665,26 @@ void Executor::enqueue_op(const Plan& plan, int i, bool train, int n_items, int6
     const Op& op = plan.ops[static_cast<size_t>(i)];
     cudaStream_t st = stream_of(op.kind);
     auto wait = [&](int dep) {
-        if (stream_of(plan.ops[static_cast<size_t>(dep)].kind) != st)
-            CUDA_OK(cudaStreamWaitEvent(st, ev_dep_[static_cast<size_t>(dep)], 0));
+        const Op& d = plan.ops[static_cast<size_t>(dep)];
+        if (stream_of(d.kind) == st) return;
+        // A compute waits only for the move of its own layer in a multi-layer H2D job
+        const int base = move_ev_base_[static_cast<size_t>(dep)];
+        if (op.kind == OpKind::Compute && base >= 0) {
+            for (size_t j = 0; j + 1 < d.layers.size(); ++j)
+                if (d.layers[j] == op.layer && d.slots[j] == op.slot) {
+                    CUDA_OK(cudaStreamWaitEvent(st, ev_move_[static_cast<size_t>(base) + j], 0));
+                    return;
+                }
+        }
+        CUDA_OK(cudaStreamWaitEvent(st, ev_dep_[static_cast<size_t>(dep)], 0));
     };
     // Eager H2D: each moved layer waits for its own slot just before its copy (deps is then
     // exactly the union of move_deps); otherwise everything up front (policy trigger).
-    const bool per_move = op.kind == OpKind::H2D && eager_prefetch_ && !op.move_deps.empty();
+    static const bool per_move_on = [] {  // SP_PER_MOVE=0: A/B measurement only
+        const char* e = std::getenv("SP_PER_MOVE");
+        return !e || std::atoi(e) != 0;
+    }();
+    const bool per_move = per_move_on && op.kind == OpKind::H2D && eager_prefetch_ && !op.move_deps.empty();
     if (!per_move)
         for (int dep : op.deps) wait(dep);
     // Timing events are "external" so that, under graph capture, they become event-record
@@ -720,6 +735,9 @@ void Executor::enqueue_op(const Plan& plan, int i, bool train, int n_items, int6
                     }
                     h2d_bytes_ += 2 * (hi - lo);
                 }
+                const int base = move_ev_base_[static_cast<size_t>(i)];
+                if (base >= 0 && j + 1 < op.layers.size())  // this layer has landed
+                    CUDA_OK(cudaEventRecord(ev_move_[static_cast<size_t>(base) + j], st));
             }
             break;
         case OpKind::Compute:
@@ -800,6 +818,22 @@ void Executor::enqueue_call(const Plan& plan, const CallIO& io) {
         for (int dep : plan.ops[j].deps)
             if (stream_of(plan.ops[static_cast<size_t>(dep)].kind) != stream_of(plan.ops[j].kind))
                 cross_dep_[static_cast<size_t>(dep)] = 1;
+    move_ev_base_.assign(plan.ops.size(), -1);
+    static const bool move_events = [] {  // SP_MOVE_EVENTS=0: A/B measurement only
+        const char* e = std::getenv("SP_MOVE_EVENTS");
+        return !e || std::atoi(e) != 0;
+    }();
+    size_t moves = 0;
+    for (size_t j = 0; j < plan.ops.size() && move_events; ++j)
+        if (plan.ops[j].kind == OpKind::H2D && plan.ops[j].layers.size() > 1) {
+            move_ev_base_[j] = static_cast<int>(moves);
+            moves += plan.ops[j].layers.size() - 1;
+        }
+    while (ev_move_.size() < moves) {
+        cudaEvent_t e;
+        CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        ev_move_.push_back(e);
+    }
     record_timing(ev_call0_, s_h2d_);
     CUDA_OK(cudaEventRecord(ev_fork_, s_h2d_));
     for (auto s : {s_comp_, s_d2h_, s_upd_}) CUDA_OK(cudaStreamWaitEvent(s, ev_fork_, 0));

@@ -140,6 +140,10 @@ private:
     cudaStream_t s_h2d_ = nullptr, s_comp_ = nullptr, s_d2h_ = nullptr, s_upd_ = nullptr;
     std::vector<cudaEvent_t> ev_done_, ev_start_;  // per-op timing (external records)
     std::vector<cudaEvent_t> ev_dep_;              // per-op dependency edges
+    // Per-move completion of multi-layer H2D jobs: a layer's compute waits for its own copy,
+    // not for the whole job (move_ev_base_[op] indexes ev_move_; -1 = none).
+    std::vector<cudaEvent_t> ev_move_;
+    std::vector<int> move_ev_base_;
     cudaEvent_t ev_call0_ = nullptr, ev_io_in_ = nullptr, ev_io_out_ = nullptr;
     cudaEvent_t ev_fork_ = nullptr, ev_join_[3] = {nullptr, nullptr, nullptr};
     cudaEvent_t ev_call1_ = nullptr, ev_loss_ = nullptr;

@@ -18,8 +18,11 @@ its own offload). Buffers modelled:
   write-back stage[i] UPDATE(stage=i) writes (copy of its slot); D2H(stage=i) reads it instead
                       of the slot. A deferred D2H moves nothing in its call; the next call's
                       plan starts with that write-back (SP_PLAN_WRITEBACK shows the steady state)
-Eager prefetch: the executor waits each moved layer's own dependencies (md=) right before its
-copy, so an H2D job is checked as one sub-op per moved layer in stream order.
+An H2D job is checked as one sub-op per moved layer, in stream order, as the executor runs
+it: with eager prefetch each moved layer waits for its own dependencies (md=) right before its
+copy (otherwise the job's first copy waits for all of them), and a COMPUTE that depends on the
+job waits only for the sub-op that moved its own layer (a per-move completion event); every
+other dependent waits for the whole job.
 """
 import itertools
 
@@ -105,21 +108,33 @@ def happens_before(ops):
     return lambda a, b: bool(reach[b] >> a & 1)
 
 
-def split_moves(ops):
-    """Eager mode: one sub-op per moved layer of each H2D job, waiting only its own md deps
-    (plus stream order); dependents of the job wait for its last sub-op."""
-    last, out = {}, []
+def split_moves(ops, eager=True):
+    """One sub-op per moved layer of each H2D job (see the module docstring)."""
+    last, first, out = {}, {}, []
+    by_index = {op["index"]: op for op in ops}
+
+    def dep_of(op, d):
+        src = by_index[d]
+        if op["kind"] == "COMPUTE" and src["kind"] == "H2D":
+            for j, (L, s) in enumerate(zip(src["layers"], src["slots"])):
+                if L == op["layer"] and s == op["slot"]:
+                    return first[d] + j
+        return last[d]
+
     for op in ops:
-        if op["kind"] == "H2D" and op.get("md") is not None and len(op["layers"]) > 0:
+        if op["kind"] == "H2D" and len(op["layers"]) > 0:
+            first[op["index"]] = len(out)
             for j in range(len(op["layers"])):
                 sub = {k: ([v[j]] if k in ("layers", "slots", "w", "a", "o") and isinstance(v, list) else v)
                        for k, v in op.items()}
-                sub["deps"] = [last[d] for d in (op["md"][j] if j < len(op["md"]) else [])]
+                if eager and op.get("md") is not None:
+                    sub["deps"] = [last[d] for d in (op["md"][j] if j < len(op["md"]) else [])]
+                else:
+                    sub["deps"] = [last[d] for d in op["deps"]] if j == 0 else []
                 sub["index"] = len(out)
                 out.append(sub)
         else:
-            sub = dict(op, deps=[last[d] for d in op["deps"]], index=len(out))
-            out.append(sub)
+            out.append(dict(op, deps=[dep_of(op, d) for d in op["deps"]], index=len(out)))
         last[op["index"]] = len(out) - 1
     return out
 
@@ -140,8 +155,7 @@ def check_one(n, strategy, train, ckpt, items, frozen, sharded, eager, opt=False
                            writeback=wb)
     assert not txt.startswith("ERROR"), txt
     head, ops = parse_plan(txt)
-    if eager:
-        ops = split_moves(ops)
+    ops = split_moves(ops, eager)
     ck = ckpt and train and strategy.kind != sp.STANDARD
     hb = happens_before(ops)
     by_res = {}
