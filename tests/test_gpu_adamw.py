@@ -189,17 +189,44 @@ def test_adamw_bf16_window_invariant_and_close(d, rows):
     assert abs(float(got[0][-1]) - float(ref[0][-1])) <= 2e-2 * abs(float(ref[0][-1]))
 
 
-def test_adamw_trains_and_survives_graph_replay_over_many_steps():
-    """20 steps (one graph capture, 19 replays with new per-step scalars): bitwise equal to the
-    oracle and the loss falls."""
-    model = sp.build_model(3, 4, 16, 0)
-    batches = [(sp.make_input(3, 0, 8, 16), sp.make_input(3, 1, 8, 16))]
+@pytest.mark.parametrize("numerics", [sp.EXACT, sp.BF16])
+def test_adamw_trains_and_survives_graph_replay_over_many_steps(numerics):
+    """20 steps from pinned host buffers, so each call replays one captured CUDA graph whose
+    AdamW scalars are re-read from device memory (refreshed per call): exact numerics stay
+    bitwise equal to the oracle, bf16 replays equal an eager (uncaptured) run bitwise, and
+    the loss falls."""
+    d = 16 if numerics == sp.EXACT else 128
+    rows = 8 if numerics == sp.EXACT else 256
+    model = sp.build_model(3, 4, d, 0)
+    x, t = sp.make_input(3, 0, rows, d), sp.make_input(3, 1, rows, d)
+    hx, ht = sp.HostBuffer(x.shape), sp.HostBuffer(t.shape)
+    hx.array[...] = x
+    ht.array[...] = t
     lr = F(0.003)
-    ref = oracle_adamw(model, batches, lr, 20, **HP)
-    got = run_adamw(model, batches, lr, 20, S(sp.SUPERPIPELINE, 2, 1), **HP)
-    assert same(got[1:], ref[1:])
-    assert [x.tobytes() for x in got[0]] == [x.tobytes() for x in ref[0]]
-    assert got[0][-1] < got[0][0]
+
+    def run(pinned):
+        with sp.Executor(4, d, S(sp.SUPERPIPELINE, 2, 1), numerics=numerics) as ex:
+            ex.register_model(model)
+            ex.set_optimizer(sp.OPT_ADAMW, **HP)
+            if pinned:
+                losses = [np.float32(ex.train_step_ptr(hx.ptr, ht.ptr, rows, lr, device=False))
+                          for _ in range(20)]
+                assert ex.stats()["graph_replays"] >= 18
+            else:
+                losses = [np.float32(ex.train_step(x.copy(), t.copy(), lr)) for _ in range(20)]
+            return losses, ex.read_model(model), [ex.read_optimizer_state(L) for L in range(4)]
+
+    g_losses, g_model, g_state = run(True)
+    e_losses, e_model, e_state = run(False)
+    assert [v.tobytes() for v in g_losses] == [v.tobytes() for v in e_losses]
+    assert np.array_equal(g_model.W, e_model.W) and np.array_equal(g_model.b, e_model.b)
+    for a, b in zip(g_state, e_state):
+        assert all(np.array_equal(u, v) for u, v in zip(a, b))
+    if numerics == sp.EXACT:
+        ref = oracle_adamw(model, [(x, t)], lr, 20, **HP)
+        assert np.array_equal(g_model.W, ref[1]) and np.array_equal(g_model.b, ref[2])
+        assert [v.tobytes() for v in g_losses] == [v.tobytes() for v in ref[0]]
+    assert g_losses[-1] < g_losses[0]
 
 
 @pytest.mark.parametrize("n,strats", [
