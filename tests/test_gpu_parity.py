@@ -627,3 +627,40 @@ def test_staged_and_deferred_writeback_is_bitwise_and_flushes_on_read(numerics, 
         for _ in range(4):
             _, W, bb = ORC.train_step(W, bb, x, t, 0.02, frozen=model.frozen)
         assert np.array_equal(b[6], W)
+
+
+@pytest.mark.parametrize("numerics", [sp.EXACT, sp.BF16])
+def test_graph_replayed_steps_with_deferred_writeback_equal_eager_steps(numerics):
+    """Consecutive train steps from pinned host buffers replay one captured graph per plan
+    (the steady-state plan starts with the previous step's deferred write-backs, and compute
+    waits on per-move completion events); they must equal the same steps enqueued eagerly
+    (pageable inputs, no capture) bitwise, and the oracle in exact numerics."""
+    d = 16 if numerics == sp.EXACT else 128
+    rows = 6 if numerics == sp.EXACT else 256
+    model = sp.build_model(27, 9, d, 1)
+    x, t = sp.make_input(27, 0, rows, d), sp.make_input(27, 1, rows, d)
+    hx, ht = sp.HostBuffer(x.shape), sp.HostBuffer(t.shape)
+    hx.array[...] = x
+    ht.array[...] = t
+    for s in (S(sp.SUPERPIPELINE, 4, 2), S(sp.SUPERPIPELINE, 3, 1, sp.SEQUENTIAL), S(sp.STANDARD)):
+        runs = []
+        for pinned in (True, False):
+            with sp.Executor(9, d, s, numerics=numerics) as ex:
+                ex.register_model(model)
+                losses = []
+                for _ in range(6):
+                    if pinned:
+                        losses.append(ex.train_step_ptr(hx.ptr, ht.ptr, rows, 0.02, device=False))
+                    else:
+                        losses.append(ex.train_step(x.copy(), t.copy(), 0.02))
+                if pinned:
+                    assert ex.stats()["graph_replays"] >= 4, s
+                runs.append((losses, ex.read_model(model)))
+        (lg, mg), (le, me) = runs
+        assert lg == le, s
+        assert np.array_equal(mg.W, me.W) and np.array_equal(mg.b, me.b), s
+        if numerics == sp.EXACT:
+            W, b = model.W.copy(), model.b.copy()
+            for _ in range(6):
+                _, W, b = ORC.train_step(W, b, x, t, 0.02, frozen=model.frozen)
+            assert np.array_equal(mg.W, W) and np.array_equal(mg.b, b), s
