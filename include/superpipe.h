@@ -198,6 +198,17 @@ int sp_read_optimizer_state(sp_exec* ex, int32_t index, float* mW, float* mb, fl
 /* Copies up to cap events of the last call's measured timeline; *count = total rows. */
 int sp_get_trace(const sp_exec* ex, sp_trace_event* events, int32_t cap, int32_t* count);
 
+/* One pinned host master per node (every rank streams from a shared pinned copy):
+ * create = 1 moves this executor's fp32 master (and the layers' activation / frozen flags)
+ * into the POSIX shared-memory segment `name` (replacing any stale one); create = 0 attaches
+ * to the segment another process created for the same (n_layers, d) and drops the private
+ * copy. Each process registers the segment with CUDA (cudaHostRegisterPortable), so copies
+ * stay pinned-speed. Layers registered through any attached executor are visible to all.
+ * Sharded data parallel then needs no all-gather of the weights in sp_dp_sync (each rank's
+ * write-back lands in the one copy; sp_dp_sync is a barrier for them). Without sharding, every
+ * rank writes back the same all-reduced update, so concurrent write-backs agree bitwise. */
+int sp_share_host_master(sp_exec* ex, const char* name, int32_t create);
+
 /* ---- data parallel ----------------------------------------------------------------- */
 /* Per-layer NCCL all-reduce of dW/db as each layer's backward completes. */
 int sp_nccl_unique_id(uint8_t id[128]);

@@ -64,7 +64,7 @@ EXPORTS = [
     "sp_create", "sp_register_layer", "sp_destroy", "sp_last_error", "sp_abi_version",
     "sp_forward", "sp_forward_device", "sp_train_step", "sp_train_step_device",
     "sp_read_layer", "sp_get_stats", "sp_get_trace", "sp_set_trace", "sp_last_plan", "sp_set_item_batching", "sp_set_eager_prefetch",
-    "sp_set_optimizer", "sp_read_optimizer_state",
+    "sp_set_optimizer", "sp_read_optimizer_state", "sp_share_host_master",
     "sp_nccl_unique_id",
     "sp_dp_init", "sp_dp_init2", "sp_dp_sync",
     "sp_host_alloc", "sp_host_free", "sp_peak_weight_residency", "sp_validate_strategy",
@@ -101,6 +101,7 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "sp_set_eager_prefetch": ([ex, i32], C.c_int),
         "sp_set_optimizer": ([ex, i32, C.c_float, C.c_float, C.c_float, C.c_float], C.c_int),
         "sp_read_optimizer_state": ([ex, i32, vp, vp, vp, vp], C.c_int),
+        "sp_share_host_master": ([ex, C.c_char_p, i32], C.c_int),
         "sp_last_plan": ([ex, C.c_char_p, i64], i64),
         "sp_nccl_unique_id": ([C.c_char_p], C.c_int),
         "sp_dp_init": ([ex, C.c_char_p, i32, i32], C.c_int),

@@ -145,6 +145,11 @@ int sp_set_item_batching(sp_exec* ex, int32_t on) {
     return SP_OK;
 }
 
+int sp_share_host_master(sp_exec* ex, const char* name, int32_t create) {
+    if (!ex) return SP_ERR_INVALID;
+    return guarded(ex, [&] { ex->impl->share_host_master(name, create != 0); });
+}
+
 int sp_set_optimizer(sp_exec* ex, int32_t kind, float beta1, float beta2, float eps, float weight_decay) {
     if (!ex) return SP_ERR_INVALID;
     return guarded(ex, [&] { ex->impl->set_optimizer(kind, beta1, beta2, eps, weight_decay); });

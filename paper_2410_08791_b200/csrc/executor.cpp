@@ -12,6 +12,10 @@
 #include "executor.hpp"
 
 #include <cuda_bf16.h>
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <chrono>
@@ -148,7 +152,13 @@ Executor::~Executor() {
     if (ev_call1_) cudaEventDestroy(ev_call1_);
     if (ev_io_in_) cudaEventDestroy(ev_io_in_);
     if (ev_io_out_) cudaEventDestroy(ev_io_out_);
-    if (host32_) cudaFreeHost(host32_);
+    if (shm_) {
+        cudaHostUnregister(host32_);
+        munmap(shm_, shm_bytes_);
+        if (shm_owner_) shm_unlink(shm_name_.c_str());
+    } else if (host32_) {
+        cudaFreeHost(host32_);
+    }
     if (host_m_) cudaFreeHost(host_m_);
     if (host_v_) cudaFreeHost(host_v_);
     if (adamw_host_) cudaFreeHost(adamw_host_);
@@ -219,8 +229,129 @@ void Executor::flush_writebacks() {
         host16_stale_[static_cast<size_t>(L)] = 1;
     }
     CUDA_OK(cudaStreamSynchronize(s_d2h_));
+    for (int L : pending_wb_layers_) bump_version(L);
     pending_wb_layers_.clear();
     pending_wb_slots_.clear();
+}
+
+// Shared master segment: [header | relu[n] frozen[n] registered[n] (int32) | pad | master].
+struct Executor::ShmHeader {
+    uint64_t magic;
+    int32_t n, d;
+    uint64_t master_offset, master_bytes;
+    int32_t meta[1];  // 3 * n int32 follow
+};
+namespace {
+constexpr uint64_t kShmMagic = 0x3176'4D48'5350'5053ull;  // "SPSPHMv1"
+}
+
+void Executor::sync_layer_meta(int index) {
+    if (!shm_) return;
+    int32_t* meta = shm_->meta;
+    if (index >= 0) {  // this process registered a layer: publish its metadata
+        meta[index] = relu_[static_cast<size_t>(index)];
+        meta[n_ + index] = frozen_[static_cast<size_t>(index)];
+        meta[2 * n_ + index] = registered_[static_cast<size_t>(index)];
+        return;
+    }
+    for (int L = 0; L < n_; ++L) {  // pick up what other processes registered
+        relu_[static_cast<size_t>(L)] = meta[L];
+        frozen_[static_cast<size_t>(L)] = meta[n_ + L];
+        registered_[static_cast<size_t>(L)] = static_cast<uint8_t>(meta[2 * n_ + L]);
+    }
+}
+
+void Executor::share_host_master(const char* name, bool create) {
+    if (!name || !*name) throw Error(SP_ERR_INVALID, "share_host_master: empty segment name");
+    if (shm_) throw Error(SP_ERR_STATE, "share_host_master: the master is already shared");
+    flush_writebacks();
+    if (create) require_full_host(-1, "share_host_master");
+    CUDA_OK(cudaSetDevice(cfg_.device));
+    for (auto s : {s_h2d_, s_comp_, s_d2h_, s_upd_}) CUDA_OK(cudaStreamSynchronize(s));
+    const std::string nm = name[0] == '/' ? std::string(name) : "/" + std::string(name);
+    const size_t master = static_cast<size_t>(n_) * (static_cast<size_t>(d_) * d_ + d_) * 4;
+    const size_t ver_off = round_up(offsetof(ShmHeader, meta) + 12 * static_cast<size_t>(n_), 8);
+    const size_t off = round_up(ver_off + 8 * static_cast<size_t>(n_), 4096);
+    const size_t bytes = off + master;
+    int fd = -1;
+    if (create) {
+        shm_unlink(nm.c_str());  // a stale segment of a crashed run
+        fd = shm_open(nm.c_str(), O_CREAT | O_EXCL | O_RDWR, 0600);
+        if (fd < 0 || ftruncate(fd, static_cast<off_t>(bytes)) != 0) {
+            if (fd >= 0) close(fd);
+            throw Error(SP_ERR_INTERNAL, "share_host_master: cannot create shared segment " + nm);
+        }
+    } else {
+        fd = shm_open(nm.c_str(), O_RDWR, 0);
+        struct stat st{};
+        if (fd < 0 || fstat(fd, &st) != 0 || static_cast<size_t>(st.st_size) != bytes) {
+            if (fd >= 0) close(fd);
+            throw Error(SP_ERR_INVALID, "share_host_master: no segment " + nm + " of this model's size");
+        }
+    }
+    void* p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+    close(fd);
+    if (p == MAP_FAILED) throw Error(SP_ERR_INTERNAL, "share_host_master: mmap failed");
+    auto* h = static_cast<ShmHeader*>(p);
+    float* base = reinterpret_cast<float*>(static_cast<uint8_t*>(p) + off);
+    if (create) {
+        std::memcpy(base, host32_, master);
+        h->n = n_;
+        h->d = d_;
+        h->master_offset = off;
+        h->master_bytes = master;
+        for (int L = 0; L < n_; ++L) {
+            h->meta[L] = relu_[static_cast<size_t>(L)];
+            h->meta[n_ + L] = frozen_[static_cast<size_t>(L)];
+            h->meta[2 * n_ + L] = registered_[static_cast<size_t>(L)];
+        }
+        __atomic_store_n(&h->magic, kShmMagic, __ATOMIC_RELEASE);
+    } else if (__atomic_load_n(&h->magic, __ATOMIC_ACQUIRE) != kShmMagic || h->n != n_ || h->d != d_) {
+        munmap(p, bytes);
+        throw Error(SP_ERR_INVALID, "share_host_master: segment " + nm + " holds another model");
+    }
+    const cudaError_t e = cudaHostRegister(base, master, cudaHostRegisterPortable);
+    if (e != cudaSuccess) {
+        munmap(p, bytes);
+        if (create) shm_unlink(nm.c_str());
+        throw Error(SP_ERR_CUDA, std::string("share_host_master: cudaHostRegister: ") + cudaGetErrorString(e));
+    }
+    cudaFreeHost(host32_);
+    host32_ = base;
+    shm_ = h;
+    shm_bytes_ = bytes;
+    shm_name_ = nm;
+    shm_owner_ = create;
+    ver_off_ = ver_off;
+    cache_ver_.assign(static_cast<size_t>(n_), ~0ull);
+    host16_ver_.assign(static_cast<size_t>(n_), ~0ull);
+    plan_ver_.assign(static_cast<size_t>(n_), 0);
+    sync_layer_meta(-1);
+    std::fill(host16_stale_.begin(), host16_stale_.end(), 1);
+    for (auto& c : cache_) c.valid = false;
+    std::fill(w16_layer_.begin(), w16_layer_.end(), -1);
+    for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second.exec);  // host pointers are baked in
+    graphs_.clear();
+}
+
+uint64_t Executor::layer_version(int L) const {
+    return shm_ ? __atomic_load_n(&shm_versions()[L], __ATOMIC_ACQUIRE) : 0;
+}
+
+void Executor::bump_version(int L) {
+    if (shm_) cache_ver_[static_cast<size_t>(L)] = __atomic_add_fetch(&shm_versions()[L], 1, __ATOMIC_ACQ_REL);
+}
+
+// After a call's streams are synchronised: publish this call's host writes (write-backs run in
+// it, including the previous call's deferred ones) and note which versions the loads saw.
+void Executor::after_call(const Plan& plan) {
+    if (!shm_) return;
+    for (const Op& op : plan.ops) {
+        if (op.kind == OpKind::D2H && !op.deferred) bump_version(op.layers[0]);
+        if (op.kind == OpKind::H2D)
+            for (size_t j = 0; j < op.layers.size(); ++j)
+                if (op.weights[j]) cache_ver_[static_cast<size_t>(op.layers[j])] = plan_ver_[static_cast<size_t>(op.layers[j])];
+    }
 }
 
 void Executor::register_layer(int index, const float* W, const float* b, int activation,
@@ -239,6 +370,8 @@ void Executor::register_layer(int index, const float* W, const float* b, int act
     registered_[index] = 1;
     host16_stale_[index] = 1;
     host_partial_[index] = 0;
+    sync_layer_meta(index);
+    bump_version(index);
     for (auto& c : cache_)
         if (c.layer == index) c.valid = false;
 }
@@ -251,7 +384,8 @@ void Executor::require_full_host(int layer, const char* what) const {
                                           "call sp_dp_sync() on every rank first");
 }
 
-void Executor::check_ready() const {
+void Executor::check_ready() {
+    if (shm_) sync_layer_meta(-1);  // layers registered by another process sharing the master
     for (int i = 0; i < n_; ++i)
         if (!registered_[i])
             throw Error(SP_ERR_STATE, "layer " + std::to_string(i) + " was never registered");
@@ -260,8 +394,11 @@ void Executor::check_ready() const {
 void Executor::refresh_host16() {
     if (!bf16_) return;
     std::vector<int> todo;
-    for (int i = 0; i < n_; ++i)
-        if (host16_stale_[i]) todo.push_back(i);
+    for (int i = 0; i < n_; ++i) {
+        const uint64_t v = layer_version(i);  // another process may have written the master
+        if (host16_stale_[i] || (shm_ && v != host16_ver_[static_cast<size_t>(i)])) todo.push_back(i);
+        if (shm_) host16_ver_[static_cast<size_t>(i)] = v;
+    }
     if (todo.empty()) return;
     const size_t dd = static_cast<size_t>(d_) * d_;
     parallel_for(static_cast<int>(todo.size()), [&](int t) {
@@ -358,8 +495,17 @@ Plan Executor::make_plan(bool train, int n_items, int64_t rows, int fmt) {
     in.eager = eager_prefetch_;
     in.optimizer_state = train && adamw();
     in.wb_stages = train && stages_dev_ ? n_stages_ : 0;
-    // (checkpointing: the D2H engine carries the forward's activation offloads - no deferral)
-    in.defer_writeback = train && staged_writeback_ && !cfg_.checkpointing;
+    // (checkpointing: the D2H engine carries the forward's activation offloads - no deferral;
+    // a master shared outside data parallel must be complete when the call returns)
+    const bool foreign_writers = shm_ && !comm_;
+    in.defer_writeback = train && staged_writeback_ && !cfg_.checkpointing && !foreign_writers;
+    if (shm_) {
+        for (int L = 0; L < n_; ++L) plan_ver_[static_cast<size_t>(L)] = layer_version(L);
+        if (foreign_writers)
+            for (auto& c : cache_)
+                if (c.valid && c.layer >= 0 && plan_ver_[static_cast<size_t>(c.layer)] != cache_ver_[static_cast<size_t>(c.layer)])
+                    c.valid = false;
+    }
     if (train && fmt == cache_fmt_) {
         in.pending_wb_layers = pending_wb_layers_;
         in.pending_wb_slots = pending_wb_slots_;
@@ -902,6 +1048,8 @@ uint64_t Executor::call_signature(const Plan& plan, const CallIO& io) const {
     mix(reinterpret_cast<uintptr_t>(io.t));
     mix(reinterpret_cast<uintptr_t>(io.y));
     for (int v : w16_layer_) mix(static_cast<uint64_t>(static_cast<uint32_t>(v)));
+    for (int L = 0; L < n_; ++L)  // activations are baked into the captured kernels
+        mix(static_cast<uint64_t>(relu_[static_cast<size_t>(L)] != 0) | static_cast<uint64_t>(L) << 1);
     mix(static_cast<uint64_t>(splits_) | static_cast<uint64_t>(col_chunks_) << 32);
     mix(reinterpret_cast<uintptr_t>(comm_));
     mix(alloc_gen_);
@@ -1117,6 +1265,7 @@ void Executor::forward(const float* x, int64_t rows, int n_items, float* y, bool
     host_enqueue_ms_ = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     for (auto s : {s_h2d_, s_comp_, s_d2h_, s_upd_}) CUDA_OK(cudaStreamSynchronize(s));
     CUDA_OK(cudaGetLastError());
+    after_call(plan);
     collect_stats(plan, n_items, false);
     stats_.loss = 0.0f;
     std::memset(stats_.digest, 0, sizeof(stats_.digest));  // on demand: sp_digest_tensors(y)
@@ -1166,6 +1315,7 @@ float Executor::train_step(const float* x, const float* target, int64_t rows, fl
     host_enqueue_ms_ = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     for (auto s : {s_h2d_, s_comp_, s_d2h_, s_upd_}) CUDA_OK(cudaStreamSynchronize(s));
     CUDA_OK(cudaGetLastError());
+    after_call(plan);
     collect_stats(plan, 1, true);
     if (sharded_)
         for (int L = 0; L < n_; ++L)
@@ -1288,10 +1438,15 @@ void Executor::dp_sync() {
     size_t lo = 0, hi = 0;
     shard_range(shardA_, img, lo, hi);
     uint8_t* stage = slot_ptr(0);
+    if (shm_) {  // every rank's train steps (and their write-backs) have completed past here
+        NCCL_OK(nccl().AllReduce(loss_dev_ + 1, loss_dev_ + 1, 1, ncclFloat, ncclSum, comm_, s_upd_));
+        CUDA_OK(cudaStreamSynchronize(s_upd_));
+    }
     for (int L = 0; L < n_; ++L) {
         if (!host_partial_[static_cast<size_t>(L)]) continue;
-        // The weights, then (AdamW) the moments: all three are written back shard-only.
-        for (float* base : {host32_, adamw() ? host_m_ : nullptr, adamw() ? host_v_ : nullptr}) {
+        // The weights, then (AdamW) the moments: all three are written back shard-only. A
+        // shared master (share_host_master) already holds every rank's shard: a barrier below.
+        for (float* base : {shm_ ? nullptr : host32_, adamw() ? host_m_ : nullptr, adamw() ? host_v_ : nullptr}) {
             if (!base) continue;
             uint8_t* host = reinterpret_cast<uint8_t*>(base + static_cast<size_t>(L) * (dd + d_));
             if (hi > lo) CUDA_OK(cudaMemcpyAsync(stage + lo, host + lo, hi - lo, cudaMemcpyHostToDevice, s_upd_));

@@ -47,6 +47,10 @@ public:
     // host memory, streamed with each trainable layer's backward). Resets the state and step.
     void set_optimizer(int kind, float beta1, float beta2, float eps, float weight_decay);
     void read_optimizer_state(int index, float* mW, float* mb, float* vW, float* vb);
+    // Moves the pinned fp32 master into a named POSIX shared-memory segment (create) or
+    // attaches to one another process created (layer metadata included), registered with
+    // CUDA in every process: one host copy serves all ranks of a node.
+    void share_host_master(const char* name, bool create);
 
     const sp_stats& stats() const { return stats_; }
     const std::vector<sp_trace_event>& trace() const { return trace_; }
@@ -93,7 +97,7 @@ private:
     void ensure_stages();
     void flush_writebacks();
     uint8_t* stage_ptr(int i) const { return stages_dev_ + static_cast<size_t>(i) * stage_bytes_; }
-    void check_ready() const;
+    void check_ready();
     void ensure_buffers(int64_t rows, int n_items, bool train, bool device_io);
     void refresh_host16();
     Plan make_plan(bool train, int n_items, int64_t rows, int fmt);
@@ -117,6 +121,23 @@ private:
     bool tc_ = false;    // either tensor-core path (split-K partials, masks, fused loss)
     // pinned host copies
     float* host32_ = nullptr;  // [n][d*d + d] fp32 master (W then b)
+    // Shared master (share_host_master): header + master in a POSIX shm segment.
+    struct ShmHeader;
+    ShmHeader* shm_ = nullptr;
+    size_t shm_bytes_ = 0;
+    std::string shm_name_;
+    bool shm_owner_ = false;
+    void sync_layer_meta(int index);
+    // Per-layer write versions in the segment: every host write of layer L (registration,
+    // write-back) increments version[L]. Outside data parallel, where another process may
+    // have written a layer, a cached ring slot or bf16 wire image is reused only if its
+    // version is current (in data parallel every rank writes the same update it caches).
+    size_t ver_off_ = 0;
+    std::vector<uint64_t> cache_ver_, host16_ver_, plan_ver_;
+    uint64_t* shm_versions() const { return reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(shm_) + ver_off_); }
+    uint64_t layer_version(int L) const;
+    void bump_version(int L);
+    void after_call(const Plan& plan);
     uint8_t* host16_ = nullptr;  // [n][wire16] bf16 W + fp32 b (bf16 inference wire)
     std::vector<uint8_t> host16_stale_;
     std::vector<int> relu_, frozen_;

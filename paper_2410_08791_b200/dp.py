@@ -47,3 +47,17 @@ def init_executor_dp(ex, dist, rank: int, world: int) -> None:
         return
     uid = broadcast_unique_id(dist, ex.nccl_unique_id() if rank == 0 else None)
     ex.dp_init(uid, rank, world)
+
+
+def share_host_master(ex, dist, local_rank: int, name: str) -> None:
+    """One pinned host master per node: local rank 0 moves its registered master
+    into the shared-memory segment `name`, then every other local rank attaches to it (and
+    drops its private copy). Collective over the node's ranks."""
+    if local_rank == 0:
+        ex.share_host_master(name, create=True)
+    if dist is not None:
+        dist.barrier()
+    if local_rank != 0:
+        ex.share_host_master(name, create=False)
+    if dist is not None:
+        dist.barrier()
