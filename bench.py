@@ -54,6 +54,8 @@ def parse():
                    help="sgd: the reference's update (default); adamw: fp32 m, v in pinned host "
                         "memory streamed with each backward layer, fused AdamW update")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--private-host-copies", action="store_true",
+                   help="N>1: one pinned master per rank instead of one per node (shared memory)")
     p.add_argument("--no-variants", action="store_true",
                    help="skip the in-run AdamW and tf32 variants of the same step ('variants')")
     p.add_argument("--sweep", default="", help="comma list of k:kp to report extra lines")
@@ -303,6 +305,8 @@ def config_of(a, world):
             "layers": a.layers, "d": a.d, "rows_per_gpu": a.rows, "global_batch": a.rows * world,
             "strategy": a.strategy, "k": a.k, "k_prime": a.kp, "transfer_mode": a.mode,
             "weights": "pinned host DRAM (fp32 master), streamed per step",
+            "host_master": ("one per rank" if world == 1 or a.private_host_copies
+                            else "one per node, shared by all ranks (sp_share_host_master)"),
             "optimizer": a.optimizer if a.optimizer == "sgd" else
             "adamw (fp32 m, v in pinned host DRAM, streamed per step)",
             "parallelism": f"dp{world}", "l2": "working set (weights+activations) >> 126 MB L2"}
@@ -343,10 +347,17 @@ def main():
             e.register_layer(i, Wl, bl)
         if opt == "adamw":
             e.set_optimizer(sp.OPT_ADAMW, 0.9, 0.999, 1e-8, 0.01)
+        if world > 1 and not a.private_host_copies:
+            # every rank of the node streams from one shared pinned master
+            tag = f"/sp_bench_{os.environ.get('MASTER_PORT', '0')}_{opt}_{numerics}"
+            err = dp.share_host_master(e, dist, local, tag)
+            if err:
+                host_copies_note.append(f"rank {rank}: private host copy ({err})")
         return e
 
-    ex = make_executor(strategy)
     from paper_2410_08791_b200 import dp
+    host_copies_note = []
+    ex = make_executor(strategy)
     if world > 1:
         dp.init_executor_dp(ex, dist, rank, world)  # per-layer NCCL all-reduce of dW/db
 
@@ -486,6 +497,7 @@ def main():
                          "method": "CUDA events around 20 back-to-back launches per shape on the "
                                    "launching stream, step-weighted by launches per step"},
             "variants": variants,
+            "host_copies_note": host_copies_note or None,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e, "unit": "samples/s",
                     "h2d_bytes_per_step": 2 * a.rows * a.d * 4, "d2h_bytes_per_step": 4},

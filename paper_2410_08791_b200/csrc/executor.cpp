@@ -277,9 +277,13 @@ void Executor::share_host_master(const char* name, bool create) {
     if (create) {
         shm_unlink(nm.c_str());  // a stale segment of a crashed run
         fd = shm_open(nm.c_str(), O_CREAT | O_EXCL | O_RDWR, 0600);
-        if (fd < 0 || ftruncate(fd, static_cast<off_t>(bytes)) != 0) {
+        // reserve the pages now: a tmpfs too small for the model fails here, not with SIGBUS
+        if (fd < 0 || ftruncate(fd, static_cast<off_t>(bytes)) != 0 ||
+            posix_fallocate(fd, 0, static_cast<off_t>(bytes)) != 0) {
             if (fd >= 0) close(fd);
-            throw Error(SP_ERR_INTERNAL, "share_host_master: cannot create shared segment " + nm);
+            shm_unlink(nm.c_str());
+            throw Error(SP_ERR_INTERNAL, "share_host_master: cannot create a " + std::to_string(bytes) +
+                                             "-byte shared segment " + nm + " (is /dev/shm large enough?)");
         }
     } else {
         fd = shm_open(nm.c_str(), O_RDWR, 0);

@@ -49,15 +49,24 @@ def init_executor_dp(ex, dist, rank: int, world: int) -> None:
     ex.dp_init(uid, rank, world)
 
 
-def share_host_master(ex, dist, local_rank: int, name: str) -> None:
+def share_host_master(ex, dist, local_rank: int, name: str) -> str | None:
     """One pinned host master per node: local rank 0 moves its registered master
     into the shared-memory segment `name`, then every other local rank attaches to it (and
-    drops its private copy). Collective over the node's ranks."""
+    drops its private copy). Collective over the node's ranks; the barriers are always
+    reached. Returns None on success, else the error (that rank keeps its private copy)."""
+    err = None
     if local_rank == 0:
-        ex.share_host_master(name, create=True)
+        try:
+            ex.share_host_master(name, create=True)
+        except Exception as e:  # e.g. /dev/shm too small: keep the private copy
+            err = str(e)
     if dist is not None:
         dist.barrier()
     if local_rank != 0:
-        ex.share_host_master(name, create=False)
+        try:
+            ex.share_host_master(name, create=False)
+        except Exception as e:
+            err = str(e)
     if dist is not None:
         dist.barrier()
+    return err

@@ -180,3 +180,45 @@ def test_sharded_streaming_step_equals_full_batch_step(world):
         assert np.array_equal(img, imgs[0])
         assert np.allclose(img, want, rtol=1e-5, atol=1e-6)
     assert all(r[2] for r in res)  # the step did change the host masters
+
+
+def _share_worker(rank, world, port, fail_rank, out):
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2410_08791_b200 import dp
+
+    class FakeExecutor:  # records the calls; the real one needs a GPU (test_gpu_shared_master)
+        calls = []
+
+        def share_host_master(self, name, create):
+            self.calls.append((name, create))
+            if rank == fail_rank:
+                raise RuntimeError("no room in /dev/shm")
+
+    ex = FakeExecutor()
+    err = dp.share_host_master(ex, dist, rank, "/seg")
+    dist.barrier()  # every rank got here: no barrier was skipped
+    out.put((rank, ex.calls, err))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("fail_rank", [-1, 0, 1])
+def test_share_host_master_is_collective_even_when_a_rank_fails(fail_rank):
+    """Local rank 0 creates the segment, the others attach after a barrier; a failing rank keeps
+    its private copy and reports why, and no rank is left waiting at a barrier."""
+    ctx = mp.get_context("spawn")
+    out = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_share_worker, args=(r, 2, port, fail_rank, out)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = dict((r, (calls, err)) for r, calls, err in (out.get(timeout=120) for _ in ps))
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res[0][0] == [("/seg", True)] and res[1][0] == [("/seg", False)]
+    for r in range(2):
+        assert (res[r][1] is not None) == (r == fail_rank)
