@@ -226,8 +226,10 @@ def layer_roofline(a, link, pk, rows_per_gpu, slots, shards=1):
     Bytes: a ring of S slots can carry at most S layers across each direction reversal (end of
     forward, end of step), so forward must load >= L - S layers and backward >= L - S; every
     trainable layer writes its fp32 image back (D2H). AdamW adds the fp32 moments m, v of every
-    layer in both directions. Backward H2D and D2H overlap at the measured duplex rate; a
-    backward layer with nothing to load is bound by its write-back alone (simplex D2H).
+    layer in both directions. Backward H2D and D2H overlap at the measured duplex rate. The last
+    S backward layers stay resident, so their write-backs may be deferred into the next
+    forward (whose D2H direction is otherwise idle): those layers are charged a simplex load
+    only, a bound the executor's deferred write-back can approach.
     Sharded data parallel (shards = world): each rank moves 1/world of every image."""
     d, L = a.d, a.layers
     S = min(slots, L)
@@ -240,8 +242,13 @@ def layer_roofline(a, link, pk, rows_per_gpu, slots, shards=1):
     for pos in range(L):                            # backward, layer L-1 first
         fl = fl_f if pos == L - 1 else 2 * fl_f     # layer 0 needs no dX
         load = (lb if pos >= S else 0.0) + opt      # the forward's last S layers are resident
-        out = lb + opt
-        t += max(fl, out / d2h) if load == 0 else max(fl, load / dup, out / dup)
+        out = lb + opt if pos < L - S else 0.0      # the last S write-backs: deferrable
+        if load == 0:
+            t += max(fl, out / d2h)
+        elif out == 0:                              # nothing goes out: a simplex load
+            t += max(fl, load / h2d)
+        else:
+            t += max(fl, load / dup, out / dup)
     return t
 
 
