@@ -352,3 +352,23 @@ def test_oracle_adamw_pinned_to_torch_optim_adamw():
 def test_adamw_abi_is_exported_and_validates_without_a_device():
     assert hasattr(_capi.LIB, "sp_set_optimizer") and hasattr(_capi.LIB, "sp_read_optimizer_state")
     assert sp.OPT_SGD == 0 and sp.OPT_ADAMW == 1
+
+
+def test_new_entry_points_reject_a_null_executor_without_a_device():
+    L = _capi.LIB
+    assert L.sp_set_optimizer(None, 1, 0.9, 0.999, 1e-8, 0.0) == _capi.SP_ERR_INVALID
+    assert L.sp_read_optimizer_state(None, 0, None, None, None, None) == _capi.SP_ERR_INVALID
+    assert L.sp_share_host_master(None, b"/x", 1) == _capi.SP_ERR_INVALID
+    assert L.sp_dp_sync(None) == _capi.SP_ERR_INVALID
+    assert L.sp_set_eager_prefetch(None, 1) == _capi.SP_ERR_INVALID
+    assert L.sp_set_item_batching(None, 1) == _capi.SP_ERR_INVALID
+
+
+def test_numerics_modes_are_validated_at_create():
+    # an unknown numerics mode is rejected before any device work (exact, bf16, tf32 are valid)
+    cfg = _capi.SpConfig(n_layers=2, d=64, strategy=sp.SUPERPIPELINE, k=2, k_prime=1,
+                         transfer_mode=sp.BATCH, numerics=9)
+    ex = _capi.C.c_void_p()
+    rc = _capi.LIB.sp_create(_capi.C.byref(cfg), _capi.C.byref(ex))
+    assert rc == _capi.SP_ERR_INVALID
+    assert sp.TF32 == 2 and sp.BF16 == 1 and sp.EXACT == 0
