@@ -1,5 +1,7 @@
+"""Narrower CTA-pair tiles against wave quantization: dX at 16384 x 1600 (and 65792 x 1280) with
+N = 256 / 192 / 160 tiles, warm back-to-back CUDA-event timing (rejected)."""
 import json, os, sys
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2410_08791_b200 import _capi
 L = _capi.LIB

@@ -1,5 +1,7 @@
+"""dX = (dz W^T) gated: warm back-to-back timing of the tcgen05 kernel variants against cuBLAS
+at the C2 / C4 layer shapes (CUDA events)."""
 import json, os, sys
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2410_08791_b200 import _capi
 LIB = _capi.LIB

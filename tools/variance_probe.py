@@ -1,5 +1,7 @@
+"""Run-to-run variance of the bench step on one box: repeated step timings (CUDA events) in fresh
+processes, to size the noise band A/B comparisons must beat."""
 import os, sys, time, json, subprocess
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import paper_2410_08791_b200 as sp
 from paper_2410_08791_b200 import _capi
