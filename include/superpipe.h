@@ -147,7 +147,11 @@ int sp_forward_device(sp_exec* ex, const void* x_dev, int64_t rows, int32_t n_it
                       void* y_dev);
 /* Replaces run_train_step (engine.hpp:48-50, engine.cpp:558-563): forward, MSE loss,
  * reverse backward with SGD (model.cpp:157-184) through the ring; the updated weights are
- * written back into the pinned host copy. x, target: host fp32 [rows][d]. */
+ * written back into the pinned host copy. x, target: host fp32 [rows][d]. The write-backs
+ * of the layers still resident in the ring at the end of the step run at the start of the
+ * next call (on the otherwise idle D2H engine); every host read through this API
+ * (sp_read_layer, sp_digest_train, sp_read_optimizer_state, sp_forward, sp_dp_sync, ...)
+ * completes them first, so callers always observe the post-step weights. */
 int sp_train_step(sp_exec* ex, const float* x, const float* target, int64_t rows, float lr,
                   float* loss);
 int sp_train_step_device(sp_exec* ex, const void* x_dev, const void* target_dev, int64_t rows,
@@ -225,7 +229,9 @@ int sp_dp_init2(sp_exec* ex, const uint8_t id[128], int32_t rank, int32_t world,
  * master holds only its own shard of every trained layer; sp_dp_sync all-gathers those shards
  * (NCCL over NVLink) so the host copy is whole again. Until then sp_read_layer,
  * sp_digest_train, bf16 sp_forward and sp_dp_init fail with SP_ERR_STATE instead of returning
- * a mix of current and stale shards. No-op when nothing is partial. */
+ * a mix of current and stale shards. No-op when nothing is partial. With a shared host master
+ * (sp_share_host_master) every rank's shard already landed in the one copy: the weights need
+ * only a barrier (AdamW moments, kept per rank, are still gathered). */
 int sp_dp_sync(sp_exec* ex);
 
 /* ---- host utilities ---------------------------------------------------------------- */
