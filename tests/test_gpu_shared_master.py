@@ -76,3 +76,30 @@ def test_another_process_streams_from_the_shared_copy(tmp_path):
         r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
         assert r.returncode == 0, r.stdout + r.stderr
         assert np.array_equal(np.load(tmp_path / "y.npy"), want)
+
+
+@pytest.mark.parametrize("shard", [True, False])
+def test_shared_master_through_the_dp_code_path(shard):
+    """A 1-rank communicator over a shared master: sharded (dp_sync is then a barrier for the
+    weights, the moments still gather) and all-reduce streaming both stay bit-identical to the
+    oracle in exact numerics, with AdamW."""
+    from test_gpu_adamw import HP, F, oracle_adamw
+    d = 16
+    model = sp.build_model(12, 5, d, 1)
+    batches = [(sp.make_input(12, 0, 6, d), sp.make_input(12, 1, 6, d))]
+    lr = F(0.01)
+    ref = oracle_adamw(model, batches, lr, 3, **HP)
+    name = f"/sp_test_{uuid.uuid4().hex[:12]}"
+    with sp.Executor(5, d, S(sp.SUPERPIPELINE, 2, 1)) as ex:
+        ex.register_model(model)
+        ex.share_host_master(name, create=True)
+        ex.dp_init(sp.Executor.nccl_unique_id(), 0, 1, shard_weights=shard)
+        ex.set_optimizer(sp.OPT_ADAMW, **HP)
+        losses = [np.float32(ex.train_step(*batches[0], lr)) for _ in range(3)]
+        ex.dp_sync()
+        m = ex.read_model(model)
+        st = [ex.read_optimizer_state(L) for L in range(5)]
+    assert [v.tobytes() for v in losses] == [v.tobytes() for v in ref[0]]
+    assert np.array_equal(m.W, ref[1]) and np.array_equal(m.b, ref[2])
+    assert np.array_equal(np.stack([s[0] for s in st]), ref[3])
+    assert np.array_equal(np.stack([s[2] for s in st]), ref[5])
