@@ -247,7 +247,7 @@ int64_t sp_describe_plan(const sp_config* cfg, int32_t n_items, int32_t train,
     sp::Plan plan = sp::build_plan(in, {});
     if ((flags & SP_PLAN_WRITEBACK) && in.train && plan.error.empty()) {
         // the executor's training write-back scheme, steady state: the second of two calls
-        in.wb_stages = std::max(1, std::min(plan.n_slots, 8));
+        in.wb_stages = std::max(1, std::min(plan.n_slots, 3));  // as the executor (ensure_stages)
         in.defer_writeback = !in.checkpointing;
         plan = sp::build_plan(in, {});
         in.pending_wb_layers = plan.deferred_layers;

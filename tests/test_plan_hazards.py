@@ -313,7 +313,7 @@ def test_writeback_scheme_edges_are_each_necessary(opt):
     """The staged / deferred write-back plan is race-free (above) and each of its new edges is
     load-bearing: dropping the waits on the previous call's write-backs, or on a stage's last
     reader, or one moved layer's own md deps, makes the checker fire."""
-    n, s = 16, sp.StrategyConfig(sp.SUPERPIPELINE, 4, 2)  # 10 staged write-backs > 6 stages
+    n, s = 16, sp.StrategyConfig(sp.SUPERPIPELINE, 4, 2)  # 10 staged write-backs > 3 stages
     txt = sp.describe_plan(n, 8, s, train=True, eager=True, writeback=True, optimizer_state=opt)
     head, ops = parse_plan(txt)
     pend = {o["index"] for o in ops if o["kind"] == "D2H" and o["pass"] == 0}

@@ -20,6 +20,8 @@ b = np.empty((d,), np.float32)
 for i in range(L):
     _capi.LIB.sp_build_layer(7, i, d, 0, 0, W.ctypes.data, b.ctypes.data)
     ex.register_layer(i, W, b)
+if os.environ.get("OPT") == "adamw":  # the AdamW variant of the step
+    ex.set_optimizer(sp.OPT_ADAMW, 0.9, 0.999, 1e-8, 0.01)
 x = torch.from_numpy(sp.make_input(7, 0, rows, d)).cuda()
 t = torch.from_numpy(sp.make_input(7, 1, rows, d)).cuda()
 for _ in range(3):
