@@ -1321,7 +1321,12 @@ float Executor::train_step(const float* x, const float* target, int64_t rows, fl
     }
     CallIO io{true, 1, rows, lr, fmt, device_io, x, target, nullptr};
     const auto t0 = std::chrono::steady_clock::now();
-    run_call(plan, io);
+    try {
+        run_call(plan, io);
+    } catch (...) {
+        if (adamw()) --step_t_;  // no update was applied for this step
+        throw;
+    }
     host_enqueue_ms_ = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     for (auto s : {s_h2d_, s_comp_, s_d2h_, s_upd_}) CUDA_OK(cudaStreamSynchronize(s));
     CUDA_OK(cudaGetLastError());
