@@ -79,6 +79,8 @@ Executor::Executor(const sp_config& cfg) : cfg_(cfg) {
     if (n_ < 1) throw Error(SP_ERR_INVALID, "build_model: n_layers must be >= 1");
     if (d_ < 1) throw Error(SP_ERR_INVALID, "build_model: d must be >= 1");
     if (const char* e = std::getenv("SP_WB")) staged_writeback_ = std::atoi(e) != 0;  // A/B only
+    if (const char* e = std::getenv("SP_POISON")) poison_ = std::atoi(e) != 0;        // debug only
+    if (const char* e = std::getenv("SP_FAULT_DROP_LOAD_EDGES")) drop_load_edges_ = std::atoi(e) != 0;
     const std::string v = validate_strategy(cfg.strategy, cfg.k, cfg.k_prime, n_);
     if (!v.empty()) throw Error(SP_ERR_INVALID, v);
     if (cfg.strategy == static_cast<int>(Strategy::CpuOnly))
@@ -823,6 +825,8 @@ void Executor::enqueue_op(const Plan& plan, int i, bool train, int n_items, int6
     auto wait = [&](int dep) {
         const Op& d = plan.ops[static_cast<size_t>(dep)];
         if (stream_of(d.kind) == st) return;
+        // fault injection for the poison test only: computes stop waiting for their loads
+        if (drop_load_edges_ && op.kind == OpKind::Compute && d.kind == OpKind::H2D) return;
         // A compute waits only for the move of its own layer in a multi-layer H2D job
         const int base = move_ev_base_[static_cast<size_t>(dep)];
         if (op.kind == OpKind::Compute && base >= 0) {
@@ -867,12 +871,16 @@ void Executor::enqueue_op(const Plan& plan, int i, bool train, int n_items, int6
                                               : reinterpret_cast<const uint8_t*>(
                                                     host32_ + static_cast<size_t>(L) * (dd + d_));
                     uint8_t* dst = wire ? slot_ptr(s) + off_w16_ : slot_ptr(s);
+                    // Debug (SP_POISON=1): NaN-fill the whole image first, so a compute that
+                    // reads the slot before this copy lands (a missing edge) produces NaNs.
+                    if (poison_) CUDA_OK(cudaMemsetAsync(dst, 0xFF, img, st));
                     if (hi > lo)
                         CUDA_OK(cudaMemcpyAsync(dst + lo, src + lo, hi - lo, cudaMemcpyHostToDevice, st));
                     h2d_bytes_ += hi - lo;
                     if (!wire) w16_layer_[s] = -1;
                 }
                 if (op.acts[j]) {
+                    if (poison_) CUDA_OK(cudaMemsetAsync(ba_[s], 0xFF, act_b, st));
                     CUDA_OK(cudaMemcpyAsync(ba_[s], host_act_ + static_cast<size_t>(L) * act_b, act_b,
                                             cudaMemcpyHostToDevice, st));
                     h2d_bytes_ += act_b;

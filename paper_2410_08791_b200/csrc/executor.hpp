@@ -155,6 +155,11 @@ private:
     int n_stages_ = 0;
     size_t stage_bytes_ = 0;
     bool staged_writeback_ = true;
+    // Debug (SP_POISON=1): every ring-slot / activation-reload copy is preceded by a NaN fill
+    // of its destination, so a read that overtakes the copy shows up as NaN (a dynamic check
+    // of the plan's edges next to the static one in tests/test_plan_hazards.py).
+    bool poison_ = false;
+    bool drop_load_edges_ = false;  // fault injection (SP_FAULT_DROP_LOAD_EDGES=1): tests only
     std::vector<int> pending_wb_layers_, pending_wb_slots_;
     std::vector<int> w16_layer_;  // bf16 training: layer whose bf16 copy is current per slot
     // streams / events

@@ -664,3 +664,62 @@ def test_graph_replayed_steps_with_deferred_writeback_equal_eager_steps(numerics
             for _ in range(6):
                 _, W, b = ORC.train_step(W, b, x, t, 0.02, frozen=model.frozen)
             assert np.array_equal(mg.W, W) and np.array_equal(mg.b, b), s
+
+
+@pytest.mark.parametrize("numerics", [sp.EXACT, sp.BF16])
+def test_poisoned_slots_change_nothing(numerics, monkeypatch):
+    """Dynamic check of the plan's edges (the static one is tests/test_plan_hazards.py): with
+    SP_POISON=1 every ring-slot and activation-reload copy is preceded by a NaN fill of its
+    destination, so any read that overtakes a copy would surface as NaN. Training (with and
+    without activation offload, AdamW, 1-rank sharded DP) and inference stay bitwise equal to
+    the unpoisoned runs."""
+    d = 16 if numerics == sp.EXACT else 128
+    rows = 6 if numerics == sp.EXACT else 256
+    model = sp.build_model(33, 7, d, 1)
+    x, t = sp.make_input(33, 0, rows, d), sp.make_input(33, 1, rows, d)
+
+    def run(poison):
+        monkeypatch.setenv("SP_POISON", "1" if poison else "0")
+        out = []
+        for s in (S(sp.SUPERPIPELINE, 3, 1), S(sp.SUPERPIPELINE, 2, 1, sp.SEQUENTIAL), S(sp.NAIVE, 2)):
+            for ckpt in (False, True):
+                with sp.Executor(7, d, s, numerics=numerics, checkpointing=ckpt) as ex:
+                    ex.register_model(model)
+                    out += [ex.train_step(x, t, 0.02) for _ in range(3)]
+                    ex.set_optimizer(sp.OPT_ADAMW, 0.9, 0.999, 1e-8, 0.0)
+                    out.append(ex.train_step(x, t, 0.01))
+                    out.append(ex.read_model(model).W.copy())
+                    out.append(ex.forward([x[:5], x[1:6]]))
+        with sp.Executor(7, d, S(sp.SUPERPIPELINE, 3, 1), numerics=numerics) as ex:
+            ex.register_model(model)
+            ex.dp_init(sp.Executor.nccl_unique_id(), 0, 1, shard_weights=True)
+            out += [ex.train_step(x, t, 0.02) for _ in range(2)]
+            ex.dp_sync()
+            out.append(ex.read_model(model).W.copy())
+        return out
+
+    a, b = run(False), run(True)
+    for u, v in zip(a, b):
+        assert np.array_equal(np.asarray(u), np.asarray(v))
+        assert np.isfinite(np.asarray(v)).all()
+
+
+def test_poison_detects_a_dropped_load_edge(monkeypatch):
+    """The detector itself: with the computes' waits on their weight loads removed (fault
+    injection), poisoned slots make the race visible as NaN / wrong outputs."""
+    d, n = 2048, 6  # 16 MB layer copies (~0.3 ms) against a few-microsecond 8-row compute
+    model = sp.build_model(35, n, d, 0)
+    x = sp.make_input(35, 0, 8, d)
+    monkeypatch.setenv("SP_POISON", "0")
+    with sp.Executor(n, d, S(sp.SUPERPIPELINE, 2, 1)) as ex:
+        ex.register_model(model)
+        want = ex.forward([x])[0]
+    monkeypatch.setenv("SP_POISON", "1")
+    monkeypatch.setenv("SP_FAULT_DROP_LOAD_EDGES", "1")
+    bad = 0
+    for _ in range(5):
+        with sp.Executor(n, d, S(sp.SUPERPIPELINE, 2, 1)) as ex:
+            ex.register_model(model)
+            y = ex.forward([x])[0]
+        bad += int(not np.array_equal(y, want))
+    assert bad > 0
