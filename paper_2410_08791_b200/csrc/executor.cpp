@@ -1039,11 +1039,9 @@ bool pinned_or_null(const void* p) {
 
 uint64_t Executor::call_signature(const Plan& plan, const CallIO& io) const {
     uint64_t h = 0xCBF29CE484222325ull;
-    auto mix = [&](uint64_t v) {
-        for (int b = 0; b < 8; ++b) {
-            h ^= (v >> (8 * b)) & 0xFF;
-            h *= 0x100000001B3ull;
-        }
+    auto mix = [&](uint64_t v) {  // word-wise multiply-xorshift (host time per call matters)
+        h = (h ^ v) * 0x9E3779B97F4A7C15ull;
+        h ^= h >> 29;
     };
     for (const Op& op : plan.ops) {
         mix(static_cast<uint64_t>(op.kind) | static_cast<uint64_t>(op.pass) << 8 |
@@ -1281,7 +1279,7 @@ void Executor::forward(const float* x, int64_t rows, int n_items, float* y, bool
     const auto t0 = std::chrono::steady_clock::now();
     run_call(plan, io);
     host_enqueue_ms_ = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-    for (auto s : {s_h2d_, s_comp_, s_d2h_, s_upd_}) CUDA_OK(cudaStreamSynchronize(s));
+    CUDA_OK(cudaStreamSynchronize(s_h2d_));  // every stream joined into s_h2d_ (enqueue_call)
     CUDA_OK(cudaGetLastError());
     after_call(plan);
     collect_stats(plan, n_items, false);
