@@ -218,19 +218,23 @@ def gemm_kernel_timing(torch, capi, a, reps=20):
     return res
 
 
-def layer_roofline(a, link, pk, rows_per_gpu, slots, shards=1):
-    """Lower bound on the step time of a k-window ring with `slots` HBM slots: per layer
-    max(FLOP at the sustained tensor peak, its host-link bytes at the measured pinned bandwidth),
-    summed over the step.
+def layer_roofline(a, link, pk, rows_per_gpu, slots, shards=1, ckpt=False):
+    """Ring roofline: a model of the step's lower time bound for a k-window ring of S slots,
+    from per-layer FLOPs at the sustained tensor peak and host-link bytes at the measured
+    pinned rates.
 
-    Bytes: a ring of S slots can carry at most S layers across each direction reversal (end of
-    forward, end of step), so forward must load >= L - S layers and backward >= L - S; every
-    trainable layer writes its fp32 image back (D2H). AdamW adds the fp32 moments m, v of every
-    layer in both directions. Backward H2D and D2H overlap at the measured duplex rate. The last
-    S backward layers stay resident, so their write-backs may be deferred into the next
-    forward (whose D2H direction is otherwise idle): those layers are charged a simplex load
-    only, a bound the executor's deferred write-back can approach.
-    Sharded data parallel (shards = world): each rank moves 1/world of every image."""
+    Bytes: S slots carry at most S layers across each direction reversal (end of forward, end
+    of step), so the forward loads >= L - S layers and the backward >= L - S; every trained
+    layer writes its fp32 image back. AdamW adds the moments m, v of every layer both ways.
+    Up to min(S, L - S) of the write-backs (the layers still resident at the end) can run in
+    the next forward, whose D2H engine is otherwise idle (no deferral with activation offload).
+      forward  = sum over layers of max(FLOP, load / H2D rate), and at least the forward's
+                 link bytes (loads + deferred write-backs) at the duplex rate;
+      backward = max(sum over layers of max(FLOP, load / duplex rate),
+                     its write-backs / D2H rate, its loads + write-backs / (2 x duplex rate)).
+    Per-layer serialisation is applied to the loads (a layer computes after its load) but not
+    to the write-backs, which overlap later layers' loads. Sharded data parallel (shards =
+    world): each rank moves 1/world of every image."""
     d, L = a.d, a.layers
     S = min(slots, L)
     lb = (d * d + d) * 4 / shards
@@ -238,18 +242,21 @@ def layer_roofline(a, link, pk, rows_per_gpu, slots, shards=1):
     peak = pk["bf16_tflops_sustained"] * 1e12
     h2d, d2h, dup = link["h2d_gbs"] * 1e9, link["d2h_gbs"] * 1e9, link["duplex_gbs_per_dir"] * 1e9
     fl_f = 2.0 * rows_per_gpu * d * d / peak
-    t = (L - S) * max(fl_f, lb / h2d) + S * fl_f  # forward: S layers still resident
-    for pos in range(L):                            # backward, layer L-1 first
-        fl = fl_f if pos == L - 1 else 2 * fl_f     # layer 0 needs no dX
-        load = (lb if pos >= S else 0.0) + opt      # the forward's last S layers are resident
-        out = lb + opt if pos < L - S else 0.0      # the last S write-backs: deferrable
-        if load == 0:
-            t += max(fl, out / d2h)
-        elif out == 0:                              # nothing goes out: a simplex load
-            t += max(fl, load / h2d)
-        else:
-            t += max(fl, load / dup, out / dup)
-    return t
+    deferred = 0 if ckpt else min(S, L - S)
+    out_layer = lb + opt
+    # forward: S layers still resident; the deferred write-backs share the link
+    fwd = (L - S) * max(fl_f, lb / h2d) + S * fl_f
+    fwd = max(fwd, ((L - S) * lb + deferred * out_layer) / (2 * dup), deferred * out_layer / d2h)
+    # backward: layer L-1 first; the forward's last S layers are resident (no weight load)
+    per_layer, loads = 0.0, 0.0
+    for pos in range(L):
+        fl = fl_f if pos == L - 1 else 2 * fl_f  # layer 0 needs no dX
+        load = (lb if pos >= S else 0.0) + opt
+        loads += load
+        per_layer += max(fl, load / dup) if load else fl
+    outs = (L - deferred) * out_layer
+    bwd = max(per_layer, outs / d2h, (loads + outs) / (2 * dup))
+    return fwd + bwd
 
 
 def cpu_baseline_ref(a, threads, rows_per_thread=2, layers_sample=6):

@@ -619,7 +619,11 @@ void Executor::compute_op(const Op& op, bool train, int64_t rows, int fmt) {
                 convert_f32_to_bf16(cur_x_, xL, static_cast<int64_t>(act), st);
                 ++kernels_;
             } else {
-                CUDA_OK(cudaMemcpyAsync(xL, cur_x_, act * 4, cudaMemcpyDeviceToDevice, st));
+                // an SM copy: a copy-engine D2D here would queue behind the ring's PCIe copies
+                void* dst[1] = {xL};
+                const void* src[1] = {cur_x_};
+                copy_regions(dst, src, 1, static_cast<int64_t>(act * 4), st);
+                ++kernels_;
             }
         }
         if (!tc_) {
@@ -746,10 +750,9 @@ void Executor::loss_op(int64_t rows) {
         CUDA_OK(cudaEventRecord(ev_loss_, s_comp_));
         CUDA_OK(cudaStreamWaitEvent(s_upd_, ev_loss_, 0));
         NCCL_OK(nccl().AllReduce(loss_dev_, loss_dev_, 1, ncclFloat, ncclSum, comm_, s_upd_));
-        CUDA_OK(cudaMemcpyAsync(loss_host_, loss_dev_, 4, cudaMemcpyDeviceToHost, s_upd_));
-    } else {
-        CUDA_OK(cudaMemcpyAsync(loss_host_, loss_dev_, 4, cudaMemcpyDeviceToHost, s_comp_));
     }
+    // (the 4-byte loss is read back after the final join, enqueue_call: a copy here would queue
+    // on the D2H copy engine behind the write-backs and stall this stream until they drain)
 }
 
 void Executor::update_op(const Op& op, float lr) {
@@ -1021,6 +1024,7 @@ void Executor::enqueue_call(const Plan& plan, const CallIO& io) {
         CUDA_OK(cudaStreamWaitEvent(s_h2d_, ev_join_[k], 0));
         ++k;
     }
+    if (io.train) CUDA_OK(cudaMemcpyAsync(loss_host_, loss_dev_, 4, cudaMemcpyDeviceToHost, s_h2d_));
     record_timing(ev_call1_, s_h2d_);  // all streams joined: the call's device makespan
 }
 

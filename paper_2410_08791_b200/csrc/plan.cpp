@@ -90,6 +90,7 @@ public:
         ckpt_ = in.train && in.checkpointing &&
                 in.strategy != static_cast<int>(Strategy::Standard);
         plan_.n_slots = n_slots;
+        plan_.first_writer.assign(static_cast<std::size_t>(n_slots), std::numeric_limits<int>::max());
         slots_.resize(static_cast<std::size_t>(n_slots));
         for (int s = 0; s < n_slots && s < static_cast<int>(initial.size()); ++s) {
             slots_[s].layer = initial[s].layer;
@@ -112,13 +113,10 @@ public:
 
     Plan run() {
         // The previous call's deferred write-backs: first on the D2H engine, reading slots
-        // that still hold those layers (only the writers of those slots wait for them), in
-        // layer order - the order in which the forward releases, and overwrites, their slots.
-        std::vector<std::pair<int, int>> pending;
-        for (std::size_t i = 0; i < in_.pending_wb_layers.size(); ++i)
-            pending.emplace_back(in_.pending_wb_layers[i], in_.pending_wb_slots[i]);
-        std::sort(pending.begin(), pending.end());
-        for (const auto& [L, s] : pending) {
+        // that still hold those layers (only the writers of those slots wait for them), in the
+        // order given - build_plan passes them sorted by when each slot is first overwritten.
+        for (std::size_t i = 0; i < in_.pending_wb_layers.size(); ++i) {
+            const int L = in_.pending_wb_layers[i], s = in_.pending_wb_slots[i];
             if (s < 0 || s >= static_cast<int>(slots_.size())) continue;
             Op wb;
             wb.kind = OpKind::D2H;
@@ -160,16 +158,29 @@ public:
     }
 
     // Write-backs of layers that end the call resident (and valid) in their slot move to the
-    // next call; their Update skips the staging copy.
+    // next call; their Update skips the staging copy. The next call's forward has its D2H
+    // engine idle for about one layer copy per layer it loads (n - S of them), so at most that
+    // many write-backs are deferred - those whose slots the next forward recycles first (the
+    // lowest layers); the rest stay in this backward. (Standard, S = n: none.)
     void defer_final_writebacks() {
+        std::vector<std::pair<int, std::size_t>> cand;  // (layer, D2H op)
         for (std::size_t i = 0; i < plan_.ops.size(); ++i) {
-            Op& op = plan_.ops[i];
+            const Op& op = plan_.ops[i];
             if (op.kind != OpKind::D2H || op.pass != 1) continue;
             const int L = op.layers[0], s = op.slots[0];
-            if (!plan_.final_slots[static_cast<std::size_t>(s)].valid ||
-                plan_.final_slots[static_cast<std::size_t>(s)].layer != L)
-                continue;
+            if (plan_.final_slots[static_cast<std::size_t>(s)].valid &&
+                plan_.final_slots[static_cast<std::size_t>(s)].layer == L)
+                cand.emplace_back(L, i);
+        }
+        std::sort(cand.begin(), cand.end());
+        const std::size_t budget = static_cast<std::size_t>(std::max(0, n_ - plan_.n_slots));
+        if (cand.size() > budget) cand.resize(budget);
+        std::vector<uint8_t> deferred(plan_.ops.size(), 0);
+        for (const auto& c : cand) {
+            Op& op = plan_.ops[c.second];
+            const int L = op.layers[0], s = op.slots[0];
             op.deferred = true;
+            deferred[c.second] = 1;
             for (int dep : op.deps)
                 if (plan_.ops[static_cast<std::size_t>(dep)].kind == OpKind::Update)
                     plan_.ops[static_cast<std::size_t>(dep)].stage = -1;
@@ -177,6 +188,14 @@ public:
             plan_.deferred_layers.push_back(L);
             plan_.deferred_slots.push_back(s);
         }
+        // A deferred write-back reads no stage, and its (empty) op sits behind the next call's
+        // D2H queue: later updates reusing that stage need not wait for it (they are ordered
+        // after this layer's update, which waited for the stage's previous reader).
+        for (Op& op : plan_.ops)
+            if (op.kind == OpKind::Update)
+                op.deps.erase(std::remove_if(op.deps.begin(), op.deps.end(),
+                                             [&](int d) { return deferred[static_cast<std::size_t>(d)] != 0; }),
+                              op.deps.end());
     }
 
     // The first op that overwrites slot s after a pending write-back of its old content waits
@@ -185,6 +204,7 @@ public:
         if (slots_[s].wb_op < 0) return;
         deps.push_back(slots_[s].wb_op);
         slots_[s].wb_op = -1;
+        plan_.first_writer[static_cast<std::size_t>(s)] = static_cast<int>(plan_.ops.size());  // op about to be pushed
     }
 
 private:
@@ -587,6 +607,29 @@ Plan build_plan(const PlanInput& in, const std::vector<SlotCache>& initial) {
     for (;;) {
         Builder b(in, initial, S);
         Plan p = b.run();
+        if (!p.oom && in.pending_wb_layers.size() > 1) {
+            // Issue the previous call's write-backs in the order their slots are first
+            // overwritten: ascending layers for slots the forward recycles, backward order for
+            // layers that stay resident (Standard, or a ring wider than the model), so no
+            // writer queues behind write-backs it does not need.
+            std::vector<std::size_t> idx(in.pending_wb_layers.size());
+            for (std::size_t i = 0; i < idx.size(); ++i) idx[i] = i;
+            auto when = [&](std::size_t i) {
+                const int s = in.pending_wb_slots[i];
+                return s >= 0 && s < static_cast<int>(p.first_writer.size()) ? p.first_writer[static_cast<std::size_t>(s)]
+                                                                            : std::numeric_limits<int>::max();
+            };
+            std::stable_sort(idx.begin(), idx.end(), [&](std::size_t a, std::size_t b2) {
+                return when(a) != when(b2) ? when(a) < when(b2) : in.pending_wb_layers[a] < in.pending_wb_layers[b2];
+            });
+            PlanInput sorted = in;
+            for (std::size_t i = 0; i < idx.size(); ++i) {
+                sorted.pending_wb_layers[i] = in.pending_wb_layers[idx[i]];
+                sorted.pending_wb_slots[i] = in.pending_wb_slots[idx[i]];
+            }
+            Builder b2(sorted, initial, S);
+            return b2.run();
+        }
         if (!p.oom || S <= smin) return p;
         --S;
     }

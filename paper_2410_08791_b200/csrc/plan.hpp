@@ -118,6 +118,7 @@ struct Plan {
     LedgerPeaks ledger;
     std::vector<SlotCache> final_slots;
     std::vector<int> deferred_layers, deferred_slots;  // write-backs left for the next call
+    std::vector<int> first_writer;  // per slot: the op that waits for its pending write-back
     uint64_t n_h2d_jobs = 0, n_d2h_jobs = 0, n_evictions = 0;
     uint64_t h2d_weight_layers = 0, h2d_act_layers = 0, d2h_weight_layers = 0,
              d2h_act_layers = 0;

@@ -17,7 +17,8 @@ from paper_2410_08791_b200 import _capi  # noqa: E402
 args = sys.argv[1:]
 L, d, rows, k, kp = (int(v) for v in (args[:5] if len(args) >= 5 else (48, 1600, 16384, 4, 2)))
 opt = args[5] if len(args) > 5 else "sgd"
-ex = sp.Executor(L, d, sp.StrategyConfig(sp.SUPERPIPELINE, k, kp), numerics=sp.BF16, trace=True)
+strat = sp.StrategyConfig(sp.STANDARD) if k == 0 else sp.StrategyConfig(sp.SUPERPIPELINE, k, kp)  # k=0: Standard
+ex = sp.Executor(L, d, strat, numerics=sp.BF16, trace=True)
 W = np.empty((d, d), np.float32)
 b = np.empty((d,), np.float32)
 for i in range(L):
@@ -91,6 +92,6 @@ if os.environ.get("SEGMENT"):
     lo, hi = (float(v) for v in os.environ["SEGMENT"].split(","))
     print("segment:")
     for e in sorted(tr, key=lambda e: e["t_start"]):
-        if lo <= e["t_start"] <= hi and e["kind"] != "Stall":
+        if lo <= e["t_start"] <= hi and (e["kind"] != "Stall" or os.environ.get("STALLS")):
             print(f"  {e['kind']:8s} L={e['layer']:3d} bwd={int(e['backward'])} [{e['t_start']:8.3f} {e['t_end']:8.3f}] "
                   f"dur={e['t_end'] - e['t_start']:.3f}")
