@@ -511,6 +511,22 @@ Plan Executor::make_plan(bool train, int n_items, int64_t rows, int fmt) {
     // a master shared outside data parallel must be complete when the call returns)
     const bool foreign_writers = shm_ && !comm_;
     in.defer_writeback = train && staged_writeback_ && !cfg_.checkpointing && !foreign_writers;
+    if (in.defer_writeback) {
+        // Write-backs the next forward absorbs: one per layer it loads (n - S; measured best for
+        // rings up to half the model), or, when the forward is mostly compute on resident layers
+        // (Standard, wide rings), what fits in its compute time beyond its loads - from a rough
+        // model: tensor rate ~1 PFLOP/s bf16, half for tf32, ~20 TFLOP/s for the exact SIMT
+        // kernels; ~50 GB/s over the host link. (Measured at C2: Standard 13.0 -> 12.2 ms.)
+        const int S = std::min(n_slots_, n_);
+        const double rate = tf32_ ? 0.5e15 : bf16_ ? 1.0e15 : 2.0e13;
+        const double t_c = 2.0 * static_cast<double>(rows) * d_ * d_ / rate;
+        const double t_load = static_cast<double>(layer_bytes()) / 5.0e10;
+        const double t_wb = t_load * (adamw() ? 3.0 : 1.0);
+        const double spare = n_ * t_c - (n_ - S) * t_load;  // forward compute beyond its loads
+        const int fit = spare > 0 ? static_cast<int>(spare / t_wb) : 0;
+        in.defer_budget = std::min(S, std::max(n_ - S, fit));
+        if (const char* e = std::getenv("SP_DEFER_BUDGET")) in.defer_budget = std::atoi(e);  // A/B only
+    }
     if (shm_) {
         for (int L = 0; L < n_; ++L) plan_ver_[static_cast<size_t>(L)] = layer_version(L);
         if (foreign_writers)

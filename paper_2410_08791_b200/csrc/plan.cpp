@@ -158,10 +158,10 @@ public:
     }
 
     // Write-backs of layers that end the call resident (and valid) in their slot move to the
-    // next call; their Update skips the staging copy. The next call's forward has its D2H
-    // engine idle for about one layer copy per layer it loads (n - S of them), so at most that
-    // many write-backs are deferred - those whose slots the next forward recycles first (the
-    // lowest layers); the rest stay in this backward. (Standard, S = n: none.)
+    // next call; their Update skips the staging copy. Only as many as the next forward's idle
+    // D2H time absorbs (in_.defer_budget, estimated by the executor from the layer's compute and
+    // copy times) are deferred - the lowest layers, whose slots the next forward recycles first
+    // and which the next backward rewrites last; the rest stay in this backward.
     void defer_final_writebacks() {
         std::vector<std::pair<int, std::size_t>> cand;  // (layer, D2H op)
         for (std::size_t i = 0; i < plan_.ops.size(); ++i) {
@@ -173,7 +173,8 @@ public:
                 cand.emplace_back(L, i);
         }
         std::sort(cand.begin(), cand.end());
-        const std::size_t budget = static_cast<std::size_t>(std::max(0, n_ - plan_.n_slots));
+        const int b = in_.defer_budget >= 0 ? in_.defer_budget : n_ - plan_.n_slots;
+        const std::size_t budget = static_cast<std::size_t>(std::max(0, std::min(b, plan_.n_slots)));
         if (cand.size() > budget) cand.resize(budget);
         std::vector<uint8_t> deferred(plan_.ops.size(), 0);
         for (const auto& c : cand) {

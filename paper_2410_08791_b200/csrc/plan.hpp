@@ -72,6 +72,9 @@ struct PlanInput {
     // pending_wb_* and gets one D2H per layer at its start, which every later writer of that
     // slot depends on. The caller flushes pending write-backs before the host copy is read.
     bool defer_writeback = false;
+    // How many write-backs the next forward can absorb (its idle D2H time / one write-back);
+    // -1 = n_layers - S (one per layer the forward loads). At most S are ever deferred.
+    int defer_budget = -1;
     std::vector<int> pending_wb_layers, pending_wb_slots;
     std::vector<uint8_t> frozen;  // per layer
     uint64_t layer_bytes = 0;     // reference ledger units: (d*d + d) * 4

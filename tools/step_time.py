@@ -14,7 +14,8 @@ import paper_2410_08791_b200 as sp  # noqa: E402
 from paper_2410_08791_b200 import _capi  # noqa: E402
 
 L, d, rows, k, kp, steps = (int(v) for v in (sys.argv[1:7] if len(sys.argv) > 6 else (48, 1600, 16384, 4, 2, 10)))
-ex = sp.Executor(L, d, sp.StrategyConfig(sp.SUPERPIPELINE, k, kp), numerics=sp.BF16, trace=0)
+strat = sp.StrategyConfig(sp.STANDARD) if k == 0 else sp.StrategyConfig(sp.SUPERPIPELINE, k, kp)  # k=0: Standard
+ex = sp.Executor(L, d, strat, numerics=sp.BF16, trace=0)
 W = np.empty((d, d), np.float32)
 b = np.empty((d,), np.float32)
 for i in range(L):
