@@ -253,3 +253,26 @@ def test_adamw_edge_windows_and_digest_after_deferred_writeback(n, strats):
         assert [x.tobytes() for x in losses] == [x.tobytes() for x in ref[0]], s
         assert np.array_equal(m.W, ref[1]) and np.array_equal(m.b, ref[2]), s
         assert digest == ORC.digest_train(ref[0][-1], ref[1], ref[2]), s
+
+
+@pytest.mark.parametrize("numerics", [sp.BF16, sp.TF32])
+def test_adamw_at_a_large_layer_is_window_invariant(numerics):
+    """d = 4096 (a 64 MB fp32 layer, 192 MB with its moments), where the split-K dW, the
+    write-back stages and the 3-region staging copy run at their largest: every window gives the
+    same bits, and the moments are finite and nonzero."""
+    n, d, rows = 5, 4096, 512
+    model = sp.build_model(37, n, d, 0)
+    x, t = sp.make_input(37, 0, rows, d), sp.make_input(37, 1, rows, d)
+    outs = []
+    for s in (S(sp.SUPERPIPELINE, 2, 1), S(sp.SUPERPIPELINE, 3, 1), S(sp.STANDARD)):
+        with sp.Executor(n, d, s, numerics=numerics) as ex:
+            ex.register_model(model)
+            ex.set_optimizer(sp.OPT_ADAMW, **HP)
+            losses = [ex.train_step(x, t, F(0.001)) for _ in range(2)]
+            m = ex.read_model(model)
+            mW, mb, vW, vb = ex.read_optimizer_state(n - 1)
+        outs.append((losses, m.W, m.b, mW, vW))
+    for o in outs[1:]:
+        assert o[0] == outs[0][0]
+        assert all(np.array_equal(u, v) for u, v in zip(o[1:], outs[0][1:]))
+    assert np.isfinite(outs[0][3]).all() and np.abs(outs[0][3]).max() > 0 and (outs[0][4] >= 0).all()
