@@ -1142,6 +1142,11 @@ bool use_tma_epilogue(const GemmProblem& g, int splits) {
 // for the activation GEMMs they were neutral warm and, being scheduled last, re-read every A
 // panel after it has left L2 (82 vs 58 MB DRAM reads per forward launch at 16384 x 1600).
 bool narrow_tiles(int epi_base, int bn, int last_cols) {
+    static const int forced = [] {  // SP_NARROW=1: every epilogue (A/B measurement only)
+        const char* e = std::getenv("SP_NARROW");
+        return e ? std::atoi(e) : -1;
+    }();
+    if (forced == 1) return epi_base != EPI_SGD_F32 && bn == 256 && last_cols <= 128;
     return epi_base == EPI_F32 && bn == 256 && last_cols <= 128;
 }
 
