@@ -372,3 +372,47 @@ def test_numerics_modes_are_validated_at_create():
     rc = _capi.LIB.sp_create(_capi.C.byref(cfg), _capi.C.byref(ex))
     assert rc == _capi.SP_ERR_INVALID
     assert sp.TF32 == 2 and sp.BF16 == 1 and sp.EXACT == 0
+
+
+def test_c_abi_compiles_links_and_runs_from_plain_c(tmp_path):
+    """The boundary is consumable from C99 (what cgo / JNI / N-API stubs bind): the headers
+    compile as C, the library links, and the host-only entry points answer without a device."""
+    import shutil
+    import subprocess
+    if not shutil.which("gcc"):
+        pytest.skip("no gcc")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    src = tmp_path / "t.c"
+    src.write_text(r'''
+#include <stdio.h>
+#include <string.h>
+#include "superpipe.h"
+#include "superpipe_debug.h"
+int main(void) {
+    sp_config c;
+    memset(&c, 0, sizeof c);
+    c.n_layers = 8; c.d = 16; c.strategy = SP_SUPERPIPELINE; c.k = 4; c.k_prime = 2;
+    c.transfer_mode = SP_BATCH; c.numerics = SP_NUMERICS_TF32;
+    char buf[1 << 14];
+    if (sp_abi_version() != SP_ABI_VERSION) return 1;
+    if (sp_validate_strategy(SP_SUPERPIPELINE, 4, 2, 8) != SP_OK) return 2;
+    if (sp_validate_strategy(SP_SUPERPIPELINE, 2, 2, 8) != SP_ERR_INVALID) return 3;
+    if (sp_peak_weight_residency(SP_SUPERPIPELINE, 4, 2, 8, 1088) != 6 * 1088) return 4;
+    if (sp_describe_plan(&c, 4, 0, NULL, SP_PLAN_EAGER, buf, sizeof buf) <= 0) return 5;
+    if (strncmp(buf, "slots=6", 7) != 0) return 6;
+    sp_exec* ex = NULL;
+    if (sp_create(&c, &ex) != SP_ERR_INVALID) return 7;  /* tf32 needs d % 64 == 0 */
+    c.numerics = SP_NUMERICS_EXACT;
+    if (sp_create(&c, &ex) != SP_ERR_CUDA) return 8;     /* no device here: loud, no fallback */
+    puts("ok");
+    return 0;
+}
+''')
+    exe = tmp_path / "t"
+    lib = os.path.join(root, "paper_2410_08791_b200")
+    r = subprocess.run(["gcc", "-std=c99", "-Wall", "-I", os.path.join(root, "include"), str(src),
+                        "-L", lib, "-lsuperpipe", f"-Wl,-rpath,{lib}", "-o", str(exe)],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=60)
+    assert r.returncode == 0 and r.stdout.strip() == "ok", (r.returncode, r.stdout, r.stderr)
