@@ -50,11 +50,32 @@ def build_weights(n, d, threads=16):
     return out
 
 
+def cpu_reference_rate(d, rows_total, n_layers, sample_rows=64):
+    """the reference's reference_forward (oracle/_ref, built from its sources) on one
+    host core, timed on ONE d-wide layer over `sample_rows` rows and extrapolated linearly in
+    rows and layers (every block costs the same). Returns (rows/s, description)."""
+    import time
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from pyoracle import Reference
+    ref = Reference()
+    W, b, _ = ref.build_model(7, 1, d)
+    rows = min(sample_rows, rows_total)
+    x = ref.make_input(7, 0, rows, d)
+    t0 = time.perf_counter()
+    ref.forward(W, b, x)
+    dt = time.perf_counter() - t0
+    full = dt * (rows_total / rows) * n_layers
+    return rows_total / full, (f"reference_forward, 1 core, 1 of {n_layers} layers x {rows} of {rows_total} rows "
+                               f"({dt:.2f} s), extrapolated linearly")
+
+
 def main():
     p = argparse.ArgumentParser()
     p.add_argument("configs", nargs="*", default=["c1", "c1b", "c3"])
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--mode", default="batch", choices=["batch", "sequential"])
+    p.add_argument("--cpu-baseline", action="store_true",
+                   help="also time the reference's CPU forward per config (one layer, extrapolated)")
     p.add_argument("--reference-prefetch", action="store_true",
                    help="copies wait for the reference policy's trigger compute (no eager prefetch)")
     a = p.parse_args()
@@ -98,6 +119,11 @@ def main():
                 "full_residency_bf16_gb": n * wire / 1e9,
                 "h2d_gb_per_call": st["h2d_bytes"] / 1e9}), flush=True)
             ex.close()
+        if a.cpu_baseline:
+            rate, how = cpu_reference_rate(d, items * rows, n)
+            print(json.dumps({"config": name, "cpu_baseline": {"value": rate, "unit": "samples/s",
+                                                               "cores": 1, "kind": "reference",
+                                                               "sample": how}}), flush=True)
 
 
 if __name__ == "__main__":

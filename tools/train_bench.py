@@ -52,11 +52,31 @@ def roofline_ms(n, d, rows, ckpt, link, peak, slots):
     return 1e3 * t
 
 
+def cpu_reference_rate(d, rows_total, n_layers, sample_rows=64):
+    """the reference's reference_train_step (oracle/_ref) on one host core, timed on a
+    one-layer model over `sample_rows` rows, extrapolated linearly in rows and layers."""
+    import time
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from pyoracle import Reference
+    ref = Reference()
+    W, b, _ = ref.build_model(7, 1, d)
+    rows = min(sample_rows, rows_total)
+    x, t = ref.make_input(7, 0, rows, d), ref.make_input(7, 1, rows, d)
+    t0 = time.perf_counter()
+    ref.train_step(W, b, x, t, 0.01)
+    dt = time.perf_counter() - t0
+    full = dt * (rows_total / rows) * n_layers
+    return rows_total / full, (f"reference_train_step, 1 core, 1 of {n_layers} layers x {rows} of "
+                               f"{rows_total} rows ({dt:.2f} s), extrapolated linearly")
+
+
 def main():
     p = argparse.ArgumentParser()
     p.add_argument("configs", nargs="*", default=["c4"])
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--lr", type=float, default=0.01)
+    p.add_argument("--cpu-baseline", action="store_true",
+                   help="also time the reference's CPU train step per config (one layer, extrapolated)")
     a = p.parse_args()
     peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["bf16_tflops_sustained"] * 1e12
     link = bench.measure_link(torch, chunk=(1280 * 1280 + 1280) * 4)
@@ -96,6 +116,10 @@ def main():
                     "hbm_reserved_gb": st["hbm_reserved_bytes"] / 1e9,
                     "graph_replays": st["graph_replays"]}), flush=True)
                 ex.close()
+        if a.cpu_baseline:
+            rate, how = cpu_reference_rate(d, rows, n)
+            print(json.dumps({"config": name, "cpu_baseline": {"value": rate, "unit": "samples/s", "cores": 1,
+                                                               "kind": "reference", "sample": how}}), flush=True)
 
 
 if __name__ == "__main__":
