@@ -33,3 +33,32 @@ def test_reference_arm_other_ranks_exit_quietly():
     r = _run({"RANK": "1", "WORLD_SIZE": "2", "LOCAL_RANK": "1"})
     assert r.returncode == 0, r.stderr
     assert not [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+
+
+import pytest  # noqa: E402
+
+
+@pytest.mark.gpu
+def test_gpu_bench_line_has_every_contract_key():
+    """bench.py on a small model (N = 1): one JSON line carrying the driver contract's keys,
+    the roofline and e2e objects, our kernel launch count and the clock sample."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--layers", "6", "--d", "256",
+                        "--rows", "1024", "--steps", "3", "--warmup", "3"],
+                       capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+              "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e",
+              "gpu_launches", "clocks", "north_star", "variants", "peak_hbm_gb"):
+        assert k in d, k
+    assert d["value"] > 0 and d["n_gpus"] == 1 and d["gpu_launches"] > 0
+    for k in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
+        assert k in d["roofline"], k
+    for k in ("value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step"):
+        assert k in d["e2e"], k
+    assert d["e2e"]["h2d_bytes_per_step"] == 2 * 1024 * 256 * 4
+    assert d["cpu_baseline"]["kind"] == "reference" and d["cpu_baseline"]["cores"] == 1
+    assert set(d["variants"]) == {"adamw", "tf32"}
+    assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
