@@ -326,11 +326,31 @@ def config_of(a, world):
             "parallelism": f"dp{world}", "l2": "working set (weights+activations) >> 126 MB L2"}
 
 
+def spawn_ranks(a):
+    """`--gpus N` without a torchrun environment: re-launch this command as N ranks (one
+    process per GPU, 127.0.0.1 rendezvous) and return their exit code. Only rank 0 prints."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    if os.environ.get("SP_BENCH_DRY_SPAWN"):  # CPU test: show the launch, do not run it
+        print(json.dumps({"spawn": cmd}), flush=True)
+        return 0
+    return subprocess.call(cmd)
+
+
 def main():
     a = parse()
+    if a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(a))
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
+    if world != a.gpus:
+        print(json.dumps({"error": f"--gpus {a.gpus} but WORLD_SIZE={world}"}), flush=True)
+        sys.exit(2)
     if a.impl == "reference":
         run_reference(a, rank, world)
         return

@@ -9,6 +9,8 @@
 
 #include <stdint.h>
 
+#include "superpipe.h"
+
 #ifdef __cplusplus
 extern "C" {
 #endif
@@ -61,6 +63,26 @@ int32_t sp_debug_dw_choice(int32_t d, int64_t rows, int32_t fused_ok, int32_t* c
                            int32_t* block_n);
 /* Split count the GEMM will use for a given K and requested splits. */
 int32_t sp_debug_effective_splits(int32_t K, int32_t splits);
+
+/* Debug and A/B measurement knobs (defaults = the product behaviour; nothing on the product
+ * path sets them). Executor keys (ex != NULL): "staged_writeback" (0: write back straight from
+ * the slot), "wb_stages" (staging buffer count, default 3), "defer_budget" (-1 = the executor's
+ * rule), "per_move" / "move_events" (0: batched H2D jobs wait up front / no per-move completion
+ * events), "graphs" (0: no CUDA-graph capture), "poison" (1: NaN-fill every slot / activation
+ * reload destination before its copy), "drop_load_edges" (fault injection: computes stop
+ * waiting for their loads - tests only). Process-wide GEMM keys (ex may be NULL): "epi_mode"
+ * (0 auto, 1 direct stores, 2 TMA-staged stores), "narrow" (1: half-width ragged last tiles for
+ * every epilogue). Returns SP_OK or SP_ERR_INVALID for an unknown key. */
+struct sp_exec;
+int sp_debug_set(struct sp_exec* ex, const char* key, int32_t value);
+
+/* Two consecutive training plans exactly as the executor builds them (eager prefetch, staged
+ * and deferred write-back, the largest deferral budget): call 1 with act_bytes1, then call 2 with act_bytes2 and call 1's
+ * deferred write-backs pending. Text: "DEFERRED <layers>", then "FLUSHED <layers>" when call 2's
+ * capacity-shrunk ring could not keep them (the executor completes them before planning), then
+ * call 2's plan listing. Returns the needed length. Host-only. */
+int64_t sp_debug_plan_two_calls(const sp_config* cfg, uint64_t act_bytes1, uint64_t act_bytes2,
+                                char* buf, int64_t cap);
 
 #ifdef __cplusplus
 }

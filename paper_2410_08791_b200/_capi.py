@@ -74,6 +74,7 @@ EXPORTS = [
     "sp_debug_gemm_tf32_async",
     "sp_debug_effective_splits",
     "sp_debug_shard_range", "sp_debug_dw_splits", "sp_debug_dw_choice",
+    "sp_debug_plan_two_calls", "sp_debug_set",
 ]
 
 
@@ -129,6 +130,8 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "sp_debug_dw_splits": ([i32, i64], i32),
         "sp_debug_dw_choice": ([i32, i64, i32, C.POINTER(i32), C.POINTER(i32)], i32),
         "sp_debug_shard_range": ([u64, i32, i32, C.POINTER(u64), C.POINTER(u64)], u64),
+        "sp_debug_plan_two_calls": ([C.POINTER(SpConfig), u64, u64, C.c_char_p, i64], i64),
+        "sp_debug_set": ([ex, C.c_char_p, i32], C.c_int),
     }
     for name, (args, res) in sig.items():
         if os.environ.get("SUPERPIPE_LIB") and not hasattr(lib, name):

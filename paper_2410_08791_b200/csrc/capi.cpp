@@ -162,8 +162,10 @@ int sp_read_optimizer_state(sp_exec* ex, int32_t index, float* mW, float* mb, fl
 
 int sp_digest_train(const sp_exec* ex, float loss, char out[17]) {
     if (!ex || !out) return SP_ERR_INVALID;
-    ex->impl->digest_train(loss, out);
-    return SP_OK;
+    // digest_train flushes pending write-backs and refuses a shard-only master: both throw,
+    // and exceptions never cross the ABI
+    sp_exec* mex = const_cast<sp_exec*>(ex);
+    return guarded(mex, [&] { mex->impl->digest_train(loss, out); });
 }
 
 int sp_get_stats(const sp_exec* ex, sp_stats* out) {
@@ -443,6 +445,70 @@ extern "C" int32_t sp_debug_dw_choice(int32_t d, int64_t rows, int32_t fused_ok,
     return c.splits;
 }
 
+namespace sp {
+void set_gemm_debug(const char* key, int value, bool* known);
+}
+
+extern "C" int sp_debug_set(sp_exec* ex, const char* key, int32_t value) {
+    if (!key) return SP_ERR_INVALID;
+    bool known = false;
+    sp::set_gemm_debug(key, value, &known);
+    if (known) return SP_OK;
+    if (!ex) return SP_ERR_INVALID;
+    return guarded(ex, [&] { ex->impl->set_debug(key, value); });
+}
+
 extern "C" int32_t sp_debug_effective_splits(int32_t K, int32_t splits) {
     return sp::effective_splits(K, splits);
+}
+
+// Two consecutive training plans as the executor makes them (make_plan): call 1 at act_bytes1,
+// call 2 at act_bytes2 with call 1's deferred write-backs pending. When the second ring would
+// shrink below a pending slot the executor flushes them first; the text then starts "FLUSHED".
+extern "C" int64_t sp_debug_plan_two_calls(const sp_config* cfg, uint64_t act_bytes1,
+                                           uint64_t act_bytes2, char* buf, int64_t cap) {
+    if (!cfg) return -1;
+    sp::PlanInput in;
+    in.n_layers = cfg->n_layers;
+    in.strategy = cfg->strategy;
+    in.k = cfg->k;
+    in.k_prime = cfg->k_prime;
+    in.transfer_mode = cfg->transfer_mode;
+    in.train = true;
+    in.layer_bytes = (static_cast<uint64_t>(cfg->d) * cfg->d + cfg->d) * 4;
+    in.capacity = cfg->capacity_bytes;
+    in.eager = true;
+    in.wb_stages = 3;
+    in.defer_writeback = true;
+    in.defer_budget = in.n_layers;  // the most the executor ever defers (clipped to S)
+    in.act_bytes = act_bytes1;
+    sp::Plan p1 = sp::build_plan(in, {});
+    std::string text;
+    if (!p1.error.empty()) {
+        text = "ERROR " + p1.error + "\n";
+    } else {
+        in.act_bytes = act_bytes2;
+        in.pending_wb_layers = p1.deferred_layers;
+        in.pending_wb_slots = p1.deferred_slots;
+        sp::Plan p2 = sp::build_plan(in, p1.final_slots);
+        std::string head;
+        if (p2.pending_conflict) {
+            head = "FLUSHED";
+            for (int L : p1.deferred_layers) head += " " + std::to_string(L);
+            head += "\n";
+            in.pending_wb_layers.clear();
+            in.pending_wb_slots.clear();
+            p2 = sp::build_plan(in, p1.final_slots);
+        }
+        std::string deferred = "DEFERRED";
+        for (int L : p1.deferred_layers) deferred += " " + std::to_string(L);
+        text = deferred + "\n" + head +
+               (p2.error.empty() ? sp::describe_plan(p2) : ("ERROR " + p2.error + "\n"));
+    }
+    if (buf && cap > 0) {
+        const int64_t n = std::min<int64_t>(cap - 1, static_cast<int64_t>(text.size()));
+        std::memcpy(buf, text.data(), static_cast<size_t>(n));
+        buf[n] = '\0';
+    }
+    return static_cast<int64_t>(text.size()) + 1;
 }

@@ -78,9 +78,6 @@ Executor::Executor(const sp_config& cfg) : cfg_(cfg) {
     d_ = cfg.d;
     if (n_ < 1) throw Error(SP_ERR_INVALID, "build_model: n_layers must be >= 1");
     if (d_ < 1) throw Error(SP_ERR_INVALID, "build_model: d must be >= 1");
-    if (const char* e = std::getenv("SP_WB")) staged_writeback_ = std::atoi(e) != 0;  // A/B only
-    if (const char* e = std::getenv("SP_POISON")) poison_ = std::atoi(e) != 0;        // debug only
-    if (const char* e = std::getenv("SP_FAULT_DROP_LOAD_EDGES")) drop_load_edges_ = std::atoi(e) != 0;
     const std::string v = validate_strategy(cfg.strategy, cfg.k, cfg.k_prime, n_);
     if (!v.empty()) throw Error(SP_ERR_INVALID, v);
     if (cfg.strategy == static_cast<int>(Strategy::CpuOnly))
@@ -122,12 +119,12 @@ Executor::Executor(const sp_config& cfg) : cfg_(cfg) {
     CUDA_OK(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
     CUDA_OK(cudaEventCreateWithFlags(&ev_loss_, cudaEventDisableTiming));
     for (auto& e : ev_join_) CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    if (const char* g = std::getenv("SUPERPIPE_GRAPHS")) use_graphs_ = std::atoi(g) != 0;
     CUDA_OK(cudaHostAlloc(&loss_host_, 16, cudaHostAllocPortable));
 
     relu_.assign(static_cast<size_t>(n_), 1);
     frozen_.assign(static_cast<size_t>(n_), 0);
     registered_.assign(static_cast<size_t>(n_), 0);
+    inconsistent_.assign(static_cast<size_t>(n_), 0);
     host16_stale_.assign(static_cast<size_t>(n_), 1);
     host_partial_.assign(static_cast<size_t>(n_), 0);
 }
@@ -210,11 +207,7 @@ void Executor::layout_slots(int world) {
 // the same (SGD and AdamW, interleaved A/B), and each stage is a slot's worth of HBM.
 void Executor::ensure_stages() {
     if (stages_dev_ || !staged_writeback_) return;
-    static const int cap = [] {  // SP_WB_STAGES=n: A/B measurement only
-        const char* e = std::getenv("SP_WB_STAGES");
-        return e ? std::max(1, std::atoi(e)) : 3;
-    }();
-    n_stages_ = std::max(1, std::min(n_slots_, cap));
+    n_stages_ = std::max(1, std::min(n_slots_, wb_stages_cap_));
     stage_bytes_ = off_w16_;  // [A] or [A][M][V]: the slot minus its bf16 wire region
     CUDA_OK(cudaMalloc(&stages_dev_, static_cast<size_t>(n_stages_) * stage_bytes_));
 }
@@ -380,6 +373,7 @@ void Executor::register_layer(int index, const float* W, const float* b, int act
     relu_[index] = activation == SP_RELU;
     frozen_[index] = frozen != 0;
     registered_[index] = 1;
+    inconsistent_[static_cast<size_t>(index)] = 0;
     host16_stale_[index] = 1;
     host_partial_[index] = 0;
     sync_layer_meta(index);
@@ -398,9 +392,14 @@ void Executor::require_full_host(int layer, const char* what) const {
 
 void Executor::check_ready() {
     if (shm_) sync_layer_meta(-1);  // layers registered by another process sharing the master
-    for (int i = 0; i < n_; ++i)
+    for (int i = 0; i < n_; ++i) {
         if (!registered_[i])
             throw Error(SP_ERR_STATE, "layer " + std::to_string(i) + " was never registered");
+        if (inconsistent_[static_cast<size_t>(i)])
+            throw Error(SP_ERR_STATE, "layer " + std::to_string(i) +
+                                          ": a failed train step left the host master part-updated; "
+                                          "register the layers again");
+    }
 }
 
 void Executor::refresh_host16() {
@@ -525,7 +524,7 @@ Plan Executor::make_plan(bool train, int n_items, int64_t rows, int fmt) {
         const double spare = n_ * t_c - (n_ - S) * t_load;  // forward compute beyond its loads
         const int fit = spare > 0 ? static_cast<int>(spare / t_wb) : 0;
         in.defer_budget = std::min(S, std::max(n_ - S, fit));
-        if (const char* e = std::getenv("SP_DEFER_BUDGET")) in.defer_budget = std::atoi(e);  // A/B only
+        if (defer_budget_override_ >= 0) in.defer_budget = defer_budget_override_;  // A/B only
     }
     if (shm_) {
         for (int L = 0; L < n_; ++L) plan_ver_[static_cast<size_t>(L)] = layer_version(L);
@@ -542,6 +541,15 @@ Plan Executor::make_plan(bool train, int n_items, int64_t rows, int fmt) {
     }
     const std::vector<SlotCache> none;
     Plan plan = build_plan(in, fmt == cache_fmt_ ? cache_ : none);
+    if (plan.pending_conflict && !in.pending_wb_layers.empty()) {
+        // A capacity-shrunk ring would drop a deferred write-back: complete them now, then plan
+        // from the (unchanged, still valid) slot cache without pending ones.
+        flush_writebacks();
+        in.pending_wb_layers.clear();
+        in.pending_wb_slots.clear();
+        plan = build_plan(in, fmt == cache_fmt_ ? cache_ : none);
+    }
+    if (plan.pending_conflict) throw Error(SP_ERR_INTERNAL, plan.error);
     if (!plan.error.empty()) throw Error(plan.oom ? SP_ERR_OOM : SP_ERR_INVALID, plan.error);
     return plan;
 }
@@ -859,11 +867,7 @@ void Executor::enqueue_op(const Plan& plan, int i, bool train, int n_items, int6
     };
     // Eager H2D: each moved layer waits for its own slot just before its copy (deps is then
     // exactly the union of move_deps); otherwise everything up front (policy trigger).
-    static const bool per_move_on = [] {  // SP_PER_MOVE=0: A/B measurement only
-        const char* e = std::getenv("SP_PER_MOVE");
-        return !e || std::atoi(e) != 0;
-    }();
-    const bool per_move = per_move_on && op.kind == OpKind::H2D && eager_prefetch_ && !op.move_deps.empty();
+    const bool per_move = per_move_ && op.kind == OpKind::H2D && eager_prefetch_ && !op.move_deps.empty();
     if (!per_move)
         for (int dep : op.deps) wait(dep);
     // Timing events are "external" so that, under graph capture, they become event-record
@@ -1002,12 +1006,8 @@ void Executor::enqueue_call(const Plan& plan, const CallIO& io) {
             if (stream_of(plan.ops[static_cast<size_t>(dep)].kind) != stream_of(plan.ops[j].kind))
                 cross_dep_[static_cast<size_t>(dep)] = 1;
     move_ev_base_.assign(plan.ops.size(), -1);
-    static const bool move_events = [] {  // SP_MOVE_EVENTS=0: A/B measurement only
-        const char* e = std::getenv("SP_MOVE_EVENTS");
-        return !e || std::atoi(e) != 0;
-    }();
     size_t moves = 0;
-    for (size_t j = 0; j < plan.ops.size() && move_events; ++j)
+    for (size_t j = 0; j < plan.ops.size() && move_events_; ++j)
         if (plan.ops[j].kind == OpKind::H2D && plan.ops[j].layers.size() > 1) {
             move_ev_base_[j] = static_cast<int>(moves);
             moves += plan.ops[j].layers.size() - 1;
@@ -1094,17 +1094,60 @@ uint64_t Executor::call_signature(const Plan& plan, const CallIO& io) const {
 }
 
 void Executor::run_call(const Plan& plan, const CallIO& io) {
+    launched_ = false;
     try {
         run_call_impl(plan, io);
     } catch (...) {
+        if (!launched_) {
+            // Nothing reached the device (capture / instantiation failed): the ring still
+            // holds the previous step's deferred updates - complete them before giving up.
+            try {
+                flush_writebacks();
+            } catch (...) {
+                if (io.train || !pending_wb_layers_.empty()) mark_inconsistent();
+            }
+        } else if (io.train) {
+            // Part of the step may have run: some layers updated and written back, others
+            // not, and deferred updates possibly overwritten. The host master is no longer
+            // one consistent model; every later call refuses until the layers are registered
+            // again (SP_ERR_STATE) instead of silently training a mixed model.
+            mark_inconsistent();
+        }
         // A failed call may have overwritten ring slots part-way: nothing cached on the device
         // can be trusted by the next call (the host master copy is the source of truth).
         for (auto& c : cache_) c.valid = false;
         std::fill(w16_layer_.begin(), w16_layer_.end(), -1);
-        pending_wb_layers_.clear();  // their slots may have been overwritten as well
+        pending_wb_layers_.clear();
         pending_wb_slots_.clear();
         throw;
     }
+}
+
+// Debug / A/B knobs (include/superpipe_debug.h sp_debug_set): never set on the product path.
+void Executor::set_debug(const std::string& key, int value) {
+    flush_writebacks();
+    if (key == "staged_writeback") staged_writeback_ = value != 0;
+    else if (key == "poison") poison_ = value != 0;
+    else if (key == "drop_load_edges") drop_load_edges_ = value != 0;
+    else if (key == "graphs") use_graphs_ = value != 0;
+    else if (key == "wb_stages") wb_stages_cap_ = std::max(1, value);
+    else if (key == "defer_budget") defer_budget_override_ = value;
+    else if (key == "per_move") per_move_ = value != 0;
+    else if (key == "move_events") move_events_ = value != 0;
+    else throw Error(SP_ERR_INVALID, "sp_debug_set: unknown key " + key);
+    if (stages_dev_) {  // re-sized (or dropped) on the next training call
+        CUDA_OK(cudaDeviceSynchronize());
+        cudaFree(stages_dev_);
+        stages_dev_ = nullptr;
+        n_stages_ = 0;
+    }
+    for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second.exec);
+    graphs_.clear();
+}
+
+void Executor::mark_inconsistent() {
+    for (int L = 0; L < n_; ++L)
+        if (!frozen_[static_cast<size_t>(L)]) inconsistent_[static_cast<size_t>(L)] = 1;
 }
 
 void Executor::run_call_impl(const Plan& plan, const CallIO& io) {
@@ -1122,6 +1165,7 @@ void Executor::run_call_impl(const Plan& plan, const CallIO& io) {
                                                             pinned_or_null(io.t) &&
                                                             pinned_or_null(io.y)));
     if (!graphable) {
+        launched_ = true;  // eager: ops reach the device as they are enqueued
         enqueue_call(plan, io);
     } else {
         const uint64_t sig = call_signature(plan, io);
@@ -1130,6 +1174,7 @@ void Executor::run_call_impl(const Plan& plan, const CallIO& io) {
             // Replay: one launch for the whole step; re-apply the host-side effects the
             // captured enqueue had (bf16-copy tracking, stale inference wire, counters).
             const GraphEntry& g = it->second;
+            launched_ = true;
             CUDA_OK(cudaGraphLaunch(g.exec, s_h2d_));
             w16_layer_ = g.w16_after;
             for (int L : g.stale_layers) host16_stale_[static_cast<size_t>(L)] = 1;
@@ -1171,6 +1216,7 @@ void Executor::run_call_impl(const Plan& plan, const CallIO& io) {
             g.d2h_bytes = d2h_bytes_;
             g.gemm_count = gemm_count_;
             g.gemm_flops = gemm_flops_;
+            launched_ = true;
             CUDA_OK(cudaGraphLaunch(g.exec, s_h2d_));
             graphs_.emplace(sig, std::move(g));
         }

@@ -40,6 +40,7 @@ public:
     void set_trace(int level) { cfg_.trace = level; }
     void set_item_batching(bool on) { item_batching_ = on; }
     void set_eager_prefetch(bool on) { eager_prefetch_ = on; }
+    void set_debug(const std::string& key, int value);
     std::string last_plan_text() const { return describe_plan(last_plan_); }
     void dp_init(const uint8_t id[128], int rank, int world, bool shard_weights);
     void dp_sync();
@@ -142,6 +143,11 @@ private:
     std::vector<uint8_t> host16_stale_;
     std::vector<int> relu_, frozen_;
     std::vector<uint8_t> registered_;
+    // Layers whose host master may be part-updated by a train step that failed after reaching
+    // the device (run_call); calls refuse with SP_ERR_STATE until they are registered again.
+    std::vector<uint8_t> inconsistent_;
+    bool launched_ = false;  // the current call has put work on the device
+    void mark_inconsistent();
     // HBM ring
     int n_slots_ = 0;
     size_t slot_bytes_ = 0, off_w16_ = 0, off_m_ = 0, off_v_ = 0;
@@ -155,6 +161,10 @@ private:
     int n_stages_ = 0;
     size_t stage_bytes_ = 0;
     bool staged_writeback_ = true;
+    // A/B and debug knobs (set_debug; defaults are the product behaviour)
+    int wb_stages_cap_ = 3;
+    int defer_budget_override_ = -1;
+    bool per_move_ = true, move_events_ = true;
     // Debug (SP_POISON=1): every ring-slot / activation-reload copy is preceded by a NaN fill
     // of its destination, so a read that overtakes the copy shows up as NaN (a dynamic check
     // of the plan's edges next to the static one in tests/test_plan_hazards.py).

@@ -7,7 +7,7 @@
 #include <cuda_bf16.h>
 
 #include "kernels.hpp"
-#include "pdl.cuh"
+#include "launch.cuh"
 
 namespace sp {
 namespace {
@@ -16,7 +16,6 @@ constexpr int kThreads = 256;
 
 __global__ void convert_kernel(const float* __restrict__ src, __nv_bfloat16* __restrict__ dst,
                                int64_t count) {
-    pdl_wait_then_release();
     const int64_t n4 = count / 4;
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n4; i += stride) {
@@ -78,7 +77,6 @@ template <typename T>
 __global__ void loss_grad_kernel(const float* __restrict__ y, const float* __restrict__ t,
                                  int64_t count, float inv_n, int relu,
                                  T* __restrict__ g, float* __restrict__ partials) {
-    pdl_wait_then_release();
     const int64_t n4 = count / 4;
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
     float acc = 0.0f;
@@ -100,7 +98,6 @@ __global__ void loss_grad_kernel(const float* __restrict__ y, const float* __res
 }
 
 __global__ void finalize_kernel(const float* __restrict__ partials, int n, float* __restrict__ out) {
-    pdl_wait_then_release();
     float acc = 0.0f;
     for (int i = threadIdx.x; i < n; i += blockDim.x) acc += partials[i];
     const float s = block_sum(acc);
@@ -117,7 +114,6 @@ constexpr int kColLanes = 8;
 __global__ void __launch_bounds__(256) colsum_kernel(const __nv_bfloat16* __restrict__ x,
                                                      int64_t rows, int d,
                                                      float* __restrict__ partials) {
-    pdl_wait_then_release();
     __shared__ float red[kColLanes][32][9];
     const int g = blockIdx.x * 32 + threadIdx.x;  // 8-column group
     const int lane_r = threadIdx.y;
@@ -164,7 +160,6 @@ __global__ void __launch_bounds__(256) colsum_kernel(const __nv_bfloat16* __rest
 // The same for an fp32 [rows][d] matrix (tf32 path): 32 groups of 4 columns x 8 row-lanes.
 __global__ void __launch_bounds__(256) colsum_f32_kernel(const float* __restrict__ x, int64_t rows,
                                                          int d, float* __restrict__ partials) {
-    pdl_wait_then_release();
     __shared__ float red[kColLanes][32][5];
     const int g = blockIdx.x * 32 + threadIdx.x;  // 4-column group
     const int lane_r = threadIdx.y;
@@ -204,7 +199,6 @@ __global__ void __launch_bounds__(256) colsum_f32_kernel(const float* __restrict
 
 __global__ void reduce_kernel(const float* __restrict__ parts, int nparts, int64_t stride,
                               int64_t count, float* __restrict__ grad) {
-    pdl_wait_then_release();
     const int64_t gs = static_cast<int64_t>(gridDim.x) * blockDim.x;
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += gs) {
         float s = parts[i];
@@ -215,7 +209,6 @@ __global__ void reduce_kernel(const float* __restrict__ parts, int nparts, int64
 
 __global__ void sgd_reduce_kernel(float* __restrict__ w, const float* __restrict__ parts,
                                   int nparts, int64_t stride, int64_t count, float lr) {
-    pdl_wait_then_release();
     const int64_t n4 = (stride % 4 == 0) ? count / 4 : 0;
     const int64_t gs = static_cast<int64_t>(gridDim.x) * blockDim.x;
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n4; i += gs) {
@@ -251,7 +244,6 @@ __device__ __forceinline__ void adamw_elem(float& w, float& m, float& v, float g
 __global__ void adamw_reduce_kernel(float* __restrict__ w, float* __restrict__ m, float* __restrict__ v,
                                     const float* __restrict__ parts, int nparts, int64_t stride,
                                     int64_t count, const AdamwScalars* __restrict__ sc) {
-    pdl_wait_then_release();
     const AdamwScalars s = *sc;
     const int64_t n4 = (stride % 4 == 0) ? count / 4 : 0;
     const int64_t gs = static_cast<int64_t>(gridDim.x) * blockDim.x;
@@ -288,7 +280,6 @@ __global__ void __launch_bounds__(256) sgd_reduce_narrow_kernel(float* __restric
                                                                 const float* __restrict__ parts,
                                                                 int nparts, int64_t stride,
                                                                 int64_t count, float lr) {
-    pdl_wait_then_release();
     __shared__ float red[8][33];
     const int64_t j = static_cast<int64_t>(blockIdx.x) * 32 + threadIdx.x;
     float s = 0.0f;
@@ -304,7 +295,6 @@ __global__ void __launch_bounds__(256) sgd_reduce_narrow_kernel(float* __restric
 }
 
 __global__ void scale_kernel(float* __restrict__ x, int64_t count, float s) {
-    pdl_wait_then_release();
     const int64_t gs = static_cast<int64_t>(gridDim.x) * blockDim.x;
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += gs)
         x[i] *= s;
@@ -329,7 +319,7 @@ int num_sms() {
 }
 
 void convert_f32_to_bf16(const float* src, void* dst, int64_t count, cudaStream_t st) {
-    launch_pdl(convert_kernel, dim3(grid_for(count / 4 + 1)), dim3(kThreads), 0, st, src,
+    launch_kernel(convert_kernel, dim3(grid_for(count / 4 + 1)), dim3(kThreads), 0, st, src,
                static_cast<__nv_bfloat16*>(dst), count);
 }
 
@@ -338,7 +328,7 @@ int loss_grad_bf16(const float* y, const float* t, int64_t count, float inv_n, i
     // Fixed grid (a function of count only) => a fixed summation tree.
     const int64_t need = (count / 4 + kThreads) / kThreads;
     const int blocks = static_cast<int>(need < 1 ? 1 : (need < 1184 ? need : 1184));
-    launch_pdl(loss_grad_kernel<__nv_bfloat16>, dim3(blocks), dim3(kThreads), 0, st, y, t, count, inv_n,
+    launch_kernel(loss_grad_kernel<__nv_bfloat16>, dim3(blocks), dim3(kThreads), 0, st, y, t, count, inv_n,
                relu, static_cast<__nv_bfloat16*>(g), partials);
     return blocks;
 }
@@ -347,13 +337,13 @@ int loss_grad_f32(const float* y, const float* t, int64_t count, float inv_n, in
                   float* g, float* partials, cudaStream_t st) {
     const int64_t need = (count / 4 + kThreads) / kThreads;
     const int blocks = static_cast<int>(need < 1 ? 1 : (need < 1184 ? need : 1184));
-    launch_pdl(loss_grad_kernel<float>, dim3(blocks), dim3(kThreads), 0, st, y, t, count, inv_n, relu, g,
+    launch_kernel(loss_grad_kernel<float>, dim3(blocks), dim3(kThreads), 0, st, y, t, count, inv_n, relu, g,
                partials);
     return blocks;
 }
 
 void loss_finalize(const float* partials, int n, float* out, cudaStream_t st) {
-    launch_pdl(finalize_kernel, dim3(1), dim3(kThreads), 0, st, partials, n, out);
+    launch_kernel(finalize_kernel, dim3(1), dim3(kThreads), 0, st, partials, n, out);
 }
 
 int colsum_chunks(int64_t rows) { return static_cast<int>((rows + kColRows - 1) / kColRows); }
@@ -361,7 +351,7 @@ int colsum_chunks(int64_t rows) { return static_cast<int>((rows + kColRows - 1) 
 int colsum_bf16(const void* x, int64_t rows, int d, float* partials, cudaStream_t st) {
     const int chunks = colsum_chunks(rows);  // requires d % 8 == 0 (bf16 path: d % 64 == 0)
     dim3 grid((d / 8 + 31) / 32, chunks);
-    launch_pdl(colsum_kernel, grid, dim3(32, kColLanes), 0, st,
+    launch_kernel(colsum_kernel, grid, dim3(32, kColLanes), 0, st,
                static_cast<const __nv_bfloat16*>(x), rows, d, partials);
     return chunks;
 }
@@ -369,30 +359,30 @@ int colsum_bf16(const void* x, int64_t rows, int d, float* partials, cudaStream_
 int colsum_f32(const float* x, int64_t rows, int d, float* partials, cudaStream_t st) {
     const int chunks = colsum_chunks(rows);  // requires d % 4 == 0
     dim3 grid((d / 4 + 31) / 32, chunks);
-    launch_pdl(colsum_f32_kernel, grid, dim3(32, kColLanes), 0, st, x, rows, d, partials);
+    launch_kernel(colsum_f32_kernel, grid, dim3(32, kColLanes), 0, st, x, rows, d, partials);
     return chunks;
 }
 
 void reduce_partials(const float* parts, int nparts, int64_t stride, int64_t count,
                      float* grad, cudaStream_t st) {
-    launch_pdl(reduce_kernel, dim3(grid_for(count)), dim3(kThreads), 0, st, parts, nparts, stride,
+    launch_kernel(reduce_kernel, dim3(grid_for(count)), dim3(kThreads), 0, st, parts, nparts, stride,
                count, grad);
 }
 
 void sgd_reduce(float* w, const float* parts, int nparts, int64_t stride, int64_t count,
                 float lr, cudaStream_t st) {
     if (count <= 65536 && nparts > 8) {  // short vector, many partials (bias from colsum)
-        launch_pdl(sgd_reduce_narrow_kernel, dim3(static_cast<unsigned>((count + 31) / 32)),
+        launch_kernel(sgd_reduce_narrow_kernel, dim3(static_cast<unsigned>((count + 31) / 32)),
                    dim3(32, 8), 0, st, w, parts, nparts, stride, count, lr);
         return;
     }
-    launch_pdl(sgd_reduce_kernel, dim3(grid_for(count / 4 + 1)), dim3(kThreads), 0, st, w, parts,
+    launch_kernel(sgd_reduce_kernel, dim3(grid_for(count / 4 + 1)), dim3(kThreads), 0, st, w, parts,
                nparts, stride, count, lr);
 }
 
 void adamw_reduce(float* w, float* m, float* v, const float* parts, int nparts, int64_t stride,
                   int64_t count, const AdamwScalars* scalars, cudaStream_t st) {
-    launch_pdl(adamw_reduce_kernel, dim3(grid_for(count / 4 + 1)), dim3(kThreads), 0, st, w, m, v,
+    launch_kernel(adamw_reduce_kernel, dim3(grid_for(count / 4 + 1)), dim3(kThreads), 0, st, w, m, v,
                parts, nparts, stride, count, scalars);
 }
 
@@ -404,7 +394,6 @@ struct CopyRegions {
 };
 
 __global__ void copy_regions_kernel(CopyRegions r, int64_t bytes) {
-    pdl_wait_then_release();
     const int k = blockIdx.y;
     const int64_t n16 = bytes / 16;
     const int64_t gs = static_cast<int64_t>(gridDim.x) * blockDim.x;
@@ -426,11 +415,11 @@ void copy_regions(void* const* dst, const void* const* src, int n, int64_t bytes
     }
     const int64_t n16 = bytes / 16 + 1;
     const int blocks = static_cast<int>(std::min<int64_t>((n16 + kThreads - 1) / kThreads, 296));
-    launch_pdl(copy_regions_kernel, dim3(blocks, std::min(n, 3)), dim3(kThreads), 0, st, r, bytes);
+    launch_kernel(copy_regions_kernel, dim3(blocks, std::min(n, 3)), dim3(kThreads), 0, st, r, bytes);
 }
 
 void scale_inplace(float* x, int64_t count, float s, cudaStream_t st) {
-    launch_pdl(scale_kernel, dim3(grid_for(count)), dim3(kThreads), 0, st, x, count, s);
+    launch_kernel(scale_kernel, dim3(grid_for(count)), dim3(kThreads), 0, st, x, count, s);
 }
 
 }  // namespace sp

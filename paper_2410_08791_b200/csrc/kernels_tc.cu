@@ -24,7 +24,6 @@
 #include <unordered_map>
 
 #include "kernels.hpp"
-#include "pdl.cuh"
 
 namespace sp {
 namespace tc {
@@ -556,7 +555,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     fence_after();
     const uint32_t tmem_base = *tmem_slot;
-    pdl_wait_then_release();  // prologue above overlaps the previous kernel's tail (pdl.cuh)
 
     const int tiles_mn = p.m_tiles * p.n_tiles;
     const int total = tiles_mn * p.splits;
@@ -845,7 +843,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     cluster_sync();
     fence_after();
     const uint32_t tmem_base = *tmem_slot;
-    pdl_wait_then_release();  // prologue above overlaps the previous kernel's tail (pdl.cuh)
 
     const int m_tiles2 = (p.M + 2 * BM - 1) / (2 * BM);
     const PairSched sched(p, m_tiles2, blockIdx.x >> 1, gridDim.x >> 1);
@@ -1122,15 +1119,17 @@ bool make_epilogue_maps(const GemmProblem& g, int splits, CUtensorMap* to, CUten
     return true;
 }
 
+// A/B knobs (sp_debug_set): epilogue kind 0 auto / 1 direct / 2 TMA; half-width ragged tiles
+// for every epilogue (1) or the split-K partials only (0, the product choice).
+int g_epi_mode = 0;
+int g_narrow = 0;
+
 // Epilogue kind: TMA staging when the tile's K loop is short (the epilogue is then on the
 // critical path: +8..15% on the d=1280/1600 layer GEMMs, ncu, fixed clocks), direct per-lane
 // stores for long K (where the epilogue hides and the TMA kind costs ~5%, d=4096).
-// SP_EPI_MODE=1/2 forces direct/TMA (A/B measurement only).
+// sp_debug_set("epi_mode", 1|2) forces direct/TMA (A/B measurement only).
 bool use_tma_epilogue(const GemmProblem& g, int splits) {
-    static const int forced = [] {
-        const char* e = std::getenv("SP_EPI_MODE");
-        return e ? std::atoi(e) : 0;
-    }();
+    const int forced = g_epi_mode;
     if (g.epilogue == EPI_SGD_F32) return false;
     if (forced == 1) return false;
     if (forced == 2) return true;
@@ -1142,11 +1141,7 @@ bool use_tma_epilogue(const GemmProblem& g, int splits) {
 // for the activation GEMMs they were neutral warm and, being scheduled last, re-read every A
 // panel after it has left L2 (82 vs 58 MB DRAM reads per forward launch at 16384 x 1600).
 bool narrow_tiles(int epi_base, int bn, int last_cols) {
-    static const int forced = [] {  // SP_NARROW=1: every epilogue (A/B measurement only)
-        const char* e = std::getenv("SP_NARROW");
-        return e ? std::atoi(e) : -1;
-    }();
-    if (forced == 1) return epi_base != EPI_SGD_F32 && bn == 256 && last_cols <= 128;
+    if (g_narrow == 1)  // every epilogue (A/B measurement only) return epi_base != EPI_SGD_F32 && bn == 256 && last_cols <= 128;
     return epi_base == EPI_F32 && bn == 256 && last_cols <= 128;
 }
 
@@ -1194,7 +1189,8 @@ cudaError_t launch(const GemmProblem& g, cudaStream_t st) {
     if (!make_epilogue_maps<EPI>(g, p.splits, &to, &tg)) return cudaErrorInvalidValue;
     const int total = p.m_tiles * p.n_tiles * p.splits;
     const int grid = total < num_sms() ? total : num_sms();
-    return launch_pdl(kern, dim3(grid), dim3(kThreads), C::SMEM, st, ta, tb, to, tg, p);
+    kern<<<dim3(grid), dim3(kThreads), C::SMEM, st>>>(ta, tb, to, tg, p);
+    return cudaGetLastError();
 }
 
 // 2-CTA launch: BN is the pair's N (each CTA stages BN/2 columns of B); grid = 2 x clusters.
@@ -1246,7 +1242,8 @@ cudaError_t launch2(const GemmProblem& g, cudaStream_t st) {
     const int total = p.m_tiles * p.n_tiles * p.splits;
     const int pairs = num_sms() / 2;
     const int grid = 2 * (total < pairs ? total : pairs);
-    return launch_pdl(kern, dim3(grid), dim3(kThreads), C::SMEM, st, ta, tb, to, tg, p);
+    kern<<<dim3(grid), dim3(kThreads), C::SMEM, st>>>(ta, tb, to, tg, p);
+    return cudaGetLastError();
 }
 
 // Picks the epilogue kind at run time; each kind is its own kernel instantiation.
@@ -1316,6 +1313,13 @@ cudaError_t dispatch2_bn_kmajor(const GemmProblem& g, cudaStream_t st) {
 }
 
 }  // namespace tc
+
+void set_gemm_debug(const char* key, int value, bool* known) {
+    *known = true;
+    if (std::strcmp(key, "epi_mode") == 0) tc::g_epi_mode = value;
+    else if (std::strcmp(key, "narrow") == 0) tc::g_narrow = value;
+    else *known = false;
+}
 
 // Kernel choice from a wave-quantised cost model: time ~ waves x per-SM tile work / per-SM
 // rate. Relative per-SM rates calibrated on B200 (tools/gemm_bench.py, grouped rasterisation):

@@ -117,7 +117,15 @@ public:
         // order given - build_plan passes them sorted by when each slot is first overwritten.
         for (std::size_t i = 0; i < in_.pending_wb_layers.size(); ++i) {
             const int L = in_.pending_wb_layers[i], s = in_.pending_wb_slots[i];
-            if (s < 0 || s >= static_cast<int>(slots_.size())) continue;
+            if (s < 0 || s >= static_cast<int>(slots_.size())) {
+                // build_plan never shrinks the ring below a pending slot (the executor
+                // flushes first), so this is an internal invariant, never a silent skip.
+                plan_.error = "internal: pending write-back of layer " + std::to_string(L) +
+                              " targets slot " + std::to_string(s) + " outside a " +
+                              std::to_string(slots_.size()) + "-slot ring";
+                plan_.pending_conflict = true;
+                return plan_;
+            }
             Op wb;
             wb.kind = OpKind::D2H;
             wb.pass = 0;
@@ -605,7 +613,18 @@ Plan build_plan(const PlanInput& in, const std::vector<SlotCache>& initial) {
     // set (k slots, or n for Standard) it deadlocks -> OOM.
     int S = ring_slots(in.strategy, in.k, in.k_prime, in.n_layers);
     const int smin = in.strategy == static_cast<int>(Strategy::Standard) ? in.n_layers : in.k;
+    // The previous call's deferred write-backs read their slots at this call's start: a ring
+    // shrunk below one of them (a capacity cap with a larger batch) would lose that update.
+    // Such a plan is refused with pending_conflict; the caller flushes and plans again.
+    int wb_min = 0;
+    for (int s : in.pending_wb_slots) wb_min = std::max(wb_min, s + 1);
     for (;;) {
+        if (S < wb_min) {
+            Plan c;
+            c.pending_conflict = true;
+            c.error = "internal: the ring would shrink below a pending write-back slot";
+            return c;
+        }
         Builder b(in, initial, S);
         Plan p = b.run();
         if (!p.oom && in.pending_wb_layers.size() > 1) {

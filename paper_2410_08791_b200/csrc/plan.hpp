@@ -126,6 +126,8 @@ struct Plan {
     uint64_t h2d_weight_layers = 0, h2d_act_layers = 0, d2h_weight_layers = 0,
              d2h_act_layers = 0;
     bool oom = false;
+    // The ring cannot keep a pending write-back's slot (see build_plan): flush, plan again.
+    bool pending_conflict = false;
     std::string error;  // invalid configuration or OOM reason
 };
 

@@ -30,9 +30,29 @@ def test_reference_arm_prints_one_contract_line():
 
 
 def test_reference_arm_other_ranks_exit_quietly():
-    r = _run({"RANK": "1", "WORLD_SIZE": "2", "LOCAL_RANK": "1"})
+    r = _run({"RANK": "1", "WORLD_SIZE": "2", "LOCAL_RANK": "1"}, "--gpus", "2")
     assert r.returncode == 0, r.stderr
     assert not [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+
+
+def test_gpus_flag_without_torchrun_spawns_that_many_ranks():
+    # `python bench.py --gpus 2` re-launches itself under torch.distributed.run with 2 ranks
+    # (dry run: print the launch instead of running it)
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
+    env["SP_BENCH_DRY_SPAWN"] = "1"
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "1"],
+                       capture_output=True, text=True, timeout=300, env=env, cwd=ROOT)
+    assert r.returncode == 0, r.stderr
+    cmd = json.loads(r.stdout.strip().splitlines()[-1])["spawn"]
+    assert "torch.distributed.run" in cmd and "--nproc-per-node=2" in cmd
+    assert "127.0.0.1" in cmd and cmd[-4:] == ["--gpus", "2", "--steps", "1"]
+
+
+def test_gpus_flag_must_match_the_torchrun_world():
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "4", "--steps", "1"],
+                       capture_output=True, text=True, timeout=300, cwd=ROOT,
+                       env=dict(os.environ, RANK="0", WORLD_SIZE="2", LOCAL_RANK="0"))
+    assert r.returncode == 2 and "WORLD_SIZE=2" in r.stdout
 
 
 import pytest  # noqa: E402

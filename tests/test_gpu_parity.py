@@ -594,7 +594,7 @@ def test_training_reduces_the_loss(numerics):
 def test_staged_and_deferred_writeback_is_bitwise_and_flushes_on_read(numerics, monkeypatch):
     """The executor's write-back scheme (updates copied to staging buffers; the ring's final
     residents written back by the next call, or by a flush before any host read) against the
-    plain one (SP_WB=0, A/B switch): identical weights / losses after every step, with reads,
+    plain one (debug knob staged_writeback=0): identical weights / losses after every step, with reads,
     an inference call and a re-registration interleaved, for every strategy."""
     d = 16 if numerics == sp.EXACT else 128
     rows = 5 if numerics == sp.EXACT else 256
@@ -602,9 +602,9 @@ def test_staged_and_deferred_writeback_is_bitwise_and_flushes_on_read(numerics, 
     x, t = sp.make_input(23, 0, rows, d), sp.make_input(23, 1, rows, d)
 
     def run(wb, s):
-        monkeypatch.setenv("SP_WB", wb)
         out = []
         with sp.Executor(7, d, s, numerics=numerics) as ex:
+            ex.debug_set("staged_writeback", int(wb))
             ex.register_model(model)
             for i in range(4):
                 out.append(ex.train_step(x, t, 0.02))
@@ -669,7 +669,7 @@ def test_graph_replayed_steps_with_deferred_writeback_equal_eager_steps(numerics
 @pytest.mark.parametrize("numerics", [sp.EXACT, sp.BF16])
 def test_poisoned_slots_change_nothing(numerics, monkeypatch):
     """Dynamic check of the plan's edges (the static one is tests/test_plan_hazards.py): with
-    SP_POISON=1 every ring-slot and activation-reload copy is preceded by a NaN fill of its
+    the debug knob poison=1 every ring-slot and activation-reload copy is preceded by a NaN fill of its
     destination, so any read that overtakes a copy would surface as NaN. Training (with and
     without activation offload, AdamW, 1-rank sharded DP) and inference stay bitwise equal to
     the unpoisoned runs."""
@@ -679,11 +679,11 @@ def test_poisoned_slots_change_nothing(numerics, monkeypatch):
     x, t = sp.make_input(33, 0, rows, d), sp.make_input(33, 1, rows, d)
 
     def run(poison):
-        monkeypatch.setenv("SP_POISON", "1" if poison else "0")
         out = []
         for s in (S(sp.SUPERPIPELINE, 3, 1), S(sp.SUPERPIPELINE, 2, 1, sp.SEQUENTIAL), S(sp.NAIVE, 2)):
             for ckpt in (False, True):
                 with sp.Executor(7, d, s, numerics=numerics, checkpointing=ckpt) as ex:
+                    ex.debug_set("poison", int(poison))
                     ex.register_model(model)
                     out += [ex.train_step(x, t, 0.02) for _ in range(3)]
                     ex.set_optimizer(sp.OPT_ADAMW, 0.9, 0.999, 1e-8, 0.0)
@@ -691,6 +691,7 @@ def test_poisoned_slots_change_nothing(numerics, monkeypatch):
                     out.append(ex.read_model(model).W.copy())
                     out.append(ex.forward([x[:5], x[1:6]]))
         with sp.Executor(7, d, S(sp.SUPERPIPELINE, 3, 1), numerics=numerics) as ex:
+            ex.debug_set("poison", int(poison))
             ex.register_model(model)
             ex.dp_init(sp.Executor.nccl_unique_id(), 0, 1, shard_weights=True)
             out += [ex.train_step(x, t, 0.02) for _ in range(2)]
@@ -710,15 +711,14 @@ def test_poison_detects_a_dropped_load_edge(monkeypatch):
     d, n = 2048, 6  # 16 MB layer copies (~0.3 ms) against a few-microsecond 8-row compute
     model = sp.build_model(35, n, d, 0)
     x = sp.make_input(35, 0, 8, d)
-    monkeypatch.setenv("SP_POISON", "0")
     with sp.Executor(n, d, S(sp.SUPERPIPELINE, 2, 1)) as ex:
         ex.register_model(model)
         want = ex.forward([x])[0]
-    monkeypatch.setenv("SP_POISON", "1")
-    monkeypatch.setenv("SP_FAULT_DROP_LOAD_EDGES", "1")
     bad = 0
     for _ in range(5):
         with sp.Executor(n, d, S(sp.SUPERPIPELINE, 2, 1)) as ex:
+            ex.debug_set("poison", 1)
+            ex.debug_set("drop_load_edges", 1)
             ex.register_model(model)
             y = ex.forward([x])[0]
         bad += int(not np.array_equal(y, want))

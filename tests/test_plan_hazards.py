@@ -356,3 +356,55 @@ def test_writeback_scheme_keeps_policy_ops_and_moves_tail_writebacks():
     deferred = [o["layers"][0] for o in steady if o.get("deferred")]
     assert sorted(pending) == sorted(deferred) == list(range(6))  # S = k + k' = 6
     assert pending == sorted(pending)  # forward order: the first slot reused is freed first
+
+
+def _two_calls(n, d, k, kp, cap, act1, act2):
+    from paper_2410_08791_b200 import _capi as capi
+    import ctypes as C
+    cfg = capi.SpConfig(n_layers=n, d=d, strategy=SUPERPIPELINE_, k=k, k_prime=kp,
+                        transfer_mode=1, numerics=0, checkpointing=0, device=0, trace=0,
+                        capacity_bytes=cap)
+    need = capi.LIB.sp_debug_plan_two_calls(C.byref(cfg), act1, act2, None, 0)
+    buf = C.create_string_buffer(int(need))
+    capi.LIB.sp_debug_plan_two_calls(C.byref(cfg), act1, act2, buf, need)
+    return buf.value.decode()
+
+
+SUPERPIPELINE_ = 3
+
+
+def test_growing_batch_under_capacity_never_drops_a_deferred_writeback():
+    # n=8, SP(4,2), capacity 5600 B, d=16 (1088-B layers). Call 1 at 10 B of
+    # activations per layer runs a 5-slot ring and defers the write-backs of the layers still
+    # resident; call 2 at 600 B (a larger batch) shrinks the ring below their slots. Every
+    # deferred layer must either get its D2H at the start of call 2 or be flushed (completed)
+    # before call 2 is planned; before the fix the shrunk plan silently skipped them.
+    text = _two_calls(8, 16, 4, 2, 5600, 10, 600)
+    lines = text.splitlines()
+    deferred = [int(x) for x in lines[0].split()[1:]]
+    assert deferred, text
+    flushed = []
+    body = lines[1:]
+    if body and body[0].startswith("FLUSHED"):
+        flushed = [int(x) for x in body[0].split()[1:]]
+        body = body[1:]
+    head, ops = parse_plan("\n".join(body))
+    leading = []
+    for op in ops:
+        if op["kind"] != "D2H":
+            break
+        leading += op["layers"]
+    for L in deferred:
+        assert L in flushed or L in leading, (L, text)
+    # the scenario really shrinks the ring: the pending write-backs could not all be kept
+    assert flushed == deferred
+
+
+def test_steady_batch_keeps_deferred_writebacks_pending():
+    text = _two_calls(8, 16, 4, 2, 0, 100, 100)
+    lines = text.splitlines()
+    deferred = [int(x) for x in lines[0].split()[1:]]
+    assert deferred and not lines[1].startswith("FLUSHED")
+    head, ops = parse_plan("\n".join(lines[1:]))
+    leading = [L for op in ops[:len(deferred)] if op["kind"] == "D2H" for L in op["layers"]]
+    assert sorted(leading) == sorted(deferred)

@@ -1,5 +1,6 @@
 """Warm back-to-back timing (CUDA events, real clocks) of the step's GEMMs through the
-product's auto dispatch, under the current SP_EPI_MODE / SP_NARROW environment. Prints one JSON
+product's auto dispatch, with the GEMM debug knobs epi_mode / narrow (sp_debug_set) taken from
+the SP_EPI_MODE / SP_NARROW environment of this probe. Prints one JSON
 line of microseconds per launch for each (rows, d, gemm). Used to pick the epilogue policy."""
 import json
 import os
@@ -12,6 +13,8 @@ from paper_2410_08791_b200 import _capi  # noqa: E402
 
 LIB = _capi.LIB
 out = {"env": {k: os.environ.get(k) for k in ("SP_EPI_MODE", "SP_NARROW")}}
+LIB.sp_debug_set(None, b"epi_mode", int(os.environ.get("SP_EPI_MODE", "0")))
+LIB.sp_debug_set(None, b"narrow", int(os.environ.get("SP_NARROW", "0")))
 for rows, d in [(16384, 1600), (65792, 1280), (65536, 4096)]:
     x = torch.randn(rows, d, device="cuda").to(torch.bfloat16)
     dz = torch.randn(rows, d, device="cuda").to(torch.bfloat16)
