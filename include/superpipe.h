@@ -112,6 +112,9 @@ typedef struct {
      * a captured CUDA graph (the plan is static, so repeated steps are one graph launch). */
     double host_enqueue_ms;
     uint64_t graph_replays;
+    /* attention-core launches and their algorithmic FLOPs (transformer blocks) in the last call */
+    uint64_t attn_launches;
+    double attn_flops;
 } sp_stats;
 
 /* One timeline row (TraceEvent, trace.hpp:20-50); times in ms from the call's start. */
@@ -125,6 +128,60 @@ typedef struct {
     int32_t reserved;
 } sp_trace_event;
 
+/* ---- named-shape layers ------------------------------------------------------------- */
+/* The reference's block is one square dense layer y = act(xW + b) (model.hpp:11-26), "an
+ * explicit stand-in, not a paper artifact"; the paper streams real transformer
+ * layers. A transformer block is a pre-norm decoder / encoder layer whose
+ * parameters form one flat fp32 image per layer (the unit the ring streams, exactly as the
+ * reference streams one LayerBlock):
+ *   norm1 gamma[d] (beta[d])          LayerNorm (SP_NORM_LAYER) or RMSNorm (SP_NORM_RMS)
+ *   Wqkv[d][(H + 2 Hkv) hd] (bqkv)    q heads, k heads, v heads; hd = d / H
+ *   Wo[H hd][d] (bo)
+ *   norm2 gamma[d] (beta[d])
+ *   W1[d][ff] (b1)  or  Wgu[d][2 ff]  GELU MLP, or SwiGLU with gate / up interleaved in
+ *                                      32-column chunks: columns [g0..g31 u0..u31 g32..]
+ *   W2[ff][d] (b2)
+ * (bias terms only with bias = 1). Matrices are [in][out] row-major like LayerBlock::weight;
+ * every tensor starts on a 64-float boundary; sp_block_layout gives the offsets. Forward:
+ *   h = x + attn(norm1(x)) Wo + bo,  y = h + mlp(norm2(h))   (x, h, y: fp32 residual stream)
+ * with causal (decoder) or bidirectional (encoder) softmax attention over sequences of
+ * seq_len consecutive rows, grouped-query when Hkv < H. Rows = tokens; the training loss is
+ * the reference's MSE against a [rows][d] target (mse_loss, model.cpp:131-148). */
+typedef enum { SP_BLOCK_DENSE = 0, SP_BLOCK_TRANSFORMER = 1 } sp_block_kind;
+typedef enum { SP_NORM_LAYER = 0, SP_NORM_RMS = 1 } sp_norm_kind;
+typedef enum { SP_MLP_GELU_TANH = 0, SP_MLP_GELU_ERF = 1, SP_MLP_SWIGLU = 2 } sp_mlp_kind;
+typedef struct {
+    int32_t kind;        /* sp_block_kind */
+    int32_t d;           /* model width (the residual stream) */
+    int32_t ff;          /* MLP hidden width */
+    int32_t n_heads;     /* query heads H; head_dim = d / H (64, 80 or 128) */
+    int32_t n_kv_heads;  /* key/value heads Hkv (divides H; = H without grouped-query) */
+    int32_t seq_len;     /* tokens per sequence (rows per call must be a multiple) */
+    int32_t norm;        /* sp_norm_kind */
+    int32_t mlp;         /* sp_mlp_kind */
+    int32_t bias;        /* linear layers carry biases */
+    int32_t causal;      /* 1 decoder (causal) attention, 0 encoder (bidirectional) */
+    float norm_eps;
+    int32_t reserved[5];
+} sp_block_desc;
+/* One parameter tensor of a block image. */
+typedef struct {
+    char name[16];
+    int64_t rows, cols;      /* vectors: rows = 1 */
+    uint64_t offset;         /* in floats, within the fp32 layer image */
+    uint64_t wire_offset;    /* in bytes, within the bf16 inference wire image */
+    int32_t matrix;          /* 1: bf16 on the wire; 0: fp32 vector */
+    int32_t reserved;
+} sp_block_tensor;
+/* Layout of a block's image: up to cap tensors, their count, the image size in floats and the
+ * inference wire image size in bytes (matrices bf16, vectors fp32). Host-only. */
+int sp_block_layout(const sp_block_desc* blk, sp_block_tensor* tensors, int32_t cap, int32_t* count,
+                    uint64_t* n_floats, uint64_t* wire_bytes);
+/* Deterministic random init of layer `index` of a named-shape model (host-only): the
+ * reference's per-layer splitmix64 stream (model.cpp:11-14), each matrix and its bias
+ * U(+-1/sqrt(fan_in)) in layout order, norm gains 1 and shifts 0. */
+int sp_build_block(const sp_block_desc* blk, uint64_t seed, int32_t index, float* params);
+
 /* ---- lifecycle --------------------------------------------------------------------- */
 /* Replaces Engine::Engine (engine.cpp:35-49): validates StrategyConfig (strategy.cpp:19-36),
  * allocates the pinned host weight pool and the HBM slot ring. */
@@ -133,6 +190,13 @@ int sp_create(const sp_config* cfg, sp_exec** out);
  * copies W[d*d] ([in][out]) and b[d] into executor-owned pinned host memory. */
 int sp_register_layer(sp_exec* ex, int32_t index, const float* W, const float* b,
                       int32_t activation, int32_t frozen);
+/* Executor over named-shape layers: cfg as for sp_create with cfg->d == blk->d; bf16 numerics
+ * only (SP_NUMERICS_BF16). Layers are registered with sp_register_block. */
+int sp_create_blocks(const sp_config* cfg, const sp_block_desc* blk, sp_exec** out);
+/* Copies one layer's fp32 image (sp_block_layout's n_floats floats) into the pinned master. */
+int sp_register_block(sp_exec* ex, int32_t index, const float* params, int32_t frozen);
+/* Reads one layer's current fp32 image back (RunResult::model for named-shape layers). */
+int sp_read_block(sp_exec* ex, int32_t index, float* params);
 int sp_destroy(sp_exec* ex);
 const char* sp_last_error(const sp_exec* ex);
 int sp_abi_version(void);

@@ -64,6 +64,48 @@ int32_t sp_debug_dw_choice(int32_t d, int64_t rows, int32_t fused_ok, int32_t* c
 /* Split count the GEMM will use for a given K and requested splits. */
 int32_t sp_debug_effective_splits(int32_t K, int32_t splits);
 
+/* Every GEMM epilogue of the executor, including the transformer-block ones (kernels.hpp
+ * GemmEpilogue 6..9: residual add, GELU with pre-activation side output, GELU' gate, SwiGLU).
+ * Fields as sp_debug_gemm_bf16_masked_async; aux/ldaux the pre-activation output; act the
+ * GELU kind (0 tanh, 1 erf). Launched on `stream` without synchronising. */
+typedef struct {
+    int32_t M, N, K;
+    const void* A;
+    int32_t lda, a_mn;
+    const void* B;
+    int32_t ldb, b_mn;
+    int32_t epilogue;
+    void* out;
+    int32_t ldo;
+    const float* bias;
+    int32_t relu;
+    const void* gate;
+    int32_t ldg, splits, block_n, cta;
+    void* aux;
+    int32_t ldaux, act;
+    void* stream;
+} sp_debug_gemm_args;
+int sp_debug_gemm_ex(const sp_debug_gemm_args* a);
+/* The attention core of the transformer blocks (kernels.hpp AttnProblem), device pointers,
+ * launched on `stream`. Forward: qkv -> o, lse. Backward: (qkv, o, lse, dout) -> dqkv, with
+ * delta a scratch of tokens * n_heads floats. */
+int sp_debug_attention(int32_t backward, int64_t tokens, int32_t seq_len, int32_t n_heads,
+                       int32_t n_kv_heads, int32_t head_dim, int32_t causal, const void* qkv, void* o,
+                       float* lse, const void* dout, float* delta, void* dqkv, void* stream);
+/* LayerNorm (rms = 0) / RMSNorm (rms = 1) forward and backward (kernels.hpp norm_forward /
+ * norm_backward), device pointers, on `stream`. Backward returns the partial chunk count. */
+int sp_debug_norm_forward(const float* x, const float* gamma, const float* beta, int32_t rms, float eps,
+                          int64_t rows, int32_t d, void* y, float* stats, void* stream);
+int sp_debug_norm_backward(const float* dy, const float* x, const float* stats, const float* gamma,
+                           int32_t rms, int64_t rows, int32_t d, const float* dres_in, float* dres_out,
+                           void* dres_out16, float* part, void* stream);
+
+/* Transformer-block executors: the fp32 gradient image (the layer's parameter layout) of
+ * layer `index` from the last train step, as the UPDATE op consumed it. Gradient images are
+ * double-buffered by layer parity, so only the last two layers the backward reached (layers 0
+ * and 1) are still intact. Not available in sharded data parallel. */
+int sp_debug_read_grad(struct sp_exec* ex, int32_t index, float* out);
+
 /* Debug and A/B measurement knobs (defaults = the product behaviour; nothing on the product
  * path sets them). Executor keys (ex != NULL): "staged_writeback" (0: write back straight from
  * the slot), "wb_stages" (staging buffer count, default 3), "defer_budget" (-1 = the executor's

@@ -38,7 +38,7 @@ class SpStats(C.Structure):
         ("loss", C.c_float), ("n_slots", C.c_int32), ("digest", C.c_char * 17),
         ("_pad", C.c_char * 3), ("gemm_launches", C.c_uint64), ("gemm_ms", C.c_double),
         ("gemm_flops", C.c_double), ("host_enqueue_ms", C.c_double),
-        ("graph_replays", C.c_uint64)]
+        ("graph_replays", C.c_uint64), ("attn_launches", C.c_uint64), ("attn_flops", C.c_double)]
 
     def as_dict(self):
         out = {}
@@ -50,6 +50,22 @@ class SpStats(C.Structure):
         return out
 
 
+BLOCK_DENSE, BLOCK_TRANSFORMER = 0, 1                 # sp_block_kind
+NORM_LAYER, NORM_RMS = 0, 1                           # sp_norm_kind
+MLP_GELU_TANH, MLP_GELU_ERF, MLP_SWIGLU = 0, 1, 2     # sp_mlp_kind
+
+
+class SpBlockDesc(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in (
+        "kind", "d", "ff", "n_heads", "n_kv_heads", "seq_len", "norm", "mlp", "bias", "causal")] + [
+        ("norm_eps", C.c_float), ("reserved", C.c_int32 * 5)]
+
+
+class SpBlockTensor(C.Structure):
+    _fields_ = [("name", C.c_char * 16), ("rows", C.c_int64), ("cols", C.c_int64), ("offset", C.c_uint64),
+                ("wire_offset", C.c_uint64), ("matrix", C.c_int32), ("reserved", C.c_int32)]
+
+
 class SpTraceEvent(C.Structure):
     _fields_ = [("t_start", C.c_double), ("t_end", C.c_double)] + [
         (n, C.c_int32) for n in ("kind", "item", "layer", "backward", "first_layer",
@@ -58,10 +74,21 @@ class SpTraceEvent(C.Structure):
         ("op_index", C.c_int32), ("reserved", C.c_int32)]
 
 
+class GemmArgs(C.Structure):
+    """sp_debug_gemm_args (include/superpipe_debug.h)."""
+    _fields_ = [("M", C.c_int32), ("N", C.c_int32), ("K", C.c_int32), ("A", C.c_void_p),
+                ("lda", C.c_int32), ("a_mn", C.c_int32), ("B", C.c_void_p), ("ldb", C.c_int32),
+                ("b_mn", C.c_int32), ("epilogue", C.c_int32), ("out", C.c_void_p), ("ldo", C.c_int32),
+                ("bias", C.c_void_p), ("relu", C.c_int32), ("gate", C.c_void_p), ("ldg", C.c_int32),
+                ("splits", C.c_int32), ("block_n", C.c_int32), ("cta", C.c_int32), ("aux", C.c_void_p),
+                ("ldaux", C.c_int32), ("act", C.c_int32), ("stream", C.c_void_p)]
+
+
 # Every symbol include/superpipe.h and include/superpipe_debug.h declare (checked by the
 # CPU test suite against the built library).
 EXPORTS = [
-    "sp_create", "sp_register_layer", "sp_destroy", "sp_last_error", "sp_abi_version",
+    "sp_create", "sp_create_blocks", "sp_register_block", "sp_read_block", "sp_block_layout",
+    "sp_build_block", "sp_register_layer", "sp_destroy", "sp_last_error", "sp_abi_version",
     "sp_forward", "sp_forward_device", "sp_train_step", "sp_train_step_device",
     "sp_read_layer", "sp_get_stats", "sp_get_trace", "sp_set_trace", "sp_last_plan", "sp_set_item_batching", "sp_set_eager_prefetch",
     "sp_set_optimizer", "sp_read_optimizer_state", "sp_share_host_master",
@@ -74,7 +101,8 @@ EXPORTS = [
     "sp_debug_gemm_tf32_async",
     "sp_debug_effective_splits",
     "sp_debug_shard_range", "sp_debug_dw_splits", "sp_debug_dw_choice",
-    "sp_debug_plan_two_calls", "sp_debug_set",
+    "sp_debug_plan_two_calls", "sp_debug_set", "sp_debug_gemm_ex", "sp_debug_attention",
+    "sp_debug_norm_forward", "sp_debug_norm_backward", "sp_debug_read_grad",
 ]
 
 
@@ -87,6 +115,12 @@ def load(path: str = LIB_PATH) -> C.CDLL:
     sig = {
         "sp_create": ([C.POINTER(SpConfig), C.POINTER(ex)], C.c_int),
         "sp_register_layer": ([ex, i32, vp, vp, i32, i32], C.c_int),
+        "sp_create_blocks": ([C.POINTER(SpConfig), C.POINTER(SpBlockDesc), C.POINTER(ex)], C.c_int),
+        "sp_register_block": ([ex, i32, vp, i32], C.c_int),
+        "sp_read_block": ([ex, i32, vp], C.c_int),
+        "sp_block_layout": ([C.POINTER(SpBlockDesc), C.POINTER(SpBlockTensor), i32, C.POINTER(i32),
+                             C.POINTER(u64), C.POINTER(u64)], C.c_int),
+        "sp_build_block": ([C.POINTER(SpBlockDesc), u64, i32, vp], C.c_int),
         "sp_destroy": ([ex], C.c_int),
         "sp_last_error": ([ex], C.c_char_p),
         "sp_abi_version": ([], C.c_int),
@@ -132,6 +166,11 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "sp_debug_shard_range": ([u64, i32, i32, C.POINTER(u64), C.POINTER(u64)], u64),
         "sp_debug_plan_two_calls": ([C.POINTER(SpConfig), u64, u64, C.c_char_p, i64], i64),
         "sp_debug_set": ([ex, C.c_char_p, i32], C.c_int),
+        "sp_debug_gemm_ex": ([C.POINTER(GemmArgs)], C.c_int),
+        "sp_debug_read_grad": ([ex, i32, vp], C.c_int),
+        "sp_debug_attention": ([i32, i64, i32, i32, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp], C.c_int),
+        "sp_debug_norm_forward": ([vp, vp, vp, i32, C.c_float, i64, i32, vp, vp, vp], C.c_int),
+        "sp_debug_norm_backward": ([vp, vp, vp, vp, i32, i64, i32, vp, vp, vp, vp, vp], C.c_int),
     }
     for name, (args, res) in sig.items():
         if os.environ.get("SUPERPIPE_LIB") and not hasattr(lib, name):

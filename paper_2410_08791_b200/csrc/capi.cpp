@@ -61,6 +61,31 @@ int sp_create(const sp_config* cfg, sp_exec** out) {
     return SP_OK;
 }
 
+int sp_create_blocks(const sp_config* cfg, const sp_block_desc* blk, sp_exec** out) {
+    if (!cfg || !blk || !out) return SP_ERR_INVALID;
+    *out = nullptr;
+    auto* ex = new (std::nothrow) sp_exec;
+    if (!ex) return SP_ERR_OOM;
+    const int rc = guarded(ex, [&] { ex->impl = new sp::Executor(*cfg, blk); });
+    if (rc != SP_OK) {
+        g_create_error = ex->error;
+        delete ex;
+        return rc;
+    }
+    *out = ex;
+    return SP_OK;
+}
+
+int sp_register_block(sp_exec* ex, int32_t index, const float* params, int32_t frozen) {
+    if (!ex) return SP_ERR_INVALID;
+    return guarded(ex, [&] { ex->impl->register_block(index, params, frozen); });
+}
+
+int sp_read_block(sp_exec* ex, int32_t index, float* params) {
+    if (!ex) return SP_ERR_INVALID;
+    return guarded(ex, [&] { ex->impl->read_block(index, params); });
+}
+
 int sp_register_layer(sp_exec* ex, int32_t index, const float* W, const float* b,
                       int32_t activation, int32_t frozen) {
     if (!ex) return SP_ERR_INVALID;
@@ -511,4 +536,72 @@ extern "C" int64_t sp_debug_plan_two_calls(const sp_config* cfg, uint64_t act_by
         buf[n] = '\0';
     }
     return static_cast<int64_t>(text.size()) + 1;
+}
+
+extern "C" int sp_debug_gemm_ex(const sp_debug_gemm_args* a) {
+    if (!a) return static_cast<int>(cudaErrorInvalidValue);
+    sp::GemmProblem g;
+    g.M = a->M;
+    g.N = a->N;
+    g.K = a->K;
+    g.A = a->A;
+    g.lda = a->lda;
+    g.a_mn = a->a_mn != 0;
+    g.B = a->B;
+    g.ldb = a->ldb;
+    g.b_mn = a->b_mn != 0;
+    g.epilogue = a->epilogue;
+    g.out = a->out;
+    g.ldo = a->ldo;
+    g.bias = a->bias;
+    g.relu = a->relu;
+    g.gate = a->gate;
+    g.ldg = a->ldg;
+    g.splits = a->splits;
+    g.split_stride = static_cast<int64_t>(a->M) * a->ldo;
+    g.block_n = a->block_n;
+    g.cta = a->cta;
+    g.lr = 1.0f;
+    g.aux = a->aux;
+    g.ldaux = a->ldaux;
+    g.act = a->act;
+    return static_cast<int>(sp::gemm_bf16(g, static_cast<cudaStream_t>(a->stream)));
+}
+
+extern "C" int sp_debug_attention(int32_t backward, int64_t tokens, int32_t seq_len, int32_t n_heads,
+                                  int32_t n_kv_heads, int32_t head_dim, int32_t causal, const void* qkv, void* o,
+                                  float* lse, const void* dout, float* delta, void* dqkv, void* stream) {
+    sp::AttnProblem a;
+    a.tokens = tokens;
+    a.seq_len = seq_len;
+    a.n_heads = n_heads;
+    a.n_kv_heads = n_kv_heads;
+    a.head_dim = head_dim;
+    a.causal = causal;
+    a.qkv = qkv;
+    a.o = o;
+    a.lse = lse;
+    a.dout = dout;
+    a.delta = delta;
+    a.dqkv = dqkv;
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    return static_cast<int>(backward ? sp::attention_backward(a, st) : sp::attention_forward(a, st));
+}
+
+extern "C" int sp_debug_norm_forward(const float* x, const float* gamma, const float* beta, int32_t rms, float eps,
+                                     int64_t rows, int32_t d, void* y, float* stats, void* stream) {
+    sp::norm_forward(x, gamma, beta, rms, eps, rows, d, y, stats, static_cast<cudaStream_t>(stream));
+    return static_cast<int>(cudaGetLastError());
+}
+
+extern "C" int sp_debug_norm_backward(const float* dy, const float* x, const float* stats, const float* gamma,
+                                      int32_t rms, int64_t rows, int32_t d, const float* dres_in, float* dres_out,
+                                      void* dres_out16, float* part, void* stream) {
+    return sp::norm_backward(dy, x, stats, gamma, rms, rows, d, dres_in, dres_out, dres_out16, part,
+                             static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int sp_debug_read_grad(sp_exec* ex, int32_t index, float* out) {
+    if (!ex || !out) return SP_ERR_INVALID;
+    return guarded(ex, [&] { ex->impl->debug_read_grad(index, out); });
 }

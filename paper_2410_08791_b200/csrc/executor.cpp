@@ -73,9 +73,17 @@ void parallel_for(int n, F&& f) {
 
 }  // namespace
 
-Executor::Executor(const sp_config& cfg) : cfg_(cfg) {
+Executor::Executor(const sp_config& cfg, const sp_block_desc* block) : cfg_(cfg) {
     n_ = cfg.n_layers;
     d_ = cfg.d;
+    if (block && block->kind != SP_BLOCK_DENSE) {
+        const std::string e = make_block_layout(*block, lay_);
+        if (!e.empty()) throw Error(SP_ERR_INVALID, e);
+        if (block->d != cfg.d) throw Error(SP_ERR_INVALID, "block: d must equal the executor's d");
+        if (cfg.numerics != SP_NUMERICS_BF16)
+            throw Error(SP_ERR_INVALID, "transformer blocks run in bf16 numerics (SP_NUMERICS_BF16)");
+        blk_ = true;
+    }
     if (n_ < 1) throw Error(SP_ERR_INVALID, "build_model: n_layers must be >= 1");
     if (d_ < 1) throw Error(SP_ERR_INVALID, "build_model: d must be >= 1");
     const std::string v = validate_strategy(cfg.strategy, cfg.k, cfg.k_prime, n_);
@@ -100,9 +108,8 @@ Executor::Executor(const sp_config& cfg) : cfg_(cfg) {
     if (cfg.device < 0 || cfg.device >= ndev) throw Error(SP_ERR_INVALID, "device ordinal out of range");
     CUDA_OK(cudaSetDevice(cfg.device));
 
-    const size_t dd = static_cast<size_t>(d_) * d_;
-    CUDA_OK(cudaHostAlloc(&host32_, static_cast<size_t>(n_) * (dd + d_) * 4, cudaHostAllocPortable));
-    std::memset(host32_, 0, static_cast<size_t>(n_) * (dd + d_) * 4);
+    CUDA_OK(cudaHostAlloc(&host32_, static_cast<size_t>(n_) * img_f() * 4, cudaHostAllocPortable));
+    std::memset(host32_, 0, static_cast<size_t>(n_) * img_f() * 4);
     if (bf16_) CUDA_OK(cudaHostAlloc(&host16_, static_cast<size_t>(n_) * wire16_bytes(), cudaHostAllocPortable));
 
     n_slots_ = ring_slots(cfg.strategy, cfg.k, cfg.k_prime, n_);
@@ -218,10 +225,10 @@ void Executor::flush_writebacks() {
     if (pending_wb_layers_.empty()) return;
     CUDA_OK(cudaSetDevice(cfg_.device));
     for (auto s : {s_h2d_, s_comp_, s_d2h_, s_upd_}) CUDA_OK(cudaStreamSynchronize(s));
-    const size_t img = layer_bytes(), dd = static_cast<size_t>(d_) * d_;
+    const size_t img = layer_bytes();
     for (size_t i = 0; i < pending_wb_layers_.size(); ++i) {
         const int L = pending_wb_layers_[i], s = pending_wb_slots_[i];
-        const size_t off = static_cast<size_t>(L) * (dd + d_);
+        const size_t off = static_cast<size_t>(L) * img_f();
         CUDA_OK(cudaMemcpyAsync(host32_ + off, slot_ptr(s), img, cudaMemcpyDeviceToHost, s_d2h_));
         if (adamw()) {
             CUDA_OK(cudaMemcpyAsync(host_m_ + off, slot_m32(s), img, cudaMemcpyDeviceToHost, s_d2h_));
@@ -270,7 +277,7 @@ void Executor::share_host_master(const char* name, bool create) {
     CUDA_OK(cudaSetDevice(cfg_.device));
     for (auto s : {s_h2d_, s_comp_, s_d2h_, s_upd_}) CUDA_OK(cudaStreamSynchronize(s));
     const std::string nm = name[0] == '/' ? std::string(name) : "/" + std::string(name);
-    const size_t master = static_cast<size_t>(n_) * (static_cast<size_t>(d_) * d_ + d_) * 4;
+    const size_t master = static_cast<size_t>(n_) * img_f() * 4;
     const size_t ver_off = round_up(offsetof(ShmHeader, meta) + 12 * static_cast<size_t>(n_), 8);
     const size_t off = round_up(ver_off + 8 * static_cast<size_t>(n_), 4096);
     const size_t bytes = off + master;
@@ -363,6 +370,7 @@ void Executor::register_layer(int index, const float* W, const float* b, int act
                               int frozen) {
     if (index < 0 || index >= n_) throw Error(SP_ERR_INVALID, "register_layer: index out of range");
     if (!W || !b) throw Error(SP_ERR_INVALID, "register_layer: null weight or bias");
+    if (blk_) throw Error(SP_ERR_INVALID, "register_layer: this executor streams transformer blocks (sp_register_block)");
     flush_writebacks();  // a pending write-back must not land on top of the new weights
     if (activation != SP_RELU && activation != SP_IDENTITY)
         throw Error(SP_ERR_INVALID, "register_layer: unknown activation");
@@ -412,6 +420,23 @@ void Executor::refresh_host16() {
     }
     if (todo.empty()) return;
     const size_t dd = static_cast<size_t>(d_) * d_;
+    if (blk_) {  // wire image: matrices bf16, vectors fp32, each at its layout offset
+        parallel_for(static_cast<int>(todo.size()), [&](int t) {
+            const int L = todo[t];
+            const float* src = host32_ + static_cast<size_t>(L) * img_f();
+            uint8_t* dst = host16_ + static_cast<size_t>(L) * wire16_bytes();
+            for (const BlockTensor& x : lay_.t) {
+                if (x.matrix) {
+                    uint16_t* w16 = reinterpret_cast<uint16_t*>(dst + x.wire_off);
+                    for (uint64_t e = 0; e < x.count(); ++e) w16[e] = bf16_rne(src[x.off + e]);
+                } else {
+                    std::memcpy(dst + x.wire_off, src + x.off, x.count() * 4);
+                }
+            }
+        });
+        for (int L : todo) host16_stale_[L] = 0;
+        return;
+    }
     parallel_for(static_cast<int>(todo.size()), [&](int t) {
         const int L = todo[t];
         const float* src = host32_ + static_cast<size_t>(L) * (dd + d_);
@@ -452,11 +477,29 @@ void Executor::ensure_buffers(int64_t rows, int n_items, bool train, bool device
     const size_t dd = static_cast<size_t>(d_) * d_;
     xin_ = static_cast<float*>(alloc(std::max<size_t>(static_cast<size_t>(items), 1) * act * 4));
     yout_ = static_cast<float*>(alloc(std::max<size_t>(static_cast<size_t>(items), 1) * act * 4));
-    for (auto& p : pp_) p = alloc(act * elt);
-    xconv_ = alloc(act * 2);
     act_.clear();
     ba_.clear();
     masks_.clear();
+    if (blk_) {
+        if (tr) {
+            tgt_ = static_cast<float*>(alloc(act * 4));
+            loss_parts_ = static_cast<float*>(alloc(4096 * 4));
+            loss_dev_ = static_cast<float*>(alloc(16));
+            if (cfg_.checkpointing && cfg_.strategy != SP_STANDARD) {  // the layer input (fp32) rides
+                for (auto& f : fa_) f = alloc(act * 4);
+                for (int s = 0; s < n_slots_; ++s) ba_.push_back(alloc(act * 4));
+                host_act_bytes_ = static_cast<size_t>(n_) * act * 4;
+                CUDA_OK(cudaHostAlloc(&host_act_, host_act_bytes_, cudaHostAllocPortable));
+            }
+        }
+        block_alloc(R, items, tr, alloc);
+        cap_rows_ = R;
+        cap_items_ = items;
+        cap_train_ = tr;
+        return;
+    }
+    for (auto& p : pp_) p = alloc(act * elt);
+    xconv_ = alloc(act * 2);
     if (tr) {
         tgt_ = static_cast<float*>(alloc(act * 4));
         for (int l = 0; l < n_; ++l) act_.push_back(alloc(act * elt));
@@ -518,7 +561,8 @@ Plan Executor::make_plan(bool train, int n_items, int64_t rows, int fmt) {
         // kernels; ~50 GB/s over the host link. (Measured at C2: Standard 13.0 -> 12.2 ms.)
         const int S = std::min(n_slots_, n_);
         const double rate = tf32_ ? 0.5e15 : bf16_ ? 1.0e15 : 2.0e13;
-        const double t_c = 2.0 * static_cast<double>(rows) * d_ * d_ / rate;
+        const double t_c = static_cast<double>(rows) *
+                           (blk_ ? lay_.linear_flops_per_token() + lay_.attn_flops_per_token() : 2.0 * d_ * d_) / rate;
         const double t_load = static_cast<double>(layer_bytes()) / 5.0e10;
         const double t_wb = t_load * (adamw() ? 3.0 : 1.0);
         const double spare = n_ * t_c - (n_ - S) * t_load;  // forward compute beyond its loads
@@ -590,7 +634,10 @@ void Executor::gemm(const GemmProblem& g, cudaStream_t st) {
 }
 
 void Executor::compute_op(const Op& op, bool train, int64_t rows, int fmt) {
-    (void)fmt;
+    if (blk_) {
+        block_compute(op, train, rows, fmt);
+        return;
+    }
     const int L = op.layer, s = op.slot;
     const size_t act = static_cast<size_t>(rows) * d_;
     const bool ckpt = train && cfg_.checkpointing && cfg_.strategy != SP_STANDARD;
@@ -757,7 +804,9 @@ void Executor::loss_op(int64_t rows) {
     const float inv_n = 1.0f / static_cast<float>(count * world_);
     const int last = n_ - 1;
     void* g = gbuf_[last % 2];
-    if (!tc_) {
+    if (blk_) {
+        block_loss(rows);
+    } else if (!tc_) {
         exact_loss_grad(yout_, cur_t_, count, inv_n, relu_[last], static_cast<float*>(g), loss_dev_, s_comp_);
         kernels_ += 2;
     } else {
@@ -783,8 +832,8 @@ void Executor::update_op(const Op& op, float lr) {
     const int L = op.layer, s = op.slot;
     const size_t dd = static_cast<size_t>(d_) * d_;
     cudaStream_t st = s_upd_;
-    float* ws = gws_[L % 2];
-    if (adamw() && tc_ && !comm_) {
+    float* ws = blk_ ? bgimg_[L % 2] : gws_[L % 2];
+    if (adamw() && tc_ && !comm_ && !blk_) {
         // AdamW straight from the partials: dW split-K partials, db column-sum partials
         adamw_reduce(slot_w32(s), slot_m32(s), slot_v32(s), ws, splits_, static_cast<int64_t>(dd),
                      static_cast<int64_t>(dd), adamw_dev_, st);
@@ -794,7 +843,7 @@ void Executor::update_op(const Op& op, float lr) {
         w16_layer_[s] = -1;
         return;
     }
-    if (tc_ && !comm_) {
+    if (tc_ && !comm_ && !blk_) {
         // W: updated in the dW epilogue (fused), or here from the split-K partials in a fixed
         // order; bias from the db column-sum partials.
         const size_t db_off = dw_fused_ ? 0 : static_cast<size_t>(splits_) * dd;
@@ -807,9 +856,11 @@ void Executor::update_op(const Op& op, float lr) {
         w16_layer_[s] = -1;
         return;
     }
-    // The full-batch gradient [dW | db] (fp32, the slot's [W | b] layout) in `g`.
+    // The full-batch gradient [dW | db] (fp32, the slot's [W | b] layout; a block's gradient
+    // image in its parameter layout) in `g`.
+    const size_t imgf = img_f();
     float* g = ws;
-    if (tc_) {
+    if (tc_ && !blk_) {
         reduce_partials(ws, splits_, static_cast<int64_t>(dd), static_cast<int64_t>(dd), grad_red_, st);
         reduce_partials(ws + splits_ * dd, col_chunks_, d_, d_, grad_red_ + dd, st);
         kernels_ += 2;
@@ -833,12 +884,12 @@ void Executor::update_op(const Op& op, float lr) {
             ++kernels_;
         }
     } else {
-        if (comm_) NCCL_OK(nccl().AllReduce(g, g, dd + d_, ncclFloat, ncclSum, comm_, st));
+        if (comm_) NCCL_OK(nccl().AllReduce(g, g, imgf, ncclFloat, ncclSum, comm_, st));
         if (adamw())  // [W|b], [mW|mb], [vW|vb] are each contiguous
-            adamw_reduce(slot_w32(s), slot_m32(s), slot_v32(s), g, 1, 0, static_cast<int64_t>(dd + d_),
+            adamw_reduce(slot_w32(s), slot_m32(s), slot_v32(s), g, 1, 0, static_cast<int64_t>(imgf),
                          adamw_dev_, st);
         else
-            exact_sgd(slot_w32(s), g, static_cast<int64_t>(dd + d_), lr, st);
+            exact_sgd(slot_w32(s), g, static_cast<int64_t>(imgf), lr, st);
         ++kernels_;
     }
     w16_layer_[s] = -1;  // the bf16 copy is now stale
@@ -874,8 +925,7 @@ void Executor::enqueue_op(const Plan& plan, int i, bool train, int n_items, int6
     // nodes; the dependency events (ev_dep_) become graph edges.
     // (per-move H2D: the start is taken once the first copy's own waits are satisfied)
     if (cfg_.trace >= 1 && !per_move) record_timing(ev_start_[static_cast<size_t>(i)], st);
-    const size_t dd = static_cast<size_t>(d_) * d_;
-    const size_t act_b = static_cast<size_t>(rows) * d_ * (bf16_ ? 2 : 4);
+    const size_t act_b = static_cast<size_t>(rows) * d_ * act_elt();
     switch (op.kind) {
         case OpKind::H2D:
             for (size_t j = 0; j < op.layers.size(); ++j) {
@@ -892,7 +942,7 @@ void Executor::enqueue_op(const Plan& plan, int i, bool train, int n_items, int6
                     if (sharded_) shard_range(wire ? shardB_ : shardA_, img, lo, hi);
                     const uint8_t* src = wire ? host16_ + static_cast<size_t>(L) * wire16_bytes()
                                               : reinterpret_cast<const uint8_t*>(
-                                                    host32_ + static_cast<size_t>(L) * (dd + d_));
+                                                    host32_ + static_cast<size_t>(L) * img_f());
                     uint8_t* dst = wire ? slot_ptr(s) + off_w16_ : slot_ptr(s);
                     // Debug (SP_POISON=1): NaN-fill the whole image first, so a compute that
                     // reads the slot before this copy lands (a missing edge) produces NaNs.
@@ -911,7 +961,7 @@ void Executor::enqueue_op(const Plan& plan, int i, bool train, int n_items, int6
                 if (j < op.opts.size() && op.opts[j]) {  // AdamW m, v (sharded: this rank's shard)
                     size_t lo = 0, hi = layer_bytes();
                     if (sharded_) shard_range(shardA_, layer_bytes(), lo, hi);
-                    const size_t off = static_cast<size_t>(L) * (dd + d_);
+                    const size_t off = static_cast<size_t>(L) * img_f();
                     if (hi > lo) {
                         CUDA_OK(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(slot_m32(s)) + lo,
                                                 reinterpret_cast<const uint8_t*>(host_m_ + off) + lo, hi - lo,
@@ -960,7 +1010,7 @@ void Executor::enqueue_op(const Plan& plan, int i, bool train, int n_items, int6
             size_t lo = 0, hi = layer_bytes();
             if (sharded_) shard_range(shardA_, layer_bytes(), lo, hi);
             const uint8_t* src = op.stage >= 0 ? stage_ptr(op.stage) : slot_ptr(s);
-            const size_t off = static_cast<size_t>(L) * (dd + d_);
+            const size_t off = static_cast<size_t>(L) * img_f();
             if (hi > lo)
                 CUDA_OK(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(host32_ + off) + lo, src + lo, hi - lo,
                                         cudaMemcpyDeviceToHost, st));
@@ -1183,6 +1233,8 @@ void Executor::run_call_impl(const Plan& plan, const CallIO& io) {
             d2h_bytes_ = g.d2h_bytes;
             gemm_count_ = g.gemm_count;
             gemm_flops_ = g.gemm_flops;
+            attn_launches_ = g.attn_launches;
+            attn_flops_ = g.attn_flops;
             ++graph_replays_;
         } else {
             if (graphs_.size() >= 16) {
@@ -1216,6 +1268,8 @@ void Executor::run_call_impl(const Plan& plan, const CallIO& io) {
             g.d2h_bytes = d2h_bytes_;
             g.gemm_count = gemm_count_;
             g.gemm_flops = gemm_flops_;
+            g.attn_launches = attn_launches_;
+            g.attn_flops = attn_flops_;
             launched_ = true;
             CUDA_OK(cudaGraphLaunch(g.exec, s_h2d_));
             graphs_.emplace(sig, std::move(g));
@@ -1310,6 +1364,8 @@ void Executor::collect_stats(const Plan& plan, int n_items, bool train) {
     stats_.gemm_launches = gemm_count_;
     stats_.gemm_flops = gemm_flops_;
     stats_.gemm_ms = 0.0;
+    stats_.attn_launches = attn_launches_;
+    stats_.attn_flops = attn_flops_;
     if (cfg_.trace >= 2)
         for (size_t g = 0; g < gemm_count_; ++g) {
             float ms = 0;
@@ -1365,7 +1421,11 @@ float Executor::train_step(const float* x, const float* target, int64_t rows, fl
     Plan plan = make_plan(true, 1, rows, fmt);
     ensure_buffers(rows, 1, true, device_io);
     CUDA_OK(cudaSetDevice(cfg_.device));
-    if (tc_) {  // split-K depends only on (d, rows): identical for every window setting
+    if (blk_ && rows % lay_.desc.seq_len != 0)
+        throw Error(SP_ERR_INVALID, "train: rows must be a multiple of the block's seq_len");
+    if (blk_ && lay_.swiglu())
+        throw Error(SP_ERR_INVALID, "train: SwiGLU blocks are inference-only in this build");
+    if (tc_ && !blk_) {  // split-K depends only on (d, rows): identical for every window setting
         const DwChoice c = choose_dw(d_, d_, static_cast<int>(rows), splits_cap_, comm_ == nullptr, tf32_);
         splits_ = c.splits;
         dw_cta_ = c.cta;
@@ -1427,8 +1487,7 @@ void Executor::digest_train(float loss, char out[17]) {
         }
     };
     fnv(&loss, 4);
-    const size_t dd = static_cast<size_t>(d_) * d_;
-    fnv(host32_, static_cast<size_t>(n_) * (dd + d_) * 4);
+    fnv(host32_, static_cast<size_t>(n_) * img_f() * 4);
     static const char digits[] = "0123456789abcdef";
     for (int i = 15; i >= 0; --i) {
         out[i] = digits[h & 0xF];
@@ -1439,12 +1498,40 @@ void Executor::digest_train(float loss, char out[17]) {
 
 void Executor::read_layer(int index, float* W, float* b) {
     if (index < 0 || index >= n_) throw Error(SP_ERR_INVALID, "read_layer: index out of range");
+    if (blk_) throw Error(SP_ERR_INVALID, "read_layer: this executor streams transformer blocks (sp_read_block)");
     flush_writebacks();
     require_full_host(index, "read_layer");
     const size_t dd = static_cast<size_t>(d_) * d_;
     const float* src = host32_ + static_cast<size_t>(index) * (dd + d_);
     if (W) std::memcpy(W, src, dd * 4);
     if (b) std::memcpy(b, src + dd, static_cast<size_t>(d_) * 4);
+}
+
+void Executor::register_block(int index, const float* params, int frozen) {
+    if (!blk_) throw Error(SP_ERR_INVALID, "register_block: this executor streams dense layers (sp_register_layer)");
+    if (index < 0 || index >= n_) throw Error(SP_ERR_INVALID, "register_block: index out of range");
+    if (!params) throw Error(SP_ERR_INVALID, "register_block: null parameters");
+    flush_writebacks();
+    std::memcpy(host32_ + static_cast<size_t>(index) * img_f(), params, img_f() * 4);
+    relu_[index] = 0;
+    frozen_[index] = frozen != 0;
+    registered_[index] = 1;
+    inconsistent_[static_cast<size_t>(index)] = 0;
+    host16_stale_[index] = 1;
+    host_partial_[index] = 0;
+    sync_layer_meta(index);
+    bump_version(index);
+    for (auto& c : cache_)
+        if (c.layer == index) c.valid = false;
+}
+
+void Executor::read_block(int index, float* params) {
+    if (!blk_) throw Error(SP_ERR_INVALID, "read_block: this executor streams dense layers (sp_read_layer)");
+    if (index < 0 || index >= n_) throw Error(SP_ERR_INVALID, "read_block: index out of range");
+    if (!params) throw Error(SP_ERR_INVALID, "read_block: null output");
+    flush_writebacks();
+    require_full_host(index, "read_block");
+    std::memcpy(params, host32_ + static_cast<size_t>(index) * img_f(), img_f() * 4);
 }
 
 void Executor::dp_init(const uint8_t id[128], int rank, int world, bool shard_weights) {
@@ -1486,7 +1573,7 @@ void Executor::set_optimizer(int kind, float beta1, float beta2, float eps, floa
     eps_ = eps;
     wd_ = weight_decay;
     step_t_ = 0;
-    const size_t img = static_cast<size_t>(n_) * (static_cast<size_t>(d_) * d_ + d_) * 4;
+    const size_t img = static_cast<size_t>(n_) * img_f() * 4;
     if (kind == SP_OPT_ADAMW) {
         if (!host_m_) CUDA_OK(cudaHostAlloc(&host_m_, img, cudaHostAllocPortable));
         if (!host_v_) CUDA_OK(cudaHostAlloc(&host_v_, img, cudaHostAllocPortable));
@@ -1503,6 +1590,12 @@ void Executor::read_optimizer_state(int index, float* mW, float* mb, float* vW, 
     if (!adamw()) throw Error(SP_ERR_STATE, "read_optimizer_state: the optimizer has no state (SGD)");
     flush_writebacks();
     require_full_host(index, "read_optimizer_state");
+    if (blk_) {  // a block's state is flat like its image: mW, vW receive all of it
+        const size_t off = static_cast<size_t>(index) * img_f();
+        if (mW) std::memcpy(mW, host_m_ + off, img_f() * 4);
+        if (vW) std::memcpy(vW, host_v_ + off, img_f() * 4);
+        return;
+    }
     const size_t dd = static_cast<size_t>(d_) * d_, off = static_cast<size_t>(index) * (dd + d_);
     if (mW) std::memcpy(mW, host_m_ + off, dd * 4);
     if (mb) std::memcpy(mb, host_m_ + off + dd, static_cast<size_t>(d_) * 4);
@@ -1521,7 +1614,7 @@ void Executor::dp_sync() {
     if (!comm_) throw Error(SP_ERR_STATE, "dp_sync: no communicator");
     CUDA_OK(cudaSetDevice(cfg_.device));
     for (auto s : {s_h2d_, s_comp_, s_d2h_, s_upd_}) CUDA_OK(cudaStreamSynchronize(s));
-    const size_t img = layer_bytes(), dd = static_cast<size_t>(d_) * d_;
+    const size_t img = layer_bytes();
     size_t lo = 0, hi = 0;
     shard_range(shardA_, img, lo, hi);
     uint8_t* stage = slot_ptr(0);
@@ -1535,7 +1628,7 @@ void Executor::dp_sync() {
         // shared master (share_host_master) already holds every rank's shard: a barrier below.
         for (float* base : {shm_ ? nullptr : host32_, adamw() ? host_m_ : nullptr, adamw() ? host_v_ : nullptr}) {
             if (!base) continue;
-            uint8_t* host = reinterpret_cast<uint8_t*>(base + static_cast<size_t>(L) * (dd + d_));
+            uint8_t* host = reinterpret_cast<uint8_t*>(base + static_cast<size_t>(L) * img_f());
             if (hi > lo) CUDA_OK(cudaMemcpyAsync(stage + lo, host + lo, hi - lo, cudaMemcpyHostToDevice, s_upd_));
             NCCL_OK(nccl().AllGather(stage + shardA_ * static_cast<size_t>(rank_), stage, shardA_,
                                      ncclUint8, comm_, s_upd_));

@@ -5,6 +5,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <functional>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -12,6 +13,7 @@
 #include <vector>
 
 #include "../../include/superpipe.h"
+#include "block.hpp"
 #include "kernels.hpp"
 #include "plan.hpp"
 
@@ -28,7 +30,7 @@ enum SlotFormat : int { kFmtExactF32 = 0, kFmtBf16Train = 1, kFmtBf16Infer = 2 }
 
 class Executor {
 public:
-    explicit Executor(const sp_config& cfg);
+    explicit Executor(const sp_config& cfg, const sp_block_desc* block = nullptr);
     ~Executor();
 
     void register_layer(int index, const float* W, const float* b, int activation, int frozen);
@@ -36,6 +38,11 @@ public:
     float train_step(const float* x, const float* target, int64_t rows, float lr,
                      bool device_io);
     void read_layer(int index, float* W, float* b);
+    // named-shape layers (transformer blocks): one flat fp32 image per layer
+    void register_block(int index, const float* params, int frozen);
+    void read_block(int index, float* params);
+    bool is_block() const { return blk_; }
+    void debug_read_grad(int index, float* out);
     void digest_train(float loss, char out[17]);
     void set_trace(int level) { cfg_.trace = level; }
     void set_item_batching(bool on) { item_batching_ = on; }
@@ -58,9 +65,13 @@ public:
     std::string error;
 
 private:
-    // layout helpers
-    uint64_t layer_bytes() const { return (static_cast<uint64_t>(d_) * d_ + d_) * 4; }
-    uint64_t wire16_bytes() const { return static_cast<uint64_t>(d_) * d_ * 2 + d_ * 4ull; }
+    // layout helpers: a layer's fp32 image is [W | b] (dense) or the block image (block.hpp)
+    size_t img_f() const { return blk_ ? static_cast<size_t>(lay_.n_floats) : static_cast<size_t>(d_) * d_ + d_; }
+    uint64_t layer_bytes() const { return static_cast<uint64_t>(img_f()) * 4; }
+    uint64_t wire16_bytes() const {
+        return blk_ ? lay_.wire_bytes : static_cast<uint64_t>(d_) * d_ * 2 + d_ * 4ull;
+    }
+    size_t act_elt() const { return (blk_ || !bf16_) ? 4 : 2; }  // saved layer-input element
     uint8_t* slot_ptr(int s) const { return slots_dev_ + static_cast<size_t>(s) * slot_bytes_; }
     float* slot_w32(int s) const { return reinterpret_cast<float*>(slot_ptr(s)); }
     float* slot_m32(int s) const { return reinterpret_cast<float*>(slot_ptr(s) + off_m_); }  // AdamW
@@ -92,6 +103,8 @@ private:
         uint64_t kernels = 0, h2d_bytes = 0, d2h_bytes = 0;
         size_t gemm_count = 0;
         double gemm_flops = 0.0;
+        uint64_t attn_launches = 0;
+        double attn_flops = 0.0;
     };
 
     void layout_slots(int world);
@@ -113,10 +126,46 @@ private:
     void update_op(const Op& op, float lr);
     void collect_stats(const Plan& plan, int n_items, bool train);
     void gemm(const struct GemmProblem& g, cudaStream_t st);
+    // transformer blocks (block_exec.cpp)
+    struct BlockActs {  // one layer's forward intermediates (saved for its backward)
+        void *xn1 = nullptr, *qkv = nullptr, *o = nullptr, *xn2 = nullptr, *h = nullptr, *g = nullptr;
+        float *st1 = nullptr, *st2 = nullptr, *lse = nullptr, *xmid = nullptr;
+    };
+    struct WirePtrs {  // bf16 matrices + fp32 vectors of one layer image in wire layout
+        const void *wqkv = nullptr, *wo = nullptr, *w1 = nullptr, *w2 = nullptr;
+        const float *ln1_g = nullptr, *ln1_b = nullptr, *bqkv = nullptr, *bo = nullptr, *ln2_g = nullptr,
+                    *ln2_b = nullptr, *b1 = nullptr, *b2 = nullptr;
+    };
+    WirePtrs wire_ptrs(const uint8_t* wire) const;
+    void block_alloc(int64_t R, int items, bool train, const std::function<void*(size_t)>& alloc);
+    void block_convert(int slot, cudaStream_t st);
+    void block_forward_layer(const WirePtrs& w, const float* x, const BlockActs& a, float* y, int64_t rows,
+                             bool train, cudaStream_t st);
+    void block_backward_layer(int L, const WirePtrs& w, const float* x, const BlockActs& a, int64_t rows,
+                              cudaStream_t st);
+    void block_compute(const Op& op, bool train, int64_t rows, int fmt);
+    void block_loss(int64_t rows);
+    void block_dw(const void* act, int M, const void* grad, int N, int64_t rows, float* out, cudaStream_t st);
+    void block_colsum(const void* x, int64_t rows, int N, float* out, cudaStream_t st);
+    void attention(bool backward, const BlockActs& a, const void* dout, void* dqkv, int64_t rows, cudaStream_t st);
     cudaStream_t stream_of(OpKind k) const;
 
     sp_config cfg_;
     int n_ = 0, d_ = 0;
+    bool blk_ = false;  // named-shape transformer layers (block.hpp) instead of dense blocks
+    BlockLayout lay_;
+    // block-mode device buffers
+    std::vector<float*> bx_;            // training: residual stream x_0..x_n (fp32; x_n = yout_)
+    std::vector<BlockActs> bsv_;        // training: per-layer saved intermediates (no offload)
+    BlockActs bscr_;                    // inference / offload recompute: one scratch set
+    float *bdxn_ = nullptr, *bdmid_ = nullptr, *bdelta_ = nullptr, *bws_ = nullptr, *bcol_ = nullptr;
+    void *bdmid16_ = nullptr, *bdbig_ = nullptr, *bdo_ = nullptr;
+    float* bdres_[2] = {nullptr, nullptr};
+    void* bdres16_[2] = {nullptr, nullptr};
+    float* bgimg_[2] = {nullptr, nullptr};  // per-layer gradient images (ping-pong)
+    size_t bws_floats_ = 0;
+    uint64_t attn_launches_ = 0;
+    double attn_flops_ = 0.0;
     bool bf16_ = false;  // bf16 tensor-core path (bf16 operands / activations)
     bool tf32_ = false;  // tf32 tensor-core path (fp32 operands / activations, kind::tf32)
     bool tc_ = false;    // either tensor-core path (split-K partials, masks, fused loss)
@@ -265,6 +314,8 @@ private:
         h2d_bytes_ = d2h_bytes_ = 0;
         gemm_count_ = 0;
         gemm_flops_ = 0.0;
+        attn_launches_ = 0;
+        attn_flops_ = 0.0;
     }
 };
 

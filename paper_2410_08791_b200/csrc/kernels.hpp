@@ -32,8 +32,16 @@ enum GemmEpilogue : int {
     EPI_GATE_BF16 = 2,      // out(bf16) = (relu && gate <= 0) ? 0 : acc
     EPI_F32 = 3,            // out(f32)  = acc  (split-K partial at out + split*split_stride)
     EPI_SGD_F32 = 4,        // out(f32) -= lr * acc  (fused SGD on the fp32 master; splits == 1)
-    EPI_GATE_F32 = 5        // out(f32)  = (relu && gate <= 0) ? 0 : acc  (tf32 path; fp32 gate)
+    EPI_GATE_F32 = 5,       // out(f32)  = (relu && gate <= 0) ? 0 : acc  (tf32 path; fp32 gate)
+    // transformer blocks (named-shape layers)
+    EPI_RESID_F32 = 6,      // out(f32)  = acc + bias + gate(f32 residual [M][ldg]); bias optional
+    EPI_GELU_BF16 = 7,      // out(bf16) = gelu(acc + bias); aux(bf16) = acc + bias (pre-activation)
+    EPI_GELU_GATE_BF16 = 8, // out(bf16) = acc * gelu'(gate)  (gate = the saved pre-activation, bf16)
+    EPI_SWIGLU_BF16 = 9     // out(bf16)[M][N/2] = silu(acc_g) * acc_u over 32-column chunk pairs
+                            // (g = chunk 2c, u = chunk 2c+1 of each tile); aux(bf16)[M][N] = acc
 };
+// EPI_GELU_BF16 / EPI_GELU_GATE_BF16 activation (GemmProblem::act)
+enum GeluKind : int { GELU_TANH = 0, GELU_ERF = 1 };
 
 struct GemmProblem {
     // C[M,N] = A[M,K] * B[K,N]; A given K-major ([M][lda]) or M-major ([K][lda]);
@@ -67,6 +75,11 @@ struct GemmProblem {
     // (kind::f16). Epilogues: EPI_BIAS_ACT_F32 (with mask_out), EPI_GATE_F32 (gate: fp32
     // tensor or gate_mask), EPI_F32, EPI_SGD_F32.
     bool tf32 = false;
+    // EPI_GELU_BF16 / EPI_SWIGLU_BF16: second output (pre-activation), bf16 [M][ldaux]; may be
+    // null for SWIGLU (inference).
+    void* aux = nullptr;
+    int ldaux = 0;
+    int act = GELU_TANH;  // GeluKind for the GELU epilogues
 };
 
 struct GemmChoice {
@@ -121,9 +134,50 @@ void scale_inplace(float* x, int64_t count, float s, cudaStream_t st);
 struct AdamwScalars {
     float decay, omb1, b2, omb2, bc2_sqrt, eps, neg_step, pad;
 };
+// Up to 16 fp32 regions converted to bf16 (to_bf16) or copied as fp32, one launch: a layer
+// image's matrices -> the bf16 operand copy, its vectors -> fp32 next to them (wire layout).
+struct ConvertRegions {
+    int n = 0;
+    const float* src[16];
+    void* dst[16];
+    int64_t count[16];  // elements, multiple of 4
+    int to_bf16[16];
+};
+void convert_regions(const ConvertRegions& r, cudaStream_t st);
 // n (<= 3) device-to-device copies of `bytes` each (multiple of 4, 4-byte aligned) on the SMs.
 void copy_regions(void* const* dst, const void* const* src, int n, int64_t bytes, cudaStream_t st);
 void adamw_reduce(float* w, float* m, float* v, const float* parts, int nparts, int64_t stride,
                   int64_t count, const AdamwScalars* scalars, cudaStream_t st);
+
+// ---- named-shape transformer blocks (kernels_attn.cu, kernels_block.cu) ------------------
+// Attention over the packed projections qkv[T][(H + 2 Hkv) hd] (bf16, token-major; q heads,
+// then k heads, then v heads), sequences of seq_len consecutive tokens. head_dim 64, 80 or 128.
+struct AttnProblem {
+    int64_t tokens = 0;
+    int seq_len = 0, n_heads = 0, n_kv_heads = 0, head_dim = 0;
+    int causal = 1;
+    const void* qkv = nullptr;   // [T][(H + 2 Hkv) hd] bf16
+    void* o = nullptr;           // [T][H hd] bf16 (forward output; backward input)
+    float* lse = nullptr;        // [T / seq_len][H][seq_len] fp32, log2 units of scaled scores
+    const void* dout = nullptr;  // backward: dO [T][H hd] bf16
+    float* delta = nullptr;      // backward scratch [T / seq_len][H][seq_len]
+    void* dqkv = nullptr;        // backward output, same layout as qkv
+};
+cudaError_t attention_forward(const AttnProblem& a, cudaStream_t st);
+cudaError_t attention_backward(const AttnProblem& a, cudaStream_t st);
+
+// LayerNorm (gamma, beta; rms = 0) or RMSNorm (gamma only; rms = 1) of fp32 rows [T][d]:
+// y (bf16) = norm(x) * gamma (+ beta); stats[T][2] = {mean, rstd} (RMSNorm: {0, rstd}).
+void norm_forward(const float* x, const float* gamma, const float* beta, int rms, float eps,
+                  int64_t rows, int d, void* y, float* stats, cudaStream_t st);
+// Backward of the norm given dy (fp32 [T][d], the gradient of its output):
+//   dx = rstd (dy*gamma - mean(dy*gamma) - xhat mean(dy*gamma*xhat))   (RMSNorm: no mean term)
+//   dres_out (fp32) = dres_in + dx and dres_out16 (bf16) = the same rounded, when non-null.
+// Parameter gradients: per 128-row chunk partials part[chunk][2][d] = {sum dy*xhat, sum dy}
+// (reduce with reduce_partials over chunks; fixed decomposition). Returns the chunk count.
+int norm_backward(const float* dy, const float* x, const float* stats, const float* gamma, int rms,
+                  int64_t rows, int d, const float* dres_in, float* dres_out, void* dres_out16,
+                  float* part, cudaStream_t st);
+int norm_param_chunks(int64_t rows);
 
 }  // namespace sp

@@ -1,0 +1,197 @@
+// kernels_block.cu — normalisation kernels of the named-shape transformer blocks (sm_100a).
+//
+// LayerNorm / RMSNorm forward (fp32 residual stream in, bf16 GEMM operand out) and backward
+// (fused with the residual-gradient add and the bf16 copy the next dW / dX GEMMs read), plus
+// the fixed-decomposition column partials of the norm's parameter gradients. One warp per row,
+// 128-bit loads; every reduction has a fixed order, so results depend only on the shapes.
+#include <cuda_bf16.h>
+
+#include "kernels.hpp"
+#include "launch.cuh"
+
+namespace sp {
+namespace {
+
+constexpr int kRowsPerBlock = 8;  // one warp per row
+constexpr int kChunkRows = 128;   // parameter-gradient partials: rows per chunk
+constexpr int kRowLanes = 8;
+
+__device__ __forceinline__ float warp_allsum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+template <bool RMS>
+__global__ void __launch_bounds__(32 * kRowsPerBlock) norm_fwd_kernel(const float* __restrict__ x,
+                                                                      const float* __restrict__ gamma,
+                                                                      const float* __restrict__ beta, float eps,
+                                                                      int64_t rows, int d,
+                                                                      __nv_bfloat16* __restrict__ y,
+                                                                      float* __restrict__ stats) {
+    const int lane = threadIdx.x & 31;
+    const int64_t r = static_cast<int64_t>(blockIdx.x) * kRowsPerBlock + (threadIdx.x >> 5);
+    if (r >= rows) return;
+    const float4* xr = reinterpret_cast<const float4*>(x + r * d);
+    const int n4 = d / 4;
+    float mean = 0.0f;
+    if (!RMS) {
+        float s = 0.0f;
+        for (int i = lane; i < n4; i += 32) {
+            const float4 v = __ldg(xr + i);
+            s += (v.x + v.y) + (v.z + v.w);
+        }
+        mean = warp_allsum(s) / static_cast<float>(d);
+    }
+    float q = 0.0f;
+    for (int i = lane; i < n4; i += 32) {
+        const float4 v = __ldg(xr + i);
+        const float a = v.x - mean, b = v.y - mean, c = v.z - mean, e = v.w - mean;
+        q += (a * a + b * b) + (c * c + e * e);
+    }
+    const float rstd = rsqrtf(warp_allsum(q) / static_cast<float>(d) + eps);
+    const float4* g4 = reinterpret_cast<const float4*>(gamma);
+    const float4* b4 = reinterpret_cast<const float4*>(beta);
+    uint2* yr = reinterpret_cast<uint2*>(y + r * d);
+    for (int i = lane; i < n4; i += 32) {
+        const float4 v = __ldg(xr + i);
+        const float4 g = __ldg(g4 + i);
+        float4 o;
+        o.x = (v.x - mean) * rstd * g.x;
+        o.y = (v.y - mean) * rstd * g.y;
+        o.z = (v.z - mean) * rstd * g.z;
+        o.w = (v.w - mean) * rstd * g.w;
+        if (!RMS) {
+            const float4 bb = __ldg(b4 + i);
+            o.x += bb.x, o.y += bb.y, o.z += bb.z, o.w += bb.w;
+        }
+        __nv_bfloat162 lo = __floats2bfloat162_rn(o.x, o.y), hi = __floats2bfloat162_rn(o.z, o.w);
+        uint2 pk;
+        pk.x = *reinterpret_cast<uint32_t*>(&lo);
+        pk.y = *reinterpret_cast<uint32_t*>(&hi);
+        yr[i] = pk;
+    }
+    if (lane == 0) {
+        stats[2 * r] = mean;
+        stats[2 * r + 1] = rstd;
+    }
+}
+
+template <bool RMS>
+__global__ void __launch_bounds__(32 * kRowsPerBlock) norm_bwd_kernel(
+    const float* __restrict__ dy, const float* __restrict__ x, const float* __restrict__ stats,
+    const float* __restrict__ gamma, int64_t rows, int d, const float* __restrict__ dres_in,
+    float* __restrict__ dres_out, __nv_bfloat16* __restrict__ dres_out16) {
+    const int lane = threadIdx.x & 31;
+    const int64_t r = static_cast<int64_t>(blockIdx.x) * kRowsPerBlock + (threadIdx.x >> 5);
+    if (r >= rows) return;
+    const float mean = stats[2 * r], rstd = stats[2 * r + 1];
+    const float4* xr = reinterpret_cast<const float4*>(x + r * d);
+    const float4* dr = reinterpret_cast<const float4*>(dy + r * d);
+    const float4* g4 = reinterpret_cast<const float4*>(gamma);
+    const int n4 = d / 4;
+    float sg = 0.0f, sgx = 0.0f;  // sum of dy*gamma, sum of dy*gamma*xhat
+    for (int i = lane; i < n4; i += 32) {
+        const float4 v = __ldg(xr + i), e = __ldg(dr + i), g = __ldg(g4 + i);
+        const float g0 = e.x * g.x, g1 = e.y * g.y, g2 = e.z * g.z, g3 = e.w * g.w;
+        sg += (g0 + g1) + (g2 + g3);
+        sgx += (g0 * (v.x - mean) + g1 * (v.y - mean)) + (g2 * (v.z - mean) + g3 * (v.w - mean));
+    }
+    const float inv_d = 1.0f / static_cast<float>(d);
+    const float c_mean = RMS ? 0.0f : warp_allsum(sg) * inv_d;
+    const float c_x = warp_allsum(sgx) * rstd * inv_d;  // mean(dy*gamma*xhat)
+    const float4* ri = reinterpret_cast<const float4*>(dres_in + r * d);
+    float4* ro = reinterpret_cast<float4*>(dres_out + r * d);
+    uint2* r16 = dres_out16 ? reinterpret_cast<uint2*>(dres_out16 + r * d) : nullptr;
+    for (int i = lane; i < n4; i += 32) {
+        const float4 v = __ldg(xr + i), e = __ldg(dr + i), g = __ldg(g4 + i);
+        const float4 base = __ldg(ri + i);
+        float4 o;
+        o.x = base.x + rstd * (e.x * g.x - c_mean - (v.x - mean) * rstd * c_x);
+        o.y = base.y + rstd * (e.y * g.y - c_mean - (v.y - mean) * rstd * c_x);
+        o.z = base.z + rstd * (e.z * g.z - c_mean - (v.z - mean) * rstd * c_x);
+        o.w = base.w + rstd * (e.w * g.w - c_mean - (v.w - mean) * rstd * c_x);
+        ro[i] = o;
+        if (r16) {
+            __nv_bfloat162 lo = __floats2bfloat162_rn(o.x, o.y), hi = __floats2bfloat162_rn(o.z, o.w);
+            uint2 pk;
+            pk.x = *reinterpret_cast<uint32_t*>(&lo);
+            pk.y = *reinterpret_cast<uint32_t*>(&hi);
+            r16[i] = pk;
+        }
+    }
+}
+
+// part[chunk][0][j] = sum_r dy[r][j] xhat[r][j], part[chunk][1][j] = sum_r dy[r][j] over the
+// chunk's 128 rows. Block = 32 threads x 4 columns, 8 row lanes; lanes combined in a fixed
+// order through shared memory.
+__global__ void __launch_bounds__(32 * kRowLanes) norm_param_kernel(const float* __restrict__ dy,
+                                                                    const float* __restrict__ x,
+                                                                    const float* __restrict__ stats,
+                                                                    int64_t rows, int d, int rms,
+                                                                    float* __restrict__ part) {
+    __shared__ float4 red[2][kRowLanes][32];
+    const int c4 = blockIdx.x * 32 + threadIdx.x;  // float4 column group
+    const int lane_r = threadIdx.y;
+    const int64_t r0 = static_cast<int64_t>(blockIdx.y) * kChunkRows;
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (4 * c4 < d) {
+        for (int i = 0; i < kChunkRows / kRowLanes; ++i) {
+            const int64_t r = r0 + lane_r + static_cast<int64_t>(i) * kRowLanes;
+            if (r >= rows) break;
+            const float mean = rms ? 0.0f : stats[2 * r], rstd = stats[2 * r + 1];
+            const float4 e = __ldg(reinterpret_cast<const float4*>(dy + r * d) + c4);
+            const float4 v = __ldg(reinterpret_cast<const float4*>(x + r * d) + c4);
+            a.x += e.x * ((v.x - mean) * rstd);
+            a.y += e.y * ((v.y - mean) * rstd);
+            a.z += e.z * ((v.z - mean) * rstd);
+            a.w += e.w * ((v.w - mean) * rstd);
+            b.x += e.x, b.y += e.y, b.z += e.z, b.w += e.w;
+        }
+    }
+    red[0][lane_r][threadIdx.x] = a;
+    red[1][lane_r][threadIdx.x] = b;
+    __syncthreads();
+    if (lane_r < 2 && 4 * c4 < d) {
+        float4 s = red[lane_r][0][threadIdx.x];
+        for (int l = 1; l < kRowLanes; ++l) {
+            const float4 v = red[lane_r][l][threadIdx.x];
+            s.x += v.x, s.y += v.y, s.z += v.z, s.w += v.w;
+        }
+        reinterpret_cast<float4*>(part + (static_cast<int64_t>(blockIdx.y) * 2 + lane_r) * d)[c4] = s;
+    }
+}
+
+}  // namespace
+
+int norm_param_chunks(int64_t rows) { return static_cast<int>((rows + kChunkRows - 1) / kChunkRows); }
+
+void norm_forward(const float* x, const float* gamma, const float* beta, int rms, float eps, int64_t rows, int d,
+                  void* y, float* stats, cudaStream_t st) {
+    const dim3 grid(static_cast<unsigned>((rows + kRowsPerBlock - 1) / kRowsPerBlock));
+    auto* yo = static_cast<__nv_bfloat16*>(y);
+    if (rms) launch_kernel(norm_fwd_kernel<true>, grid, dim3(32 * kRowsPerBlock), 0, st, x, gamma, beta, eps, rows, d, yo, stats);
+    else launch_kernel(norm_fwd_kernel<false>, grid, dim3(32 * kRowsPerBlock), 0, st, x, gamma, beta, eps, rows, d, yo, stats);
+}
+
+int norm_backward(const float* dy, const float* x, const float* stats, const float* gamma, int rms, int64_t rows,
+                  int d, const float* dres_in, float* dres_out, void* dres_out16, float* part, cudaStream_t st) {
+    if (dres_out) {
+        const dim3 grid(static_cast<unsigned>((rows + kRowsPerBlock - 1) / kRowsPerBlock));
+        auto* o16 = static_cast<__nv_bfloat16*>(dres_out16);
+        if (rms)
+            launch_kernel(norm_bwd_kernel<true>, grid, dim3(32 * kRowsPerBlock), 0, st, dy, x, stats, gamma, rows, d,
+                          dres_in, dres_out, o16);
+        else
+            launch_kernel(norm_bwd_kernel<false>, grid, dim3(32 * kRowsPerBlock), 0, st, dy, x, stats, gamma, rows, d,
+                          dres_in, dres_out, o16);
+    }
+    const int chunks = norm_param_chunks(rows);
+    if (part) {
+        const dim3 grid(static_cast<unsigned>((d / 4 + 31) / 32), static_cast<unsigned>(chunks));
+        launch_kernel(norm_param_kernel, grid, dim3(32, kRowLanes), 0, st, dy, x, stats, rows, d, rms, part);
+    }
+    return chunks;
+}
+
+}  // namespace sp

@@ -422,4 +422,35 @@ void scale_inplace(float* x, int64_t count, float s, cudaStream_t st) {
     launch_kernel(scale_kernel, dim3(grid_for(count)), dim3(kThreads), 0, st, x, count, s);
 }
 
+namespace {
+__global__ void convert_regions_kernel(ConvertRegions r) {
+    const int i = blockIdx.y;
+    const int64_t n4 = r.count[i] / 4;
+    const float4* src = reinterpret_cast<const float4*>(r.src[i]);
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    if (r.to_bf16[i]) {
+        uint2* dst = static_cast<uint2*>(r.dst[i]);
+        for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n4; e += stride) {
+            const float4 v = src[e];
+            __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
+            uint2 pk;
+            pk.x = *reinterpret_cast<uint32_t*>(&lo);
+            pk.y = *reinterpret_cast<uint32_t*>(&hi);
+            dst[e] = pk;
+        }
+    } else {
+        float4* dst = static_cast<float4*>(r.dst[i]);
+        for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n4; e += stride) dst[e] = src[e];
+    }
+}
+}  // namespace
+
+void convert_regions(const ConvertRegions& r, cudaStream_t st) {
+    if (r.n <= 0) return;
+    int64_t most = 0;
+    for (int i = 0; i < r.n; ++i) most = most > r.count[i] ? most : r.count[i];
+    const unsigned bx = static_cast<unsigned>(grid_for(most / 4 + 1));
+    launch_kernel(convert_regions_kernel, dim3(bx, static_cast<unsigned>(r.n)), dim3(kThreads), 0, st, r);
+}
+
 }  // namespace sp

@@ -95,6 +95,9 @@ struct Params {
     int narrow;  // 2-CTA: the ragged last N tile is computed with an MMA of N = BN/2
     uint32_t* mask_out;         // EPI_BIAS_ACT_BF16: ReLU bit mask of the output (or nullptr)
     const uint32_t* gate_mask;  // EPI_GATE_BF16: gate from a bit mask (or nullptr: gate tensor)
+    void* aux;                  // EPI_GELU_BF16 / EPI_SWIGLU_BF16: pre-activation output
+    int ldaux;
+    int act;                    // GeluKind
 };
 
 // ---------------------------------------------------------------------------------------
@@ -240,10 +243,15 @@ struct EpiSmem {
     static constexpr int BASE = EPI & (EPI_TMA - 1);
     static constexpr bool TMA = (EPI & EPI_TMA) != 0 && BASE != EPI_SGD_F32;
     static constexpr bool TMA_OUT = TMA;
-    static constexpr int OUT_ELT = (BASE == EPI_BIAS_ACT_BF16 || BASE == EPI_GATE_BF16) ? 2 : 4;
+    static constexpr int OUT_ELT = (BASE == EPI_BIAS_ACT_BF16 || BASE == EPI_GATE_BF16 || BASE == EPI_GELU_BF16 ||
+                                    BASE == EPI_GELU_GATE_BF16 || BASE == EPI_SWIGLU_BF16)
+                                       ? 2
+                                       : 4;
     static constexpr int OUT_BUF = 32 * 32 * OUT_ELT;  // one warp's 32 x 32 chunk
-    static constexpr bool IS_GATE = BASE == EPI_GATE_BF16 || BASE == EPI_GATE_F32;
-    static constexpr int GATE_ELT = BASE == EPI_GATE_F32 ? 4 : 2;
+    // epilogues that read a [M][ldg] tensor tile next to the accumulator (ReLU / GELU gate, residual)
+    static constexpr bool IS_GATE = BASE == EPI_GATE_BF16 || BASE == EPI_GATE_F32 || BASE == EPI_RESID_F32 ||
+                                    BASE == EPI_GELU_GATE_BF16;
+    static constexpr int GATE_ELT = (BASE == EPI_GATE_F32 || BASE == EPI_RESID_F32) ? 4 : 2;
     static constexpr bool GATE = TMA && IS_GATE;
     static constexpr int GATE_BUF = 32 * 32 * GATE_ELT;
     static constexpr int OUT_BYTES = TMA_OUT ? 4 * 2 * OUT_BUF : 0;  // 4 warps x 2 buffers
@@ -282,6 +290,21 @@ __device__ __forceinline__ uint32_t swz(int r, int i) {
                            : static_cast<uint32_t>(r * 128 + ((i ^ (r & 7)) << 4));
 }
 
+// GELU (tanh approximation, GPT-2's gelu_new; or the exact erf form, ViT's nn.GELU) and its
+// derivative, in fp32.
+__device__ __forceinline__ float gelu_f(float x, int kind) {
+    if (kind == GELU_ERF) return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f));
+    const float u = 0.79788456080286536f * (x + 0.044715f * x * x * x);
+    return 0.5f * x * (1.0f + tanhf(u));
+}
+__device__ __forceinline__ float gelu_grad_f(float x, int kind) {
+    if (kind == GELU_ERF)
+        return 0.5f * (1.0f + erff(x * 0.70710678118654752f)) + x * 0.39894228040143268f * __expf(-0.5f * x * x);
+    const float u = 0.79788456080286536f * (x + 0.044715f * x * x * x);
+    const float t = tanhf(u);
+    return 0.5f * (1.0f + t) + 0.5f * x * (1.0f - t * t) * 0.79788456080286536f * (1.0f + 0.134145f * x * x);
+}
+
 template <int BN, int EPI>
 struct TileEpilogue {
     using E = EpiSmem<EPI>;
@@ -310,13 +333,133 @@ struct TileEpilogue {
         ++gate_issued;
     }
     static constexpr bool kMaskGate = E::IS_GATE;
+    // The gate / residual tensor is read for this tile: always for the residual and GELU-gate
+    // epilogues, for the ReLU gates only when gating from the tensor (not a bit mask).
+    __device__ __forceinline__ static bool tensor_gate(const Params& p) {
+        return (BASE == EPI_RESID_F32 || BASE == EPI_GELU_GATE_BF16) ? true : (p.relu && !p.gate_mask);
+    }
     __device__ __forceinline__ uint32_t mask_word(const Params& p, int row, int col0) const {
         return row < p.M && col0 < p.N ? __ldg(p.gate_mask + static_cast<long long>(col0 / 32) * p.M + row) : 0u;
     }
     // before the accumulator wait: the gate of the tile's first chunk starts loading
     __device__ __forceinline__ void begin_tile(const CUtensorMap* tmG, const Params& p, int row0, int n0) {
-        if (E::GATE && p.relu && !p.gate_mask) gate_issue(tmG, row0, n0);
+        if (E::GATE && tensor_gate(p)) gate_issue(tmG, row0, n0);
         if (kMaskGate && p.relu && p.gate_mask) mask_next = mask_word(p, row0 + lane, n0);
+    }
+
+    // This lane's row of the chunk's gate tensor as fp32: from the TMA-staged smem buffer, or
+    // (direct kind) from global memory; false when the row is past M (direct kind only).
+    __device__ __forceinline__ bool gate_f32(const Params& p, int row, int col0, float (&g)[32]) {
+        if (E::GATE) {
+            const int b = gate_used & 1;
+            mbar_wait(&gbar[b], (gate_used >> 1) & 1);
+            ++gate_used;
+            const uint8_t* gb = gbuf + b * E::GATE_BUF;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const float4 f = *reinterpret_cast<const float4*>(gb + swz<128>(lane, i));
+                g[4 * i] = f.x, g[4 * i + 1] = f.y, g[4 * i + 2] = f.z, g[4 * i + 3] = f.w;
+            }
+            return true;
+        }
+        if (row >= p.M) return false;
+        const float4* gp = reinterpret_cast<const float4*>(static_cast<const float*>(p.gate) +
+                                                           static_cast<long long>(row) * p.ldg + col0);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const float4 f = __ldg(gp + i);
+            g[4 * i] = f.x, g[4 * i + 1] = f.y, g[4 * i + 2] = f.z, g[4 * i + 3] = f.w;
+        }
+        return true;
+    }
+    __device__ __forceinline__ bool gate_bf16(const Params& p, int row, int col0, float (&g)[32]) {
+        uint4 gv[4];
+        if (E::GATE) {
+            const int b = gate_used & 1;
+            mbar_wait(&gbar[b], (gate_used >> 1) & 1);
+            ++gate_used;
+            const uint8_t* gb = gbuf + b * E::GATE_BUF;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) gv[i] = *reinterpret_cast<const uint4*>(gb + swz<64>(lane, i));
+        } else {
+            if (row >= p.M) return false;
+            const uint4* gp = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(p.gate) +
+                                                             static_cast<long long>(row) * p.ldg + col0);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) gv[i] = __ldg(gp + i);
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const uint32_t gw[4] = {gv[i].x, gv[i].y, gv[i].z, gv[i].w};
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                const float2 gf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&gw[h]));
+                g[8 * i + 2 * h] = gf.x;
+                g[8 * i + 2 * h + 1] = gf.y;
+            }
+        }
+        return true;
+    }
+    __device__ __forceinline__ static void add_bias(const Params& p, int col0, float (&v)[32]) {
+        if (!p.bias) return;
+        const float4* bp = reinterpret_cast<const float4*>(p.bias + col0);  // one address per warp
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const float4 bv = __ldg(bp + i);
+            v[4 * i + 0] += bv.x;
+            v[4 * i + 1] += bv.y;
+            v[4 * i + 2] += bv.z;
+            v[4 * i + 3] += bv.w;
+        }
+    }
+    // 32 bf16 values of this lane's row straight to global memory (the pre-activation side
+    // output: four 16-byte stores covering two full 32-byte sectors each).
+    __device__ __forceinline__ static void store_row_bf16(void* base, int ld, int row, int col0, const uint32_t (&pk)[16]) {
+        uint4* op = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(base) + static_cast<long long>(row) * ld + col0);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) op[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+    }
+
+    // Stores the chunk's final values: packed bf16 (pk) or fp32 (v), per-lane rows or staged
+    // through shared memory and one TMA store (col0 = the output column of the chunk).
+    __device__ __forceinline__ void store_out(const CUtensorMap* tmO, const Params& p, const float (&v)[32],
+                                              const uint32_t (&pk)[16], int row0, int col0, int split) {
+        const int row = row0 + lane;
+        if (!E::TMA_OUT) {  // per-lane row stores straight to global
+            if (row >= p.M) return;
+            if (E::OUT_ELT == 2) {
+                store_row_bf16(p.out, p.ldo, row, col0, pk);
+            } else {
+                float4* op = reinterpret_cast<float4*>(static_cast<float*>(p.out) +
+                                                       (BASE == EPI_F32 ? split * p.split_stride : 0LL) +
+                                                       static_cast<long long>(row) * p.ldo + col0);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) op[i] = make_float4(v[4 * i + 0], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+            }
+        } else {  // swizzled smem staging -> one TMA store per 32 x 32 chunk
+            uint8_t* ob = obuf + (out_n & 1) * E::OUT_BUF;
+            if (lane == 0) bulk_wait_read<1>();  // the store that last read this buffer is done
+            __syncwarp();
+            if (E::OUT_ELT == 2) {
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    *reinterpret_cast<uint4*>(ob + swz<64>(lane, i)) =
+                        make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+            } else {
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                    *reinterpret_cast<float4*>(ob + swz<128>(lane, i)) =
+                        make_float4(v[4 * i + 0], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+            }
+            fence_proxy_async_smem();  // generic-proxy writes -> visible to the TMA (async proxy)
+            __syncwarp();
+            if (lane == 0) {
+                if (BASE == EPI_F32) tma_store_3d(tmO, ob, col0, row0, split);
+                else tma_store_2d(tmO, ob, col0, row0);
+                bulk_commit();
+            }
+            ++out_n;
+        }
     }
 
     __device__ __forceinline__ void chunk(const CUtensorMap* tmO, const Params& p, const uint32_t (&r)[32],
@@ -326,73 +469,49 @@ struct TileEpilogue {
         for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
         const int row = row0 + lane;
         if (BASE == EPI_BIAS_ACT_BF16 || BASE == EPI_BIAS_ACT_F32) {
-            const float4* bp = reinterpret_cast<const float4*>(p.bias + col0);  // one address per warp
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const float4 bv = __ldg(bp + i);
-                v[4 * i + 0] += bv.x;
-                v[4 * i + 1] += bv.y;
-                v[4 * i + 2] += bv.z;
-                v[4 * i + 3] += bv.w;
-            }
+            add_bias(p, col0, v);
             if (p.relu) {
 #pragma unroll
                 for (int i = 0; i < 32; ++i) v[i] = v[i] < 0.0f ? 0.0f : v[i];
             }
+        }
+        if (BASE == EPI_GELU_BF16) {
+            // pre-activation h = acc + b (bf16 side output for the backward's GELU'), out = gelu(h)
+            add_bias(p, col0, v);
+            uint32_t hk[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) hk[i] = pack_bf16(v[2 * i], v[2 * i + 1]);
+            if (row < p.M && p.aux) store_row_bf16(p.aux, p.ldaux, row, col0, hk);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = gelu_f(v[i], p.act);
         }
         if (E::IS_GATE && p.relu && p.gate_mask != nullptr) {
 #pragma unroll
             for (int i = 0; i < 32; ++i)
                 if (!((gate_bits >> i) & 1u)) v[i] = 0.0f;
         } else if (BASE == EPI_GATE_F32 && p.relu) {  // fp32 gate tensor (tf32 path)
-            float4 gv[8];
-            if (E::GATE) {
-                const int b = gate_used & 1;
-                mbar_wait(&gbar[b], (gate_used >> 1) & 1);
-                ++gate_used;
-                const uint8_t* gb = gbuf + b * E::GATE_BUF;
+            float g[32];
+            if (!gate_f32(p, row, col0, g)) return;
 #pragma unroll
-                for (int i = 0; i < 8; ++i) gv[i] = *reinterpret_cast<const float4*>(gb + swz<128>(lane, i));
-            } else {
-                if (row >= p.M) return;
-                const float4* gp = reinterpret_cast<const float4*>(static_cast<const float*>(p.gate) +
-                                                                   static_cast<long long>(row) * p.ldg + col0);
-#pragma unroll
-                for (int i = 0; i < 8; ++i) gv[i] = __ldg(gp + i);
-            }
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                if (gv[i].x <= 0.0f) v[4 * i + 0] = 0.0f;
-                if (gv[i].y <= 0.0f) v[4 * i + 1] = 0.0f;
-                if (gv[i].z <= 0.0f) v[4 * i + 2] = 0.0f;
-                if (gv[i].w <= 0.0f) v[4 * i + 3] = 0.0f;
-            }
+            for (int i = 0; i < 32; ++i)
+                if (g[i] <= 0.0f) v[i] = 0.0f;
         } else if (BASE == EPI_GATE_BF16 && p.relu) {
-            uint4 gv[4];
-            if (E::GATE) {
-                const int b = gate_used & 1;
-                mbar_wait(&gbar[b], (gate_used >> 1) & 1);
-                ++gate_used;
-                const uint8_t* gb = gbuf + b * E::GATE_BUF;
+            float g[32];
+            if (!gate_bf16(p, row, col0, g)) return;
 #pragma unroll
-                for (int i = 0; i < 4; ++i) gv[i] = *reinterpret_cast<const uint4*>(gb + swz<64>(lane, i));
-            } else {
-                if (row >= p.M) return;
-                const uint4* gp = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(p.gate) +
-                                                                 static_cast<long long>(row) * p.ldg + col0);
+            for (int i = 0; i < 32; ++i)
+                if (g[i] <= 0.0f) v[i] = 0.0f;
+        } else if (BASE == EPI_RESID_F32) {  // out = acc + b + residual (fp32 residual stream)
+            float g[32];
+            add_bias(p, col0, v);
+            if (!gate_f32(p, row, col0, g)) return;
 #pragma unroll
-                for (int i = 0; i < 4; ++i) gv[i] = __ldg(gp + i);
-            }
+            for (int i = 0; i < 32; ++i) v[i] += g[i];
+        } else if (BASE == EPI_GELU_GATE_BF16) {  // dh = dg * gelu'(h)
+            float g[32];
+            if (!gate_bf16(p, row, col0, g)) return;
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const uint32_t gw[4] = {gv[i].x, gv[i].y, gv[i].z, gv[i].w};
-#pragma unroll
-                for (int h = 0; h < 4; ++h) {
-                    const float2 gf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&gw[h]));
-                    if (gf.x <= 0.0f) v[8 * i + 2 * h] = 0.0f;
-                    if (gf.y <= 0.0f) v[8 * i + 2 * h + 1] = 0.0f;
-                }
-            }
+            for (int i = 0; i < 32; ++i) v[i] *= gelu_grad_f(g[i], p.act);
         }
         if (BASE == EPI_SGD_F32) {
             // fused SGD (apply_sgd, model.cpp:150-155): w -= lr * dW, no FMA, in place on the
@@ -432,44 +551,32 @@ struct TileEpilogue {
             for (int i = 0; i < 32; ++i) bits |= ((__float_as_uint(v[i]) & 0x7FFFFFFFu) ? 1u : 0u) << i;
             p.mask_out[static_cast<long long>(col0 / 32) * p.M + row] = bits;
         }
-        if (!E::TMA_OUT) {  // per-lane row stores straight to global
-            if (row >= p.M) return;
-            if (E::OUT_ELT == 2) {
-                uint4* op = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.out) +
-                                                     static_cast<long long>(row) * p.ldo + col0);
+        store_out(tmO, p, v, pk, row0, col0, split);
+    }
+
+    // SwiGLU: chunk 2c holds the gate pre-activations g, chunk 2c+1 the up projections u of the
+    // same 32 hidden units; out[:, n0/2 + 32c ..] = silu(g) * u, aux = both pre-activations.
+    __device__ __forceinline__ void chunk_swiglu(const CUtensorMap* tmO, const Params& p, const uint32_t (&rg)[32],
+                                                 const uint32_t (&ru)[32], int row0, int col0) {
+        const int row = row0 + lane;
+        float v[32];
+        uint32_t pk[16];
+        if (p.aux && row < p.M) {  // col0 = colg / 2 with colg (the gate chunk's column) % 64 == 0
 #pragma unroll
-                for (int i = 0; i < 4; ++i) op[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
-            } else {
-                float4* op = reinterpret_cast<float4*>(static_cast<float*>(p.out) +
-                                                       (BASE == EPI_F32 ? split * p.split_stride : 0LL) +
-                                                       static_cast<long long>(row) * p.ldo + col0);
+            for (int i = 0; i < 16; ++i) pk[i] = pack_bf16(__uint_as_float(rg[2 * i]), __uint_as_float(rg[2 * i + 1]));
+            store_row_bf16(p.aux, p.ldaux, row, 2 * col0, pk);
 #pragma unroll
-                for (int i = 0; i < 8; ++i) op[i] = make_float4(v[4 * i + 0], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-            }
-        } else {  // swizzled smem staging -> one TMA store per 32 x 32 chunk
-            uint8_t* ob = obuf + (out_n & 1) * E::OUT_BUF;
-            if (lane == 0) bulk_wait_read<1>();  // the store that last read this buffer is done
-            __syncwarp();
-            if (E::OUT_ELT == 2) {
-#pragma unroll
-                for (int i = 0; i < 4; ++i)
-                    *reinterpret_cast<uint4*>(ob + swz<64>(lane, i)) =
-                        make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
-            } else {
-#pragma unroll
-                for (int i = 0; i < 8; ++i)
-                    *reinterpret_cast<float4*>(ob + swz<128>(lane, i)) =
-                        make_float4(v[4 * i + 0], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-            }
-            fence_proxy_async_smem();  // generic-proxy writes -> visible to the TMA (async proxy)
-            __syncwarp();
-            if (lane == 0) {
-                if (BASE == EPI_F32) tma_store_3d(tmO, ob, col0, row0, split);
-                else tma_store_2d(tmO, ob, col0, row0);
-                bulk_commit();
-            }
-            ++out_n;
+            for (int i = 0; i < 16; ++i) pk[i] = pack_bf16(__uint_as_float(ru[2 * i]), __uint_as_float(ru[2 * i + 1]));
+            store_row_bf16(p.aux, p.ldaux, row, 2 * col0 + 32, pk);
         }
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+            const float g = __uint_as_float(rg[i]), u = __uint_as_float(ru[i]);
+            v[i] = g / (1.0f + __expf(-g)) * u;
+        }
+#pragma unroll
+        for (int i = 0; i < 16; ++i) pk[i] = pack_bf16(v[2 * i], v[2 * i + 1]);
+        store_out(tmO, p, v, pk, row0, col0, 0);
     }
 
     // One accumulator tile: chunk by chunk out of TMEM; the accumulator stage is released to the
@@ -478,12 +585,26 @@ struct TileEpilogue {
     __device__ __forceinline__ void run(const CUtensorMap* tmO, const CUtensorMap* tmG, const Params& p,
                                         uint32_t tmem_acc, int row0, int n0, int split, Release&& release) {
         uint32_t ra[32];
+        if (BASE == EPI_SWIGLU_BF16) {
+            uint32_t rb[32];
+#pragma unroll 1
+            for (int c = 0; c < CHUNKS / 2; ++c) {
+                tmem_ld32_async(tmem_acc + (2 * c) * 32, ra);
+                tmem_ld_wait(ra);
+                tmem_ld32_async(tmem_acc + (2 * c + 1) * 32, rb);
+                tmem_ld_wait(rb);
+                const int colg = n0 + 2 * c * 32;  // gate column in the GEMM's N
+                if (colg < p.N) chunk_swiglu(tmO, p, ra, rb, row0, colg / 2);
+            }
+            release();
+            return;
+        }
 #pragma unroll 1
         for (int c = 0; c < CHUNKS; ++c) {
             const int col0 = n0 + c * 32;
             tmem_ld32_async(tmem_acc + c * 32, ra);
             tmem_ld_wait(ra);
-            if (E::GATE && p.relu && !p.gate_mask && c + 1 < CHUNKS && col0 + 32 < p.N)
+            if (E::GATE && tensor_gate(p) && c + 1 < CHUNKS && col0 + 32 < p.N)
                 gate_issue(tmG, row0, col0 + 32);
             const uint32_t mask_cur = mask_next;
             if (kMaskGate && p.relu && p.gate_mask && c + 1 < CHUNKS)
@@ -1084,7 +1205,7 @@ bool make_epilogue_maps(const GemmProblem& g, int splits, CUtensorMap* to, CUten
         MapDesc k{};
         k.dtype = E::OUT_ELT == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
         k.base = g.out;
-        k.dims[0] = static_cast<uint64_t>(g.N);
+        k.dims[0] = static_cast<uint64_t>(E::BASE == EPI_SWIGLU_BF16 ? g.N / 2 : g.N);
         k.dims[1] = static_cast<uint64_t>(g.M);
         k.strides[0] = static_cast<uint64_t>(g.ldo) * E::OUT_ELT;
         k.box[0] = 32;
@@ -1101,7 +1222,8 @@ bool make_epilogue_maps(const GemmProblem& g, int splits, CUtensorMap* to, CUten
         }
         if (!make_map(to, k)) return false;
     }
-    if (E::GATE && g.relu && !g.gate_mask) {
+    const bool tensor_gate = (E::BASE == EPI_RESID_F32 || E::BASE == EPI_GELU_GATE_BF16) || (g.relu && !g.gate_mask);
+    if (E::GATE && tensor_gate) {
         MapDesc k{};
         k.dtype = E::GATE_ELT == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
         k.rank = 2;
@@ -1184,6 +1306,9 @@ cudaError_t launch(const GemmProblem& g, cudaStream_t st) {
     p.narrow = 0;
     p.mask_out = g.mask_out;
     p.gate_mask = g.gate_mask;
+    p.aux = g.aux;
+    p.ldaux = g.ldaux;
+    p.act = g.act;
     if ((EPI & (EPI_TMA - 1)) == EPI_SGD_F32 && p.splits != 1) return cudaErrorInvalidValue;
     CUtensorMap to, tg;
     if (!make_epilogue_maps<EPI>(g, p.splits, &to, &tg)) return cudaErrorInvalidValue;
@@ -1232,6 +1357,9 @@ cudaError_t launch2(const GemmProblem& g, cudaStream_t st) {
     p.lr = g.lr;
     p.mask_out = g.mask_out;
     p.gate_mask = g.gate_mask;
+    p.aux = g.aux;
+    p.ldaux = g.ldaux;
+    p.act = g.act;
     {
         const int last = g.N - (p.n_tiles - 1) * BN;  // columns in the last N tile
         p.narrow = narrow_tiles(EPI & (EPI_TMA - 1), BN, last) ? 1 : 0;
@@ -1267,6 +1395,10 @@ cudaError_t dispatch_bn(const GemmProblem& g, cudaStream_t st) {
     if (g.a_mn && g.b_mn && g.epilogue == EPI_SGD_F32) return launch_k<BN, true, true, EPI_SGD_F32>(g, st);
     if (!g.a_mn && !g.b_mn && g.epilogue == EPI_F32) return launch_k<BN, false, false, EPI_F32>(g, st);
     if (!g.a_mn && g.b_mn && g.epilogue == EPI_F32) return launch_k<BN, false, true, EPI_F32>(g, st);
+    if (!g.a_mn && g.b_mn && g.epilogue == EPI_RESID_F32) return launch_k<BN, false, true, EPI_RESID_F32>(g, st);
+    if (!g.a_mn && g.b_mn && g.epilogue == EPI_GELU_BF16) return launch_k<BN, false, true, EPI_GELU_BF16>(g, st);
+    if (!g.a_mn && g.b_mn && g.epilogue == EPI_SWIGLU_BF16) return launch_k<BN, false, true, EPI_SWIGLU_BF16>(g, st);
+    if (!g.a_mn && !g.b_mn && g.epilogue == EPI_GELU_GATE_BF16) return launch_k<BN, false, false, EPI_GELU_GATE_BF16>(g, st);
     return cudaErrorNotSupported;
 }
 
@@ -1279,6 +1411,10 @@ cudaError_t dispatch2_bn(const GemmProblem& g, cudaStream_t st) {
     if (g.a_mn && g.b_mn && g.epilogue == EPI_SGD_F32) return launch2_k<BN, true, true, EPI_SGD_F32>(g, st);
     if (!g.a_mn && !g.b_mn && g.epilogue == EPI_F32) return launch2_k<BN, false, false, EPI_F32>(g, st);
     if (!g.a_mn && g.b_mn && g.epilogue == EPI_F32) return launch2_k<BN, false, true, EPI_F32>(g, st);
+    if (!g.a_mn && g.b_mn && g.epilogue == EPI_RESID_F32) return launch2_k<BN, false, true, EPI_RESID_F32>(g, st);
+    if (!g.a_mn && g.b_mn && g.epilogue == EPI_GELU_BF16) return launch2_k<BN, false, true, EPI_GELU_BF16>(g, st);
+    if (!g.a_mn && g.b_mn && g.epilogue == EPI_SWIGLU_BF16) return launch2_k<BN, false, true, EPI_SWIGLU_BF16>(g, st);
+    if (!g.a_mn && !g.b_mn && g.epilogue == EPI_GELU_GATE_BF16) return launch2_k<BN, false, false, EPI_GELU_GATE_BF16>(g, st);
     return cudaErrorNotSupported;
 }
 
@@ -1453,6 +1589,8 @@ cudaError_t gemm_bf16(const GemmProblem& g, cudaStream_t st) {
     if (g.M <= 0 || g.N <= 0 || g.K <= 0) return cudaErrorInvalidValue;
     const int align = g.tf32 ? 4 : 8;  // 16-byte rows for TMA
     if (g.N % 32 != 0 || g.lda % align != 0 || g.ldb % align != 0) return cudaErrorInvalidValue;
+    if (g.epilogue == EPI_SWIGLU_BF16 && (g.N % 64 != 0 || (g.block_n && g.block_n % 64 != 0)))
+        return cudaErrorInvalidValue;  // whole (gate, up) chunk pairs per tile
     if (g.tf32) {
         int cta = g.cta, bn = g.block_n;
         if (cta == 0) {
