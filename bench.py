@@ -1,19 +1,23 @@
 #!/usr/bin/env python
 """bench.py — Superpipeline layer-streaming training step on B200 (driver contract).
 
-Workload (BASELINE.json configs[1]): a GPT-2 XL-shape stack — 48 of the reference's dense
-blocks at d=1600 (LayerBlock y = relu(xW+b), model.hpp:14-26) — one bf16 training step
-(forward, MSE, reverse backward + SGD, reference_train_step semantics) streamed through a
-Superpipeline ring (k=4, k'=2) from pinned host memory. A "step" = one train step over a
-batch of ROWS synthetic rows (make_input, seed 7). Weights: build_model(7, 48, 1600).
+Workload (BASELINE.json configs[1]): a GPT-2 XL-shape stack — 48
+transformer layers at their real shape (d 1600, ff 6400, 25 heads of 64, LayerNorm, GELU,
+causal attention; 30.7M parameters per layer, include/superpipe.h "named-shape layers") — one
+bf16 training step (forward, the reference's MSE loss, reverse backward + SGD:
+reference_train_step semantics, model.cpp:157-184) streamed through a Superpipeline ring
+(k=4, k'=2) from pinned host memory. A "step" = one train step over 16 sequences x 1024
+tokens of synthetic input (make_input, seed 7); weights: sp_build_block(seed 7). A sample is
+one token (one row of the [tokens, d] activations, as the reference's rows).
 
-value: samples (rows) per second with x/target already in HBM (sp_train_step_device);
+value: samples (tokens) per second with x/target already in HBM (sp_train_step_device);
 e2e:   the same through the host-buffer C-ABI call (sp_train_step): x/target H2D from pinned
        host memory and the loss D2H inside the timed region.
 Weights always stream from pinned host memory — that is the path being measured.
+--model dense: round 1's stand-in (48 square reference blocks, d=1600).
 
 --impl reference: the reference's own CPU implementation (oracle/_ref, built from the
-reference sources) on the host cores, same metric.
+reference sources) on the host cores: reference_train_step on FLOP-equivalent square blocks.
 """
 from __future__ import annotations
 
@@ -40,14 +44,19 @@ def parse():
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--layers", type=int, default=48)
-    p.add_argument("--d", type=int, default=1600)
-    p.add_argument("--rows", type=int, default=16384, help="batch rows per GPU per step")
+    p.add_argument("--model", default="gpt2-xl", choices=["gpt2-xl", "vit-h14", "llama3-8b", "dense"],
+                   help="named-shape transformer layers (SURVEY 8(d)) or round 1's square stand-in")
+    p.add_argument("--layers", type=int, default=0, help="0 = the model's own layer count")
+    p.add_argument("--seqs", type=int, default=16, help="sequences per GPU per step (named shapes)")
+    p.add_argument("--seq-len", type=int, default=0, help="0 = the model's own sequence length")
+    p.add_argument("--d", type=int, default=1600, help="--model dense: block width")
+    p.add_argument("--rows", type=int, default=16384, help="--model dense: batch rows per GPU per step")
     p.add_argument("--k", type=int, default=4)
     p.add_argument("--kp", type=int, default=2)
     p.add_argument("--strategy", default="superpipeline",
                    choices=["superpipeline", "standard", "naive"])
     p.add_argument("--lr", type=float, default=0.01)
+    p.add_argument("--ckpt", action="store_true", help="activation offload (the reference's checkpointing)")
     p.add_argument("--mode", default="batch", choices=["batch", "sequential"],
                    help="TransferMode (sim.hpp:15): one H2D op per k' group, or per layer")
     p.add_argument("--optimizer", default="sgd", choices=["sgd", "adamw"],
@@ -57,9 +66,12 @@ def parse():
     p.add_argument("--private-host-copies", action="store_true",
                    help="N>1: one pinned master per rank instead of one per node (shared memory)")
     p.add_argument("--no-variants", action="store_true",
-                   help="skip the in-run AdamW and tf32 variants of the same step ('variants')")
+                   help="skip the in-run variants of the same step ('variants')")
     p.add_argument("--sweep", default="", help="comma list of k:kp to report extra lines")
-    return p.parse_args()
+    a = p.parse_args()
+    if a.layers == 0:
+        a.layers = {"dense": 48, "gpt2-xl": 48, "vit-h14": 32, "llama3-8b": 32}[a.model]
+    return a
 
 
 def peaks():
@@ -218,39 +230,36 @@ def gemm_kernel_timing(torch, capi, a, reps=20):
     return res
 
 
-def layer_roofline(a, link, pk, rows_per_gpu, slots, shards=1, ckpt=False):
+def ring_roofline(L, S, lb, opt, fl_f, fl_b, link, pk, ckpt=False, fl_b_first=None):
     """Ring roofline: a model of the step's lower time bound for a k-window ring of S slots,
     from per-layer FLOPs at the sustained tensor peak and host-link bytes at the measured
     pinned rates.
 
     Bytes: S slots carry at most S layers across each direction reversal (end of forward, end
     of step), so the forward loads >= L - S layers and the backward >= L - S; every trained
-    layer writes its fp32 image back. AdamW adds the moments m, v of every layer both ways.
-    Up to min(S, L - S) of the write-backs (the layers still resident at the end) can run in
-    the next forward, whose D2H engine is otherwise idle (no deferral with activation offload).
+    layer writes its fp32 image (lb bytes) back. AdamW adds the moments m, v (opt bytes) of
+    every layer both ways. Up to min(S, L - S) of the write-backs (the layers still resident at
+    the end) can run in the next forward, whose D2H engine is otherwise idle (no deferral with
+    activation offload).
       forward  = sum over layers of max(FLOP, load / H2D rate), and at least the forward's
                  link bytes (loads + deferred write-backs) at the duplex rate;
       backward = max(sum over layers of max(FLOP, load / duplex rate),
                      its write-backs / D2H rate, its loads + write-backs / (2 x duplex rate)).
     Per-layer serialisation is applied to the loads (a layer computes after its load) but not
-    to the write-backs, which overlap later layers' loads. Sharded data parallel (shards =
-    world): each rank moves 1/world of every image."""
-    d, L = a.d, a.layers
-    S = min(slots, L)
-    lb = (d * d + d) * 4 / shards
-    opt = 2 * lb if a.optimizer == "adamw" else 0.0
+    to the write-backs, which overlap later layers' loads. fl_f / fl_b: one layer's forward /
+    backward FLOPs (fl_b_first: the bottom layer's, which needs no input gradient)."""
+    S = min(S, L)
     peak = pk["bf16_tflops_sustained"] * 1e12
     h2d, d2h, dup = link["h2d_gbs"] * 1e9, link["d2h_gbs"] * 1e9, link["duplex_gbs_per_dir"] * 1e9
-    fl_f = 2.0 * rows_per_gpu * d * d / peak
+    tf, tb = fl_f / peak, fl_b / peak
+    tb0 = (fl_b_first if fl_b_first is not None else fl_b) / peak
     deferred = 0 if ckpt else min(S, L - S)
     out_layer = lb + opt
-    # forward: S layers still resident; the deferred write-backs share the link
-    fwd = (L - S) * max(fl_f, lb / h2d) + S * fl_f
+    fwd = (L - S) * max(tf, lb / h2d) + S * tf
     fwd = max(fwd, ((L - S) * lb + deferred * out_layer) / (2 * dup), deferred * out_layer / d2h)
-    # backward: layer L-1 first; the forward's last S layers are resident (no weight load)
     per_layer, loads = 0.0, 0.0
     for pos in range(L):
-        fl = fl_f if pos == L - 1 else 2 * fl_f  # layer 0 needs no dX
+        fl = tb0 if pos == L - 1 else tb
         load = (lb if pos >= S else 0.0) + opt
         loads += load
         per_layer += max(fl, load / dup) if load else fl
@@ -259,17 +268,29 @@ def layer_roofline(a, link, pk, rows_per_gpu, slots, shards=1, ckpt=False):
     return fwd + bwd
 
 
-def cpu_baseline_ref(a, threads, rows_per_thread=2, layers_sample=6):
+def layer_roofline(a, link, pk, rows_per_gpu, slots, shards=1, ckpt=False):
+    """ring_roofline for the dense stand-in (square reference blocks of width a.d)."""
+    d = a.d
+    lb = (d * d + d) * 4 / shards
+    opt = 2 * lb if a.optimizer == "adamw" else 0.0
+    fl_f = 2.0 * rows_per_gpu * d * d
+    return ring_roofline(a.layers, slots, lb, opt, fl_f, 2 * fl_f, link, pk, ckpt, fl_b_first=fl_f)
+
+
+def cpu_baseline_ref(a, threads, rows_per_thread=2, layers_sample=6, d=None, layers_full=None):
     """The reference's reference_train_step (oracle/_ref = the reference compiled from its own
     sources) on host cores: `threads` concurrent single-threaded replicas, each training a
-    layers_sample-layer slice of the d-wide model on rows_per_thread rows; scaled linearly in
-    layers (every block costs the same) to the full model."""
+    layers_sample-layer slice of d-wide square blocks on rows_per_thread rows. Returns the
+    measured seconds and the samples/s of the full model (layers_full square blocks), scaled
+    linearly in layers (every block costs the same)."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     from pyoracle import Reference
     ref = Reference()
-    W, b, _ = ref.build_model(7, layers_sample, a.d)
-    xs = [ref.make_input(7, 100 + t, rows_per_thread, a.d) for t in range(threads)]
-    ts = [ref.make_input(7, 200 + t, rows_per_thread, a.d) for t in range(threads)]
+    d = d or a.d
+    layers_full = layers_full or a.layers
+    W, b, _ = ref.build_model(7, layers_sample, d)
+    xs = [ref.make_input(7, 100 + t, rows_per_thread, d) for t in range(threads)]
+    ts = [ref.make_input(7, 200 + t, rows_per_thread, d) for t in range(threads)]
     out = [None] * threads
 
     def work(t):
@@ -282,30 +303,50 @@ def cpu_baseline_ref(a, threads, rows_per_thread=2, layers_sample=6):
     for x in th:
         x.join()
     dt = time.perf_counter() - t0
-    full = dt * a.layers / layers_sample
+    full = dt * layers_full / layers_sample
     return threads * rows_per_thread / full, dt
 
 
 REF_ROWS = 16  # rows per host thread per reference-arm step (~1 s of CPU work per step)
 
 
+def reference_equivalent(a):
+    """The reference can only run its square dense block (model.hpp:14-26). The CPU arm of a
+    named-shape workload runs reference_train_step on square d-wide blocks carrying the same
+    linear-layer FLOPs per token: round(params per layer / d^2) blocks per transformer layer."""
+    if a.model == "dense":
+        return a.d, a.layers, 1
+    from paper_2410_08791_b200 import blocks as B
+    spec = B.NAMED_SHAPES[a.model][0]
+    lay = B.block_layout(spec)
+    per = max(1, round(sum(t.rows * t.cols for t in lay.tensors.values() if t.matrix) / (spec.d * spec.d)))
+    return spec.d, a.layers * per, per
+
+
 def run_reference(a, rank, world):
     if rank != 0:
         return
     threads = max(1, min(os.cpu_count() or 1, 64))
-    rates = []
+    d, layers_full, per = reference_equivalent(a)
+    rates, times = [], []
     for i in range(a.warmup + a.steps):
-        v, dt = cpu_baseline_ref(a, threads, rows_per_thread=REF_ROWS)
+        v, dt = cpu_baseline_ref(a, threads, rows_per_thread=REF_ROWS, d=d, layers_full=layers_full)
         if i >= a.warmup:
             rates.append(v)
+            times.append(dt)
     value = statistics.mean(rates)
-    sample = (f"{threads} concurrent reference_train_step replicas x {REF_ROWS} rows x 6 of "
-              f"{a.layers} layers (d={a.d}), time scaled x{a.layers / 6:g} to the full model")
+    sample = (f"{threads} concurrent reference_train_step replicas x {REF_ROWS} rows x 6 square d={d} "
+              f"blocks of the {layers_full}-block FLOP-equivalent model ({per} per layer x {a.layers} layers); "
+              f"value scaled x{layers_full / 6:g} in blocks")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "samples/s",
             "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
-            "ms_per_step": 1e3 * (REF_ROWS * threads) / value, "higher_is_better": True,
+            "ms_per_step": 1e3 * statistics.mean(times), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": config_of(a, world),
+            "extrapolation": {"measured": "each step trains 6 square blocks on every host thread; "
+                                          "ms_per_step is that measured time",
+                              "blocks_run": 6, "blocks_full_model": layers_full,
+                              "rows_run_per_step": REF_ROWS * threads, "value_scale": layers_full / 6},
             "cpu_baseline": {"value": value, "unit": "samples/s", "cores": threads,
                              "kind": "reference", "sample": sample},
             "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0,
@@ -314,16 +355,241 @@ def run_reference(a, rank, world):
 
 
 def config_of(a, world):
-    return {"workload": f"GPT-2 XL-shape layer stack: {a.layers} x d={a.d} dense ReLU blocks "
-                        f"(reference LayerBlock), bf16 train step (fwd+MSE+bwd+{a.optimizer.upper()})",
-            "layers": a.layers, "d": a.d, "rows_per_gpu": a.rows, "global_batch": a.rows * world,
+    if a.model == "dense":
+        return {"workload": f"square-block stand-in: {a.layers} x d={a.d} dense ReLU blocks "
+                            f"(reference LayerBlock), bf16 train step (fwd+MSE+bwd+{a.optimizer.upper()})",
+                "model": "dense", "layers": a.layers, "d": a.d, "rows_per_gpu": a.rows,
+                "global_batch": a.rows * world,
+                "strategy": a.strategy, "k": a.k, "k_prime": a.kp, "transfer_mode": a.mode,
+                "weights": "pinned host DRAM (fp32 master), streamed per step",
+                "host_master": ("one per rank" if world == 1 or a.private_host_copies
+                                else "one per node, shared by all ranks (sp_share_host_master)"),
+                "optimizer": a.optimizer if a.optimizer == "sgd" else
+                "adamw (fp32 m, v in pinned host DRAM, streamed per step)",
+                "parallelism": f"dp{world}", "l2": "working set (weights+activations) >> 126 MB L2"}
+    from paper_2410_08791_b200 import blocks as B
+    spec, _ = B.NAMED_SHAPES[a.model]
+    if a.seq_len:
+        spec = spec.with_seq(a.seq_len)
+    lay = B.block_layout(spec)
+    rows = a.seqs * spec.seq_len
+    return {"workload": f"{spec.name}-shape stack: {a.layers} transformer layers (d {spec.d}, ff {spec.ff}, "
+                        f"{spec.n_heads} heads / {spec.n_kv_heads} kv of {spec.head_dim}, "
+                        f"{'causal' if spec.causal else 'bidirectional'} attention), {lay.n_params / 1e6:.2f}M "
+                        f"params per layer; bf16 train step (fwd + MSE + bwd + {a.optimizer.upper()})"
+                        + (", activation offload" if a.ckpt else ""),
+            "model": a.model, "layers": a.layers, "d": spec.d, "ff": spec.ff, "heads": spec.n_heads,
+            "kv_heads": spec.n_kv_heads, "seq_len": spec.seq_len, "seqs_per_gpu": a.seqs,
+            "rows_per_gpu": rows, "global_batch": rows * world, "sample": "one token (row)",
+            "params_per_layer": lay.n_params,
             "strategy": a.strategy, "k": a.k, "k_prime": a.kp, "transfer_mode": a.mode,
+            "activation_offload": a.ckpt,
             "weights": "pinned host DRAM (fp32 master), streamed per step",
             "host_master": ("one per rank" if world == 1 or a.private_host_copies
                             else "one per node, shared by all ranks (sp_share_host_master)"),
             "optimizer": a.optimizer if a.optimizer == "sgd" else
             "adamw (fp32 m, v in pinned host DRAM, streamed per step)",
             "parallelism": f"dp{world}", "l2": "working set (weights+activations) >> 126 MB L2"}
+
+
+def timed_steps(torch, dist, world, steps, fn, collect=None):
+    """Device time of `steps` calls of fn between a barrier + synchronize on both sides (CUDA
+    events on the current stream, which the executor's streams join every call), max over ranks."""
+    from paper_2410_08791_b200 import dp
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    out = []
+    for _ in range(steps):
+        out.append(fn())
+        if collect is not None:
+            collect()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        dist.barrier()
+        ms = dp.max_over_ranks(dist, torch, ms)
+    return ms, out
+
+
+def run_block(a, rank, world, local, torch, dist, sp, pk, pk_src, strategy):
+    """The named-shape workload (default: C2, GPT-2 XL layers, bf16 train step)."""
+    from paper_2410_08791_b200 import blocks as B
+    from paper_2410_08791_b200 import dp
+    spec, _ = B.NAMED_SHAPES[a.model]
+    if a.seq_len:
+        spec = spec.with_seq(a.seq_len)
+    lay = B.block_layout(spec)
+    rows = a.seqs * spec.seq_len
+    model = B.build_block_model(spec, 7, a.layers)
+    host_copies_note = []
+
+    def make_executor(strat, opt=a.optimizer, ckpt=a.ckpt):
+        e = B.BlockExecutor(a.layers, spec, strat, checkpointing=ckpt, device=local, trace=0)
+        e.register_model(model)
+        if opt == "adamw":
+            e.set_optimizer(sp.OPT_ADAMW, 0.9, 0.999, 1e-8, 0.01)
+        if world > 1 and not a.private_host_copies:
+            tag = f"/sp_bench_{os.environ.get('MASTER_PORT', '0')}_{opt}_{int(ckpt)}_{strat.kind}"
+            err = dp.share_host_master(e, dist, local, tag)
+            if err:
+                host_copies_note.append(f"rank {rank}: private host copy ({err})")
+        if world > 1:
+            dp.init_executor_dp(e, dist, rank, world)
+        return e
+
+    x = sp.make_input(7, 2 * rank, rows, spec.d)
+    t = sp.make_input(7, 2 * rank + 1, rows, spec.d)
+    x_dev, t_dev = torch.from_numpy(x).cuda(), torch.from_numpy(t).cuda()
+    hx, ht = sp.HostBuffer(x.shape), sp.HostBuffer(t.shape)
+    hx.array[...] = x
+    ht.array[...] = t
+    link = measure_link(torch, chunk=min(lay.n_floats * 4, 128 << 20))
+    shards = world if world > 1 else 1
+    lb = lay.n_floats * 4 / shards
+    fl_f = rows * (lay.linear_flops_per_token() + lay.attn_flops_per_token())
+    fl_b = rows * (2 * lay.linear_flops_per_token() + 3.5 * lay.attn_flops_per_token())
+
+    def roof(n_slots, opt, ckpt):
+        return ring_roofline(a.layers, n_slots, lb, 2 * lb if opt == "adamw" else 0.0, fl_f, fl_b, link, pk, ckpt)
+
+    ex = make_executor(strategy)
+    dev = lambda e: (lambda: e.train_step_ptr(x_dev.data_ptr(), t_dev.data_ptr(), rows, a.lr, device=True))  # noqa: E731
+    step_dev = dev(ex)
+    for _ in range(a.warmup):
+        step_dev()
+    stats = []
+    with Clocks(local) as clk:
+        ms, losses = timed_steps(torch, dist, world, a.steps, step_dev, lambda: stats.append(ex.stats()))
+    step_e2e = lambda: ex.train_step_ptr(hx.ptr, ht.ptr, rows, a.lr, device=False)  # noqa: E731
+    step_e2e()
+    ms_e2e, _ = timed_steps(torch, dist, world, a.steps, step_e2e)
+    last = stats[-1]
+    # One extra step with per-op and per-GEMM CUDA events (not timed): the GEMMs inside the
+    # step, the stall / compute split.
+    ex.set_trace(2)
+    step_dev()
+    traced = ex.stats()
+    ex.set_trace(0)
+    ex.close()
+    step_s = ms * 1e-3 / a.steps
+    roof_s = roof(last["n_slots"], a.optimizer, a.ckpt)
+    variants = {}
+    # The same step under other settings, timed the same way in the same run: AdamW (north_star:
+    # optimizer state in pinned host DRAM), activation offload (the reference's checkpointing),
+    # and Standard (every layer resident: the full-residency HBM the window is compared with).
+    specs = [] if a.no_variants else [("adamw", strategy, "adamw", a.ckpt), ("offload", strategy, a.optimizer, True),
+                                       ("standard", sp.StrategyConfig(sp.STANDARD), a.optimizer, False)]
+    for vname, vstrat, vopt, vckpt in specs:
+        if vname == "offload" and a.ckpt:
+            continue
+        ev = make_executor(vstrat, vopt, vckpt)
+        fn = dev(ev)
+        for _ in range(a.warmup):
+            fn()
+        vsteps = max(2, a.steps // 2)
+        vms, _ = timed_steps(torch, dist, world, vsteps, fn)
+        st = ev.stats()
+        vroof = roof(st["n_slots"], vopt, vckpt)
+        variants[vname] = {"value": world * rows * vsteps / (vms * 1e-3), "unit": "samples/s",
+                           "ms_per_step": vms / vsteps, "ring_roofline_ms": vroof * 1e3,
+                           "frac_of_ring_roofline": vroof / (vms * 1e-3 / vsteps),
+                           "h2d_gb_per_step": st["h2d_bytes"] / 1e9, "d2h_gb_per_step": st["d2h_bytes"] / 1e9,
+                           "hbm_reserved_gb": st["hbm_reserved_bytes"] / 1e9,
+                           "ledger_peak_gb": st["peak_bytes"] / 1e9, "n_slots": st["n_slots"],
+                           "optimizer": vopt, "activation_offload": vckpt,
+                           "strategy": ["standard", "cpu_only", "naive", "superpipeline"][vstrat.kind]}
+        ev.close()
+
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        d, layers_full, per = reference_equivalent(a)
+        v, dt = cpu_baseline_ref(a, 1, rows_per_thread=64, layers_sample=6, d=d, layers_full=layers_full)
+        cpu = {"value": v, "unit": "samples/s", "cores": 1, "kind": "reference",
+               "sample": f"reference_train_step (oracle/_ref), 64 rows x 6 square d={d} blocks, {dt:.1f}s; "
+                         f"the model as {layers_full} FLOP-equivalent square blocks ({per} per layer), "
+                         f"scaled x{layers_full / 6:g} in blocks"}
+    gemm_ms, gemm_fl = traced["gemm_ms"], traced["gemm_flops"]
+    achieved = gemm_fl / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else 0.0
+    peak_tf = pk["bf16_tflops_sustained"]
+    traffic = None
+    tr_path = os.path.join(ROOT, "profiles", "block_gemm_traffic.json")
+    if os.path.exists(tr_path):
+        try:
+            traffic = json.load(open(tr_path))
+        except Exception:
+            traffic = None
+    value = world * rows * a.steps / (ms * 1e-3)
+    e2e = world * rows * a.steps / (ms_e2e * 1e-3)
+    std = variants.get("standard", {}).get("hbm_reserved_gb")
+    off = variants.get("offload", {}).get("hbm_reserved_gb") if not a.ckpt else last["hbm_reserved_bytes"] / 1e9
+    line = {"metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms / a.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (sp_build_block / make_input seed 7)", "config": config_of(a, world),
+            "sequences_per_sec": value / spec.seq_len,
+            "peak_hbm_gb": {"ledger": last["peak_bytes"] / 1e9,
+                            "ledger_weights": last["peak_weight_bytes"] / 1e9,
+                            "measured_reserved": last["hbm_reserved_bytes"] / 1e9,
+                            "standard_measured_reserved": std,
+                            "offload_measured_reserved": off,
+                            "reduction_vs_standard": (1 - last["hbm_reserved_bytes"] / 1e9 / std) if std else None,
+                            "offload_reduction_vs_standard": (1 - off / std) if (std and off) else None,
+                            "full_residency_weights": a.layers * lay.n_floats * 4 / 1e9},
+            "north_star": {"layer_roofline_ms": roof_s * 1e3, "measured_ms": step_s * 1e3,
+                           "frac_of_layer_roofline": roof_s / step_s, "link": link,
+                           "per_layer": {"fwd_flops": fl_f, "bwd_flops": fl_b, "image_bytes": lb,
+                                         "t_fwd_compute_ms": fl_f / (peak_tf * 1e12) * 1e3,
+                                         "t_link_ms": lb / (link["h2d_gbs"] * 1e9) * 1e3},
+                           "traced_step": {k: traced[k] for k in (
+                               "makespan_ms", "compute_ms", "stall_ms", "h2d_bytes", "d2h_bytes", "n_slots",
+                               "graph_replays", "gemm_launches", "attn_launches", "attn_flops")},
+                           "loss": losses[-1]},
+            "roofline": {"bound": "tensor", "kernel": "tcgen05 bf16 GEMMs of the step (4 forward, 8 backward per layer)",
+                         "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
+                         "frac": achieved / peak_tf, "traffic": traffic,
+                         "peak_source": f"{pk_src} bf16_tflops_sustained",
+                         "gemm_flops_per_step": gemm_fl, "gemm_ms_per_step": gemm_ms,
+                         "gemm_launches_per_step": traced["gemm_launches"],
+                         "gemm_share_of_step": gemm_ms * 1e-3 / step_s,
+                         "method": "CUDA events around every GEMM launch inside one traced step (trace=2) on "
+                                   "the compute stream; algorithmic 2MNK FLOPs / summed event time; "
+                                   "sustained peak because the kernels run inside a long step"},
+            "variants": variants,
+            "host_copies_note": host_copies_note or None,
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e, "unit": "samples/s",
+                    "h2d_bytes_per_step": 2 * rows * spec.d * 4, "d2h_bytes_per_step": 4},
+            "gpu_launches": int(sum(s["kernels_launched"] for s in stats)),
+            "clocks": clk.summary()}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    for spec_ in [s for s in a.sweep.split(",") if s]:
+        if spec_ == "standard":
+            strat, k, kp = sp.StrategyConfig(sp.STANDARD), a.layers, 0
+        else:
+            k, kp = (int(v) for v in spec_.split(":"))
+            strat = (sp.StrategyConfig(sp.NAIVE, k) if kp == 0
+                     else sp.StrategyConfig(sp.SUPERPIPELINE, k, kp, sp.BATCH if a.mode == "batch" else sp.SEQUENTIAL))
+        e = make_executor(strat)
+        fn = dev(e)
+        for _ in range(a.warmup):
+            fn()
+        sms, _ = timed_steps(torch, dist, world, a.steps, fn)
+        st = e.stats()
+        if rank == 0:
+            print(json.dumps({
+                "sweep": spec_, "strategy": ["standard", "cpu_only", "naive", "superpipeline"][strat.kind],
+                "k": k, "k_prime": kp, "value": world * rows * a.steps / (sms * 1e-3),
+                "unit": "samples/s", "ms_per_step": sms / a.steps, "n_slots": st["n_slots"],
+                "peak_hbm_gb": {"ledger_weights": st["peak_weight_bytes"] / 1e9, "ledger": st["peak_bytes"] / 1e9,
+                                "measured_reserved": st["hbm_reserved_bytes"] / 1e9},
+                "h2d_gb_per_step": st["h2d_bytes"] / 1e9, "d2h_gb_per_step": st["d2h_bytes"] / 1e9,
+                "layer_roofline_ms": roof(st["n_slots"], a.optimizer, a.ckpt) * 1e3}), flush=True)
+        e.close()
 
 
 def spawn_ranks(a):
@@ -368,6 +634,11 @@ def main():
     strategy = {"superpipeline": sp.StrategyConfig(sp.SUPERPIPELINE, a.k, a.kp, tmode),
                 "standard": sp.StrategyConfig(sp.STANDARD),
                 "naive": sp.StrategyConfig(sp.NAIVE, a.k)}[a.strategy]
+    if a.model != "dense":
+        run_block(a, rank, world, local, torch, dist, sp, pk, pk_src, strategy)
+        if world > 1:
+            dist.destroy_process_group()
+        return
     weights = []  # build_model(7, layers, d) — generated once, registered per executor
     for i in range(a.layers):
         Wl = np.empty((a.d, a.d), np.float32)

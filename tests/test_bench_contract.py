@@ -12,7 +12,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def _run(env_extra, *args):
     env = dict(os.environ, **env_extra)
     return subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
-                           "--layers", "2", "--d", "64", "--steps", "1", "--warmup", "0", *args],
+                           "--model", "dense", "--layers", "2", "--d", "64", "--steps", "1", "--warmup", "0",
+                           *args],
                           capture_output=True, text=True, timeout=300, env=env, cwd=ROOT)
 
 
@@ -62,8 +63,8 @@ import pytest  # noqa: E402
 def test_gpu_bench_line_has_every_contract_key():
     """bench.py on a small model (N = 1): one JSON line carrying the driver contract's keys,
     the roofline and e2e objects, our kernel launch count and the clock sample."""
-    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--layers", "6", "--d", "256",
-                        "--rows", "1024", "--steps", "3", "--warmup", "3"],
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--model", "dense", "--layers", "6",
+                        "--d", "256", "--rows", "1024", "--steps", "3", "--warmup", "3"],
                        capture_output=True, text=True, timeout=900, cwd=ROOT)
     assert r.returncode == 0, r.stderr[-2000:]
     lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
@@ -82,3 +83,24 @@ def test_gpu_bench_line_has_every_contract_key():
     assert d["cpu_baseline"]["kind"] == "reference" and d["cpu_baseline"]["cores"] == 1
     assert set(d["variants"]) == {"adamw", "tf32"}
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
+
+
+@pytest.mark.gpu
+def test_gpu_bench_named_shape_line():
+    """The default workload's code path (GPT-2 XL transformer layers) on a short stack: one
+    contract line with the named-shape config, the in-step GEMM roofline, the HBM comparison
+    against Standard and activation offload, and the FLOP-equivalent reference CPU baseline."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--layers", "4", "--seqs", "2",
+                        "--k", "2", "--kp", "1", "--steps", "3", "--warmup", "3"],
+                       capture_output=True, text=True, timeout=1200, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["config"]["model"] == "gpt2-xl" and d["config"]["params_per_layer"] > 30e6
+    assert d["config"]["rows_per_gpu"] == 2048 and d["value"] > 0
+    assert d["roofline"]["achieved"] > 0 and d["roofline"]["gemm_launches_per_step"] > 0
+    assert set(d["variants"]) == {"adamw", "offload", "standard"}
+    assert d["peak_hbm_gb"]["standard_measured_reserved"] > d["peak_hbm_gb"]["offload_measured_reserved"]
+    assert d["e2e"]["h2d_bytes_per_step"] == 2 * 2048 * 1600 * 4
+    assert d["north_star"]["traced_step"]["attn_launches"] > 0
