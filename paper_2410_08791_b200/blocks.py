@@ -83,10 +83,22 @@ class Layout:
     tensors: dict
     n_floats: int
     wire_bytes: int
+    spec: BlockSpec = None
 
     @property
     def n_params(self) -> int:
         return sum(t.rows * t.cols for t in self.tensors.values())
+
+    def linear_flops_per_token(self) -> float:
+        """Forward FLOPs per token of the block's linear layers (2 x matrix parameters)."""
+        return 2.0 * sum(t.rows * t.cols for t in self.tensors.values() if t.matrix)
+
+    def attn_flops_per_token(self) -> float:
+        """Forward FLOPs per token of the attention core (QK^T and PV: 4 hd per attended key
+        per head; causal sequences attend (S + 1) / 2 keys on average) - block.cpp's count."""
+        s = self.spec
+        keys = (s.seq_len + 1) / 2 if s.causal else s.seq_len
+        return 4.0 * keys * s.head_dim * s.n_heads
 
 
 def block_layout(spec: BlockSpec) -> Layout:
@@ -100,7 +112,7 @@ def block_layout(spec: BlockSpec) -> Layout:
     for i in range(n.value):
         t = ts[i]
         tensors[t.name.decode()] = BlockTensor(t.name.decode(), t.rows, t.cols, t.offset, t.wire_offset, bool(t.matrix))
-    return Layout(tensors, nf.value, wb.value)
+    return Layout(tensors, nf.value, wb.value, spec)
 
 
 @dataclass
