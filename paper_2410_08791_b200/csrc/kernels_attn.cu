@@ -60,6 +60,11 @@ __device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], 
         : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
         : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
+__device__ __forceinline__ float ex2f(float x) {  // MUFU.EX2 (ex2(-inf) = +0)
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
 __device__ __forceinline__ uint32_t pack2(float a, float b) {
     __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
     return *reinterpret_cast<uint32_t*>(&v);
@@ -187,14 +192,18 @@ __global__ void __launch_bounds__(kThreads) attn_fwd_kernel(const __nv_bfloat16*
             }
             // scale, mask, online softmax (rows g and g + 8 of the warp's 16)
             float mx[2] = {m_run[0], m_run[1]};
+            // only the diagonal (causal) and a ragged last block need masks
+            const bool need_mask = (sh.causal && k0 + kBN - 1 > q0 + warp * 16) || k0 + kBN > sh.S;
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
-                    const int key = k0 + i * 8 + 2 * t + (e & 1);
-                    const int q = qr0 + (e >> 1) * 8;
                     float v = s[i][e] * sh.scale_log2;
-                    if (key >= sh.S || (sh.causal && key > q)) v = -INFINITY;
+                    if (need_mask) {
+                        const int key = k0 + i * 8 + 2 * t + (e & 1);
+                        const int q = qr0 + (e >> 1) * 8;
+                        if (key >= sh.S || (sh.causal && key > q)) v = -INFINITY;
+                    }
                     s[i][e] = v;
                     mx[e >> 1] = fmaxf(mx[e >> 1], v);
                 }
@@ -208,14 +217,14 @@ __global__ void __launch_bounds__(kThreads) attn_fwd_kernel(const __nv_bfloat16*
 #pragma unroll
             for (int r = 0; r < 2; ++r) {
                 base[r] = mx[r] == -INFINITY ? 0.0f : mx[r];  // a fully masked row so far
-                corr[r] = exp2f(m_run[r] - base[r]);
+                corr[r] = ex2f(m_run[r] - base[r]);
                 m_run[r] = mx[r];
             }
             uint32_t pf[4][4];  // P as A fragments of the four k16 key blocks
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-                const float p0 = exp2f(s[i][0] - base[0]), p1 = exp2f(s[i][1] - base[0]);
-                const float p2 = exp2f(s[i][2] - base[1]), p3 = exp2f(s[i][3] - base[1]);
+                const float p0 = ex2f(s[i][0] - base[0]), p1 = ex2f(s[i][1] - base[0]);
+                const float p2 = ex2f(s[i][2] - base[1]), p3 = ex2f(s[i][3] - base[1]);
                 rs[0] += p0 + p1;
                 rs[1] += p2 + p3;
                 pf[i >> 1][(i & 1) * 2 + 0] = pack2(p0, p1);
@@ -332,6 +341,10 @@ __global__ void __launch_bounds__(kThreads) attn_bwd_dkdv_kernel(
     const int n_iter = (n_qb - qb0) * group;
     const int kr0 = k0 + warp * 16 + g;  // this thread's key rows kr0, kr0 + 8
 
+    // head dims up to 80: this warp's K and V rows stay in registers as A fragments
+    constexpr bool KV_REGS = HD <= 80;
+    constexpr int KBR = KV_REGS ? KB : 1;
+    uint32_t kreg[KBR][4], vreg[KBR][4];
     auto issue = [&](int it, int st) {
         const int hq = kvh * group + it / (n_qb - qb0);
         const int q0 = (qb0 + it % (n_qb - qb0)) * kBN;
@@ -356,6 +369,13 @@ __global__ void __launch_bounds__(kThreads) attn_bwd_dkdv_kernel(
             cp_wait<0>();
         }
         __syncthreads();
+        if (KV_REGS && it == 0) {
+#pragma unroll
+            for (int k = 0; k < KBR; ++k) {
+                ldsm_x4(kreg[k], a_addr<LD>(sK, warp * 16, k * 16, lane));
+                ldsm_x4(vreg[k], a_addr<LD>(sV, warp * 16, k * 16, lane));
+            }
+        }
         const int q0 = (qb0 + it % (n_qb - qb0)) * kBN;
         const __nv_bfloat16* tQ = sQ + st * kBN * LD;
         const __nv_bfloat16* tD = sD + st * kBN * LD;
@@ -372,8 +392,13 @@ __global__ void __launch_bounds__(kThreads) attn_bwd_dkdv_kernel(
 #pragma unroll
             for (int k = 0; k < KB; ++k) {
                 uint32_t kf[4], vf[4];
-                ldsm_x4(kf, a_addr<LD>(sK, warp * 16, k * 16, lane));
-                ldsm_x4(vf, a_addr<LD>(sV, warp * 16, k * 16, lane));
+                if (KV_REGS) {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) kf[u] = kreg[k % KBR][u], vf[u] = vreg[k % KBR][u];
+                } else {
+                    ldsm_x4(kf, a_addr<LD>(sK, warp * 16, k * 16, lane));
+                    ldsm_x4(vf, a_addr<LD>(sV, warp * 16, k * 16, lane));
+                }
 #pragma unroll
                 for (int np = 0; np < 4; ++np) {
                     uint32_t qf[4], df[4];
@@ -385,6 +410,8 @@ __global__ void __launch_bounds__(kThreads) attn_bwd_dkdv_kernel(
                     mma16816(dp[2 * np + 1], vf, df[2], df[3]);
                 }
             }
+            // masks only where a key follows a query (causal diagonal) or lies past the sequence
+            const bool need_mask = (sh.causal && k0 + warp * 16 + 15 > q0) || k0 + kBM > sh.S;
             uint32_t pf[4][4], dsf[4][4];
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
@@ -392,9 +419,11 @@ __global__ void __launch_bounds__(kThreads) attn_bwd_dkdv_kernel(
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
                     const int qi = i * 8 + 2 * t + (e & 1);  // query within the block
-                    const int key = kr0 + (e >> 1) * 8;
-                    float v = exp2f(s[i][e] * sh.scale_log2 - tL[qi]);
-                    if (key >= sh.S || (sh.causal && key > q0 + qi)) v = 0.0f;
+                    float v = ex2f(fmaf(s[i][e], sh.scale_log2, -tL[qi]));
+                    if (need_mask) {
+                        const int key = kr0 + (e >> 1) * 8;
+                        if (key >= sh.S || (sh.causal && key > q0 + qi)) v = 0.0f;
+                    }
                     p[e] = v;
                     ds[e] = v * (dp[i][e] - tDl[qi]);
                 }
@@ -515,16 +544,19 @@ __global__ void __launch_bounds__(kThreads) attn_bwd_dq_kernel(
                     mma16816(dp[2 * np + 1], df[k], vf[2], vf[3]);
                 }
             }
+            const bool need_mask = (sh.causal && k0 + kBN - 1 > q0 + warp * 16) || k0 + kBN > sh.S;
             uint32_t dsf[4][4];
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
                 float ds[4];
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
-                    const int key = k0 + i * 8 + 2 * t + (e & 1);
                     const int r = e >> 1;
-                    float p = exp2f(s[i][e] * sh.scale_log2 - L[r]);
-                    if (key >= sh.S || (sh.causal && key > qr0 + r * 8)) p = 0.0f;
+                    float p = ex2f(fmaf(s[i][e], sh.scale_log2, -L[r]));
+                    if (need_mask) {
+                        const int key = k0 + i * 8 + 2 * t + (e & 1);
+                        if (key >= sh.S || (sh.causal && key > qr0 + r * 8)) p = 0.0f;
+                    }
                     ds[e] = p * (dp[i][e] - Dl[r]);
                 }
                 dsf[i >> 1][(i & 1) * 2 + 0] = pack2(ds[0], ds[1]);
@@ -633,8 +665,18 @@ bool valid(const AttnProblem& a) {
 
 }  // namespace
 
+// 0: tcgen05 forward where it is faster (head_dim 128), 1: always the mma.sync kernel, 2: tcgen05
+// wherever the head dim allows (64, 128) (A/B knob "attn_fwd", sp_debug_set)
+int g_attn_fwd_kind = 0;
+
+cudaError_t attention_forward_tc(const AttnProblem& a, cudaStream_t st);  // kernels_attn_tc.cu
+
 cudaError_t attention_forward(const AttnProblem& a, cudaStream_t st) {
     if (!valid(a)) return cudaErrorInvalidValue;
+    // tcgen05 forward for head_dim 128 (Llama: 3.5 vs 4.8 ms at 32 x 2048); at head_dim 64 the
+    // mma.sync kernel is faster (310 vs 400 us at GPT-2 XL, tools/attn_probe.py) - knob 2 forces it
+    if ((g_attn_fwd_kind == 0 && a.head_dim == 128) || (g_attn_fwd_kind == 2 && a.head_dim == 64))
+        return attention_forward_tc(a, st);
     switch (a.head_dim) {
         case 64: return fwd_hd<64>(a, st);
         case 80: return fwd_hd<80>(a, st);

@@ -24,6 +24,7 @@
 #include <unordered_map>
 
 #include "kernels.hpp"
+#include "tc_ptx.cuh"
 
 namespace sp {
 namespace tc {
@@ -99,114 +100,6 @@ struct Params {
     int ldaux;
     int act;                    // GeluKind
 };
-
-// ---------------------------------------------------------------------------------------
-// PTX wrappers
-// ---------------------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-                 "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    const uint32_t addr = smem_u32(bar);
-    uint32_t done = 0;
-    do {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(done)
-            : "r"(addr), "r"(parity)
-            : "memory");
-    } while (!done);
-}
-__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst,
-                                            int c0, int c1) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes "
-        "[%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
-        : "memory");
-}
-__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
-}
-__device__ __forceinline__ void fence_before() {
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void fence_after() {
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-}
-// Shared-memory matrix descriptor (tcgen05 "smem descriptor"): start, LBO, SBO in 16-byte
-// units, version 1 (sm_100), layout SWIZZLE_128B (2). Tiles are 1024-byte aligned so the
-// base-offset field stays 0.
-// layout 2 = SWIZZLE_128B; 1 = SWIZZLE_128B_BASE32B (32-byte swizzle granules: the only
-// MN-major layout tcgen05 accepts for tf32 operands).
-__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout = 2) {
-    uint64_t d = 0;
-    d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
-    d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16;
-    d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32;
-    d |= static_cast<uint64_t>(1) << 46;
-    d |= static_cast<uint64_t>(layout) << 61;
-    return d;
-}
-// Instruction descriptor: D fp32, A/B bf16 (kind::f16, format 1) or tf32 (kind::tf32, format
-// 2), majors, N>>3, M>>4.
-__host__ __device__ constexpr uint32_t make_idesc(int M, int N, bool a_mn, bool b_mn, bool tf32 = false) {
-    return (1u << 4) | ((tf32 ? 2u : 1u) << 7) | ((tf32 ? 2u : 1u) << 10) | ((a_mn ? 1u : 0u) << 15) |
-           ((b_mn ? 1u : 0u) << 16) | (static_cast<uint32_t>(N >> 3) << 17) |
-           (static_cast<uint32_t>(M >> 4) << 24);
-}
-template <bool TF32>
-__device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
-                                     uint32_t idesc, uint32_t accumulate) {
-    if (TF32)
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "setp.ne.b32 p, %4, 0;\n\t"
-            "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-            "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
-    else
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "setp.ne.b32 p, %4, 0;\n\t"
-            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-            "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
-}
-__device__ __forceinline__ void umma_commit(uint64_t* bar) {
-    asm volatile(
-        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-            smem_u32(bar))
-        : "memory");
-}
-// Split form for a pipelined epilogue: issue the load, work on the previous chunk, then wait.
-// The wait names the destination registers as read-write operands, so the compiler cannot
-// hoist any use of them above it.
-__device__ __forceinline__ void tmem_ld32_async(uint32_t taddr, uint32_t (&r)[32]) {
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-        : "r"(taddr));
-}
-__device__ __forceinline__ void tmem_ld_wait(uint32_t (&r)[32]) {
-    asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]), "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15]), "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]), "+r"(r[22]), "+r"(r[23]), "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]), "+r"(r[29]), "+r"(r[30]), "+r"(r[31]) : : "memory");
-}
-
-__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
-    __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
-    return *reinterpret_cast<uint32_t*>(&v);
-}
 
 // Grouped rasterisation: consecutive tile indices walk G m-blocks x every n-block, so the CTAs
 // resident at any moment share their A panels (and B panels) in L2 instead of re-streaming each
@@ -291,18 +184,30 @@ __device__ __forceinline__ uint32_t swz(int r, int i) {
 }
 
 // GELU (tanh approximation, GPT-2's gelu_new; or the exact erf form, ViT's nn.GELU) and its
-// derivative, in fp32.
+// derivative, in fp32. The tanh is the SFU's tanh.approx.f32 (one MUFU op, max relative error
+// ~2^-11, below the bf16 rounding of the stored result): the precise tanhf made the GELU
+// epilogues 2.5x slower than their MMAs (ncu, GPT-2 XL FC1 / its dX).
+__device__ __forceinline__ float tanh_fast(float x) {
+    float y;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
 __device__ __forceinline__ float gelu_f(float x, int kind) {
     if (kind == GELU_ERF) return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f));
-    const float u = 0.79788456080286536f * (x + 0.044715f * x * x * x);
-    return 0.5f * x * (1.0f + tanhf(u));
+    const float x2 = x * x;
+    const float u = x * fmaf(0.0356774081f, x2, 0.79788456080286536f);  // sqrt(2/pi) (x + 0.044715 x^3)
+    const float hx = 0.5f * x;
+    return fmaf(hx, tanh_fast(u), hx);
 }
 __device__ __forceinline__ float gelu_grad_f(float x, int kind) {
     if (kind == GELU_ERF)
         return 0.5f * (1.0f + erff(x * 0.70710678118654752f)) + x * 0.39894228040143268f * __expf(-0.5f * x * x);
-    const float u = 0.79788456080286536f * (x + 0.044715f * x * x * x);
-    const float t = tanhf(u);
-    return 0.5f * (1.0f + t) + 0.5f * x * (1.0f - t * t) * 0.79788456080286536f * (1.0f + 0.134145f * x * x);
+    const float x2 = x * x;
+    const float u = x * fmaf(0.0356774081f, x2, 0.79788456080286536f);
+    const float t = tanh_fast(u);
+    const float du = fmaf(0.1070322243f, x2, 0.79788456080286536f);  // d u / d x
+    // 0.5 (1 + t) + 0.5 x (1 - t^2) du
+    return fmaf(0.5f * x * du, fmaf(-t, t, 1.0f), fmaf(0.5f, t, 0.5f));
 }
 
 template <int BN, int EPI>
@@ -1177,7 +1082,7 @@ bool make_map(CUtensorMap* m, const MapDesc& k) {
 // Operand [outer][ld] (inner contiguous; bf16, or fp32 for tf32), 128B-swizzled box
 // {box_inner, box_outer}
 bool make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint64_t ld,
-              uint32_t box_inner, uint32_t box_outer, bool f32 = false, bool base32 = false) {
+              uint32_t box_inner, uint32_t box_outer, bool f32, bool base32) {
     MapDesc k{};
     k.dtype = f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
     k.rank = 2;
@@ -1280,9 +1185,9 @@ cudaError_t launch(const GemmProblem& g, cudaStream_t st) {
     using O = Opnd<EPI>;
     CUtensorMap ta, tb;
     bool ok = A_MN ? make_map(&ta, g.A, g.M, g.K, g.lda, O::ATOM, O::BKE, O::TF32, O::TF32)
-                   : make_map(&ta, g.A, g.K, g.M, g.lda, O::BKE, BM, O::TF32);
+                   : make_map(&ta, g.A, g.K, g.M, g.lda, O::BKE, BM, O::TF32, false);
     ok = ok && (B_MN ? make_map(&tb, g.B, g.N, g.K, g.ldb, O::ATOM, O::BKE, O::TF32, O::TF32)
-                     : make_map(&tb, g.B, g.K, g.N, g.ldb, O::BKE, BN, O::TF32));
+                     : make_map(&tb, g.B, g.K, g.N, g.ldb, O::BKE, BN, O::TF32, false));
     if (!ok) return cudaErrorInvalidValue;
     Params p;
     p.M = g.M;
@@ -1332,9 +1237,9 @@ cudaError_t launch2(const GemmProblem& g, cudaStream_t st) {
     using O = Opnd<EPI>;
     CUtensorMap ta, tb;
     bool ok = A_MN ? make_map(&ta, g.A, g.M, g.K, g.lda, O::ATOM, O::BKE, O::TF32, O::TF32)
-                   : make_map(&ta, g.A, g.K, g.M, g.lda, O::BKE, BM, O::TF32);
+                   : make_map(&ta, g.A, g.K, g.M, g.lda, O::BKE, BM, O::TF32, false);
     ok = ok && (B_MN ? make_map(&tb, g.B, g.N, g.K, g.ldb, O::ATOM, O::BKE, O::TF32, O::TF32)
-                     : make_map(&tb, g.B, g.K, g.N, g.ldb, O::BKE, BN / 2, O::TF32));
+                     : make_map(&tb, g.B, g.K, g.N, g.ldb, O::BKE, BN / 2, O::TF32, false));
     if (!ok) return cudaErrorInvalidValue;
     Params p;
     p.M = g.M;
@@ -1450,9 +1355,12 @@ cudaError_t dispatch2_bn_kmajor(const GemmProblem& g, cudaStream_t st) {
 
 }  // namespace tc
 
+extern int g_attn_fwd_kind;  // kernels_attn.cu
+
 void set_gemm_debug(const char* key, int value, bool* known) {
     *known = true;
     if (std::strcmp(key, "epi_mode") == 0) tc::g_epi_mode = value;
+    else if (std::strcmp(key, "attn_fwd") == 0) g_attn_fwd_kind = value;
     else if (std::strcmp(key, "narrow") == 0) tc::g_narrow = value;
     else *known = false;
 }
