@@ -1,0 +1,4 @@
+// model.hpp — the reference header name (proj/core/include/pipesim/model.hpp) for source
+// compatibility; every declaration lives in the one mirror header.
+#pragma once
+#include "../pipesim.hpp"

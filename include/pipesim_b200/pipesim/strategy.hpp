@@ -1,0 +1,5 @@
+// strategy.hpp — the reference header name (proj/core/include/pipesim/strategy.hpp) for source
+// compatibility; every declaration lives in the one mirror header.
+#pragma once
+#include "../pipesim.hpp"
+#include "sim.hpp"

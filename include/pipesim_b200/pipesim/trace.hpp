@@ -1,0 +1,4 @@
+// trace.hpp — the reference header name (proj/core/include/pipesim/trace.hpp) for source
+// compatibility; every declaration lives in the one mirror header.
+#pragma once
+#include "../pipesim.hpp"

@@ -229,6 +229,12 @@ int sp_get_stats(const sp_exec* ex, sp_stats* out);
  * with the reference-semantics ledger snapshot "led=weight,activation,gradient"); returns the
  * needed length. Joined with sp_get_trace rows (op_index) it yields the reference's trace CSV. */
 int64_t sp_last_plan(const sp_exec* ex, char* buf, int64_t cap);
+/* One op of the last call's plan (op_index as in sp_get_trace rows): the reference-semantics
+ * ledger snapshot after it (weight, activation, gradient bytes; DeviceArena, arena.hpp:69-80,
+ * as TraceEvent::footprint_after, trace.hpp:44-45) and, for transfers, the moved layers in
+ * order (TraceEvent::layers). Either output may be NULL; *count = number of moved layers. */
+int sp_get_op_info(const sp_exec* ex, int32_t op_index, uint64_t ledger[3], int32_t* layers, int32_t cap,
+                   int32_t* count);
 /* Changes the trace level (sp_config.trace) for subsequent calls. */
 int sp_set_trace(sp_exec* ex, int32_t level);
 /* Item batching for sp_forward (layer-major streaming). 0 (default): the

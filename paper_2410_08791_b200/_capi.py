@@ -90,7 +90,7 @@ EXPORTS = [
     "sp_create", "sp_create_blocks", "sp_register_block", "sp_read_block", "sp_block_layout",
     "sp_build_block", "sp_register_layer", "sp_destroy", "sp_last_error", "sp_abi_version",
     "sp_forward", "sp_forward_device", "sp_train_step", "sp_train_step_device",
-    "sp_read_layer", "sp_get_stats", "sp_get_trace", "sp_set_trace", "sp_last_plan", "sp_set_item_batching", "sp_set_eager_prefetch",
+    "sp_read_layer", "sp_get_stats", "sp_get_trace", "sp_get_op_info", "sp_set_trace", "sp_last_plan", "sp_set_item_batching", "sp_set_eager_prefetch",
     "sp_set_optimizer", "sp_read_optimizer_state", "sp_share_host_master",
     "sp_nccl_unique_id",
     "sp_dp_init", "sp_dp_init2", "sp_dp_sync",
@@ -132,6 +132,7 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "sp_get_stats": ([ex, C.POINTER(SpStats)], C.c_int),
         "sp_get_trace": ([ex, C.POINTER(SpTraceEvent), i32, C.POINTER(i32)], C.c_int),
         "sp_set_trace": ([ex, i32], C.c_int),
+        "sp_get_op_info": ([ex, i32, C.POINTER(u64), C.POINTER(i32), i32, C.POINTER(i32)], C.c_int),
         "sp_set_item_batching": ([ex, i32], C.c_int),
         "sp_set_eager_prefetch": ([ex, i32], C.c_int),
         "sp_set_optimizer": ([ex, i32, C.c_float, C.c_float, C.c_float, C.c_float], C.c_int),

@@ -152,6 +152,23 @@ int64_t sp_last_plan(const sp_exec* ex, char* buf, int64_t cap) {
     return static_cast<int64_t>(text.size()) + 1;
 }
 
+int sp_get_op_info(const sp_exec* ex, int32_t op_index, uint64_t ledger[3], int32_t* layers, int32_t cap,
+                   int32_t* count) {
+    if (!ex) return SP_ERR_INVALID;
+    const sp::Plan& plan = ex->impl->last_plan();
+    if (op_index < 0 || op_index >= static_cast<int32_t>(plan.ops.size())) return SP_ERR_INVALID;
+    const sp::Op& op = plan.ops[static_cast<size_t>(op_index)];
+    if (ledger) {
+        ledger[0] = op.led_w;
+        ledger[1] = op.led_a;
+        ledger[2] = op.led_g;
+    }
+    const int32_t n = static_cast<int32_t>(op.layers.size());
+    if (count) *count = n;
+    for (int32_t i = 0; layers && i < n && i < cap; ++i) layers[i] = op.layers[static_cast<size_t>(i)];
+    return SP_OK;
+}
+
 int sp_set_trace(sp_exec* ex, int32_t level) {
     if (!ex || level < 0 || level > 2) return SP_ERR_INVALID;
     ex->impl->set_trace(level);

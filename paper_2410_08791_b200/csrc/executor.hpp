@@ -49,6 +49,7 @@ public:
     void set_eager_prefetch(bool on) { eager_prefetch_ = on; }
     void set_debug(const std::string& key, int value);
     std::string last_plan_text() const { return describe_plan(last_plan_); }
+    const Plan& last_plan() const { return last_plan_; }
     void dp_init(const uint8_t id[128], int rank, int world, bool shard_weights);
     void dp_sync();
     // Optimizer: SP_OPT_SGD (apply_sgd, the reference) or SP_OPT_ADAMW (state m, v in pinned

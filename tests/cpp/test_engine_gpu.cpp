@@ -51,7 +51,7 @@ struct Flat {
     }
 };
 
-Tensor reference_forward(const LayeredModel& m, const Tensor& x) {
+Tensor oracle_forward(const LayeredModel& m, const Tensor& x) {
     Flat f(m);
     Tensor y = Tensor::zeros(x.shape);
     orc_forward(m.n_layers, m.d, f.W.data(), f.b.data(), f.relu.data(), x.values.data(), x.rows(),
@@ -59,7 +59,7 @@ Tensor reference_forward(const LayeredModel& m, const Tensor& x) {
     return y;
 }
 
-float reference_train_step(LayeredModel& m, const Tensor& x, const Tensor& t, float lr) {
+float oracle_train_step(LayeredModel& m, const Tensor& x, const Tensor& t, float lr) {
     Flat f(m);
     const float loss = orc_train_step(m.n_layers, m.d, f.W.data(), f.b.data(), f.relu.data(),
                                       f.frozen.data(), x.values.data(), t.values.data(), x.rows(),
@@ -126,7 +126,7 @@ TEST_CASE("configs/default.json reproduces the reference digest and ledger [gpu]
     CHECK(r.summary.output_digest == "046c06b54d8304c5");
     CHECK(r.summary.peak_bytes == 6592);
     CHECK(r.summary.n_transfers_h2d == 15);
-    for (std::size_t i = 0; i < inputs.size(); ++i) CHECK(r.outputs[i] == reference_forward(model, inputs[i]));
+    for (std::size_t i = 0; i < inputs.size(); ++i) CHECK(r.outputs[i] == oracle_forward(model, inputs[i]));
 }
 
 TEST_CASE("all strategies produce bitwise-identical outputs and digests [gpu]") {
@@ -138,7 +138,7 @@ TEST_CASE("all strategies produce bitwise-identical outputs and digests [gpu]") 
                           strat(StrategyKind::Superpipeline, 3, 2, TransferMode::Sequential)}) {
         RunResult r = run_inference(model, inputs, s, roomy_arena());
         REQUIRE(r.outputs.size() == inputs.size());
-        for (std::size_t i = 0; i < inputs.size(); ++i) CHECK(r.outputs[i] == reference_forward(model, inputs[i]));
+        for (std::size_t i = 0; i < inputs.size(); ++i) CHECK(r.outputs[i] == oracle_forward(model, inputs[i]));
         if (first.empty()) first = r.summary.output_digest;
         else CHECK(r.summary.output_digest == first);
     }
@@ -170,7 +170,7 @@ TEST_CASE("train step is bitwise-faithful for every strategy and option [gpu]") 
         Tensor x = make_input(7, 0, 3, 5);
         Tensor target = make_input(7, 1, 3, 5);
         LayeredModel expected = ref;
-        const float expected_loss = reference_train_step(expected, x, target, 0.02f);
+        const float expected_loss = oracle_train_step(expected, x, target, 0.02f);
         for (const auto& s : {strat(StrategyKind::Standard), strat(StrategyKind::Naive, 2),
                               strat(StrategyKind::Superpipeline, 2, 1)}) {
             for (bool ckpt : {false, true}) {
@@ -228,7 +228,7 @@ TEST_CASE("insufficient capacity is reported as an OOM deadlock [gpu]") {
         CHECK_THROWS_AS(run_inference(model, inputs, strat(StrategyKind::Standard), arena), OomDeadlockError);
     }
     RunResult r = run_inference(model, inputs, strat(StrategyKind::Superpipeline, 2, 1), arena);
-    CHECK(r.outputs[0] == reference_forward(model, inputs[0]));
+    CHECK(r.outputs[0] == oracle_forward(model, inputs[0]));
     CHECK_THROWS_AS(run_inference(model, inputs, strat(StrategyKind::CpuOnly), arena), std::invalid_argument);
 }
 
@@ -252,10 +252,10 @@ TEST_CASE("randomized small configs stay faithful (acceptance C1) [gpu]") {
         auto inputs = make_inputs(model.seed, items, b, d);
         Tensor x = make_input(model.seed, 1001, b, d), t = make_input(model.seed, 1002, b, d);
         LayeredModel expected = model;
-        const float expected_loss = reference_train_step(expected, x, t, 0.02f);
+        const float expected_loss = oracle_train_step(expected, x, t, 0.02f);
         for (const auto& s : strategies) {
             RunResult r = run_inference(model, inputs, s, roomy_arena());
-            for (std::size_t i = 0; i < inputs.size(); ++i) CHECK(r.outputs[i] == reference_forward(model, inputs[i]));
+            for (std::size_t i = 0; i < inputs.size(); ++i) CHECK(r.outputs[i] == oracle_forward(model, inputs[i]));
             CHECK(r.summary.peak_weight_bytes <= peak_weight_residency(s, n, model.layer_bytes()));
             for (bool ckpt : {false, true}) {
                 RunResult rt = run_train_step(model, x, t, s, roomy_arena(), TrainConfig{0.02f, ckpt, b});
@@ -270,7 +270,7 @@ TEST_CASE("bf16 tensor-core path is window-invariant and close to the reference 
     set_numerics(Numerics::Bf16);
     LayeredModel model = build_model(5, 8, 128, 0);
     auto inputs = make_inputs(5, 1, 256, 128);
-    Tensor want = reference_forward(model, inputs[0]);
+    Tensor want = oracle_forward(model, inputs[0]);
     std::vector<float> first;
     for (const auto& s : {strat(StrategyKind::Standard), strat(StrategyKind::Superpipeline, 2, 1),
                           strat(StrategyKind::Superpipeline, 5, 3)}) {
@@ -291,7 +291,7 @@ TEST_CASE("tf32 tensor-core path is window-invariant and within 2e-3 of the refe
     set_numerics(Numerics::Tf32);
     LayeredModel model = build_model(5, 8, 128, 0);
     auto inputs = make_inputs(5, 1, 256, 128);
-    Tensor want = reference_forward(model, inputs[0]);
+    Tensor want = oracle_forward(model, inputs[0]);
     std::vector<float> first;
     for (const auto& s : {strat(StrategyKind::Standard), strat(StrategyKind::Superpipeline, 2, 1),
                           strat(StrategyKind::Naive, 3)}) {
