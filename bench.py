@@ -57,6 +57,9 @@ def parse():
                    choices=["superpipeline", "standard", "naive"])
     p.add_argument("--lr", type=float, default=0.01)
     p.add_argument("--ckpt", action="store_true", help="activation offload (the reference's checkpointing)")
+    p.add_argument("--infer", action="store_true",
+                   help="inference (run_inference) instead of a train step; N > 1 runs N replicas "
+                        "(SURVEY 8(e): inference is replicas only, no collective)")
     p.add_argument("--mode", default="batch", choices=["batch", "sequential"],
                    help="TransferMode (sim.hpp:15): one H2D op per k' group, or per layer")
     p.add_argument("--optimizer", default="sgd", choices=["sgd", "adamw"],
@@ -592,6 +595,115 @@ def run_block(a, rank, world, local, torch, dist, sp, pk, pk_src, strategy):
         e.close()
 
 
+def run_block_infer(a, rank, world, local, torch, dist, sp, pk, pk_src, strategy):
+    """Named-shape inference (Llama-3-8B layers, 32 x 2048 tokens per GPU, k=4):
+    every rank runs its own ring on its own batch from the node's one pinned master - replicas,
+    no collective. Weights stream as the bf16 wire image (2 B per matrix parameter)."""
+    import ctypes
+    from paper_2410_08791_b200 import _capi
+    from paper_2410_08791_b200 import blocks as B
+    from paper_2410_08791_b200 import dp
+    spec, _ = B.NAMED_SHAPES[a.model]
+    if a.seq_len:
+        spec = spec.with_seq(a.seq_len)
+    lay = B.block_layout(spec)
+    rows = a.seqs * spec.seq_len
+    ex = B.BlockExecutor(a.layers, spec, strategy, device=local, trace=0)
+    params = np.empty(lay.n_floats, np.float32)
+    desc = spec.desc()
+    for i in range(a.layers):  # layer by layer: no second full host copy of the model
+        _capi.check(_capi.LIB.sp_build_block(ctypes.byref(desc), 7, i, params.ctypes.data))
+        ex.register_block(i, params)
+    note = None
+    if world > 1 and not a.private_host_copies:
+        note = dp.share_host_master(ex, dist, local, f"/sp_bench_infer_{os.environ.get('MASTER_PORT', '0')}")
+    x = sp.make_input(7, rank, rows, spec.d)
+    x_dev = torch.from_numpy(x).cuda()
+    y_dev = torch.empty_like(x_dev)
+    hx, hy = sp.HostBuffer(x.shape), sp.HostBuffer(x.shape)
+    hx.array[...] = x
+    link = measure_link(torch, chunk=min(lay.wire_bytes, 128 << 20))
+    step = lambda: ex.forward_ptr(x_dev.data_ptr(), rows, 1, y_dev.data_ptr(), device=True)  # noqa: E731
+    for _ in range(a.warmup):
+        step()
+    stats = []
+    with Clocks(local) as clk:
+        ms, _ = timed_steps(torch, dist, world, a.steps, step, lambda: stats.append(ex.stats()))
+    step_e2e = lambda: ex.forward_ptr(hx.ptr, rows, 1, hy.ptr, device=False)  # noqa: E731
+    step_e2e()
+    ms_e2e, _ = timed_steps(torch, dist, world, a.steps, step_e2e)
+    last = stats[-1]
+    ex.set_trace(2)
+    step()
+    traced = ex.stats()
+    ex.set_trace(0)
+    peak = pk["bf16_tflops_sustained"] * 1e12
+    fl = rows * (lay.linear_flops_per_token() + lay.attn_flops_per_token())
+    per_layer = max(fl / peak, lay.wire_bytes / (link["h2d_gbs"] * 1e9))
+    loads = int(round(traced["h2d_bytes"] / lay.wire_bytes))  # layers actually streamed per call
+    # north_star's per-layer roofline: a streamed layer costs max(FLOPs at peak, wire bytes over
+    # the link), a layer still resident from the previous call its FLOPs alone
+    roof_s = loads * per_layer + (a.layers - loads) * fl / peak
+    step_s = ms * 1e-3 / a.steps
+    gemm_ms, gemm_fl = traced["gemm_ms"], traced["gemm_flops"]
+    achieved = gemm_fl / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else 0.0
+    value = world * rows * a.steps / (ms * 1e-3)
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        cpu = cpu_baseline_infer(a, spec, lay)
+    line = {"metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic (sp_build_block / make_input seed 7)",
+            "config": dict(config_of(a, world), workload=f"{spec.name}-shape stack: {a.layers} transformer "
+                           f"layers, bf16 inference (run_inference), {a.seqs} x {spec.seq_len} tokens per GPU, "
+                           f"{'replicas' if world > 1 else 'one ring'}", mode="inference",
+                           parallelism=f"replicas x{world}" if world > 1 else "dp1"),
+            "sequences_per_sec": value / spec.seq_len,
+            "peak_hbm_gb": {"ledger": last["peak_bytes"] / 1e9, "ledger_weights": last["peak_weight_bytes"] / 1e9,
+                            "measured_reserved": last["hbm_reserved_bytes"] / 1e9,
+                            "full_residency_weights_bf16": a.layers * lay.wire_bytes / 1e9},
+            "north_star": {"layer_roofline_ms": roof_s * 1e3, "measured_ms": step_s * 1e3,
+                           "frac_of_layer_roofline": roof_s / step_s, "link": link,
+                           "per_layer": {"flops": fl, "wire_bytes": lay.wire_bytes,
+                                         "t_compute_ms": fl / peak * 1e3,
+                                         "t_link_ms": lay.wire_bytes / (link["h2d_gbs"] * 1e9) * 1e3,
+                                         "bound_ms": per_layer * 1e3, "layers_loaded_per_call": loads},
+                           "traced_step": {k: traced[k] for k in ("makespan_ms", "compute_ms", "stall_ms", "h2d_bytes",
+                                                                   "n_slots", "gemm_launches", "attn_launches",
+                                                                   "attn_flops")}},
+            "roofline": {"bound": "tensor", "kernel": "tcgen05 bf16 GEMMs of the step (4 per layer)",
+                         "achieved": achieved, "peak": pk["bf16_tflops_sustained"], "unit": "TFLOP/s",
+                         "frac": achieved / pk["bf16_tflops_sustained"], "traffic": None,
+                         "peak_source": f"{pk_src} bf16_tflops_sustained", "gemm_flops_per_step": gemm_fl,
+                         "gemm_ms_per_step": gemm_ms, "gemm_share_of_step": gemm_ms * 1e-3 / step_s,
+                         "method": "CUDA events around every GEMM inside one traced call (trace=2)"},
+            "host_copies_note": note, "cpu_baseline": cpu,
+            "e2e": {"value": world * rows * a.steps / (ms_e2e * 1e-3), "unit": "samples/s",
+                    "h2d_bytes_per_step": rows * spec.d * 4, "d2h_bytes_per_step": rows * spec.d * 4},
+            "gpu_launches": int(sum(s_["kernels_launched"] for s_ in stats)), "clocks": clk.summary()}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    ex.close()
+
+
+def cpu_baseline_infer(a, spec, lay):
+    """reference_forward (oracle/_ref) on one core over FLOP-equivalent square blocks: one
+    d-wide block on 16 rows, scaled to the model's linear FLOPs and the step's rows."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from pyoracle import Reference
+    ref = Reference()
+    W, b, _ = ref.build_model(7, 1, spec.d)
+    xs = ref.make_input(7, 3, 16, spec.d)
+    t0 = time.perf_counter()
+    ref.forward(W, b, xs)
+    dt = time.perf_counter() - t0
+    per = lay.linear_flops_per_token() / (2.0 * spec.d * spec.d)  # square blocks per layer
+    tokens_per_s = 16 / (dt * per * a.layers)
+    return {"value": tokens_per_s, "unit": "samples/s", "cores": 1, "kind": "reference",
+            "sample": f"reference_forward (oracle/_ref), one square d={spec.d} block on 16 rows, {dt:.2f}s; "
+                      f"scaled to {per:.1f} FLOP-equivalent blocks per layer x {a.layers} layers"}
+
+
 def spawn_ranks(a):
     """`--gpus N` without a torchrun environment: re-launch this command as N ranks (one
     process per GPU, 127.0.0.1 rendezvous) and return their exit code. Only rank 0 prints."""
@@ -634,6 +746,11 @@ def main():
     strategy = {"superpipeline": sp.StrategyConfig(sp.SUPERPIPELINE, a.k, a.kp, tmode),
                 "standard": sp.StrategyConfig(sp.STANDARD),
                 "naive": sp.StrategyConfig(sp.NAIVE, a.k)}[a.strategy]
+    if a.model != "dense" and a.infer:
+        run_block_infer(a, rank, world, local, torch, dist, sp, pk, pk_src, strategy)
+        if world > 1:
+            dist.destroy_process_group()
+        return
     if a.model != "dense":
         run_block(a, rank, world, local, torch, dist, sp, pk, pk_src, strategy)
         if world > 1:

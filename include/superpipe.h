@@ -284,7 +284,9 @@ int sp_get_trace(const sp_exec* ex, sp_trace_event* events, int32_t cap, int32_t
 int sp_share_host_master(sp_exec* ex, const char* name, int32_t create);
 
 /* ---- data parallel ----------------------------------------------------------------- */
-/* Per-layer NCCL all-reduce of dW/db as each layer's backward completes. */
+/* Per-layer NCCL all-reduce of dW/db as each layer's backward completes. The first dp_init of
+ * a process sets NCCL_ALGO=Ring and NCCL_PROTO=Simple unless the caller set them, so every
+ * call reduces in one fixed order (results are bit-identical across windows and runs). */
 int sp_nccl_unique_id(uint8_t id[128]);
 int sp_dp_init(sp_exec* ex, const uint8_t id[128], int32_t rank, int32_t world);
 /* Same, choosing the weight-streaming mode explicitly. shard_weights = 1: each rank copies only

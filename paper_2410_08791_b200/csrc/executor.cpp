@@ -1542,6 +1542,11 @@ void Executor::dp_init(const uint8_t id[128], int rank, int world, bool shard_we
     // partials, fixed-order reduce, NCCL all-reduce inside the captured graph, SGD on the
     // update stream) then runs end to end on a single GPU.
     if (!nccl().ok()) throw Error(SP_ERR_NCCL, nccl().error);
+    // One reduction order for every call: the per-layer collectives have the same sizes for
+    // every (k, k') window, and pinning the algorithm and protocol (unless the caller chose
+    // them) keeps NCCL's tuner from picking different reduction trees across runs or boxes.
+    setenv("NCCL_ALGO", "Ring", 0);
+    setenv("NCCL_PROTO", "Simple", 0);
     CUDA_OK(cudaSetDevice(cfg_.device));
     for (auto s : {s_h2d_, s_comp_, s_d2h_, s_upd_}) CUDA_OK(cudaStreamSynchronize(s));
     if (comm_) {
