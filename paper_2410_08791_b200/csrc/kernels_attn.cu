@@ -665,17 +665,16 @@ bool valid(const AttnProblem& a) {
 
 }  // namespace
 
-// 0: tcgen05 forward where it is faster (head_dim 128), 1: always the mma.sync kernel, 2: tcgen05
-// wherever the head dim allows (64, 128) (A/B knob "attn_fwd", sp_debug_set)
+// 0 (default) / 2: tcgen05 forward where the head dim allows (64, 128), 1: always the mma.sync
+// kernel (A/B knob "attn_fwd", sp_debug_set)
 int g_attn_fwd_kind = 0;
 
 cudaError_t attention_forward_tc(const AttnProblem& a, cudaStream_t st);  // kernels_attn_tc.cu
 
 cudaError_t attention_forward(const AttnProblem& a, cudaStream_t st) {
     if (!valid(a)) return cudaErrorInvalidValue;
-    // tcgen05 forward for head_dim 128 (Llama: 3.5 vs 4.8 ms at 32 x 2048); at head_dim 64 the
-    // mma.sync kernel is faster (310 vs 400 us at GPT-2 XL, tools/attn_probe.py) - knob 2 forces it
-    if ((g_attn_fwd_kind == 0 && a.head_dim == 128) || (g_attn_fwd_kind == 2 && a.head_dim == 64))
+    // tcgen05 forward for head_dim 64 / 128 (persistent; tools/attn_probe.py), mma.sync for 80
+    if ((g_attn_fwd_kind == 0 || g_attn_fwd_kind == 2) && (a.head_dim == 64 || a.head_dim == 128))
         return attention_forward_tc(a, st);
     switch (a.head_dim) {
         case 64: return fwd_hd<64>(a, st);
