@@ -147,8 +147,12 @@ struct EpiSmem {
     static constexpr int GATE_ELT = (BASE == EPI_GATE_F32 || BASE == EPI_RESID_F32) ? 4 : 2;
     static constexpr bool GATE = TMA && IS_GATE;
     static constexpr int GATE_BUF = 32 * 32 * GATE_ELT;
-    static constexpr int OUT_BYTES = TMA_OUT ? 4 * 2 * OUT_BUF : 0;  // 4 warps x 2 buffers
-    static constexpr int GATE_BYTES = GATE ? 4 * 2 * GATE_BUF : 0;
+    // Epilogue warps: 8 for the GELU epilogues (two per TMEM lane quarter, each half of the
+    // tile's columns: their per-element math outruns 4 warps at short K), else 4.
+    static constexpr int EW = (BASE == EPI_GELU_BF16 || BASE == EPI_GELU_GATE_BF16) ? 8 : 4;
+    static constexpr int THREADS = 128 + 32 * EW;
+    static constexpr int OUT_BYTES = TMA_OUT ? EW * 2 * OUT_BUF : 0;  // EW warps x 2 buffers
+    static constexpr int GATE_BYTES = GATE ? EW * 2 * GATE_BUF : 0;
     static constexpr int BYTES = OUT_BYTES + GATE_BYTES;
 };
 
@@ -219,14 +223,18 @@ struct TileEpilogue {
     uint8_t* gbuf;    // this warp's two gate buffers (TMA kind)
     uint64_t* gbar;   // their two mbarriers
     int lane;
+    int c_begin, c_end;  // this warp's 32-column chunks of the tile
     uint32_t out_n = 0, gate_issued = 0, gate_used = 0;
     uint32_t mask_next = 0;  // ReLU bit-mask word of the next chunk (loaded one chunk ahead)
 
-    __device__ __forceinline__ TileEpilogue(uint8_t* epi_smem, uint64_t* gate_bars, int q, int ln)
-        : obuf(epi_smem + q * 2 * E::OUT_BUF),
-          gbuf(epi_smem + E::OUT_BYTES + q * 2 * E::GATE_BUF),
-          gbar(gate_bars + 2 * q),
-          lane(ln) {}
+    // e: epilogue warp index (0 .. EW-1); lane quarter e % 4, column half e / 4 when EW == 8
+    __device__ __forceinline__ TileEpilogue(uint8_t* epi_smem, uint64_t* gate_bars, int e, int ln)
+        : obuf(epi_smem + e * 2 * E::OUT_BUF),
+          gbuf(epi_smem + E::OUT_BYTES + e * 2 * E::GATE_BUF),
+          gbar(gate_bars + 2 * e),
+          lane(ln),
+          c_begin(E::EW == 8 ? (e / 4) * (CHUNKS / 2) : 0),
+          c_end(E::EW == 8 ? (e / 4 + 1) * (CHUNKS / 2) : CHUNKS) {}
 
     __device__ __forceinline__ void gate_issue(const CUtensorMap* tmG, int row0, int col0) {
         const int b = gate_issued & 1;
@@ -248,8 +256,9 @@ struct TileEpilogue {
     }
     // before the accumulator wait: the gate of the tile's first chunk starts loading
     __device__ __forceinline__ void begin_tile(const CUtensorMap* tmG, const Params& p, int row0, int n0) {
-        if (E::GATE && tensor_gate(p)) gate_issue(tmG, row0, n0);
-        if (kMaskGate && p.relu && p.gate_mask) mask_next = mask_word(p, row0 + lane, n0);
+        const int c0 = n0 + c_begin * 32;
+        if (E::GATE && tensor_gate(p) && c0 < p.N) gate_issue(tmG, row0, c0);
+        if (kMaskGate && p.relu && p.gate_mask) mask_next = mask_word(p, row0 + lane, c0);
     }
 
     // This lane's row of the chunk's gate tensor as fp32: from the TMA-staged smem buffer, or
@@ -505,14 +514,14 @@ struct TileEpilogue {
             return;
         }
 #pragma unroll 1
-        for (int c = 0; c < CHUNKS; ++c) {
+        for (int c = c_begin; c < c_end; ++c) {
             const int col0 = n0 + c * 32;
             tmem_ld32_async(tmem_acc + c * 32, ra);
             tmem_ld_wait(ra);
-            if (E::GATE && tensor_gate(p) && c + 1 < CHUNKS && col0 + 32 < p.N)
+            if (E::GATE && tensor_gate(p) && c + 1 < c_end && col0 + 32 < p.N)
                 gate_issue(tmG, row0, col0 + 32);
             const uint32_t mask_cur = mask_next;
-            if (kMaskGate && p.relu && p.gate_mask && c + 1 < CHUNKS)
+            if (kMaskGate && p.relu && p.gate_mask && c + 1 < c_end)
                 mask_next = mask_word(p, row0 + lane, col0 + 32);
             if (col0 < p.N) chunk(tmO, p, ra, row0, col0, split, mask_cur);
         }
@@ -528,7 +537,7 @@ struct TileEpilogue {
 // the kernel (1-CTA: M = 128 per MMA)
 // ---------------------------------------------------------------------------------------
 template <int BN, bool A_MN, bool B_MN, int EPI>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(EpiSmem<EPI>::THREADS, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmG,
                 const Params p) {
@@ -549,7 +558,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* tfull = empty + STAGES;
     uint64_t* tempty = tfull + 2;
     uint64_t* gbar = tempty + 2;  // 4 epilogue warps x 2 gate buffers
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbar + 8);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbar + 16);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -565,9 +574,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(&tfull[s], 1);
-            mbar_init(&tempty[s], 128);
+            mbar_init(&tempty[s], 32 * EpiSmem<EPI>::EW);
         }
-        for (int s = 0; s < 8; ++s) mbar_init(&gbar[s], 1);
+        for (int s = 0; s < 16; ++s) mbar_init(&gbar[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
@@ -668,7 +677,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else if (warp >= 4) {
         // ===== epilogue: TMEM -> registers -> fused op -> smem -> TMA store =====
         const int q = warp & 3;  // TMEM lanes [32q, 32q+32)
-        TileEpilogue<BN, EPI> ep(sE, gbar, q, lane);
+        TileEpilogue<BN, EPI> ep(sE, gbar, warp - 4, lane);
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int t = blockIdx.x; t < total; t += gridDim.x) {
@@ -814,7 +823,7 @@ struct Cfg2 {
 };
 
 template <int BN, bool A_MN, bool B_MN, int EPI>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiSmem<EPI>::THREADS, 1)
     gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmG,
                  const Params p) {
@@ -835,7 +844,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     uint64_t* tfull = empty + STAGES;
     uint64_t* tempty = tfull + 2;
     uint64_t* gbar = tempty + 2;  // 4 epilogue warps x 2 gate buffers
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbar + 8);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbar + 16);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -853,9 +862,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(&tfull[s], 1);
-            mbar_init(&tempty[s], 2 * 128);  // both CTAs' epilogue threads (leader's copy used)
+            mbar_init(&tempty[s], 2 * 32 * EpiSmem<EPI>::EW);  // both CTAs' epilogue threads (leader's copy)
         }
-        for (int s = 0; s < 8; ++s) mbar_init(&gbar[s], 1);
+        for (int s = 0; s < 16; ++s) mbar_init(&gbar[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
@@ -965,7 +974,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int q = warp & 3;
         const uint32_t tempty_leader0 = map_to_rank0(smem_u32(&tempty[0]));
         const uint32_t tempty_leader1 = map_to_rank0(smem_u32(&tempty[1]));
-        TileEpilogue<BN, EPI> ep(sE, gbar, q, lane);
+        TileEpilogue<BN, EPI> ep(sE, gbar, warp - 4, lane);
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int i = 0;; ++i) {
@@ -1219,7 +1228,7 @@ cudaError_t launch(const GemmProblem& g, cudaStream_t st) {
     if (!make_epilogue_maps<EPI>(g, p.splits, &to, &tg)) return cudaErrorInvalidValue;
     const int total = p.m_tiles * p.n_tiles * p.splits;
     const int grid = total < num_sms() ? total : num_sms();
-    kern<<<dim3(grid), dim3(kThreads), C::SMEM, st>>>(ta, tb, to, tg, p);
+    kern<<<dim3(grid), dim3(EpiSmem<EPI>::THREADS), C::SMEM, st>>>(ta, tb, to, tg, p);
     return cudaGetLastError();
 }
 
@@ -1275,7 +1284,7 @@ cudaError_t launch2(const GemmProblem& g, cudaStream_t st) {
     const int total = p.m_tiles * p.n_tiles * p.splits;
     const int pairs = num_sms() / 2;
     const int grid = 2 * (total < pairs ? total : pairs);
-    kern<<<dim3(grid), dim3(kThreads), C::SMEM, st>>>(ta, tb, to, tg, p);
+    kern<<<dim3(grid), dim3(EpiSmem<EPI>::THREADS), C::SMEM, st>>>(ta, tb, to, tg, p);
     return cudaGetLastError();
 }
 
