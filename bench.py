@@ -233,7 +233,7 @@ def gemm_kernel_timing(torch, capi, a, reps=20):
     return res
 
 
-def ring_roofline(L, S, lb, opt, fl_f, fl_b, link, pk, ckpt=False, fl_b_first=None):
+def ring_roofline(L, S, lb, opt, fl_f, fl_b, link, pk, ckpt=False, fl_b_first=None, lb_fwd=None, lb_hit=0.0):
     """Ring roofline: a model of the step's lower time bound for a k-window ring of S slots,
     from per-layer FLOPs at the sustained tensor peak and host-link bytes at the measured
     pinned rates.
@@ -250,7 +250,10 @@ def ring_roofline(L, S, lb, opt, fl_f, fl_b, link, pk, ckpt=False, fl_b_first=No
                      its write-backs / D2H rate, its loads + write-backs / (2 x duplex rate)).
     Per-layer serialisation is applied to the loads (a layer computes after its load) but not
     to the write-backs, which overlap later layers' loads. fl_f / fl_b: one layer's forward /
-    backward FLOPs (fl_b_first: the bottom layer's, which needs no input gradient)."""
+    backward FLOPs (fl_b_first: the bottom layer's, which needs no input gradient). A split
+    master (named-shape layers) loads only lb_fwd bytes per forward layer (its bf16 wire prefix)
+    and lb_hit bytes for a backward layer still resident (the low halves the update needs)."""
+    lb_fwd = lb if lb_fwd is None else lb_fwd
     S = min(S, L)
     peak = pk["bf16_tflops_sustained"] * 1e12
     h2d, d2h, dup = link["h2d_gbs"] * 1e9, link["d2h_gbs"] * 1e9, link["duplex_gbs_per_dir"] * 1e9
@@ -258,12 +261,12 @@ def ring_roofline(L, S, lb, opt, fl_f, fl_b, link, pk, ckpt=False, fl_b_first=No
     tb0 = (fl_b_first if fl_b_first is not None else fl_b) / peak
     deferred = 0 if ckpt else min(S, L - S)
     out_layer = lb + opt
-    fwd = (L - S) * max(tf, lb / h2d) + S * tf
-    fwd = max(fwd, ((L - S) * lb + deferred * out_layer) / (2 * dup), deferred * out_layer / d2h)
+    fwd = (L - S) * max(tf, lb_fwd / h2d) + S * tf
+    fwd = max(fwd, ((L - S) * lb_fwd + deferred * out_layer) / (2 * dup), deferred * out_layer / d2h)
     per_layer, loads = 0.0, 0.0
     for pos in range(L):
         fl = tb0 if pos == L - 1 else tb
-        load = (lb if pos >= S else 0.0) + opt
+        load = (lb if pos >= S else lb_hit) + opt
         loads += load
         per_layer += max(fl, load / dup) if load else fl
     outs = (L - deferred) * out_layer
@@ -455,9 +458,16 @@ def run_block(a, rank, world, local, torch, dist, sp, pk, pk_src, strategy):
     lb = lay.n_floats * 4 / shards
     fl_f = rows * (lay.linear_flops_per_token() + lay.attn_flops_per_token())
     fl_b = rows * (2 * lay.linear_flops_per_token() + 3.5 * lay.attn_flops_per_token())
+    # one GPU / all-reduce data parallel: the split master (forward streams the bf16 wire prefix,
+    # a resident backward layer loads its low halves); sharded: the fp32 image in 1/world shards
+    split = shards == 1
+    mat = sum(t.rows * t.cols for t in lay.tensors.values() if t.matrix)
+    lb_fwd = lay.wire_bytes if split else lb
+    lb_hit = 2.0 * mat if split else 0.0
 
     def roof(n_slots, opt, ckpt):
-        return ring_roofline(a.layers, n_slots, lb, 2 * lb if opt == "adamw" else 0.0, fl_f, fl_b, link, pk, ckpt)
+        return ring_roofline(a.layers, n_slots, lb, 2 * lb if opt == "adamw" else 0.0, fl_f, fl_b, link, pk, ckpt,
+                             lb_fwd=lb_fwd, lb_hit=lb_hit)
 
     ex = make_executor(strategy)
     dev = lambda e: (lambda: e.train_step_ptr(x_dev.data_ptr(), t_dev.data_ptr(), rows, a.lr, device=True))  # noqa: E731
@@ -545,6 +555,7 @@ def run_block(a, rank, world, local, torch, dist, sp, pk, pk_src, strategy):
             "north_star": {"layer_roofline_ms": roof_s * 1e3, "measured_ms": step_s * 1e3,
                            "frac_of_layer_roofline": roof_s / step_s, "link": link,
                            "per_layer": {"fwd_flops": fl_f, "bwd_flops": fl_b, "image_bytes": lb,
+                                         "fwd_wire_bytes": lb_fwd, "bwd_resident_load_bytes": lb_hit,
                                          "t_fwd_compute_ms": fl_f / (peak_tf * 1e12) * 1e3,
                                          "t_link_ms": lb / (link["h2d_gbs"] * 1e9) * 1e3},
                            "traced_step": {k: traced[k] for k in (

@@ -71,6 +71,14 @@ std::string make_block_layout(const sp_block_desc& d, BlockLayout& L) {
     if (d.bias) L.b2 = add("b2", 1, d.d, false);
     L.n_floats = off;
     L.wire_bytes = woff;
+    uint64_t lo = 0;
+    for (BlockTensor& t : L.t) {
+        if (!t.matrix) continue;
+        t.lo_off = lo;
+        lo = up(lo + t.count() * 2, kAlignBytes);
+    }
+    L.lo_bytes = lo;
+    L.split_bytes = L.wire_bytes + L.lo_bytes;
     return "";
 }
 

@@ -20,6 +20,7 @@ struct BlockTensor {
     bool matrix = false;
     uint64_t off = 0;       // floats, in the fp32 image
     uint64_t wire_off = 0;  // bytes, in the bf16 wire image (matrices bf16, vectors fp32)
+    uint64_t lo_off = 0;    // matrices: bytes in the low-half plane of the split image
     uint64_t count() const { return static_cast<uint64_t>(rows) * static_cast<uint64_t>(cols); }
 };
 
@@ -31,6 +32,11 @@ struct BlockLayout {
     int ln1_g = -1, ln1_b = -1, wqkv = -1, bqkv = -1, wo = -1, bo = -1, ln2_g = -1, ln2_b = -1,
         w1 = -1, b1 = -1, w2 = -1, b2 = -1;
     uint64_t n_floats = 0, wire_bytes = 0, n_params = 0;
+    // Split master image: [wire image | low halves of the matrices]. A matrix parameter's fp32
+    // bits are (hi << 16 | lo): hi, the bf16 truncation the GEMMs multiply, lives in the wire
+    // image, lo in the plane after it. The forward streams the wire prefix alone (2 B per
+    // matrix parameter), the backward the whole image; the master stays exact fp32.
+    uint64_t lo_bytes = 0, split_bytes = 0;
     bool rms() const { return desc.norm == SP_NORM_RMS; }
     bool swiglu() const { return desc.mlp == SP_MLP_SWIGLU; }
     int gelu_kind() const { return desc.mlp == SP_MLP_GELU_ERF ? 1 : 0; }

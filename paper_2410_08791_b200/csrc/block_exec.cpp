@@ -117,6 +117,21 @@ void Executor::block_alloc(int64_t R, int items, bool train, const std::function
     bcol_ = static_cast<float*>(alloc(col * 4));
 }
 
+// The update regions of a split master in slot `slot` (block.hpp): each tensor's halves or fp32
+// vector, at its logical offset in the gradient / moment arrays.
+SplitRegions Executor::split_regions(int slot) const {
+    SplitRegions r;
+    uint8_t* base = slot_ptr(slot);
+    for (const BlockTensor& t : lay_.t) {
+        r.hi[r.n] = base + t.wire_off;
+        r.lo[r.n] = t.matrix ? reinterpret_cast<uint16_t*>(base + lay_.wire_bytes + t.lo_off) : nullptr;
+        r.off[r.n] = static_cast<int64_t>(t.off);
+        r.count[r.n] = static_cast<int64_t>(t.count());
+        ++r.n;
+    }
+    return r;
+}
+
 // The slot's bf16 operand region in wire layout: matrices converted, vectors copied (fp32).
 void Executor::block_convert(int slot, cudaStream_t st) {
     ConvertRegions r;
@@ -385,7 +400,7 @@ void Executor::block_compute(const Op& op, bool train, int64_t rows, int fmt) {
     cudaStream_t st = s_comp_;
     if (rows % lay_.desc.seq_len != 0)
         throw Error(SP_ERR_INVALID, "rows must be a multiple of the block's seq_len");
-    if (fmt != kFmtBf16Infer && w16_layer_[s] != L) {  // training: the slot's bf16 operand copy
+    if (!split_ && fmt != kFmtBf16Infer && w16_layer_[s] != L) {  // plain master: the bf16 operand copy
         block_convert(s, st);
         w16_layer_[s] = L;
     }

@@ -83,6 +83,7 @@ Executor::Executor(const sp_config& cfg, const sp_block_desc* block) : cfg_(cfg)
         if (cfg.numerics != SP_NUMERICS_BF16)
             throw Error(SP_ERR_INVALID, "transformer blocks run in bf16 numerics (SP_NUMERICS_BF16)");
         blk_ = true;
+        split_ = true;
     }
     if (n_ < 1) throw Error(SP_ERR_INVALID, "build_model: n_layers must be >= 1");
     if (d_ < 1) throw Error(SP_ERR_INVALID, "build_model: d must be >= 1");
@@ -108,9 +109,12 @@ Executor::Executor(const sp_config& cfg, const sp_block_desc* block) : cfg_(cfg)
     if (cfg.device < 0 || cfg.device >= ndev) throw Error(SP_ERR_INVALID, "device ordinal out of range");
     CUDA_OK(cudaSetDevice(cfg.device));
 
-    CUDA_OK(cudaHostAlloc(&host32_, static_cast<size_t>(n_) * img_f() * 4, cudaHostAllocPortable));
-    std::memset(host32_, 0, static_cast<size_t>(n_) * img_f() * 4);
-    if (bf16_) CUDA_OK(cudaHostAlloc(&host16_, static_cast<size_t>(n_) * wire16_bytes(), cudaHostAllocPortable));
+    host_stride_ = blk_ ? round_up(std::max<size_t>(lay_.split_bytes, img_f() * 4), 256) : img_f() * 4;
+    CUDA_OK(cudaHostAlloc(&host32_, static_cast<size_t>(n_) * host_stride_, cudaHostAllocPortable));
+    std::memset(host32_, 0, static_cast<size_t>(n_) * host_stride_);
+    // the bf16 inference wire image: a separate host copy for dense layers, the split master's
+    // own prefix for blocks (allocated when dp_init turns the split layout off)
+    if (bf16_ && !split_) CUDA_OK(cudaHostAlloc(&host16_, static_cast<size_t>(n_) * wire16_bytes(), cudaHostAllocPortable));
 
     n_slots_ = ring_slots(cfg.strategy, cfg.k, cfg.k_prime, n_);
     layout_slots(1);
@@ -183,11 +187,22 @@ Executor::~Executor() {
 void Executor::layout_slots(int world) {
     shardA_ = shard_bytes(layer_bytes(), world);
     shardB_ = shard_bytes(wire16_bytes(), world);
-    const size_t a_region = round_up(shardA_ * world, 1024);
-    off_m_ = adamw() ? a_region : 0;
-    off_v_ = adamw() ? 2 * a_region : 0;
-    off_w16_ = adamw() ? 3 * a_region : a_region;
-    slot_bytes_ = bf16_ ? round_up(off_w16_ + shardB_ * world, 1024) : off_w16_;
+    if (split_) {
+        // [A: split image, whose wire prefix is the GEMM operand] [M][V: AdamW, fp32 logical]
+        const size_t a_region = round_up(layer_bytes(), 1024), o_region = round_up(opt_bytes(), 1024);
+        off_m_ = adamw() ? a_region : 0;
+        off_v_ = adamw() ? a_region + o_region : 0;
+        fp_bytes_ = a_region + (adamw() ? 2 * o_region : 0);
+        off_w16_ = 0;
+        slot_bytes_ = fp_bytes_;
+    } else {
+        const size_t a_region = round_up(shardA_ * world, 1024);
+        off_m_ = adamw() ? a_region : 0;
+        off_v_ = adamw() ? 2 * a_region : 0;
+        off_w16_ = adamw() ? 3 * a_region : a_region;
+        fp_bytes_ = off_w16_;
+        slot_bytes_ = bf16_ ? round_up(off_w16_ + shardB_ * world, 1024) : off_w16_;
+    }
     if (slots_dev_) {
         CUDA_OK(cudaDeviceSynchronize());
         cudaFree(slots_dev_);
@@ -215,7 +230,7 @@ void Executor::layout_slots(int world) {
 void Executor::ensure_stages() {
     if (stages_dev_ || !staged_writeback_) return;
     n_stages_ = std::max(1, std::min(n_slots_, wb_stages_cap_));
-    stage_bytes_ = off_w16_;  // [A] or [A][M][V]: the slot minus its bf16 wire region
+    stage_bytes_ = fp_bytes_;  // [A] or [A][M][V]: the slot minus its bf16 wire region
     CUDA_OK(cudaMalloc(&stages_dev_, static_cast<size_t>(n_stages_) * stage_bytes_));
 }
 
@@ -225,14 +240,13 @@ void Executor::flush_writebacks() {
     if (pending_wb_layers_.empty()) return;
     CUDA_OK(cudaSetDevice(cfg_.device));
     for (auto s : {s_h2d_, s_comp_, s_d2h_, s_upd_}) CUDA_OK(cudaStreamSynchronize(s));
-    const size_t img = layer_bytes();
+    const size_t img = layer_bytes(), ob = opt_bytes();
     for (size_t i = 0; i < pending_wb_layers_.size(); ++i) {
         const int L = pending_wb_layers_[i], s = pending_wb_slots_[i];
-        const size_t off = static_cast<size_t>(L) * img_f();
-        CUDA_OK(cudaMemcpyAsync(host32_ + off, slot_ptr(s), img, cudaMemcpyDeviceToHost, s_d2h_));
+        CUDA_OK(cudaMemcpyAsync(host_layer(L), slot_ptr(s), img, cudaMemcpyDeviceToHost, s_d2h_));
         if (adamw()) {
-            CUDA_OK(cudaMemcpyAsync(host_m_ + off, slot_m32(s), img, cudaMemcpyDeviceToHost, s_d2h_));
-            CUDA_OK(cudaMemcpyAsync(host_v_ + off, slot_v32(s), img, cudaMemcpyDeviceToHost, s_d2h_));
+            CUDA_OK(cudaMemcpyAsync(host_opt(host_m_, L), slot_m32(s), ob, cudaMemcpyDeviceToHost, s_d2h_));
+            CUDA_OK(cudaMemcpyAsync(host_opt(host_v_, L), slot_v32(s), ob, cudaMemcpyDeviceToHost, s_d2h_));
         }
         host16_stale_[static_cast<size_t>(L)] = 1;
     }
@@ -277,7 +291,7 @@ void Executor::share_host_master(const char* name, bool create) {
     CUDA_OK(cudaSetDevice(cfg_.device));
     for (auto s : {s_h2d_, s_comp_, s_d2h_, s_upd_}) CUDA_OK(cudaStreamSynchronize(s));
     const std::string nm = name[0] == '/' ? std::string(name) : "/" + std::string(name);
-    const size_t master = static_cast<size_t>(n_) * img_f() * 4;
+    const size_t master = static_cast<size_t>(n_) * host_stride_;
     const size_t ver_off = round_up(offsetof(ShmHeader, meta) + 12 * static_cast<size_t>(n_), 8);
     const size_t off = round_up(ver_off + 8 * static_cast<size_t>(n_), 4096);
     const size_t bytes = off + master;
@@ -411,7 +425,7 @@ void Executor::check_ready() {
 }
 
 void Executor::refresh_host16() {
-    if (!bf16_) return;
+    if (!bf16_ || split_) return;  // (split masters stream their own wire prefix)
     std::vector<int> todo;
     for (int i = 0; i < n_; ++i) {
         const uint64_t v = layer_version(i);  // another process may have written the master
@@ -423,7 +437,7 @@ void Executor::refresh_host16() {
     if (blk_) {  // wire image: matrices bf16, vectors fp32, each at its layout offset
         parallel_for(static_cast<int>(todo.size()), [&](int t) {
             const int L = todo[t];
-            const float* src = host32_ + static_cast<size_t>(L) * img_f();
+            const float* src = reinterpret_cast<const float*>(host_layer(L));
             uint8_t* dst = host16_ + static_cast<size_t>(L) * wire16_bytes();
             for (const BlockTensor& x : lay_.t) {
                 if (x.matrix) {
@@ -547,7 +561,8 @@ Plan Executor::make_plan(bool train, int n_items, int64_t rows, int fmt) {
     in.capacity = cfg_.capacity_bytes;
     in.sharded = sharded_;
     in.eager = eager_prefetch_;
-    in.optimizer_state = train && adamw();
+    // AdamW state, and the split master's low halves, ride every trainable backward claim
+    in.optimizer_state = train && (adamw() || split_);
     in.wb_stages = train && stages_dev_ ? n_stages_ : 0;
     // (checkpointing: the D2H engine carries the forward's activation offloads - no deferral;
     // a master shared outside data parallel must be complete when the call returns)
@@ -883,6 +898,12 @@ void Executor::update_op(const Op& op, float lr) {
                 exact_sgd(slot_w32(s) + lo / 4, mine, count, lr, st);
             ++kernels_;
         }
+    } else if (split_) {
+        // split master: the (all-reduced) logical gradient updates the halves in place
+        if (comm_) NCCL_OK(nccl().AllReduce(g, g, imgf, ncclFloat, ncclSum, comm_, st));
+        split_update(split_regions(s), g, adamw() ? slot_m32(s) : nullptr, adamw() ? slot_v32(s) : nullptr, lr,
+                     adamw() ? 1 : 0, adamw_dev_, st);
+        ++kernels_;
     } else {
         if (comm_) NCCL_OK(nccl().AllReduce(g, g, imgf, ncclFloat, ncclSum, comm_, st));
         if (adamw())  // [W|b], [mW|mb], [vW|vb] are each contiguous
@@ -934,15 +955,19 @@ void Executor::enqueue_op(const Plan& plan, int i, bool train, int n_items, int6
                     for (int dep : op.move_deps[j]) wait(dep);
                     if (j == 0 && cfg_.trace >= 1) record_timing(ev_start_[static_cast<size_t>(i)], st);
                 }
-                if (op.weights[j]) {
+                if (op.weights[j] && split_) {
+                    // the split master's wire prefix: the bf16 operands (forward, backward, inference)
+                    uint8_t* dst = slot_ptr(s);
+                    if (poison_) CUDA_OK(cudaMemsetAsync(dst, 0xFF, layer_bytes(), st));
+                    CUDA_OK(cudaMemcpyAsync(dst, host_layer(L), lay_.wire_bytes, cudaMemcpyHostToDevice, st));
+                    h2d_bytes_ += lay_.wire_bytes;
+                } else if (op.weights[j]) {
                     // Whole image, or (sharded) only this rank's [lo, hi) byte range of it.
                     const bool wire = fmt == kFmtBf16Infer;
                     const size_t img = wire ? wire16_bytes() : layer_bytes();
                     size_t lo = 0, hi = img;
                     if (sharded_) shard_range(wire ? shardB_ : shardA_, img, lo, hi);
-                    const uint8_t* src = wire ? host16_ + static_cast<size_t>(L) * wire16_bytes()
-                                              : reinterpret_cast<const uint8_t*>(
-                                                    host32_ + static_cast<size_t>(L) * img_f());
+                    const uint8_t* src = wire ? host16_ + static_cast<size_t>(L) * wire16_bytes() : host_layer(L);
                     uint8_t* dst = wire ? slot_ptr(s) + off_w16_ : slot_ptr(s);
                     // Debug (SP_POISON=1): NaN-fill the whole image first, so a compute that
                     // reads the slot before this copy lands (a missing edge) produces NaNs.
@@ -958,16 +983,21 @@ void Executor::enqueue_op(const Plan& plan, int i, bool train, int n_items, int6
                                             cudaMemcpyHostToDevice, st));
                     h2d_bytes_ += act_b;
                 }
-                if (j < op.opts.size() && op.opts[j]) {  // AdamW m, v (sharded: this rank's shard)
-                    size_t lo = 0, hi = layer_bytes();
-                    if (sharded_) shard_range(shardA_, layer_bytes(), lo, hi);
-                    const size_t off = static_cast<size_t>(L) * img_f();
+                if (j < op.opts.size() && op.opts[j] && split_) {
+                    // the low halves the update needs (whether or not the prefix was a hit)
+                    CUDA_OK(cudaMemcpyAsync(slot_ptr(s) + lay_.wire_bytes, host_layer(L) + lay_.wire_bytes,
+                                            lay_.lo_bytes, cudaMemcpyHostToDevice, st));
+                    h2d_bytes_ += lay_.lo_bytes;
+                }
+                if (j < op.opts.size() && op.opts[j] && adamw()) {  // AdamW m, v (sharded: this rank's shard)
+                    size_t lo = 0, hi = opt_bytes();
+                    if (sharded_) shard_range(shardA_, opt_bytes(), lo, hi);
                     if (hi > lo) {
                         CUDA_OK(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(slot_m32(s)) + lo,
-                                                reinterpret_cast<const uint8_t*>(host_m_ + off) + lo, hi - lo,
+                                                reinterpret_cast<const uint8_t*>(host_opt(host_m_, L)) + lo, hi - lo,
                                                 cudaMemcpyHostToDevice, st));
                         CUDA_OK(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(slot_v32(s)) + lo,
-                                                reinterpret_cast<const uint8_t*>(host_v_ + off) + lo, hi - lo,
+                                                reinterpret_cast<const uint8_t*>(host_opt(host_v_, L)) + lo, hi - lo,
                                                 cudaMemcpyHostToDevice, st));
                     }
                     h2d_bytes_ += 2 * (hi - lo);
@@ -990,7 +1020,18 @@ void Executor::enqueue_op(const Plan& plan, int i, bool train, int n_items, int6
                 if (sharded_) shard_range(shardA_, layer_bytes(), lo, hi);
                 uint8_t* stage = stage_ptr(op.stage);
                 const uint8_t* slot = slot_ptr(op.slot);
-                if (hi > lo) {  // an SM kernel: copy engines stay with the PCIe transfers
+                if (hi > lo && split_) {  // split master: its image, and the moments (own size)
+                    void* dst[1] = {stage};
+                    const void* src[1] = {slot};
+                    copy_regions(dst, src, 1, static_cast<int64_t>(layer_bytes()), st);
+                    ++kernels_;
+                    if (adamw()) {
+                        void* dm[2] = {stage + off_m_, stage + off_v_};
+                        const void* sm[2] = {slot + off_m_, slot + off_v_};
+                        copy_regions(dm, sm, 2, static_cast<int64_t>(opt_bytes()), st);
+                        ++kernels_;
+                    }
+                } else if (hi > lo) {  // an SM kernel: copy engines stay with the PCIe transfers
                     void* dst[3] = {stage + lo, stage + off_m_ + lo, stage + off_v_ + lo};
                     const void* src[3] = {slot + lo, slot + off_m_ + lo, slot + off_v_ + lo};
                     copy_regions(dst, src, adamw() ? 3 : 1, static_cast<int64_t>(hi - lo), st);
@@ -1010,17 +1051,17 @@ void Executor::enqueue_op(const Plan& plan, int i, bool train, int n_items, int6
             size_t lo = 0, hi = layer_bytes();
             if (sharded_) shard_range(shardA_, layer_bytes(), lo, hi);
             const uint8_t* src = op.stage >= 0 ? stage_ptr(op.stage) : slot_ptr(s);
-            const size_t off = static_cast<size_t>(L) * img_f();
             if (hi > lo)
-                CUDA_OK(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(host32_ + off) + lo, src + lo, hi - lo,
-                                        cudaMemcpyDeviceToHost, st));
+                CUDA_OK(cudaMemcpyAsync(host_layer(L) + lo, src + lo, hi - lo, cudaMemcpyDeviceToHost, st));
             d2h_bytes_ += hi - lo;
-            if (adamw() && hi > lo) {  // the optimizer state rides the write-back
-                CUDA_OK(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(host_m_ + off) + lo, src + off_m_ + lo,
-                                        hi - lo, cudaMemcpyDeviceToHost, st));
-                CUDA_OK(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(host_v_ + off) + lo, src + off_v_ + lo,
-                                        hi - lo, cudaMemcpyDeviceToHost, st));
-                d2h_bytes_ += 2 * (hi - lo);
+            size_t mlo = 0, mhi = opt_bytes();
+            if (sharded_) shard_range(shardA_, opt_bytes(), mlo, mhi);
+            if (adamw() && mhi > mlo) {  // the optimizer state rides the write-back
+                CUDA_OK(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(host_opt(host_m_, L)) + mlo, src + off_m_ + mlo,
+                                        mhi - mlo, cudaMemcpyDeviceToHost, st));
+                CUDA_OK(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(host_opt(host_v_, L)) + mlo, src + off_v_ + mlo,
+                                        mhi - mlo, cudaMemcpyDeviceToHost, st));
+                d2h_bytes_ += 2 * (mhi - mlo);
             }
             break;
         }
@@ -1487,7 +1528,15 @@ void Executor::digest_train(float loss, char out[17]) {
         }
     };
     fnv(&loss, 4);
-    fnv(host32_, static_cast<size_t>(n_) * img_f() * 4);
+    if (split_) {  // hash the fp32 images, as the reference's digest_train does
+        std::vector<float> img(img_f());
+        for (int L = 0; L < n_; ++L) {
+            unsplit_image(host_layer(L), img.data());
+            fnv(img.data(), img.size() * 4);
+        }
+    } else {
+        fnv(host32_, static_cast<size_t>(n_) * host_stride_);
+    }
     static const char digits[] = "0123456789abcdef";
     for (int i = 15; i >= 0; --i) {
         out[i] = digits[h & 0xF];
@@ -1507,12 +1556,79 @@ void Executor::read_layer(int index, float* W, float* b) {
     if (b) std::memcpy(b, src + dd, static_cast<size_t>(d_) * 4);
 }
 
+void Executor::split_image(const float* params, uint8_t* dst) const {
+    for (const BlockTensor& t : lay_.t) {
+        const float* src = params + t.off;
+        if (t.matrix) {
+            uint16_t* hi = reinterpret_cast<uint16_t*>(dst + t.wire_off);
+            uint16_t* lo = reinterpret_cast<uint16_t*>(dst + lay_.wire_bytes + t.lo_off);
+            for (uint64_t e = 0; e < t.count(); ++e) {
+                uint32_t u;
+                std::memcpy(&u, src + e, 4);
+                hi[e] = static_cast<uint16_t>(u >> 16);
+                lo[e] = static_cast<uint16_t>(u & 0xFFFFu);
+            }
+        } else {
+            std::memcpy(dst + t.wire_off, src, t.count() * 4);
+        }
+    }
+}
+
+void Executor::unsplit_image(const uint8_t* src, float* params) const {
+    std::memset(params, 0, img_f() * 4);
+    for (const BlockTensor& t : lay_.t) {
+        float* out = params + t.off;
+        if (t.matrix) {
+            const uint16_t* hi = reinterpret_cast<const uint16_t*>(src + t.wire_off);
+            const uint16_t* lo = reinterpret_cast<const uint16_t*>(src + lay_.wire_bytes + t.lo_off);
+            for (uint64_t e = 0; e < t.count(); ++e) {
+                const uint32_t u = static_cast<uint32_t>(hi[e]) << 16 | lo[e];
+                std::memcpy(out + e, &u, 4);
+            }
+        } else {
+            std::memcpy(out, src + t.wire_off, t.count() * 4);
+        }
+    }
+}
+
+// Switches a block master between the split image and the plain fp32 image (host side; the
+// slots are re-laid out by the caller).
+void Executor::set_split(bool on) {
+    if (split_ == on || !blk_) return;
+    flush_writebacks();
+    CUDA_OK(cudaSetDevice(cfg_.device));
+    for (auto st : {s_h2d_, s_comp_, s_d2h_, s_upd_}) CUDA_OK(cudaStreamSynchronize(st));
+    if (!shm_ || shm_owner_) {
+        std::vector<float> img(img_f());
+        std::vector<uint8_t> tmp(host_stride_);
+        for (int L = 0; L < n_; ++L) {
+            if (on) {
+                std::memcpy(img.data(), host_layer(L), img_f() * 4);
+                std::memset(tmp.data(), 0, tmp.size());
+                split_image(img.data(), tmp.data());
+                std::memcpy(host_layer(L), tmp.data(), host_stride_);
+            } else {
+                unsplit_image(host_layer(L), img.data());
+                std::memcpy(host_layer(L), img.data(), img_f() * 4);
+            }
+        }
+    }
+    split_ = on;
+    if (!split_ && bf16_ && !host16_)
+        CUDA_OK(cudaHostAlloc(&host16_, static_cast<size_t>(n_) * wire16_bytes(), cudaHostAllocPortable));
+    std::fill(host16_stale_.begin(), host16_stale_.end(), 1);
+    for (auto& c : cache_) c.valid = false;
+    std::fill(w16_layer_.begin(), w16_layer_.end(), -1);
+    for (int L = 0; L < n_; ++L) bump_version(L);
+}
+
 void Executor::register_block(int index, const float* params, int frozen) {
     if (!blk_) throw Error(SP_ERR_INVALID, "register_block: this executor streams dense layers (sp_register_layer)");
     if (index < 0 || index >= n_) throw Error(SP_ERR_INVALID, "register_block: index out of range");
     if (!params) throw Error(SP_ERR_INVALID, "register_block: null parameters");
     flush_writebacks();
-    std::memcpy(host32_ + static_cast<size_t>(index) * img_f(), params, img_f() * 4);
+    if (split_) split_image(params, host_layer(index));
+    else std::memcpy(host_layer(index), params, img_f() * 4);
     relu_[index] = 0;
     frozen_[index] = frozen != 0;
     registered_[index] = 1;
@@ -1531,7 +1647,8 @@ void Executor::read_block(int index, float* params) {
     if (!params) throw Error(SP_ERR_INVALID, "read_block: null output");
     flush_writebacks();
     require_full_host(index, "read_block");
-    std::memcpy(params, host32_ + static_cast<size_t>(index) * img_f(), img_f() * 4);
+    if (split_) unsplit_image(host_layer(index), params);
+    else std::memcpy(params, host_layer(index), img_f() * 4);
 }
 
 void Executor::dp_init(const uint8_t id[128], int rank, int world, bool shard_weights) {
@@ -1555,6 +1672,10 @@ void Executor::dp_init(const uint8_t id[128], int rank, int world, bool shard_we
     }
     ncclUniqueId uid;
     std::memcpy(uid.internal, id, sizeof(uid.internal));
+    // Byte shards of a split master would not line up with the gradient's logical shards: sharded
+    // streaming keeps the fp32 image (the owner of a shared master converts it; CommInitRank below
+    // waits for every rank, so the others see the converted copy).
+    if (shard_weights && split_) set_split(false);
     NCCL_OK(nccl().CommInitRank(&comm_, world, uid, rank));
     rank_ = rank;
     world_ = world;
@@ -1596,9 +1717,8 @@ void Executor::read_optimizer_state(int index, float* mW, float* mb, float* vW, 
     flush_writebacks();
     require_full_host(index, "read_optimizer_state");
     if (blk_) {  // a block's state is flat like its image: mW, vW receive all of it
-        const size_t off = static_cast<size_t>(index) * img_f();
-        if (mW) std::memcpy(mW, host_m_ + off, img_f() * 4);
-        if (vW) std::memcpy(vW, host_v_ + off, img_f() * 4);
+        if (mW) std::memcpy(mW, host_opt(host_m_, index), img_f() * 4);
+        if (vW) std::memcpy(vW, host_opt(host_v_, index), img_f() * 4);
         return;
     }
     const size_t dd = static_cast<size_t>(d_) * d_, off = static_cast<size_t>(index) * (dd + d_);
@@ -1633,7 +1753,7 @@ void Executor::dp_sync() {
         // shared master (share_host_master) already holds every rank's shard: a barrier below.
         for (float* base : {shm_ ? nullptr : host32_, adamw() ? host_m_ : nullptr, adamw() ? host_v_ : nullptr}) {
             if (!base) continue;
-            uint8_t* host = reinterpret_cast<uint8_t*>(base + static_cast<size_t>(L) * img_f());
+            uint8_t* host = base == host32_ ? host_layer(L) : reinterpret_cast<uint8_t*>(host_opt(base, L));
             if (hi > lo) CUDA_OK(cudaMemcpyAsync(stage + lo, host + lo, hi - lo, cudaMemcpyHostToDevice, s_upd_));
             NCCL_OK(nccl().AllGather(stage + shardA_ * static_cast<size_t>(rank_), stage, shardA_,
                                      ncclUint8, comm_, s_upd_));

@@ -67,8 +67,15 @@ public:
 
 private:
     // layout helpers: a layer's fp32 image is [W | b] (dense) or the block image (block.hpp)
+    // img_f: floats of a layer's logical fp32 image (the gradient / AdamW-state layout).
+    // layer_bytes: bytes of the master as stored and streamed - the fp32 image, or (split_) the
+    // split image [wire | low halves] of block.hpp. opt_bytes: one AdamW moment array.
     size_t img_f() const { return blk_ ? static_cast<size_t>(lay_.n_floats) : static_cast<size_t>(d_) * d_ + d_; }
-    uint64_t layer_bytes() const { return static_cast<uint64_t>(img_f()) * 4; }
+    uint64_t layer_bytes() const { return split_ ? lay_.split_bytes : static_cast<uint64_t>(img_f()) * 4; }
+    uint64_t opt_bytes() const { return static_cast<uint64_t>(img_f()) * 4; }
+    // host master of layer L: one stride fits either block layout, so dp_init can switch in place
+    uint8_t* host_layer(int L) const { return reinterpret_cast<uint8_t*>(host32_) + static_cast<size_t>(L) * host_stride_; }
+    float* host_opt(float* base, int L) const { return base + static_cast<size_t>(L) * img_f(); }
     uint64_t wire16_bytes() const {
         return blk_ ? lay_.wire_bytes : static_cast<uint64_t>(d_) * d_ * 2 + d_ * 4ull;
     }
@@ -155,6 +162,16 @@ private:
     int n_ = 0, d_ = 0;
     bool blk_ = false;  // named-shape transformer layers (block.hpp) instead of dense blocks
     BlockLayout lay_;
+    // Split master (block.hpp): the forward streams only the wire prefix of each layer. Off in
+    // sharded data parallel (whose byte shards assume the fp32 image), where the slot keeps a
+    // device-converted bf16 copy instead.
+    bool split_ = false;
+    size_t host_stride_ = 0;
+    size_t fp_bytes_ = 0;  // slot bytes of the fp32 master regions [A][M][V] (the write-back stage)
+    void split_image(const float* params, uint8_t* dst) const;    // fp32 image -> split image
+    void unsplit_image(const uint8_t* src, float* params) const;  // split image -> fp32 image
+    void set_split(bool on);
+    SplitRegions split_regions(int slot) const;
     // block-mode device buffers
     std::vector<float*> bx_;            // training: residual stream x_0..x_n (fp32; x_n = yout_)
     std::vector<BlockActs> bsv_;        // training: per-layer saved intermediates (no offload)

@@ -144,6 +144,19 @@ struct ConvertRegions {
     int to_bf16[16];
 };
 void convert_regions(const ConvertRegions& r, cudaStream_t st);
+// Update of a split master image (block.hpp): per tensor region, the fp32 parameter is
+// (hi << 16 | lo) for matrices (hi in the wire prefix, lo in the low plane) or a plain fp32
+// vector; g (and AdamW m, v) are in the logical fp32 layout. SGD (opt 0, model.cpp:150-155:
+// w -= lr g, no FMA) or AdamW (opt 1, adamw_reduce's arithmetic). Up to 16 regions, one launch.
+struct SplitRegions {
+    int n = 0;
+    void* hi[16];        // matrices: uint16 hi halves; vectors: fp32 values
+    uint16_t* lo[16];    // matrices: low halves; vectors: nullptr
+    int64_t off[16];     // logical offset (floats) of the region in g / m / v
+    int64_t count[16];   // elements
+};
+void split_update(const SplitRegions& r, const float* g, float* m, float* v, float lr, int opt,
+                  const AdamwScalars* scalars, cudaStream_t st);
 // n (<= 3) device-to-device copies of `bytes` each (multiple of 4, 4-byte aligned) on the SMs.
 void copy_regions(void* const* dst, const void* const* src, int n, int64_t bytes, cudaStream_t st);
 void adamw_reduce(float* w, float* m, float* v, const float* parts, int nparts, int64_t stride,

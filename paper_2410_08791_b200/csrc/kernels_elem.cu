@@ -453,4 +453,53 @@ void convert_regions(const ConvertRegions& r, cudaStream_t st) {
     launch_kernel(convert_regions_kernel, dim3(bx, static_cast<unsigned>(r.n)), dim3(kThreads), 0, st, r);
 }
 
+namespace {
+// One thread per parameter of region blockIdx.y: rebuild the fp32 master from its halves (or
+// read the fp32 vector), apply the update in the reference's order, store it back split.
+__global__ void split_update_kernel(SplitRegions r, const float* __restrict__ g, float* __restrict__ m,
+                                    float* __restrict__ v, float lr, int opt, const AdamwScalars* __restrict__ sc) {
+    const int i = blockIdx.y;
+    const int64_t n = r.count[i];
+    const int64_t base = r.off[i];
+    const bool matrix = r.lo[i] != nullptr;
+    AdamwScalars s{};
+    if (opt == 1) s = *sc;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += stride) {
+        float w;
+        if (matrix) {
+            const uint32_t hi = static_cast<const uint16_t*>(r.hi[i])[e], lo = r.lo[i][e];
+            w = __uint_as_float(hi << 16 | lo);
+        } else {
+            w = static_cast<const float*>(r.hi[i])[e];
+        }
+        const float gr = g[base + e];
+        if (opt == 1) {
+            float mm = m[base + e], vv = v[base + e];
+            adamw_elem(w, mm, vv, gr, s);
+            m[base + e] = mm;
+            v[base + e] = vv;
+        } else {
+            w = __fsub_rn(w, __fmul_rn(lr, gr));
+        }
+        if (matrix) {
+            const uint32_t bits = __float_as_uint(w);
+            static_cast<uint16_t*>(r.hi[i])[e] = static_cast<uint16_t>(bits >> 16);
+            r.lo[i][e] = static_cast<uint16_t>(bits & 0xFFFFu);
+        } else {
+            static_cast<float*>(r.hi[i])[e] = w;
+        }
+    }
+}
+}  // namespace
+
+void split_update(const SplitRegions& r, const float* g, float* m, float* v, float lr, int opt,
+                  const AdamwScalars* scalars, cudaStream_t st) {
+    if (r.n <= 0) return;
+    int64_t most = 0;
+    for (int i = 0; i < r.n; ++i) most = most > r.count[i] ? most : r.count[i];
+    launch_kernel(split_update_kernel, dim3(grid_for(most), static_cast<unsigned>(r.n)), dim3(kThreads), 0, st, r,
+                  g, m, v, lr, opt, scalars);
+}
+
 }  // namespace sp

@@ -136,9 +136,12 @@ def test_block_adamw_and_single_rank_dp_paths_are_window_invariant():
         if mode in by_mode:
             assert by_mode[mode][0] == losses and np.array_equal(by_mode[mode][1], params), mode
         by_mode[mode] = (losses, params)
-    # 1-rank data parallel (NCCL all-reduce / reduce-scatter + shard SGD) equals itself across
-    # modes: the gradient is the same image, reduced over one rank
-    assert np.array_equal(by_mode["dp-allreduce"][1], by_mode["dp-sharded"][1])
+    # All-reduce mode keeps the split master (the GEMMs multiply the bf16 truncation of each
+    # weight); sharded streaming keeps the fp32 image and converts it on the device (round to
+    # nearest). Each is window-invariant above; across the two only the operand rounding differs.
+    base = model.params
+    a_, b_ = by_mode["dp-allreduce"][1], by_mode["dp-sharded"][1]
+    assert nrm(a_ - base, b_ - base) < 5e-2  # the two updates agree to bf16 operand precision
 
 
 def test_bench_shape_gpt2_xl_two_layers_against_torch_fp32():
