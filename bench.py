@@ -44,7 +44,7 @@ def parse():
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--model", default="gpt2-xl", choices=["gpt2-xl", "vit-h14", "llama3-8b", "dense"],
+    p.add_argument("--model", default="gpt2-xl", choices=["gpt2-xl", "vit-h14", "llama3-8b", "llama3-70b", "dense"],
                    help="named-shape transformer layers (SURVEY 8(d)) or round 1's square stand-in")
     p.add_argument("--layers", type=int, default=0, help="0 = the model's own layer count")
     p.add_argument("--seqs", type=int, default=16, help="sequences per GPU per step (named shapes)")
@@ -71,9 +71,14 @@ def parse():
     p.add_argument("--no-variants", action="store_true",
                    help="skip the in-run variants of the same step ('variants')")
     p.add_argument("--sweep", default="", help="comma list of k:kp to report extra lines")
+    p.add_argument("--capacity-gb", type=float, default=0.0,
+                   help="HBM budget of the ledger (ArenaConfig::capacity_bytes; C5: 40 GB)")
+    p.add_argument("--distinct-layers", type=int, default=0,
+                   help="--infer: initialise this many distinct layers and register them round-robin "
+                        "(0 = every layer distinct; a 70B-shape model's 80 layers take minutes to generate)")
     a = p.parse_args()
     if a.layers == 0:
-        a.layers = {"dense": 48, "gpt2-xl": 48, "vit-h14": 32, "llama3-8b": 32}[a.model]
+        a.layers = {"dense": 48, "gpt2-xl": 48, "vit-h14": 32, "llama3-8b": 32, "llama3-70b": 80}[a.model]
     return a
 
 
@@ -619,12 +624,21 @@ def run_block_infer(a, rank, world, local, torch, dist, sp, pk, pk_src, strategy
         spec = spec.with_seq(a.seq_len)
     lay = B.block_layout(spec)
     rows = a.seqs * spec.seq_len
-    ex = B.BlockExecutor(a.layers, spec, strategy, device=local, trace=0)
-    params = np.empty(lay.n_floats, np.float32)
+    ex = B.BlockExecutor(a.layers, spec, strategy, device=local, trace=0,
+                         capacity_bytes=int(a.capacity_gb * 1e9))
     desc = spec.desc()
-    for i in range(a.layers):  # layer by layer: no second full host copy of the model
+    distinct = a.distinct_layers or a.layers
+    images = []
+    for i in range(min(distinct, a.layers)):  # layer by layer: no second full host copy of the model
+        params = np.empty(lay.n_floats, np.float32)
         _capi.check(_capi.LIB.sp_build_block(ctypes.byref(desc), 7, i, params.ctypes.data))
-        ex.register_block(i, params)
+        images.append(params)
+        if distinct >= a.layers:
+            ex.register_block(i, params)
+            images = []
+    if images:
+        for i in range(a.layers):
+            ex.register_block(i, images[i % len(images)])
     note = None
     if world > 1 and not a.private_host_copies:
         note = dp.share_host_master(ex, dist, local, f"/sp_bench_infer_{os.environ.get('MASTER_PORT', '0')}")
@@ -668,7 +682,9 @@ def run_block_infer(a, rank, world, local, torch, dist, sp, pk, pk_src, strategy
             "config": dict(config_of(a, world), workload=f"{spec.name}-shape stack: {a.layers} transformer "
                            f"layers, bf16 inference (run_inference), {a.seqs} x {spec.seq_len} tokens per GPU, "
                            f"{'replicas' if world > 1 else 'one ring'}", mode="inference",
-                           parallelism=f"replicas x{world}" if world > 1 else "dp1"),
+                           parallelism=f"replicas x{world}" if world > 1 else "dp1",
+                           capacity_gb=a.capacity_gb or None,
+                           distinct_layer_images=min(a.distinct_layers or a.layers, a.layers)),
             "sequences_per_sec": value / spec.seq_len,
             "peak_hbm_gb": {"ledger": last["peak_bytes"] / 1e9, "ledger_weights": last["peak_weight_bytes"] / 1e9,
                             "measured_reserved": last["hbm_reserved_bytes"] / 1e9,

@@ -1556,21 +1556,27 @@ void Executor::read_layer(int index, float* W, float* b) {
     if (b) std::memcpy(b, src + dd, static_cast<size_t>(d_) * 4);
 }
 
+// Host conversions between a block's fp32 image and its split image, over host threads (a
+// Llama-3-70B-shape layer holds 856M parameters).
 void Executor::split_image(const float* params, uint8_t* dst) const {
     for (const BlockTensor& t : lay_.t) {
         const float* src = params + t.off;
-        if (t.matrix) {
-            uint16_t* hi = reinterpret_cast<uint16_t*>(dst + t.wire_off);
-            uint16_t* lo = reinterpret_cast<uint16_t*>(dst + lay_.wire_bytes + t.lo_off);
-            for (uint64_t e = 0; e < t.count(); ++e) {
+        if (!t.matrix) {
+            std::memcpy(dst + t.wire_off, src, t.count() * 4);
+            continue;
+        }
+        uint16_t* hi = reinterpret_cast<uint16_t*>(dst + t.wire_off);
+        uint16_t* lo = reinterpret_cast<uint16_t*>(dst + lay_.wire_bytes + t.lo_off);
+        const uint64_t n = t.count(), chunk = 1 << 20;
+        parallel_for(static_cast<int>((n + chunk - 1) / chunk), [&](int c) {
+            const uint64_t e1 = std::min<uint64_t>(n, (static_cast<uint64_t>(c) + 1) * chunk);
+            for (uint64_t e = static_cast<uint64_t>(c) * chunk; e < e1; ++e) {
                 uint32_t u;
                 std::memcpy(&u, src + e, 4);
                 hi[e] = static_cast<uint16_t>(u >> 16);
                 lo[e] = static_cast<uint16_t>(u & 0xFFFFu);
             }
-        } else {
-            std::memcpy(dst + t.wire_off, src, t.count() * 4);
-        }
+        });
     }
 }
 
@@ -1578,16 +1584,20 @@ void Executor::unsplit_image(const uint8_t* src, float* params) const {
     std::memset(params, 0, img_f() * 4);
     for (const BlockTensor& t : lay_.t) {
         float* out = params + t.off;
-        if (t.matrix) {
-            const uint16_t* hi = reinterpret_cast<const uint16_t*>(src + t.wire_off);
-            const uint16_t* lo = reinterpret_cast<const uint16_t*>(src + lay_.wire_bytes + t.lo_off);
-            for (uint64_t e = 0; e < t.count(); ++e) {
+        if (!t.matrix) {
+            std::memcpy(out, src + t.wire_off, t.count() * 4);
+            continue;
+        }
+        const uint16_t* hi = reinterpret_cast<const uint16_t*>(src + t.wire_off);
+        const uint16_t* lo = reinterpret_cast<const uint16_t*>(src + lay_.wire_bytes + t.lo_off);
+        const uint64_t n = t.count(), chunk = 1 << 20;
+        parallel_for(static_cast<int>((n + chunk - 1) / chunk), [&](int c) {
+            const uint64_t e1 = std::min<uint64_t>(n, (static_cast<uint64_t>(c) + 1) * chunk);
+            for (uint64_t e = static_cast<uint64_t>(c) * chunk; e < e1; ++e) {
                 const uint32_t u = static_cast<uint32_t>(hi[e]) << 16 | lo[e];
                 std::memcpy(out + e, &u, 4);
             }
-        } else {
-            std::memcpy(out, src + t.wire_off, t.count() * 4);
-        }
+        });
     }
 }
 
