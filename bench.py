@@ -624,8 +624,10 @@ def run_block_infer(a, rank, world, local, torch, dist, sp, pk, pk_src, strategy
         spec = spec.with_seq(a.seq_len)
     lay = B.block_layout(spec)
     rows = a.seqs * spec.seq_len
+    # inference keeps only the bf16 wire image on the host (SP_BLOCK_INFER_ONLY): a 70B-shape
+    # model's fp32 master (274 GB) would not fit a 196 GB host
     ex = B.BlockExecutor(a.layers, spec, strategy, device=local, trace=0,
-                         capacity_bytes=int(a.capacity_gb * 1e9))
+                         capacity_bytes=int(a.capacity_gb * 1e9), infer_only=True)
     desc = spec.desc()
     distinct = a.distinct_layers or a.layers
     images = []

@@ -162,8 +162,15 @@ typedef struct {
     int32_t bias;        /* linear layers carry biases */
     int32_t causal;      /* 1 decoder (causal) attention, 0 encoder (bidirectional) */
     float norm_eps;
-    int32_t reserved[5];
+    int32_t flags;       /* SP_BLOCK_INFER_ONLY: the host keeps only the bf16 wire image */
+    int32_t reserved[4];
 } sp_block_desc;
+/* sp_block_desc.flags. SP_BLOCK_INFER_ONLY: an inference-only executor whose pinned host copy
+ * is the bf16 wire image alone (2 B per matrix parameter instead of 4), for models whose fp32
+ * master would not fit host memory (a Llama-3-70B-shape stack: 137 GB of wire image against
+ * 274 GB of fp32). Registration keeps the bf16 truncation of each matrix; training calls fail
+ * with SP_ERR_INVALID; sp_read_block returns the stored (bf16-valued) parameters. */
+#define SP_BLOCK_INFER_ONLY 1
 /* One parameter tensor of a block image. */
 typedef struct {
     char name[16];

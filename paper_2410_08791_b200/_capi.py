@@ -58,7 +58,7 @@ MLP_GELU_TANH, MLP_GELU_ERF, MLP_SWIGLU = 0, 1, 2     # sp_mlp_kind
 class SpBlockDesc(C.Structure):
     _fields_ = [(n, C.c_int32) for n in (
         "kind", "d", "ff", "n_heads", "n_kv_heads", "seq_len", "norm", "mlp", "bias", "causal")] + [
-        ("norm_eps", C.c_float), ("reserved", C.c_int32 * 5)]
+        ("norm_eps", C.c_float), ("flags", C.c_int32), ("reserved", C.c_int32 * 4)]
 
 
 class SpBlockTensor(C.Structure):

@@ -44,8 +44,9 @@ class BlockSpec:
     def head_dim(self) -> int:
         return self.d // self.n_heads
 
-    def desc(self) -> capi.SpBlockDesc:
+    def desc(self, infer_only: bool = False) -> capi.SpBlockDesc:
         c = capi.SpBlockDesc()
+        c.flags = 1 if infer_only else 0  # SP_BLOCK_INFER_ONLY
         c.kind, c.d, c.ff, c.n_heads, c.n_kv_heads = capi.BLOCK_TRANSFORMER, self.d, self.ff, self.n_heads, self.n_kv_heads
         c.seq_len, c.norm, c.mlp, c.bias, c.causal = self.seq_len, self.norm, self.mlp, int(self.bias), int(self.causal)
         c.norm_eps = self.norm_eps
@@ -151,13 +152,14 @@ class BlockExecutor(Executor):
     """A ring executor over transformer blocks (sp_create_blocks); bf16 numerics."""
 
     def __init__(self, n_layers: int, spec: BlockSpec, strategy: StrategyConfig | None = None,
-                 checkpointing: bool = False, capacity_bytes: int = 0, device: int = 0, trace: bool = True):
+                 checkpointing: bool = False, capacity_bytes: int = 0, device: int = 0, trace: bool = True,
+                 infer_only: bool = False):
         strategy = strategy or StrategyConfig(SUPERPIPELINE, 2, 1)
         self.n_layers, self.d, self.strategy, self.numerics = n_layers, spec.d, strategy, BF16
         self.spec, self.layout = spec, block_layout(spec)
         self._h = C.c_void_p()
         cfg = _config(n_layers, spec.d, strategy, BF16, checkpointing, capacity_bytes, device, trace)
-        desc = spec.desc()
+        desc = spec.desc(infer_only)
         capi.check(_LIB.sp_create_blocks(C.byref(cfg), C.byref(desc), C.byref(self._h)), None)
 
     def register_block(self, index: int, params: np.ndarray, frozen: bool = False):

@@ -84,6 +84,7 @@ Executor::Executor(const sp_config& cfg, const sp_block_desc* block) : cfg_(cfg)
             throw Error(SP_ERR_INVALID, "transformer blocks run in bf16 numerics (SP_NUMERICS_BF16)");
         blk_ = true;
         split_ = true;
+        infer_only_ = (block->flags & SP_BLOCK_INFER_ONLY) != 0;
     }
     if (n_ < 1) throw Error(SP_ERR_INVALID, "build_model: n_layers must be >= 1");
     if (d_ < 1) throw Error(SP_ERR_INVALID, "build_model: d must be >= 1");
@@ -109,7 +110,9 @@ Executor::Executor(const sp_config& cfg, const sp_block_desc* block) : cfg_(cfg)
     if (cfg.device < 0 || cfg.device >= ndev) throw Error(SP_ERR_INVALID, "device ordinal out of range");
     CUDA_OK(cudaSetDevice(cfg.device));
 
-    host_stride_ = blk_ ? round_up(std::max<size_t>(lay_.split_bytes, img_f() * 4), 256) : img_f() * 4;
+    host_stride_ = infer_only_ ? round_up(lay_.wire_bytes, 256)
+                 : blk_       ? round_up(std::max<size_t>(lay_.split_bytes, img_f() * 4), 256)
+                              : img_f() * 4;
     CUDA_OK(cudaHostAlloc(&host32_, static_cast<size_t>(n_) * host_stride_, cudaHostAllocPortable));
     std::memset(host32_, 0, static_cast<size_t>(n_) * host_stride_);
     // the bf16 inference wire image: a separate host copy for dense layers, the split master's
@@ -1464,6 +1467,8 @@ float Executor::train_step(const float* x, const float* target, int64_t rows, fl
     CUDA_OK(cudaSetDevice(cfg_.device));
     if (blk_ && rows % lay_.desc.seq_len != 0)
         throw Error(SP_ERR_INVALID, "train: rows must be a multiple of the block's seq_len");
+    if (infer_only_)
+        throw Error(SP_ERR_INVALID, "train: this executor was created SP_BLOCK_INFER_ONLY (no fp32 master)");
     if (blk_ && lay_.swiglu())
         throw Error(SP_ERR_INVALID, "train: SwiGLU blocks are inference-only in this build");
     if (tc_ && !blk_) {  // split-K depends only on (d, rows): identical for every window setting
@@ -1566,7 +1571,7 @@ void Executor::split_image(const float* params, uint8_t* dst) const {
             continue;
         }
         uint16_t* hi = reinterpret_cast<uint16_t*>(dst + t.wire_off);
-        uint16_t* lo = reinterpret_cast<uint16_t*>(dst + lay_.wire_bytes + t.lo_off);
+        uint16_t* lo = infer_only_ ? nullptr : reinterpret_cast<uint16_t*>(dst + lay_.wire_bytes + t.lo_off);
         const uint64_t n = t.count(), chunk = 1 << 20;
         parallel_for(static_cast<int>((n + chunk - 1) / chunk), [&](int c) {
             const uint64_t e1 = std::min<uint64_t>(n, (static_cast<uint64_t>(c) + 1) * chunk);
@@ -1574,7 +1579,7 @@ void Executor::split_image(const float* params, uint8_t* dst) const {
                 uint32_t u;
                 std::memcpy(&u, src + e, 4);
                 hi[e] = static_cast<uint16_t>(u >> 16);
-                lo[e] = static_cast<uint16_t>(u & 0xFFFFu);
+                if (lo) lo[e] = static_cast<uint16_t>(u & 0xFFFFu);
             }
         });
     }
@@ -1589,12 +1594,12 @@ void Executor::unsplit_image(const uint8_t* src, float* params) const {
             continue;
         }
         const uint16_t* hi = reinterpret_cast<const uint16_t*>(src + t.wire_off);
-        const uint16_t* lo = reinterpret_cast<const uint16_t*>(src + lay_.wire_bytes + t.lo_off);
+        const uint16_t* lo = infer_only_ ? nullptr : reinterpret_cast<const uint16_t*>(src + lay_.wire_bytes + t.lo_off);
         const uint64_t n = t.count(), chunk = 1 << 20;
         parallel_for(static_cast<int>((n + chunk - 1) / chunk), [&](int c) {
             const uint64_t e1 = std::min<uint64_t>(n, (static_cast<uint64_t>(c) + 1) * chunk);
             for (uint64_t e = static_cast<uint64_t>(c) * chunk; e < e1; ++e) {
-                const uint32_t u = static_cast<uint32_t>(hi[e]) << 16 | lo[e];
+                const uint32_t u = static_cast<uint32_t>(hi[e]) << 16 | (lo ? lo[e] : 0u);
                 std::memcpy(out + e, &u, 4);
             }
         });
@@ -1605,6 +1610,7 @@ void Executor::unsplit_image(const uint8_t* src, float* params) const {
 // slots are re-laid out by the caller).
 void Executor::set_split(bool on) {
     if (split_ == on || !blk_) return;
+    if (infer_only_) return;  // inference replicas never shard: the wire image stays
     flush_writebacks();
     CUDA_OK(cudaSetDevice(cfg_.device));
     for (auto st : {s_h2d_, s_comp_, s_d2h_, s_upd_}) CUDA_OK(cudaStreamSynchronize(st));

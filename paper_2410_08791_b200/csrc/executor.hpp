@@ -71,7 +71,9 @@ private:
     // layer_bytes: bytes of the master as stored and streamed - the fp32 image, or (split_) the
     // split image [wire | low halves] of block.hpp. opt_bytes: one AdamW moment array.
     size_t img_f() const { return blk_ ? static_cast<size_t>(lay_.n_floats) : static_cast<size_t>(d_) * d_ + d_; }
-    uint64_t layer_bytes() const { return split_ ? lay_.split_bytes : static_cast<uint64_t>(img_f()) * 4; }
+    uint64_t layer_bytes() const {
+        return infer_only_ ? lay_.wire_bytes : split_ ? lay_.split_bytes : static_cast<uint64_t>(img_f()) * 4;
+    }
     uint64_t opt_bytes() const { return static_cast<uint64_t>(img_f()) * 4; }
     // host master of layer L: one stride fits either block layout, so dp_init can switch in place
     uint8_t* host_layer(int L) const { return reinterpret_cast<uint8_t*>(host32_) + static_cast<size_t>(L) * host_stride_; }
@@ -166,6 +168,7 @@ private:
     // sharded data parallel (whose byte shards assume the fp32 image), where the slot keeps a
     // device-converted bf16 copy instead.
     bool split_ = false;
+    bool infer_only_ = false;  // SP_BLOCK_INFER_ONLY: the split master without its low halves
     size_t host_stride_ = 0;
     size_t fp_bytes_ = 0;  // slot bytes of the fp32 master regions [A][M][V] (the write-back stage)
     void split_image(const float* params, uint8_t* dst) const;    // fp32 image -> split image

@@ -173,3 +173,22 @@ def test_bench_shape_gpt2_xl_two_layers_against_torch_fp32():
             worst[(i, name)] = nrm(tt.view(g[i]), tt.view(ref))
     bad = {k: v for k, v in worst.items() if v >= 3e-2}
     assert not bad, bad
+
+
+def test_inference_only_master_streams_the_same_bits():
+    """SP_BLOCK_INFER_ONLY keeps only the bf16 wire image on the host (half the pinned memory);
+    its outputs equal the full split master's bitwise (the GEMMs multiply the same truncated
+    halves), and training is refused."""
+    spec = LLAMA
+    model = B.build_block_model(spec, 16, 3)
+    x, t = inputs(spec, 2)
+    outs = []
+    for infer_only in (False, True):
+        with B.BlockExecutor(3, spec, S(sp.SUPERPIPELINE, 2, 1), infer_only=infer_only) as ex:
+            ex.register_model(model)
+            outs.append(ex.forward([x])[0])
+            if infer_only:
+                assert ex.stats()["h2d_bytes"] == 3 * model.layout.wire_bytes
+                with pytest.raises(sp.InvalidArgument):
+                    ex.train_step(x, t, 0.01)
+    assert np.array_equal(outs[0], outs[1])
