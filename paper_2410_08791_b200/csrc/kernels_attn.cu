@@ -22,6 +22,8 @@
 #include "launch.cuh"
 
 namespace sp {
+cudaError_t attention_backward_tc(const AttnProblem& a, cudaStream_t st);  // kernels_attn_tc.cu
+extern int g_attn_bwd_kind;
 namespace {
 
 constexpr int kWarps = 4;        // 16 rows per warp
@@ -647,6 +649,10 @@ cudaError_t bwd_hd(const AttnProblem& a, cudaStream_t st) {
                                   st, static_cast<const __nv_bfloat16*>(a.o), static_cast<const __nv_bfloat16*>(a.dout),
                                   a.delta, a.tokens, sh);
     if (e != cudaSuccess) return e;
+    if (g_attn_bwd_kind == 0) {  // tcgen05 dK/dV and dQ passes where the shape allows
+        e = attention_backward_tc(a, st);
+        if (e != cudaErrorNotSupported) return e;
+    }
     dim3 gkv((a.seq_len + kBM - 1) / kBM, a.n_kv_heads, n_seq);
     e = launch_kernel(attn_bwd_dkdv_kernel<HD>, gkv, dim3(kThreads), dkdv_smem<HD>(), st,
                       static_cast<const __nv_bfloat16*>(a.qkv), static_cast<const __nv_bfloat16*>(a.dout), a.lse,
@@ -666,8 +672,9 @@ bool valid(const AttnProblem& a) {
 }  // namespace
 
 // 0 (default) / 2: tcgen05 forward where the head dim allows (64, 128), 1: always the mma.sync
-// kernel (A/B knob "attn_fwd", sp_debug_set)
+// kernel (A/B knob "attn_fwd", sp_debug_set); the same for the backward ("attn_bwd": 0 / 1)
 int g_attn_fwd_kind = 0;
+int g_attn_bwd_kind = 0;
 
 cudaError_t attention_forward_tc(const AttnProblem& a, cudaStream_t st);  // kernels_attn_tc.cu
 

@@ -404,6 +404,536 @@ cudaError_t launch_fwd_tc(const AttnProblem& a, cudaStream_t st) {
     return cudaGetLastError();
 }
 
+
+// ---------------------------------------------------------------------------------------
+// backward (tcgen05): dK / dV per key block, dQ per query block (no atomics: deterministic)
+// ---------------------------------------------------------------------------------------
+// Tiles in smem are stored as ATOMS boxes of 128 rows x 128 bytes (64 elements of the head dim),
+// 128B-swizzled: the same tile is a K-major operand (rows = M or N, K = head dim) and an
+// N-major B operand (rows = K, N = head dim; atoms 16 KB apart), so Q, dO and K each serve
+// both products they appear in without a transposed copy.
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+template <int ATOMS>
+__device__ __forceinline__ uint64_t kdesc(uint32_t base, int kk) {  // K-major, 16-element K step kk
+    return make_desc(base + (kk / 4) * 16384 + (kk % 4) * 32, 16, 1024);
+}
+__device__ __forceinline__ uint64_t ndesc(uint32_t base, int kk) {  // N-major B, 16-row K step kk
+    return make_desc(base + kk * 16 * 128, 16384, 1024);
+}
+// P / dS row chunk (32 values of row r, columns 32c..32c+31) into a K-major swizzled tile
+__device__ __forceinline__ void store_row_chunk(uint8_t* tile, int r, int c, const uint32_t (&pk)[16]) {
+    uint8_t* row = tile + (c / 2) * 16384 + r * 128;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int chunk = (c % 2) * 4 + u;
+        *reinterpret_cast<uint4*>(row + ((chunk ^ (r & 7)) << 4)) =
+            make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+    }
+}
+
+template <int HD>
+struct BwdCfg {
+    static constexpr int ATOMS = HD / 64;
+    static constexpr int TILE = 128 * HD * 2;  // one 128-row operand tile
+    static constexpr int QB = HD <= 64 ? 2 : 1;  // Q / dO buffers (dK/dV kernel)
+    static constexpr int SMEM_KV = 2 * TILE + QB * 2 * TILE + 2 * 32768 + QB * 2 * 512 + 1024 + 256;
+    static constexpr int SMEM_Q = 2 * TILE + 2 * 2 * TILE + 32768 + 1024 + 256;
+};
+
+// dK, dV: tile = (128 keys, kv head, sequence); for every query head of the group and every
+// query block: S^T = K Q^T, dP^T = V dO^T (TMEM), the softmax warps (thread = key row) form
+// P^T = exp2(S^T c - lse) and dS^T = P^T (dP^T - delta) in smem, then dV += P^T dO, dK += dS^T Q.
+template <int HD>
+__global__ void __launch_bounds__(kThreadsTc, 1)
+    attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmQK, const __grid_constant__ CUtensorMap tmDO,
+                            const float* __restrict__ lse, const float* __restrict__ delta,
+                            __nv_bfloat16* __restrict__ dqkv, TcShape sh, int n_seq, float scale) {
+    using C = BwdCfg<HD>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sK = smem;
+    uint8_t* sV = sK + C::TILE;
+    uint8_t* sQ = sV + C::TILE;              // QB tiles
+    uint8_t* sDO = sQ + C::QB * C::TILE;     // QB tiles
+    uint8_t* sP = sDO + C::QB * C::TILE;     // 32 KB: P^T [key][q]
+    uint8_t* sDS = sP + 32768;               // 32 KB: dS^T [key][q]
+    float* sL = reinterpret_cast<float*>(sDS + 32768);  // QB x 128 lse
+    float* sD = sL + C::QB * 128;                       // QB x 128 delta
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sD + C::QB * 128);
+    uint64_t* kv_full = bars;
+    uint64_t* kv_empty = bars + 1;
+    uint64_t* q_full = bars + 2;      // QB
+    uint64_t* q_empty = bars + 4;     // QB
+    uint64_t* s_full = bars + 6;
+    uint64_t* s_empty = bars + 7;
+    uint64_t* p_full = bars + 8;
+    uint64_t* p_empty = bars + 9;
+    uint64_t* dkv_full = bars + 10;
+    uint64_t* dkv_empty = bars + 11;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int n_qb = sh.S / kQ, n_kb = sh.S / kKV;
+    const int group = sh.H / sh.Hkv;
+    const int n_tiles = n_kb * sh.Hkv * n_seq;
+    constexpr uint32_t T_S = 0, T_DP = 128, T_DV = 256, T_DK = 256 + HD;
+    // tile t: key block ascending (causal: the first key blocks see the most query blocks)
+    auto tile_of_kv = [&](int t, int& kb, int& kvh, int& b) {
+        const int per = sh.Hkv * n_seq;
+        kb = t / per;
+        const int rest = t % per;
+        kvh = rest % sh.Hkv;
+        b = rest / sh.Hkv;
+    };
+    auto n_steps = [&](int kb) { return group * (sh.causal ? n_qb - kb : n_qb); };
+    auto step_of = [&](int kb, int kvh, int j, int& hq, int& qb) {
+        const int per = sh.causal ? n_qb - kb : n_qb;
+        hq = kvh * group + j / per;
+        qb = (sh.causal ? kb : 0) + j % per;
+    };
+
+    if (warp == 0 && lane == 0) {
+        prefetch_tmap(&tmQK);
+        prefetch_tmap(&tmDO);
+        for (int i = 0; i < 12; ++i) mbar_init(&bars[i], 1);
+        mbar_init(s_empty, 128);
+        mbar_init(p_full, 128);
+        mbar_init(dkv_empty, 128);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {  // ===== TMA producer =====
+            int g = 0, lt = 0;
+            for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++lt) {
+                int kb, kvh, b;
+                tile_of_kv(t, kb, kvh, b);
+                const int row0 = b * sh.S;
+                const int kcol = (sh.H + kvh) * HD, vcol = (sh.H + sh.Hkv + kvh) * HD;
+                mbar_wait(kv_empty, (lt & 1) ^ 1);
+                mbar_expect_tx(kv_full, 2 * C::TILE);
+                for (int a = 0; a < C::ATOMS; ++a) {
+                    tma_load_2d(&tmQK, kv_full, sK + a * 16384, kcol + 64 * a, row0 + kb * kKV);
+                    tma_load_2d(&tmQK, kv_full, sV + a * 16384, vcol + 64 * a, row0 + kb * kKV);
+                }
+                const int n = n_steps(kb);
+                for (int j = 0; j < n; ++j, ++g) {
+                    int hq, qb;
+                    step_of(kb, kvh, j, hq, qb);
+                    const int buf = g % C::QB;
+                    mbar_wait(&q_empty[buf], ((g / C::QB) & 1) ^ 1);
+                    mbar_expect_tx(&q_full[buf], 2 * C::TILE + 2 * 512);
+                    for (int a = 0; a < C::ATOMS; ++a) {
+                        tma_load_2d(&tmQK, &q_full[buf], sQ + buf * C::TILE + a * 16384, hq * HD + 64 * a,
+                                    row0 + qb * kQ);
+                        tma_load_2d(&tmDO, &q_full[buf], sDO + buf * C::TILE + a * 16384, hq * HD + 64 * a,
+                                    row0 + qb * kQ);
+                    }
+                    const int64_t li = (static_cast<int64_t>(b) * sh.H + hq) * sh.S + qb * kQ;
+                    bulk_load(sL + buf * 128, lse + li, 512, &q_full[buf]);
+                    bulk_load(sD + buf * 128, delta + li, 512, &q_full[buf]);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ===== MMA issuer =====
+            constexpr uint32_t IDESC_S = make_idesc(128, 128, false, false);
+            constexpr uint32_t IDESC_D = make_idesc(128, HD, false, true);
+            const uint32_t k_base = smem_u32(sK), v_base = smem_u32(sV);
+            const uint32_t p_base = smem_u32(sP), ds_base = smem_u32(sDS);
+            auto issue_sdp = [&](int g) {
+                const int buf = g % C::QB;
+                mbar_wait(&q_full[buf], (g / C::QB) & 1);
+                mbar_wait(s_empty, (g & 1) ^ 1);
+                fence_after();
+                const uint32_t qb_ = smem_u32(sQ + buf * C::TILE), db_ = smem_u32(sDO + buf * C::TILE);
+#pragma unroll
+                for (int kk = 0; kk < HD / 16; ++kk) {
+                    umma<false>(tmem + T_S, kdesc<C::ATOMS>(k_base, kk), kdesc<C::ATOMS>(qb_, kk), IDESC_S, kk > 0);
+                    umma<false>(tmem + T_DP, kdesc<C::ATOMS>(v_base, kk), kdesc<C::ATOMS>(db_, kk), IDESC_S, kk > 0);
+                }
+                umma_commit(s_full);
+            };
+            auto issue_dkv = [&](int g, bool first) {
+                const int buf = g % C::QB;
+                mbar_wait(p_full, g & 1);
+                fence_after();
+                const uint32_t qb_ = smem_u32(sQ + buf * C::TILE), db_ = smem_u32(sDO + buf * C::TILE);
+#pragma unroll
+                for (int kk = 0; kk < 128 / 16; ++kk) {
+                    const uint32_t acc = (!first || kk > 0) ? 1u : 0u;
+                    umma<false>(tmem + T_DV, kdesc<2>(p_base, kk), ndesc(db_, kk), IDESC_D, acc);
+                    umma<false>(tmem + T_DK, kdesc<2>(ds_base, kk), ndesc(qb_, kk), IDESC_D, acc);
+                }
+                umma_commit(p_empty);
+                umma_commit(&q_empty[buf]);
+            };
+            int g = 0, lt = 0;
+            for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++lt) {
+                int kb, kvh, b;
+                tile_of_kv(t, kb, kvh, b);
+                const int n = n_steps(kb);
+                mbar_wait(kv_full, lt & 1);
+                mbar_wait(dkv_empty, (lt & 1) ^ 1);  // the previous tile's dK / dV are read out
+                fence_after();
+                issue_sdp(g);
+                for (int j = 0; j < n; ++j) {
+                    // the next block's S^T / dP^T run under this block's softmax; with one Q / dO
+                    // buffer (head_dim 128) its loads wait for this block's dK / dV MMAs first
+                    if (C::QB > 1 && j + 1 < n) issue_sdp(g + j + 1);
+                    issue_dkv(g + j, j == 0);
+                    if (C::QB == 1 && j + 1 < n) issue_sdp(g + j + 1);
+                }
+                umma_commit(dkv_full);
+                umma_commit(kv_empty);
+                g += n;
+            }
+        }
+    } else if (warp >= 4) {
+        // ===== softmax: one key row per thread =====
+        const int q = warp & 3;
+        const int r = q * 32 + lane;
+        const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
+        uint32_t vs[32], vp[32];
+        int g = 0, lt = 0;
+        for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++lt) {
+            int kb, kvh, b;
+            tile_of_kv(t, kb, kvh, b);
+            const int key = kb * kKV + r;
+            const int n = n_steps(kb);
+            for (int j = 0; j < n; ++j, ++g) {
+                int hq, qb;
+                step_of(kb, kvh, j, hq, qb);
+                const int buf = g % C::QB;
+                const float* L = sL + buf * 128;
+                const float* D = sD + buf * 128;
+                mbar_wait(s_full, g & 1);
+                fence_after();
+                if (g > 0) mbar_wait(p_empty, (g & 1) ^ 1);  // the previous block's dK / dV MMAs read P, dS
+                const bool diag = sh.causal && qb == kb;  // keys above a query of this block: masked
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    tmem_ld32_async(tmem + lane_off + T_S + c * 32, vs);
+                    tmem_ld32_async(tmem + lane_off + T_DP + c * 32, vp);
+                    tmem_ld_wait(vs);
+                    tmem_ld_wait(vp);
+                    uint32_t pp[16], dd[16];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        const int q0 = c * 32 + 2 * i;
+                        float p0 = ex2_fast(fmaf(__uint_as_float(vs[2 * i]), sh.scale_log2, -L[q0]));
+                        float p1 = ex2_fast(fmaf(__uint_as_float(vs[2 * i + 1]), sh.scale_log2, -L[q0 + 1]));
+                        if (diag) {
+                            if (r > q0) p0 = 0.0f;
+                            if (r > q0 + 1) p1 = 0.0f;
+                        }
+                        const float d0 = p0 * (__uint_as_float(vp[2 * i]) - D[q0]);
+                        const float d1 = p1 * (__uint_as_float(vp[2 * i + 1]) - D[q0 + 1]);
+                        pp[i] = pack_bf16(p0, p1);
+                        dd[i] = pack_bf16(d0, d1);
+                    }
+                    store_row_chunk(sP, r, c, pp);
+                    store_row_chunk(sDS, r, c, dd);
+                }
+                fence_before();
+                mbar_arrive(s_empty);
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_arrive(p_full);
+            }
+            // the tile's dK, dV out of TMEM (dK gets the softmax scale)
+            mbar_wait(dkv_full, lt & 1);
+            fence_after();
+            __nv_bfloat16* row = dqkv + static_cast<int64_t>(b * sh.S + key) * sh.ld;
+            const int kcol = (sh.H + kvh) * HD, vcol = (sh.H + sh.Hkv + kvh) * HD;
+#pragma unroll
+            for (int c = 0; c < HD / 32; ++c) {
+                tmem_ld32_async(tmem + lane_off + T_DK + c * 32, vs);
+                tmem_ld32_async(tmem + lane_off + T_DV + c * 32, vp);
+                tmem_ld_wait(vs);
+                tmem_ld_wait(vp);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    uint4 wk, wv;
+                    wk.x = pack_bf16(__uint_as_float(vs[8 * u + 0]) * scale, __uint_as_float(vs[8 * u + 1]) * scale);
+                    wk.y = pack_bf16(__uint_as_float(vs[8 * u + 2]) * scale, __uint_as_float(vs[8 * u + 3]) * scale);
+                    wk.z = pack_bf16(__uint_as_float(vs[8 * u + 4]) * scale, __uint_as_float(vs[8 * u + 5]) * scale);
+                    wk.w = pack_bf16(__uint_as_float(vs[8 * u + 6]) * scale, __uint_as_float(vs[8 * u + 7]) * scale);
+                    wv.x = pack_bf16(__uint_as_float(vp[8 * u + 0]), __uint_as_float(vp[8 * u + 1]));
+                    wv.y = pack_bf16(__uint_as_float(vp[8 * u + 2]), __uint_as_float(vp[8 * u + 3]));
+                    wv.z = pack_bf16(__uint_as_float(vp[8 * u + 4]), __uint_as_float(vp[8 * u + 5]));
+                    wv.w = pack_bf16(__uint_as_float(vp[8 * u + 6]), __uint_as_float(vp[8 * u + 7]));
+                    reinterpret_cast<uint4*>(row + kcol + c * 32)[u] = wk;
+                    reinterpret_cast<uint4*>(row + vcol + c * 32)[u] = wv;
+                }
+            }
+            fence_before();
+            mbar_arrive(dkv_empty);
+        }
+    }
+    __syncwarp();
+    fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+    }
+}
+
+// dQ: tile = (128 queries, head, sequence); for every key block: S = Q K^T, dP = dO V^T (TMEM),
+// the softmax warps (thread = query row) form dS = P (dP - delta) in smem, then dQ += dS K.
+template <int HD>
+__global__ void __launch_bounds__(kThreadsTc, 1)
+    attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQK, const __grid_constant__ CUtensorMap tmDO,
+                          const float* __restrict__ lse, const float* __restrict__ delta,
+                          __nv_bfloat16* __restrict__ dqkv, TcShape sh, int n_seq, float scale) {
+    using C = BwdCfg<HD>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sQ = smem;
+    uint8_t* sDO = sQ + C::TILE;
+    uint8_t* sK = sDO + C::TILE;           // 2 stages
+    uint8_t* sV = sK + 2 * C::TILE;        // 2 stages
+    uint8_t* sDS = sV + 2 * C::TILE;       // 32 KB: dS [q][key]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sDS + 32768);
+    uint64_t* q_full = bars;
+    uint64_t* q_empty = bars + 1;
+    uint64_t* kv_full = bars + 2;   // 2
+    uint64_t* kv_empty = bars + 4;  // 2
+    uint64_t* s_full = bars + 6;
+    uint64_t* s_empty = bars + 7;
+    uint64_t* p_full = bars + 8;
+    uint64_t* p_empty = bars + 9;
+    uint64_t* dq_full = bars + 10;
+    uint64_t* dq_empty = bars + 11;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int n_qb = sh.S / kQ, n_kb_total = sh.S / kKV;
+    const int n_tiles = n_qb * sh.H * n_seq;
+    constexpr uint32_t T_S = 0, T_DP = 128, T_DQ = 256;
+    auto blocks_of = [&](int qb) { return sh.causal ? min(n_kb_total, qb + 1) : n_kb_total; };
+
+    if (warp == 0 && lane == 0) {
+        prefetch_tmap(&tmQK);
+        prefetch_tmap(&tmDO);
+        for (int i = 0; i < 12; ++i) mbar_init(&bars[i], 1);
+        mbar_init(s_empty, 128);
+        mbar_init(p_full, 128);
+        mbar_init(dq_empty, 128);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {  // ===== TMA producer =====
+            int g = 0, lt = 0;
+            for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++lt) {
+                const TileOf w = tile_of(t, sh, n_qb, n_seq);
+                const int kvh = w.h / (sh.H / sh.Hkv);
+                const int row0 = w.b * sh.S;
+                const int kcol = (sh.H + kvh) * HD, vcol = (sh.H + sh.Hkv + kvh) * HD;
+                mbar_wait(q_empty, (lt & 1) ^ 1);
+                mbar_expect_tx(q_full, 2 * C::TILE);
+                for (int a = 0; a < C::ATOMS; ++a) {
+                    tma_load_2d(&tmQK, q_full, sQ + a * 16384, w.h * HD + 64 * a, row0 + w.qb * kQ);
+                    tma_load_2d(&tmDO, q_full, sDO + a * 16384, w.h * HD + 64 * a, row0 + w.qb * kQ);
+                }
+                const int n = blocks_of(w.qb);
+                for (int j = 0; j < n; ++j, ++g) {
+                    const int st = g & 1;
+                    mbar_wait(&kv_empty[st], ((g >> 1) & 1) ^ 1);
+                    mbar_expect_tx(&kv_full[st], 2 * C::TILE);
+                    for (int a = 0; a < C::ATOMS; ++a) {
+                        tma_load_2d(&tmQK, &kv_full[st], sK + st * C::TILE + a * 16384, kcol + 64 * a, row0 + j * kKV);
+                        tma_load_2d(&tmQK, &kv_full[st], sV + st * C::TILE + a * 16384, vcol + 64 * a, row0 + j * kKV);
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ===== MMA issuer =====
+            constexpr uint32_t IDESC_S = make_idesc(128, 128, false, false);
+            constexpr uint32_t IDESC_D = make_idesc(128, HD, false, true);
+            const uint32_t q_base = smem_u32(sQ), do_base = smem_u32(sDO), ds_base = smem_u32(sDS);
+            auto issue_sdp = [&](int g) {
+                const int st = g & 1;
+                mbar_wait(&kv_full[st], (g >> 1) & 1);
+                mbar_wait(s_empty, (g & 1) ^ 1);
+                fence_after();
+                const uint32_t kb_ = smem_u32(sK + st * C::TILE), vb_ = smem_u32(sV + st * C::TILE);
+#pragma unroll
+                for (int kk = 0; kk < HD / 16; ++kk) {
+                    umma<false>(tmem + T_S, kdesc<C::ATOMS>(q_base, kk), kdesc<C::ATOMS>(kb_, kk), IDESC_S, kk > 0);
+                    umma<false>(tmem + T_DP, kdesc<C::ATOMS>(do_base, kk), kdesc<C::ATOMS>(vb_, kk), IDESC_S, kk > 0);
+                }
+                umma_commit(s_full);
+            };
+            auto issue_dq = [&](int g, bool first) {
+                const int st = g & 1;
+                mbar_wait(p_full, g & 1);
+                fence_after();
+                const uint32_t kb_ = smem_u32(sK + st * C::TILE);
+#pragma unroll
+                for (int kk = 0; kk < 128 / 16; ++kk)
+                    umma<false>(tmem + T_DQ, kdesc<2>(ds_base, kk), ndesc(kb_, kk), IDESC_D, (!first || kk > 0) ? 1u : 0u);
+                umma_commit(p_empty);
+                umma_commit(&kv_empty[st]);
+            };
+            int g = 0, lt = 0;
+            for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++lt) {
+                const TileOf w = tile_of(t, sh, n_qb, n_seq);
+                const int n = blocks_of(w.qb);
+                mbar_wait(q_full, lt & 1);
+                mbar_wait(dq_empty, (lt & 1) ^ 1);
+                fence_after();
+                issue_sdp(g);
+                for (int j = 0; j < n; ++j) {
+                    if (j + 1 < n) issue_sdp(g + j + 1);
+                    issue_dq(g + j, j == 0);
+                }
+                umma_commit(dq_full);
+                umma_commit(q_empty);
+                g += n;
+            }
+        }
+    } else if (warp >= 4) {
+        // ===== softmax: one query row per thread =====
+        const int q = warp & 3;
+        const int r = q * 32 + lane;
+        const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
+        uint32_t vs[32], vp[32];
+        int g = 0, lt = 0;
+        for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++lt) {
+            const TileOf w = tile_of(t, sh, n_qb, n_seq);
+            const int qi = w.qb * kQ + r;
+            const int64_t li = (static_cast<int64_t>(w.b) * sh.H + w.h) * sh.S + qi;
+            const float L = lse[li], Dl = delta[li];
+            const int n = blocks_of(w.qb);
+            for (int j = 0; j < n; ++j, ++g) {
+                mbar_wait(s_full, g & 1);
+                fence_after();
+                if (g > 0) mbar_wait(p_empty, (g & 1) ^ 1);
+                const bool diag = sh.causal && j == w.qb;
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    tmem_ld32_async(tmem + lane_off + T_S + c * 32, vs);
+                    tmem_ld32_async(tmem + lane_off + T_DP + c * 32, vp);
+                    tmem_ld_wait(vs);
+                    tmem_ld_wait(vp);
+                    uint32_t dd[16];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        const int k0 = c * 32 + 2 * i;  // key within the block
+                        float p0 = ex2_fast(fmaf(__uint_as_float(vs[2 * i]), sh.scale_log2, -L));
+                        float p1 = ex2_fast(fmaf(__uint_as_float(vs[2 * i + 1]), sh.scale_log2, -L));
+                        if (diag) {
+                            if (k0 > r) p0 = 0.0f;
+                            if (k0 + 1 > r) p1 = 0.0f;
+                        }
+                        dd[i] = pack_bf16(p0 * (__uint_as_float(vp[2 * i]) - Dl), p1 * (__uint_as_float(vp[2 * i + 1]) - Dl));
+                    }
+                    store_row_chunk(sDS, r, c, dd);
+                }
+                fence_before();
+                mbar_arrive(s_empty);
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_arrive(p_full);
+            }
+            mbar_wait(dq_full, lt & 1);
+            fence_after();
+            __nv_bfloat16* row = dqkv + static_cast<int64_t>(w.b * sh.S + qi) * sh.ld + w.h * HD;
+#pragma unroll
+            for (int c = 0; c < HD / 32; ++c) {
+                tmem_ld32_async(tmem + lane_off + T_DQ + c * 32, vs);
+                tmem_ld_wait(vs);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    uint4 wq;
+                    wq.x = pack_bf16(__uint_as_float(vs[8 * u + 0]) * scale, __uint_as_float(vs[8 * u + 1]) * scale);
+                    wq.y = pack_bf16(__uint_as_float(vs[8 * u + 2]) * scale, __uint_as_float(vs[8 * u + 3]) * scale);
+                    wq.z = pack_bf16(__uint_as_float(vs[8 * u + 4]) * scale, __uint_as_float(vs[8 * u + 5]) * scale);
+                    wq.w = pack_bf16(__uint_as_float(vs[8 * u + 6]) * scale, __uint_as_float(vs[8 * u + 7]) * scale);
+                    reinterpret_cast<uint4*>(row + c * 32)[u] = wq;
+                }
+            }
+            fence_before();
+            mbar_arrive(dq_empty);
+        }
+    }
+    __syncwarp();
+    fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+    }
+}
+
+template <int HD>
+cudaError_t launch_bwd_tc(const AttnProblem& a, cudaStream_t st) {
+    using C = BwdCfg<HD>;
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(attn_bwd_dkdv_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             C::SMEM_KV);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(attn_bwd_dq_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_Q);
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    const int ld = (a.n_heads + 2 * a.n_kv_heads) * a.head_dim;
+    const int ldo = a.n_heads * a.head_dim;
+    CUtensorMap tqk, tdo;
+    if (!make_map(&tqk, a.qkv, static_cast<uint64_t>(ld), static_cast<uint64_t>(a.tokens), static_cast<uint64_t>(ld), 64,
+                  128, false, false) ||
+        !make_map(&tdo, a.dout, static_cast<uint64_t>(ldo), static_cast<uint64_t>(a.tokens), static_cast<uint64_t>(ldo),
+                  64, 128, false, false))
+        return cudaErrorInvalidValue;
+    TcShape sh;
+    sh.S = a.seq_len;
+    sh.H = a.n_heads;
+    sh.Hkv = a.n_kv_heads;
+    sh.ld = ld;
+    sh.ldo = ldo;
+    sh.causal = a.causal;
+    const float scale = 1.0f / sqrtf(static_cast<float>(a.head_dim));
+    sh.scale_log2 = 1.4426950408889634f * scale;
+    const int n_seq = static_cast<int>(a.tokens / a.seq_len);
+    const int kv_tiles = (a.seq_len / 128) * a.n_kv_heads * n_seq;
+    const int q_tiles = (a.seq_len / 128) * a.n_heads * n_seq;
+    auto* dq = static_cast<__nv_bfloat16*>(a.dqkv);
+    attn_bwd_dkdv_tc_kernel<HD><<<kv_tiles < num_sms() ? kv_tiles : num_sms(), kThreadsTc, C::SMEM_KV, st>>>(
+        tqk, tdo, a.lse, a.delta, dq, sh, n_seq, scale);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    attn_bwd_dq_tc_kernel<HD><<<q_tiles < num_sms() ? q_tiles : num_sms(), kThreadsTc, C::SMEM_Q, st>>>(
+        tqk, tdo, a.lse, a.delta, dq, sh, n_seq, scale);
+    return cudaGetLastError();
+}
 }  // namespace
 
 // The tensor-core forward for head_dim 64 / 128 (the GPT-2 XL and Llama-3 shapes);
@@ -414,4 +944,15 @@ cudaError_t attention_forward_tc(const AttnProblem& a, cudaStream_t st) {
     return cudaErrorNotSupported;
 }
 
+}  // namespace sp
+
+namespace sp {
+// The tensor-core dK/dV and dQ passes for head_dim 64 / 128 and sequences that are whole 128-row
+// blocks (GPT-2 XL, Llama-3); cudaErrorNotSupported otherwise. delta must be filled first.
+cudaError_t attention_backward_tc(const AttnProblem& a, cudaStream_t st) {
+    if (a.seq_len % 128 != 0) return cudaErrorNotSupported;
+    if (a.head_dim == 64) return launch_bwd_tc<64>(a, st);
+    if (a.head_dim == 128) return launch_bwd_tc<128>(a, st);
+    return cudaErrorNotSupported;
+}
 }  // namespace sp

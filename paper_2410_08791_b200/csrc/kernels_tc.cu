@@ -1365,11 +1365,13 @@ cudaError_t dispatch2_bn_kmajor(const GemmProblem& g, cudaStream_t st) {
 }  // namespace tc
 
 extern int g_attn_fwd_kind;  // kernels_attn.cu
+extern int g_attn_bwd_kind;
 
 void set_gemm_debug(const char* key, int value, bool* known) {
     *known = true;
     if (std::strcmp(key, "epi_mode") == 0) tc::g_epi_mode = value;
     else if (std::strcmp(key, "attn_fwd") == 0) g_attn_fwd_kind = value;
+    else if (std::strcmp(key, "attn_bwd") == 0) g_attn_bwd_kind = value;
     else if (std::strcmp(key, "narrow") == 0) tc::g_narrow = value;
     else *known = false;
 }

@@ -169,11 +169,13 @@ def _split(qkv, B, S, H, Hkv, hd):
     return t[:, :H], t[:, H:H + Hkv], t[:, H + Hkv:]
 
 
-@pytest.mark.parametrize("fwd_kind", [2, 1], ids=["tcgen05-fwd", "mma-sync-fwd"])
+@pytest.mark.parametrize("fwd_kind", [2, 1], ids=["tcgen05", "mma-sync"])
 @pytest.mark.parametrize("B,S,H,Hkv,hd,causal", ATTN)
 def test_attention_forward_and_backward(B, S, H, Hkv, hd, causal, fwd_kind):
-    # fwd_kind 2: the tcgen05 forward (head dims 64 / 128; 80 always takes the mma.sync one)
+    # kind 2 / 0: the tcgen05 forward and backward (head dims 64 / 128, whole 128-row sequence
+    # blocks for the backward; other shapes take the mma.sync kernels), 1: the mma.sync kernels
     assert LIB.sp_debug_set(None, b"attn_fwd", fwd_kind) == 0
+    assert LIB.sp_debug_set(None, b"attn_bwd", 0 if fwd_kind == 2 else 1) == 0
     T, W = B * S, (H + 2 * Hkv) * hd
     qkv = bf(torch.randn(T, W, device="cuda"))
     o = torch.empty(T, H * hd, device="cuda", dtype=torch.bfloat16)
@@ -202,6 +204,7 @@ def test_attention_forward_and_backward(B, S, H, Hkv, hd, causal, fwd_kind):
     for got_g, ref_g in ((dq, q.grad), (dk, k.grad), (dv, v.grad)):
         assert rel(got_g, ref_g) < 2e-2
     LIB.sp_debug_set(None, b"attn_fwd", 0)
+    LIB.sp_debug_set(None, b"attn_bwd", 0)
 
 
 def test_attention_is_deterministic():

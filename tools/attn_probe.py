@@ -14,6 +14,7 @@ from paper_2410_08791_b200 import _capi  # noqa: E402
 LIB = _capi.LIB
 # SP_ATTN_FWD=0|1|2: the forward kernel choice (sp_debug_set "attn_fwd"; 2 = tcgen05 at head_dim 64 too)
 LIB.sp_debug_set(None, b"attn_fwd", int(os.environ.get("SP_ATTN_FWD", "0")))
+LIB.sp_debug_set(None, b"attn_bwd", int(os.environ.get("SP_ATTN_BWD", "0")))
 
 
 def timeit(fn, reps=10):
