@@ -93,12 +93,19 @@ int sp_debug_attention(int32_t backward, int64_t tokens, int32_t seq_len, int32_
                        int32_t n_kv_heads, int32_t head_dim, int32_t causal, const void* qkv, void* o,
                        float* lse, const void* dout, float* delta, void* dqkv, void* stream);
 /* LayerNorm (rms = 0) / RMSNorm (rms = 1) forward and backward (kernels.hpp norm_forward /
- * norm_backward), device pointers, on `stream`. Backward returns the partial chunk count. */
+ * norm_backward), device pointers, on `stream`. Backward: dres_out = dres_in + dx (and its bf16
+ * copy); when `out` is non-null also the parameter gradients out[0, d) (gamma) and out[d, 2d)
+ * (LayerNorm beta) through the scratch `part` / `counters` (sp_debug_col_scratch sizes; the
+ * counters zeroed before first use, left zero). */
 int sp_debug_norm_forward(const float* x, const float* gamma, const float* beta, int32_t rms, float eps,
                           int64_t rows, int32_t d, void* y, float* stats, void* stream);
 int sp_debug_norm_backward(const float* dy, const float* x, const float* stats, const float* gamma,
                            int32_t rms, int64_t rows, int32_t d, const float* dres_in, float* dres_out,
-                           void* dres_out16, float* part, void* stream);
+                           void* dres_out16, float* part, int32_t* counters, float* out, void* stream);
+/* out[j] = sum over rows of a bf16 [rows][n] matrix (a bias gradient; n % 8 == 0), with the
+ * same scratch (kernels.hpp colsum_total_bf16). */
+int sp_debug_colsum(const void* x, int64_t rows, int32_t n, float* part, int32_t* counters, float* out, void* stream);
+void sp_debug_col_scratch(int64_t rows, int32_t widest, int64_t* part_floats, int64_t* counters);
 
 /* Transformer-block executors: the fp32 gradient image (the layer's parameter layout) of
  * layer `index` from the last train step, as the UPDATE op consumed it. Gradient images are

@@ -103,18 +103,30 @@ void Executor::block_alloc(int64_t R, int items, bool train, const std::function
         CUDA_OK(cudaMemset(g, 0, grad_f * 4));  // alignment gaps between tensors stay zero
     }
     grad_red_ = bgimg_[0];  // (unused in block mode: the gradient image is reduced in place)
+    // dW split-K partial regions, one per split matrix, per layer parity (sized by the split
+    // count at the allocation's row capacity; smaller calls never use more: block_dw caps it)
+    bdw_off_.assign(lay_.t.size(), 0);
+    bdw_cap_.assign(lay_.t.size(), 1);
     size_t ws = 0;
-    for (const BlockTensor& t : lay_.t) {
+    for (size_t i = 0; i < lay_.t.size(); ++i) {
+        const BlockTensor& t = lay_.t[i];
         if (!t.matrix) continue;
         const DwChoice c = choose_dw(static_cast<int>(t.rows), static_cast<int>(t.cols), static_cast<int>(R), 16, false);
-        if (c.splits > 1) ws = std::max(ws, static_cast<size_t>(c.splits) * t.count());
+        if (c.splits <= 1) continue;
+        bdw_cap_[i] = c.splits;
+        bdw_off_[i] = ws;
+        ws += static_cast<size_t>(c.splits) * t.count();
     }
-    bws_floats_ = ws;
-    bws_ = ws ? static_cast<float*>(alloc(ws * 4)) : nullptr;
-    const size_t widest = static_cast<size_t>(std::max({lay_.qkv_cols, lay_.mlp_cols, d_}));
-    const size_t col = std::max(static_cast<size_t>(colsum_chunks(R)) * widest,
-                                static_cast<size_t>(norm_param_chunks(R)) * 2 * d);
-    bcol_ = static_cast<float*>(alloc(col * 4));
+    for (int p = 0; p < 2; ++p) {
+        bws_[p] = ws ? static_cast<float*>(alloc(ws * 4)) : nullptr;
+        bdw_pending_[p].clear();
+        bdw_last_[p].clear();
+    }
+    const int widest = std::max({lay_.qkv_cols, lay_.mlp_cols, d_});
+    const ColScratchSize cs = col_scratch_size(R, widest);
+    bcs_.part = static_cast<float*>(alloc(cs.part_floats * 4));
+    bcs_.counters = static_cast<int*>(alloc(cs.counters * 4));
+    CUDA_OK(cudaMemset(bcs_.counters, 0, cs.counters * 4));  // each kernel leaves them zero
 }
 
 // The update regions of a split master in slot `slot` (block.hpp): each tensor's halves or fp32
@@ -254,10 +266,16 @@ void Executor::block_forward_layer(const WirePtrs& w, const float* x, const Bloc
     gemm(g, st);
 }
 
-// dW = act^T grad ([rows][M] and [rows][N] bf16) into out[M][N] (fp32, the gradient image),
-// split-K partials reduced in a fixed order when the shape needs them (choose_dw).
-void Executor::block_dw(const void* act, int M, const void* grad, int N, int64_t rows, float* out, cudaStream_t st) {
-    const DwChoice c = choose_dw(M, N, static_cast<int>(rows), 16, false);
+// dW = act^T grad ([rows][M] and [rows][N] bf16) of matrix tensor `ti` (M x N fp32). With one
+// split the GEMM writes the layer's gradient image directly; with several it writes fp32
+// partials into the matrix's region of the parity's workspace, and the layer's UPDATE op sums
+// them in a fixed order on the update stream (block_reduce_pending / split_update), off the
+// compute stream. The split count depends only on the shape (and the workspace's capacity).
+void Executor::block_dw(int L, int ti, const void* act, const void* grad, int64_t rows, cudaStream_t st) {
+    const BlockTensor& t = lay_.t[static_cast<size_t>(ti)];
+    const int M = static_cast<int>(t.rows), N = static_cast<int>(t.cols);
+    const int cap = bdw_cap_[static_cast<size_t>(ti)];
+    const DwChoice c = choose_dw(M, N, static_cast<int>(rows), cap, false);
     GemmProblem g;
     g.M = M;
     g.N = N;
@@ -275,21 +293,33 @@ void Executor::block_dw(const void* act, int M, const void* grad, int N, int64_t
     g.ldo = N;
     g.split_stride = static_cast<int64_t>(M) * N;  // (a valid 3-D partial map even for one split)
     if (c.splits == 1) {
-        g.out = out;
+        g.out = bgimg_[L % 2] + t.off;
         gemm(g, st);
         return;
     }
-    g.out = bws_;
+    DwPartials p;
+    p.tensor = ti;
+    p.splits = effective_splits(g.K, c.splits);
+    p.parts = bws_[L % 2] + bdw_off_[static_cast<size_t>(ti)];
+    g.out = p.parts;
     gemm(g, st);
-    reduce_partials(bws_, effective_splits(g.K, c.splits), static_cast<int64_t>(M) * N, static_cast<int64_t>(M) * N,
-                    out, st);
-    ++kernels_;
+    bdw_pending_[L % 2].push_back(p);
+}
+
+// The pending dW partials of the layer of parity `parity` -> its gradient image (fixed order).
+void Executor::block_reduce_pending(int parity, cudaStream_t st) {
+    for (const DwPartials& p : bdw_pending_[parity]) {
+        const BlockTensor& t = lay_.t[static_cast<size_t>(p.tensor)];
+        const int64_t n = static_cast<int64_t>(t.count());
+        reduce_partials(p.parts, p.splits, n, n, bgimg_[parity] + t.off, st);
+        ++kernels_;
+    }
+    bdw_pending_[parity].clear();
 }
 
 void Executor::block_colsum(const void* x, int64_t rows, int N, float* out, cudaStream_t st) {
-    const int chunks = colsum_bf16(x, rows, N, bcol_, st);
-    reduce_partials(bcol_, chunks, N, N, out, st);
-    kernels_ += 2;
+    colsum_total_bf16(x, rows, N, bcs_, out, st);
+    ++kernels_;
 }
 
 void Executor::block_backward_layer(int L, const WirePtrs& w, const float* x, const BlockActs& a, int64_t rows,
@@ -306,7 +336,7 @@ void Executor::block_backward_layer(int L, const WirePtrs& w, const float* x, co
     const void* dy16 = bdres16_[L % 2];
     // --- MLP: y = h + W2^T g(h W1 + b1) + b2
     if (trainable) {
-        block_dw(a.g, ff, dy16, d, rows, at(lay_.w2), st);
+        block_dw(L, lay_.w2, a.g, dy16, rows, st);
         if (lay_.b2 >= 0) block_colsum(dy16, rows, d, at(lay_.b2), st);
     }
     GemmProblem g;
@@ -325,7 +355,7 @@ void Executor::block_backward_layer(int L, const WirePtrs& w, const float* x, co
     g.ldo = ff;
     gemm(g, st);
     if (trainable) {
-        block_dw(a.xn2, d, bdbig_, ff, rows, at(lay_.w1), st);
+        block_dw(L, lay_.w1, a.xn2, bdbig_, rows, st);
         if (lay_.b1 >= 0) block_colsum(bdbig_, rows, ff, at(lay_.b1), st);
     }
     g = GemmProblem{};
@@ -341,16 +371,12 @@ void Executor::block_backward_layer(int L, const WirePtrs& w, const float* x, co
     g.ldo = d;
     gemm(g, st);
     // norm2: dh_res = dy + norm2'(dxn2)
-    const int chunks2 = norm_backward(bdxn_, a.xmid, a.st2, w.ln2_g, rms, rows, d, dy, bdmid_, bdmid16_,
-                                      trainable ? bcol_ : nullptr, st);
+    norm_backward(bdxn_, a.xmid, a.st2, w.ln2_g, rms, rows, d, dy, bdmid_, bdmid16_, bcs_,
+                  trainable ? at(lay_.ln2_g) : nullptr, st);
     kernels_ += trainable ? 2 : 1;
-    if (trainable) {
-        reduce_partials(bcol_, chunks2, 2 * static_cast<int64_t>(d), lay_.ln2_b >= 0 ? 2 * d : d, at(lay_.ln2_g), st);
-        ++kernels_;
-    }
     // --- attention: h = x + Wo^T attn(norm1(x) Wqkv + bqkv) + bo
     if (trainable) {
-        block_dw(a.o, hhd, bdmid16_, d, rows, at(lay_.wo), st);
+        block_dw(L, lay_.wo, a.o, bdmid16_, rows, st);
         if (lay_.bo >= 0) block_colsum(bdmid16_, rows, d, at(lay_.bo), st);
     }
     g = GemmProblem{};
@@ -367,7 +393,7 @@ void Executor::block_backward_layer(int L, const WirePtrs& w, const float* x, co
     gemm(g, st);
     attention(true, a, bdo_, bdbig_, rows, st);  // dqkv
     if (trainable) {
-        block_dw(a.xn1, d, bdbig_, lay_.qkv_cols, rows, at(lay_.wqkv), st);
+        block_dw(L, lay_.wqkv, a.xn1, bdbig_, rows, st);
         if (lay_.bqkv >= 0) block_colsum(bdbig_, rows, lay_.qkv_cols, at(lay_.bqkv), st);
     }
     g = GemmProblem{};
@@ -383,14 +409,9 @@ void Executor::block_backward_layer(int L, const WirePtrs& w, const float* x, co
     g.ldo = d;
     gemm(g, st);
     // norm1: dx = dh_res + norm1'(dxn1) -> the gradient the layer below reads (layer 0: none)
-    const int chunks1 = norm_backward(bdxn_, x, a.st1, w.ln1_g, rms, rows, d, bdmid_,
-                                      need_dx ? bdres_[(L + 1) % 2] : nullptr, need_dx ? bdres16_[(L + 1) % 2] : nullptr,
-                                      trainable ? bcol_ : nullptr, st);
+    norm_backward(bdxn_, x, a.st1, w.ln1_g, rms, rows, d, bdmid_, need_dx ? bdres_[(L + 1) % 2] : nullptr,
+                  need_dx ? bdres16_[(L + 1) % 2] : nullptr, bcs_, trainable ? at(lay_.ln1_g) : nullptr, st);
     kernels_ += (need_dx ? 1 : 0) + (trainable ? 1 : 0);
-    if (trainable) {
-        reduce_partials(bcol_, chunks1, 2 * static_cast<int64_t>(d), lay_.ln1_b >= 0 ? 2 * d : d, at(lay_.ln1_g), st);
-        ++kernels_;
-    }
 }
 
 void Executor::block_compute(const Op& op, bool train, int64_t rows, int fmt) {
@@ -462,6 +483,13 @@ void Executor::debug_read_grad(int index, float* out) {
     if (index < 0 || index > 1 || index >= n_) throw Error(SP_ERR_INVALID, "debug_read_grad: layers 0 and 1 only");
     if (sharded_) throw Error(SP_ERR_STATE, "debug_read_grad: not in sharded data parallel");
     if (!bgimg_[index % 2]) throw Error(SP_ERR_STATE, "debug_read_grad: no train step yet");
+    CUDA_OK(cudaDeviceSynchronize());
+    // split-K dW partials the update summed in place: fold them into the image first
+    for (const DwPartials& p : bdw_last_[index % 2]) {
+        const BlockTensor& t = lay_.t[static_cast<size_t>(p.tensor)];
+        const int64_t n = static_cast<int64_t>(t.count());
+        reduce_partials(p.parts, p.splits, n, n, bgimg_[index % 2] + t.off, nullptr);
+    }
     CUDA_OK(cudaDeviceSynchronize());
     CUDA_OK(cudaMemcpy(out, bgimg_[index % 2], img_f() * 4, cudaMemcpyDeviceToHost));
 }

@@ -613,9 +613,28 @@ extern "C" int sp_debug_norm_forward(const float* x, const float* gamma, const f
 
 extern "C" int sp_debug_norm_backward(const float* dy, const float* x, const float* stats, const float* gamma,
                                       int32_t rms, int64_t rows, int32_t d, const float* dres_in, float* dres_out,
-                                      void* dres_out16, float* part, void* stream) {
-    return sp::norm_backward(dy, x, stats, gamma, rms, rows, d, dres_in, dres_out, dres_out16, part,
-                             static_cast<cudaStream_t>(stream));
+                                      void* dres_out16, float* part, int32_t* counters, float* out, void* stream) {
+    sp::ColScratch scr;
+    scr.part = part;
+    scr.counters = counters;
+    sp::norm_backward(dy, x, stats, gamma, rms, rows, d, dres_in, dres_out, dres_out16, scr, out,
+                      static_cast<cudaStream_t>(stream));
+    return static_cast<int>(cudaGetLastError());
+}
+
+extern "C" int sp_debug_colsum(const void* x, int64_t rows, int32_t n, float* part, int32_t* counters, float* out,
+                               void* stream) {
+    sp::ColScratch scr;
+    scr.part = part;
+    scr.counters = counters;
+    sp::colsum_total_bf16(x, rows, n, scr, out, static_cast<cudaStream_t>(stream));
+    return static_cast<int>(cudaGetLastError());
+}
+
+extern "C" void sp_debug_col_scratch(int64_t rows, int32_t widest, int64_t* part_floats, int64_t* counters) {
+    const sp::ColScratchSize s = sp::col_scratch_size(rows, widest);
+    *part_floats = static_cast<int64_t>(s.part_floats);
+    *counters = static_cast<int64_t>(s.counters);
 }
 
 extern "C" int sp_debug_read_grad(sp_exec* ex, int32_t index, float* out) {

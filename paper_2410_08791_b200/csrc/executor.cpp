@@ -878,6 +878,13 @@ void Executor::update_op(const Op& op, float lr) {
     // image in its parameter layout) in `g`.
     const size_t imgf = img_f();
     float* g = ws;
+    // block layers: the split-K dW partials the layer's backward left; summed inside the split
+    // update when nothing else reads the image first, else into the image here
+    const bool fuse_parts = blk_ && split_ && !comm_;
+    if (blk_) {
+        bdw_last_[L % 2] = bdw_pending_[L % 2];
+        if (!fuse_parts) block_reduce_pending(L % 2, st);
+    }
     if (tc_ && !blk_) {
         reduce_partials(ws, splits_, static_cast<int64_t>(dd), static_cast<int64_t>(dd), grad_red_, st);
         reduce_partials(ws + splits_ * dd, col_chunks_, d_, d_, grad_red_ + dd, st);
@@ -904,8 +911,18 @@ void Executor::update_op(const Op& op, float lr) {
     } else if (split_) {
         // split master: the (all-reduced) logical gradient updates the halves in place
         if (comm_) NCCL_OK(nccl().AllReduce(g, g, imgf, ncclFloat, ncclSum, comm_, st));
-        split_update(split_regions(s), g, adamw() ? slot_m32(s) : nullptr, adamw() ? slot_v32(s) : nullptr, lr,
-                     adamw() ? 1 : 0, adamw_dev_, st);
+        SplitRegions r = split_regions(s);
+        if (fuse_parts) {
+            for (const DwPartials& p : bdw_pending_[L % 2])
+                for (int i = 0; i < r.n; ++i)
+                    if (r.off[i] == static_cast<int64_t>(lay_.t[static_cast<size_t>(p.tensor)].off)) {
+                        r.parts[i] = p.parts;
+                        r.nparts[i] = p.splits;
+                    }
+            bdw_pending_[L % 2].clear();
+        }
+        split_update(r, g, adamw() ? slot_m32(s) : nullptr, adamw() ? slot_v32(s) : nullptr, lr, adamw() ? 1 : 0,
+                     adamw_dev_, st);
         ++kernels_;
     } else {
         if (comm_) NCCL_OK(nccl().AllReduce(g, g, imgf, ncclFloat, ncclSum, comm_, st));

@@ -155,7 +155,7 @@ private:
                               cudaStream_t st);
     void block_compute(const Op& op, bool train, int64_t rows, int fmt);
     void block_loss(int64_t rows);
-    void block_dw(const void* act, int M, const void* grad, int N, int64_t rows, float* out, cudaStream_t st);
+    void block_dw(int L, int tensor, const void* act, const void* grad, int64_t rows, cudaStream_t st);
     void block_colsum(const void* x, int64_t rows, int N, float* out, cudaStream_t st);
     void attention(bool backward, const BlockActs& a, const void* dout, void* dqkv, int64_t rows, cudaStream_t st);
     cudaStream_t stream_of(OpKind k) const;
@@ -179,12 +179,26 @@ private:
     std::vector<float*> bx_;            // training: residual stream x_0..x_n (fp32; x_n = yout_)
     std::vector<BlockActs> bsv_;        // training: per-layer saved intermediates (no offload)
     BlockActs bscr_;                    // inference / offload recompute: one scratch set
-    float *bdxn_ = nullptr, *bdmid_ = nullptr, *bdelta_ = nullptr, *bws_ = nullptr, *bcol_ = nullptr;
+    float *bdxn_ = nullptr, *bdmid_ = nullptr, *bdelta_ = nullptr;
+    ColScratch bcs_;  // column-sum partials + counters (bias / norm parameter gradients)
+    // dW split-K partials, per layer parity: each split matrix has its own region (bdw_cap_
+    // splits of its size), so the UPDATE op (update stream) reduces them while the compute
+    // stream moves on to the layer below. bdw_pending_[p]: what the last backward of a layer of
+    // parity p left there (tensor index, partial base, split count).
+    struct DwPartials {
+        int tensor = -1, splits = 1;
+        float* parts = nullptr;
+    };
+    float* bws_[2] = {nullptr, nullptr};
+    std::vector<size_t> bdw_off_;  // per tensor: float offset of its region (matrices with splits)
+    std::vector<int> bdw_cap_;     // per tensor: the most splits its region holds (1: none)
+    std::vector<DwPartials> bdw_pending_[2];
+    std::vector<DwPartials> bdw_last_[2];  // what the last UPDATE of each parity consumed
+    void block_reduce_pending(int parity, cudaStream_t st);  // partials -> the gradient image
     void *bdmid16_ = nullptr, *bdbig_ = nullptr, *bdo_ = nullptr;
     float* bdres_[2] = {nullptr, nullptr};
     void* bdres16_[2] = {nullptr, nullptr};
     float* bgimg_[2] = {nullptr, nullptr};  // per-layer gradient images (ping-pong)
-    size_t bws_floats_ = 0;
     uint64_t attn_launches_ = 0;
     double attn_flops_ = 0.0;
     bool bf16_ = false;  // bf16 tensor-core path (bf16 operands / activations)

@@ -154,6 +154,10 @@ struct SplitRegions {
     uint16_t* lo[16];    // matrices: low halves; vectors: nullptr
     int64_t off[16];     // logical offset (floats) of the region in g / m / v
     int64_t count[16];   // elements
+    // optional: the gradient of region i is the fixed-order sum of nparts[i] split-K partials
+    // at parts[i] (stride count[i]) instead of g[off[i] ...]
+    const float* parts[16] = {};
+    int nparts[16] = {};
 };
 void split_update(const SplitRegions& r, const float* g, float* m, float* v, float lr, int opt,
                   const AdamwScalars* scalars, cudaStream_t st);
@@ -183,14 +187,29 @@ cudaError_t attention_backward(const AttnProblem& a, cudaStream_t st);
 // y (bf16) = norm(x) * gamma (+ beta); stats[T][2] = {mean, rstd} (RMSNorm: {0, rstd}).
 void norm_forward(const float* x, const float* gamma, const float* beta, int rms, float eps,
                   int64_t rows, int d, void* y, float* stats, cudaStream_t st);
+// Scratch of the column-sum kernels below: part (fp32 chunk partials) and counters (ints, zero
+// before first use; each kernel leaves them zero), sized by col_scratch_size for the widest
+// matrix. Kernels on one stream may share one scratch.
+struct ColScratch {
+    float* part = nullptr;
+    int* counters = nullptr;
+};
+struct ColScratchSize {
+    size_t part_floats = 0, counters = 0;
+};
+ColScratchSize col_scratch_size(int64_t rows, int widest);
 // Backward of the norm given dy (fp32 [T][d], the gradient of its output):
 //   dx = rstd (dy*gamma - mean(dy*gamma) - xhat mean(dy*gamma*xhat))   (RMSNorm: no mean term)
 //   dres_out (fp32) = dres_in + dx and dres_out16 (bf16) = the same rounded, when non-null.
-// Parameter gradients: per 128-row chunk partials part[chunk][2][d] = {sum dy*xhat, sum dy}
-// (reduce with reduce_partials over chunks; fixed decomposition). Returns the chunk count.
-int norm_backward(const float* dy, const float* x, const float* stats, const float* gamma, int rms,
-                  int64_t rows, int d, const float* dres_in, float* dres_out, void* dres_out16,
-                  float* part, cudaStream_t st);
+// Parameter gradients, when out is non-null: out[0, d) = sum_r dy*xhat (gamma), out[d, 2d) =
+// sum_r dy (LayerNorm's beta), through 512-row chunk partials summed in chunk order by the last
+// block of each column group (fixed decomposition: depends on the shape only).
+void norm_backward(const float* dy, const float* x, const float* stats, const float* gamma, int rms,
+                   int64_t rows, int d, const float* dres_in, float* dres_out, void* dres_out16,
+                   const ColScratch& scr, float* out, cudaStream_t st);
+// out[j] = sum_r x[r][j] of a bf16 [rows][n] matrix (n % 8 == 0; a bias gradient), the same
+// chunking and in-kernel fixed-order reduction.
+void colsum_total_bf16(const void* x, int64_t rows, int n, const ColScratch& scr, float* out, cudaStream_t st);
 int norm_param_chunks(int64_t rows);
 
 }  // namespace sp

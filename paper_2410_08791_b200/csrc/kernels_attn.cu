@@ -22,7 +22,8 @@
 #include "launch.cuh"
 
 namespace sp {
-cudaError_t attention_backward_tc(const AttnProblem& a, cudaStream_t st);  // kernels_attn_tc.cu
+cudaError_t attention_backward_tc(const AttnProblem& a, cudaStream_t st);   // kernels_attn_tc.cu
+cudaError_t attention_backward_tc2(const AttnProblem& a, cudaStream_t st);  // kernels_attn_bwd.cu
 extern int g_attn_bwd_kind;
 namespace {
 
@@ -645,11 +646,15 @@ cudaError_t bwd_hd(const AttnProblem& a, cudaStream_t st) {
     const int n_seq = static_cast<int>(a.tokens / a.seq_len);
     const float scale = 1.0f / sqrtf(static_cast<float>(a.head_dim));
     const int64_t th = a.tokens * a.n_heads;
+    if (g_attn_bwd_kind == 0) {  // tcgen05 dQ (+ delta) and dK/dV passes, v2, where the shape allows
+        cudaError_t e2 = attention_backward_tc2(a, st);
+        if (e2 != cudaErrorNotSupported) return e2;
+    }
     cudaError_t e = launch_kernel(attn_bwd_delta_kernel<HD>, dim3(static_cast<unsigned>((th + 255) / 256)), dim3(256), 0,
                                   st, static_cast<const __nv_bfloat16*>(a.o), static_cast<const __nv_bfloat16*>(a.dout),
                                   a.delta, a.tokens, sh);
     if (e != cudaSuccess) return e;
-    if (g_attn_bwd_kind == 0) {  // tcgen05 dK/dV and dQ passes where the shape allows
+    if (g_attn_bwd_kind == 0 || g_attn_bwd_kind == 2) {  // tcgen05 dK/dV and dQ passes, v1
         e = attention_backward_tc(a, st);
         if (e != cudaErrorNotSupported) return e;
     }
@@ -672,7 +677,8 @@ bool valid(const AttnProblem& a) {
 }  // namespace
 
 // 0 (default) / 2: tcgen05 forward where the head dim allows (64, 128), 1: always the mma.sync
-// kernel (A/B knob "attn_fwd", sp_debug_set); the same for the backward ("attn_bwd": 0 / 1)
+// kernel (A/B knob "attn_fwd", sp_debug_set). Backward ("attn_bwd"): 0 (default) the v2 tcgen05
+// passes (kernels_attn_bwd.cu), 2 the v1 tcgen05 passes (kernels_attn_tc.cu), 1 mma.sync.
 int g_attn_fwd_kind = 0;
 int g_attn_bwd_kind = 0;
 

@@ -1,0 +1,718 @@
+// kernels_attn_bwd.cu — tcgen05 flash-attention backward (sm_100a), head_dim 64 / 128.
+//
+// Two persistent kernels, deterministic (every output element is one fixed-order reduction, no
+// atomics), for sequences made of whole 128-row blocks:
+//
+//   dQ pass   tile = 128 queries of one (sequence, head); streams 64-key steps of K, V:
+//               S = Q K^T, dP = dO V^T                        (TMEM, fp32, M 128 x N 64)
+//               dS = exp2(S c - lse) (dP - delta)             (softmax warps, bf16 -> TMEM)
+//               dQ += dS K                                    (A = dS from TMEM, B = K N-major)
+//             delta = rowsum(dO . O) is formed here (thread = query row) and written for the
+//             dK/dV pass, so no separate delta kernel runs.
+//   dK/dV pass tile = 128 keys of one (sequence, kv head); streams 64-query steps of Q, dO for
+//             every query head of the group:
+//               S^T = K Q^T, dP^T = V dO^T                    (TMEM)
+//               P^T = exp2(S^T c - lse), dS^T = P^T (dP^T - delta)   (bf16 -> TMEM)
+//               dV += P^T dO, dK += dS^T Q                    (A from TMEM, B = dO / Q N-major)
+//
+// Warp roles (384 threads): warp 0 TMA producer, warp 1 MMA issuer (one thread), warp 2 TMEM
+// allocator, warps 4..11 the elementwise ("softmax") work: TWO warps per TMEM lane quarter, each
+// taking one 32-column half of a step, so every SM sub-partition has two such warps to overlap
+// TMEM-load, MUFU and FMA latencies. S / dP are double-buffered in TMEM: the MMAs of step j+1
+// (and the products of step j-1) run while the softmax warps work on step j. P / dS are written
+// back over the S / dP columns they were computed from (each thread only its own lane and
+// half) and consumed straight from TMEM by the tcgen05.mma A operand — no shared-memory round
+// trip for the probability tiles.
+//
+// TMEM columns: S[b] at 128 b, dP[b] at 128 b + 64 (b = step mod NB, NB = 3 buffers, 2 for
+// dK/dV at head_dim 128), accumulators from 128 NB (dQ: HD columns; dK then dV: 2 HD) <= 512.
+// Three buffers give the MMA issuer two steps of slack: S of step j + 3 is issued once the
+// products of step j (which read the P / dS written over buffer j mod 3) are queued.
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include <cstdint>
+
+#include "kernels.hpp"
+#include "tc_ptx.cuh"
+
+namespace sp {
+namespace {
+using namespace tc;
+
+constexpr int kThreadsB = 384;
+constexpr int kRowsB = 128;  // the CTA tile's own rows (queries in dQ, keys in dK/dV)
+constexpr int kStepB = 64;   // rows streamed per step (keys in dQ, queries in dK/dV)
+
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// tcgen05.mma with the A operand in TMEM (M 128 lanes x K 16, two bf16 per 32-bit column)
+__device__ __forceinline__ void umma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                        uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+            taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+        "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+        : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void bulk_load_b(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+// K-major tile of `atom` bytes per 64-element column atom (128 B rows, 128B swizzle), 16-element
+// K step kk
+__device__ __forceinline__ uint64_t kmaj(uint32_t base, int kk, int atom) {
+    return make_desc(base + (kk / 4) * atom + (kk % 4) * 32, 16, 1024);
+}
+// the same tile as an N-major B operand (K = its rows): 16-row K step kk, atoms `atom` apart in N
+__device__ __forceinline__ uint64_t nmaj(uint32_t base, int kk, int atom) {
+    return make_desc(base + kk * 16 * 128, atom, 1024);
+}
+// A-operand TMEM column of K step kk (16 rows of the step) of a P / dS tile written by the two
+// half-warps: separate regions hold it contiguously (half h at 16 h); written back over S / dP,
+// half h sits at its own columns 32 h .. 32 h + 15
+template <bool SEP>
+__device__ __forceinline__ uint32_t ts_col(int kk) {
+    return SEP ? static_cast<uint32_t>(8 * kk) : static_cast<uint32_t>((kk >> 1) * 32 + (kk & 1) * 8);
+}
+// a descriptor advanced by `bytes` (the 14-bit start field cannot carry: smem < 256 KB)
+__device__ __forceinline__ uint64_t dadd(uint64_t d, uint32_t bytes) { return d + (bytes >> 4); }
+
+struct BShape {
+    int S, H, Hkv, ld, ldo, causal;
+    float scale_log2, scale;
+};
+
+template <int HD>
+struct BCfg {
+    static constexpr int ATOMS = HD / 64;
+    static constexpr int BIG = kRowsB * HD * 2;    // a 128-row tile (ATOMS atoms of 16 KB)
+    static constexpr int SMALL = kStepB * HD * 2;  // a 64-row tile (ATOMS atoms of 8 KB)
+    static constexpr int A_BIG = kRowsB * 128, A_SMALL = kStepB * 128;
+    static constexpr int ST = HD == 64 ? 4 : 3;         // streamed-tile stages
+    static constexpr int OWN = HD == 64 ? 2 : 1;        // own-tile stages (next tile prefetch)
+    static constexpr bool SEP_DKDV = HD == 64;  // separate P / dS regions fit (TMEM map above)
+    static constexpr int SMEM_DKDV = OWN * 2 * BIG + ST * 2 * SMALL + ST * 2 * 256 + 1024 + 512;
+    static constexpr int SMEM_DQ = OWN * 2 * BIG + ST * 2 * SMALL + 1024 + 512;
+};
+
+// ------------------------------------------------------------------------------------------
+// dQ (+ delta)
+// ------------------------------------------------------------------------------------------
+template <int HD>
+__global__ void __launch_bounds__(kThreadsB, 1)
+    attn_bwd_dq2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmDO,
+                        const __grid_constant__ CUtensorMap tmKV, const __nv_bfloat16* __restrict__ o,
+                        const __nv_bfloat16* __restrict__ dout, const float* __restrict__ lse,
+                        float* __restrict__ delta, __nv_bfloat16* __restrict__ dqkv, BShape sh, int n_seq) {
+    using C = BCfg<HD>;
+    constexpr uint32_t T_DS = 256, T_ACC = 320;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // (stays a shared pointer)
+    uint8_t* sQ = smem;                      // OWN
+    uint8_t* sDO = sQ + C::OWN * C::BIG;     // OWN
+    uint8_t* sK = sDO + C::OWN * C::BIG;     // ST
+    uint8_t* sV = sK + C::ST * C::SMALL;     // ST
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sV + C::ST * C::SMALL);
+    uint64_t* q_full = bars;                 // OWN
+    uint64_t* q_empty = bars + 2;            // OWN
+    uint64_t* kv_full = bars + 4;            // ST
+    uint64_t* kv_empty = kv_full + C::ST;    // ST
+    uint64_t* s_full = kv_empty + C::ST;     // 2: S / dP of the step are in TMEM
+    uint64_t* s_free = s_full + 2;           // 2: the softmax warps have loaded them
+    uint64_t* p_full = s_free + 2;           // 2: dS is in TMEM
+    uint64_t* ds_free = p_full + 2;          // 2: the dQ MMAs have read it
+    uint64_t* acc_full = ds_free + 2;
+    uint64_t* acc_empty = acc_full + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int n_qb = sh.S / kRowsB, n_ks = sh.S / kStepB;
+    const int n_tiles = n_qb * sh.H * n_seq;
+    // tile t: (query block, head, sequence), query blocks descending (causal: longest first)
+    auto tile = [&](int t, int& qb, int& h, int& b) {
+        const int per = sh.H * n_seq;
+        qb = n_qb - 1 - t / per;
+        const int rest = t % per;
+        h = rest % sh.H;
+        b = rest / sh.H;
+    };
+    auto steps = [&](int qb) { return sh.causal ? 2 * (qb + 1) : n_ks; };
+
+    if (warp == 0 && lane == 0) {
+        prefetch_tmap(&tmQ);
+        prefetch_tmap(&tmDO);
+        prefetch_tmap(&tmKV);
+        for (int i = 0; i < C::OWN; ++i) {
+            mbar_init(&q_full[i], 1);
+            mbar_init(&q_empty[i], 1);
+        }
+        for (int i = 0; i < C::ST; ++i) {
+            mbar_init(&kv_full[i], 1);
+            mbar_init(&kv_empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&s_full[i], 1);
+            mbar_init(&s_free[i], 256);
+            mbar_init(&p_full[i], 256);
+            mbar_init(&ds_free[i], 1);
+        }
+        mbar_init(acc_full, 1);
+        mbar_init(acc_empty, 256);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {  // ===== TMA producer =====
+            int g = 0, lt = 0;
+            for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++lt) {
+                int qb, h, b;
+                tile(t, qb, h, b);
+                const int kvh = h / (sh.H / sh.Hkv);
+                const int row0 = b * sh.S;
+                const int ob = lt % C::OWN;
+                mbar_wait(&q_empty[ob], ((lt / C::OWN) & 1) ^ 1);
+                mbar_expect_tx(&q_full[ob], 2 * C::BIG);
+                for (int a = 0; a < C::ATOMS; ++a) {
+                    tma_load_2d(&tmQ, &q_full[ob], sQ + ob * C::BIG + a * C::A_BIG, h * HD + 64 * a, row0 + qb * kRowsB);
+                    tma_load_2d(&tmDO, &q_full[ob], sDO + ob * C::BIG + a * C::A_BIG, h * HD + 64 * a,
+                                row0 + qb * kRowsB);
+                }
+                const int kcol = (sh.H + kvh) * HD, vcol = (sh.H + sh.Hkv + kvh) * HD;
+                const int n = steps(qb);
+                for (int j = 0; j < n; ++j, ++g) {
+                    const int st = g % C::ST;
+                    mbar_wait(&kv_empty[st], ((g / C::ST) & 1) ^ 1);
+                    mbar_expect_tx(&kv_full[st], 2 * C::SMALL);
+                    for (int a = 0; a < C::ATOMS; ++a) {
+                        tma_load_2d(&tmKV, &kv_full[st], sK + st * C::SMALL + a * C::A_SMALL, kcol + 64 * a,
+                                    row0 + j * kStepB);
+                        tma_load_2d(&tmKV, &kv_full[st], sV + st * C::SMALL + a * C::A_SMALL, vcol + 64 * a,
+                                    row0 + j * kStepB);
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ===== MMA issuer =====
+            constexpr uint32_t ID_S = make_idesc(128, kStepB, false, false);
+            constexpr uint32_t ID_D = make_idesc(128, HD, false, true);
+            uint64_t dq_, ddo_;  // the tile's Q / dO descriptors (K-major, k step 0)
+            // S / dP of step gg into buffer gg & 1, once the softmax warps have loaded step gg - 2's
+            auto issue_s = [&](int gg) {
+                const int st = gg % C::ST, bb = gg & 1;
+                mbar_wait(&kv_full[st], (gg / C::ST) & 1);
+                if (gg >= 2) mbar_wait(&s_free[bb], ((gg - 2) >> 1) & 1);
+                fence_after();
+                const uint64_t dk = make_desc(smem_u32(sK + st * C::SMALL), 16, 1024);
+                const uint64_t dv = make_desc(smem_u32(sV + st * C::SMALL), 16, 1024);
+#pragma unroll
+                for (int kk = 0; kk < HD / 16; ++kk) {
+                    const uint32_t ob = (kk / 4) * C::A_BIG + (kk % 4) * 32, sb = (kk / 4) * C::A_SMALL + (kk % 4) * 32;
+                    umma<false>(tmem + 128 * bb, dadd(dq_, ob), dadd(dk, sb), ID_S, kk > 0);
+                    umma<false>(tmem + 128 * bb + 64, dadd(ddo_, ob), dadd(dv, sb), ID_S, kk > 0);
+                }
+                umma_commit(&s_full[bb]);
+            };
+            // dQ += dS K of step gg
+            auto issue_d = [&](int gg, bool first) {
+                const int st = gg % C::ST, bb = gg & 1;
+                mbar_wait(&p_full[bb], (gg >> 1) & 1);
+                fence_after();
+                const uint64_t dk = make_desc(smem_u32(sK + st * C::SMALL), C::A_SMALL, 1024);
+#pragma unroll
+                for (int kk = 0; kk < kStepB / 16; ++kk)
+                    umma_ts(tmem + T_ACC, tmem + T_DS + 32 * bb + ts_col<true>(kk), dadd(dk, kk * 2048), ID_D,
+                            (!first || kk > 0) ? 1u : 0u);
+                umma_commit(&ds_free[bb]);
+                umma_commit(&kv_empty[st]);
+            };
+            int g = 0, lt = 0;
+            for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++lt) {
+                int qb, h, b;
+                tile(t, qb, h, b);
+                const int n = steps(qb);
+                const int ob = lt % C::OWN;
+                mbar_wait(&q_full[ob], (lt / C::OWN) & 1);
+                dq_ = make_desc(smem_u32(sQ + ob * C::BIG), 16, 1024);
+                ddo_ = make_desc(smem_u32(sDO + ob * C::BIG), 16, 1024);
+                issue_s(g);
+                issue_s(g + 1);  // (n >= 2: sequences are whole 128-row blocks)
+                mbar_wait(acc_empty, (lt & 1) ^ 1);  // the previous tile's dQ is read out
+                fence_after();
+                for (int j = 0; j < n; ++j) {
+                    if (j + 2 < n) issue_s(g + j + 2);
+                    issue_d(g + j, j == 0);
+                }
+                umma_commit(acc_full);
+                umma_commit(&q_empty[ob]);
+                g += n;
+            }
+        }
+    } else if (warp >= 4) {
+        // ===== elementwise: thread = query row, half = which 32 keys of a 64-key step =====
+        const int q4 = warp & 3, half = (warp - 4) >> 2;
+        const int r = q4 * 32 + lane;
+        const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
+        uint32_t vs[32], vp[32];
+        uint4 ro[HD / 8], rd[HD / 8];  // this thread's O and dO rows (of the next tile)
+        auto load_rows = [&](int tt) {
+            int qb_, h_, b_;
+            tile(tt, qb_, h_, b_);
+            const int64_t tk = static_cast<int64_t>(b_) * sh.S + qb_ * kRowsB + r;
+            const uint4* a4 = reinterpret_cast<const uint4*>(o + tk * sh.ldo + h_ * HD);
+            const uint4* c4 = reinterpret_cast<const uint4*>(dout + tk * sh.ldo + h_ * HD);
+#pragma unroll
+            for (int j = 0; j < HD / 8; ++j) {
+                ro[j] = __ldg(a4 + j);
+                rd[j] = __ldg(c4 + j);
+            }
+        };
+        int g = 0, lt = 0;
+        for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++lt) {
+            int qb, h, b;
+            tile(t, qb, h, b);
+            const int qi = qb * kRowsB + r;
+            const int64_t tok = static_cast<int64_t>(b) * sh.S + qi;
+            const int64_t li = (static_cast<int64_t>(b) * sh.H + h) * sh.S + qi;
+            const float L = lse[li];
+            // delta = sum_d dO . O of this row (both halves compute it identically; half 0 stores
+            // it), from rows prefetched into registers during the previous tile (head_dim 64)
+            constexpr bool kPrefetch = HD == 64;
+            if (!kPrefetch || t == static_cast<int>(blockIdx.x)) load_rows(t);
+            float Dl = 0.0f;
+#pragma unroll
+            for (int j = 0; j < HD / 8; ++j) {
+                const uint32_t wa[4] = {ro[j].x, ro[j].y, ro[j].z, ro[j].w}, wc[4] = {rd[j].x, rd[j].y, rd[j].z, rd[j].w};
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const float2 fa = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wa[k]));
+                    const float2 fc = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wc[k]));
+                    Dl += fa.x * fc.x + fa.y * fc.y;
+                }
+            }
+            if (kPrefetch && t + static_cast<int>(gridDim.x) < n_tiles) load_rows(t + gridDim.x);
+            if (half == 0) delta[li] = Dl;
+            const int n = steps(qb);
+            for (int j = 0; j < n; ++j, ++g) {
+                const int bb = g & 1;
+                mbar_wait(&s_full[bb], (g >> 1) & 1);
+                fence_after();
+                tmem_ld32_async(tmem + lane_off + 128 * bb + 32 * half, vs);
+                tmem_ld32_async(tmem + lane_off + 128 * bb + 64 + 32 * half, vp);
+                tmem_ld_wait(vs);
+                tmem_ld_wait(vp);
+                fence_before();
+                mbar_arrive(&s_free[bb]);  // the MMAs of step g + 2 may overwrite S / dP now
+                const int k0 = j * kStepB + 32 * half;               // first key of this half
+                const bool mask = sh.causal && k0 + 31 > qb * kRowsB;  // some key above some query
+                uint32_t dd[16];
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    float p0 = ex2_approx(fmaf(__uint_as_float(vs[2 * i]), sh.scale_log2, -L));
+                    float p1 = ex2_approx(fmaf(__uint_as_float(vs[2 * i + 1]), sh.scale_log2, -L));
+                    if (mask) {
+                        if (k0 + 2 * i > qi) p0 = 0.0f;
+                        if (k0 + 2 * i + 1 > qi) p1 = 0.0f;
+                    }
+                    dd[i] = pack_bf16(p0 * (__uint_as_float(vp[2 * i]) - Dl), p1 * (__uint_as_float(vp[2 * i + 1]) - Dl));
+                }
+                if (g >= 2) {  // the dQ MMAs of step g - 2 have read this dS buffer
+                    mbar_wait(&ds_free[bb], ((g - 2) >> 1) & 1);
+                    fence_after();
+                }
+                tmem_st16(tmem + lane_off + T_DS + 32 * bb + 16 * half, dd);
+                tmem_st_wait();
+                fence_before();
+                mbar_arrive(&p_full[bb]);
+            }
+            mbar_wait(acc_full, lt & 1);
+            fence_after();
+            __nv_bfloat16* row = dqkv + tok * sh.ld + h * HD;
+#pragma unroll
+            for (int c = 0; c < HD / 64; ++c) {  // this half's HD / 2 columns
+                const int col = half * (HD / 2) + c * 32;
+                tmem_ld32_async(tmem + lane_off + T_ACC + col, vs);
+                tmem_ld_wait(vs);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    uint4 w;
+                    w.x = pack_bf16(__uint_as_float(vs[8 * u + 0]) * sh.scale, __uint_as_float(vs[8 * u + 1]) * sh.scale);
+                    w.y = pack_bf16(__uint_as_float(vs[8 * u + 2]) * sh.scale, __uint_as_float(vs[8 * u + 3]) * sh.scale);
+                    w.z = pack_bf16(__uint_as_float(vs[8 * u + 4]) * sh.scale, __uint_as_float(vs[8 * u + 5]) * sh.scale);
+                    w.w = pack_bf16(__uint_as_float(vs[8 * u + 6]) * sh.scale, __uint_as_float(vs[8 * u + 7]) * sh.scale);
+                    reinterpret_cast<uint4*>(row + col)[u] = w;
+                }
+            }
+            fence_before();
+            mbar_arrive(acc_empty);
+        }
+    }
+    __syncwarp();
+    fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// dK, dV
+// ------------------------------------------------------------------------------------------
+template <int HD, bool SEP>
+__global__ void __launch_bounds__(kThreadsB, 1)
+    attn_bwd_dkdv2_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmQ,
+                          const __grid_constant__ CUtensorMap tmDO, const float* __restrict__ lse,
+                          const float* __restrict__ delta, __nv_bfloat16* __restrict__ dqkv, BShape sh, int n_seq) {
+    using C = BCfg<HD>;
+    // TMEM map (header): P / dS regions of buffer b, then dK and dV
+    constexpr uint32_t T_ACC = SEP ? 384 : 256;
+    static_assert(T_ACC + 2 * HD <= 512, "dK / dV do not fit in TMEM");
+    auto p_col = [](int bb) { return SEP ? 256u + 64u * bb : 128u * bb; };
+    auto ds_col = [](int bb) { return SEP ? 288u + 64u * bb : 128u * bb + 64u; };
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // (stays a shared pointer)
+    uint8_t* sK = smem;                      // OWN
+    uint8_t* sV = sK + C::OWN * C::BIG;      // OWN
+    uint8_t* sQ = sV + C::OWN * C::BIG;      // ST
+    uint8_t* sDO = sQ + C::ST * C::SMALL;    // ST
+    float* sL = reinterpret_cast<float*>(sDO + C::ST * C::SMALL);  // ST x 64
+    float* sD = sL + C::ST * kStepB;                                // ST x 64
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sD + C::ST * kStepB);
+    uint64_t* kv_full = bars;                // OWN
+    uint64_t* kv_empty = bars + 2;           // OWN
+    uint64_t* q_full = bars + 4;             // ST
+    uint64_t* q_empty = q_full + C::ST;      // ST
+    uint64_t* s_full = q_empty + C::ST;      // 2
+    uint64_t* s_free = s_full + 2;           // 2 (SEP)
+    uint64_t* p_full = s_free + 2;           // 2
+    uint64_t* ds_free = p_full + 2;          // 2 (SEP)
+    uint64_t* acc_full = ds_free + 2;
+    uint64_t* acc_empty = acc_full + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int n_kb = sh.S / kRowsB, n_qs = sh.S / kStepB;
+    const int group = sh.H / sh.Hkv;
+    const int n_tiles = n_kb * sh.Hkv * n_seq;
+    // tile t: (key block, kv head, sequence), key blocks ascending (causal: longest first)
+    auto tile = [&](int t, int& kb, int& kvh, int& b) {
+        const int per = sh.Hkv * n_seq;
+        kb = t / per;
+        const int rest = t % per;
+        kvh = rest % sh.Hkv;
+        b = rest / sh.Hkv;
+    };
+    auto per_head = [&](int kb) { return sh.causal ? n_qs - 2 * kb : n_qs; };
+    auto step_of = [&](int kb, int kvh, int j, int& hq, int& qs) {
+        const int per = per_head(kb);
+        hq = kvh * group + j / per;
+        qs = (sh.causal ? 2 * kb : 0) + j % per;
+    };
+
+    if (warp == 0 && lane == 0) {
+        prefetch_tmap(&tmK);
+        prefetch_tmap(&tmQ);
+        prefetch_tmap(&tmDO);
+        for (int i = 0; i < C::OWN; ++i) {
+            mbar_init(&kv_full[i], 1);
+            mbar_init(&kv_empty[i], 1);
+        }
+        for (int i = 0; i < C::ST; ++i) {
+            mbar_init(&q_full[i], 1);
+            mbar_init(&q_empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&s_full[i], 1);
+            mbar_init(&s_free[i], 256);
+            mbar_init(&p_full[i], 256);
+            mbar_init(&ds_free[i], 1);
+        }
+        mbar_init(acc_full, 1);
+        mbar_init(acc_empty, 256);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {  // ===== TMA producer =====
+            int g = 0, lt = 0;
+            for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++lt) {
+                int kb, kvh, b;
+                tile(t, kb, kvh, b);
+                const int row0 = b * sh.S;
+                const int kcol = (sh.H + kvh) * HD, vcol = (sh.H + sh.Hkv + kvh) * HD;
+                const int ob = lt % C::OWN;
+                mbar_wait(&kv_empty[ob], ((lt / C::OWN) & 1) ^ 1);
+                mbar_expect_tx(&kv_full[ob], 2 * C::BIG);
+                for (int a = 0; a < C::ATOMS; ++a) {
+                    tma_load_2d(&tmK, &kv_full[ob], sK + ob * C::BIG + a * C::A_BIG, kcol + 64 * a, row0 + kb * kRowsB);
+                    tma_load_2d(&tmK, &kv_full[ob], sV + ob * C::BIG + a * C::A_BIG, vcol + 64 * a, row0 + kb * kRowsB);
+                }
+                const int n = group * per_head(kb);
+                for (int j = 0; j < n; ++j, ++g) {
+                    int hq, qs;
+                    step_of(kb, kvh, j, hq, qs);
+                    const int st = g % C::ST;
+                    mbar_wait(&q_empty[st], ((g / C::ST) & 1) ^ 1);
+                    mbar_expect_tx(&q_full[st], 2 * C::SMALL + 2 * kStepB * 4);
+                    for (int a = 0; a < C::ATOMS; ++a) {
+                        tma_load_2d(&tmQ, &q_full[st], sQ + st * C::SMALL + a * C::A_SMALL, hq * HD + 64 * a,
+                                    row0 + qs * kStepB);
+                        tma_load_2d(&tmDO, &q_full[st], sDO + st * C::SMALL + a * C::A_SMALL, hq * HD + 64 * a,
+                                    row0 + qs * kStepB);
+                    }
+                    const int64_t li = (static_cast<int64_t>(b) * sh.H + hq) * sh.S + qs * kStepB;
+                    bulk_load_b(sL + st * kStepB, lse + li, kStepB * 4, &q_full[st]);
+                    bulk_load_b(sD + st * kStepB, delta + li, kStepB * 4, &q_full[st]);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ===== MMA issuer =====
+            constexpr uint32_t ID_S = make_idesc(128, kStepB, false, false);
+            constexpr uint32_t ID_D = make_idesc(128, HD, false, true);
+            uint64_t dk_, dv_;  // the tile's K / V descriptors (K-major, k step 0)
+            auto issue_s = [&](int gg) {
+                const int st = gg % C::ST, bb = gg & 1;
+                mbar_wait(&q_full[st], (gg / C::ST) & 1);
+                if (SEP && gg >= 2) mbar_wait(&s_free[bb], ((gg - 2) >> 1) & 1);
+                fence_after();
+                const uint64_t dq = make_desc(smem_u32(sQ + st * C::SMALL), 16, 1024);
+                const uint64_t ddo = make_desc(smem_u32(sDO + st * C::SMALL), 16, 1024);
+#pragma unroll
+                for (int kk = 0; kk < HD / 16; ++kk) {
+                    const uint32_t ob = (kk / 4) * C::A_BIG + (kk % 4) * 32, sb = (kk / 4) * C::A_SMALL + (kk % 4) * 32;
+                    umma<false>(tmem + 128 * bb, dadd(dk_, ob), dadd(dq, sb), ID_S, kk > 0);
+                    umma<false>(tmem + 128 * bb + 64, dadd(dv_, ob), dadd(ddo, sb), ID_S, kk > 0);
+                }
+                umma_commit(&s_full[bb]);
+            };
+            auto issue_d = [&](int gg, bool first) {
+                const int st = gg % C::ST, bb = gg & 1;
+                mbar_wait(&p_full[bb], (gg >> 1) & 1);
+                fence_after();
+                const uint64_t dq = make_desc(smem_u32(sQ + st * C::SMALL), C::A_SMALL, 1024);
+                const uint64_t ddo = make_desc(smem_u32(sDO + st * C::SMALL), C::A_SMALL, 1024);
+#pragma unroll
+                for (int kk = 0; kk < kStepB / 16; ++kk) {
+                    const uint32_t acc = (!first || kk > 0) ? 1u : 0u;
+                    umma_ts(tmem + T_ACC, tmem + ds_col(bb) + ts_col<SEP>(kk), dadd(dq, kk * 2048), ID_D, acc);
+                    umma_ts(tmem + T_ACC + HD, tmem + p_col(bb) + ts_col<SEP>(kk), dadd(ddo, kk * 2048), ID_D, acc);
+                }
+                if (SEP) umma_commit(&ds_free[bb]);
+                umma_commit(&q_empty[st]);
+            };
+            int g = 0, lt = 0;
+            for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++lt) {
+                int kb, kvh, b;
+                tile(t, kb, kvh, b);
+                const int n = group * per_head(kb);
+                const int ob = lt % C::OWN;
+                mbar_wait(&kv_full[ob], (lt / C::OWN) & 1);
+                dk_ = make_desc(smem_u32(sK + ob * C::BIG), 16, 1024);
+                dv_ = make_desc(smem_u32(sV + ob * C::BIG), 16, 1024);
+                issue_s(g);
+                issue_s(g + 1);  // (n >= 2: sequences are whole 128-row blocks)
+                mbar_wait(acc_empty, (lt & 1) ^ 1);  // the previous tile's dK / dV are read out
+                fence_after();
+                for (int j = 0; j < n; ++j) {
+                    // separate P / dS: S / dP of step j + 2 as soon as step j's are loaded;
+                    // written back over S / dP: only after the products that read them
+                    if (SEP && j + 2 < n) issue_s(g + j + 2);
+                    issue_d(g + j, j == 0);
+                    if (!SEP && j + 2 < n) issue_s(g + j + 2);
+                }
+                umma_commit(acc_full);
+                umma_commit(&kv_empty[ob]);
+                g += n;
+            }
+        }
+    } else if (warp >= 4) {
+        // ===== elementwise: thread = key row, half = which 32 queries of a 64-query step =====
+        const int q4 = warp & 3, half = (warp - 4) >> 2;
+        const int r = q4 * 32 + lane;
+        const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
+        uint32_t vs[32], vp[32];
+        int g = 0, lt = 0;
+        for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++lt) {
+            int kb, kvh, b;
+            tile(t, kb, kvh, b);
+            const int key = kb * kRowsB + r;
+            const int n = group * per_head(kb);
+            for (int j = 0; j < n; ++j, ++g) {
+                int hq, qs;
+                step_of(kb, kvh, j, hq, qs);
+                const int st = g % C::ST, bb = g & 1;
+                mbar_wait(&s_full[bb], (g >> 1) & 1);
+                fence_after();
+                const uint32_t cs = tmem + lane_off + 128 * bb + 32 * half;
+                tmem_ld32_async(cs, vs);
+                tmem_ld32_async(cs + 64, vp);
+                // lse / delta of this half's 32 queries (landed with the step's Q tile, which the
+                // S MMA already waited for)
+                const float4* L4 = reinterpret_cast<const float4*>(sL + st * kStepB + 32 * half);
+                const float4* D4 = reinterpret_cast<const float4*>(sD + st * kStepB + 32 * half);
+                tmem_ld_wait(vs);
+                tmem_ld_wait(vp);
+                if (SEP) {
+                    fence_before();
+                    mbar_arrive(&s_free[bb]);  // the MMAs of step g + 2 may overwrite S / dP now
+                }
+                const int q0 = qs * kStepB + 32 * half;  // first query of this half
+                const bool mask = sh.causal && kb * kRowsB + kRowsB - 1 > q0;
+                uint32_t pp[16], dd[16];
+#pragma unroll
+                for (int i4 = 0; i4 < 8; ++i4) {
+                    const float4 l = L4[i4], dl = D4[i4];
+                    const float lv[4] = {l.x, l.y, l.z, l.w}, dv[4] = {dl.x, dl.y, dl.z, dl.w};
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                        const int i = 2 * i4 + u;  // query pair (2 i, 2 i + 1)
+                        float p0 = ex2_approx(fmaf(__uint_as_float(vs[2 * i]), sh.scale_log2, -lv[2 * u]));
+                        float p1 = ex2_approx(fmaf(__uint_as_float(vs[2 * i + 1]), sh.scale_log2, -lv[2 * u + 1]));
+                        if (mask) {
+                            if (key > q0 + 2 * i) p0 = 0.0f;
+                            if (key > q0 + 2 * i + 1) p1 = 0.0f;
+                        }
+                        pp[i] = pack_bf16(p0, p1);
+                        dd[i] = pack_bf16(p0 * (__uint_as_float(vp[2 * i]) - dv[2 * u]),
+                                          p1 * (__uint_as_float(vp[2 * i + 1]) - dv[2 * u + 1]));
+                    }
+                }
+                if (SEP && g >= 2) {  // the products of step g - 2 have read these P / dS buffers
+                    mbar_wait(&ds_free[bb], ((g - 2) >> 1) & 1);
+                    fence_after();
+                }
+                const uint32_t pofs = SEP ? 16 * half : 32 * half;
+                tmem_st16(tmem + lane_off + p_col(bb) + pofs, pp);
+                tmem_st16(tmem + lane_off + ds_col(bb) + pofs, dd);
+                tmem_st_wait();
+                fence_before();
+                mbar_arrive(&p_full[bb]);
+            }
+            // the tile's dK (half 0, with the softmax scale) or dV (half 1) out of TMEM
+            mbar_wait(acc_full, lt & 1);
+            fence_after();
+            __nv_bfloat16* row = dqkv + (static_cast<int64_t>(b) * sh.S + key) * sh.ld +
+                                 (half == 0 ? (sh.H + kvh) * HD : (sh.H + sh.Hkv + kvh) * HD);
+            const float sc = half == 0 ? sh.scale : 1.0f;
+#pragma unroll
+            for (int c = 0; c < HD / 32; ++c) {
+                tmem_ld32_async(tmem + lane_off + T_ACC + half * HD + c * 32, vs);
+                tmem_ld_wait(vs);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    uint4 w;
+                    w.x = pack_bf16(__uint_as_float(vs[8 * u + 0]) * sc, __uint_as_float(vs[8 * u + 1]) * sc);
+                    w.y = pack_bf16(__uint_as_float(vs[8 * u + 2]) * sc, __uint_as_float(vs[8 * u + 3]) * sc);
+                    w.z = pack_bf16(__uint_as_float(vs[8 * u + 4]) * sc, __uint_as_float(vs[8 * u + 5]) * sc);
+                    w.w = pack_bf16(__uint_as_float(vs[8 * u + 6]) * sc, __uint_as_float(vs[8 * u + 7]) * sc);
+                    reinterpret_cast<uint4*>(row + c * 32)[u] = w;
+                }
+            }
+            fence_before();
+            mbar_arrive(acc_empty);
+        }
+    }
+    __syncwarp();
+    fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+    }
+}
+
+template <int HD>
+cudaError_t launch_bwd2(const AttnProblem& a, cudaStream_t st) {
+    using C = BCfg<HD>;
+    constexpr bool SEP = C::SEP_DKDV;
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(attn_bwd_dq2_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             C::SMEM_DQ);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(attn_bwd_dkdv2_kernel<HD, SEP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     C::SMEM_DKDV);
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    const int ld = (a.n_heads + 2 * a.n_kv_heads) * a.head_dim;
+    const int ldo = a.n_heads * a.head_dim;
+    const uint64_t T = static_cast<uint64_t>(a.tokens);
+    CUtensorMap t128, t64, do128, do64;
+    if (!make_map(&t128, a.qkv, ld, T, ld, 64, kRowsB, false, false) ||
+        !make_map(&t64, a.qkv, ld, T, ld, 64, kStepB, false, false) ||
+        !make_map(&do128, a.dout, ldo, T, ldo, 64, kRowsB, false, false) ||
+        !make_map(&do64, a.dout, ldo, T, ldo, 64, kStepB, false, false))
+        return cudaErrorInvalidValue;
+    BShape sh;
+    sh.S = a.seq_len;
+    sh.H = a.n_heads;
+    sh.Hkv = a.n_kv_heads;
+    sh.ld = ld;
+    sh.ldo = ldo;
+    sh.causal = a.causal;
+    sh.scale = 1.0f / sqrtf(static_cast<float>(a.head_dim));
+    sh.scale_log2 = 1.4426950408889634f * sh.scale;
+    const int n_seq = static_cast<int>(a.tokens / a.seq_len);
+    const int q_tiles = (a.seq_len / kRowsB) * a.n_heads * n_seq;
+    const int kv_tiles = (a.seq_len / kRowsB) * a.n_kv_heads * n_seq;
+    auto* dq = static_cast<__nv_bfloat16*>(a.dqkv);
+    attn_bwd_dq2_kernel<HD><<<q_tiles < num_sms() ? q_tiles : num_sms(), kThreadsB, C::SMEM_DQ, st>>>(
+        t128, do128, t64, static_cast<const __nv_bfloat16*>(a.o), static_cast<const __nv_bfloat16*>(a.dout), a.lse,
+        a.delta, dq, sh, n_seq);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    attn_bwd_dkdv2_kernel<HD, SEP><<<kv_tiles < num_sms() ? kv_tiles : num_sms(), kThreadsB, C::SMEM_DKDV, st>>>(
+        t128, t64, do64, a.lse, a.delta, dq, sh, n_seq);
+    return cudaGetLastError();
+}
+}  // namespace
+
+// The backward for head_dim 64 / 128 and sequences of whole 128-row blocks; delta is formed
+// inside (no separate kernel). cudaErrorNotSupported for other shapes.
+cudaError_t attention_backward_tc2(const AttnProblem& a, cudaStream_t st) {
+    if (a.seq_len % kRowsB != 0) return cudaErrorNotSupported;
+    if (a.head_dim == 64) return launch_bwd2<64>(a, st);
+    if (a.head_dim == 128) return launch_bwd2<128>(a, st);
+    return cudaErrorNotSupported;
+}
+
+}  // namespace sp

@@ -13,7 +13,7 @@ namespace sp {
 namespace {
 
 constexpr int kRowsPerBlock = 8;  // one warp per row
-constexpr int kChunkRows = 128;   // parameter-gradient partials: rows per chunk
+constexpr int kChunkRows = 512;   // column-sum partials: rows per chunk
 constexpr int kRowLanes = 8;
 
 __device__ __forceinline__ float warp_allsum(float v) {
@@ -122,23 +122,57 @@ __global__ void __launch_bounds__(32 * kRowsPerBlock) norm_bwd_kernel(
     }
 }
 
-// part[chunk][0][j] = sum_r dy[r][j] xhat[r][j], part[chunk][1][j] = sum_r dy[r][j] over the
-// chunk's 128 rows. Block = 32 threads x 4 columns, 8 row lanes; lanes combined in a fixed
-// order through shared memory.
+// The last block of a column group to finish (of nchunks) sees every chunk's partial: the
+// writes of each block are fenced before its counter increment, the last block fences again
+// before reading. It re-arms the counter for the next launch on the stream.
+__device__ __forceinline__ bool last_chunk_block(int* counter, int nchunks) {
+    __shared__ int s_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0 && threadIdx.y == 0) {
+        s_last = atomicAdd(counter, 1) == nchunks - 1;
+        if (s_last) *counter = 0;
+    }
+    __syncthreads();
+    if (s_last) __threadfence();
+    return s_last;
+}
+
+// Sum over chunks 0..n-1 of part[c * stride + j], in chunk order (L2 reads: other blocks wrote
+// them). Loads are issued eight at a time; the adds stay sequential.
+__device__ __forceinline__ float chunk_sum(const float* part, int n, int64_t stride, int64_t j) {
+    float s = 0.0f;
+    int c = 0;
+    for (; c + 8 <= n; c += 8) {
+        float v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = __ldcg(part + static_cast<int64_t>(c + u) * stride + j);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) s += v[u];
+    }
+    for (; c < n; ++c) s += __ldcg(part + static_cast<int64_t>(c) * stride + j);
+    return s;
+}
+
+// Norm parameter gradients: per kChunkRows-row chunk, part[chunk][0][j] = sum_r dy xhat and
+// part[chunk][1][j] = sum_r dy (block = 32 threads x 4 columns, 8 row lanes combined in a fixed
+// order through shared memory); the last chunk block of each column group then sums the chunks
+// in order into out[j] (and out[d + j] for LayerNorm's beta).
 __global__ void __launch_bounds__(32 * kRowLanes) norm_param_kernel(const float* __restrict__ dy,
                                                                     const float* __restrict__ x,
                                                                     const float* __restrict__ stats,
                                                                     int64_t rows, int d, int rms,
-                                                                    float* __restrict__ part) {
+                                                                    float* __restrict__ part, int* __restrict__ counters,
+                                                                    float* __restrict__ out) {
     __shared__ float4 red[2][kRowLanes][32];
     const int c4 = blockIdx.x * 32 + threadIdx.x;  // float4 column group
     const int lane_r = threadIdx.y;
     const int64_t r0 = static_cast<int64_t>(blockIdx.y) * kChunkRows;
     float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = make_float4(0.f, 0.f, 0.f, 0.f);
     if (4 * c4 < d) {
-        for (int i = 0; i < kChunkRows / kRowLanes; ++i) {
-            const int64_t r = r0 + lane_r + static_cast<int64_t>(i) * kRowLanes;
-            if (r >= rows) break;
+        const int64_t rend = min(rows, r0 + kChunkRows);
+#pragma unroll 4
+        for (int64_t r = r0 + lane_r; r < rend; r += kRowLanes) {
             const float mean = rms ? 0.0f : stats[2 * r], rstd = stats[2 * r + 1];
             const float4 e = __ldg(reinterpret_cast<const float4*>(dy + r * d) + c4);
             const float4 v = __ldg(reinterpret_cast<const float4*>(x + r * d) + c4);
@@ -160,6 +194,59 @@ __global__ void __launch_bounds__(32 * kRowLanes) norm_param_kernel(const float*
         }
         reinterpret_cast<float4*>(part + (static_cast<int64_t>(blockIdx.y) * 2 + lane_r) * d)[c4] = s;
     }
+    if (!last_chunk_block(counters + blockIdx.x, gridDim.y)) return;
+    // 256 threads: (which, column) for the group's 128 columns
+    const int t = threadIdx.y * 32 + threadIdx.x;
+    const int which = t >> 7, j = blockIdx.x * 128 + (t & 127);
+    if (j >= d || (rms && which == 1)) return;
+    out[static_cast<int64_t>(which) * d + j] = chunk_sum(part + static_cast<int64_t>(which) * d, gridDim.y, 2 * static_cast<int64_t>(d), j);
+}
+
+// Column sums of a bf16 [rows][N] matrix (a bias gradient): per kChunkRows-row chunk, block =
+// 32 groups of 8 columns (one 16-byte load each) x 8 row lanes, lanes combined in a fixed order
+// into part[chunk][N]; the last chunk block of each 256-column group sums the chunks in order.
+__global__ void __launch_bounds__(32 * kRowLanes) colsum_total_kernel(const __nv_bfloat16* __restrict__ x, int64_t rows,
+                                                                      int n, float* __restrict__ part,
+                                                                      int* __restrict__ counters, float* __restrict__ out) {
+    __shared__ float red[kRowLanes][32][9];
+    const int g = blockIdx.x * 32 + threadIdx.x;  // 8-column group
+    const int lane_r = threadIdx.y;
+    const int64_t r0 = static_cast<int64_t>(blockIdx.y) * kChunkRows;
+    float acc[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
+    if (8 * g < n) {
+        const int64_t rend = min(rows, r0 + kChunkRows);
+#pragma unroll 8
+        for (int64_t r = r0 + lane_r; r < rend; r += kRowLanes) {
+            const uint4 v = __ldg(reinterpret_cast<const uint4*>(x + r * n) + g);
+            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[h]));
+                acc[2 * h] += f.x;
+                acc[2 * h + 1] += f.y;
+            }
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) red[lane_r][threadIdx.x][i] = acc[i];
+    __syncthreads();
+    if (lane_r == 0 && 8 * g < n) {
+        float o[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            float s = red[0][threadIdx.x][i];
+            for (int l = 1; l < kRowLanes; ++l) s += red[l][threadIdx.x][i];
+            o[i] = s;
+        }
+        float4* dst = reinterpret_cast<float4*>(part + static_cast<int64_t>(blockIdx.y) * n + 8 * g);
+        dst[0] = make_float4(o[0], o[1], o[2], o[3]);
+        dst[1] = make_float4(o[4], o[5], o[6], o[7]);
+    }
+    if (!last_chunk_block(counters + blockIdx.x, gridDim.y)) return;
+    const int j = blockIdx.x * 256 + threadIdx.y * 32 + threadIdx.x;
+    if (j < n) out[j] = chunk_sum(part, gridDim.y, n, j);
 }
 
 }  // namespace
@@ -174,8 +261,9 @@ void norm_forward(const float* x, const float* gamma, const float* beta, int rms
     else launch_kernel(norm_fwd_kernel<false>, grid, dim3(32 * kRowsPerBlock), 0, st, x, gamma, beta, eps, rows, d, yo, stats);
 }
 
-int norm_backward(const float* dy, const float* x, const float* stats, const float* gamma, int rms, int64_t rows,
-                  int d, const float* dres_in, float* dres_out, void* dres_out16, float* part, cudaStream_t st) {
+void norm_backward(const float* dy, const float* x, const float* stats, const float* gamma, int rms, int64_t rows,
+                   int d, const float* dres_in, float* dres_out, void* dres_out16, const ColScratch& scr, float* out,
+                   cudaStream_t st) {
     if (dres_out) {
         const dim3 grid(static_cast<unsigned>((rows + kRowsPerBlock - 1) / kRowsPerBlock));
         auto* o16 = static_cast<__nv_bfloat16*>(dres_out16);
@@ -186,12 +274,24 @@ int norm_backward(const float* dy, const float* x, const float* stats, const flo
             launch_kernel(norm_bwd_kernel<false>, grid, dim3(32 * kRowsPerBlock), 0, st, dy, x, stats, gamma, rows, d,
                           dres_in, dres_out, o16);
     }
-    const int chunks = norm_param_chunks(rows);
-    if (part) {
-        const dim3 grid(static_cast<unsigned>((d / 4 + 31) / 32), static_cast<unsigned>(chunks));
-        launch_kernel(norm_param_kernel, grid, dim3(32, kRowLanes), 0, st, dy, x, stats, rows, d, rms, part);
+    if (out) {
+        const dim3 grid(static_cast<unsigned>((d / 4 + 31) / 32), static_cast<unsigned>(norm_param_chunks(rows)));
+        launch_kernel(norm_param_kernel, grid, dim3(32, kRowLanes), 0, st, dy, x, stats, rows, d, rms, scr.part,
+                      scr.counters, out);
     }
-    return chunks;
+}
+
+void colsum_total_bf16(const void* x, int64_t rows, int n, const ColScratch& scr, float* out, cudaStream_t st) {
+    const dim3 grid(static_cast<unsigned>((n / 8 + 31) / 32), static_cast<unsigned>(norm_param_chunks(rows)));
+    launch_kernel(colsum_total_kernel, grid, dim3(32, kRowLanes), 0, st, static_cast<const __nv_bfloat16*>(x), rows, n,
+                  scr.part, scr.counters, out);
+}
+
+ColScratchSize col_scratch_size(int64_t rows, int widest) {
+    ColScratchSize s;
+    s.part_floats = static_cast<size_t>(norm_param_chunks(rows)) * 2 * static_cast<size_t>(widest);
+    s.counters = static_cast<size_t>((widest + 127) / 128);
+    return s;
 }
 
 }  // namespace sp

@@ -200,7 +200,18 @@ __global__ void __launch_bounds__(256) colsum_f32_kernel(const float* __restrict
 __global__ void reduce_kernel(const float* __restrict__ parts, int nparts, int64_t stride,
                               int64_t count, float* __restrict__ grad) {
     const int64_t gs = static_cast<int64_t>(gridDim.x) * blockDim.x;
-    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += gs) {
+    const int64_t t0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const bool vec = stride % 4 == 0 && ((reinterpret_cast<uintptr_t>(parts) | reinterpret_cast<uintptr_t>(grad)) & 15) == 0;
+    const int64_t n4 = vec ? count / 4 : 0;
+    for (int64_t i = t0; i < n4; i += gs) {
+        float4 s = __ldg(reinterpret_cast<const float4*>(parts) + i);
+        for (int p = 1; p < nparts; ++p) {
+            const float4 v = __ldg(reinterpret_cast<const float4*>(parts + p * stride) + i);
+            s.x += v.x, s.y += v.y, s.z += v.z, s.w += v.w;
+        }
+        reinterpret_cast<float4*>(grad)[i] = s;
+    }
+    for (int64_t i = 4 * n4 + t0; i < count; i += gs) {
         float s = parts[i];
         for (int p = 1; p < nparts; ++p) s += parts[p * stride + i];
         grad[i] = s;
@@ -365,7 +376,7 @@ int colsum_f32(const float* x, int64_t rows, int d, float* partials, cudaStream_
 
 void reduce_partials(const float* parts, int nparts, int64_t stride, int64_t count,
                      float* grad, cudaStream_t st) {
-    launch_kernel(reduce_kernel, dim3(grid_for(count)), dim3(kThreads), 0, st, parts, nparts, stride,
+    launch_kernel(reduce_kernel, dim3(grid_for(count / 4 + 1)), dim3(kThreads), 0, st, parts, nparts, stride,
                count, grad);
 }
 
@@ -454,40 +465,80 @@ void convert_regions(const ConvertRegions& r, cudaStream_t st) {
 }
 
 namespace {
-// One thread per parameter of region blockIdx.y: rebuild the fp32 master from its halves (or
-// read the fp32 vector), apply the update in the reference's order, store it back split.
+// Eight parameters per thread of region blockIdx.y (every region is 256-byte aligned and a
+// multiple of 64 elements, block.cpp): rebuild the fp32 master from its halves (or read the
+// fp32 vector), take the gradient from g, or as the fixed-order sum of the region's split-K
+// partials, apply the update in the reference's order, and store it back split.
+__device__ __forceinline__ void load8(const float* p, float (&v)[8]) {
+    const float4 a = __ldg(reinterpret_cast<const float4*>(p)), b = __ldg(reinterpret_cast<const float4*>(p) + 1);
+    v[0] = a.x, v[1] = a.y, v[2] = a.z, v[3] = a.w, v[4] = b.x, v[5] = b.y, v[6] = b.z, v[7] = b.w;
+}
+__device__ __forceinline__ void store8(float* p, const float (&v)[8]) {
+    reinterpret_cast<float4*>(p)[0] = make_float4(v[0], v[1], v[2], v[3]);
+    reinterpret_cast<float4*>(p)[1] = make_float4(v[4], v[5], v[6], v[7]);
+}
+
 __global__ void split_update_kernel(SplitRegions r, const float* __restrict__ g, float* __restrict__ m,
                                     float* __restrict__ v, float lr, int opt, const AdamwScalars* __restrict__ sc) {
     const int i = blockIdx.y;
-    const int64_t n = r.count[i];
+    const int64_t n8 = r.count[i] / 8;
     const int64_t base = r.off[i];
     const bool matrix = r.lo[i] != nullptr;
+    const float* parts = r.parts[i];
+    const int np = r.nparts[i];
     AdamwScalars s{};
     if (opt == 1) s = *sc;
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-    for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += stride) {
-        float w;
+    for (int64_t e8 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e8 < n8; e8 += stride) {
+        const int64_t e = 8 * e8;
+        float w[8], gr[8];
         if (matrix) {
-            const uint32_t hi = static_cast<const uint16_t*>(r.hi[i])[e], lo = r.lo[i][e];
-            w = __uint_as_float(hi << 16 | lo);
+            const uint4 hv = *reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(r.hi[i]) + e);
+            const uint4 lv = *reinterpret_cast<const uint4*>(r.lo[i] + e);
+            const uint32_t h4[4] = {hv.x, hv.y, hv.z, hv.w}, l4[4] = {lv.x, lv.y, lv.z, lv.w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                w[2 * k] = __uint_as_float((h4[k] << 16) | (l4[k] & 0xFFFFu));
+                w[2 * k + 1] = __uint_as_float((h4[k] & 0xFFFF0000u) | (l4[k] >> 16));
+            }
         } else {
-            w = static_cast<const float*>(r.hi[i])[e];
+            load8(static_cast<const float*>(r.hi[i]) + e, w);
         }
-        const float gr = g[base + e];
+        if (parts) {
+            load8(parts + e, gr);
+            for (int p = 1; p < np; ++p) {
+                float q[8];
+                load8(parts + static_cast<int64_t>(p) * r.count[i] + e, q);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) gr[k] += q[k];
+            }
+        } else {
+            load8(g + base + e, gr);
+        }
         if (opt == 1) {
-            float mm = m[base + e], vv = v[base + e];
-            adamw_elem(w, mm, vv, gr, s);
-            m[base + e] = mm;
-            v[base + e] = vv;
+            float mm[8], vv[8];
+            load8(m + base + e, mm);
+            load8(v + base + e, vv);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) adamw_elem(w[k], mm[k], vv[k], gr[k], s);
+            store8(m + base + e, mm);
+            store8(v + base + e, vv);
         } else {
-            w = __fsub_rn(w, __fmul_rn(lr, gr));
+#pragma unroll
+            for (int k = 0; k < 8; ++k) w[k] = __fsub_rn(w[k], __fmul_rn(lr, gr[k]));
         }
         if (matrix) {
-            const uint32_t bits = __float_as_uint(w);
-            static_cast<uint16_t*>(r.hi[i])[e] = static_cast<uint16_t>(bits >> 16);
-            r.lo[i][e] = static_cast<uint16_t>(bits & 0xFFFFu);
+            uint32_t h4[4], l4[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t b0 = __float_as_uint(w[2 * k]), b1 = __float_as_uint(w[2 * k + 1]);
+                h4[k] = (b0 >> 16) | (b1 & 0xFFFF0000u);
+                l4[k] = (b0 & 0xFFFFu) | (b1 << 16);
+            }
+            *reinterpret_cast<uint4*>(static_cast<uint16_t*>(r.hi[i]) + e) = make_uint4(h4[0], h4[1], h4[2], h4[3]);
+            *reinterpret_cast<uint4*>(r.lo[i] + e) = make_uint4(l4[0], l4[1], l4[2], l4[3]);
         } else {
-            static_cast<float*>(r.hi[i])[e] = w;
+            store8(static_cast<float*>(r.hi[i]) + e, w);
         }
     }
 }
@@ -498,8 +549,8 @@ void split_update(const SplitRegions& r, const float* g, float* m, float* v, flo
     if (r.n <= 0) return;
     int64_t most = 0;
     for (int i = 0; i < r.n; ++i) most = most > r.count[i] ? most : r.count[i];
-    launch_kernel(split_update_kernel, dim3(grid_for(most), static_cast<unsigned>(r.n)), dim3(kThreads), 0, st, r,
-                  g, m, v, lr, opt, scalars);
+    launch_kernel(split_update_kernel, dim3(grid_for((most + 7) / 8), static_cast<unsigned>(r.n)), dim3(kThreads), 0,
+                  st, r, g, m, v, lr, opt, scalars);
 }
 
 }  // namespace sp

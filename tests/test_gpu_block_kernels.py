@@ -161,6 +161,8 @@ ATTN = [  # (batch, S, H, Hkv, hd, causal)
     (3, 257, 2, 2, 80, 0),      # ViT-H/14: 257 tokens, head dim 80, bidirectional
     (2, 256, 8, 2, 128, 1),     # Llama-3 GQA: 4 q heads per kv head, head dim 128
     (1, 100, 2, 1, 64, 1),      # ragged
+    (2, 256, 2, 2, 64, 0),      # bidirectional, whole 128-row blocks (the tcgen05 backward)
+    (1, 384, 4, 4, 128, 0),
 ]
 
 
@@ -169,13 +171,14 @@ def _split(qkv, B, S, H, Hkv, hd):
     return t[:, :H], t[:, H:H + Hkv], t[:, H + Hkv:]
 
 
-@pytest.mark.parametrize("fwd_kind", [2, 1], ids=["tcgen05", "mma-sync"])
+@pytest.mark.parametrize("fwd_kind,bwd_kind", [(2, 0), (2, 2), (1, 1)], ids=["tcgen05", "tcgen05-bwd-v1", "mma-sync"])
 @pytest.mark.parametrize("B,S,H,Hkv,hd,causal", ATTN)
-def test_attention_forward_and_backward(B, S, H, Hkv, hd, causal, fwd_kind):
-    # kind 2 / 0: the tcgen05 forward and backward (head dims 64 / 128, whole 128-row sequence
-    # blocks for the backward; other shapes take the mma.sync kernels), 1: the mma.sync kernels
+def test_attention_forward_and_backward(B, S, H, Hkv, hd, causal, fwd_kind, bwd_kind):
+    # forward kind 2 / 0: the tcgen05 kernel (head dims 64 / 128), 1: mma.sync. Backward kind 0:
+    # the v2 tcgen05 passes (dQ + delta, then dK/dV; whole 128-row sequence blocks), 2: the v1
+    # tcgen05 passes, 1: mma.sync; shapes a tcgen05 kind does not cover take the mma.sync kernels
     assert LIB.sp_debug_set(None, b"attn_fwd", fwd_kind) == 0
-    assert LIB.sp_debug_set(None, b"attn_bwd", 0 if fwd_kind == 2 else 1) == 0
+    assert LIB.sp_debug_set(None, b"attn_bwd", bwd_kind) == 0
     T, W = B * S, (H + 2 * Hkv) * hd
     qkv = bf(torch.randn(T, W, device="cuda"))
     o = torch.empty(T, H * hd, device="cuda", dtype=torch.bfloat16)
@@ -254,16 +257,45 @@ def test_norm_forward_backward(T, d, rms):
     dres_in = torch.randn(T, d, device="cuda")
     dres_out = torch.empty(T, d, device="cuda")
     d16 = torch.empty(T, d, device="cuda", dtype=torch.bfloat16)
-    chunks = (T + 127) // 128
-    part = torch.empty(chunks, 2, d, device="cuda")
-    n = LIB.sp_debug_norm_backward(dy.data_ptr(), x.data_ptr(), stats.data_ptr(), g.data_ptr(), rms, T, d,
-                                   dres_in.data_ptr(), dres_out.data_ptr(), d16.data_ptr(), part.data_ptr(), st)
-    torch.cuda.synchronize()
-    assert n == chunks
+    part, cnt = _col_scratch(T, d)
+    out = torch.zeros(2, d, device="cuda")
+    for rep in range(2):  # the counters re-arm: a second launch on the same scratch is identical
+        assert LIB.sp_debug_norm_backward(dy.data_ptr(), x.data_ptr(), stats.data_ptr(), g.data_ptr(), rms, T, d,
+                                          dres_in.data_ptr(), dres_out.data_ptr(), d16.data_ptr(), part.data_ptr(),
+                                          cnt.data_ptr(), out.data_ptr(), st) == 0
+        torch.cuda.synchronize()
+        if rep == 0:
+            first = out.clone()
+    assert torch.equal(first, out) and int(cnt.abs().sum()) == 0
     want = dres_in + xv.grad
     assert rel(dres_out, want) < 1e-4
     assert rel(d16, want) < 1e-2
-    sums = part.sum(0)
-    assert rel(sums[0], gv.grad) < 1e-4
+    assert rel(out[0], gv.grad) < 1e-4
     if not rms:
-        assert rel(sums[1], bv.grad) < 1e-4
+        assert rel(out[1], bv.grad) < 1e-4
+
+
+def _col_scratch(rows, widest):
+    import ctypes
+    pf, nc = ctypes.c_int64(), ctypes.c_int64()
+    LIB.sp_debug_col_scratch(rows, widest, ctypes.byref(pf), ctypes.byref(nc))
+    return (torch.empty(pf.value, device="cuda"), torch.zeros(nc.value, device="cuda", dtype=torch.int32))
+
+
+@pytest.mark.parametrize("T,n", [(16384, 1600), (16384, 6400), (1000, 4800), (64, 64), (513, 256)])
+def test_colsum_total_fixed_order(T, n):
+    """Bias gradients: the column sums of a bf16 [T][n] matrix reduced inside one launch (the last
+    block of each column group sums the chunk partials in order) against fp64, and bitwise
+    repeatable with the scratch the first launch left behind."""
+    x = (torch.randn(T, n, device="cuda") * 0.1).to(torch.bfloat16)
+    part, cnt = _col_scratch(T, n)
+    st = _stream()
+    outs = []
+    for _ in range(2):
+        out = torch.empty(n, device="cuda")
+        assert LIB.sp_debug_colsum(x.data_ptr(), T, n, part.data_ptr(), cnt.data_ptr(), out.data_ptr(), st) == 0
+        torch.cuda.synchronize()
+        outs.append(out)
+    assert torch.equal(outs[0], outs[1]) and int(cnt.abs().sum()) == 0
+    ref = x.double().sum(0)
+    assert (outs[0].double() - ref).abs().max().item() <= 1e-5 * max(1.0, ref.abs().max().item()) + 1e-4
