@@ -106,6 +106,14 @@ int sp_debug_norm_backward(const float* dy, const float* x, const float* stats, 
  * same scratch (kernels.hpp colsum_total_bf16). */
 int sp_debug_colsum(const void* x, int64_t rows, int32_t n, float* part, int32_t* counters, float* out, void* stream);
 void sp_debug_col_scratch(int64_t rows, int32_t widest, int64_t* part_floats, int64_t* counters);
+/* The single-pass norm backward (kernels.hpp norm_backward_fused, d % 4 == 0 and d <= 2048, else
+ * SP_ERR_INVALID) and its chunk reduction: dres_out / dres_out16 as above (dres_out null: none),
+ * out_param[0, d) / [d, 2d) the parameter gradients (null: none) and out_csum[j] = sum over rows
+ * of dres_out (null: none). ppart holds 2 d, cpart d floats per 64-row chunk. */
+int sp_debug_norm_backward_fused(const float* dy, const float* x, const float* stats, const float* gamma,
+                                 int32_t rms, int64_t rows, int32_t d, const float* dres_in, float* dres_out,
+                                 void* dres_out16, float* ppart, float* cpart, float* out_param, float* out_csum,
+                                 void* stream);
 
 /* Transformer-block executors: the fp32 gradient image (the layer's parameter layout) of
  * layer `index` from the last train step, as the UPDATE op consumed it. Gradient images are

@@ -102,7 +102,7 @@ EXPORTS = [
     "sp_debug_effective_splits",
     "sp_debug_shard_range", "sp_debug_dw_splits", "sp_debug_dw_choice",
     "sp_debug_plan_two_calls", "sp_debug_set", "sp_debug_gemm_ex", "sp_debug_attention",
-    "sp_debug_norm_forward", "sp_debug_norm_backward", "sp_debug_colsum", "sp_debug_col_scratch",
+    "sp_debug_norm_forward", "sp_debug_norm_backward", "sp_debug_norm_backward_fused", "sp_debug_colsum", "sp_debug_col_scratch",
     "sp_debug_read_grad",
 ]
 
@@ -173,6 +173,8 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "sp_debug_attention": ([i32, i64, i32, i32, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp], C.c_int),
         "sp_debug_norm_forward": ([vp, vp, vp, i32, C.c_float, i64, i32, vp, vp, vp], C.c_int),
         "sp_debug_norm_backward": ([vp, vp, vp, vp, i32, i64, i32, vp, vp, vp, vp, vp, vp, vp], C.c_int),
+        "sp_debug_norm_backward_fused": ([vp, vp, vp, vp, i32, i64, i32, vp, vp, vp, vp, vp, vp, vp, vp],
+                                         C.c_int),
         "sp_debug_colsum": ([vp, i64, i32, vp, vp, vp, vp], C.c_int),
         "sp_debug_col_scratch": ([i64, i32, vp, vp], None),
     }

@@ -127,6 +127,13 @@ void Executor::block_alloc(int64_t R, int items, bool train, const std::function
     bcs_.part = static_cast<float*>(alloc(cs.part_floats * 4));
     bcs_.counters = static_cast<int*>(alloc(cs.counters * 4));
     CUDA_OK(cudaMemset(bcs_.counters, 0, cs.counters * 4));  // each kernel leaves them zero
+    fused_norm_ = norm_backward_fused_ok(d_);
+    if (fused_norm_) {
+        const size_t nc = static_cast<size_t>(norm_bwd_chunks(R));
+        bnp_ = static_cast<float*>(alloc(nc * 2 * d * 4));
+        bnc_ = static_cast<float*>(alloc(nc * d * 4));
+        bcarry_ = static_cast<float*>(alloc(nc * d * 4));
+    }
 }
 
 // The update regions of a split master in slot `slot` (block.hpp): each tensor's halves or fp32
@@ -337,7 +344,13 @@ void Executor::block_backward_layer(int L, const WirePtrs& w, const float* x, co
     // --- MLP: y = h + W2^T g(h W1 + b1) + b2
     if (trainable) {
         block_dw(L, lay_.w2, a.g, dy16, rows, st);
-        if (lay_.b2 >= 0) block_colsum(dy16, rows, d, at(lay_.b2), st);
+        if (lay_.b2 >= 0) {
+            if (fused_norm_ && L < n_ - 1) {  // the layer above's norm1 left its output's chunk sums
+                norm_param_reduce(rows, nullptr, bcarry_, at(lay_.b2), st);
+            } else {
+                block_colsum(dy16, rows, d, at(lay_.b2), st);
+            }
+        }
     }
     GemmProblem g;
     g.M = T;
@@ -371,13 +384,21 @@ void Executor::block_backward_layer(int L, const WirePtrs& w, const float* x, co
     g.ldo = d;
     gemm(g, st);
     // norm2: dh_res = dy + norm2'(dxn2)
-    norm_backward(bdxn_, a.xmid, a.st2, w.ln2_g, rms, rows, d, dy, bdmid_, bdmid16_, bcs_,
-                  trainable ? at(lay_.ln2_g) : nullptr, st);
-    kernels_ += trainable ? 2 : 1;
+    if (fused_norm_) {  // + its parameter gradients and bo's (the column sums of dh_res), one pass
+        const bool csum = trainable && lay_.bo >= 0;
+        norm_backward_fused(bdxn_, a.xmid, a.st2, w.ln2_g, rms, rows, d, dy, bdmid_, bdmid16_,
+                            trainable ? bnp_ : nullptr, csum ? bnc_ : nullptr, st);
+        ++kernels_;
+        if (trainable) norm_param_reduce(rows, at(lay_.ln2_g), csum ? bnc_ : nullptr, csum ? at(lay_.bo) : nullptr, st);
+    } else {
+        norm_backward(bdxn_, a.xmid, a.st2, w.ln2_g, rms, rows, d, dy, bdmid_, bdmid16_, bcs_,
+                      trainable ? at(lay_.ln2_g) : nullptr, st);
+        kernels_ += trainable ? 2 : 1;
+    }
     // --- attention: h = x + Wo^T attn(norm1(x) Wqkv + bqkv) + bo
     if (trainable) {
         block_dw(L, lay_.wo, a.o, bdmid16_, rows, st);
-        if (lay_.bo >= 0) block_colsum(bdmid16_, rows, d, at(lay_.bo), st);
+        if (lay_.bo >= 0 && !fused_norm_) block_colsum(bdmid16_, rows, d, at(lay_.bo), st);
     }
     g = GemmProblem{};
     g.M = T;
@@ -409,9 +430,41 @@ void Executor::block_backward_layer(int L, const WirePtrs& w, const float* x, co
     g.ldo = d;
     gemm(g, st);
     // norm1: dx = dh_res + norm1'(dxn1) -> the gradient the layer below reads (layer 0: none)
+    if (fused_norm_) {  // + the chunk sums of dx: the layer below's b2 gradient (carried)
+        const bool carry = need_dx && !frozen_[static_cast<size_t>(L) - 1] && lay_.b2 >= 0;
+        norm_backward_fused(bdxn_, x, a.st1, w.ln1_g, rms, rows, d, bdmid_, need_dx ? bdres_[(L + 1) % 2] : nullptr,
+                            need_dx ? bdres16_[(L + 1) % 2] : nullptr, trainable ? bnp_ : nullptr,
+                            carry ? bcarry_ : nullptr, st);
+        ++kernels_;
+        if (trainable) norm_param_reduce(rows, at(lay_.ln1_g), nullptr, nullptr, st);
+        return;
+    }
     norm_backward(bdxn_, x, a.st1, w.ln1_g, rms, rows, d, bdmid_, need_dx ? bdres_[(L + 1) % 2] : nullptr,
                   need_dx ? bdres16_[(L + 1) % 2] : nullptr, bcs_, trainable ? at(lay_.ln1_g) : nullptr, st);
     kernels_ += (need_dx ? 1 : 0) + (trainable ? 1 : 0);
+}
+
+// The fused norm backward's chunk partials -> the gradient image: the norm parameters (g_out:
+// gamma, then LayerNorm's beta) and / or one column-sum vector (csum_part -> csum_out).
+void Executor::norm_param_reduce(int64_t rows, float* g_out, float* csum_part, float* csum_out, cudaStream_t st) {
+    ColChunks c;
+    c.chunks = norm_bwd_chunks(rows);
+    if (g_out) {
+        c.part[c.n] = bnp_;
+        c.stride[c.n] = 2 * static_cast<int64_t>(d_);
+        c.width[c.n] = lay_.rms() ? d_ : 2 * d_;
+        c.out[c.n] = g_out;
+        ++c.n;
+    }
+    if (csum_part) {
+        c.part[c.n] = csum_part;
+        c.stride[c.n] = d_;
+        c.width[c.n] = d_;
+        c.out[c.n] = csum_out;
+        ++c.n;
+    }
+    reduce_col_chunks(c, st);
+    ++kernels_;
 }
 
 void Executor::block_compute(const Op& op, bool train, int64_t rows, int fmt) {

@@ -631,6 +631,32 @@ extern "C" int sp_debug_colsum(const void* x, int64_t rows, int32_t n, float* pa
     return static_cast<int>(cudaGetLastError());
 }
 
+extern "C" int sp_debug_norm_backward_fused(const float* dy, const float* x, const float* stats, const float* gamma,
+                                            int32_t rms, int64_t rows, int32_t d, const float* dres_in, float* dres_out,
+                                            void* dres_out16, float* ppart, float* cpart, float* out_param,
+                                            float* out_csum, void* stream) {
+    if (!sp::norm_backward_fused_ok(d) || (out_csum && !dres_out)) return SP_ERR_INVALID;
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    sp::norm_backward_fused(dy, x, stats, gamma, rms, rows, d, dres_in, dres_out, dres_out16,
+                            out_param ? ppart : nullptr, out_csum ? cpart : nullptr, st);
+    sp::ColChunks c;
+    c.chunks = sp::norm_bwd_chunks(rows);
+    if (out_param) {
+        c.part[c.n] = ppart;
+        c.stride[c.n] = 2 * static_cast<int64_t>(d);
+        c.width[c.n] = rms ? d : 2 * d;
+        c.out[c.n++] = out_param;
+    }
+    if (out_csum) {
+        c.part[c.n] = cpart;
+        c.stride[c.n] = d;
+        c.width[c.n] = d;
+        c.out[c.n++] = out_csum;
+    }
+    sp::reduce_col_chunks(c, st);
+    return static_cast<int>(cudaGetLastError());
+}
+
 extern "C" void sp_debug_col_scratch(int64_t rows, int32_t widest, int64_t* part_floats, int64_t* counters) {
     const sp::ColScratchSize s = sp::col_scratch_size(rows, widest);
     *part_floats = static_cast<int64_t>(s.part_floats);

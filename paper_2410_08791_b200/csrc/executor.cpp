@@ -235,6 +235,8 @@ void Executor::ensure_stages() {
     n_stages_ = std::max(1, std::min(n_slots_, wb_stages_cap_));
     stage_bytes_ = fp_bytes_;  // [A] or [A][M][V]: the slot minus its bf16 wire region
     CUDA_OK(cudaMalloc(&stages_dev_, static_cast<size_t>(n_stages_) * stage_bytes_));
+    // (a split update writes only the tensors into a stage: alignment gaps stay zero)
+    CUDA_OK(cudaMemset(stages_dev_, 0, static_cast<size_t>(n_stages_) * stage_bytes_));
 }
 
 // Completes the previous train step's deferred write-backs now (host readers, inference,
@@ -548,7 +550,26 @@ void Executor::ensure_buffers(int64_t rows, int n_items, bool train, bool device
     (void)device_io;
 }
 
-Plan Executor::make_plan(bool train, int n_items, int64_t rows, int fmt) {
+namespace {
+bool same_input(const PlanInput& a, const PlanInput& b) {
+    return a.n_layers == b.n_layers && a.strategy == b.strategy && a.k == b.k && a.k_prime == b.k_prime &&
+           a.transfer_mode == b.transfer_mode && a.train == b.train && a.n_items == b.n_items &&
+           a.checkpointing == b.checkpointing && a.sharded == b.sharded && a.eager == b.eager &&
+           a.optimizer_state == b.optimizer_state && a.wb_stages == b.wb_stages &&
+           a.defer_writeback == b.defer_writeback && a.defer_budget == b.defer_budget &&
+           a.pending_wb_layers == b.pending_wb_layers && a.pending_wb_slots == b.pending_wb_slots &&
+           a.frozen == b.frozen && a.layer_bytes == b.layer_bytes && a.act_bytes == b.act_bytes &&
+           a.capacity == b.capacity;
+}
+bool same_slots(const std::vector<SlotCache>& a, const std::vector<SlotCache>& b) {
+    if (a.size() != b.size()) return false;
+    for (size_t i = 0; i < a.size(); ++i)
+        if (a[i].layer != b[i].layer || a[i].valid != b[i].valid) return false;
+    return true;
+}
+}  // namespace
+
+const Plan& Executor::make_plan(bool train, int n_items, int64_t rows, int fmt) {
     PlanInput in;
     in.n_layers = n_;
     in.strategy = cfg_.strategy;
@@ -602,18 +623,25 @@ Plan Executor::make_plan(bool train, int n_items, int64_t rows, int fmt) {
         flush_writebacks();
     }
     const std::vector<SlotCache> none;
-    Plan plan = build_plan(in, fmt == cache_fmt_ ? cache_ : none);
+    const std::vector<SlotCache>& initial = fmt == cache_fmt_ ? cache_ : none;
+    if (memo_.valid && same_input(in, memo_.in) && same_slots(initial, memo_.initial)) return memo_.plan;
+    memo_.valid = false;
+    Plan plan = build_plan(in, initial);
     if (plan.pending_conflict && !in.pending_wb_layers.empty()) {
         // A capacity-shrunk ring would drop a deferred write-back: complete them now, then plan
         // from the (unchanged, still valid) slot cache without pending ones.
         flush_writebacks();
         in.pending_wb_layers.clear();
         in.pending_wb_slots.clear();
-        plan = build_plan(in, fmt == cache_fmt_ ? cache_ : none);
+        plan = build_plan(in, initial);
     }
     if (plan.pending_conflict) throw Error(SP_ERR_INTERNAL, plan.error);
     if (!plan.error.empty()) throw Error(plan.oom ? SP_ERR_OOM : SP_ERR_INVALID, plan.error);
-    return plan;
+    memo_.in = std::move(in);
+    memo_.initial = initial;
+    memo_.plan = std::move(plan);
+    memo_.valid = true;
+    return memo_.plan;
 }
 
 void Executor::record_timing(cudaEvent_t ev, cudaStream_t st) {
@@ -846,7 +874,7 @@ void Executor::loss_op(int64_t rows) {
     // on the D2H copy engine behind the write-backs and stall this stream until they drain)
 }
 
-void Executor::update_op(const Op& op, float lr) {
+bool Executor::update_op(const Op& op, float lr) {
     const int L = op.layer, s = op.slot;
     const size_t dd = static_cast<size_t>(d_) * d_;
     cudaStream_t st = s_upd_;
@@ -859,7 +887,7 @@ void Executor::update_op(const Op& op, float lr) {
                      col_chunks_, d_, d_, adamw_dev_, st);
         kernels_ += 2;
         w16_layer_[s] = -1;
-        return;
+        return false;
     }
     if (tc_ && !comm_ && !blk_) {
         // W: updated in the dW epilogue (fused), or here from the split-K partials in a fixed
@@ -872,12 +900,13 @@ void Executor::update_op(const Op& op, float lr) {
         sgd_reduce(slot_b32(s), ws + db_off, col_chunks_, d_, d_, lr, st);
         kernels_ += 1;
         w16_layer_[s] = -1;
-        return;
+        return false;
     }
     // The full-batch gradient [dW | db] (fp32, the slot's [W | b] layout; a block's gradient
     // image in its parameter layout) in `g`.
     const size_t imgf = img_f();
     float* g = ws;
+    bool staged = false;
     // block layers: the split-K dW partials the layer's backward left; summed inside the split
     // update when nothing else reads the image first, else into the image here
     const bool fuse_parts = blk_ && split_ && !comm_;
@@ -921,6 +950,10 @@ void Executor::update_op(const Op& op, float lr) {
                     }
             bdw_pending_[L % 2].clear();
         }
+        if (op.stage >= 0) {  // also into the write-back stage (same layout): no staging copy
+            r.stage_delta = static_cast<int64_t>(stage_ptr(op.stage) - slot_ptr(s));
+            staged = true;
+        }
         split_update(r, g, adamw() ? slot_m32(s) : nullptr, adamw() ? slot_v32(s) : nullptr, lr, adamw() ? 1 : 0,
                      adamw_dev_, st);
         ++kernels_;
@@ -934,6 +967,7 @@ void Executor::update_op(const Op& op, float lr) {
         ++kernels_;
     }
     w16_layer_[s] = -1;  // the bf16 copy is now stale
+    return staged;
 }
 
 void Executor::enqueue_op(const Plan& plan, int i, bool train, int n_items, int64_t rows,
@@ -1034,7 +1068,7 @@ void Executor::enqueue_op(const Plan& plan, int i, bool train, int n_items, int6
             loss_op(rows);
             break;
         case OpKind::Update:
-            update_op(op, lr);
+            if (update_op(op, lr)) break;  // the update filled the stage itself
             if (op.stage >= 0) {  // copy the updated image [+ m, v] out: the slot is free now
                 size_t lo = 0, hi = layer_bytes();
                 if (sharded_) shard_range(shardA_, layer_bytes(), lo, hi);
@@ -1451,7 +1485,7 @@ void Executor::forward(const float* x, int64_t rows, int n_items, float* y, bool
     // The bf16 wire image is derived from the whole fp32 master; its shards do not line up
     // with the fp32 shards, so it needs every element current on this rank.
     if (bf16_) require_full_host(-1, "run_inference");
-    Plan plan = make_plan(false, n_items, rows, fmt);
+    const Plan& plan = make_plan(false, n_items, rows, fmt);
     refresh_host16();
     ensure_buffers(rows, n_items, false, device_io);
     CUDA_OK(cudaSetDevice(cfg_.device));
@@ -1479,7 +1513,7 @@ float Executor::train_step(const float* x, const float* target, int64_t rows, fl
     const int fmt = bf16_ ? kFmtBf16Train : kFmtExactF32;
     CUDA_OK(cudaSetDevice(cfg_.device));
     ensure_stages();
-    Plan plan = make_plan(true, 1, rows, fmt);
+    const Plan& plan = make_plan(true, 1, rows, fmt);
     ensure_buffers(rows, 1, true, device_io);
     CUDA_OK(cudaSetDevice(cfg_.device));
     if (blk_ && rows % lay_.desc.seq_len != 0)

@@ -124,7 +124,16 @@ private:
     void check_ready();
     void ensure_buffers(int64_t rows, int n_items, bool train, bool device_io);
     void refresh_host16();
-    Plan make_plan(bool train, int n_items, int64_t rows, int fmt);
+    // The call's plan: build_plan is a pure function of (PlanInput, initial slot content), so a
+    // call whose inputs equal the previous call's reuses that plan (steady-state calls skip the
+    // host-side planning). The reference is valid until the next make_plan.
+    const Plan& make_plan(bool train, int n_items, int64_t rows, int fmt);
+    struct PlanMemo {
+        bool valid = false;
+        PlanInput in;
+        std::vector<SlotCache> initial;
+        Plan plan;
+    } memo_;
     void enqueue_call(const Plan& plan, const CallIO& io);
     void run_call(const Plan& plan, const CallIO& io);
     void run_call_impl(const Plan& plan, const CallIO& io);
@@ -133,7 +142,7 @@ private:
                     int fmt);
     void compute_op(const Op& op, bool train, int64_t rows, int fmt);
     void loss_op(int64_t rows);
-    void update_op(const Op& op, float lr);
+    bool update_op(const Op& op, float lr);  // true: it also filled the op's write-back stage
     void collect_stats(const Plan& plan, int n_items, bool train);
     void gemm(const struct GemmProblem& g, cudaStream_t st);
     // transformer blocks (block_exec.cpp)
@@ -181,6 +190,12 @@ private:
     BlockActs bscr_;                    // inference / offload recompute: one scratch set
     float *bdxn_ = nullptr, *bdmid_ = nullptr, *bdelta_ = nullptr;
     ColScratch bcs_;  // column-sum partials + counters (bias / norm parameter gradients)
+    // single-pass norm backward (d <= 2048): chunk partials of the norm parameter gradients, of
+    // norm2's output column sums (bo) and of norm1's (the next layer down's b2, carried across
+    // the layer boundary: that layer's gradient image may still be read by an update)
+    bool fused_norm_ = false;
+    float *bnp_ = nullptr, *bnc_ = nullptr, *bcarry_ = nullptr;
+    void norm_param_reduce(int64_t rows, float* g_out, float* csum_part, float* csum_out, cudaStream_t st);
     // dW split-K partials, per layer parity: each split matrix has its own region (bdw_cap_
     // splits of its size), so the UPDATE op (update stream) reduces them while the compute
     // stream moves on to the layer below. bdw_pending_[p]: what the last backward of a layer of

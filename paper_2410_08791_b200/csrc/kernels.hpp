@@ -158,6 +158,10 @@ struct SplitRegions {
     // at parts[i] (stride count[i]) instead of g[off[i] ...]
     const float* parts[16] = {};
     int nparts[16] = {};
+    // optional: every updated value (halves, vectors, m, v) is also stored at its address +
+    // stage_delta bytes (the write-back stage, which has the slot's layout), so no separate
+    // staging copy re-reads the slot
+    int64_t stage_delta = 0;
 };
 void split_update(const SplitRegions& r, const float* g, float* m, float* v, float lr, int opt,
                   const AdamwScalars* scalars, cudaStream_t st);
@@ -211,5 +215,24 @@ void norm_backward(const float* dy, const float* x, const float* stats, const fl
 // chunking and in-kernel fixed-order reduction.
 void colsum_total_bf16(const void* x, int64_t rows, int n, const ColScratch& scr, float* out, cudaStream_t st);
 int norm_param_chunks(int64_t rows);
+// The single-pass form of norm_backward (d % 4 == 0, d <= 2048; norm_backward_fused_ok): the
+// same dres_out / dres_out16 (skipped when dres_out is null), plus per 64-row chunk c the column
+// partials param_part[c][0][j] = sum dy*xhat, param_part[c][1][j] = sum dy (LayerNorm only) and
+// csum_part[c][j] = sum dres_out (each skipped when null). reduce_col_chunks sums the chunks.
+bool norm_backward_fused_ok(int d);
+int norm_bwd_chunks(int64_t rows);
+void norm_backward_fused(const float* dy, const float* x, const float* stats, const float* gamma, int rms,
+                         int64_t rows, int d, const float* dres_in, float* dres_out, void* dres_out16,
+                         float* param_part, float* csum_part, cudaStream_t st);
+// Up to three chunk-partial segments, out[s][j] = sum_c part[s][c * stride[s] + j] in a fixed
+// order (chunk ranges of ceil(chunks / 8), each in chunk order, then the ranges in order).
+struct ColChunks {
+    int n = 0, chunks = 0;
+    const float* part[3] = {nullptr, nullptr, nullptr};
+    int64_t stride[3] = {0, 0, 0};
+    int width[3] = {0, 0, 0};
+    float* out[3] = {nullptr, nullptr, nullptr};
+};
+void reduce_col_chunks(const ColChunks& r, cudaStream_t st);
 
 }  // namespace sp

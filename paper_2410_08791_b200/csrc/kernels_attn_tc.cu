@@ -372,6 +372,330 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     }
 }
 
+// ---------------------------------------------------------------------------------------
+// forward v2: TWO softmax warps per TMEM lane quarter (warps 4..11; warp 4 + 4 h takes keys
+// [64 h, 64 h + 64) of each 128-key block), P written back over its own S columns in TMEM and
+// fed to the PV MMA as the A operand from TMEM (no shared-memory P tile). A row's max is the
+// two halves' maxima exchanged through shared memory (one 64-thread named barrier per block);
+// the row sums stay per half until the end of the tile. Each half accumulates its HD / 2 output
+// columns in registers, one block behind, as the 4-warp kernel does. 384 threads; TMEM: S / P
+// double-buffered at 128 b, O[b] at 256 + HD b.
+// ---------------------------------------------------------------------------------------
+constexpr int kThreadsF2 = 384;
+
+template <int HD>
+struct Fwd2Cfg {
+    static constexpr int ATOMS = HD / 64;
+    static constexpr int Q_BYTES = kQ * HD * 2;
+    static constexpr int KV_BYTES = kKV * HD * 2;
+    static constexpr int ST = HD <= 64 ? 3 : 2;  // K / V ring
+    static constexpr int XCH_BYTES = (2 * 2 * 128 + 2 * 128) * 4;  // row max (x2 parity) and sum exchange
+    static constexpr int SMEM = 2 * Q_BYTES + 2 * ST * KV_BYTES + XCH_BYTES + 1024 + 512;
+    static constexpr uint32_t T_O = 256;
+};
+
+__device__ __forceinline__ void named_bar_sync(int id, int threads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
+template <int HD>
+__global__ void __launch_bounds__(kThreadsF2, 1)
+    attn_fwd_tc2_kernel(const __grid_constant__ CUtensorMap tmQK, const __grid_constant__ CUtensorMap tmV,
+                        __nv_bfloat16* __restrict__ o, float* __restrict__ lse, TcShape sh, int n_seq) {
+    using C = Fwd2Cfg<HD>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sQ = smem;                        // 2 tiles (the next tile's Q loads early)
+    uint8_t* sK = sQ + 2 * C::Q_BYTES;         // ST tiles
+    uint8_t* sV = sK + C::ST * C::KV_BYTES;    // ST tiles
+    float* xmax = reinterpret_cast<float*>(sV + C::ST * C::KV_BYTES);  // [block parity][half][row]
+    float* xl = xmax + 2 * 2 * 128;                                     // [half][row]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(xl + 2 * 128);
+    uint64_t* q_full = bars;                   // 2
+    uint64_t* q_empty = bars + 2;              // 2
+    uint64_t* kv_full = bars + 4;              // ST
+    uint64_t* kv_empty = kv_full + C::ST;      // ST
+    uint64_t* s_full = kv_empty + C::ST;       // 2: S[b] computed
+    uint64_t* p_full = s_full + 2;             // 2: P[b] written (256 arrivals)
+    uint64_t* pv_done = p_full + 2;            // 2: the PV MMAs have read P[b] (S[b] reusable)
+    uint64_t* o_full = pv_done + 2;            // 2
+    uint64_t* o_empty = o_full + 2;            // 2 (256 arrivals)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int n_qb = (sh.S + kQ - 1) / kQ;
+    const int n_tiles = n_qb * sh.H * n_seq;
+    const int n_kb_total = (sh.S + kKV - 1) / kKV;
+    auto blocks_of = [&](int qb) { return sh.causal ? min(n_kb_total, (qb * kQ + kQ - 1) / kKV + 1) : n_kb_total; };
+
+    if (warp == 0 && lane == 0) {
+        prefetch_tmap(&tmQK);
+        prefetch_tmap(&tmV);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&q_full[i], 1);
+            mbar_init(&q_empty[i], 1);
+            mbar_init(&s_full[i], 1);
+            mbar_init(&p_full[i], 256);
+            mbar_init(&pv_done[i], 1);
+            mbar_init(&o_full[i], 1);
+            mbar_init(&o_empty[i], 256);
+        }
+        for (int i = 0; i < C::ST; ++i) {
+            mbar_init(&kv_full[i], 1);
+            mbar_init(&kv_empty[i], 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ===== TMA producer =====
+            int g = 0, lt = 0;
+            for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++lt) {
+                const TileOf w = tile_of(t, sh, n_qb, n_seq);
+                const int kvh = w.h / (sh.H / sh.Hkv);
+                const int row0 = w.b * sh.S;
+                const int qcol = w.h * HD, kcol = (sh.H + kvh) * HD, vcol = (sh.H + sh.Hkv + kvh) * HD;
+                const int qbuf = lt & 1;
+                mbar_wait(&q_empty[qbuf], ((lt >> 1) & 1) ^ 1);
+                mbar_expect_tx(&q_full[qbuf], C::Q_BYTES);
+                for (int a = 0; a < C::ATOMS; ++a)
+                    tma_load_2d(&tmQK, &q_full[qbuf], sQ + qbuf * C::Q_BYTES + a * kQ * 128, qcol + 64 * a,
+                                row0 + w.qb * kQ);
+                const int n_kb = blocks_of(w.qb);
+                for (int j = 0; j < n_kb; ++j, ++g) {
+                    const int st = g % C::ST;
+                    mbar_wait(&kv_empty[st], ((g / C::ST) & 1) ^ 1);
+                    mbar_expect_tx(&kv_full[st], 2 * C::KV_BYTES);
+                    const int k0 = row0 + j * kKV;
+                    uint8_t* k = sK + st * C::KV_BYTES;
+                    uint8_t* v = sV + st * C::KV_BYTES;
+                    for (int a = 0; a < C::ATOMS; ++a) tma_load_2d(&tmQK, &kv_full[st], k + a * kKV * 128, kcol + 64 * a, k0);
+                    for (int kb = 0; kb < 2; ++kb)
+                        for (int a = 0; a < C::ATOMS; ++a)
+                            tma_load_2d(&tmV, &kv_full[st], v + (kb * C::ATOMS + a) * 8192, vcol + 64 * a, k0 + 64 * kb);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // ===== MMA issuer =====
+            constexpr uint32_t IDESC_S = make_idesc(kQ, kKV, false, false);
+            constexpr uint32_t IDESC_O = make_idesc(kQ, HD, false, true);
+            auto issue_s = [&](int g, uint32_t q_base) {
+                const int st = g % C::ST, sb = g & 1;
+                mbar_wait(&kv_full[st], (g / C::ST) & 1);
+                if (g >= 2) mbar_wait(&pv_done[sb], ((g - 2) >> 1) & 1);
+                fence_after();
+                const uint32_t k_base = smem_u32(sK + st * C::KV_BYTES);
+#pragma unroll
+                for (int kk = 0; kk < HD / 16; ++kk) {
+                    const int a = kk / 4, w = kk % 4;
+                    const uint64_t ad = make_desc(q_base + a * kQ * 128 + w * 32, 16, 1024);
+                    const uint64_t bd = make_desc(k_base + a * kKV * 128 + w * 32, 16, 1024);
+                    umma<false>(tmem + sb * 128, ad, bd, IDESC_S, kk > 0 ? 1u : 0u);
+                }
+                umma_commit(&s_full[sb]);
+            };
+            auto issue_o = [&](int g) {
+                const int st = g % C::ST, sb = g & 1;
+                mbar_wait(&p_full[sb], (g >> 1) & 1);
+                mbar_wait(&o_empty[sb], ((g >> 1) & 1) ^ 1);
+                fence_after();
+                const uint32_t v_base = smem_u32(sV + st * C::KV_BYTES);
+#pragma unroll
+                for (int kk = 0; kk < kKV / 16; ++kk) {
+                    // P of keys 16 kk .. 16 kk + 15: half kk / 4 wrote its 64 keys as 32 packed
+                    // columns at 128 sb + 64 half
+                    const uint32_t pcol = static_cast<uint32_t>(sb * 128 + (kk / 4) * 64 + (kk % 4) * 8);
+                    const uint64_t bd = make_desc(v_base + (kk / 4) * C::ATOMS * 8192 + (kk % 4) * 16 * 128, 8192, 1024);
+                    umma_ts(tmem + C::T_O + sb * HD, tmem + pcol, bd, IDESC_O, kk > 0 ? 1u : 0u);
+                }
+                umma_commit(&o_full[sb]);
+                umma_commit(&pv_done[sb]);
+                umma_commit(&kv_empty[st]);
+            };
+            int g = 0, lt = 0;
+            for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++lt) {
+                const TileOf w = tile_of(t, sh, n_qb, n_seq);
+                const int n_kb = blocks_of(w.qb);
+                const int qbuf = lt & 1;
+                mbar_wait(&q_full[qbuf], (lt >> 1) & 1);
+                fence_after();
+                const uint32_t q_base = smem_u32(sQ + qbuf * C::Q_BYTES);
+                issue_s(g, q_base);
+                for (int j = 0; j < n_kb; ++j) {
+                    if (j + 1 < n_kb) issue_s(g + j + 1, q_base);
+                    if (j + 1 == n_kb) umma_commit(&q_empty[qbuf]);
+                    issue_o(g + j);
+                }
+                g += n_kb;
+            }
+        }
+    } else if (warp >= 4) {
+        // ===== softmax: thread = query row (TMEM lane) x key half =====
+        const int q4 = warp & 3, h = (warp - 4) >> 2;
+        const int r = q4 * 32 + lane;
+        const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
+        constexpr int HH = HD / 2;  // output columns of this half
+        uint32_t v[32], v2[32];
+        float acc[HH];
+        int g = 0;
+        for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+            const TileOf w = tile_of(t, sh, n_qb, n_seq);
+            const int n_kb = blocks_of(w.qb);
+            const int q0 = w.qb * kQ;
+            const int qi = q0 + r;
+#pragma unroll
+            for (int i = 0; i < HH; ++i) acc[i] = 0.0f;
+            float m_run = -INFINITY, l_h = 0.0f, corr_prev = 1.0f;
+            auto accumulate_o = [&](int gg, float corr) {
+                const int ob = gg & 1;
+                mbar_wait(&o_full[ob], (gg >> 1) & 1);
+                fence_after();
+#pragma unroll
+                for (int c = 0; c < HH / 32; ++c) {
+                    tmem_ld32(tmem + lane_off + C::T_O + ob * HD + h * HH + c * 32, v);
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) acc[c * 32 + i] = fmaf(acc[c * 32 + i], corr, __uint_as_float(v[i]));
+                }
+                fence_before();
+                mbar_arrive(&o_empty[ob]);
+            };
+            for (int j = 0; j < n_kb; ++j, ++g) {
+                const int sb = g & 1;
+                const int k0 = j * kKV + 64 * h;  // first key of this half
+                mbar_wait(&s_full[sb], (g >> 1) & 1);
+                fence_after();
+                const uint32_t s_addr = tmem + lane_off + sb * 128 + 64 * h;
+                tmem_ld32_async(s_addr, v);
+                tmem_ld32_async(s_addr + 32, v2);
+                tmem_ld_wait(v);
+                tmem_ld_wait(v2);
+                const bool need_mask = (sh.causal && k0 + 63 > q0) || k0 + 64 > sh.S;
+                const int lim = need_mask ? min(sh.S, sh.causal ? qi + 1 : sh.S) - k0 : 64;  // valid keys
+                float mraw = -INFINITY;
+                if (need_mask) {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        const float x0 = i < lim ? __uint_as_float(v[i]) : -INFINITY;
+                        const float x1 = 32 + i < lim ? __uint_as_float(v2[i]) : -INFINITY;
+                        mraw = fmaxf(mraw, fmaxf(x0, x1));
+                    }
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) mraw = fmaxf(mraw, fmaxf(__uint_as_float(v[i]), __uint_as_float(v2[i])));
+                }
+                float* xm = xmax + (g & 1) * 256;
+                xm[h * 128 + r] = mraw;
+                named_bar_sync(1 + q4, 64);
+                const float mrow = fmaxf(mraw, xm[(1 - h) * 128 + r]);
+                const float mx = fmaxf(m_run, mrow * sh.scale_log2);
+                const float base = mx == -INFINITY ? 0.0f : mx;
+                const float corr = ex2_fast(m_run - base);
+                m_run = mx;
+                uint32_t pk[32];
+                float rs0 = 0.0f, rs1 = 0.0f;
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    float p0 = ex2_fast(fmaf(__uint_as_float(v[2 * i]), sh.scale_log2, -base));
+                    float p1 = ex2_fast(fmaf(__uint_as_float(v[2 * i + 1]), sh.scale_log2, -base));
+                    float p2 = ex2_fast(fmaf(__uint_as_float(v2[2 * i]), sh.scale_log2, -base));
+                    float p3 = ex2_fast(fmaf(__uint_as_float(v2[2 * i + 1]), sh.scale_log2, -base));
+                    if (need_mask) {
+                        if (2 * i >= lim) p0 = 0.0f;
+                        if (2 * i + 1 >= lim) p1 = 0.0f;
+                        if (32 + 2 * i >= lim) p2 = 0.0f;
+                        if (32 + 2 * i + 1 >= lim) p3 = 0.0f;
+                    }
+                    rs0 += p0 + p1;
+                    rs1 += p2 + p3;
+                    pk[i] = pack_bf16(p0, p1);
+                    pk[16 + i] = pack_bf16(p2, p3);
+                }
+                // P over the first 32 of this half's S columns (already read into registers)
+                tmem_st16(s_addr, *reinterpret_cast<const uint32_t(*)[16]>(pk));
+                tmem_st16(s_addr + 16, *reinterpret_cast<const uint32_t(*)[16]>(pk + 16));
+                tmem_st_wait();
+                fence_before();
+                mbar_arrive(&p_full[sb]);
+                l_h = l_h * corr + (rs0 + rs1);
+                if (j > 0) accumulate_o(g - 1, corr_prev);
+                corr_prev = corr;
+            }
+            if (n_kb > 0) accumulate_o(g - 1, corr_prev);
+            xl[h * 128 + r] = l_h;
+            named_bar_sync(1 + q4, 64);
+            const float l_run = xl[r] + xl[128 + r];
+            if (qi < sh.S) {
+                const float inv = l_run > 0.0f ? 1.0f / l_run : 0.0f;
+                __nv_bfloat16* orow = o + static_cast<int64_t>(w.b * sh.S + qi) * sh.ldo + w.h * HD + h * HH;
+#pragma unroll
+                for (int c = 0; c < HH / 8; ++c) {
+                    uint4 u4;
+                    u4.x = pack_bf16(acc[8 * c + 0] * inv, acc[8 * c + 1] * inv);
+                    u4.y = pack_bf16(acc[8 * c + 2] * inv, acc[8 * c + 3] * inv);
+                    u4.z = pack_bf16(acc[8 * c + 4] * inv, acc[8 * c + 5] * inv);
+                    u4.w = pack_bf16(acc[8 * c + 6] * inv, acc[8 * c + 7] * inv);
+                    reinterpret_cast<uint4*>(orow)[c] = u4;
+                }
+                if (h == 0)
+                    lse[(static_cast<int64_t>(w.b) * sh.H + w.h) * sh.S + qi] =
+                        l_run > 0.0f ? m_run + log2f(l_run) : INFINITY;
+            }
+        }
+    }
+    __syncwarp();
+    fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+    }
+}
+
+template <int HD>
+cudaError_t launch_fwd_tc2(const AttnProblem& a, cudaStream_t st) {
+    using C = Fwd2Cfg<HD>;
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(attn_fwd_tc2_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    const int ld = (a.n_heads + 2 * a.n_kv_heads) * a.head_dim;
+    CUtensorMap tqk, tv;
+    if (!make_map(&tqk, a.qkv, static_cast<uint64_t>(ld), static_cast<uint64_t>(a.tokens), static_cast<uint64_t>(ld), 64,
+                  128, false, false) ||
+        !make_map(&tv, a.qkv, static_cast<uint64_t>(ld), static_cast<uint64_t>(a.tokens), static_cast<uint64_t>(ld), 64, 64,
+                  false, false))
+        return cudaErrorInvalidValue;
+    TcShape sh;
+    sh.S = a.seq_len;
+    sh.H = a.n_heads;
+    sh.Hkv = a.n_kv_heads;
+    sh.ld = ld;
+    sh.ldo = a.n_heads * a.head_dim;
+    sh.causal = a.causal;
+    sh.scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(a.head_dim));
+    const int n_seq = static_cast<int>(a.tokens / a.seq_len);
+    const int tiles = ((a.seq_len + kQ - 1) / kQ) * a.n_heads * n_seq;
+    const int grid = tiles < num_sms() ? tiles : num_sms();
+    attn_fwd_tc2_kernel<HD><<<grid, kThreadsF2, C::SMEM, st>>>(tqk, tv, static_cast<__nv_bfloat16*>(a.o), a.lse, sh,
+                                                                n_seq);
+    return cudaGetLastError();
+}
+
 template <int HD>
 cudaError_t launch_fwd_tc(const AttnProblem& a, cudaStream_t st) {
     using C = AttnCfg<HD>;
@@ -938,9 +1262,9 @@ cudaError_t launch_bwd_tc(const AttnProblem& a, cudaStream_t st) {
 
 // The tensor-core forward for head_dim 64 / 128 (the GPT-2 XL and Llama-3 shapes);
 // cudaErrorNotSupported for other head dims (the caller falls back to the mma.sync kernel).
-cudaError_t attention_forward_tc(const AttnProblem& a, cudaStream_t st) {
-    if (a.head_dim == 64) return launch_fwd_tc<64>(a, st);
-    if (a.head_dim == 128) return launch_fwd_tc<128>(a, st);
+cudaError_t attention_forward_tc(const AttnProblem& a, cudaStream_t st, bool v2) {
+    if (a.head_dim == 64) return v2 ? launch_fwd_tc2<64>(a, st) : launch_fwd_tc<64>(a, st);
+    if (a.head_dim == 128) return v2 ? launch_fwd_tc2<128>(a, st) : launch_fwd_tc<128>(a, st);
     return cudaErrorNotSupported;
 }
 

@@ -249,9 +249,200 @@ __global__ void __launch_bounds__(32 * kRowLanes) colsum_total_kernel(const __nv
     if (j < n) out[j] = chunk_sum(part, gridDim.y, n, j);
 }
 
+// Fused norm backward (d <= 2048): one pass over dy, x and dres_in produces dres_out (fp32 and
+// bf16) AND the per-chunk column partials of the norm's parameter gradients (sum dy*xhat, sum
+// dy) and of dres_out itself (the bias gradient of the linear that produced the norm's input),
+// so neither dy / x nor dres_out is read a second time. Block = 8 warps over kNbRows rows: two
+// row groups x four column quarters; warp (rg, q) owns the 32-float4 stripes q, q+4, q+8, ... of
+// every row of its group, so a row's reductions are four warp sums combined through shared
+// memory in quarter order (one named barrier per row, double-buffered by row parity), and each
+// lane keeps its stripes' column partials in registers across the rows. The two row groups are
+// added (rg 0 + rg 1) into the chunk's partial row; reduce_col_chunks sums the chunks in order.
+constexpr int kNbRows = 64;
+constexpr int kNbMaxS = 4;  // stripes per warp: d <= 4 * 4 * 32 * 4 = 2048
+
+__device__ __forceinline__ void named_bar(int id, int threads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+__device__ __forceinline__ void f4_add(float4& a, const float4& b) { a.x += b.x, a.y += b.y, a.z += b.z, a.w += b.w; }
+
+template <bool RMS>
+__global__ void __launch_bounds__(256, 2) norm_bwd_fused_kernel(
+    const float* __restrict__ dy, const float* __restrict__ x, const float* __restrict__ stats,
+    const float* __restrict__ gamma, int64_t rows, int d, const float* __restrict__ dres_in,
+    float* __restrict__ dres_out, __nv_bfloat16* __restrict__ dres_out16, float* __restrict__ ppart,
+    float* __restrict__ cpart) {
+    __shared__ float2 red[2][2][4];                 // [row parity][row group][quarter]
+    __shared__ float4 xch[4][kNbMaxS][3][32];       // row group 1's column partials
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, rg = w >> 2, q = w & 3;
+    const int n4 = d >> 2;
+    const int64_t r0 = static_cast<int64_t>(blockIdx.x) * kNbRows;
+    const int64_t r1 = min(rows, r0 + kNbRows);
+    const bool dx = dres_out != nullptr;
+    const float inv_d = 1.0f / static_cast<float>(d);
+    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4* g4 = reinterpret_cast<const float4*>(gamma);  // (re-read per row: L1 hits)
+    float4 A[kNbMaxS], B[kNbMaxS], Cs[kNbMaxS];
+    int jj[kNbMaxS];
+#pragma unroll
+    for (int i = 0; i < kNbMaxS; ++i) {
+        jj[i] = (q + 4 * i) * 32 + lane;
+        A[i] = z4, B[i] = z4, Cs[i] = z4;
+    }
+    int par = 0;
+    for (int64_t r = r0 + rg; r < r1; r += 2) {
+        const float mean = RMS ? 0.0f : stats[2 * r], rstd = stats[2 * r + 1];
+        const float4* dr = reinterpret_cast<const float4*>(dy + r * d);
+        const float4* xr = reinterpret_cast<const float4*>(x + r * d);
+        float4 e[kNbMaxS], v[kNbMaxS];
+#pragma unroll
+        for (int i = 0; i < kNbMaxS; ++i) {
+            e[i] = jj[i] < n4 ? __ldg(dr + jj[i]) : z4;
+            v[i] = jj[i] < n4 ? __ldg(xr + jj[i]) : z4;
+        }
+        if (dx) {
+            float sg = 0.0f, sgx = 0.0f;
+#pragma unroll
+            for (int i = 0; i < kNbMaxS; ++i) {  // (padding lanes hold zeros)
+                const float4 gi = jj[i] < n4 ? __ldg(g4 + jj[i]) : z4;
+                const float g0 = e[i].x * gi.x, g1 = e[i].y * gi.y, g2 = e[i].z * gi.z, g3 = e[i].w * gi.w;
+                sg += (g0 + g1) + (g2 + g3);
+                sgx += (g0 * (v[i].x - mean) + g1 * (v[i].y - mean)) + (g2 * (v[i].z - mean) + g3 * (v[i].w - mean));
+            }
+            sg = warp_allsum(sg);
+            sgx = warp_allsum(sgx);
+            if (lane == 0) red[par][rg][q] = make_float2(sg, sgx);
+            named_bar(1 + rg, 128);
+            float tg = red[par][rg][0].x, tx = red[par][rg][0].y;
+#pragma unroll
+            for (int k = 1; k < 4; ++k) tg += red[par][rg][k].x, tx += red[par][rg][k].y;
+            par ^= 1;
+            const float c_mean = RMS ? 0.0f : tg * inv_d;
+            const float c_x = tx * rstd * inv_d;
+            float4 base[kNbMaxS];  // (loaded after the barrier: fewer registers live across it)
+            const float4* ri = reinterpret_cast<const float4*>(dres_in + r * d);
+#pragma unroll
+            for (int i = 0; i < kNbMaxS; ++i) base[i] = jj[i] < n4 ? __ldg(ri + jj[i]) : z4;
+            float4* ro = reinterpret_cast<float4*>(dres_out + r * d);
+            uint2* r16 = dres_out16 ? reinterpret_cast<uint2*>(dres_out16 + r * d) : nullptr;
+#pragma unroll
+            for (int i = 0; i < kNbMaxS; ++i) {
+                if (jj[i] >= n4) continue;
+                const float4 gi = __ldg(g4 + jj[i]);
+                float4 o;
+                o.x = base[i].x + rstd * (e[i].x * gi.x - c_mean - (v[i].x - mean) * rstd * c_x);
+                o.y = base[i].y + rstd * (e[i].y * gi.y - c_mean - (v[i].y - mean) * rstd * c_x);
+                o.z = base[i].z + rstd * (e[i].z * gi.z - c_mean - (v[i].z - mean) * rstd * c_x);
+                o.w = base[i].w + rstd * (e[i].w * gi.w - c_mean - (v[i].w - mean) * rstd * c_x);
+                ro[jj[i]] = o;
+                if (r16) {
+                    __nv_bfloat162 lo = __floats2bfloat162_rn(o.x, o.y), hi = __floats2bfloat162_rn(o.z, o.w);
+                    uint2 pk;
+                    pk.x = *reinterpret_cast<uint32_t*>(&lo);
+                    pk.y = *reinterpret_cast<uint32_t*>(&hi);
+                    r16[jj[i]] = pk;
+                }
+                f4_add(Cs[i], o);
+            }
+        }
+        if (ppart) {
+#pragma unroll
+            for (int i = 0; i < kNbMaxS; ++i) {
+                A[i].x += e[i].x * ((v[i].x - mean) * rstd);
+                A[i].y += e[i].y * ((v[i].y - mean) * rstd);
+                A[i].z += e[i].z * ((v[i].z - mean) * rstd);
+                A[i].w += e[i].w * ((v[i].w - mean) * rstd);
+                f4_add(B[i], e[i]);
+            }
+        }
+    }
+    if (rg == 1) {
+#pragma unroll
+        for (int i = 0; i < kNbMaxS; ++i) {
+            xch[q][i][0][lane] = A[i];
+            xch[q][i][1][lane] = B[i];
+            xch[q][i][2][lane] = Cs[i];
+        }
+    }
+    __syncthreads();
+    if (rg != 0) return;
+#pragma unroll
+    for (int i = 0; i < kNbMaxS; ++i) {
+        if (jj[i] >= n4) continue;
+        if (ppart) {
+            f4_add(A[i], xch[q][i][0][lane]);
+            reinterpret_cast<float4*>(ppart + static_cast<int64_t>(blockIdx.x) * 2 * d)[jj[i]] = A[i];
+            if (!RMS) {
+                f4_add(B[i], xch[q][i][1][lane]);
+                reinterpret_cast<float4*>(ppart + (static_cast<int64_t>(blockIdx.x) * 2 + 1) * d)[jj[i]] = B[i];
+            }
+        }
+        if (cpart) {
+            f4_add(Cs[i], xch[q][i][2][lane]);
+            reinterpret_cast<float4*>(cpart + static_cast<int64_t>(blockIdx.x) * d)[jj[i]] = Cs[i];
+        }
+    }
+}
+
+// out_s[j] = sum over chunks c (in order) of part_s[c * stride_s + j] for up to three segments.
+// Block = 32 columns x 8 chunk ranges; each range is summed in chunk order, then the ranges in
+// range order (a fixed decomposition of the shape).
+__global__ void __launch_bounds__(256) reduce_col_chunks_kernel(ColChunks r) {
+    __shared__ float sub[8][33];
+    const int col = blockIdx.x * 32 + threadIdx.x;
+    int s = 0, j = col;
+    while (s < r.n && j >= r.width[s]) j -= r.width[s++];
+    float acc = 0.0f;
+    if (s < r.n) {
+        const int per = (r.chunks + 7) / 8;
+        const int c0 = threadIdx.y * per, c1 = min(r.chunks, c0 + per);
+        const float* p = r.part[s] + j;
+        const int64_t stride = r.stride[s];
+        int c = c0;
+        for (; c + 8 <= c1; c += 8) {
+            float v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = __ldcg(p + static_cast<int64_t>(c + u) * stride);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc += v[u];
+        }
+        for (; c < c1; ++c) acc += __ldcg(p + static_cast<int64_t>(c) * stride);
+    }
+    sub[threadIdx.y][threadIdx.x] = acc;
+    __syncthreads();
+    if (threadIdx.y != 0 || s >= r.n) return;
+    float t = sub[0][threadIdx.x];
+#pragma unroll
+    for (int k = 1; k < 8; ++k) t += sub[k][threadIdx.x];
+    r.out[s][j] = t;
+}
+
 }  // namespace
 
 int norm_param_chunks(int64_t rows) { return static_cast<int>((rows + kChunkRows - 1) / kChunkRows); }
+
+bool norm_backward_fused_ok(int d) { return d % 4 == 0 && d <= 4 * kNbMaxS * 32 * 4; }
+int norm_bwd_chunks(int64_t rows) { return static_cast<int>((rows + kNbRows - 1) / kNbRows); }
+
+void norm_backward_fused(const float* dy, const float* x, const float* stats, const float* gamma, int rms,
+                         int64_t rows, int d, const float* dres_in, float* dres_out, void* dres_out16,
+                         float* param_part, float* csum_part, cudaStream_t st) {
+    const dim3 grid(static_cast<unsigned>(norm_bwd_chunks(rows)));
+    auto* o16 = static_cast<__nv_bfloat16*>(dres_out16);
+    if (rms)
+        launch_kernel(norm_bwd_fused_kernel<true>, grid, dim3(256), 0, st, dy, x, stats, gamma, rows, d, dres_in,
+                      dres_out, o16, param_part, csum_part);
+    else
+        launch_kernel(norm_bwd_fused_kernel<false>, grid, dim3(256), 0, st, dy, x, stats, gamma, rows, d, dres_in,
+                      dres_out, o16, param_part, csum_part);
+}
+
+void reduce_col_chunks(const ColChunks& r, cudaStream_t st) {
+    int total = 0;
+    for (int s = 0; s < r.n; ++s) total += r.width[s];
+    if (total == 0) return;
+    launch_kernel(reduce_col_chunks_kernel, dim3(static_cast<unsigned>((total + 31) / 32)), dim3(32, 8), 0, st, r);
+}
 
 void norm_forward(const float* x, const float* gamma, const float* beta, int rms, float eps, int64_t rows, int d,
                   void* y, float* stats, cudaStream_t st) {

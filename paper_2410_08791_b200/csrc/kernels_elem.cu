@@ -478,6 +478,11 @@ __device__ __forceinline__ void store8(float* p, const float (&v)[8]) {
     reinterpret_cast<float4*>(p)[1] = make_float4(v[4], v[5], v[6], v[7]);
 }
 
+template <typename T>
+__device__ __forceinline__ T* shifted(T* p, int64_t bytes) {
+    return reinterpret_cast<T*>(reinterpret_cast<char*>(p) + bytes);
+}
+
 __global__ void split_update_kernel(SplitRegions r, const float* __restrict__ g, float* __restrict__ m,
                                     float* __restrict__ v, float lr, int opt, const AdamwScalars* __restrict__ sc) {
     const int i = blockIdx.y;
@@ -523,6 +528,10 @@ __global__ void split_update_kernel(SplitRegions r, const float* __restrict__ g,
             for (int k = 0; k < 8; ++k) adamw_elem(w[k], mm[k], vv[k], gr[k], s);
             store8(m + base + e, mm);
             store8(v + base + e, vv);
+            if (r.stage_delta) {
+                store8(shifted(m + base + e, r.stage_delta), mm);
+                store8(shifted(v + base + e, r.stage_delta), vv);
+            }
         } else {
 #pragma unroll
             for (int k = 0; k < 8; ++k) w[k] = __fsub_rn(w[k], __fmul_rn(lr, gr[k]));
@@ -535,10 +544,16 @@ __global__ void split_update_kernel(SplitRegions r, const float* __restrict__ g,
                 h4[k] = (b0 >> 16) | (b1 & 0xFFFF0000u);
                 l4[k] = (b0 & 0xFFFFu) | (b1 << 16);
             }
-            *reinterpret_cast<uint4*>(static_cast<uint16_t*>(r.hi[i]) + e) = make_uint4(h4[0], h4[1], h4[2], h4[3]);
-            *reinterpret_cast<uint4*>(r.lo[i] + e) = make_uint4(l4[0], l4[1], l4[2], l4[3]);
+            const uint4 hv = make_uint4(h4[0], h4[1], h4[2], h4[3]), lv = make_uint4(l4[0], l4[1], l4[2], l4[3]);
+            *reinterpret_cast<uint4*>(static_cast<uint16_t*>(r.hi[i]) + e) = hv;
+            *reinterpret_cast<uint4*>(r.lo[i] + e) = lv;
+            if (r.stage_delta) {
+                *shifted(reinterpret_cast<uint4*>(static_cast<uint16_t*>(r.hi[i]) + e), r.stage_delta) = hv;
+                *shifted(reinterpret_cast<uint4*>(r.lo[i] + e), r.stage_delta) = lv;
+            }
         } else {
             store8(static_cast<float*>(r.hi[i]) + e, w);
+            if (r.stage_delta) store8(shifted(static_cast<float*>(r.hi[i]) + e, r.stage_delta), w);
         }
     }
 }

@@ -171,10 +171,11 @@ def _split(qkv, B, S, H, Hkv, hd):
     return t[:, :H], t[:, H:H + Hkv], t[:, H + Hkv:]
 
 
-@pytest.mark.parametrize("fwd_kind,bwd_kind", [(2, 0), (2, 2), (1, 1)], ids=["tcgen05", "tcgen05-bwd-v1", "mma-sync"])
+@pytest.mark.parametrize("fwd_kind,bwd_kind", [(2, 0), (3, 2), (1, 1)], ids=["tcgen05", "tcgen05-v1", "mma-sync"])
 @pytest.mark.parametrize("B,S,H,Hkv,hd,causal", ATTN)
 def test_attention_forward_and_backward(B, S, H, Hkv, hd, causal, fwd_kind, bwd_kind):
-    # forward kind 2 / 0: the tcgen05 kernel (head dims 64 / 128), 1: mma.sync. Backward kind 0:
+    # forward kind 2 / 0: the v2 tcgen05 kernel (head dims 64 / 128), 3: the v1 tcgen05 kernel,
+    # 1: mma.sync. Backward kind 0:
     # the v2 tcgen05 passes (dQ + delta, then dK/dV; whole 128-row sequence blocks), 2: the v1
     # tcgen05 passes, 1: mma.sync; shapes a tcgen05 kind does not cover take the mma.sync kernels
     assert LIB.sp_debug_set(None, b"attn_fwd", fwd_kind) == 0
@@ -273,6 +274,63 @@ def test_norm_forward_backward(T, d, rms):
     assert rel(out[0], gv.grad) < 1e-4
     if not rms:
         assert rel(out[1], bv.grad) < 1e-4
+
+
+@pytest.mark.parametrize("rms", [0, 1])
+@pytest.mark.parametrize("T,d", [(16384, 1600), (1000, 1280), (64, 2048), (65, 64), (3, 1600)])
+def test_norm_backward_fused(T, d, rms):
+    """The single-pass norm backward (the executor's path for d <= 2048): dres_out and its bf16
+    copy equal the two-pass kernel's elementwise (same per-row arithmetic), the parameter
+    gradients and the column sums of dres_out (the bias gradient below) match fp64, and a
+    repeated launch is bitwise identical (fixed reduction order)."""
+    x = torch.randn(T, d, device="cuda") * 2 + 0.5
+    g = 1 + 0.1 * torch.randn(d, device="cuda")
+    b = 0.1 * torch.randn(d, device="cuda")
+    y = torch.empty(T, d, device="cuda", dtype=torch.bfloat16)
+    stats = torch.empty(T, 2, device="cuda")
+    st = _stream()
+    assert LIB.sp_debug_norm_forward(x.data_ptr(), g.data_ptr(), b.data_ptr(), rms, 1e-5, T, d, y.data_ptr(),
+                                     stats.data_ptr(), st) == 0
+    dy = torch.randn(T, d, device="cuda")
+    dres_in = torch.randn(T, d, device="cuda")
+    # the two-pass kernels as the elementwise reference
+    ref_out = torch.empty(T, d, device="cuda")
+    ref16 = torch.empty(T, d, device="cuda", dtype=torch.bfloat16)
+    part, cnt = _col_scratch(T, d)
+    ref_param = torch.zeros(2, d, device="cuda")
+    assert LIB.sp_debug_norm_backward(dy.data_ptr(), x.data_ptr(), stats.data_ptr(), g.data_ptr(), rms, T, d,
+                                      dres_in.data_ptr(), ref_out.data_ptr(), ref16.data_ptr(), part.data_ptr(),
+                                      cnt.data_ptr(), ref_param.data_ptr(), st) == 0
+    chunks = (T + 63) // 64
+    ppart = torch.empty(chunks, 2, d, device="cuda")
+    cpart = torch.empty(chunks, d, device="cuda")
+    runs = []
+    for _ in range(2):
+        out = torch.empty(T, d, device="cuda")
+        o16 = torch.empty(T, d, device="cuda", dtype=torch.bfloat16)
+        op = torch.zeros(2, d, device="cuda")
+        oc = torch.empty(d, device="cuda")
+        assert LIB.sp_debug_norm_backward_fused(dy.data_ptr(), x.data_ptr(), stats.data_ptr(), g.data_ptr(), rms, T,
+                                                d, dres_in.data_ptr(), out.data_ptr(), o16.data_ptr(), ppart.data_ptr(),
+                                                cpart.data_ptr(), op.data_ptr(), oc.data_ptr(), st) == 0
+        torch.cuda.synchronize()
+        runs.append((out, o16, op, oc))
+    out, o16, op, oc = runs[0]
+    for a, bb in zip(runs[0], runs[1]):
+        assert torch.equal(a, bb)
+    assert rel(out, ref_out) < 1e-6 and rel(o16, ref16) < 1e-2
+    xh = ((x.double() - (0 if rms else stats[:, :1].double())) * stats[:, 1:].double())
+    assert rel(op[0], (dy.double() * xh).sum(0)) < 1e-5
+    if not rms:
+        assert rel(op[1], dy.double().sum(0)) < 1e-5
+    assert rel(oc, out.double().sum(0)) < 1e-5
+    # parameter gradients only (the layer-0 norm1: no dx)
+    op2 = torch.zeros(2, d, device="cuda")
+    assert LIB.sp_debug_norm_backward_fused(dy.data_ptr(), x.data_ptr(), stats.data_ptr(), g.data_ptr(), rms, T, d,
+                                            dres_in.data_ptr(), None, None, ppart.data_ptr(), cpart.data_ptr(),
+                                            op2.data_ptr(), None, st) == 0
+    torch.cuda.synchronize()
+    assert torch.equal(op2, op)
 
 
 def _col_scratch(rows, widest):

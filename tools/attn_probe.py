@@ -12,7 +12,7 @@ import torch  # noqa: E402
 from paper_2410_08791_b200 import _capi  # noqa: E402
 
 LIB = _capi.LIB
-# SP_ATTN_FWD=0|1|2: the forward kernel choice (sp_debug_set "attn_fwd"; 2 = tcgen05 at head_dim 64 too)
+# SP_ATTN_FWD=0|1|3: the forward kernel choice (sp_debug_set "attn_fwd"; 0 = v2 tcgen05, 3 = v1, 1 = mma.sync)
 LIB.sp_debug_set(None, b"attn_fwd", int(os.environ.get("SP_ATTN_FWD", "0")))
 LIB.sp_debug_set(None, b"attn_bwd", int(os.environ.get("SP_ATTN_BWD", "0")))
 
