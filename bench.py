@@ -533,11 +533,13 @@ def run_block(a, rank, world, local, torch, dist, sp, pk, pk_src, strategy):
     gemm_ms, gemm_fl = traced["gemm_ms"], traced["gemm_flops"]
     achieved = gemm_fl / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else 0.0
     peak_tf = pk["bf16_tflops_sustained"]
-    traffic = None
+    traffic, traffic_src = None, None
     tr_path = os.path.join(ROOT, "profiles", "block_gemm_traffic.json")
-    if os.path.exists(tr_path):
+    if os.path.exists(tr_path):  # per-launch DRAM bytes of the step's GEMMs, one ncu --set full capture
         try:
-            traffic = json.load(open(tr_path))
+            tr = json.load(open(tr_path))
+            traffic = tr["bytes_per_launch"]
+            traffic_src = {k: tr[k] for k in ("algorithmic_bytes_per_launch", "launches_captured", "source")}
         except Exception:
             traffic = None
     value = world * rows * a.steps / (ms * 1e-3)
@@ -569,7 +571,7 @@ def run_block(a, rank, world, local, torch, dist, sp, pk, pk_src, strategy):
                            "loss": losses[-1]},
             "roofline": {"bound": "tensor", "kernel": "tcgen05 bf16 GEMMs of the step (4 forward, 8 backward per layer)",
                          "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
-                         "frac": achieved / peak_tf, "traffic": traffic,
+                         "frac": achieved / peak_tf, "traffic": traffic, "traffic_source": traffic_src,
                          "peak_source": f"{pk_src} bf16_tflops_sustained",
                          "gemm_flops_per_step": gemm_fl, "gemm_ms_per_step": gemm_ms,
                          "gemm_launches_per_step": traced["gemm_launches"],
@@ -905,11 +907,12 @@ def main():
     achieved = gemm_fl / gemm_s / 1e12
     gemm_n = sum(g["per_step"] for g in gemm.values())
     peak_tf = pk["bf16_tflops_sustained"]
-    traffic = None
+    traffic, traffic_src = None, None
     tr_path = os.path.join(ROOT, "profiles", "gemm_traffic.json")
     if os.path.exists(tr_path):
         try:
-            traffic = json.load(open(tr_path)).get("bytes_per_launch")
+            tr = json.load(open(tr_path))
+            traffic, traffic_src = tr.get("bytes_per_launch"), tr.get("source")
         except Exception:
             traffic = None
     step_s = ms * 1e-3 / a.steps
@@ -941,7 +944,7 @@ def main():
                            "loss": losses[-1]},
             "roofline": {"bound": "tensor", "kernel": "tcgen05 bf16 GEMM (fwd / dX / dW)",
                          "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
-                         "frac": achieved / peak_tf, "traffic": traffic,
+                         "frac": achieved / peak_tf, "traffic": traffic, "traffic_source": traffic_src,
                          "peak_source": f"{pk_src} bf16_tflops_sustained",
                          "per_shape": gemm, "launches_per_step": gemm_n,
                          "gemm_share_of_step": gemm_s / step_s,
