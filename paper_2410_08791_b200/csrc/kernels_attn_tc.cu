@@ -584,18 +584,24 @@ __global__ void __launch_bounds__(kThreadsF2, 1)
                 tmem_ld_wait(v2);
                 const bool need_mask = (sh.causal && k0 + 63 > q0) || k0 + 64 > sh.S;
                 const int lim = need_mask ? min(sh.S, sh.causal ? qi + 1 : sh.S) - k0 : 64;  // valid keys
-                float mraw = -INFINITY;
+                // row max of the half: eight independent chains, then a tree (short dependency chains)
+                float mx8[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) mx8[u] = -INFINITY;
                 if (need_mask) {
 #pragma unroll
                     for (int i = 0; i < 32; ++i) {
                         const float x0 = i < lim ? __uint_as_float(v[i]) : -INFINITY;
                         const float x1 = 32 + i < lim ? __uint_as_float(v2[i]) : -INFINITY;
-                        mraw = fmaxf(mraw, fmaxf(x0, x1));
+                        mx8[i & 7] = fmaxf(mx8[i & 7], fmaxf(x0, x1));
                     }
                 } else {
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) mraw = fmaxf(mraw, fmaxf(__uint_as_float(v[i]), __uint_as_float(v2[i])));
+                    for (int i = 0; i < 32; ++i)
+                        mx8[i & 7] = fmaxf(mx8[i & 7], fmaxf(__uint_as_float(v[i]), __uint_as_float(v2[i])));
                 }
+                const float mraw = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                                         fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
                 float* xm = xmax + (g & 1) * 256;
                 xm[h * 128 + r] = mraw;
                 named_bar_sync(1 + q4, 64);
@@ -605,7 +611,7 @@ __global__ void __launch_bounds__(kThreadsF2, 1)
                 const float corr = ex2_fast(m_run - base);
                 m_run = mx;
                 uint32_t pk[32];
-                float rs0 = 0.0f, rs1 = 0.0f;
+                float rs[4] = {0.0f, 0.0f, 0.0f, 0.0f};  // four row-sum chains
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
                     float p0 = ex2_fast(fmaf(__uint_as_float(v[2 * i]), sh.scale_log2, -base));
@@ -618,11 +624,12 @@ __global__ void __launch_bounds__(kThreadsF2, 1)
                         if (32 + 2 * i >= lim) p2 = 0.0f;
                         if (32 + 2 * i + 1 >= lim) p3 = 0.0f;
                     }
-                    rs0 += p0 + p1;
-                    rs1 += p2 + p3;
+                    rs[i & 1] += p0 + p1;
+                    rs[2 + (i & 1)] += p2 + p3;
                     pk[i] = pack_bf16(p0, p1);
                     pk[16 + i] = pack_bf16(p2, p3);
                 }
+                const float rs0 = rs[0] + rs[1], rs1 = rs[2] + rs[3];
                 // P over the first 32 of this half's S columns (already read into registers)
                 tmem_st16(s_addr, *reinterpret_cast<const uint32_t(*)[16]>(pk));
                 tmem_st16(s_addr + 16, *reinterpret_cast<const uint32_t(*)[16]>(pk + 16));

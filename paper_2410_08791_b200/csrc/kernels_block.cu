@@ -22,13 +22,78 @@ __device__ __forceinline__ float warp_allsum(float v) {
     return v;
 }
 
-template <bool RMS>
+// One warp per row; the row is held in registers (NJ float4 per lane), so x is read from
+// memory once and all NJ loads of a lane are in flight together. Sums run in the same per-lane
+// order as a strided loop would (j ascending), then across lanes.
+template <bool RMS, int NJ>
 __global__ void __launch_bounds__(32 * kRowsPerBlock) norm_fwd_kernel(const float* __restrict__ x,
                                                                       const float* __restrict__ gamma,
                                                                       const float* __restrict__ beta, float eps,
                                                                       int64_t rows, int d,
                                                                       __nv_bfloat16* __restrict__ y,
                                                                       float* __restrict__ stats) {
+    const int lane = threadIdx.x & 31;
+    const int64_t r = static_cast<int64_t>(blockIdx.x) * kRowsPerBlock + (threadIdx.x >> 5);
+    if (r >= rows) return;
+    const float4* xr = reinterpret_cast<const float4*>(x + r * d);
+    const int n4 = d / 4;
+    float4 v[NJ];
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) v[j] = lane + 32 * j < n4 ? __ldg(xr + lane + 32 * j) : make_float4(0.f, 0.f, 0.f, 0.f);
+    float mean = 0.0f;
+    if (!RMS) {
+        float s = 0.0f;
+#pragma unroll
+        for (int j = 0; j < NJ; ++j)
+            if (lane + 32 * j < n4) s += (v[j].x + v[j].y) + (v[j].z + v[j].w);
+        mean = warp_allsum(s) / static_cast<float>(d);
+    }
+    float q = 0.0f;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+        if (lane + 32 * j >= n4) continue;
+        const float a = v[j].x - mean, b = v[j].y - mean, c = v[j].z - mean, e = v[j].w - mean;
+        q += (a * a + b * b) + (c * c + e * e);
+    }
+    const float rstd = rsqrtf(warp_allsum(q) / static_cast<float>(d) + eps);
+    const float4* g4 = reinterpret_cast<const float4*>(gamma);
+    const float4* b4 = reinterpret_cast<const float4*>(beta);
+    uint2* yr = reinterpret_cast<uint2*>(y + r * d);
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+        const int i = lane + 32 * j;
+        if (i >= n4) continue;
+        const float4 g = __ldg(g4 + i);
+        float4 o;
+        o.x = (v[j].x - mean) * rstd * g.x;
+        o.y = (v[j].y - mean) * rstd * g.y;
+        o.z = (v[j].z - mean) * rstd * g.z;
+        o.w = (v[j].w - mean) * rstd * g.w;
+        if (!RMS) {
+            const float4 bb = __ldg(b4 + i);
+            o.x += bb.x, o.y += bb.y, o.z += bb.z, o.w += bb.w;
+        }
+        __nv_bfloat162 lo = __floats2bfloat162_rn(o.x, o.y), hi = __floats2bfloat162_rn(o.z, o.w);
+        uint2 pk;
+        pk.x = *reinterpret_cast<uint32_t*>(&lo);
+        pk.y = *reinterpret_cast<uint32_t*>(&hi);
+        yr[i] = pk;
+    }
+    if (lane == 0) {
+        stats[2 * r] = mean;
+        stats[2 * r + 1] = rstd;
+    }
+}
+
+// Rows wider than 32 float4 per lane (d > 4096: Llama-3-70B's 8192): three strided passes over
+// the row (L1 hits after the first), the same per-lane summation order.
+template <bool RMS>
+__global__ void __launch_bounds__(32 * kRowsPerBlock) norm_fwd_wide_kernel(const float* __restrict__ x,
+                                                                           const float* __restrict__ gamma,
+                                                                           const float* __restrict__ beta, float eps,
+                                                                           int64_t rows, int d,
+                                                                           __nv_bfloat16* __restrict__ y,
+                                                                           float* __restrict__ stats) {
     const int lane = threadIdx.x & 31;
     const int64_t r = static_cast<int64_t>(blockIdx.x) * kRowsPerBlock + (threadIdx.x >> 5);
     if (r >= rows) return;
@@ -448,8 +513,19 @@ void norm_forward(const float* x, const float* gamma, const float* beta, int rms
                   void* y, float* stats, cudaStream_t st) {
     const dim3 grid(static_cast<unsigned>((rows + kRowsPerBlock - 1) / kRowsPerBlock));
     auto* yo = static_cast<__nv_bfloat16*>(y);
-    if (rms) launch_kernel(norm_fwd_kernel<true>, grid, dim3(32 * kRowsPerBlock), 0, st, x, gamma, beta, eps, rows, d, yo, stats);
-    else launch_kernel(norm_fwd_kernel<false>, grid, dim3(32 * kRowsPerBlock), 0, st, x, gamma, beta, eps, rows, d, yo, stats);
+    const int nj = (d / 4 + 31) / 32;  // float4 per lane (d <= 4096 held in registers)
+    auto go = [&](auto kern) { launch_kernel(kern, grid, dim3(32 * kRowsPerBlock), 0, st, x, gamma, beta, eps, rows, d, yo, stats); };
+    if (rms) {
+        if (nj <= 8) go(norm_fwd_kernel<true, 8>);
+        else if (nj <= 16) go(norm_fwd_kernel<true, 16>);
+        else if (nj <= 32) go(norm_fwd_kernel<true, 32>);
+        else go(norm_fwd_wide_kernel<true>);
+    } else {
+        if (nj <= 8) go(norm_fwd_kernel<false, 8>);
+        else if (nj <= 16) go(norm_fwd_kernel<false, 16>);
+        else if (nj <= 32) go(norm_fwd_kernel<false, 32>);
+        else go(norm_fwd_wide_kernel<false>);
+    }
 }
 
 void norm_backward(const float* dy, const float* x, const float* stats, const float* gamma, int rms, int64_t rows,

@@ -214,6 +214,40 @@ __device__ __forceinline__ float gelu_grad_f(float x, int kind) {
     return fmaf(0.5f * x * du, fmaf(-t, t, 1.0f), fmaf(0.5f, t, 0.5f));
 }
 
+// Packed fp32 pairs (FFMA2 / FMUL2 on sm_100): each lane op is the same IEEE operation as its
+// scalar form, so results are bitwise those of the scalar code; the instruction count halves,
+// which matters for the GELU epilogues (issue slots and, under the board's power cap, energy).
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+    uint64_t r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;"
+        : "=l"(r)
+        : "l"(*reinterpret_cast<uint64_t*>(&a)), "l"(*reinterpret_cast<uint64_t*>(&b)), "l"(*reinterpret_cast<uint64_t*>(&c)));
+    return *reinterpret_cast<float2*>(&r);
+}
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
+    uint64_t r;
+    asm("mul.rn.f32x2 %0, %1, %2;"
+        : "=l"(r)
+        : "l"(*reinterpret_cast<uint64_t*>(&a)), "l"(*reinterpret_cast<uint64_t*>(&b)));
+    return *reinterpret_cast<float2*>(&r);
+}
+__device__ __forceinline__ float2 f2(float v) { return make_float2(v, v); }
+// gelu_f / gelu_grad_f (tanh form) on a pair, operation for operation
+__device__ __forceinline__ float2 gelu2_tanh(float2 x) {
+    const float2 x2 = mul2(x, x);
+    const float2 u = mul2(x, fma2(f2(0.0356774081f), x2, f2(0.79788456080286536f)));
+    const float2 hx = mul2(f2(0.5f), x);
+    return fma2(hx, make_float2(tanh_fast(u.x), tanh_fast(u.y)), hx);
+}
+__device__ __forceinline__ float2 gelu_grad2_tanh(float2 x) {
+    const float2 x2 = mul2(x, x);
+    const float2 u = mul2(x, fma2(f2(0.0356774081f), x2, f2(0.79788456080286536f)));
+    const float2 t = make_float2(tanh_fast(u.x), tanh_fast(u.y));
+    const float2 du = fma2(f2(0.1070322243f), x2, f2(0.79788456080286536f));
+    const float2 a = mul2(mul2(f2(0.5f), x), du);
+    return fma2(a, fma2(make_float2(-t.x, -t.y), t, f2(1.0f)), fma2(f2(0.5f), t, f2(0.5f)));
+}
+
 template <int BN, int EPI>
 struct TileEpilogue {
     using E = EpiSmem<EPI>;
@@ -396,8 +430,16 @@ struct TileEpilogue {
 #pragma unroll
             for (int i = 0; i < 16; ++i) hk[i] = pack_bf16(v[2 * i], v[2 * i + 1]);
             if (row < p.M && p.aux) store_row_bf16(p.aux, p.ldaux, row, col0, hk);
+            if (p.act == GELU_ERF) {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = gelu_f(v[i], p.act);
+                for (int i = 0; i < 32; ++i) v[i] = gelu_f(v[i], GELU_ERF);
+            } else {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const float2 y = gelu2_tanh(make_float2(v[2 * i], v[2 * i + 1]));
+                    v[2 * i] = y.x, v[2 * i + 1] = y.y;
+                }
+            }
         }
         if (E::IS_GATE && p.relu && p.gate_mask != nullptr) {
 #pragma unroll
@@ -424,8 +466,17 @@ struct TileEpilogue {
         } else if (BASE == EPI_GELU_GATE_BF16) {  // dh = dg * gelu'(h)
             float g[32];
             if (!gate_bf16(p, row, col0, g)) return;
+            if (p.act == GELU_ERF) {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] *= gelu_grad_f(g[i], p.act);
+                for (int i = 0; i < 32; ++i) v[i] *= gelu_grad_f(g[i], GELU_ERF);
+            } else {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const float2 y = mul2(make_float2(v[2 * i], v[2 * i + 1]),
+                                          gelu_grad2_tanh(make_float2(g[2 * i], g[2 * i + 1])));
+                    v[2 * i] = y.x, v[2 * i + 1] = y.y;
+                }
+            }
         }
         if (BASE == EPI_SGD_F32) {
             // fused SGD (apply_sgd, model.cpp:150-155): w -= lr * dW, no FMA, in place on the

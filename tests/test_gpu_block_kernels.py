@@ -233,7 +233,7 @@ def test_attention_is_deterministic():
 
 
 @pytest.mark.parametrize("rms", [0, 1])
-@pytest.mark.parametrize("T,d", [(16384, 1600), (1000, 1280), (64, 4096)])
+@pytest.mark.parametrize("T,d", [(16384, 1600), (1000, 1280), (64, 4096), (16, 8192)])
 def test_norm_forward_backward(T, d, rms):
     x = torch.randn(T, d, device="cuda") * 2 + 0.5
     g = 1 + 0.1 * torch.randn(d, device="cuda")
