@@ -86,7 +86,7 @@ struct BCfg {
     static constexpr int BIG = kRowsB * HD * 2;    // a 128-row tile (ATOMS atoms of 16 KB)
     static constexpr int SMALL = kStepB * HD * 2;  // a 64-row tile (ATOMS atoms of 8 KB)
     static constexpr int A_BIG = kRowsB * 128, A_SMALL = kStepB * 128;
-    static constexpr int ST = HD == 64 ? 4 : 3;         // streamed-tile stages
+    static constexpr int ST = HD == 64 ? 8 : 3;         // streamed-tile stages
     static constexpr int OWN = HD == 64 ? 2 : 1;        // own-tile stages (next tile prefetch)
     static constexpr bool SEP_DKDV = HD == 64;  // separate P / dS regions fit (TMEM map above)
     static constexpr int SMEM_DKDV = OWN * 2 * BIG + ST * 2 * SMALL + ST * 2 * 256 + 1024 + 512;
@@ -248,8 +248,11 @@ __global__ void __launch_bounds__(kThreadsB, 1)
                 mbar_wait(acc_empty, (lt & 1) ^ 1);  // the previous tile's dQ is read out
                 fence_after();
                 for (int j = 0; j < n; ++j) {
-                    if (j + 2 < n) issue_s(g + j + 2);
+                    // dQ of step j first, then S / dP of step j + 2: an S issue that waits for its
+                    // K / V tile (TMA) must not hold back the product the softmax warps' next
+                    // dS buffer waits for
                     issue_d(g + j, j == 0);
+                    if (j + 2 < n) issue_s(g + j + 2);
                 }
                 umma_commit(acc_full);
                 umma_commit(&q_empty[ob]);
@@ -534,11 +537,10 @@ __global__ void __launch_bounds__(kThreadsB, 1)
                 mbar_wait(acc_empty, (lt & 1) ^ 1);  // the previous tile's dK / dV are read out
                 fence_after();
                 for (int j = 0; j < n; ++j) {
-                    // separate P / dS: S / dP of step j + 2 as soon as step j's are loaded;
-                    // written back over S / dP: only after the products that read them
-                    if (SEP && j + 2 < n) issue_s(g + j + 2);
+                    // the products of step j first, then S / dP of step j + 2 (which may wait for
+                    // its Q / dO tile): see the dQ pass
                     issue_d(g + j, j == 0);
-                    if (!SEP && j + 2 < n) issue_s(g + j + 2);
+                    if (j + 2 < n) issue_s(g + j + 2);
                 }
                 umma_commit(acc_full);
                 umma_commit(&kv_empty[ob]);
@@ -557,9 +559,9 @@ __global__ void __launch_bounds__(kThreadsB, 1)
             tile(t, kb, kvh, b);
             const int key = kb * kRowsB + r;
             const int n = group * per_head(kb);
-            for (int j = 0; j < n; ++j, ++g) {
-                int hq, qs;
-                step_of(kb, kvh, j, hq, qs);
+            const int qs0 = sh.causal ? 2 * kb : 0;
+            int hq = kvh * group, qs = qs0;  // step j's query head and block (step_of, incrementally)
+            for (int j = 0; j < n; ++j, ++g, (++qs == n_qs ? (qs = qs0, ++hq) : 0)) {
                 const int st = g % C::ST, bb = g & 1;
                 mbar_wait(&s_full[bb], (g >> 1) & 1);
                 fence_after();

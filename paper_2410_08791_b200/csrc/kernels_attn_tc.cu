@@ -389,8 +389,7 @@ struct Fwd2Cfg {
     static constexpr int Q_BYTES = kQ * HD * 2;
     static constexpr int KV_BYTES = kKV * HD * 2;
     static constexpr int ST = HD <= 64 ? 3 : 2;  // K / V ring
-    static constexpr int XCH_BYTES = (2 * 2 * 128 + 2 * 128) * 4;  // row max (x2 parity) and sum exchange
-    static constexpr int SMEM = 2 * Q_BYTES + 2 * ST * KV_BYTES + XCH_BYTES + 1024 + 512;
+    static constexpr int SMEM = 2 * Q_BYTES + 2 * ST * KV_BYTES + 1024 + 512;  // (+ 3 KB static exchange)
     static constexpr uint32_t T_O = 256;
 };
 
@@ -408,9 +407,9 @@ __global__ void __launch_bounds__(kThreadsF2, 1)
     uint8_t* sQ = smem;                        // 2 tiles (the next tile's Q loads early)
     uint8_t* sK = sQ + 2 * C::Q_BYTES;         // ST tiles
     uint8_t* sV = sK + C::ST * C::KV_BYTES;    // ST tiles
-    float* xmax = reinterpret_cast<float*>(sV + C::ST * C::KV_BYTES);  // [block parity][half][row]
-    float* xl = xmax + 2 * 2 * 128;                                     // [half][row]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(xl + 2 * 128);
+    __shared__ float xmax[2 * 2 * 128];  // row-max exchange [block parity][half][row] (static:
+    __shared__ float xl[2 * 128];        // plain shared loads) and row-sum exchange [half][row]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sV + C::ST * C::KV_BYTES);
     uint64_t* q_full = bars;                   // 2
     uint64_t* q_empty = bars + 2;              // 2
     uint64_t* kv_full = bars + 4;              // ST
