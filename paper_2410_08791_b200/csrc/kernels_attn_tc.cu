@@ -385,9 +385,12 @@ constexpr int kThreadsF2 = 384;
 
 template <int HD>
 struct Fwd2Cfg {
-    static constexpr int ATOMS = HD / 64;
-    static constexpr int Q_BYTES = kQ * HD * 2;
-    static constexpr int KV_BYTES = kKV * HD * 2;
+    // head_dim 80 (ViT-H/14) takes two 64-column atoms: the MMAs read only the first HD
+    // columns (5 K steps of 16 for QK^T, N = 80 for PV); the rest of the second atom (the next
+    // head's columns, or TMA zero fill past the row) is loaded but never multiplied
+    static constexpr int ATOMS = (HD + 63) / 64;
+    static constexpr int Q_BYTES = kQ * ATOMS * 64 * 2;
+    static constexpr int KV_BYTES = kKV * ATOMS * 64 * 2;
     static constexpr int ST = HD <= 64 ? 3 : 2;  // K / V ring
     static constexpr int SMEM = 2 * Q_BYTES + 2 * ST * KV_BYTES + 1024 + 512;  // (+ 3 KB static exchange)
     static constexpr uint32_t T_O = 256;
@@ -562,11 +565,21 @@ __global__ void __launch_bounds__(kThreadsF2, 1)
                 const int ob = gg & 1;
                 mbar_wait(&o_full[ob], (gg >> 1) & 1);
                 fence_after();
+                if (HH % 32 == 0) {
 #pragma unroll
-                for (int c = 0; c < HH / 32; ++c) {
-                    tmem_ld32(tmem + lane_off + C::T_O + ob * HD + h * HH + c * 32, v);
+                    for (int c = 0; c < HH / 32; ++c) {
+                        tmem_ld32(tmem + lane_off + C::T_O + ob * HD + h * HH + c * 32, v);
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) acc[c * 32 + i] = fmaf(acc[c * 32 + i], corr, __uint_as_float(v[i]));
+                        for (int i = 0; i < 32; ++i) acc[c * 32 + i] = fmaf(acc[c * 32 + i], corr, __uint_as_float(v[i]));
+                    }
+                } else {  // head_dim 80: 40 columns per half, 8 at a time
+#pragma unroll
+                    for (int c = 0; c < HH / 8; ++c) {
+                        uint32_t v8[8];
+                        tmem_ld8(tmem + lane_off + C::T_O + ob * HD + h * HH + c * 8, v8);
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) acc[c * 8 + i] = fmaf(acc[c * 8 + i], corr, __uint_as_float(v8[i]));
+                    }
                 }
                 fence_before();
                 mbar_arrive(&o_empty[ob]);
@@ -1270,6 +1283,7 @@ cudaError_t launch_bwd_tc(const AttnProblem& a, cudaStream_t st) {
 // cudaErrorNotSupported for other head dims (the caller falls back to the mma.sync kernel).
 cudaError_t attention_forward_tc(const AttnProblem& a, cudaStream_t st, bool v2) {
     if (a.head_dim == 64) return v2 ? launch_fwd_tc2<64>(a, st) : launch_fwd_tc<64>(a, st);
+    if (a.head_dim == 80) return launch_fwd_tc2<80>(a, st);  // (v2 only)
     if (a.head_dim == 128) return v2 ? launch_fwd_tc2<128>(a, st) : launch_fwd_tc<128>(a, st);
     return cudaErrorNotSupported;
 }
