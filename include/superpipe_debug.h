@@ -109,7 +109,8 @@ void sp_debug_col_scratch(int64_t rows, int32_t widest, int64_t* part_floats, in
 /* The single-pass norm backward (kernels.hpp norm_backward_fused, d % 4 == 0 and d <= 2048, else
  * SP_ERR_INVALID) and its chunk reduction: dres_out / dres_out16 as above (dres_out null: none),
  * out_param[0, d) / [d, 2d) the parameter gradients (null: none) and out_csum[j] = sum over rows
- * of dres_out (null: none). ppart holds 2 d, cpart d floats per 64-row chunk. */
+ * of dres_out (null: none). ppart holds 2 d, cpart d floats per block of the persistent grid
+ * (min(2 x SMs, ceil(rows / 2)) blocks). */
 int sp_debug_norm_backward_fused(const float* dy, const float* x, const float* stats, const float* gamma,
                                  int32_t rms, int64_t rows, int32_t d, const float* dres_in, float* dres_out,
                                  void* dres_out16, float* ppart, float* cpart, float* out_param, float* out_csum,

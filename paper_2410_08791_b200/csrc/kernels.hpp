@@ -216,9 +216,10 @@ void norm_backward(const float* dy, const float* x, const float* stats, const fl
 void colsum_total_bf16(const void* x, int64_t rows, int n, const ColScratch& scr, float* out, cudaStream_t st);
 int norm_param_chunks(int64_t rows);
 // The single-pass form of norm_backward (d % 4 == 0, d <= 2048; norm_backward_fused_ok): the
-// same dres_out / dres_out16 (skipped when dres_out is null), plus per 64-row chunk c the column
-// partials param_part[c][0][j] = sum dy*xhat, param_part[c][1][j] = sum dy (LayerNorm only) and
-// csum_part[c][j] = sum dres_out (each skipped when null). reduce_col_chunks sums the chunks.
+// same dres_out / dres_out16 (skipped when dres_out is null), plus per block c of its persistent
+// grid (norm_bwd_chunks(rows) blocks, each a fixed strided set of rows) the column partials
+// param_part[c][0][j] = sum dy*xhat, param_part[c][1][j] = sum dy (LayerNorm only) and
+// csum_part[c][j] = sum dres_out (each skipped when null). reduce_col_chunks sums the blocks.
 bool norm_backward_fused_ok(int d);
 int norm_bwd_chunks(int64_t rows);
 void norm_backward_fused(const float* dy, const float* x, const float* stats, const float* gamma, int rms,

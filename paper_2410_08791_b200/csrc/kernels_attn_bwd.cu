@@ -16,18 +16,17 @@
 //               dV += P^T dO, dK += dS^T Q                    (A from TMEM, B = dO / Q N-major)
 //
 // Warp roles (384 threads): warp 0 TMA producer, warp 1 MMA issuer (one thread), warp 2 TMEM
-// allocator, warps 4..11 the elementwise ("softmax") work: TWO warps per TMEM lane quarter, each
-// taking one 32-column half of a step, so every SM sub-partition has two such warps to overlap
-// TMEM-load, MUFU and FMA latencies. S / dP are double-buffered in TMEM: the MMAs of step j+1
-// (and the products of step j-1) run while the softmax warps work on step j. P / dS are written
-// back over the S / dP columns they were computed from (each thread only its own lane and
-// half) and consumed straight from TMEM by the tcgen05.mma A operand — no shared-memory round
-// trip for the probability tiles.
+// allocator, warps 4..11 the elementwise ("softmax") work in two warpgroups: warpgroup wg takes
+// the steps of parity wg (both 32-row halves of each), so the two warps of an SM sub-partition
+// work on different steps and overlap each other's TMEM-load, MUFU and barrier latencies. P / dS
+// are written into TMEM (each thread only its own lane) and consumed straight from TMEM by the
+// tcgen05.mma A operand — no shared-memory round trip for the probability tiles.
 //
-// TMEM columns: S[b] at 128 b, dP[b] at 128 b + 64 (b = step mod NB, NB = 3 buffers, 2 for
-// dK/dV at head_dim 128), accumulators from 128 NB (dQ: HD columns; dK then dV: 2 HD) <= 512.
-// Three buffers give the MMA issuer two steps of slack: S of step j + 3 is issued once the
-// products of step j (which read the P / dS written over buffer j mod 3) are queued.
+// TMEM columns. dQ pass: S / dP of step b at 128 b (b = step mod 2), dS in a separate region
+// from 256, dQ from 320. dK/dV pass: S / dP in NB buffers at 128 b (b = step mod NB; NB = 3 at
+// head_dim 64, 2 at 128), P / dS written back over the S / dP columns they were computed from,
+// dK then dV from 128 NB. The S / dP MMAs of step j + NB are issued after the products of step
+// j, which read that buffer (one issuing thread: in order).
 #include <cuda.h>
 #include <cuda_bf16.h>
 
@@ -88,7 +87,12 @@ struct BCfg {
     static constexpr int A_BIG = kRowsB * 128, A_SMALL = kStepB * 128;
     static constexpr int ST = HD == 64 ? 8 : 3;         // streamed-tile stages
     static constexpr int OWN = HD == 64 ? 2 : 1;        // own-tile stages (next tile prefetch)
-    static constexpr bool SEP_DKDV = HD == 64;  // separate P / dS regions fit (TMEM map above)
+    // dK/dV pass: P / dS written back over S / dP in NB_DKDV buffers. Three buffers at head_dim
+    // 64 (dK, dV from column 384) let a warpgroup's next step start without waiting for its
+    // previous step's products (the separate-region double-buffered form, SEP, waited there:
+    // ncu, 21% of the softmax warps' samples on that barrier); two at 128.
+    static constexpr bool SEP_DKDV = false;
+    static constexpr int NB_DKDV = HD == 64 ? 3 : 2;
     static constexpr int SMEM_DKDV = OWN * 2 * BIG + ST * 2 * SMALL + ST * 2 * 256 + 1024 + 512;
     static constexpr int SMEM_DQ = OWN * 2 * BIG + ST * 2 * SMALL + 1024 + 512;
 };
@@ -150,8 +154,8 @@ __global__ void __launch_bounds__(kThreadsB, 1)
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&s_full[i], 1);
-            mbar_init(&s_free[i], 256);
-            mbar_init(&p_full[i], 256);
+            mbar_init(&s_free[i], 128);  // one warpgroup per step
+            mbar_init(&p_full[i], 128);
             mbar_init(&ds_free[i], 1);
         }
         mbar_init(acc_full, 1);
@@ -248,9 +252,9 @@ __global__ void __launch_bounds__(kThreadsB, 1)
                 mbar_wait(acc_empty, (lt & 1) ^ 1);  // the previous tile's dQ is read out
                 fence_after();
                 for (int j = 0; j < n; ++j) {
-                    // dQ of step j first, then S / dP of step j + 2: an S issue that waits for its
-                    // K / V tile (TMA) must not hold back the product the softmax warps' next
-                    // dS buffer waits for
+                    // step j's dQ product first, then S / dP of step j + 2: an S issue waiting for
+                    // its K / V tile must not hold back the product the next dS buffer waits for
+                    // (Llama-3 shape: 6.2 -> 5.3 ms for both passes; GPT-2 XL unchanged)
                     issue_d(g + j, j == 0);
                     if (j + 2 < n) issue_s(g + j + 2);
                 }
@@ -260,8 +264,10 @@ __global__ void __launch_bounds__(kThreadsB, 1)
             }
         }
     } else if (warp >= 4) {
-        // ===== elementwise: thread = query row, half = which 32 keys of a 64-key step =====
-        const int q4 = warp & 3, half = (warp - 4) >> 2;
+        // ===== elementwise: thread = query row; warpgroup wg takes the steps of parity wg (both
+        // 32-key halves of each), as in the dK/dV pass =====
+        const int q4 = warp & 3, wg = (warp - 4) >> 2;
+        const int half = wg;  // (delta store and the tile's dQ readout: half the columns each)
         const int r = q4 * 32 + lane;
         const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
         uint32_t vs[32], vp[32];
@@ -305,33 +311,36 @@ __global__ void __launch_bounds__(kThreadsB, 1)
             if (half == 0) delta[li] = Dl;
             const int n = steps(qb);
             for (int j = 0; j < n; ++j, ++g) {
+                if ((g & 1) != wg) continue;  // the other warpgroup's step
                 const int bb = g & 1;
+                if (g >= 2) mbar_wait(&ds_free[bb], ((g - 2) >> 1) & 1);  // step g - 2's dQ product read it
                 mbar_wait(&s_full[bb], (g >> 1) & 1);
                 fence_after();
-                tmem_ld32_async(tmem + lane_off + 128 * bb + 32 * half, vs);
-                tmem_ld32_async(tmem + lane_off + 128 * bb + 64 + 32 * half, vp);
-                tmem_ld_wait(vs);
-                tmem_ld_wait(vp);
-                fence_before();
-                mbar_arrive(&s_free[bb]);  // the MMAs of step g + 2 may overwrite S / dP now
-                const int k0 = j * kStepB + 32 * half;               // first key of this half
-                const bool mask = sh.causal && k0 + 31 > qb * kRowsB;  // some key above some query
-                uint32_t dd[16];
 #pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    float p0 = ex2_approx(fmaf(__uint_as_float(vs[2 * i]), sh.scale_log2, -L));
-                    float p1 = ex2_approx(fmaf(__uint_as_float(vs[2 * i + 1]), sh.scale_log2, -L));
-                    if (mask) {
-                        if (k0 + 2 * i > qi) p0 = 0.0f;
-                        if (k0 + 2 * i + 1 > qi) p1 = 0.0f;
+                for (int h = 0; h < 2; ++h) {
+                    tmem_ld32_async(tmem + lane_off + 128 * bb + 32 * h, vs);
+                    tmem_ld32_async(tmem + lane_off + 128 * bb + 64 + 32 * h, vp);
+                    tmem_ld_wait(vs);
+                    tmem_ld_wait(vp);
+                    if (h == 1) {
+                        fence_before();
+                        mbar_arrive(&s_free[bb]);  // the MMAs of step g + 2 may overwrite S / dP now
                     }
-                    dd[i] = pack_bf16(p0 * (__uint_as_float(vp[2 * i]) - Dl), p1 * (__uint_as_float(vp[2 * i + 1]) - Dl));
+                    const int k0 = j * kStepB + 32 * h;                  // first key of this half
+                    const bool mask = sh.causal && k0 + 31 > qb * kRowsB;  // some key above some query
+                    uint32_t dd[16];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        float p0 = ex2_approx(fmaf(__uint_as_float(vs[2 * i]), sh.scale_log2, -L));
+                        float p1 = ex2_approx(fmaf(__uint_as_float(vs[2 * i + 1]), sh.scale_log2, -L));
+                        if (mask) {
+                            if (k0 + 2 * i > qi) p0 = 0.0f;
+                            if (k0 + 2 * i + 1 > qi) p1 = 0.0f;
+                        }
+                        dd[i] = pack_bf16(p0 * (__uint_as_float(vp[2 * i]) - Dl), p1 * (__uint_as_float(vp[2 * i + 1]) - Dl));
+                    }
+                    tmem_st16(tmem + lane_off + T_DS + 32 * bb + 16 * h, dd);
                 }
-                if (g >= 2) {  // the dQ MMAs of step g - 2 have read this dS buffer
-                    mbar_wait(&ds_free[bb], ((g - 2) >> 1) & 1);
-                    fence_after();
-                }
-                tmem_st16(tmem + lane_off + T_DS + 32 * bb + 16 * half, dd);
                 tmem_st_wait();
                 fence_before();
                 mbar_arrive(&p_full[bb]);
@@ -370,14 +379,16 @@ __global__ void __launch_bounds__(kThreadsB, 1)
 // ------------------------------------------------------------------------------------------
 // dK, dV
 // ------------------------------------------------------------------------------------------
-template <int HD, bool SEP>
+template <int HD, bool SEP, int NB>
 __global__ void __launch_bounds__(kThreadsB, 1)
     attn_bwd_dkdv2_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmQ,
                           const __grid_constant__ CUtensorMap tmDO, const float* __restrict__ lse,
                           const float* __restrict__ delta, __nv_bfloat16* __restrict__ dqkv, BShape sh, int n_seq) {
     using C = BCfg<HD>;
     // TMEM map (header): P / dS regions of buffer b, then dK and dV
-    constexpr uint32_t T_ACC = SEP ? 384 : 256;
+    // NB S / dP buffers (P / dS written back over them when !SEP); SEP uses 2 + separate P / dS
+    static_assert(!SEP || NB == 2, "separate P / dS regions are double-buffered");
+    constexpr uint32_t T_ACC = SEP ? 384 : 128 * NB;
     static_assert(T_ACC + 2 * HD <= 512, "dK / dV do not fit in TMEM");
     auto p_col = [](int bb) { return SEP ? 256u + 64u * bb : 128u * bb; };
     auto ds_col = [](int bb) { return SEP ? 288u + 64u * bb : 128u * bb + 64u; };
@@ -394,10 +405,10 @@ __global__ void __launch_bounds__(kThreadsB, 1)
     uint64_t* kv_empty = bars + 2;           // OWN
     uint64_t* q_full = bars + 4;             // ST
     uint64_t* q_empty = q_full + C::ST;      // ST
-    uint64_t* s_full = q_empty + C::ST;      // 2
-    uint64_t* s_free = s_full + 2;           // 2 (SEP)
-    uint64_t* p_full = s_free + 2;           // 2
-    uint64_t* ds_free = p_full + 2;          // 2 (SEP)
+    uint64_t* s_full = q_empty + C::ST;      // NB
+    uint64_t* s_free = s_full + NB;          // 2 (SEP)
+    uint64_t* p_full = s_free + 2;           // NB
+    uint64_t* ds_free = p_full + NB;         // 2 (SEP)
     uint64_t* acc_full = ds_free + 2;
     uint64_t* acc_empty = acc_full + 1;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
@@ -433,10 +444,12 @@ __global__ void __launch_bounds__(kThreadsB, 1)
             mbar_init(&q_full[i], 1);
             mbar_init(&q_empty[i], 1);
         }
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < NB; ++i) {
             mbar_init(&s_full[i], 1);
-            mbar_init(&s_free[i], 256);
-            mbar_init(&p_full[i], 256);
+            mbar_init(&p_full[i], 128);  // one warpgroup per step
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&s_free[i], 128);
             mbar_init(&ds_free[i], 1);
         }
         mbar_init(acc_full, 1);
@@ -494,7 +507,7 @@ __global__ void __launch_bounds__(kThreadsB, 1)
             constexpr uint32_t ID_D = make_idesc(128, HD, false, true);
             uint64_t dk_, dv_;  // the tile's K / V descriptors (K-major, k step 0)
             auto issue_s = [&](int gg) {
-                const int st = gg % C::ST, bb = gg & 1;
+                const int st = gg % C::ST, bb = gg % NB;
                 mbar_wait(&q_full[st], (gg / C::ST) & 1);
                 if (SEP && gg >= 2) mbar_wait(&s_free[bb], ((gg - 2) >> 1) & 1);
                 fence_after();
@@ -509,8 +522,8 @@ __global__ void __launch_bounds__(kThreadsB, 1)
                 umma_commit(&s_full[bb]);
             };
             auto issue_d = [&](int gg, bool first) {
-                const int st = gg % C::ST, bb = gg & 1;
-                mbar_wait(&p_full[bb], (gg >> 1) & 1);
+                const int st = gg % C::ST, bb = gg % NB;
+                mbar_wait(&p_full[bb], (gg / NB) & 1);
                 fence_after();
                 const uint64_t dq = make_desc(smem_u32(sQ + st * C::SMALL), C::A_SMALL, 1024);
                 const uint64_t ddo = make_desc(smem_u32(sDO + st * C::SMALL), C::A_SMALL, 1024);
@@ -532,15 +545,15 @@ __global__ void __launch_bounds__(kThreadsB, 1)
                 mbar_wait(&kv_full[ob], (lt / C::OWN) & 1);
                 dk_ = make_desc(smem_u32(sK + ob * C::BIG), 16, 1024);
                 dv_ = make_desc(smem_u32(sV + ob * C::BIG), 16, 1024);
-                issue_s(g);
-                issue_s(g + 1);  // (n >= 2: sequences are whole 128-row blocks)
+                for (int i = 0; i < NB && i < n; ++i) issue_s(g + i);
                 mbar_wait(acc_empty, (lt & 1) ^ 1);  // the previous tile's dK / dV are read out
                 fence_after();
                 for (int j = 0; j < n; ++j) {
-                    // the products of step j first, then S / dP of step j + 2 (which may wait for
-                    // its Q / dO tile): see the dQ pass
+                    // separate P / dS: S / dP of step j + 2 as soon as step j's are loaded;
+                    // written back over S / dP: only after the products that read them
+                    if (SEP && j + 2 < n) issue_s(g + j + 2);
                     issue_d(g + j, j == 0);
-                    if (j + 2 < n) issue_s(g + j + 2);
+                    if (!SEP && j + NB < n) issue_s(g + j + NB);  // (in order after the product)
                 }
                 umma_commit(acc_full);
                 umma_commit(&kv_empty[ob]);
@@ -548,8 +561,11 @@ __global__ void __launch_bounds__(kThreadsB, 1)
             }
         }
     } else if (warp >= 4) {
-        // ===== elementwise: thread = key row, half = which 32 queries of a 64-query step =====
-        const int q4 = warp & 3, half = (warp - 4) >> 2;
+        // ===== elementwise: thread = key row; warpgroup wg takes the steps of parity wg (all 64
+        // queries of each, in two 32-query halves), so the two warps of an SM sub-partition work
+        // on different steps and overlap each other's TMEM / MUFU / barrier latencies =====
+        const int q4 = warp & 3, wg = (warp - 4) >> 2;
+        const int half = wg;  // (the tile's dK / dV readout below: wg 0 dK, wg 1 dV)
         const int r = q4 * 32 + lane;
         const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
         uint32_t vs[32], vp[32];
@@ -562,50 +578,53 @@ __global__ void __launch_bounds__(kThreadsB, 1)
             const int qs0 = sh.causal ? 2 * kb : 0;
             int hq = kvh * group, qs = qs0;  // step j's query head and block (step_of, incrementally)
             for (int j = 0; j < n; ++j, ++g, (++qs == n_qs ? (qs = qs0, ++hq) : 0)) {
-                const int st = g % C::ST, bb = g & 1;
-                mbar_wait(&s_full[bb], (g >> 1) & 1);
+                if ((g & 1) != wg) continue;  // the other warpgroup's step
+                const int st = g % C::ST, bb = g % NB;
+                if (SEP && g >= 2) mbar_wait(&ds_free[bb], ((g - 2) >> 1) & 1);  // step g - 2's products
+                mbar_wait(&s_full[bb], (g / NB) & 1);                              // read this P / dS buffer
                 fence_after();
-                const uint32_t cs = tmem + lane_off + 128 * bb + 32 * half;
-                tmem_ld32_async(cs, vs);
-                tmem_ld32_async(cs + 64, vp);
-                // lse / delta of this half's 32 queries (landed with the step's Q tile, which the
-                // S MMA already waited for)
-                const float4* L4 = reinterpret_cast<const float4*>(sL + st * kStepB + 32 * half);
-                const float4* D4 = reinterpret_cast<const float4*>(sD + st * kStepB + 32 * half);
-                tmem_ld_wait(vs);
-                tmem_ld_wait(vp);
-                if (SEP) {
-                    fence_before();
-                    mbar_arrive(&s_free[bb]);  // the MMAs of step g + 2 may overwrite S / dP now
-                }
-                const int q0 = qs * kStepB + 32 * half;  // first query of this half
-                const bool mask = sh.causal && kb * kRowsB + kRowsB - 1 > q0;
-                uint32_t pp[16], dd[16];
 #pragma unroll
-                for (int i4 = 0; i4 < 8; ++i4) {
-                    const float4 l = L4[i4], dl = D4[i4];
-                    const float lv[4] = {l.x, l.y, l.z, l.w}, dv[4] = {dl.x, dl.y, dl.z, dl.w};
-#pragma unroll
-                    for (int u = 0; u < 2; ++u) {
-                        const int i = 2 * i4 + u;  // query pair (2 i, 2 i + 1)
-                        float p0 = ex2_approx(fmaf(__uint_as_float(vs[2 * i]), sh.scale_log2, -lv[2 * u]));
-                        float p1 = ex2_approx(fmaf(__uint_as_float(vs[2 * i + 1]), sh.scale_log2, -lv[2 * u + 1]));
-                        if (mask) {
-                            if (key > q0 + 2 * i) p0 = 0.0f;
-                            if (key > q0 + 2 * i + 1) p1 = 0.0f;
-                        }
-                        pp[i] = pack_bf16(p0, p1);
-                        dd[i] = pack_bf16(p0 * (__uint_as_float(vp[2 * i]) - dv[2 * u]),
-                                          p1 * (__uint_as_float(vp[2 * i + 1]) - dv[2 * u + 1]));
+                for (int h = 0; h < 2; ++h) {
+                    uint32_t pp[16], dd[16];
+                    const uint32_t cs = tmem + lane_off + 128 * bb + 32 * h;
+                    tmem_ld32_async(cs, vs);
+                    tmem_ld32_async(cs + 64, vp);
+                    // lse / delta of these 32 queries (landed with the step's Q tile, which the S
+                    // MMA already waited for)
+                    const float4* L4 = reinterpret_cast<const float4*>(sL + st * kStepB + 32 * h);
+                    const float4* D4 = reinterpret_cast<const float4*>(sD + st * kStepB + 32 * h);
+                    tmem_ld_wait(vs);
+                    tmem_ld_wait(vp);
+                    if (SEP && h == 1) {
+                        fence_before();
+                        mbar_arrive(&s_free[bb]);  // the MMAs of step g + 2 may overwrite S / dP now
                     }
+                    const int q0 = qs * kStepB + 32 * h;  // first query of this half
+                    const bool mask = sh.causal && kb * kRowsB + kRowsB - 1 > q0;
+#pragma unroll
+                    for (int i4 = 0; i4 < 8; ++i4) {
+                        const float4 l = L4[i4], dl = D4[i4];
+                        const float lv[4] = {l.x, l.y, l.z, l.w}, dv[4] = {dl.x, dl.y, dl.z, dl.w};
+#pragma unroll
+                        for (int u = 0; u < 2; ++u) {
+                            const int i = 2 * i4 + u;  // query pair (2 i, 2 i + 1)
+                            float p0 = ex2_approx(fmaf(__uint_as_float(vs[2 * i]), sh.scale_log2, -lv[2 * u]));
+                            float p1 = ex2_approx(fmaf(__uint_as_float(vs[2 * i + 1]), sh.scale_log2, -lv[2 * u + 1]));
+                            if (mask) {
+                                if (key > q0 + 2 * i) p0 = 0.0f;
+                                if (key > q0 + 2 * i + 1) p1 = 0.0f;
+                            }
+                            pp[i] = pack_bf16(p0, p1);
+                            dd[i] = pack_bf16(p0 * (__uint_as_float(vp[2 * i]) - dv[2 * u]),
+                                              p1 * (__uint_as_float(vp[2 * i + 1]) - dv[2 * u + 1]));
+                        }
+                    }
+                    // (written back over S / dP, half 0's P / dS columns are not half 1's S / dP
+                    // columns: TMEM map in the header)
+                    const uint32_t pofs = SEP ? 16 * h : 32 * h;
+                    tmem_st16(tmem + lane_off + p_col(bb) + pofs, pp);
+                    tmem_st16(tmem + lane_off + ds_col(bb) + pofs, dd);
                 }
-                if (SEP && g >= 2) {  // the products of step g - 2 have read these P / dS buffers
-                    mbar_wait(&ds_free[bb], ((g - 2) >> 1) & 1);
-                    fence_after();
-                }
-                const uint32_t pofs = SEP ? 16 * half : 32 * half;
-                tmem_st16(tmem + lane_off + p_col(bb) + pofs, pp);
-                tmem_st16(tmem + lane_off + ds_col(bb) + pofs, dd);
                 tmem_st_wait();
                 fence_before();
                 mbar_arrive(&p_full[bb]);
@@ -652,7 +671,7 @@ cudaError_t launch_bwd2(const AttnProblem& a, cudaStream_t st) {
         cudaError_t e = cudaFuncSetAttribute(attn_bwd_dq2_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              C::SMEM_DQ);
         if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(attn_bwd_dkdv2_kernel<HD, SEP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            e = cudaFuncSetAttribute(attn_bwd_dkdv2_kernel<HD, SEP, C::NB_DKDV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      C::SMEM_DKDV);
         if (e != cudaSuccess) return e;
         configured = true;
@@ -684,7 +703,7 @@ cudaError_t launch_bwd2(const AttnProblem& a, cudaStream_t st) {
         a.delta, dq, sh, n_seq);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    attn_bwd_dkdv2_kernel<HD, SEP><<<kv_tiles < num_sms() ? kv_tiles : num_sms(), kThreadsB, C::SMEM_DKDV, st>>>(
+    attn_bwd_dkdv2_kernel<HD, SEP, C::NB_DKDV><<<kv_tiles < num_sms() ? kv_tiles : num_sms(), kThreadsB, C::SMEM_DKDV, st>>>(
         t128, t64, do64, a.lse, a.delta, dq, sh, n_seq);
     return cudaGetLastError();
 }

@@ -315,15 +315,14 @@ __global__ void __launch_bounds__(32 * kRowLanes) colsum_total_kernel(const __nv
 }
 
 // Fused norm backward (d <= 2048): one pass over dy, x and dres_in produces dres_out (fp32 and
-// bf16) AND the per-chunk column partials of the norm's parameter gradients (sum dy*xhat, sum
+// bf16) AND the per-block column partials of the norm's parameter gradients (sum dy*xhat, sum
 // dy) and of dres_out itself (the bias gradient of the linear that produced the norm's input),
-// so neither dy / x nor dres_out is read a second time. Block = 8 warps over kNbRows rows: two
-// row groups x four column quarters; warp (rg, q) owns the 32-float4 stripes q, q+4, q+8, ... of
-// every row of its group, so a row's reductions are four warp sums combined through shared
+// so neither dy / x nor dres_out is read a second time. Persistent, two blocks per SM (one
+// partial row each); block = 8 warps: two row groups x four column quarters; warp (rg, q) owns
+// the 32-float4 stripes q, q+4, q+8, ... of every row of its group, so a row's reductions are four warp sums combined through shared
 // memory in quarter order (one named barrier per row, double-buffered by row parity), and each
 // lane keeps its stripes' column partials in registers across the rows. The two row groups are
-// added (rg 0 + rg 1) into the chunk's partial row; reduce_col_chunks sums the chunks in order.
-constexpr int kNbRows = 64;
+// added (rg 0 + rg 1) into the block's partial row; reduce_col_chunks sums them in order.
 constexpr int kNbMaxS = 4;  // stripes per warp: d <= 4 * 4 * 32 * 4 = 2048
 
 __device__ __forceinline__ void named_bar(int id, int threads) {
@@ -341,8 +340,6 @@ __global__ void __launch_bounds__(256, 2) norm_bwd_fused_kernel(
     __shared__ float4 xch[4][kNbMaxS][3][32];       // row group 1's column partials
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, rg = w >> 2, q = w & 3;
     const int n4 = d >> 2;
-    const int64_t r0 = static_cast<int64_t>(blockIdx.x) * kNbRows;
-    const int64_t r1 = min(rows, r0 + kNbRows);
     const bool dx = dres_out != nullptr;
     const float inv_d = 1.0f / static_cast<float>(d);
     const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -355,7 +352,8 @@ __global__ void __launch_bounds__(256, 2) norm_bwd_fused_kernel(
         A[i] = z4, B[i] = z4, Cs[i] = z4;
     }
     int par = 0;
-    for (int64_t r = r0 + rg; r < r1; r += 2) {
+    // persistent: block b takes the row pairs b, b + grid, b + 2 grid, ... (row 2 p + rg of pair p)
+    for (int64_t r = 2 * static_cast<int64_t>(blockIdx.x) + rg; r < rows; r += 2 * static_cast<int64_t>(gridDim.x)) {
         const float mean = RMS ? 0.0f : stats[2 * r], rstd = stats[2 * r + 1];
         const float4* dr = reinterpret_cast<const float4*>(dy + r * d);
         const float4* xr = reinterpret_cast<const float4*>(x + r * d);
@@ -487,7 +485,13 @@ __global__ void __launch_bounds__(256) reduce_col_chunks_kernel(ColChunks r) {
 int norm_param_chunks(int64_t rows) { return static_cast<int>((rows + kChunkRows - 1) / kChunkRows); }
 
 bool norm_backward_fused_ok(int d) { return d % 4 == 0 && d <= 4 * kNbMaxS * 32 * 4; }
-int norm_bwd_chunks(int64_t rows) { return static_cast<int>((rows + kNbRows - 1) / kNbRows); }
+// Grid of the persistent fused norm backward = its number of partial rows: two blocks per SM
+// (fixed for a GPU model, so the reduction order depends only on the shape there).
+int norm_bwd_chunks(int64_t rows) {
+    const int64_t pairs = (rows + 1) / 2;
+    const int64_t g = 2 * static_cast<int64_t>(num_sms());
+    return static_cast<int>(pairs < g ? pairs : g);
+}
 
 void norm_backward_fused(const float* dy, const float* x, const float* stats, const float* gamma, int rms,
                          int64_t rows, int d, const float* dres_in, float* dres_out, void* dres_out16,

@@ -301,7 +301,7 @@ def test_norm_backward_fused(T, d, rms):
     assert LIB.sp_debug_norm_backward(dy.data_ptr(), x.data_ptr(), stats.data_ptr(), g.data_ptr(), rms, T, d,
                                       dres_in.data_ptr(), ref_out.data_ptr(), ref16.data_ptr(), part.data_ptr(),
                                       cnt.data_ptr(), ref_param.data_ptr(), st) == 0
-    chunks = (T + 63) // 64
+    chunks = min(2 * torch.cuda.get_device_properties(0).multi_processor_count, (T + 1) // 2)  # norm_bwd_chunks
     ppart = torch.empty(chunks, 2, d, device="cuda")
     cpart = torch.empty(chunks, d, device="cuda")
     runs = []

@@ -80,6 +80,23 @@ def main():
                    help="copies wait for the reference policy's trigger compute (no eager prefetch)")
     a = p.parse_args()
     peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["bf16_tflops_sustained"] * 1e12
+
+    def copy_rate(nbytes, reps=40):
+        """Measured pinned host -> HBM rate for back-to-back copies of one layer's size (the rate a
+        small-layer config such as C1 can reach: per-copy latency dominates below a few MB)."""
+        src = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+        dst = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+        for _ in range(5):
+            dst.copy_(src, non_blocking=True)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            dst.copy_(src, non_blocking=True)
+        e1.record()
+        torch.cuda.synchronize()
+        return nbytes * reps / (e0.elapsed_time(e1) * 1e-3)
+
     for name in a.configs:
         c = CONFIGS[name]
         n, d, items, rows = c["n"], c["d"], c["items"], c["rows"]
@@ -108,12 +125,16 @@ def main():
             wire = d * d * 2 + d * 4
             passes = 1 if c.get("batching") else items  # layer-stack passes over the link
             roof = passes * n * max(2.0 * rows * d * d * items / passes / peak, wire / 55.5e9) * 1e3
+            small = copy_rate(wire)  # this layer size's achievable link rate
+            roof_small = passes * n * max(2.0 * rows * d * d * items / passes / peak, wire / small) * 1e3
             print(json.dumps({
                 "config": name, "layers": n, "d": d, "items": items, "rows": rows, "k": k,
                 "item_batching": bool(c.get("batching")), "eager_prefetch": not a.reference_prefetch,
                 "transfer_mode": a.mode,
                 "k_prime": kp, "ms_per_call": ms, "samples_per_s": items * rows / (ms * 1e-3),
                 "layer_roofline_ms": roof, "frac_of_roofline": roof / ms,
+                "layer_copy_gbs": small / 1e9, "small_copy_roofline_ms": roof_small,
+                "frac_of_small_copy_roofline": roof_small / ms, "host_enqueue_ms": st["host_enqueue_ms"],
                 "n_slots": st["n_slots"], "peak_weight_gb": st["peak_weight_bytes"] / 1e9,
                 "hbm_reserved_gb": st["hbm_reserved_bytes"] / 1e9,
                 "full_residency_bf16_gb": n * wire / 1e9,
