@@ -1,7 +1,7 @@
 // kernels_attn_bwd.cu — tcgen05 flash-attention backward (sm_100a), head_dim 64 / 128.
 //
 // Two persistent kernels, deterministic (every output element is one fixed-order reduction, no
-// atomics), for sequences made of whole 128-row blocks:
+// atomics), head_dim 64 / 80 / 128, any sequence length (a ragged last block is masked):
 //
 //   dQ pass   tile = 128 queries of one (sequence, head); streams 64-key steps of K, V:
 //               S = Q K^T, dP = dO V^T                        (TMEM, fp32, M 128 x N 64)
@@ -31,6 +31,7 @@
 #include <cuda_bf16.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "kernels.hpp"
 #include "tc_ptx.cuh"
@@ -42,6 +43,9 @@ using namespace tc;
 constexpr int kThreadsB = 384;
 constexpr int kRowsB = 128;  // the CTA tile's own rows (queries in dQ, keys in dK/dV)
 constexpr int kStepB = 64;   // rows streamed per step (keys in dQ, queries in dK/dV)
+// lse / delta stage stride (floats): a step's 64 values plus up to 3 of 16-byte alignment slack
+// (rows of a ragged sequence start at any float)
+constexpr int kLStride = 72;
 
 __device__ __forceinline__ float ex2_approx(float x) {
     float y;
@@ -81,9 +85,10 @@ struct BShape {
 
 template <int HD>
 struct BCfg {
-    static constexpr int ATOMS = HD / 64;
-    static constexpr int BIG = kRowsB * HD * 2;    // a 128-row tile (ATOMS atoms of 16 KB)
-    static constexpr int SMALL = kStepB * HD * 2;  // a 64-row tile (ATOMS atoms of 8 KB)
+    // head_dim 80 (ViT-H/14) takes two 64-column atoms; the MMAs read the first HD columns only
+    static constexpr int ATOMS = (HD + 63) / 64;
+    static constexpr int BIG = kRowsB * ATOMS * 128;    // a 128-row tile (ATOMS atoms of 16 KB)
+    static constexpr int SMALL = kStepB * ATOMS * 128;  // a 64-row tile (ATOMS atoms of 8 KB)
     static constexpr int A_BIG = kRowsB * 128, A_SMALL = kStepB * 128;
     static constexpr int ST = HD == 64 ? 8 : 3;         // streamed-tile stages
     static constexpr int OWN = HD == 64 ? 2 : 1;        // own-tile stages (next tile prefetch)
@@ -93,9 +98,41 @@ struct BCfg {
     // ncu, 21% of the softmax warps' samples on that barrier); two at 128.
     static constexpr bool SEP_DKDV = false;
     static constexpr int NB_DKDV = HD == 64 ? 3 : 2;
-    static constexpr int SMEM_DKDV = OWN * 2 * BIG + ST * 2 * SMALL + ST * 2 * 256 + 1024 + 512;
+    static constexpr int SMEM_DKDV = OWN * 2 * BIG + ST * 2 * SMALL + ST * 2 * kLStride * 4 + 1024 + 512;
     static constexpr int SMEM_DQ = OWN * 2 * BIG + ST * 2 * SMALL + 1024 + 512;
 };
+
+// NC accumulator columns of this thread's TMEM lane (from column `col`), times `sc`, to bf16 at
+// `dst` (NC % 8 == 0): 32-column loads while they fit, then 8-column ones (head_dim 80)
+template <int NC>
+__device__ __forceinline__ void acc_row_out(uint32_t taddr, __nv_bfloat16* dst, float sc, bool store) {
+    uint32_t v[32];
+#pragma unroll
+    for (int c = 0; c < NC / 32; ++c) {
+        tmem_ld32_async(taddr + c * 32, v);
+        tmem_ld_wait(v);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            uint4 w;
+            w.x = pack_bf16(__uint_as_float(v[8 * u + 0]) * sc, __uint_as_float(v[8 * u + 1]) * sc);
+            w.y = pack_bf16(__uint_as_float(v[8 * u + 2]) * sc, __uint_as_float(v[8 * u + 3]) * sc);
+            w.z = pack_bf16(__uint_as_float(v[8 * u + 4]) * sc, __uint_as_float(v[8 * u + 5]) * sc);
+            w.w = pack_bf16(__uint_as_float(v[8 * u + 6]) * sc, __uint_as_float(v[8 * u + 7]) * sc);
+            if (store) reinterpret_cast<uint4*>(dst + c * 32)[u] = w;
+        }
+    }
+#pragma unroll
+    for (int c = (NC / 32) * 4; c < NC / 8; ++c) {
+        uint32_t v8[8];
+        tmem_ld8(taddr + c * 8, v8);
+        uint4 w;
+        w.x = pack_bf16(__uint_as_float(v8[0]) * sc, __uint_as_float(v8[1]) * sc);
+        w.y = pack_bf16(__uint_as_float(v8[2]) * sc, __uint_as_float(v8[3]) * sc);
+        w.z = pack_bf16(__uint_as_float(v8[4]) * sc, __uint_as_float(v8[5]) * sc);
+        w.w = pack_bf16(__uint_as_float(v8[6]) * sc, __uint_as_float(v8[7]) * sc);
+        if (store) reinterpret_cast<uint4*>(dst + c * 8)[0] = w;
+    }
+}
 
 // ------------------------------------------------------------------------------------------
 // dQ (+ delta)
@@ -128,7 +165,9 @@ __global__ void __launch_bounds__(kThreadsB, 1)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int n_qb = sh.S / kRowsB, n_ks = sh.S / kStepB;
+    // ragged sequences (ViT's 257 tokens): the last query block / key step is partial; rows past
+    // the sequence are masked (keys) or never stored (queries)
+    const int n_qb = (sh.S + kRowsB - 1) / kRowsB, n_ks = (sh.S + kStepB - 1) / kStepB;
     const int n_tiles = n_qb * sh.H * n_seq;
     // tile t: (query block, head, sequence), query blocks descending (causal: longest first)
     auto tile = [&](int t, int& qb, int& h, int& b) {
@@ -138,7 +177,7 @@ __global__ void __launch_bounds__(kThreadsB, 1)
         h = rest % sh.H;
         b = rest / sh.H;
     };
-    auto steps = [&](int qb) { return sh.causal ? 2 * (qb + 1) : n_ks; };
+    auto steps = [&](int qb) { return sh.causal ? min(2 * (qb + 1), n_ks) : n_ks; };
 
     if (warp == 0 && lane == 0) {
         prefetch_tmap(&tmQ);
@@ -247,8 +286,7 @@ __global__ void __launch_bounds__(kThreadsB, 1)
                 mbar_wait(&q_full[ob], (lt / C::OWN) & 1);
                 dq_ = make_desc(smem_u32(sQ + ob * C::BIG), 16, 1024);
                 ddo_ = make_desc(smem_u32(sDO + ob * C::BIG), 16, 1024);
-                issue_s(g);
-                issue_s(g + 1);  // (n >= 2: sequences are whole 128-row blocks)
+                for (int i = 0; i < 2 && i < n; ++i) issue_s(g + i);  // (one step: a sequence <= 64 keys)
                 mbar_wait(acc_empty, (lt & 1) ^ 1);  // the previous tile's dQ is read out
                 fence_after();
                 for (int j = 0; j < n; ++j) {
@@ -275,13 +313,14 @@ __global__ void __launch_bounds__(kThreadsB, 1)
         auto load_rows = [&](int tt) {
             int qb_, h_, b_;
             tile(tt, qb_, h_, b_);
+            const bool in = qb_ * kRowsB + r < sh.S;
             const int64_t tk = static_cast<int64_t>(b_) * sh.S + qb_ * kRowsB + r;
             const uint4* a4 = reinterpret_cast<const uint4*>(o + tk * sh.ldo + h_ * HD);
             const uint4* c4 = reinterpret_cast<const uint4*>(dout + tk * sh.ldo + h_ * HD);
 #pragma unroll
             for (int j = 0; j < HD / 8; ++j) {
-                ro[j] = __ldg(a4 + j);
-                rd[j] = __ldg(c4 + j);
+                ro[j] = in ? __ldg(a4 + j) : make_uint4(0u, 0u, 0u, 0u);
+                rd[j] = in ? __ldg(c4 + j) : make_uint4(0u, 0u, 0u, 0u);
             }
         };
         int g = 0, lt = 0;
@@ -291,7 +330,8 @@ __global__ void __launch_bounds__(kThreadsB, 1)
             const int qi = qb * kRowsB + r;
             const int64_t tok = static_cast<int64_t>(b) * sh.S + qi;
             const int64_t li = (static_cast<int64_t>(b) * sh.H + h) * sh.S + qi;
-            const float L = lse[li];
+            const bool q_in = qi < sh.S;
+            const float L = q_in ? lse[li] : 0.0f;
             // delta = sum_d dO . O of this row (both halves compute it identically; half 0 stores
             // it), from rows prefetched into registers during the previous tile (head_dim 64)
             constexpr bool kPrefetch = HD == 64;
@@ -308,7 +348,7 @@ __global__ void __launch_bounds__(kThreadsB, 1)
                 }
             }
             if (kPrefetch && t + static_cast<int>(gridDim.x) < n_tiles) load_rows(t + gridDim.x);
-            if (half == 0) delta[li] = Dl;
+            if (half == 0 && q_in) delta[li] = Dl;
             const int n = steps(qb);
             for (int j = 0; j < n; ++j, ++g) {
                 if ((g & 1) != wg) continue;  // the other warpgroup's step
@@ -327,15 +367,17 @@ __global__ void __launch_bounds__(kThreadsB, 1)
                         mbar_arrive(&s_free[bb]);  // the MMAs of step g + 2 may overwrite S / dP now
                     }
                     const int k0 = j * kStepB + 32 * h;                  // first key of this half
-                    const bool mask = sh.causal && k0 + 31 > qb * kRowsB;  // some key above some query
+                    // some key above some query, or past the sequence
+                    const bool mask = (sh.causal && k0 + 31 > qb * kRowsB) || k0 + 32 > sh.S;
+                    const int klim = sh.causal ? min(qi + 1, sh.S) : sh.S;  // keys < klim are valid
                     uint32_t dd[16];
 #pragma unroll
                     for (int i = 0; i < 16; ++i) {
                         float p0 = ex2_approx(fmaf(__uint_as_float(vs[2 * i]), sh.scale_log2, -L));
                         float p1 = ex2_approx(fmaf(__uint_as_float(vs[2 * i + 1]), sh.scale_log2, -L));
                         if (mask) {
-                            if (k0 + 2 * i > qi) p0 = 0.0f;
-                            if (k0 + 2 * i + 1 > qi) p1 = 0.0f;
+                            if (k0 + 2 * i >= klim) p0 = 0.0f;
+                            if (k0 + 2 * i + 1 >= klim) p1 = 0.0f;
                         }
                         dd[i] = pack_bf16(p0 * (__uint_as_float(vp[2 * i]) - Dl), p1 * (__uint_as_float(vp[2 * i + 1]) - Dl));
                     }
@@ -347,22 +389,9 @@ __global__ void __launch_bounds__(kThreadsB, 1)
             }
             mbar_wait(acc_full, lt & 1);
             fence_after();
-            __nv_bfloat16* row = dqkv + tok * sh.ld + h * HD;
-#pragma unroll
-            for (int c = 0; c < HD / 64; ++c) {  // this half's HD / 2 columns
-                const int col = half * (HD / 2) + c * 32;
-                tmem_ld32_async(tmem + lane_off + T_ACC + col, vs);
-                tmem_ld_wait(vs);
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    uint4 w;
-                    w.x = pack_bf16(__uint_as_float(vs[8 * u + 0]) * sh.scale, __uint_as_float(vs[8 * u + 1]) * sh.scale);
-                    w.y = pack_bf16(__uint_as_float(vs[8 * u + 2]) * sh.scale, __uint_as_float(vs[8 * u + 3]) * sh.scale);
-                    w.z = pack_bf16(__uint_as_float(vs[8 * u + 4]) * sh.scale, __uint_as_float(vs[8 * u + 5]) * sh.scale);
-                    w.w = pack_bf16(__uint_as_float(vs[8 * u + 6]) * sh.scale, __uint_as_float(vs[8 * u + 7]) * sh.scale);
-                    reinterpret_cast<uint4*>(row + col)[u] = w;
-                }
-            }
+            // this half's HD / 2 columns of the query row's dQ (rows past the sequence: not stored)
+            acc_row_out<HD / 2>(tmem + lane_off + T_ACC + half * (HD / 2), dqkv + tok * sh.ld + h * HD + half * (HD / 2),
+                                sh.scale, q_in);
             fence_before();
             mbar_arrive(acc_empty);
         }
@@ -398,9 +427,9 @@ __global__ void __launch_bounds__(kThreadsB, 1)
     uint8_t* sV = sK + C::OWN * C::BIG;      // OWN
     uint8_t* sQ = sV + C::OWN * C::BIG;      // ST
     uint8_t* sDO = sQ + C::ST * C::SMALL;    // ST
-    float* sL = reinterpret_cast<float*>(sDO + C::ST * C::SMALL);  // ST x 64
-    float* sD = sL + C::ST * kStepB;                                // ST x 64
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sD + C::ST * kStepB);
+    float* sL = reinterpret_cast<float*>(sDO + C::ST * C::SMALL);  // ST x kLStride
+    float* sD = sL + C::ST * kLStride;                              // ST x kLStride
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sD + C::ST * kLStride);
     uint64_t* kv_full = bars;                // OWN
     uint64_t* kv_empty = bars + 2;           // OWN
     uint64_t* q_full = bars + 4;             // ST
@@ -414,7 +443,7 @@ __global__ void __launch_bounds__(kThreadsB, 1)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int n_kb = sh.S / kRowsB, n_qs = sh.S / kStepB;
+    const int n_kb = (sh.S + kRowsB - 1) / kRowsB, n_qs = (sh.S + kStepB - 1) / kStepB;  // (ragged: as dQ)
     const int group = sh.H / sh.Hkv;
     const int n_tiles = n_kb * sh.Hkv * n_seq;
     // tile t: (key block, kv head, sequence), key blocks ascending (causal: longest first)
@@ -488,16 +517,22 @@ __global__ void __launch_bounds__(kThreadsB, 1)
                     step_of(kb, kvh, j, hq, qs);
                     const int st = g % C::ST;
                     mbar_wait(&q_empty[st], ((g / C::ST) & 1) ^ 1);
-                    mbar_expect_tx(&q_full[st], 2 * C::SMALL + 2 * kStepB * 4);
+                    // lse / delta of the step's valid queries, from the 16-byte aligned address at
+                    // or below the first (bulk copies need it; the consumer skips `off` floats),
+                    // rounded up to 16 bytes; stage floats past them are stale and masked
+                    const int64_t li = (static_cast<int64_t>(b) * sh.H + hq) * sh.S + qs * kStepB;
+                    const int off = static_cast<int>(li & 3);
+                    const int nvalid = min(kStepB, sh.S - qs * kStepB);
+                    const uint32_t lbytes = static_cast<uint32_t>((off + nvalid + 3) / 4 * 16);
+                    mbar_expect_tx(&q_full[st], 2 * C::SMALL + 2 * lbytes);
                     for (int a = 0; a < C::ATOMS; ++a) {
                         tma_load_2d(&tmQ, &q_full[st], sQ + st * C::SMALL + a * C::A_SMALL, hq * HD + 64 * a,
                                     row0 + qs * kStepB);
                         tma_load_2d(&tmDO, &q_full[st], sDO + st * C::SMALL + a * C::A_SMALL, hq * HD + 64 * a,
                                     row0 + qs * kStepB);
                     }
-                    const int64_t li = (static_cast<int64_t>(b) * sh.H + hq) * sh.S + qs * kStepB;
-                    bulk_load_b(sL + st * kStepB, lse + li, kStepB * 4, &q_full[st]);
-                    bulk_load_b(sD + st * kStepB, delta + li, kStepB * 4, &q_full[st]);
+                    bulk_load_b(sL + st * kLStride, lse + (li - off), lbytes, &q_full[st]);
+                    bulk_load_b(sD + st * kLStride, delta + (li - off), lbytes, &q_full[st]);
                 }
             }
         }
@@ -583,48 +618,67 @@ __global__ void __launch_bounds__(kThreadsB, 1)
                 if (SEP && g >= 2) mbar_wait(&ds_free[bb], ((g - 2) >> 1) & 1);  // step g - 2's products
                 mbar_wait(&s_full[bb], (g / NB) & 1);                              // read this P / dS buffer
                 fence_after();
+                // a step's lse / delta start on a 16-byte boundary unless the sequence length is
+                // not a multiple of 4 (ViT's 257): two instantiations of the step body
+                auto step_body = [&](auto aligned_tag) {
+                    constexpr bool ALIGNED = decltype(aligned_tag)::value;
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    uint32_t pp[16], dd[16];
-                    const uint32_t cs = tmem + lane_off + 128 * bb + 32 * h;
-                    tmem_ld32_async(cs, vs);
-                    tmem_ld32_async(cs + 64, vp);
-                    // lse / delta of these 32 queries (landed with the step's Q tile, which the S
-                    // MMA already waited for)
-                    const float4* L4 = reinterpret_cast<const float4*>(sL + st * kStepB + 32 * h);
-                    const float4* D4 = reinterpret_cast<const float4*>(sD + st * kStepB + 32 * h);
-                    tmem_ld_wait(vs);
-                    tmem_ld_wait(vp);
-                    if (SEP && h == 1) {
-                        fence_before();
-                        mbar_arrive(&s_free[bb]);  // the MMAs of step g + 2 may overwrite S / dP now
-                    }
-                    const int q0 = qs * kStepB + 32 * h;  // first query of this half
-                    const bool mask = sh.causal && kb * kRowsB + kRowsB - 1 > q0;
-#pragma unroll
-                    for (int i4 = 0; i4 < 8; ++i4) {
-                        const float4 l = L4[i4], dl = D4[i4];
-                        const float lv[4] = {l.x, l.y, l.z, l.w}, dv[4] = {dl.x, dl.y, dl.z, dl.w};
-#pragma unroll
-                        for (int u = 0; u < 2; ++u) {
-                            const int i = 2 * i4 + u;  // query pair (2 i, 2 i + 1)
-                            float p0 = ex2_approx(fmaf(__uint_as_float(vs[2 * i]), sh.scale_log2, -lv[2 * u]));
-                            float p1 = ex2_approx(fmaf(__uint_as_float(vs[2 * i + 1]), sh.scale_log2, -lv[2 * u + 1]));
-                            if (mask) {
-                                if (key > q0 + 2 * i) p0 = 0.0f;
-                                if (key > q0 + 2 * i + 1) p1 = 0.0f;
-                            }
-                            pp[i] = pack_bf16(p0, p1);
-                            dd[i] = pack_bf16(p0 * (__uint_as_float(vp[2 * i]) - dv[2 * u]),
-                                              p1 * (__uint_as_float(vp[2 * i + 1]) - dv[2 * u + 1]));
+                    for (int h = 0; h < 2; ++h) {
+                        uint32_t pp[16], dd[16];
+                        const uint32_t cs = tmem + lane_off + 128 * bb + 32 * h;
+                        tmem_ld32_async(cs, vs);
+                        tmem_ld32_async(cs + 64, vp);
+                        // lse / delta of these 32 queries (landed with the step's Q tile, which the
+                        // S MMA already waited for)
+                        const int off = ALIGNED ? 0 : static_cast<int>(((static_cast<int64_t>(b) * sh.H + hq) * sh.S + qs * kStepB) & 3);
+                        const float* Ls = sL + st * kLStride + off + 32 * h;
+                        const float* Ds = sD + st * kLStride + off + 32 * h;
+                        tmem_ld_wait(vs);
+                        tmem_ld_wait(vp);
+                        if (SEP && h == 1) {
+                            fence_before();
+                            mbar_arrive(&s_free[bb]);  // the MMAs of step g + 2 may overwrite S / dP now
                         }
+                        const int q0 = qs * kStepB + 32 * h;  // first query of this half
+                        // some query below some key, or past the sequence (stale lse / delta: zeroed)
+                        const bool mask = (sh.causal && kb * kRowsB + kRowsB - 1 > q0) || q0 + 32 > sh.S;
+                        const int qlo = sh.causal ? key : 0;  // valid queries: qlo <= q < S
+#pragma unroll
+                        for (int i4 = 0; i4 < 8; ++i4) {
+                            float lv[4], dv[4];
+                            if (ALIGNED) {  // 16-byte shared loads
+                                const float4 l = reinterpret_cast<const float4*>(Ls)[i4], dl = reinterpret_cast<const float4*>(Ds)[i4];
+                                lv[0] = l.x, lv[1] = l.y, lv[2] = l.z, lv[3] = l.w;
+                                dv[0] = dl.x, dv[1] = dl.y, dv[2] = dl.z, dv[3] = dl.w;
+                            } else {
+#pragma unroll
+                                for (int k = 0; k < 4; ++k) lv[k] = Ls[4 * i4 + k], dv[k] = Ds[4 * i4 + k];
+                            }
+#pragma unroll
+                            for (int u = 0; u < 2; ++u) {
+                                const int i = 2 * i4 + u;  // query pair (2 i, 2 i + 1)
+                                float p0 = ex2_approx(fmaf(__uint_as_float(vs[2 * i]), sh.scale_log2, -lv[2 * u]));
+                                float p1 = ex2_approx(fmaf(__uint_as_float(vs[2 * i + 1]), sh.scale_log2, -lv[2 * u + 1]));
+                                float d0 = p0 * (__uint_as_float(vp[2 * i]) - dv[2 * u]);
+                                float d1 = p1 * (__uint_as_float(vp[2 * i + 1]) - dv[2 * u + 1]);
+                                if (mask) {
+                                    const int qa = q0 + 2 * i;
+                                    if (qa < qlo || qa >= sh.S) p0 = 0.0f, d0 = 0.0f;
+                                    if (qa + 1 < qlo || qa + 1 >= sh.S) p1 = 0.0f, d1 = 0.0f;
+                                }
+                                pp[i] = pack_bf16(p0, p1);
+                                dd[i] = pack_bf16(d0, d1);
+                            }
+                        }
+                        // (written back over S / dP, half 0's P / dS columns are not half 1's S / dP
+                        // columns: TMEM map in the header)
+                        const uint32_t pofs = SEP ? 16 * h : 32 * h;
+                        tmem_st16(tmem + lane_off + p_col(bb) + pofs, pp);
+                        tmem_st16(tmem + lane_off + ds_col(bb) + pofs, dd);
                     }
-                    // (written back over S / dP, half 0's P / dS columns are not half 1's S / dP
-                    // columns: TMEM map in the header)
-                    const uint32_t pofs = SEP ? 16 * h : 32 * h;
-                    tmem_st16(tmem + lane_off + p_col(bb) + pofs, pp);
-                    tmem_st16(tmem + lane_off + ds_col(bb) + pofs, dd);
-                }
+                };
+                if ((sh.S & 3) == 0) step_body(std::true_type{});
+                else step_body(std::false_type{});
                 tmem_st_wait();
                 fence_before();
                 mbar_arrive(&p_full[bb]);
@@ -634,21 +688,7 @@ __global__ void __launch_bounds__(kThreadsB, 1)
             fence_after();
             __nv_bfloat16* row = dqkv + (static_cast<int64_t>(b) * sh.S + key) * sh.ld +
                                  (half == 0 ? (sh.H + kvh) * HD : (sh.H + sh.Hkv + kvh) * HD);
-            const float sc = half == 0 ? sh.scale : 1.0f;
-#pragma unroll
-            for (int c = 0; c < HD / 32; ++c) {
-                tmem_ld32_async(tmem + lane_off + T_ACC + half * HD + c * 32, vs);
-                tmem_ld_wait(vs);
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    uint4 w;
-                    w.x = pack_bf16(__uint_as_float(vs[8 * u + 0]) * sc, __uint_as_float(vs[8 * u + 1]) * sc);
-                    w.y = pack_bf16(__uint_as_float(vs[8 * u + 2]) * sc, __uint_as_float(vs[8 * u + 3]) * sc);
-                    w.z = pack_bf16(__uint_as_float(vs[8 * u + 4]) * sc, __uint_as_float(vs[8 * u + 5]) * sc);
-                    w.w = pack_bf16(__uint_as_float(vs[8 * u + 6]) * sc, __uint_as_float(vs[8 * u + 7]) * sc);
-                    reinterpret_cast<uint4*>(row + c * 32)[u] = w;
-                }
-            }
+            acc_row_out<HD>(tmem + lane_off + T_ACC + half * HD, row, half == 0 ? sh.scale : 1.0f, key < sh.S);
             fence_before();
             mbar_arrive(acc_empty);
         }
@@ -695,8 +735,9 @@ cudaError_t launch_bwd2(const AttnProblem& a, cudaStream_t st) {
     sh.scale = 1.0f / sqrtf(static_cast<float>(a.head_dim));
     sh.scale_log2 = 1.4426950408889634f * sh.scale;
     const int n_seq = static_cast<int>(a.tokens / a.seq_len);
-    const int q_tiles = (a.seq_len / kRowsB) * a.n_heads * n_seq;
-    const int kv_tiles = (a.seq_len / kRowsB) * a.n_kv_heads * n_seq;
+    const int n_blk = (a.seq_len + kRowsB - 1) / kRowsB;
+    const int q_tiles = n_blk * a.n_heads * n_seq;
+    const int kv_tiles = n_blk * a.n_kv_heads * n_seq;
     auto* dq = static_cast<__nv_bfloat16*>(a.dqkv);
     attn_bwd_dq2_kernel<HD><<<q_tiles < num_sms() ? q_tiles : num_sms(), kThreadsB, C::SMEM_DQ, st>>>(
         t128, do128, t64, static_cast<const __nv_bfloat16*>(a.o), static_cast<const __nv_bfloat16*>(a.dout), a.lse,
@@ -709,11 +750,11 @@ cudaError_t launch_bwd2(const AttnProblem& a, cudaStream_t st) {
 }
 }  // namespace
 
-// The backward for head_dim 64 / 128 and sequences of whole 128-row blocks; delta is formed
-// inside (no separate kernel). cudaErrorNotSupported for other shapes.
+// The backward for head_dim 64 / 80 / 128, any sequence length; delta is formed inside (no
+// separate kernel). cudaErrorNotSupported for other head dims.
 cudaError_t attention_backward_tc2(const AttnProblem& a, cudaStream_t st) {
-    if (a.seq_len % kRowsB != 0) return cudaErrorNotSupported;
     if (a.head_dim == 64) return launch_bwd2<64>(a, st);
+    if (a.head_dim == 80) return launch_bwd2<80>(a, st);
     if (a.head_dim == 128) return launch_bwd2<128>(a, st);
     return cudaErrorNotSupported;
 }

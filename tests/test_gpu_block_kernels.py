@@ -163,6 +163,8 @@ ATTN = [  # (batch, S, H, Hkv, hd, causal)
     (1, 100, 2, 1, 64, 1),      # ragged
     (2, 256, 2, 2, 64, 0),      # bidirectional, whole 128-row blocks (the tcgen05 backward)
     (1, 384, 4, 4, 128, 0),
+    (3, 64, 2, 2, 64, 1),       # one 64-key step per sequence (the dQ pass issues a single S)
+    (2, 65, 4, 4, 80, 0),       # short ragged head_dim 80 (the block tests' ViT-like spec)
 ]
 
 
