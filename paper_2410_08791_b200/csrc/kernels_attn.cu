@@ -676,20 +676,20 @@ bool valid(const AttnProblem& a) {
 
 }  // namespace
 
-// 0 (default): the v2 tcgen05 forward (8 softmax warps, P in TMEM) at head_dim 64 and 80, the
-// v1 (4 softmax warps) at 128 (measured equal there: tools/attn_probe.py); 2: v2 at all three;
-// 3: v1 at 64 / 128, mma.sync at 80; 1: always the mma.sync kernel (A/B knob "attn_fwd"). Backward ("attn_bwd"): 0 (default) the v2 tcgen05
-// passes (kernels_attn_bwd.cu), 2 the v1 tcgen05 passes (kernels_attn_tc.cu), 1 mma.sync.
+// Forward kind (A/B knob "attn_fwd", sp_debug_set): 0 (default) = 4 where a tcgen05 kernel covers the
+// head dim (64, 80, 128); 4: v3 tcgen05 (8 softmax warps, P in TMEM, O accumulated in TMEM with a
+// lazy rescale); 2: v2 (O accumulated in registers, one block behind); 3: v1 (4 softmax warps;
+// head_dim 80 then takes the mma.sync kernel); 1: always the mma.sync kernel.
 int g_attn_fwd_kind = 0;
 int g_attn_bwd_kind = 0;
 
-cudaError_t attention_forward_tc(const AttnProblem& a, cudaStream_t st, bool v2);  // kernels_attn_tc.cu
+cudaError_t attention_forward_tc(const AttnProblem& a, cudaStream_t st, int kind);  // kernels_attn_tc.cu
 
 cudaError_t attention_forward(const AttnProblem& a, cudaStream_t st) {
     if (!valid(a)) return cudaErrorInvalidValue;
     // tcgen05 forward for head_dim 64 / 128 (persistent; tools/attn_probe.py), mma.sync for 80
     if (g_attn_fwd_kind != 1 && (a.head_dim == 64 || a.head_dim == 128 || (a.head_dim == 80 && g_attn_fwd_kind != 3)))
-        return attention_forward_tc(a, st, g_attn_fwd_kind == 2 || (g_attn_fwd_kind == 0 && a.head_dim != 128));
+        return attention_forward_tc(a, st, g_attn_fwd_kind == 0 ? 4 : g_attn_fwd_kind);
     switch (a.head_dim) {
         case 64: return fwd_hd<64>(a, st);
         case 80: return fwd_hd<80>(a, st);

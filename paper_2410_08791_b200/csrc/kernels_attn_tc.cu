@@ -396,11 +396,49 @@ struct Fwd2Cfg {
     static constexpr uint32_t T_O = 256;
 };
 
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+    tmem_st16(taddr, *reinterpret_cast<const uint32_t(*)[16]>(r));
+    tmem_st16(taddr + 16, *reinterpret_cast<const uint32_t(*)[16]>(r + 16));
+}
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&r)[8]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]),
+                 "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+                 : "memory");
+}
+// This lane's NC columns of O (TMEM, from `taddr`) times f, written back (the lazy rescale)
+template <int NC>
+__device__ __forceinline__ void tmem_scale(uint32_t taddr, float f) {
+    if (NC % 32 == 0) {
+        uint32_t v[32];
+#pragma unroll
+        for (int c = 0; c < NC / 32; ++c) {
+            tmem_ld32(taddr + c * 32, v);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * f);
+            tmem_st32(taddr + c * 32, v);
+        }
+    } else {
+        uint32_t v[8];
+#pragma unroll
+        for (int c = 0; c < NC / 8; ++c) {
+            tmem_ld8(taddr + c * 8, v);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * f);
+            tmem_st8(taddr + c * 8, v);
+        }
+    }
+    tmem_st_wait();
+}
+
 __device__ __forceinline__ void named_bar_sync(int id, int threads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 
-template <int HD>
+// LAZY (v3): O accumulates in TMEM across the tile's key blocks (one accumulator per tile
+// parity) and is rescaled in place only when a row's max grows by more than 2^8 over the
+// reference max its P values were computed with (P <= 256 otherwise: exact in fp32, fine in
+// bf16); the softmax warps read O once per tile instead of once per block.
+template <int HD, bool LAZY>
 __global__ void __launch_bounds__(kThreadsF2, 1)
     attn_fwd_tc2_kernel(const __grid_constant__ CUtensorMap tmQK, const __grid_constant__ CUtensorMap tmV,
                         __nv_bfloat16* __restrict__ o, float* __restrict__ lse, TcShape sh, int n_seq) {
@@ -509,10 +547,12 @@ __global__ void __launch_bounds__(kThreadsF2, 1)
                 }
                 umma_commit(&s_full[sb]);
             };
-            auto issue_o = [&](int g) {
+            auto issue_o = [&](int g, int j, int n_kb, int lt) {
                 const int st = g % C::ST, sb = g & 1;
+                const int ob = LAZY ? (lt & 1) : sb;  // LAZY: one O per tile parity
                 mbar_wait(&p_full[sb], (g >> 1) & 1);
-                mbar_wait(&o_empty[sb], ((g >> 1) & 1) ^ 1);
+                if (!LAZY) mbar_wait(&o_empty[ob], ((g >> 1) & 1) ^ 1);
+                else if (j == 0) mbar_wait(&o_empty[ob], ((lt >> 1) & 1) ^ 1);  // tile lt - 2's O read out
                 fence_after();
                 const uint32_t v_base = smem_u32(sV + st * C::KV_BYTES);
 #pragma unroll
@@ -521,9 +561,9 @@ __global__ void __launch_bounds__(kThreadsF2, 1)
                     // columns at 128 sb + 64 half
                     const uint32_t pcol = static_cast<uint32_t>(sb * 128 + (kk / 4) * 64 + (kk % 4) * 8);
                     const uint64_t bd = make_desc(v_base + (kk / 4) * C::ATOMS * 8192 + (kk % 4) * 16 * 128, 8192, 1024);
-                    umma_ts(tmem + C::T_O + sb * HD, tmem + pcol, bd, IDESC_O, kk > 0 ? 1u : 0u);
+                    umma_ts(tmem + C::T_O + ob * HD, tmem + pcol, bd, IDESC_O, (kk > 0 || (LAZY && j > 0)) ? 1u : 0u);
                 }
-                umma_commit(&o_full[sb]);
+                if (!LAZY || j + 1 == n_kb) umma_commit(&o_full[ob]);
                 umma_commit(&pv_done[sb]);
                 umma_commit(&kv_empty[st]);
             };
@@ -539,7 +579,7 @@ __global__ void __launch_bounds__(kThreadsF2, 1)
                 for (int j = 0; j < n_kb; ++j) {
                     if (j + 1 < n_kb) issue_s(g + j + 1, q_base);
                     if (j + 1 == n_kb) umma_commit(&q_empty[qbuf]);
-                    issue_o(g + j);
+                    issue_o(g + j, j, n_kb, lt);
                 }
                 g += n_kb;
             }
@@ -551,17 +591,19 @@ __global__ void __launch_bounds__(kThreadsF2, 1)
         const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
         constexpr int HH = HD / 2;  // output columns of this half
         uint32_t v[32], v2[32];
-        float acc[HH];
-        int g = 0;
-        for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        float acc[LAZY ? 1 : HH];
+        int g = 0, lt = 0;
+        for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++lt) {
             const TileOf w = tile_of(t, sh, n_qb, n_seq);
             const int n_kb = blocks_of(w.qb);
             const int q0 = w.qb * kQ;
             const int qi = q0 + r;
 #pragma unroll
-            for (int i = 0; i < HH; ++i) acc[i] = 0.0f;
+            for (int i = 0; i < (LAZY ? 1 : HH); ++i) acc[i] = 0.0f;
             float m_run = -INFINITY, l_h = 0.0f, corr_prev = 1.0f;
+            const uint32_t o_lazy = tmem + lane_off + C::T_O + (lt & 1) * HD + h * HH;  // LAZY: this half's O
             auto accumulate_o = [&](int gg, float corr) {
+                if (LAZY) return;
                 const int ob = gg & 1;
                 mbar_wait(&o_full[ob], (gg >> 1) & 1);
                 fence_after();
@@ -619,9 +661,27 @@ __global__ void __launch_bounds__(kThreadsF2, 1)
                 named_bar_sync(1 + q4, 64);
                 const float mrow = fmaxf(mraw, xm[(1 - h) * 128 + r]);
                 const float mx = fmaxf(m_run, mrow * sh.scale_log2);
-                const float base = mx == -INFINITY ? 0.0f : mx;
-                const float corr = ex2_fast(m_run - base);
-                m_run = mx;
+                float base, corr = 1.0f;
+                if (!LAZY) {
+                    base = mx == -INFINITY ? 0.0f : mx;
+                    corr = ex2_fast(m_run - base);
+                    m_run = mx;
+                } else if (j == 0) {
+                    m_run = mx;  // the tile's reference max (its first PV overwrites O)
+                    base = mx == -INFINITY ? 0.0f : mx;
+                } else {
+                    // rescale O and l only when the max has grown past 2^8 of the reference
+                    const bool need = mx > (m_run == -INFINITY ? -INFINITY : m_run + 8.0f);
+                    if (__any_sync(0xffffffffu, need)) {
+                        mbar_wait(&pv_done[(g - 1) & 1], ((g - 1) >> 1) & 1);  // PV of block j - 1 done
+                        fence_after();
+                        const float f = need ? ex2_fast(m_run - mx) : 1.0f;  // (-inf reference: 0)
+                        tmem_scale<HH>(o_lazy, f);
+                        l_h *= f;
+                        if (need) m_run = mx;
+                    }
+                    base = m_run == -INFINITY ? 0.0f : m_run;
+                }
                 uint32_t pk[32];
                 float rs[4] = {0.0f, 0.0f, 0.0f, 0.0f};  // four row-sum chains
 #pragma unroll
@@ -656,17 +716,54 @@ __global__ void __launch_bounds__(kThreadsF2, 1)
             xl[h * 128 + r] = l_h;
             named_bar_sync(1 + q4, 64);
             const float l_run = xl[r] + xl[128 + r];
-            if (qi < sh.S) {
-                const float inv = l_run > 0.0f ? 1.0f / l_run : 0.0f;
-                __nv_bfloat16* orow = o + static_cast<int64_t>(w.b * sh.S + qi) * sh.ldo + w.h * HD + h * HH;
+            const float inv = l_run > 0.0f ? 1.0f / l_run : 0.0f;
+            __nv_bfloat16* orow = o + static_cast<int64_t>(w.b * sh.S + qi) * sh.ldo + w.h * HD + h * HH;
+            if (LAZY) {  // the tile's O out of TMEM (once), normalised
+                mbar_wait(&o_full[lt & 1], (lt >> 1) & 1);
+                fence_after();
+                if (HH % 32 == 0) {
 #pragma unroll
-                for (int c = 0; c < HH / 8; ++c) {
-                    uint4 u4;
-                    u4.x = pack_bf16(acc[8 * c + 0] * inv, acc[8 * c + 1] * inv);
-                    u4.y = pack_bf16(acc[8 * c + 2] * inv, acc[8 * c + 3] * inv);
-                    u4.z = pack_bf16(acc[8 * c + 4] * inv, acc[8 * c + 5] * inv);
-                    u4.w = pack_bf16(acc[8 * c + 6] * inv, acc[8 * c + 7] * inv);
-                    reinterpret_cast<uint4*>(orow)[c] = u4;
+                    for (int c = 0; c < HH / 32; ++c) {
+                        tmem_ld32(o_lazy + c * 32, v);
+                        if (qi < sh.S) {
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                uint4 u4;
+                                u4.x = pack_bf16(__uint_as_float(v[8 * u + 0]) * inv, __uint_as_float(v[8 * u + 1]) * inv);
+                                u4.y = pack_bf16(__uint_as_float(v[8 * u + 2]) * inv, __uint_as_float(v[8 * u + 3]) * inv);
+                                u4.z = pack_bf16(__uint_as_float(v[8 * u + 4]) * inv, __uint_as_float(v[8 * u + 5]) * inv);
+                                u4.w = pack_bf16(__uint_as_float(v[8 * u + 6]) * inv, __uint_as_float(v[8 * u + 7]) * inv);
+                                reinterpret_cast<uint4*>(orow + c * 32)[u] = u4;
+                            }
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int c = 0; c < HH / 8; ++c) {
+                        uint32_t v8[8];
+                        tmem_ld8(o_lazy + c * 8, v8);
+                        uint4 u4;
+                        u4.x = pack_bf16(__uint_as_float(v8[0]) * inv, __uint_as_float(v8[1]) * inv);
+                        u4.y = pack_bf16(__uint_as_float(v8[2]) * inv, __uint_as_float(v8[3]) * inv);
+                        u4.z = pack_bf16(__uint_as_float(v8[4]) * inv, __uint_as_float(v8[5]) * inv);
+                        u4.w = pack_bf16(__uint_as_float(v8[6]) * inv, __uint_as_float(v8[7]) * inv);
+                        if (qi < sh.S) reinterpret_cast<uint4*>(orow)[c] = u4;
+                    }
+                }
+                fence_before();
+                mbar_arrive(&o_empty[lt & 1]);
+            }
+            if (qi < sh.S) {
+                if (!LAZY) {
+#pragma unroll
+                    for (int c = 0; c < HH / 8; ++c) {
+                        uint4 u4;
+                        u4.x = pack_bf16(acc[8 * c + 0] * inv, acc[8 * c + 1] * inv);
+                        u4.y = pack_bf16(acc[8 * c + 2] * inv, acc[8 * c + 3] * inv);
+                        u4.z = pack_bf16(acc[8 * c + 4] * inv, acc[8 * c + 5] * inv);
+                        u4.w = pack_bf16(acc[8 * c + 6] * inv, acc[8 * c + 7] * inv);
+                        reinterpret_cast<uint4*>(orow)[c] = u4;
+                    }
                 }
                 if (h == 0)
                     lse[(static_cast<int64_t>(w.b) * sh.H + w.h) * sh.S + qi] =
@@ -683,12 +780,12 @@ __global__ void __launch_bounds__(kThreadsF2, 1)
     }
 }
 
-template <int HD>
+template <int HD, bool LAZY>
 cudaError_t launch_fwd_tc2(const AttnProblem& a, cudaStream_t st) {
     using C = Fwd2Cfg<HD>;
     static bool configured = false;
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(attn_fwd_tc2_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+        cudaError_t e = cudaFuncSetAttribute(attn_fwd_tc2_kernel<HD, LAZY>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
         if (e != cudaSuccess) return e;
         configured = true;
     }
@@ -710,7 +807,7 @@ cudaError_t launch_fwd_tc2(const AttnProblem& a, cudaStream_t st) {
     const int n_seq = static_cast<int>(a.tokens / a.seq_len);
     const int tiles = ((a.seq_len + kQ - 1) / kQ) * a.n_heads * n_seq;
     const int grid = tiles < num_sms() ? tiles : num_sms();
-    attn_fwd_tc2_kernel<HD><<<grid, kThreadsF2, C::SMEM, st>>>(tqk, tv, static_cast<__nv_bfloat16*>(a.o), a.lse, sh,
+    attn_fwd_tc2_kernel<HD, LAZY><<<grid, kThreadsF2, C::SMEM, st>>>(tqk, tv, static_cast<__nv_bfloat16*>(a.o), a.lse, sh,
                                                                 n_seq);
     return cudaGetLastError();
 }
@@ -1281,11 +1378,14 @@ cudaError_t launch_bwd_tc(const AttnProblem& a, cudaStream_t st) {
 
 // The tensor-core forward for head_dim 64 / 128 (the GPT-2 XL and Llama-3 shapes);
 // cudaErrorNotSupported for other head dims (the caller falls back to the mma.sync kernel).
-cudaError_t attention_forward_tc(const AttnProblem& a, cudaStream_t st, bool v2) {
-    if (a.head_dim == 64) return v2 ? launch_fwd_tc2<64>(a, st) : launch_fwd_tc<64>(a, st);
-    if (a.head_dim == 80) return launch_fwd_tc2<80>(a, st);  // (v2 only)
-    if (a.head_dim == 128) return v2 ? launch_fwd_tc2<128>(a, st) : launch_fwd_tc<128>(a, st);
-    return cudaErrorNotSupported;
+cudaError_t attention_forward_tc(const AttnProblem& a, cudaStream_t st, int kind) {
+    // kind: 4 v3 (O in TMEM, lazy rescale), 2 v2 (O in registers), 3 v1 (4 softmax warps)
+    switch (a.head_dim) {
+        case 64: return kind == 4 ? launch_fwd_tc2<64, true>(a, st) : kind == 2 ? launch_fwd_tc2<64, false>(a, st) : launch_fwd_tc<64>(a, st);
+        case 80: return kind == 4 ? launch_fwd_tc2<80, true>(a, st) : launch_fwd_tc2<80, false>(a, st);
+        case 128: return kind == 4 ? launch_fwd_tc2<128, true>(a, st) : kind == 2 ? launch_fwd_tc2<128, false>(a, st) : launch_fwd_tc<128>(a, st);
+        default: return cudaErrorNotSupported;
+    }
 }
 
 }  // namespace sp

@@ -173,12 +173,13 @@ def _split(qkv, B, S, H, Hkv, hd):
     return t[:, :H], t[:, H:H + Hkv], t[:, H + Hkv:]
 
 
-@pytest.mark.parametrize("fwd_kind,bwd_kind", [(2, 0), (3, 2), (1, 1)], ids=["tcgen05", "tcgen05-v1", "mma-sync"])
+@pytest.mark.parametrize("fwd_kind,bwd_kind", [(0, 0), (2, 0), (3, 2), (1, 1)],
+                         ids=["tcgen05", "tcgen05-fwd-v2", "tcgen05-v1", "mma-sync"])
 @pytest.mark.parametrize("B,S,H,Hkv,hd,causal", ATTN)
 def test_attention_forward_and_backward(B, S, H, Hkv, hd, causal, fwd_kind, bwd_kind):
-    # forward kind 2 / 0: the v2 tcgen05 kernel (head dims 64 / 128), 3: the v1 tcgen05 kernel,
-    # 1: mma.sync. Backward kind 0:
-    # the v2 tcgen05 passes (dQ + delta, then dK/dV; whole 128-row sequence blocks), 2: the v1
+    # forward kind 0: the default (v3 tcgen05: O accumulated in TMEM, lazy rescale), 2: v2 (O in
+    # registers), 3: v1 (4 softmax warps), 1: mma.sync. Backward kind 0:
+    # the v2 tcgen05 passes (dQ + delta, then dK/dV; any sequence length), 2: the v1
     # tcgen05 passes, 1: mma.sync; shapes a tcgen05 kind does not cover take the mma.sync kernels
     assert LIB.sp_debug_set(None, b"attn_fwd", fwd_kind) == 0
     assert LIB.sp_debug_set(None, b"attn_bwd", bwd_kind) == 0
