@@ -11,6 +11,9 @@
 // replayed by the planner (reference byte semantics); real HBM use is reported separately.
 #include "executor.hpp"
 
+#include <cstdio>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX3: no-ops unless a tool (nsys) is attached
+
 #include <cuda_bf16.h>
 #include <fcntl.h>
 #include <sys/mman.h>
@@ -1172,8 +1175,20 @@ void Executor::enqueue_call(const Plan& plan, const CallIO& io) {
         CUDA_OK(cudaMemcpyAsync(xin_, io.x, act * (io.train ? 1 : io.n_items), cudaMemcpyHostToDevice, s_comp_));
         if (io.train) CUDA_OK(cudaMemcpyAsync(tgt_, io.t, act, cudaMemcpyHostToDevice, s_comp_));
     }
-    for (size_t i = 0; i < plan.ops.size(); ++i)
+    // NVTX: one range per plan op ("H2D L3 s1", "COMP L3 bwd", ...). With CUDA graphs on they
+    // annotate the capture on the host timeline; with graphs off (sp_debug_set "graphs" 0) nsys
+    // projects them onto the GPU work of each stream (overlap evidence).
+    static const char* kKind[] = {"H2D", "COMP", "D2H", "LOSS", "UPD", "ACT", "GATHER"};
+    char label[64];
+    for (size_t i = 0; i < plan.ops.size(); ++i) {
+        const Op& op = plan.ops[i];
+        const int L = op.layer >= 0 ? op.layer : (op.layers.empty() ? -1 : op.layers[0]);
+        std::snprintf(label, sizeof(label), "%s L%d s%d%s", kKind[static_cast<int>(op.kind)], L,
+                      op.slot >= 0 ? op.slot : (op.slots.empty() ? -1 : op.slots[0]), op.pass == 1 ? " bwd" : "");
+        nvtxRangePushA(label);
         enqueue_op(plan, static_cast<int>(i), io.train, io.n_items, io.rows, io.lr, io.fmt);
+        nvtxRangePop();
+    }
     if (!io.device_io && !io.train) {
         CUDA_OK(cudaEventRecord(ev_io_out_, s_comp_));
         CUDA_OK(cudaStreamWaitEvent(s_d2h_, ev_io_out_, 0));
@@ -1240,6 +1255,10 @@ uint64_t Executor::call_signature(const Plan& plan, const CallIO& io) const {
 
 void Executor::run_call(const Plan& plan, const CallIO& io) {
     launched_ = false;
+    nvtxRangePushA(io.train ? "sp_train_step" : "sp_forward");
+    struct PopRange {
+        ~PopRange() { nvtxRangePop(); }
+    } pop_range;
     try {
         run_call_impl(plan, io);
     } catch (...) {
