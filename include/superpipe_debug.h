@@ -106,6 +106,11 @@ int sp_debug_norm_backward(const float* dy, const float* x, const float* stats, 
  * same scratch (kernels.hpp colsum_total_bf16). */
 int sp_debug_colsum(const void* x, int64_t rows, int32_t n, float* part, int32_t* counters, float* out, void* stream);
 void sp_debug_col_scratch(int64_t rows, int32_t widest, int64_t* part_floats, int64_t* counters);
+/* Debug timeline of the last tcgen05 dK/dV attention pass run with sp_debug_set(NULL,
+ * "attn_trace", 1): CTA 0's events as (event << 56 | step << 40 | SM clock), up to cap; returns
+ * the count (events: 0/1 S issue entered / issued, 2/3 product issue entered / issued, 4/5/6 and
+ * 12/13/14 softmax warpgroup 0 / 1 step entered / S ready / P written). */
+int sp_debug_attn_trace(uint64_t* out, int32_t cap);
 /* The single-pass norm backward (kernels.hpp norm_backward_fused, d % 4 == 0 and d <= 2048, else
  * SP_ERR_INVALID) and its chunk reduction: dres_out / dres_out16 as above (dres_out null: none),
  * out_param[0, d) / [d, 2d) the parameter gradients (null: none) and out_csum[j] = sum over rows

@@ -102,7 +102,7 @@ EXPORTS = [
     "sp_debug_effective_splits",
     "sp_debug_shard_range", "sp_debug_dw_splits", "sp_debug_dw_choice",
     "sp_debug_plan_two_calls", "sp_debug_set", "sp_debug_gemm_ex", "sp_debug_attention",
-    "sp_debug_norm_forward", "sp_debug_norm_backward", "sp_debug_norm_backward_fused", "sp_debug_colsum", "sp_debug_col_scratch",
+    "sp_debug_norm_forward", "sp_debug_norm_backward", "sp_debug_norm_backward_fused", "sp_debug_colsum", "sp_debug_attn_trace", "sp_debug_col_scratch",
     "sp_debug_read_grad",
 ]
 
@@ -176,6 +176,7 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "sp_debug_norm_backward_fused": ([vp, vp, vp, vp, i32, i64, i32, vp, vp, vp, vp, vp, vp, vp, vp],
                                          C.c_int),
         "sp_debug_colsum": ([vp, i64, i32, vp, vp, vp, vp], C.c_int),
+        "sp_debug_attn_trace": ([vp, i32], C.c_int),
         "sp_debug_col_scratch": ([i64, i32, vp, vp], None),
     }
     for name, (args, res) in sig.items():

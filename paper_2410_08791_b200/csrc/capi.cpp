@@ -657,6 +657,13 @@ extern "C" int sp_debug_norm_backward_fused(const float* dy, const float* x, con
     return static_cast<int>(cudaGetLastError());
 }
 
+namespace sp {
+int attn_trace_read(unsigned long long* out, int cap);  // kernels_attn_bwd.cu
+}
+extern "C" int sp_debug_attn_trace(uint64_t* out, int32_t cap) {
+    return sp::attn_trace_read(reinterpret_cast<unsigned long long*>(out), cap);
+}
+
 extern "C" void sp_debug_col_scratch(int64_t rows, int32_t widest, int64_t* part_floats, int64_t* counters) {
     const sp::ColScratchSize s = sp::col_scratch_size(rows, widest);
     *part_floats = static_cast<int64_t>(s.part_floats);

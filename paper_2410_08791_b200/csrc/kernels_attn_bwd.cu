@@ -37,6 +37,7 @@
 #include "tc_ptx.cuh"
 
 namespace sp {
+extern int g_attn_trace;  // sp_debug_set "attn_trace" (defined below)
 namespace {
 using namespace tc;
 
@@ -51,6 +52,21 @@ __device__ __forceinline__ float ex2_approx(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
+}
+
+// Debug timeline of the dK/dV pass (sp_debug_set "attn_trace" 1; tools/attn_trace.py): CTA 0
+// records (event, step, SM clock) for the first kTraceCap events; a separate instantiation, so the
+// product kernel carries none of it.
+constexpr int kTraceCap = 4096;
+__device__ unsigned long long g_bwd_trace[kTraceCap];
+__device__ unsigned int g_bwd_trace_n;
+template <bool TRACE>
+__device__ __forceinline__ void trace_ev(int ev, int step) {
+    if (!TRACE || blockIdx.x != 0) return;
+    const unsigned int i = atomicAdd(&g_bwd_trace_n, 1u);
+    if (i < kTraceCap)
+        g_bwd_trace[i] = (static_cast<unsigned long long>(ev) << 56) | (static_cast<unsigned long long>(step & 0xFFFF) << 40) |
+                         (clock64() & 0xFFFFFFFFFFull);
 }
 
 __device__ __forceinline__ void bulk_load_b(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -244,7 +260,8 @@ __global__ void __launch_bounds__(kThreadsB, 1)
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {  // ===== MMA issuer =====
+        {  // the whole warp runs the loop; the elected lane issues
+            const uint32_t leader = elect_one();  // ===== MMA issuer =====
             constexpr uint32_t ID_S = make_idesc(128, kStepB, false, false);
             constexpr uint32_t ID_D = make_idesc(128, HD, false, true);
             uint64_t dq_, ddo_;  // the tile's Q / dO descriptors (K-major, k step 0)
@@ -259,10 +276,10 @@ __global__ void __launch_bounds__(kThreadsB, 1)
 #pragma unroll
                 for (int kk = 0; kk < HD / 16; ++kk) {
                     const uint32_t ob = (kk / 4) * C::A_BIG + (kk % 4) * 32, sb = (kk / 4) * C::A_SMALL + (kk % 4) * 32;
-                    umma<false>(tmem + 128 * bb, dadd(dq_, ob), dadd(dk, sb), ID_S, kk > 0);
-                    umma<false>(tmem + 128 * bb + 64, dadd(ddo_, ob), dadd(dv, sb), ID_S, kk > 0);
+                    umma_if(leader, tmem + 128 * bb, dadd(dq_, ob), dadd(dk, sb), ID_S, kk > 0);
+                    umma_if(leader, tmem + 128 * bb + 64, dadd(ddo_, ob), dadd(dv, sb), ID_S, kk > 0);
                 }
-                umma_commit(&s_full[bb]);
+                umma_commit_if(leader, &s_full[bb]);
             };
             // dQ += dS K of step gg
             auto issue_d = [&](int gg, bool first) {
@@ -272,10 +289,10 @@ __global__ void __launch_bounds__(kThreadsB, 1)
                 const uint64_t dk = make_desc(smem_u32(sK + st * C::SMALL), C::A_SMALL, 1024);
 #pragma unroll
                 for (int kk = 0; kk < kStepB / 16; ++kk)
-                    umma_ts(tmem + T_ACC, tmem + T_DS + 32 * bb + ts_col<true>(kk), dadd(dk, kk * 2048), ID_D,
+                    umma_ts_if(leader, tmem + T_ACC, tmem + T_DS + 32 * bb + ts_col<true>(kk), dadd(dk, kk * 2048), ID_D,
                             (!first || kk > 0) ? 1u : 0u);
-                umma_commit(&ds_free[bb]);
-                umma_commit(&kv_empty[st]);
+                umma_commit_if(leader, &ds_free[bb]);
+                umma_commit_if(leader, &kv_empty[st]);
             };
             int g = 0, lt = 0;
             for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++lt) {
@@ -296,8 +313,8 @@ __global__ void __launch_bounds__(kThreadsB, 1)
                     issue_d(g + j, j == 0);
                     if (j + 2 < n) issue_s(g + j + 2);
                 }
-                umma_commit(acc_full);
-                umma_commit(&q_empty[ob]);
+                umma_commit_if(leader, acc_full);
+                umma_commit_if(leader, &q_empty[ob]);
                 g += n;
             }
         }
@@ -408,7 +425,7 @@ __global__ void __launch_bounds__(kThreadsB, 1)
 // ------------------------------------------------------------------------------------------
 // dK, dV
 // ------------------------------------------------------------------------------------------
-template <int HD, bool SEP, int NB>
+template <int HD, bool SEP, int NB, bool TRACE = false>
 __global__ void __launch_bounds__(kThreadsB, 1)
     attn_bwd_dkdv2_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmQ,
                           const __grid_constant__ CUtensorMap tmDO, const float* __restrict__ lse,
@@ -537,39 +554,44 @@ __global__ void __launch_bounds__(kThreadsB, 1)
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {  // ===== MMA issuer =====
+        {  // the whole warp runs the loop; the elected lane issues
+            const uint32_t leader = elect_one();  // ===== MMA issuer =====
             constexpr uint32_t ID_S = make_idesc(128, kStepB, false, false);
             constexpr uint32_t ID_D = make_idesc(128, HD, false, true);
             uint64_t dk_, dv_;  // the tile's K / V descriptors (K-major, k step 0)
             auto issue_s = [&](int gg) {
                 const int st = gg % C::ST, bb = gg % NB;
+                if (leader) trace_ev<TRACE>(0, gg);
                 mbar_wait(&q_full[st], (gg / C::ST) & 1);
                 if (SEP && gg >= 2) mbar_wait(&s_free[bb], ((gg - 2) >> 1) & 1);
                 fence_after();
+                if (leader) trace_ev<TRACE>(1, gg);
                 const uint64_t dq = make_desc(smem_u32(sQ + st * C::SMALL), 16, 1024);
                 const uint64_t ddo = make_desc(smem_u32(sDO + st * C::SMALL), 16, 1024);
 #pragma unroll
                 for (int kk = 0; kk < HD / 16; ++kk) {
                     const uint32_t ob = (kk / 4) * C::A_BIG + (kk % 4) * 32, sb = (kk / 4) * C::A_SMALL + (kk % 4) * 32;
-                    umma<false>(tmem + 128 * bb, dadd(dk_, ob), dadd(dq, sb), ID_S, kk > 0);
-                    umma<false>(tmem + 128 * bb + 64, dadd(dv_, ob), dadd(ddo, sb), ID_S, kk > 0);
+                    umma_if(leader, tmem + 128 * bb, dadd(dk_, ob), dadd(dq, sb), ID_S, kk > 0);
+                    umma_if(leader, tmem + 128 * bb + 64, dadd(dv_, ob), dadd(ddo, sb), ID_S, kk > 0);
                 }
-                umma_commit(&s_full[bb]);
+                umma_commit_if(leader, &s_full[bb]);
             };
             auto issue_d = [&](int gg, bool first) {
                 const int st = gg % C::ST, bb = gg % NB;
+                if (leader) trace_ev<TRACE>(2, gg);
                 mbar_wait(&p_full[bb], (gg / NB) & 1);
                 fence_after();
+                if (leader) trace_ev<TRACE>(3, gg);
                 const uint64_t dq = make_desc(smem_u32(sQ + st * C::SMALL), C::A_SMALL, 1024);
                 const uint64_t ddo = make_desc(smem_u32(sDO + st * C::SMALL), C::A_SMALL, 1024);
 #pragma unroll
                 for (int kk = 0; kk < kStepB / 16; ++kk) {
                     const uint32_t acc = (!first || kk > 0) ? 1u : 0u;
-                    umma_ts(tmem + T_ACC, tmem + ds_col(bb) + ts_col<SEP>(kk), dadd(dq, kk * 2048), ID_D, acc);
-                    umma_ts(tmem + T_ACC + HD, tmem + p_col(bb) + ts_col<SEP>(kk), dadd(ddo, kk * 2048), ID_D, acc);
+                    umma_ts_if(leader, tmem + T_ACC, tmem + ds_col(bb) + ts_col<SEP>(kk), dadd(dq, kk * 2048), ID_D, acc);
+                    umma_ts_if(leader, tmem + T_ACC + HD, tmem + p_col(bb) + ts_col<SEP>(kk), dadd(ddo, kk * 2048), ID_D, acc);
                 }
-                if (SEP) umma_commit(&ds_free[bb]);
-                umma_commit(&q_empty[st]);
+                if (SEP) umma_commit_if(leader, &ds_free[bb]);
+                umma_commit_if(leader, &q_empty[st]);
             };
             int g = 0, lt = 0;
             for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++lt) {
@@ -590,8 +612,8 @@ __global__ void __launch_bounds__(kThreadsB, 1)
                     issue_d(g + j, j == 0);
                     if (!SEP && j + NB < n) issue_s(g + j + NB);  // (in order after the product)
                 }
-                umma_commit(acc_full);
-                umma_commit(&kv_empty[ob]);
+                umma_commit_if(leader, acc_full);
+                umma_commit_if(leader, &kv_empty[ob]);
                 g += n;
             }
         }
@@ -615,9 +637,11 @@ __global__ void __launch_bounds__(kThreadsB, 1)
             for (int j = 0; j < n; ++j, ++g, (++qs == n_qs ? (qs = qs0, ++hq) : 0)) {
                 if ((g & 1) != wg) continue;  // the other warpgroup's step
                 const int st = g % C::ST, bb = g % NB;
+                if (TRACE && q4 == 0 && lane == 0) trace_ev<TRACE>(4 + 8 * wg, g);
                 if (SEP && g >= 2) mbar_wait(&ds_free[bb], ((g - 2) >> 1) & 1);  // step g - 2's products
                 mbar_wait(&s_full[bb], (g / NB) & 1);                              // read this P / dS buffer
                 fence_after();
+                if (TRACE && q4 == 0 && lane == 0) trace_ev<TRACE>(5 + 8 * wg, g);
                 // a step's lse / delta start on a 16-byte boundary unless the sequence length is
                 // not a multiple of 4 (ViT's 257): two instantiations of the step body
                 auto step_body = [&](auto aligned_tag) {
@@ -682,6 +706,7 @@ __global__ void __launch_bounds__(kThreadsB, 1)
                 tmem_st_wait();
                 fence_before();
                 mbar_arrive(&p_full[bb]);
+                if (TRACE && q4 == 0 && lane == 0) trace_ev<TRACE>(6 + 8 * wg, g);
             }
             // the tile's dK (half 0, with the softmax scale) or dV (half 1) out of TMEM
             mbar_wait(acc_full, lt & 1);
@@ -744,6 +769,19 @@ cudaError_t launch_bwd2(const AttnProblem& a, cudaStream_t st) {
         a.delta, dq, sh, n_seq);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
+    if (g_attn_trace) {  // debug timeline (tools/attn_trace.py)
+        static bool configured_t = false;
+        if (!configured_t) {
+            cudaFuncSetAttribute(attn_bwd_dkdv2_kernel<HD, SEP, C::NB_DKDV, true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_DKDV);
+            configured_t = true;
+        }
+        const unsigned int zero = 0;
+        cudaMemcpyToSymbolAsync(g_bwd_trace_n, &zero, sizeof(zero), 0, cudaMemcpyHostToDevice, st);
+        attn_bwd_dkdv2_kernel<HD, SEP, C::NB_DKDV, true><<<kv_tiles < num_sms() ? kv_tiles : num_sms(), kThreadsB,
+                                                          C::SMEM_DKDV, st>>>(t128, t64, do64, a.lse, a.delta, dq, sh, n_seq);
+        return cudaGetLastError();
+    }
     attn_bwd_dkdv2_kernel<HD, SEP, C::NB_DKDV><<<kv_tiles < num_sms() ? kv_tiles : num_sms(), kThreadsB, C::SMEM_DKDV, st>>>(
         t128, t64, do64, a.lse, a.delta, dq, sh, n_seq);
     return cudaGetLastError();
@@ -752,6 +790,16 @@ cudaError_t launch_bwd2(const AttnProblem& a, cudaStream_t st) {
 
 // The backward for head_dim 64 / 80 / 128, any sequence length; delta is formed inside (no
 // separate kernel). cudaErrorNotSupported for other head dims.
+int g_attn_trace = 0;
+int attn_trace_read(unsigned long long* out, int cap) {
+    unsigned int n = 0;
+    if (cudaMemcpyFromSymbol(&n, g_bwd_trace_n, sizeof(n)) != cudaSuccess) return -1;
+    const int m = static_cast<int>(n < static_cast<unsigned>(kTraceCap) ? n : kTraceCap);
+    const int k = m < cap ? m : cap;
+    if (k > 0 && cudaMemcpyFromSymbol(out, g_bwd_trace, k * sizeof(unsigned long long)) != cudaSuccess) return -1;
+    return k;
+}
+
 cudaError_t attention_backward_tc2(const AttnProblem& a, cudaStream_t st) {
     if (a.head_dim == 64) return launch_bwd2<64>(a, st);
     if (a.head_dim == 80) return launch_bwd2<80>(a, st);

@@ -174,7 +174,8 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
+        {  // the whole warp runs the loop; the elected lane issues
+            const uint32_t leader = elect_one();
             // ===== MMA issuer =====
             constexpr uint32_t IDESC_S = make_idesc(kQ, kKV, false, false);
             constexpr uint32_t IDESC_O = make_idesc(kQ, HD, false, true);
@@ -189,9 +190,9 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
                     const int a = kk / 4, w = kk % 4;  // atom, 32-byte step within the atom
                     const uint64_t ad = make_desc(q_base + a * kQ * 128 + w * 32, 16, 1024);
                     const uint64_t bd = make_desc(k_base + a * kKV * 128 + w * 32, 16, 1024);
-                    umma<false>(tmem + sb * kKV, ad, bd, IDESC_S, kk > 0 ? 1u : 0u);
+                    umma_if(leader, tmem + sb * kKV, ad, bd, IDESC_S, kk > 0 ? 1u : 0u);
                 }
-                umma_commit(&s_full[sb]);
+                umma_commit_if(leader, &s_full[sb]);
             };
             auto issue_o = [&](int g) {
                 const int st = g % kStages, ob = g & 1, pb = g % C::P_BUFS;
@@ -206,11 +207,11 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
                     const uint64_t ad = make_desc(p_base + a * kQ * 128 + w * 32, 16, 1024);
                     // N-major V: k-block a (64 keys), 16-key step w; atoms of 64 d at 8 KB stride
                     const uint64_t bd = make_desc(v_base + a * C::ATOMS * 8192 + w * 16 * 128, 8192, 1024);
-                    umma<false>(tmem + C::O_COL0 + ob * HD, ad, bd, IDESC_O, kk > 0 ? 1u : 0u);
+                    umma_if(leader, tmem + C::O_COL0 + ob * HD, ad, bd, IDESC_O, kk > 0 ? 1u : 0u);
                 }
-                umma_commit(&o_full[ob]);
-                umma_commit(&p_empty[pb]);
-                umma_commit(&kv_empty[st]);  // both MMAs of block g are done with K_g, V_g
+                umma_commit_if(leader, &o_full[ob]);
+                umma_commit_if(leader, &p_empty[pb]);
+                umma_commit_if(leader, &kv_empty[st]);  // both MMAs of block g are done with K_g, V_g
             };
             int g = 0, lt = 0;
             for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++lt) {
@@ -223,7 +224,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
                 issue_s(g, q_base);
                 for (int j = 0; j < n_kb; ++j) {
                     if (j + 1 < n_kb) issue_s(g + j + 1, q_base);
-                    if (j + 1 == n_kb) umma_commit(&q_empty[qbuf]);  // every S MMA of the tile issued
+                    if (j + 1 == n_kb) umma_commit_if(leader, &q_empty[qbuf]);  // every S MMA of the tile issued
                     issue_o(g + j);
                 }
                 g += n_kb;
@@ -528,7 +529,8 @@ __global__ void __launch_bounds__(kThreadsF2, 1)
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
+        {  // the whole warp runs the loop; the elected lane issues
+            const uint32_t leader = elect_one();
             // ===== MMA issuer =====
             constexpr uint32_t IDESC_S = make_idesc(kQ, kKV, false, false);
             constexpr uint32_t IDESC_O = make_idesc(kQ, HD, false, true);
@@ -543,9 +545,9 @@ __global__ void __launch_bounds__(kThreadsF2, 1)
                     const int a = kk / 4, w = kk % 4;
                     const uint64_t ad = make_desc(q_base + a * kQ * 128 + w * 32, 16, 1024);
                     const uint64_t bd = make_desc(k_base + a * kKV * 128 + w * 32, 16, 1024);
-                    umma<false>(tmem + sb * 128, ad, bd, IDESC_S, kk > 0 ? 1u : 0u);
+                    umma_if(leader, tmem + sb * 128, ad, bd, IDESC_S, kk > 0 ? 1u : 0u);
                 }
-                umma_commit(&s_full[sb]);
+                umma_commit_if(leader, &s_full[sb]);
             };
             auto issue_o = [&](int g, int j, int n_kb, int lt) {
                 const int st = g % C::ST, sb = g & 1;
@@ -561,11 +563,11 @@ __global__ void __launch_bounds__(kThreadsF2, 1)
                     // columns at 128 sb + 64 half
                     const uint32_t pcol = static_cast<uint32_t>(sb * 128 + (kk / 4) * 64 + (kk % 4) * 8);
                     const uint64_t bd = make_desc(v_base + (kk / 4) * C::ATOMS * 8192 + (kk % 4) * 16 * 128, 8192, 1024);
-                    umma_ts(tmem + C::T_O + ob * HD, tmem + pcol, bd, IDESC_O, (kk > 0 || (LAZY && j > 0)) ? 1u : 0u);
+                    umma_ts_if(leader, tmem + C::T_O + ob * HD, tmem + pcol, bd, IDESC_O, (kk > 0 || (LAZY && j > 0)) ? 1u : 0u);
                 }
-                if (!LAZY || j + 1 == n_kb) umma_commit(&o_full[ob]);
-                umma_commit(&pv_done[sb]);
-                umma_commit(&kv_empty[st]);
+                if (!LAZY || j + 1 == n_kb) umma_commit_if(leader, &o_full[ob]);
+                umma_commit_if(leader, &pv_done[sb]);
+                umma_commit_if(leader, &kv_empty[st]);
             };
             int g = 0, lt = 0;
             for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++lt) {
@@ -578,7 +580,7 @@ __global__ void __launch_bounds__(kThreadsF2, 1)
                 issue_s(g, q_base);
                 for (int j = 0; j < n_kb; ++j) {
                     if (j + 1 < n_kb) issue_s(g + j + 1, q_base);
-                    if (j + 1 == n_kb) umma_commit(&q_empty[qbuf]);
+                    if (j + 1 == n_kb) umma_commit_if(leader, &q_empty[qbuf]);
                     issue_o(g + j, j, n_kb, lt);
                 }
                 g += n_kb;

@@ -584,6 +584,20 @@ struct TileEpilogue {
     }
 };
 
+template <bool TF32>
+__device__ __forceinline__ void umma1_if(uint32_t leader, uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                         uint32_t idesc, uint32_t accumulate) {
+    if (TF32)
+        asm volatile(
+            "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 e, %5, 0;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+            "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(leader));
+    else
+        asm volatile(
+            "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 e, %5, 0;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+            "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(leader));
+}
 // ---------------------------------------------------------------------------------------
 // the kernel (1-CTA: M = 128 per MMA)
 // ---------------------------------------------------------------------------------------
@@ -686,8 +700,9 @@ __global__ void __launch_bounds__(EpiSmem<EPI>::THREADS, 1)
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
-            // ===== MMA issuer (single thread) =====
+        {
+            // ===== MMA issuer: the whole warp runs the loop, the elected lane issues =====
+            const uint32_t leader = elect_one();
             int stage = 0;
             uint32_t phase = 0;
             int acc = 0;
@@ -712,15 +727,15 @@ __global__ void __launch_bounds__(EpiSmem<EPI>::THREADS, 1)
                                                  : make_desc(a_base + kk * 32, 16, 1024);
                         const uint64_t bd = B_MN ? make_desc(b_base + kk * O::KSTEP * 128, O::ATOM_BYTES, O::MN_SBO, O::MN_LAYOUT)
                                                  : make_desc(b_base + kk * 32, 16, 1024);
-                        umma<O::TF32>(d_tmem, ad, bd, IDESC, (kb > kb0 || kk > 0) ? 1u : 0u);
+                        umma1_if<O::TF32>(leader, d_tmem, ad, bd, IDESC, (kb > kb0 || kk > 0) ? 1u : 0u);
                     }
-                    umma_commit(&empty[stage]);  // frees the smem stage when these MMAs finish
+                    umma_commit_if(leader, &empty[stage]);  // frees the smem stage when these MMAs finish
                     if (++stage == STAGES) {
                         stage = 0;
                         phase ^= 1;
                     }
                 }
-                umma_commit(&tfull[acc]);  // accumulator ready for the epilogue
+                umma_commit_if(leader, &tfull[acc]);  // accumulator ready for the epilogue
                 acc ^= 1;
                 if (acc == 0) acc_phase ^= 1;
             }
@@ -793,6 +808,30 @@ __device__ __forceinline__ void tma_load_2d_pair(const CUtensorMap* map, uint64_
         "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes "
         "[%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
         "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_addr), "r"(c0), "r"(c1)
+        : "memory");
+}
+// Predicated forms for a warp-uniform issuer (only `leader`, from elect.sync, executes them).
+template <bool TF32>
+__device__ __forceinline__ void umma2_if(uint32_t leader, uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                         uint32_t idesc, uint32_t accumulate) {
+    if (TF32)
+        asm volatile(
+            "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 e, %5, 0;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+            "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(leader));
+    else
+        asm volatile(
+            "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 e, %5, 0;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+            "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(leader));
+}
+__device__ __forceinline__ void umma2_commit_both_if(uint32_t leader, uint64_t* bar) {
+    const uint16_t mask = 0x3;
+    asm volatile(
+        "{\n\t.reg .pred e;\n\tsetp.ne.b32 e, %2, 0;\n\t"
+        "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(
+            smem_u32(bar)),
+        "h"(mask), "r"(leader)
         : "memory");
 }
 template <bool TF32>
@@ -980,8 +1019,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiSmem<EPI>::THREAD
             }
         }
     } else if (warp == 1) {
-        if (lane == 0 && leader) {
-            // ===== MMA issuer: one thread of the leader CTA drives both SMs' tensor cores =====
+        if (leader) {
+            // ===== MMA issuer: the leader CTA's warp runs the loop, its elected lane drives both SMs' tensor cores =====
+            const uint32_t elect = elect_one();
             int stage = 0;
             uint32_t phase = 0;
             int acc = 0;
@@ -1007,15 +1047,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiSmem<EPI>::THREAD
                                                  : make_desc(a_base + kk * 32, 16, 1024);
                         const uint64_t bd = B_MN ? make_desc(b_base + kk * O::KSTEP * 128, O::ATOM_BYTES, O::MN_SBO, O::MN_LAYOUT)
                                                  : make_desc(b_base + kk * 32, 16, 1024);
-                        umma2<O::TF32>(d_tmem, ad, bd, idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
+                        umma2_if<O::TF32>(elect, d_tmem, ad, bd, idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
                     }
-                    umma2_commit_both(&empty[stage]);  // frees the stage in BOTH CTAs
+                    umma2_commit_both_if(elect, &empty[stage]);  // frees the stage in BOTH CTAs
                     if (++stage == STAGES) {
                         stage = 0;
                         phase ^= 1;
                     }
                 }
-                umma2_commit_both(&tfull[acc]);  // both CTAs' accumulators are ready
+                umma2_commit_both_if(elect, &tfull[acc]);  // both CTAs' accumulators are ready
                 acc ^= 1;
                 if (acc == 0) acc_phase ^= 1;
             }
@@ -1228,7 +1268,8 @@ bool use_tma_epilogue(const GemmProblem& g, int splits) {
 // for the activation GEMMs they were neutral warm and, being scheduled last, re-read every A
 // panel after it has left L2 (82 vs 58 MB DRAM reads per forward launch at 16384 x 1600).
 bool narrow_tiles(int epi_base, int bn, int last_cols) {
-    if (g_narrow == 1)  // every epilogue (A/B measurement only) return epi_base != EPI_SGD_F32 && bn == 256 && last_cols <= 128;
+    if (g_narrow == 1)  // every epilogue (A/B measurement only)
+        return epi_base != EPI_SGD_F32 && bn == 256 && last_cols <= 128;
     return epi_base == EPI_F32 && bn == 256 && last_cols <= 128;
 }
 
@@ -1417,12 +1458,14 @@ cudaError_t dispatch2_bn_kmajor(const GemmProblem& g, cudaStream_t st) {
 
 extern int g_attn_fwd_kind;  // kernels_attn.cu
 extern int g_attn_bwd_kind;
+extern int g_attn_trace;
 
 void set_gemm_debug(const char* key, int value, bool* known) {
     *known = true;
     if (std::strcmp(key, "epi_mode") == 0) tc::g_epi_mode = value;
     else if (std::strcmp(key, "attn_fwd") == 0) g_attn_fwd_kind = value;
     else if (std::strcmp(key, "attn_bwd") == 0) g_attn_bwd_kind = value;
+    else if (std::strcmp(key, "attn_trace") == 0) g_attn_trace = value;
     else if (std::strcmp(key, "narrow") == 0) tc::g_narrow = value;
     else *known = false;
 }
