@@ -41,8 +41,8 @@ METRIC = "samples/sec vs peak HBM GB at window k; % of max(FLOP, host-link bytes
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=10)
-    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--steps", type=int, default=15)
+    p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--model", default="gpt2-xl", choices=["gpt2-xl", "vit-h14", "llama3-8b", "llama3-70b", "dense"],
                    help="named-shape transformer layers (SURVEY 8(d)) or round 1's square stand-in")

@@ -877,7 +877,7 @@ void Executor::loss_op(int64_t rows) {
     // on the D2H copy engine behind the write-backs and stall this stream until they drain)
 }
 
-bool Executor::update_op(const Op& op, float lr) {
+bool Executor::update_op(const Op& op, float lr, bool keep_slot) {
     const int L = op.layer, s = op.slot;
     const size_t dd = static_cast<size_t>(d_) * d_;
     cudaStream_t st = s_upd_;
@@ -955,6 +955,7 @@ bool Executor::update_op(const Op& op, float lr) {
         }
         if (op.stage >= 0) {  // also into the write-back stage (same layout): no staging copy
             r.stage_delta = static_cast<int64_t>(stage_ptr(op.stage) - slot_ptr(s));
+            r.stage_only = !keep_slot;  // (the slot is not read again: skip its half of the writes)
             staged = true;
         }
         split_update(r, g, adamw() ? slot_m32(s) : nullptr, adamw() ? slot_v32(s) : nullptr, lr, adamw() ? 1 : 0,
@@ -1071,7 +1072,14 @@ void Executor::enqueue_op(const Plan& plan, int i, bool train, int n_items, int6
             loss_op(rows);
             break;
         case OpKind::Update:
-            if (update_op(op, lr)) break;  // the update filled the stage itself
+            {
+                const SlotCache& fin = plan.final_slots[static_cast<size_t>(op.slot)];
+                if (update_op(op, lr, fin.valid && fin.layer == op.layer)) {
+                    // the slot kept the pre-update values: it must not count as this layer's
+                    // current weights (the plan already leaves it invalid or another layer's)
+                    break;
+                }
+            }
             if (op.stage >= 0) {  // copy the updated image [+ m, v] out: the slot is free now
                 size_t lo = 0, hi = layer_bytes();
                 if (sharded_) shard_range(shardA_, layer_bytes(), lo, hi);

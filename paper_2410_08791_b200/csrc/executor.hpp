@@ -142,7 +142,9 @@ private:
                     int fmt);
     void compute_op(const Op& op, bool train, int64_t rows, int fmt);
     void loss_op(int64_t rows);
-    bool update_op(const Op& op, float lr);  // true: it also filled the op's write-back stage
+    // true: it also filled the op's write-back stage; keep_slot: the plan leaves the layer valid
+    // in its slot at the end of the call (the slot must hold the update too)
+    bool update_op(const Op& op, float lr, bool keep_slot = true);
     void collect_stats(const Plan& plan, int n_items, bool train);
     void gemm(const struct GemmProblem& g, cudaStream_t st);
     // transformer blocks (block_exec.cpp)

@@ -162,6 +162,9 @@ struct SplitRegions {
     // stage_delta bytes (the write-back stage, which has the slot's layout), so no separate
     // staging copy re-reads the slot
     int64_t stage_delta = 0;
+    // with a stage: the slot itself keeps the old values (nothing reads it again: the plan does
+    // not leave the layer valid in that slot), only the stage receives the update
+    bool stage_only = false;
 };
 void split_update(const SplitRegions& r, const float* g, float* m, float* v, float lr, int opt,
                   const AdamwScalars* scalars, cudaStream_t st);

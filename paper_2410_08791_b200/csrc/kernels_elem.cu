@@ -526,8 +526,10 @@ __global__ void split_update_kernel(SplitRegions r, const float* __restrict__ g,
             load8(v + base + e, vv);
 #pragma unroll
             for (int k = 0; k < 8; ++k) adamw_elem(w[k], mm[k], vv[k], gr[k], s);
-            store8(m + base + e, mm);
-            store8(v + base + e, vv);
+            if (!r.stage_only) {
+                store8(m + base + e, mm);
+                store8(v + base + e, vv);
+            }
             if (r.stage_delta) {
                 store8(shifted(m + base + e, r.stage_delta), mm);
                 store8(shifted(v + base + e, r.stage_delta), vv);
@@ -545,14 +547,16 @@ __global__ void split_update_kernel(SplitRegions r, const float* __restrict__ g,
                 l4[k] = (b0 & 0xFFFFu) | (b1 << 16);
             }
             const uint4 hv = make_uint4(h4[0], h4[1], h4[2], h4[3]), lv = make_uint4(l4[0], l4[1], l4[2], l4[3]);
-            *reinterpret_cast<uint4*>(static_cast<uint16_t*>(r.hi[i]) + e) = hv;
-            *reinterpret_cast<uint4*>(r.lo[i] + e) = lv;
+            if (!r.stage_only) {
+                *reinterpret_cast<uint4*>(static_cast<uint16_t*>(r.hi[i]) + e) = hv;
+                *reinterpret_cast<uint4*>(r.lo[i] + e) = lv;
+            }
             if (r.stage_delta) {
                 *shifted(reinterpret_cast<uint4*>(static_cast<uint16_t*>(r.hi[i]) + e), r.stage_delta) = hv;
                 *shifted(reinterpret_cast<uint4*>(r.lo[i] + e), r.stage_delta) = lv;
             }
         } else {
-            store8(static_cast<float*>(r.hi[i]) + e, w);
+            if (!r.stage_only) store8(static_cast<float*>(r.hi[i]) + e, w);
             if (r.stage_delta) store8(shifted(static_cast<float*>(r.hi[i]) + e, r.stage_delta), w);
         }
     }
