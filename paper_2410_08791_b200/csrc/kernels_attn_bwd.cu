@@ -390,13 +390,17 @@ __global__ void __launch_bounds__(kThreadsB, 1)
                     uint32_t dd[16];
 #pragma unroll
                     for (int i = 0; i < 16; ++i) {
-                        float p0 = ex2_approx(fmaf(__uint_as_float(vs[2 * i]), sh.scale_log2, -L));
-                        float p1 = ex2_approx(fmaf(__uint_as_float(vs[2 * i + 1]), sh.scale_log2, -L));
+                        const float2 x = ffma2(make_float2(__uint_as_float(vs[2 * i]), __uint_as_float(vs[2 * i + 1])),
+                                               make_float2(sh.scale_log2, sh.scale_log2), make_float2(-L, -L));
+                        float p0 = ex2_approx(x.x), p1 = ex2_approx(x.y);
                         if (mask) {
                             if (k0 + 2 * i >= klim) p0 = 0.0f;
                             if (k0 + 2 * i + 1 >= klim) p1 = 0.0f;
                         }
-                        dd[i] = pack_bf16(p0 * (__uint_as_float(vp[2 * i]) - Dl), p1 * (__uint_as_float(vp[2 * i + 1]) - Dl));
+                        const float2 d = fmul2(make_float2(p0, p1),
+                                               fsub2(make_float2(__uint_as_float(vp[2 * i]), __uint_as_float(vp[2 * i + 1])),
+                                                     make_float2(Dl, Dl)));
+                        dd[i] = pack_bf16(d.x, d.y);
                     }
                     tmem_st16(tmem + lane_off + T_DS + 32 * bb + 16 * h, dd);
                 }
@@ -681,10 +685,14 @@ __global__ void __launch_bounds__(kThreadsB, 1)
 #pragma unroll
                             for (int u = 0; u < 2; ++u) {
                                 const int i = 2 * i4 + u;  // query pair (2 i, 2 i + 1)
-                                float p0 = ex2_approx(fmaf(__uint_as_float(vs[2 * i]), sh.scale_log2, -lv[2 * u]));
-                                float p1 = ex2_approx(fmaf(__uint_as_float(vs[2 * i + 1]), sh.scale_log2, -lv[2 * u + 1]));
-                                float d0 = p0 * (__uint_as_float(vp[2 * i]) - dv[2 * u]);
-                                float d1 = p1 * (__uint_as_float(vp[2 * i + 1]) - dv[2 * u + 1]);
+                                const float2 x = ffma2(make_float2(__uint_as_float(vs[2 * i]), __uint_as_float(vs[2 * i + 1])),
+                                                       make_float2(sh.scale_log2, sh.scale_log2),
+                                                       make_float2(-lv[2 * u], -lv[2 * u + 1]));
+                                float p0 = ex2_approx(x.x), p1 = ex2_approx(x.y);
+                                const float2 dd2 = fmul2(make_float2(p0, p1),
+                                                         fsub2(make_float2(__uint_as_float(vp[2 * i]), __uint_as_float(vp[2 * i + 1])),
+                                                               make_float2(dv[2 * u], dv[2 * u + 1])));
+                                float d0 = dd2.x, d1 = dd2.y;
                                 if (mask) {
                                     const int qa = q0 + 2 * i;
                                     if (qa < qlo || qa >= sh.S) p0 = 0.0f, d0 = 0.0f;

@@ -688,10 +688,11 @@ __global__ void __launch_bounds__(kThreadsF2, 1)
                 float rs[4] = {0.0f, 0.0f, 0.0f, 0.0f};  // four row-sum chains
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
-                    float p0 = ex2_fast(fmaf(__uint_as_float(v[2 * i]), sh.scale_log2, -base));
-                    float p1 = ex2_fast(fmaf(__uint_as_float(v[2 * i + 1]), sh.scale_log2, -base));
-                    float p2 = ex2_fast(fmaf(__uint_as_float(v2[2 * i]), sh.scale_log2, -base));
-                    float p3 = ex2_fast(fmaf(__uint_as_float(v2[2 * i + 1]), sh.scale_log2, -base));
+                    const float2 x01 = ffma2(make_float2(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1])),
+                                             make_float2(sh.scale_log2, sh.scale_log2), make_float2(-base, -base));
+                    const float2 x23 = ffma2(make_float2(__uint_as_float(v2[2 * i]), __uint_as_float(v2[2 * i + 1])),
+                                             make_float2(sh.scale_log2, sh.scale_log2), make_float2(-base, -base));
+                    float p0 = ex2_fast(x01.x), p1 = ex2_fast(x01.y), p2 = ex2_fast(x23.x), p3 = ex2_fast(x23.y);
                     if (need_mask) {
                         if (2 * i >= lim) p0 = 0.0f;
                         if (2 * i + 1 >= lim) p1 = 0.0f;
