@@ -84,6 +84,7 @@ typedef struct {
     void* aux;
     int32_t ldaux, act;
     void* stream;
+    float* colsum_part; /* EPI_GELU_GATE_BF16, one split: [ceil(M / 32)][N] column partials (or NULL) */
 } sp_debug_gemm_args;
 int sp_debug_gemm_ex(const sp_debug_gemm_args* a);
 /* The attention core of the transformer blocks (kernels.hpp AttnProblem), device pointers,

@@ -81,7 +81,7 @@ class GemmArgs(C.Structure):
                 ("b_mn", C.c_int32), ("epilogue", C.c_int32), ("out", C.c_void_p), ("ldo", C.c_int32),
                 ("bias", C.c_void_p), ("relu", C.c_int32), ("gate", C.c_void_p), ("ldg", C.c_int32),
                 ("splits", C.c_int32), ("block_n", C.c_int32), ("cta", C.c_int32), ("aux", C.c_void_p),
-                ("ldaux", C.c_int32), ("act", C.c_int32), ("stream", C.c_void_p)]
+                ("ldaux", C.c_int32), ("act", C.c_int32), ("stream", C.c_void_p), ("colsum_part", C.c_void_p)]
 
 
 # Every symbol include/superpipe.h and include/superpipe_debug.h declare (checked by the

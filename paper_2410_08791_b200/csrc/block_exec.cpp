@@ -127,6 +127,9 @@ void Executor::block_alloc(int64_t R, int items, bool train, const std::function
     bcs_.part = static_cast<float*>(alloc(cs.part_floats * 4));
     bcs_.counters = static_cast<int*>(alloc(cs.counters * 4));
     CUDA_OK(cudaMemset(bcs_.counters, 0, cs.counters * 4));  // each kernel leaves them zero
+    // b1's gradient: column sums of dh, formed in the GELU' GEMM's epilogue per 32-row group
+    if (!lay_.swiglu() && lay_.b1 >= 0)
+        bb1p_ = static_cast<float*>(alloc(static_cast<size_t>((R + 31) / 32) * static_cast<size_t>(lay_.desc.ff) * 4));
     fused_norm_ = norm_backward_fused_ok(d_);
     if (fused_norm_) {
         const size_t nc = static_cast<size_t>(norm_bwd_chunks(R));
@@ -366,10 +369,24 @@ void Executor::block_backward_layer(int L, const WirePtrs& w, const float* x, co
     g.act = lay_.gelu_kind();
     g.out = bdbig_;  // dh
     g.ldo = ff;
+    const bool b1_fused = trainable && lay_.b1 >= 0 && bb1p_;
+    if (b1_fused) g.colsum_part = bb1p_;  // + the column sums of dh per 32-row group (b1)
     gemm(g, st);
     if (trainable) {
         block_dw(L, lay_.w1, a.xn2, bdbig_, rows, st);
-        if (lay_.b1 >= 0) block_colsum(bdbig_, rows, ff, at(lay_.b1), st);
+        if (b1_fused) {
+            ColChunks c;
+            c.n = 1;
+            c.chunks = static_cast<int>((rows + 31) / 32);
+            c.part[0] = bb1p_;
+            c.stride[0] = ff;
+            c.width[0] = ff;
+            c.out[0] = at(lay_.b1);
+            reduce_col_chunks(c, st);
+            ++kernels_;
+        } else if (lay_.b1 >= 0) {
+            block_colsum(bdbig_, rows, ff, at(lay_.b1), st);
+        }
     }
     g = GemmProblem{};
     g.M = T;

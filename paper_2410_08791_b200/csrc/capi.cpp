@@ -582,6 +582,7 @@ extern "C" int sp_debug_gemm_ex(const sp_debug_gemm_args* a) {
     g.aux = a->aux;
     g.ldaux = a->ldaux;
     g.act = a->act;
+    g.colsum_part = a->colsum_part;
     return static_cast<int>(sp::gemm_bf16(g, static_cast<cudaStream_t>(a->stream)));
 }
 

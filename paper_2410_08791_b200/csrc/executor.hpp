@@ -197,6 +197,7 @@ private:
     // the layer boundary: that layer's gradient image may still be read by an update)
     bool fused_norm_ = false;
     float *bnp_ = nullptr, *bnc_ = nullptr, *bcarry_ = nullptr;
+    float* bb1p_ = nullptr;  // b1's 32-row-group column partials, from the GELU' GEMM's epilogue
     void norm_param_reduce(int64_t rows, float* g_out, float* csum_part, float* csum_out, cudaStream_t st);
     // dW split-K partials, per layer parity: each split matrix has its own region (bdw_cap_
     // splits of its size), so the UPDATE op (update stream) reduces them while the compute

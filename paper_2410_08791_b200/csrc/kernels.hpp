@@ -80,6 +80,10 @@ struct GemmProblem {
     void* aux = nullptr;
     int ldaux = 0;
     int act = GELU_TANH;  // GeluKind for the GELU epilogues
+    // EPI_GELU_GATE_BF16 with one split: also the column sums of the output (the bias gradient
+    // of the layer that produced the gate), per 32-row group: colsum_part[ceil(M/32)][N] (fp32
+    // sums of the unrounded outputs, fixed order); reduce_col_chunks sums the groups
+    float* colsum_part = nullptr;
 };
 
 struct GemmChoice {

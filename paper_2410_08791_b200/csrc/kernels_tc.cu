@@ -99,6 +99,7 @@ struct Params {
     void* aux;                  // EPI_GELU_BF16 / EPI_SWIGLU_BF16: pre-activation output
     int ldaux;
     int act;                    // GeluKind
+    float* colsum_part;         // EPI_GELU_GATE_BF16: [ceil(M/32)][N] column partials (or nullptr)
 };
 
 // Grouped rasterisation: consecutive tile indices walk G m-blocks x every n-block, so the CTAs
@@ -410,6 +411,26 @@ struct TileEpilogue {
         }
     }
 
+    // Column sums of the warp's 32 x 32 chunk (rows past M count as 0) into the 32-row group's
+    // partial row: a lane-order reduce-scatter (31 shuffles) leaves column l's sum in lane l.
+    __device__ __forceinline__ void colsum_chunk(const Params& p, const float (&v)[32], int row0, int col0, bool in) const {
+        float a[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) a[i] = in ? v[i] : 0.0f;
+#pragma unroll
+        for (int w = 16; w >= 1; w >>= 1) {
+            const bool up = (lane & w) != 0;
+#pragma unroll
+            for (int i = 0; i < w; ++i) {
+                const float send = up ? a[i] : a[i + w];
+                const float recv = __shfl_xor_sync(0xffffffffu, send, w);
+                a[i] = (up ? a[i + w] : a[i]) + recv;
+            }
+        }
+        const int col = col0 + lane;
+        if (col < p.N) p.colsum_part[static_cast<long long>(row0 / 32) * p.N + col] = a[0];
+    }
+
     __device__ __forceinline__ void chunk(const CUtensorMap* tmO, const Params& p, const uint32_t (&r)[32],
                                           int row0, int col0, int split, uint32_t gate_bits) {
         float v[32];
@@ -465,18 +486,22 @@ struct TileEpilogue {
             for (int i = 0; i < 32; ++i) v[i] += g[i];
         } else if (BASE == EPI_GELU_GATE_BF16) {  // dh = dg * gelu'(h)
             float g[32];
-            if (!gate_bf16(p, row, col0, g)) return;
-            if (p.act == GELU_ERF) {
+            const bool ok = gate_bf16(p, row, col0, g);  // (false: a row past M, direct kind)
+            if (ok) {
+                if (p.act == GELU_ERF) {
 #pragma unroll
-                for (int i = 0; i < 32; ++i) v[i] *= gelu_grad_f(g[i], GELU_ERF);
-            } else {
+                    for (int i = 0; i < 32; ++i) v[i] *= gelu_grad_f(g[i], GELU_ERF);
+                } else {
 #pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    const float2 y = mul2(make_float2(v[2 * i], v[2 * i + 1]),
-                                          gelu_grad2_tanh(make_float2(g[2 * i], g[2 * i + 1])));
-                    v[2 * i] = y.x, v[2 * i + 1] = y.y;
+                    for (int i = 0; i < 16; ++i) {
+                        const float2 y = mul2(make_float2(v[2 * i], v[2 * i + 1]),
+                                              gelu_grad2_tanh(make_float2(g[2 * i], g[2 * i + 1])));
+                        v[2 * i] = y.x, v[2 * i + 1] = y.y;
+                    }
                 }
             }
+            if (p.colsum_part) colsum_chunk(p, v, row0, col0, ok && row < p.M);  // (every lane)
+            if (!ok) return;
         }
         if (BASE == EPI_SGD_F32) {
             // fused SGD (apply_sgd, model.cpp:150-155): w -= lr * dW, no FMA, in place on the
@@ -1315,7 +1340,9 @@ cudaError_t launch(const GemmProblem& g, cudaStream_t st) {
     p.aux = g.aux;
     p.ldaux = g.ldaux;
     p.act = g.act;
+    p.colsum_part = g.colsum_part;
     if ((EPI & (EPI_TMA - 1)) == EPI_SGD_F32 && p.splits != 1) return cudaErrorInvalidValue;
+    if (g.colsum_part && p.splits != 1) return cudaErrorInvalidValue;
     CUtensorMap to, tg;
     if (!make_epilogue_maps<EPI>(g, p.splits, &to, &tg)) return cudaErrorInvalidValue;
     const int total = p.m_tiles * p.n_tiles * p.splits;
@@ -1366,6 +1393,8 @@ cudaError_t launch2(const GemmProblem& g, cudaStream_t st) {
     p.aux = g.aux;
     p.ldaux = g.ldaux;
     p.act = g.act;
+    p.colsum_part = g.colsum_part;
+    if (g.colsum_part && p.splits != 1) return cudaErrorInvalidValue;
     {
         const int last = g.N - (p.n_tiles - 1) * BN;  // columns in the last N tile
         p.narrow = narrow_tiles(EPI & (EPI_TMA - 1), BN, last) ? 1 : 0;

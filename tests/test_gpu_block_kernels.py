@@ -28,11 +28,12 @@ def _stream():
 
 
 def gemm(M, N, K, A, lda, a_mn, B, ldb, b_mn, epi, out, ldo, bias=None, relu=0, gate=None, ldg=0,
-         splits=1, aux=None, ldaux=0, act=0, cta=0, block_n=0):
+         splits=1, aux=None, ldaux=0, act=0, cta=0, block_n=0, colsum=None):
     a = _capi.GemmArgs(M, N, K, A.data_ptr(), lda, a_mn, B.data_ptr(), ldb, b_mn, epi, out.data_ptr(), ldo,
                        bias.data_ptr() if bias is not None else None, relu,
                        gate.data_ptr() if gate is not None else None, ldg, splits, block_n, cta,
-                       aux.data_ptr() if aux is not None else None, ldaux, act, _stream())
+                       aux.data_ptr() if aux is not None else None, ldaux, act, _stream(),
+                       colsum.data_ptr() if colsum is not None else None)
     rc = LIB.sp_debug_gemm_ex(C.byref(a))
     assert rc == 0, rc
     torch.cuda.synchronize()
@@ -98,11 +99,17 @@ def test_gelu_epilogue_and_its_gate(T, K, N, erf):
     dy = bf(torch.randn(T, K, device="cuda"))
     W2 = bf(torch.randn(N, K, device="cuda") / math.sqrt(N))
     dh = torch.empty(T, N, device="cuda", dtype=torch.bfloat16)
-    gemm(T, N, K, dy, K, 0, W2, K, 0, EPI_GELU_GATE_BF16, dh, N, gate=h, ldg=N, act=erf)
+    parts = torch.full(((T + 31) // 32, N), float("nan"), device="cuda")
+    gemm(T, N, K, dy, K, 0, W2, K, 0, EPI_GELU_GATE_BF16, dh, N, gate=h, ldg=N, act=erf, colsum=parts)
     hv = h.float().requires_grad_(True)
     gelu_ref(hv, erf).sum().backward()
     ref = (dy.float() @ W2.float().t()) * hv.grad
     assert rel(dh, ref) < 1e-2
+    # the fused column sums (the b1 gradient) per 32-row group: every group written, and their
+    # total equals the column sums of the output (fp32 sums of the unrounded values)
+    assert torch.isfinite(parts).all()
+    assert rel(parts.double().sum(0), ref.double().sum(0)) < 2e-3
+    assert rel(parts.double().sum(0), dh.double().sum(0)) < 2e-3
 
 
 @pytest.mark.parametrize("T,K,FF", [(8192, 4096, 1024), (1000, 256, 320)])
