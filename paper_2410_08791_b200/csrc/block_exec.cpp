@@ -128,8 +128,12 @@ void Executor::block_alloc(int64_t R, int items, bool train, const std::function
     bcs_.counters = static_cast<int*>(alloc(cs.counters * 4));
     CUDA_OK(cudaMemset(bcs_.counters, 0, cs.counters * 4));  // each kernel leaves them zero
     // b1's gradient: column sums of dh, formed in the GELU' GEMM's epilogue per 32-row group
+    bb1p_ = nullptr;
+    bqkvp_ = nullptr;
     if (!lay_.swiglu() && lay_.b1 >= 0)
         bb1p_ = static_cast<float*>(alloc(static_cast<size_t>((R + 31) / 32) * static_cast<size_t>(lay_.desc.ff) * 4));
+    if (lay_.bqkv >= 0 && lay_.desc.seq_len % 32 == 0)
+        bqkvp_ = static_cast<float*>(alloc(static_cast<size_t>(R / 32) * static_cast<size_t>(lay_.qkv_cols) * 4));
     fused_norm_ = norm_backward_fused_ok(d_);
     if (fused_norm_) {
         const size_t nc = static_cast<size_t>(norm_bwd_chunks(R));
@@ -170,8 +174,8 @@ void Executor::block_convert(int slot, cudaStream_t st) {
     ++kernels_;
 }
 
-void Executor::attention(bool backward, const BlockActs& a, const void* dout, void* dqkv, int64_t rows,
-                         cudaStream_t st) {
+bool Executor::attention(bool backward, const BlockActs& a, const void* dout, void* dqkv, int64_t rows,
+                         cudaStream_t st, bool want_colsum) {
     AttnProblem p;
     p.tokens = rows;
     p.seq_len = lay_.desc.seq_len;
@@ -185,12 +189,15 @@ void Executor::attention(bool backward, const BlockActs& a, const void* dout, vo
     p.dout = dout;
     p.delta = bdelta_;
     p.dqkv = dqkv;
+    p.colsum_part = backward && want_colsum ? bqkvp_ : nullptr;
+    const bool fused = p.colsum_part && attention_colsum_fused(p);
     const cudaError_t e = backward ? attention_backward(p, st) : attention_forward(p, st);
     if (e != cudaSuccess) throw Error(SP_ERR_CUDA, std::string("attention: ") + cudaGetErrorString(e));
     const double fl = static_cast<double>(rows) * lay_.attn_flops_per_token();
     attn_flops_ += backward ? 3.5 * fl : fl;  // dK/dV pass 4 products, dQ pass 3 (vs 2 forward)
     attn_launches_ += backward ? 3 : 1;
     kernels_ += backward ? 3 : 1;
+    return fused;
 }
 
 void Executor::block_forward_layer(const WirePtrs& w, const float* x, const BlockActs& a, float* y, int64_t rows,
@@ -429,10 +436,23 @@ void Executor::block_backward_layer(int L, const WirePtrs& w, const float* x, co
     g.out = bdo_;
     g.ldo = hhd;
     gemm(g, st);
-    attention(true, a, bdo_, bdbig_, rows, st);  // dqkv
+    // dqkv (+ bqkv's column partials from the passes' epilogues where the shape allows)
+    const bool bqkv_fused = attention(true, a, bdo_, bdbig_, rows, st, trainable && lay_.bqkv >= 0 && bqkvp_);
     if (trainable) {
         block_dw(L, lay_.wqkv, a.xn1, bdbig_, rows, st);
-        if (lay_.bqkv >= 0) block_colsum(bdbig_, rows, lay_.qkv_cols, at(lay_.bqkv), st);
+        if (bqkv_fused) {
+            ColChunks c;
+            c.n = 1;
+            c.chunks = static_cast<int>(rows / 32);
+            c.part[0] = bqkvp_;
+            c.stride[0] = lay_.qkv_cols;
+            c.width[0] = lay_.qkv_cols;
+            c.out[0] = at(lay_.bqkv);
+            reduce_col_chunks(c, st);
+            ++kernels_;
+        } else if (lay_.bqkv >= 0) {
+            block_colsum(bdbig_, rows, lay_.qkv_cols, at(lay_.bqkv), st);
+        }
     }
     g = GemmProblem{};
     g.M = T;

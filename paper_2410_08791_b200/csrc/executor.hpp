@@ -168,7 +168,9 @@ private:
     void block_loss(int64_t rows);
     void block_dw(int L, int tensor, const void* act, const void* grad, int64_t rows, cudaStream_t st);
     void block_colsum(const void* x, int64_t rows, int N, float* out, cudaStream_t st);
-    void attention(bool backward, const BlockActs& a, const void* dout, void* dqkv, int64_t rows, cudaStream_t st);
+    // returns true when the backward also formed bqkv's column partials (bqkvp_)
+    bool attention(bool backward, const BlockActs& a, const void* dout, void* dqkv, int64_t rows, cudaStream_t st,
+                   bool want_colsum = false);
     cudaStream_t stream_of(OpKind k) const;
 
     sp_config cfg_;
@@ -198,6 +200,7 @@ private:
     bool fused_norm_ = false;
     float *bnp_ = nullptr, *bnc_ = nullptr, *bcarry_ = nullptr;
     float* bb1p_ = nullptr;  // b1's 32-row-group column partials, from the GELU' GEMM's epilogue
+    float* bqkvp_ = nullptr;  // bqkv's, from the attention backward's epilogues
     void norm_param_reduce(int64_t rows, float* g_out, float* csum_part, float* csum_out, cudaStream_t st);
     // dW split-K partials, per layer parity: each split matrix has its own region (bdw_cap_
     // splits of its size), so the UPDATE op (update stream) reduces them while the compute

@@ -190,7 +190,12 @@ struct AttnProblem {
     const void* dout = nullptr;  // backward: dO [T][H hd] bf16
     float* delta = nullptr;      // backward scratch [T / seq_len][H][seq_len]
     void* dqkv = nullptr;        // backward output, same layout as qkv
+    // backward, optional: the column sums of dqkv (bqkv's gradient) per 32-row group,
+    // colsum_part[T / 32][(H + 2 Hkv) hd], formed in the tcgen05 passes' epilogues (head_dim 64 /
+    // 128 and seq_len % 32 == 0 only: attention_colsum_fused says whether a shape gets them)
+    float* colsum_part = nullptr;
 };
+bool attention_colsum_fused(const AttnProblem& a);
 cudaError_t attention_forward(const AttnProblem& a, cudaStream_t st);
 cudaError_t attention_backward(const AttnProblem& a, cudaStream_t st);
 

@@ -38,6 +38,7 @@
 
 namespace sp {
 extern int g_attn_trace;  // sp_debug_set "attn_trace" (defined below)
+extern int g_attn_bwd_kind;  // kernels_attn.cu
 namespace {
 using namespace tc;
 
@@ -119,22 +120,46 @@ struct BCfg {
 };
 
 // NC accumulator columns of this thread's TMEM lane (from column `col`), times `sc`, to bf16 at
-// `dst` (NC % 8 == 0): 32-column loads while they fit, then 8-column ones (head_dim 80)
+// `dst` (NC % 8 == 0): 32-column loads while they fit, then 8-column ones (head_dim 80). With
+// `csum` (NC % 32 == 0), also the column sums of the warp's 32 rows (invalid rows as 0) into
+// csum[c * 32 + lane] (a lane-order reduce-scatter per 32 columns).
+__device__ __forceinline__ float warp_colsum32(float (&a)[32], int lane) {
+#pragma unroll
+    for (int w = 16; w >= 1; w >>= 1) {
+        const bool up = (lane & w) != 0;
+#pragma unroll
+        for (int i = 0; i < w; ++i) {
+            const float send = up ? a[i] : a[i + w];
+            const float recv = __shfl_xor_sync(0xffffffffu, send, w);
+            a[i] = (up ? a[i + w] : a[i]) + recv;
+        }
+    }
+    return a[0];
+}
 template <int NC>
-__device__ __forceinline__ void acc_row_out(uint32_t taddr, __nv_bfloat16* dst, float sc, bool store) {
+__device__ __forceinline__ void acc_row_out(uint32_t taddr, __nv_bfloat16* dst, float sc, bool store,
+                                            float* csum = nullptr, int lane = 0) {
     uint32_t v[32];
 #pragma unroll
     for (int c = 0; c < NC / 32; ++c) {
         tmem_ld32_async(taddr + c * 32, v);
         tmem_ld_wait(v);
+        float f[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]) * sc;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             uint4 w;
-            w.x = pack_bf16(__uint_as_float(v[8 * u + 0]) * sc, __uint_as_float(v[8 * u + 1]) * sc);
-            w.y = pack_bf16(__uint_as_float(v[8 * u + 2]) * sc, __uint_as_float(v[8 * u + 3]) * sc);
-            w.z = pack_bf16(__uint_as_float(v[8 * u + 4]) * sc, __uint_as_float(v[8 * u + 5]) * sc);
-            w.w = pack_bf16(__uint_as_float(v[8 * u + 6]) * sc, __uint_as_float(v[8 * u + 7]) * sc);
+            w.x = pack_bf16(f[8 * u + 0], f[8 * u + 1]);
+            w.y = pack_bf16(f[8 * u + 2], f[8 * u + 3]);
+            w.z = pack_bf16(f[8 * u + 4], f[8 * u + 5]);
+            w.w = pack_bf16(f[8 * u + 6], f[8 * u + 7]);
             if (store) reinterpret_cast<uint4*>(dst + c * 32)[u] = w;
+        }
+        if (csum) {  // (warp-uniform)
+#pragma unroll
+            for (int i = 0; i < 32; ++i) f[i] = store ? f[i] : 0.0f;
+            csum[c * 32 + lane] = warp_colsum32(f, lane);
         }
     }
 #pragma unroll
@@ -158,7 +183,8 @@ __global__ void __launch_bounds__(kThreadsB, 1)
     attn_bwd_dq2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmDO,
                         const __grid_constant__ CUtensorMap tmKV, const __nv_bfloat16* __restrict__ o,
                         const __nv_bfloat16* __restrict__ dout, const float* __restrict__ lse,
-                        float* __restrict__ delta, __nv_bfloat16* __restrict__ dqkv, BShape sh, int n_seq) {
+                        float* __restrict__ delta, __nv_bfloat16* __restrict__ dqkv, BShape sh, int n_seq,
+                        float* __restrict__ csum) {
     using C = BCfg<HD>;
     constexpr uint32_t T_DS = 256, T_ACC = 320;
     extern __shared__ uint8_t smem_raw[];
@@ -411,8 +437,13 @@ __global__ void __launch_bounds__(kThreadsB, 1)
             mbar_wait(acc_full, lt & 1);
             fence_after();
             // this half's HD / 2 columns of the query row's dQ (rows past the sequence: not stored)
+            // (+ bqkv's column sums of these dQ columns over the warp's 32 rows, when asked)
+            // (a warp's 32 rows are all in the sequence or all padding past it: seq_len % 32 == 0;
+            // padding warps must not write - their token index belongs to the next sequence)
+            const bool warp_in = qb * kRowsB + q4 * 32 < sh.S;
+            float* cs = csum && warp_in ? csum + (tok - r % 32) / 32 * sh.ld + h * HD + half * (HD / 2) : nullptr;
             acc_row_out<HD / 2>(tmem + lane_off + T_ACC + half * (HD / 2), dqkv + tok * sh.ld + h * HD + half * (HD / 2),
-                                sh.scale, q_in);
+                                sh.scale, q_in, cs, lane);
             fence_before();
             mbar_arrive(acc_empty);
         }
@@ -433,7 +464,8 @@ template <int HD, bool SEP, int NB, bool TRACE = false>
 __global__ void __launch_bounds__(kThreadsB, 1)
     attn_bwd_dkdv2_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmQ,
                           const __grid_constant__ CUtensorMap tmDO, const float* __restrict__ lse,
-                          const float* __restrict__ delta, __nv_bfloat16* __restrict__ dqkv, BShape sh, int n_seq) {
+                          const float* __restrict__ delta, __nv_bfloat16* __restrict__ dqkv, BShape sh, int n_seq,
+                          float* __restrict__ csum) {
     using C = BCfg<HD>;
     // TMEM map (header): P / dS regions of buffer b, then dK and dV
     // NB S / dP buffers (P / dS written back over them when !SEP); SEP uses 2 + separate P / dS
@@ -721,7 +753,11 @@ __global__ void __launch_bounds__(kThreadsB, 1)
             fence_after();
             __nv_bfloat16* row = dqkv + (static_cast<int64_t>(b) * sh.S + key) * sh.ld +
                                  (half == 0 ? (sh.H + kvh) * HD : (sh.H + sh.Hkv + kvh) * HD);
-            acc_row_out<HD>(tmem + lane_off + T_ACC + half * HD, row, half == 0 ? sh.scale : 1.0f, key < sh.S);
+            const int col0 = half == 0 ? (sh.H + kvh) * HD : (sh.H + sh.Hkv + kvh) * HD;
+            const int64_t tokk = static_cast<int64_t>(b) * sh.S + key;
+            const bool warp_in = kb * kRowsB + q4 * 32 < sh.S;  // (as in the dQ pass)
+            float* cs = csum && warp_in ? csum + (tokk - r % 32) / 32 * sh.ld + col0 : nullptr;
+            acc_row_out<HD>(tmem + lane_off + T_ACC + half * HD, row, half == 0 ? sh.scale : 1.0f, key < sh.S, cs, lane);
             fence_before();
             mbar_arrive(acc_empty);
         }
@@ -772,9 +808,10 @@ cudaError_t launch_bwd2(const AttnProblem& a, cudaStream_t st) {
     const int q_tiles = n_blk * a.n_heads * n_seq;
     const int kv_tiles = n_blk * a.n_kv_heads * n_seq;
     auto* dq = static_cast<__nv_bfloat16*>(a.dqkv);
+    float* cs = attention_colsum_fused(a) ? a.colsum_part : nullptr;
     attn_bwd_dq2_kernel<HD><<<q_tiles < num_sms() ? q_tiles : num_sms(), kThreadsB, C::SMEM_DQ, st>>>(
         t128, do128, t64, static_cast<const __nv_bfloat16*>(a.o), static_cast<const __nv_bfloat16*>(a.dout), a.lse,
-        a.delta, dq, sh, n_seq);
+        a.delta, dq, sh, n_seq, cs);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     if (g_attn_trace) {  // debug timeline (tools/attn_trace.py)
@@ -787,11 +824,11 @@ cudaError_t launch_bwd2(const AttnProblem& a, cudaStream_t st) {
         const unsigned int zero = 0;
         cudaMemcpyToSymbolAsync(g_bwd_trace_n, &zero, sizeof(zero), 0, cudaMemcpyHostToDevice, st);
         attn_bwd_dkdv2_kernel<HD, SEP, C::NB_DKDV, true><<<kv_tiles < num_sms() ? kv_tiles : num_sms(), kThreadsB,
-                                                          C::SMEM_DKDV, st>>>(t128, t64, do64, a.lse, a.delta, dq, sh, n_seq);
+                                                          C::SMEM_DKDV, st>>>(t128, t64, do64, a.lse, a.delta, dq, sh, n_seq, cs);
         return cudaGetLastError();
     }
     attn_bwd_dkdv2_kernel<HD, SEP, C::NB_DKDV><<<kv_tiles < num_sms() ? kv_tiles : num_sms(), kThreadsB, C::SMEM_DKDV, st>>>(
-        t128, t64, do64, a.lse, a.delta, dq, sh, n_seq);
+        t128, t64, do64, a.lse, a.delta, dq, sh, n_seq, cs);
     return cudaGetLastError();
 }
 }  // namespace
@@ -806,6 +843,10 @@ int attn_trace_read(unsigned long long* out, int cap) {
     const int k = m < cap ? m : cap;
     if (k > 0 && cudaMemcpyFromSymbol(out, g_bwd_trace, k * sizeof(unsigned long long)) != cudaSuccess) return -1;
     return k;
+}
+
+bool attention_colsum_fused(const AttnProblem& a) {
+    return a.colsum_part && (a.head_dim == 64 || a.head_dim == 128) && a.seq_len % 32 == 0 && g_attn_bwd_kind == 0;
 }
 
 cudaError_t attention_backward_tc2(const AttnProblem& a, cudaStream_t st) {
