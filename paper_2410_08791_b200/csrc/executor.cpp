@@ -125,10 +125,15 @@ Executor::Executor(const sp_config& cfg, const sp_block_desc* block) : cfg_(cfg)
     n_slots_ = ring_slots(cfg.strategy, cfg.k, cfg.k_prime, n_);
     layout_slots(1);
 
-    CUDA_OK(cudaStreamCreateWithFlags(&s_h2d_, cudaStreamNonBlocking));
-    CUDA_OK(cudaStreamCreateWithFlags(&s_comp_, cudaStreamNonBlocking));
-    CUDA_OK(cudaStreamCreateWithFlags(&s_d2h_, cudaStreamNonBlocking));
-    CUDA_OK(cudaStreamCreateWithFlags(&s_upd_, cudaStreamNonBlocking));
+    // Priorities: the compute stream's blocks are scheduled before the update stream's (the
+    // update kernels' many short blocks would otherwise take SM slots from the layer kernels);
+    // graphs are instantiated with per-node priority so replays keep them.
+    int prio_lo = 0, prio_hi = 0;
+    CUDA_OK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+    CUDA_OK(cudaStreamCreateWithPriority(&s_h2d_, cudaStreamNonBlocking, prio_lo));
+    CUDA_OK(cudaStreamCreateWithPriority(&s_comp_, cudaStreamNonBlocking, prio_hi));
+    CUDA_OK(cudaStreamCreateWithPriority(&s_d2h_, cudaStreamNonBlocking, prio_lo));
+    CUDA_OK(cudaStreamCreateWithPriority(&s_upd_, cudaStreamNonBlocking, prio_lo));
     CUDA_OK(cudaEventCreate(&ev_call0_));
     CUDA_OK(cudaEventCreate(&ev_call1_));
     CUDA_OK(cudaEventCreateWithFlags(&ev_io_in_, cudaEventDisableTiming));
@@ -1379,7 +1384,7 @@ void Executor::run_call_impl(const Plan& plan, const CallIO& io) {
             cudaGraph_t graph = nullptr;
             CUDA_OK(cudaStreamEndCapture(s_h2d_, &graph));
             GraphEntry g;
-            const cudaError_t ie = cudaGraphInstantiate(&g.exec, graph, 0);
+            const cudaError_t ie = cudaGraphInstantiate(&g.exec, graph, cudaGraphInstantiateFlagUseNodePriority);
             cudaGraphDestroy(graph);
             CUDA_OK(ie);
             g.w16_after = w16_layer_;
