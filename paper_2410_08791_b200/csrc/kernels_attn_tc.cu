@@ -649,12 +649,11 @@ __global__ void __launch_bounds__(kThreadsF2, 1)
                     for (int i = 0; i < 32; ++i) {
                         const float x0 = i < lim ? __uint_as_float(v[i]) : -INFINITY;
                         const float x1 = 32 + i < lim ? __uint_as_float(v2[i]) : -INFINITY;
-                        mx8[i & 7] = fmaxf(mx8[i & 7], fmaxf(x0, x1));
+                        mx8[i & 7] = fmax3(mx8[i & 7], x0, x1);
                     }
                 } else {
 #pragma unroll
-                    for (int i = 0; i < 32; ++i)
-                        mx8[i & 7] = fmaxf(mx8[i & 7], fmaxf(__uint_as_float(v[i]), __uint_as_float(v2[i])));
+                    for (int i = 0; i < 32; ++i) mx8[i & 7] = fmax3(mx8[i & 7], __uint_as_float(v[i]), __uint_as_float(v2[i]));
                 }
                 const float mraw = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
                                          fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
@@ -685,7 +684,7 @@ __global__ void __launch_bounds__(kThreadsF2, 1)
                     base = m_run == -INFINITY ? 0.0f : m_run;
                 }
                 uint32_t pk[32];
-                float rs[4] = {0.0f, 0.0f, 0.0f, 0.0f};  // four row-sum chains
+                float2 rs01 = make_float2(0.0f, 0.0f), rs23 = make_float2(0.0f, 0.0f);  // row-sum chains (pairs)
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
                     const float2 x01 = ffma2(make_float2(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1])),
@@ -699,12 +698,12 @@ __global__ void __launch_bounds__(kThreadsF2, 1)
                         if (32 + 2 * i >= lim) p2 = 0.0f;
                         if (32 + 2 * i + 1 >= lim) p3 = 0.0f;
                     }
-                    rs[i & 1] += p0 + p1;
-                    rs[2 + (i & 1)] += p2 + p3;
+                    rs01 = fadd2(rs01, make_float2(p0, p1));
+                    rs23 = fadd2(rs23, make_float2(p2, p3));
                     pk[i] = pack_bf16(p0, p1);
                     pk[16 + i] = pack_bf16(p2, p3);
                 }
-                const float rs0 = rs[0] + rs[1], rs1 = rs[2] + rs[3];
+                const float rs0 = rs01.x + rs01.y, rs1 = rs23.x + rs23.y;
                 // P over the first 32 of this half's S columns (already read into registers)
                 tmem_st16(s_addr, *reinterpret_cast<const uint32_t(*)[16]>(pk));
                 tmem_st16(s_addr + 16, *reinterpret_cast<const uint32_t(*)[16]>(pk + 16));
