@@ -357,20 +357,37 @@ __global__ void __launch_bounds__(256, 2) norm_bwd_fused_kernel(
         const float mean = RMS ? 0.0f : stats[2 * r], rstd = stats[2 * r + 1];
         const float4* dr = reinterpret_cast<const float4*>(dy + r * d);
         const float4* xr = reinterpret_cast<const float4*>(x + r * d);
-        float4 e[kNbMaxS], v[kNbMaxS];
+        // every load of the row up front (one DRAM round trip per row); e becomes dy*gamma and v
+        // becomes x - mean before the row reduction's barrier, so no register holds e, v and the
+        // products at once (the arithmetic is the same, operation for operation)
+        float4 e[kNbMaxS], v[kNbMaxS], base[kNbMaxS];
+        const float4* ri = reinterpret_cast<const float4*>(dres_in + r * d);
 #pragma unroll
         for (int i = 0; i < kNbMaxS; ++i) {
             e[i] = jj[i] < n4 ? __ldg(dr + jj[i]) : z4;
             v[i] = jj[i] < n4 ? __ldg(xr + jj[i]) : z4;
+            base[i] = dx && jj[i] < n4 ? __ldg(ri + jj[i]) : z4;
+        }
+#pragma unroll
+        for (int i = 0; i < kNbMaxS; ++i) v[i] = make_float4(v[i].x - mean, v[i].y - mean, v[i].z - mean, v[i].w - mean);
+        if (ppart) {
+#pragma unroll
+            for (int i = 0; i < kNbMaxS; ++i) {
+                A[i].x += e[i].x * (v[i].x * rstd);
+                A[i].y += e[i].y * (v[i].y * rstd);
+                A[i].z += e[i].z * (v[i].z * rstd);
+                A[i].w += e[i].w * (v[i].w * rstd);
+                f4_add(B[i], e[i]);
+            }
         }
         if (dx) {
             float sg = 0.0f, sgx = 0.0f;
 #pragma unroll
             for (int i = 0; i < kNbMaxS; ++i) {  // (padding lanes hold zeros)
                 const float4 gi = jj[i] < n4 ? __ldg(g4 + jj[i]) : z4;
-                const float g0 = e[i].x * gi.x, g1 = e[i].y * gi.y, g2 = e[i].z * gi.z, g3 = e[i].w * gi.w;
-                sg += (g0 + g1) + (g2 + g3);
-                sgx += (g0 * (v[i].x - mean) + g1 * (v[i].y - mean)) + (g2 * (v[i].z - mean) + g3 * (v[i].w - mean));
+                e[i] = make_float4(e[i].x * gi.x, e[i].y * gi.y, e[i].z * gi.z, e[i].w * gi.w);  // dy * gamma
+                sg += (e[i].x + e[i].y) + (e[i].z + e[i].w);
+                sgx += (e[i].x * v[i].x + e[i].y * v[i].y) + (e[i].z * v[i].z + e[i].w * v[i].w);
             }
             sg = warp_allsum(sg);
             sgx = warp_allsum(sgx);
@@ -382,21 +399,16 @@ __global__ void __launch_bounds__(256, 2) norm_bwd_fused_kernel(
             par ^= 1;
             const float c_mean = RMS ? 0.0f : tg * inv_d;
             const float c_x = tx * rstd * inv_d;
-            float4 base[kNbMaxS];  // (loaded after the barrier: fewer registers live across it)
-            const float4* ri = reinterpret_cast<const float4*>(dres_in + r * d);
-#pragma unroll
-            for (int i = 0; i < kNbMaxS; ++i) base[i] = jj[i] < n4 ? __ldg(ri + jj[i]) : z4;
             float4* ro = reinterpret_cast<float4*>(dres_out + r * d);
             uint2* r16 = dres_out16 ? reinterpret_cast<uint2*>(dres_out16 + r * d) : nullptr;
 #pragma unroll
             for (int i = 0; i < kNbMaxS; ++i) {
                 if (jj[i] >= n4) continue;
-                const float4 gi = __ldg(g4 + jj[i]);
                 float4 o;
-                o.x = base[i].x + rstd * (e[i].x * gi.x - c_mean - (v[i].x - mean) * rstd * c_x);
-                o.y = base[i].y + rstd * (e[i].y * gi.y - c_mean - (v[i].y - mean) * rstd * c_x);
-                o.z = base[i].z + rstd * (e[i].z * gi.z - c_mean - (v[i].z - mean) * rstd * c_x);
-                o.w = base[i].w + rstd * (e[i].w * gi.w - c_mean - (v[i].w - mean) * rstd * c_x);
+                o.x = base[i].x + rstd * (e[i].x - c_mean - v[i].x * rstd * c_x);
+                o.y = base[i].y + rstd * (e[i].y - c_mean - v[i].y * rstd * c_x);
+                o.z = base[i].z + rstd * (e[i].z - c_mean - v[i].z * rstd * c_x);
+                o.w = base[i].w + rstd * (e[i].w - c_mean - v[i].w * rstd * c_x);
                 ro[jj[i]] = o;
                 if (r16) {
                     __nv_bfloat162 lo = __floats2bfloat162_rn(o.x, o.y), hi = __floats2bfloat162_rn(o.z, o.w);
@@ -406,16 +418,6 @@ __global__ void __launch_bounds__(256, 2) norm_bwd_fused_kernel(
                     r16[jj[i]] = pk;
                 }
                 f4_add(Cs[i], o);
-            }
-        }
-        if (ppart) {
-#pragma unroll
-            for (int i = 0; i < kNbMaxS; ++i) {
-                A[i].x += e[i].x * ((v[i].x - mean) * rstd);
-                A[i].y += e[i].y * ((v[i].y - mean) * rstd);
-                A[i].z += e[i].z * ((v[i].z - mean) * rstd);
-                A[i].w += e[i].w * ((v[i].w - mean) * rstd);
-                f4_add(B[i], e[i]);
             }
         }
     }
