@@ -197,24 +197,6 @@ __device__ __forceinline__ float tanh_fast(float x) {
     asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
-__device__ __forceinline__ float gelu_f(float x, int kind) {
-    if (kind == GELU_ERF) return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f));
-    const float x2 = x * x;
-    const float u = x * fmaf(0.0356774081f, x2, 0.79788456080286536f);  // sqrt(2/pi) (x + 0.044715 x^3)
-    const float hx = 0.5f * x;
-    return fmaf(hx, tanh_fast(u), hx);
-}
-__device__ __forceinline__ float gelu_grad_f(float x, int kind) {
-    if (kind == GELU_ERF)
-        return 0.5f * (1.0f + erff(x * 0.70710678118654752f)) + x * 0.39894228040143268f * __expf(-0.5f * x * x);
-    const float x2 = x * x;
-    const float u = x * fmaf(0.0356774081f, x2, 0.79788456080286536f);
-    const float t = tanh_fast(u);
-    const float du = fmaf(0.1070322243f, x2, 0.79788456080286536f);  // d u / d x
-    // 0.5 (1 + t) + 0.5 x (1 - t^2) du
-    return fmaf(0.5f * x * du, fmaf(-t, t, 1.0f), fmaf(0.5f, t, 0.5f));
-}
-
 // Packed fp32 pairs (FFMA2 / FMUL2 on sm_100): each lane op is the same IEEE operation as its
 // scalar form, so results are bitwise those of the scalar code; the instruction count halves,
 // which matters for the GELU epilogues (issue slots and, under the board's power cap, energy).
@@ -233,7 +215,8 @@ __device__ __forceinline__ float2 mul2(float2 a, float2 b) {
     return *reinterpret_cast<float2*>(&r);
 }
 __device__ __forceinline__ float2 f2(float v) { return make_float2(v, v); }
-// gelu_f / gelu_grad_f (tanh form) on a pair, operation for operation
+// tanh-form GELU and its derivative on a pair: u = sqrt(2/pi) (x + 0.044715 x^3),
+// gelu = 0.5 x (1 + tanh u), gelu' = 0.5 (1 + t) + 0.5 x (1 - t^2) du/dx
 __device__ __forceinline__ float2 gelu2_tanh(float2 x) {
     const float2 x2 = mul2(x, x);
     const float2 u = mul2(x, fma2(f2(0.0356774081f), x2, f2(0.79788456080286536f)));
@@ -247,6 +230,48 @@ __device__ __forceinline__ float2 gelu_grad2_tanh(float2 x) {
     const float2 du = fma2(f2(0.1070322243f), x2, f2(0.79788456080286536f));
     const float2 a = mul2(mul2(f2(0.5f), x), du);
     return fma2(a, fma2(make_float2(-t.x, -t.y), t, f2(1.0f)), fma2(f2(0.5f), t, f2(0.5f)));
+}
+
+// Exact-erf GELU (ViT's nn.GELU) on a pair. erf by Abramowitz & Stegun 7.1.26 (|error| <= 1.5e-7,
+// far below the bf16 rounding of the stored result): one reciprocal and one exp2 on the SFU, and
+// that exp(-x^2/2) is also the normal density in gelu'(x) = Phi(x) + x phi(x). erff + __expf
+// made the ViT-H GELU epilogues ALU-bound (ncu: its dh GEMM at 930 TFLOP/s against 1420 for
+// GPT-2 XL's tanh form at the same tile count).
+__device__ __forceinline__ float rcp_fast(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float ex2_fast(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+// Phi(x) (the standard normal CDF) and e = exp(-x^2 / 2)
+__device__ __forceinline__ void normal_cdf2(float2 x, float2& Phi, float2& e) {
+    const float2 z = mul2(make_float2(fabsf(x.x), fabsf(x.y)), f2(0.70710678118654752f));
+    const float2 d = fma2(f2(0.3275911f), z, f2(1.0f));
+    const float2 t = make_float2(rcp_fast(d.x), rcp_fast(d.y));
+    // the A&S coefficients halved: q = 0.5 (1 - erf(|x| / sqrt 2)) = the tail 1 - Phi(|x|)
+    float2 p = fma2(f2(0.5307027145f), t, f2(-0.7265760135f));
+    p = fma2(p, t, f2(0.7107068705f));
+    p = fma2(p, t, f2(-0.142248368f));
+    p = fma2(p, t, f2(0.127414796f));
+    p = mul2(p, t);
+    const float2 a = mul2(mul2(x, x), f2(-0.72134752044448170f));  // -x^2 / 2 * log2(e)
+    e = make_float2(ex2_fast(a.x), ex2_fast(a.y));
+    const float2 q = mul2(p, e);
+    Phi = make_float2(x.x >= 0.0f ? 1.0f - q.x : q.x, x.y >= 0.0f ? 1.0f - q.y : q.y);
+}
+__device__ __forceinline__ float2 gelu2_erf(float2 x) {
+    float2 Phi, e;
+    normal_cdf2(x, Phi, e);
+    return mul2(x, Phi);
+}
+__device__ __forceinline__ float2 gelu_grad2_erf(float2 x) {
+    float2 Phi, e;
+    normal_cdf2(x, Phi, e);
+    return fma2(mul2(x, e), f2(0.39894228040143268f), Phi);  // Phi + x phi
 }
 
 template <int BN, int EPI>
@@ -453,7 +478,10 @@ struct TileEpilogue {
             if (row < p.M && p.aux) store_row_bf16(p.aux, p.ldaux, row, col0, hk);
             if (p.act == GELU_ERF) {
 #pragma unroll
-                for (int i = 0; i < 32; ++i) v[i] = gelu_f(v[i], GELU_ERF);
+                for (int i = 0; i < 16; ++i) {
+                    const float2 y = gelu2_erf(make_float2(v[2 * i], v[2 * i + 1]));
+                    v[2 * i] = y.x, v[2 * i + 1] = y.y;
+                }
             } else {
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
@@ -490,7 +518,11 @@ struct TileEpilogue {
             if (ok) {
                 if (p.act == GELU_ERF) {
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) v[i] *= gelu_grad_f(g[i], GELU_ERF);
+                    for (int i = 0; i < 16; ++i) {
+                        const float2 y = mul2(make_float2(v[2 * i], v[2 * i + 1]),
+                                              gelu_grad2_erf(make_float2(g[2 * i], g[2 * i + 1])));
+                        v[2 * i] = y.x, v[2 * i + 1] = y.y;
+                    }
                 } else {
 #pragma unroll
                     for (int i = 0; i < 16; ++i) {

@@ -1,6 +1,6 @@
 """Back-to-back named-shape train-step time through the block ABI (graphs on, device inputs), for
 A/B of two library builds via SUPERPIPE_LIB: warm-up, then STEPS steps between CUDA events.
-Usage: python tools/block_step_time.py [gpt2-xl] [steps]"""
+Usage: python tools/block_step_time.py [gpt2-xl] [steps] [seqs] [layers]"""
 import json
 import os
 import sys
@@ -15,8 +15,10 @@ from paper_2410_08791_b200 import blocks as B  # noqa: E402
 name = sys.argv[1] if len(sys.argv) > 1 else "gpt2-xl"
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 10
 spec, L = B.NAMED_SHAPES[name]
+seqs = int(sys.argv[3]) if len(sys.argv) > 3 else 16
+L = int(sys.argv[4]) if len(sys.argv) > 4 else L
 model = B.build_block_model(spec, 7, L)
-rows = 16 * spec.seq_len
+rows = seqs * spec.seq_len
 x = torch.from_numpy(sp.make_input(7, 0, rows, spec.d)).cuda()
 t = torch.from_numpy(sp.make_input(7, 1, rows, spec.d)).cuda()
 ex = B.BlockExecutor(L, spec, sp.StrategyConfig(sp.SUPERPIPELINE, 4, 2), trace=0)
