@@ -92,7 +92,7 @@ struct GemmChoice {
 };
 // The kernel variant gemm_bf16 picks when cta/block_n are 0 (depends on the shape only, so
 // results are identical for every window setting).
-GemmChoice choose_gemm(int M, int N, int K, int splits, int epilogue);
+GemmChoice choose_gemm(int M, int N, int K, int splits, int epilogue, bool b_kmajor = false);
 
 // Launches the warp-specialized tcgen05/TMEM/TMA GEMM. Returns cudaSuccess or an error.
 cudaError_t gemm_bf16(const GemmProblem& p, cudaStream_t st);

@@ -1506,8 +1506,8 @@ cudaError_t dispatch2_bn_tf32(const GemmProblem& g, cudaStream_t st) {
     return cudaErrorNotSupported;
 }
 
-// 2-CTA tiles whose per-CTA half of N is not a whole 64-column swizzle atom (N = 192 -> 96
-// per CTA) exist only for K-major B, where a CTA's B half is a plain [rows][64] TMA box.
+// 2-CTA tiles whose per-CTA half of N is not a whole 64-column swizzle atom (N = 192 -> 96,
+// N = 160 -> 80 per CTA) exist only for K-major B, where a CTA's B half is a plain [rows][64] TMA box.
 template <int BN>
 cudaError_t dispatch2_bn_kmajor(const GemmProblem& g, cudaStream_t st) {
     if (!g.a_mn && !g.b_mn && g.epilogue == EPI_GATE_BF16) return launch2_k<BN, false, false, EPI_GATE_BF16>(g, st);
@@ -1551,7 +1551,7 @@ double pair_max_load(long F, long R, long U) {
     return worst;
 }
 
-GemmChoice choose_gemm(int M, int N, int K, int splits, int epilogue) {
+GemmChoice choose_gemm(int M, int N, int K, int splits, int epilogue, bool b_kmajor) {
     const int sms = num_sms();
     GemmChoice best{1, 256};
     double best_t = 1e300;
@@ -1572,6 +1572,10 @@ GemmChoice choose_gemm(int M, int N, int K, int splits, int epilogue) {
         }
     };
     consider(2, 256, 0.95);
+    // CTA-pair N=192 tiles (K-major B, bf16 / fp32 stores): at N = d = 1600 nine whole-ish tiles
+    // beat seven 256-wide ones with a ragged last tile (tools/bn_probe.py, 16384 rows: 4-12%
+    // faster at K = 1600 / 4800 / 6400; N = 160, ten exact tiles, lands between the two)
+    if (b_kmajor && (epilogue == EPI_GATE_BF16 || epilogue == EPI_F32)) consider(2, 192, 0.96);
     consider(1, 256, 0.80);
     consider(1, 192, 0.80);
     (void)K;
@@ -1680,10 +1684,10 @@ cudaError_t gemm_bf16(const GemmProblem& g, cudaStream_t st) {
     }
     int cta = g.cta, bn = g.block_n;
     if (cta == 0) {  // auto
-        const GemmChoice c = choose_gemm(g.M, g.N, g.K, g.splits < 1 ? 1 : g.splits, g.epilogue);
+        const GemmChoice c = choose_gemm(g.M, g.N, g.K, g.splits < 1 ? 1 : g.splits, g.epilogue, !g.b_mn);
         cta = c.cta;
         if (!bn) bn = c.block_n;
-        if (cta == 2 && bn != 128 && bn != 256 && !(bn == 192 && !g.b_mn)) cta = 1;  // a forced tile width decides
+        if (cta == 2 && bn != 128 && bn != 256 && !((bn == 192 || bn == 160) && !g.b_mn)) cta = 1;  // a forced tile width decides
     }
     if (!bn) bn = cta == 2 ? 256 : choose_block_n(g.N);
     if (cta == 2) {
@@ -1691,6 +1695,7 @@ cudaError_t gemm_bf16(const GemmProblem& g, cudaStream_t st) {
             case 128: return tc::dispatch2_bn<128>(g, st);
             case 256: return tc::dispatch2_bn<256>(g, st);
             case 192: return tc::dispatch2_bn_kmajor<192>(g, st);
+            case 160: return tc::dispatch2_bn_kmajor<160>(g, st);
             default: return cudaErrorInvalidValue;
         }
     }
