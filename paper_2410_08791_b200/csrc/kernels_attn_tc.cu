@@ -628,23 +628,43 @@ __global__ void __launch_bounds__(kThreadsF2, 1)
                 fence_before();
                 mbar_arrive(&o_empty[ob]);
             };
+            if (LAZY && q0 + q4 * 32 >= sh.S) {
+                // a lane quarter wholly past the sequence (ragged S, e.g. ViT's 257 = 2 x 128 + 1:
+                // three of the last tile's four quarters): no softmax work, only the barrier
+                // protocol. Its O rows accumulate whatever P its TMEM lanes hold and are never
+                // stored. Each arrival follows the matching S / O completion, so it cannot count
+                // toward an earlier phase.
+                for (int j = 0; j < n_kb; ++j, ++g) {
+                    mbar_wait(&s_full[g & 1], (g >> 1) & 1);
+                    mbar_arrive(&p_full[g & 1]);
+                }
+                mbar_wait(&o_full[lt & 1], (lt >> 1) & 1);
+                mbar_arrive(&o_empty[lt & 1]);
+                continue;
+            }
             for (int j = 0; j < n_kb; ++j, ++g) {
                 const int sb = g & 1;
                 const int k0 = j * kKV + 64 * h;  // first key of this half
+                const bool need_mask = (sh.causal && k0 + 63 > q0) || k0 + 64 > sh.S;
+                const int lim = need_mask ? min(sh.S, sh.causal ? qi + 1 : sh.S) - k0 : 64;  // valid keys
+                // a half with no valid key for any of the warp's rows (the ragged last block):
+                // P = 0 without reading S
+                const bool half_dead = need_mask && __all_sync(0xffffffffu, lim <= 0);
                 mbar_wait(&s_full[sb], (g >> 1) & 1);
                 fence_after();
                 const uint32_t s_addr = tmem + lane_off + sb * 128 + 64 * h;
-                tmem_ld32_async(s_addr, v);
-                tmem_ld32_async(s_addr + 32, v2);
-                tmem_ld_wait(v);
-                tmem_ld_wait(v2);
-                const bool need_mask = (sh.causal && k0 + 63 > q0) || k0 + 64 > sh.S;
-                const int lim = need_mask ? min(sh.S, sh.causal ? qi + 1 : sh.S) - k0 : 64;  // valid keys
+                if (!half_dead) {
+                    tmem_ld32_async(s_addr, v);
+                    tmem_ld32_async(s_addr + 32, v2);
+                    tmem_ld_wait(v);
+                    tmem_ld_wait(v2);
+                }
                 // row max of the half: eight independent chains, then a tree (short dependency chains)
                 float mx8[8];
 #pragma unroll
                 for (int u = 0; u < 8; ++u) mx8[u] = -INFINITY;
-                if (need_mask) {
+                if (half_dead) {
+                } else if (need_mask) {
 #pragma unroll
                     for (int i = 0; i < 32; ++i) {
                         const float x0 = i < lim ? __uint_as_float(v[i]) : -INFINITY;
@@ -685,6 +705,10 @@ __global__ void __launch_bounds__(kThreadsF2, 1)
                 }
                 uint32_t pk[32];
                 float2 rs01 = make_float2(0.0f, 0.0f), rs23 = make_float2(0.0f, 0.0f);  // row-sum chains (pairs)
+                if (half_dead) {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) pk[i] = 0u;
+                } else {
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
                     const float2 x01 = ffma2(make_float2(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1])),
@@ -702,6 +726,7 @@ __global__ void __launch_bounds__(kThreadsF2, 1)
                     rs23 = fadd2(rs23, make_float2(p2, p3));
                     pk[i] = pack_bf16(p0, p1);
                     pk[16 + i] = pack_bf16(p2, p3);
+                }
                 }
                 const float rs0 = rs01.x + rs01.y, rs1 = rs23.x + rs23.y;
                 // P over the first 32 of this half's S columns (already read into registers)
