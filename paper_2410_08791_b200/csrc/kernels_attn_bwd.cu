@@ -211,11 +211,12 @@ __global__ void __launch_bounds__(kThreadsB, 1)
     // the sequence are masked (keys) or never stored (queries)
     const int n_qb = (sh.S + kRowsB - 1) / kRowsB, n_ks = (sh.S + kStepB - 1) / kStepB;
     const int n_tiles = n_qb * sh.H * n_seq;
-    // tile t: (query block, head, sequence), query blocks descending (causal: longest first)
+    // tile t: (query block, head, sequence), query blocks descending (causal: longest first);
+    // without the mask, query blocks innermost (one DRAM read of K / V, as the forward's tile_of)
     auto tile = [&](int t, int& qb, int& h, int& b) {
         const int per = sh.H * n_seq;
-        qb = n_qb - 1 - t / per;
-        const int rest = t % per;
+        const int rest = sh.causal ? t % per : t / n_qb;
+        qb = sh.causal ? n_qb - 1 - t / per : t % n_qb;
         h = rest % sh.H;
         b = rest / sh.H;
     };
@@ -499,11 +500,12 @@ __global__ void __launch_bounds__(kThreadsB, 1)
     const int n_kb = (sh.S + kRowsB - 1) / kRowsB, n_qs = (sh.S + kStepB - 1) / kStepB;  // (ragged: as dQ)
     const int group = sh.H / sh.Hkv;
     const int n_tiles = n_kb * sh.Hkv * n_seq;
-    // tile t: (key block, kv head, sequence), key blocks ascending (causal: longest first)
+    // tile t: (key block, kv head, sequence), key blocks ascending (causal: longest first);
+    // without the mask, key blocks innermost (one DRAM read of Q / dO per (sequence, head))
     auto tile = [&](int t, int& kb, int& kvh, int& b) {
         const int per = sh.Hkv * n_seq;
-        kb = t / per;
-        const int rest = t % per;
+        const int rest = sh.causal ? t % per : t / n_kb;
+        kb = sh.causal ? t / per : t % n_kb;
         kvh = rest % sh.Hkv;
         b = rest / sh.Hkv;
     };
