@@ -94,6 +94,7 @@ struct Params {
     long long split_stride;
     float lr;
     int narrow;  // 2-CTA: the ragged last N tile is computed with an MMA of N = BN/2
+    int group;   // 2-CTA: m-blocks per rasterisation group (tile_mn_g)
     uint32_t* mask_out;         // EPI_BIAS_ACT_BF16: ReLU bit mask of the output (or nullptr)
     const uint32_t* gate_mask;  // EPI_GATE_BF16: gate from a bit mask (or nullptr: gate tensor)
     void* aux;                  // EPI_GELU_BF16 / EPI_SWIGLU_BF16: pre-activation output
@@ -105,8 +106,7 @@ struct Params {
 // Grouped rasterisation: consecutive tile indices walk G m-blocks x every n-block, so the CTAs
 // resident at any moment share their A panels (and B panels) in L2 instead of re-streaming each
 // A panel from DRAM once per n-block. Only the order of tiles changes, never a tile's math.
-template <int G>
-__device__ __forceinline__ void tile_mn(int t, int m_tiles, int n_tiles, int& mb, int& nb) {
+__device__ __forceinline__ void tile_mn_g(int t, int m_tiles, int n_tiles, int G, int& mb, int& nb) {
     const int tmn = t % (m_tiles * n_tiles);
     const int per_group = G * n_tiles;
     const int g = tmn / per_group;
@@ -115,6 +115,10 @@ __device__ __forceinline__ void tile_mn(int t, int m_tiles, int n_tiles, int& mb
     const int r = tmn - g * per_group;
     mb = first + r % gm;
     nb = r / gm;
+}
+template <int G>
+__device__ __forceinline__ void tile_mn(int t, int m_tiles, int n_tiles, int& mb, int& nb) {
+    tile_mn_g(t, m_tiles, n_tiles, G, mb, nb);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -923,9 +927,10 @@ __device__ __forceinline__ void umma2_commit_both(uint64_t* bar) {
 // tiles of cost 1 and 1/2: at 16384 x 1600 the busiest pair does 6.0 tile-times instead of 7.
 // Which pair computes a tile never changes the tile's arithmetic.
 struct PairSched {
-    int U, u, F, R, r, mt, ntf, nt, per_split;
+    int U, u, F, R, r, mt, ntf, nt, per_split, group;
     __device__ __forceinline__ PairSched(const Params& p, int m_tiles2, int cid, int ncl) {
         mt = m_tiles2;
+        group = p.group;
         nt = p.n_tiles;
         ntf = p.narrow ? nt - 1 : nt;
         per_split = mt * ntf;
@@ -941,7 +946,7 @@ struct PairSched {
         if (i < nfull) {
             const int t = u + U * i;
             split = t / per_split;
-            tile_mn<8>(t - split * per_split, mt, ntf, mb, nb);
+            tile_mn_g(t - split * per_split, mt, ntf, group, mb, nb);
             narrow = false;
             return true;
         }
@@ -1307,6 +1312,7 @@ bool make_epilogue_maps(const GemmProblem& g, int splits, CUtensorMap* to, CUten
 // for every epilogue (1) or the split-K partials only (0, the product choice).
 int g_epi_mode = 0;
 int g_narrow = 0;
+int g_raster = 0;  // CTA-pair rasterisation group, 0 = by shape (debug knob "raster")
 
 // Epilogue kind: TMA staging when the tile's K loop is short (the epilogue is then on the
 // critical path: +8..15% on the d=1280/1600 layer GEMMs, ncu, fixed clocks), direct per-lane
@@ -1431,6 +1437,14 @@ cudaError_t launch2(const GemmProblem& g, cudaStream_t st) {
         const int last = g.N - (p.n_tiles - 1) * BN;  // columns in the last N tile
         p.narrow = narrow_tiles(EPI & (EPI_TMA - 1), BN, last) ? 1 : 0;
     }
+    // m-blocks per rasterisation group: each group streams the whole B (weight) matrix once, so
+    // a B too large to stay in L2 (> 64 MB: Llama-3-8B's gate/up 235 MB, down 117 MB) takes 16
+    // and is re-read from DRAM half as often; the lower DRAM power lets the clock rise under the
+    // 1000 W cap (SwiGLU gate/up 12.9-13.3 -> 12.0 ms, tools/llama_gemm_probe.py; C3 881-928 ->
+    // 841 ms). Smaller B stays in L2 either way and 8 keeps the A panels' footprint small
+    // (16 measured 0.5% slower on GPT-2 XL's step and 3% on ViT-H's, tools/block_ab.py).
+    const double b_bytes = static_cast<double>(g.N) * g.K * O::ELT;
+    p.group = g_raster > 0 ? g_raster : (b_bytes > 64e6 ? 16 : 8);
     if ((EPI & (EPI_TMA - 1)) == EPI_SGD_F32 && p.splits != 1) return cudaErrorInvalidValue;
     CUtensorMap to, tg;
     if (!make_epilogue_maps<EPI>(g, p.splits, &to, &tg)) return cudaErrorInvalidValue;
@@ -1528,6 +1542,7 @@ void set_gemm_debug(const char* key, int value, bool* known) {
     else if (std::strcmp(key, "attn_bwd") == 0) g_attn_bwd_kind = value;
     else if (std::strcmp(key, "attn_trace") == 0) g_attn_trace = value;
     else if (std::strcmp(key, "narrow") == 0) tc::g_narrow = value;
+    else if (std::strcmp(key, "raster") == 0) tc::g_raster = value;
     else *known = false;
 }
 
