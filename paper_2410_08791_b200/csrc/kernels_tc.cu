@@ -1314,17 +1314,20 @@ int g_epi_mode = 0;
 int g_narrow = 0;
 int g_raster = 0;  // CTA-pair rasterisation group, 0 = by shape (debug knob "raster")
 
-// Epilogue kind: TMA staging when the tile's K loop is short (the epilogue is then on the
-// critical path: +8..15% on the d=1280/1600 layer GEMMs, ncu, fixed clocks), direct per-lane
-// stores for long K (where the epilogue hides and the TMA kind costs ~5%, d=4096).
+// Epilogue kind: TMA staging for every epilogue but the fused SGD. At short K the epilogue is on
+// the critical path (+8..15% on the d=1280/1600 layer GEMMs, ncu, fixed clocks). At long K the
+// direct per-lane stores (half-used 32-byte sectors) were ~5% faster at fixed clocks (d=4096),
+// but the step runs at the board's power cap, where the TMA kind's whole-sector stores measured
+// even to slightly ahead (GPT-2 XL step 189.2 -> 188.4 ms, tools/block_ab.py epi_mode; Llama-3
+// QKV 2.51 -> 2.46 ms, tools/llama_gemm_probe.py).
 // sp_debug_set("epi_mode", 1|2) forces direct/TMA (A/B measurement only).
 bool use_tma_epilogue(const GemmProblem& g, int splits) {
     const int forced = g_epi_mode;
     if (g.epilogue == EPI_SGD_F32) return false;
     if (forced == 1) return false;
     if (forced == 2) return true;
-    const int k_per_tile = (g.K + splits - 1) / (splits < 1 ? 1 : splits);
-    return k_per_tile <= 2048;
+    (void)splits;
+    return true;
 }
 
 // Half-width last N tiles (PairSched) pay only for the split-K fp32 partials of dW (+5%, ncu):
