@@ -11,6 +11,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
 import paper_2410_08791_b200 as sp  # noqa: E402
+from paper_2410_08791_b200 import _capi  # noqa: E402
 from paper_2410_08791_b200 import blocks as B  # noqa: E402
 
 p = argparse.ArgumentParser()
@@ -22,6 +23,7 @@ p.add_argument("--kp", type=int, default=2)
 p.add_argument("--infer", action="store_true")
 p.add_argument("--ckpt", action="store_true")
 p.add_argument("--graphs", type=int, default=0)
+p.add_argument("--set", action="append", default=[], help="KEY=VALUE process-wide kernel knob (sp_debug_set)")
 a = p.parse_args()
 spec, L = B.NAMED_SHAPES[a.model]
 L = a.layers or L
@@ -33,6 +35,9 @@ y = torch.empty_like(x)
 ex = B.BlockExecutor(L, spec, sp.StrategyConfig(sp.SUPERPIPELINE, a.k, a.kp), checkpointing=a.ckpt, trace=0)
 ex.register_model(model)
 ex.debug_set("graphs", a.graphs)
+for kv in a.set:
+    k, v = kv.split("=")
+    assert _capi.LIB.sp_debug_set(None, k.encode(), int(v)) == 0, kv
 
 
 def step():
