@@ -847,6 +847,10 @@ int attn_trace_read(unsigned long long* out, int cap) {
     return k;
 }
 
+// ViT's ragged 257-token sequences keep the separate colsum_total: the passes' epilogues with
+// per-sequence 32-row groups (and 8-column tails for head_dim 80) were measured there, and the
+// column sums on each short tile's critical path cost dQ + dK/dV 150 us per layer against the
+// 114 us colsum they replace (profiles/r02_c4_vit_launches.txt is the kept build)
 bool attention_colsum_fused(const AttnProblem& a) {
     return a.colsum_part && (a.head_dim == 64 || a.head_dim == 128) && a.seq_len % 32 == 0 && g_attn_bwd_kind == 0;
 }
