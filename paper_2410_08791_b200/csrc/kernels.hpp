@@ -196,6 +196,8 @@ struct AttnProblem {
     float* colsum_part = nullptr;
 };
 bool attention_colsum_fused(const AttnProblem& a);
+// (sequence, head) pairs per chunk of the causal attention kernels' work order
+int attention_causal_chunk(const AttnProblem& a);
 cudaError_t attention_forward(const AttnProblem& a, cudaStream_t st);
 cudaError_t attention_backward(const AttnProblem& a, cudaStream_t st);
 

@@ -682,6 +682,17 @@ bool valid(const AttnProblem& a) {
 // head_dim 80 then takes the mma.sync kernel); 1: always the mma.sync kernel.
 int g_attn_fwd_kind = 0;
 int g_attn_bwd_kind = 0;
+int g_attn_chunk = 0;  // sp_debug_set "attn_chunk": causal work-order chunk (0 = by shape)
+
+// Chunked only when the whole K / V outgrows the 126 MB L2: Llama-3-8B's 268 MB at 32 x 2048
+// tokens (chunks of 32: forward 1809 -> 1512 us, backward 4.91 -> 4.49 ms per layer); GPT-2 XL's
+// 105 MB is re-read from L2 anyway, where chunks of 32..256 measured 1-4% slower than the plain
+// longest-first order (tools/attn_probe.py, SP_ATTN_CHUNK).
+int attention_causal_chunk(const AttnProblem& a) {
+    if (g_attn_chunk > 0) return g_attn_chunk;
+    const double kv_bytes = static_cast<double>(a.tokens) * a.n_kv_heads * a.head_dim * 4.0;
+    return kv_bytes > 126e6 ? 32 : 1 << 30;
+}
 
 cudaError_t attention_forward_tc(const AttnProblem& a, cudaStream_t st, int kind);  // kernels_attn_tc.cu
 

@@ -96,7 +96,7 @@ __device__ __forceinline__ uint32_t ts_col(int kk) {
 __device__ __forceinline__ uint64_t dadd(uint64_t d, uint32_t bytes) { return d + (bytes >> 4); }
 
 struct BShape {
-    int S, H, Hkv, ld, ldo, causal;
+    int S, H, Hkv, ld, ldo, causal, chunk;  // chunk: causal work order (causal_chunked)
     float scale_log2, scale;
 };
 
@@ -215,8 +215,13 @@ __global__ void __launch_bounds__(kThreadsB, 1)
     // without the mask, query blocks innermost (one DRAM read of K / V, as the forward's tile_of)
     auto tile = [&](int t, int& qb, int& h, int& b) {
         const int per = sh.H * n_seq;
-        const int rest = sh.causal ? t % per : t / n_qb;
-        qb = sh.causal ? n_qb - 1 - t / per : t % n_qb;
+        int rest;
+        if (sh.causal) {
+            causal_chunked(t, per, n_qb, true, sh.chunk, qb, rest);  // (the forward's chunked order)
+        } else {
+            rest = t / n_qb;
+            qb = t % n_qb;
+        }
         h = rest % sh.H;
         b = rest / sh.H;
     };
@@ -504,8 +509,13 @@ __global__ void __launch_bounds__(kThreadsB, 1)
     // without the mask, key blocks innermost (one DRAM read of Q / dO per (sequence, head))
     auto tile = [&](int t, int& kb, int& kvh, int& b) {
         const int per = sh.Hkv * n_seq;
-        const int rest = sh.causal ? t % per : t / n_kb;
-        kb = sh.causal ? t / per : t % n_kb;
+        int rest;
+        if (sh.causal) {
+            causal_chunked(t, per, n_kb, false, sh.chunk, kb, rest);  // key block 0 (the longest) first
+        } else {
+            rest = t / n_kb;
+            kb = t % n_kb;
+        }
         kvh = rest % sh.Hkv;
         b = rest / sh.Hkv;
     };
@@ -803,6 +813,7 @@ cudaError_t launch_bwd2(const AttnProblem& a, cudaStream_t st) {
     sh.ld = ld;
     sh.ldo = ldo;
     sh.causal = a.causal;
+    sh.chunk = attention_causal_chunk(a);
     sh.scale = 1.0f / sqrtf(static_cast<float>(a.head_dim));
     sh.scale_log2 = 1.4426950408889634f * sh.scale;
     const int n_seq = static_cast<int>(a.tokens / a.seq_len);

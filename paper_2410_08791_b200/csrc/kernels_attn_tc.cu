@@ -47,7 +47,7 @@ struct AttnCfg {
 };
 
 struct TcShape {
-    int S, H, Hkv, ld, ldo, causal;
+    int S, H, Hkv, ld, ldo, causal, chunk;  // chunk: causal work order (causal_chunked)
     float scale_log2;
 };
 
@@ -76,10 +76,10 @@ __device__ __forceinline__ TileOf tile_of(int t, const TcShape& sh, int n_qb, in
     const int per = sh.H * n_seq;
     TileOf o;
     if (sh.causal) {
-        o.qb = n_qb - 1 - t / per;
-        const int rest = t % per;
-        o.h = rest % sh.H;
-        o.b = rest / sh.H;
+        int pair;
+        causal_chunked(t, per, n_qb, true, sh.chunk, o.qb, pair);
+        o.h = pair % sh.H;
+        o.b = pair / sh.H;
     } else {
         o.qb = t % n_qb;
         const int rest = t / n_qb;
@@ -841,6 +841,7 @@ cudaError_t launch_fwd_tc2(const AttnProblem& a, cudaStream_t st) {
     sh.ld = ld;
     sh.ldo = a.n_heads * a.head_dim;
     sh.causal = a.causal;
+    sh.chunk = attention_causal_chunk(a);
     sh.scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(a.head_dim));
     const int n_seq = static_cast<int>(a.tokens / a.seq_len);
     const int tiles = ((a.seq_len + kQ - 1) / kQ) * a.n_heads * n_seq;
@@ -873,6 +874,7 @@ cudaError_t launch_fwd_tc(const AttnProblem& a, cudaStream_t st) {
     sh.ld = ld;
     sh.ldo = a.n_heads * a.head_dim;
     sh.causal = a.causal;
+    sh.chunk = attention_causal_chunk(a);
     sh.scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(a.head_dim));
     const int n_seq = static_cast<int>(a.tokens / a.seq_len);
     const int tiles = ((a.seq_len + kQ - 1) / kQ) * a.n_heads * n_seq;
@@ -1398,6 +1400,7 @@ cudaError_t launch_bwd_tc(const AttnProblem& a, cudaStream_t st) {
     sh.ld = ld;
     sh.ldo = ldo;
     sh.causal = a.causal;
+    sh.chunk = attention_causal_chunk(a);
     const float scale = 1.0f / sqrtf(static_cast<float>(a.head_dim));
     sh.scale_log2 = 1.4426950408889634f * scale;
     const int n_seq = static_cast<int>(a.tokens / a.seq_len);

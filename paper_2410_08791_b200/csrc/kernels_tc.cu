@@ -1537,6 +1537,7 @@ cudaError_t dispatch2_bn_kmajor(const GemmProblem& g, cudaStream_t st) {
 extern int g_attn_fwd_kind;  // kernels_attn.cu
 extern int g_attn_bwd_kind;
 extern int g_attn_trace;
+extern int g_attn_chunk;
 
 void set_gemm_debug(const char* key, int value, bool* known) {
     *known = true;
@@ -1544,6 +1545,7 @@ void set_gemm_debug(const char* key, int value, bool* known) {
     else if (std::strcmp(key, "attn_fwd") == 0) g_attn_fwd_kind = value;
     else if (std::strcmp(key, "attn_bwd") == 0) g_attn_bwd_kind = value;
     else if (std::strcmp(key, "attn_trace") == 0) g_attn_trace = value;
+    else if (std::strcmp(key, "attn_chunk") == 0) g_attn_chunk = value;
     else if (std::strcmp(key, "narrow") == 0) tc::g_narrow = value;
     else if (std::strcmp(key, "raster") == 0) tc::g_raster = value;
     else *known = false;

@@ -216,5 +216,20 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
 bool make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint64_t ld,
               uint32_t box_inner, uint32_t box_outer, bool f32, bool base32);
 
+
+// Attention work order for causal masks (kernels_attn_tc.cu / kernels_attn_bwd.cu): chunks of
+// `chunk` (sequence, head) pairs, each walked longest block first, so a chunk's K / V stay in L2
+// while all its blocks read them, and the kernel still ends on the shortest tiles. chunk >= pairs
+// is the plain longest-first order over every pair.
+__device__ __forceinline__ void causal_chunked(int t, int pairs, int n_blocks, bool descending, int chunk, int& blk,
+                                               int& pair) {
+    chunk = min(chunk, pairs);  // (and chunk * n_blocks stays in range)
+    const int c = t / (chunk * n_blocks);
+    const int first = c * chunk;
+    const int np = min(chunk, pairs - first);
+    const int idx = t - first * n_blocks;
+    blk = descending ? n_blocks - 1 - idx / np : idx / np;
+    pair = first + idx % np;
+}
 }  // namespace tc
 }  // namespace sp

@@ -15,6 +15,8 @@ LIB = _capi.LIB
 # SP_ATTN_FWD=0|1|3: the forward kernel choice (sp_debug_set "attn_fwd"; 0 = v2 tcgen05, 3 = v1, 1 = mma.sync)
 LIB.sp_debug_set(None, b"attn_fwd", int(os.environ.get("SP_ATTN_FWD", "0")))
 LIB.sp_debug_set(None, b"attn_bwd", int(os.environ.get("SP_ATTN_BWD", "0")))
+# SP_ATTN_CHUNK=N: (sequence, head) pairs per chunk of the causal work order (0 = by shape)
+LIB.sp_debug_set(None, b"attn_chunk", int(os.environ.get("SP_ATTN_CHUNK", "0")))
 
 
 def timeit(fn, reps=10):
