@@ -358,16 +358,23 @@ __global__ void __launch_bounds__(kThreadsB, 1)
         const int r = q4 * 32 + lane;
         const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
         uint32_t vs[32], vp[32];
-        uint4 ro[HD / 8], rd[HD / 8];  // this thread's O and dO rows (of the next tile)
+        // this thread's O and dO rows of the next tile, prefetched during the current one: whole
+        // rows at head_dim 64; at 80 / 128 each warpgroup takes half the columns and the two
+        // partial dot products meet in shared memory (the registers of whole rows would spill)
+        constexpr bool kHalfRows = HD != 64;
+        constexpr int NR = kHalfRows ? HD / 16 : HD / 8;
+        __shared__ float xdl[2][2][kRowsB];  // [tile parity][half][row] partial deltas
+        uint4 ro[NR], rd[NR];
         auto load_rows = [&](int tt) {
             int qb_, h_, b_;
             tile(tt, qb_, h_, b_);
             const bool in = qb_ * kRowsB + r < sh.S;
             const int64_t tk = static_cast<int64_t>(b_) * sh.S + qb_ * kRowsB + r;
-            const uint4* a4 = reinterpret_cast<const uint4*>(o + tk * sh.ldo + h_ * HD);
-            const uint4* c4 = reinterpret_cast<const uint4*>(dout + tk * sh.ldo + h_ * HD);
+            const int c0 = h_ * HD + (kHalfRows ? half * (HD / 2) : 0);
+            const uint4* a4 = reinterpret_cast<const uint4*>(o + tk * sh.ldo + c0);
+            const uint4* c4 = reinterpret_cast<const uint4*>(dout + tk * sh.ldo + c0);
 #pragma unroll
-            for (int j = 0; j < HD / 8; ++j) {
+            for (int j = 0; j < NR; ++j) {
                 ro[j] = in ? __ldg(a4 + j) : make_uint4(0u, 0u, 0u, 0u);
                 rd[j] = in ? __ldg(c4 + j) : make_uint4(0u, 0u, 0u, 0u);
             }
@@ -381,13 +388,12 @@ __global__ void __launch_bounds__(kThreadsB, 1)
             const int64_t li = (static_cast<int64_t>(b) * sh.H + h) * sh.S + qi;
             const bool q_in = qi < sh.S;
             const float L = q_in ? lse[li] : 0.0f;
-            // delta = sum_d dO . O of this row (both halves compute it identically; half 0 stores
-            // it), from rows prefetched into registers during the previous tile (head_dim 64)
-            constexpr bool kPrefetch = HD == 64;
-            if (!kPrefetch || t == static_cast<int>(blockIdx.x)) load_rows(t);
+            // delta = sum_d dO . O of this row (half 0 stores it), from rows prefetched into
+            // registers during the previous tile
+            if (t == static_cast<int>(blockIdx.x)) load_rows(t);
             float Dl = 0.0f;
 #pragma unroll
-            for (int j = 0; j < HD / 8; ++j) {
+            for (int j = 0; j < NR; ++j) {
                 const uint32_t wa[4] = {ro[j].x, ro[j].y, ro[j].z, ro[j].w}, wc[4] = {rd[j].x, rd[j].y, rd[j].z, rd[j].w};
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
@@ -396,7 +402,12 @@ __global__ void __launch_bounds__(kThreadsB, 1)
                     Dl += fa.x * fc.x + fa.y * fc.y;
                 }
             }
-            if (kPrefetch && t + static_cast<int>(gridDim.x) < n_tiles) load_rows(t + gridDim.x);
+            if (t + static_cast<int>(gridDim.x) < n_tiles) load_rows(t + gridDim.x);
+            if (kHalfRows) {  // the row's two halves (warps q4 of both warpgroups) meet
+                xdl[lt & 1][half][r] = Dl;
+                asm volatile("bar.sync %0, 64;" ::"r"(1 + q4) : "memory");
+                Dl = xdl[lt & 1][0][r] + xdl[lt & 1][1][r];
+            }
             if (half == 0 && q_in) delta[li] = Dl;
             const int n = steps(qb);
             for (int j = 0; j < n; ++j, ++g) {
