@@ -401,9 +401,13 @@ struct Fwd2Cfg {
     // columns (5 K steps of 16 for QK^T, N = 80 for PV); the rest of the second atom (the next
     // head's columns, or TMA zero fill past the row) is loaded but never multiplied
     static constexpr int ATOMS = (HD + 63) / 64;
-    static constexpr int Q_BYTES = kQ * ATOMS * 64 * 2;
-    static constexpr int KV_BYTES = kKV * ATOMS * 64 * 2;
-    static constexpr int ST = HD <= 64 ? 3 : 2;  // K / V ring
+    // head_dim 80: the 16 columns past the first atom are loaded alone, as a 32-byte-swizzled
+    // [rows][16] tile (TMA box {16, rows}), instead of a whole second 64-column atom: 160 instead
+    // of 256 bytes per row of Q / K / V, and the ring gets a third stage in the saved space
+    static constexpr bool NARROW = HD % 64 == 16;
+    static constexpr int Q_BYTES = NARROW ? kQ * (128 + 32) : kQ * ATOMS * 64 * 2;
+    static constexpr int KV_BYTES = NARROW ? kKV * (128 + 32) : kKV * ATOMS * 64 * 2;
+    static constexpr int ST = (HD <= 64 || NARROW) ? 3 : 2;  // K / V ring
     static constexpr int SMEM = 2 * Q_BYTES + 2 * ST * KV_BYTES + 1024 + 512;  // (+ 3 KB static exchange)
     static constexpr uint32_t T_O = 256;
 };
@@ -453,6 +457,7 @@ __device__ __forceinline__ void named_bar_sync(int id, int threads) {
 template <int HD, bool LAZY>
 __global__ void __launch_bounds__(kThreadsF2, 1)
     attn_fwd_tc2_kernel(const __grid_constant__ CUtensorMap tmQK, const __grid_constant__ CUtensorMap tmV,
+                        const __grid_constant__ CUtensorMap tmQK1, const __grid_constant__ CUtensorMap tmV1,
                         __nv_bfloat16* __restrict__ o, float* __restrict__ lse, TcShape sh, int n_seq) {
     using C = Fwd2Cfg<HD>;
     extern __shared__ uint8_t smem_raw[];
@@ -521,9 +526,14 @@ __global__ void __launch_bounds__(kThreadsF2, 1)
                 const int qbuf = lt & 1;
                 mbar_wait(&q_empty[qbuf], ((lt >> 1) & 1) ^ 1);
                 mbar_expect_tx(&q_full[qbuf], C::Q_BYTES);
-                for (int a = 0; a < C::ATOMS; ++a)
-                    tma_load_2d(&tmQK, &q_full[qbuf], sQ + qbuf * C::Q_BYTES + a * kQ * 128, qcol + 64 * a,
-                                row0 + w.qb * kQ);
+                if (C::NARROW) {
+                    tma_load_2d(&tmQK, &q_full[qbuf], sQ + qbuf * C::Q_BYTES, qcol, row0 + w.qb * kQ);
+                    tma_load_2d(&tmQK1, &q_full[qbuf], sQ + qbuf * C::Q_BYTES + kQ * 128, qcol + 64, row0 + w.qb * kQ);
+                } else {
+                    for (int a = 0; a < C::ATOMS; ++a)
+                        tma_load_2d(&tmQK, &q_full[qbuf], sQ + qbuf * C::Q_BYTES + a * kQ * 128, qcol + 64 * a,
+                                    row0 + w.qb * kQ);
+                }
                 const int n_kb = blocks_of(w.qb);
                 for (int j = 0; j < n_kb; ++j, ++g) {
                     const int st = g % C::ST;
@@ -532,10 +542,19 @@ __global__ void __launch_bounds__(kThreadsF2, 1)
                     const int k0 = row0 + j * kKV;
                     uint8_t* k = sK + st * C::KV_BYTES;
                     uint8_t* v = sV + st * C::KV_BYTES;
-                    for (int a = 0; a < C::ATOMS; ++a) tma_load_2d(&tmQK, &kv_full[st], k + a * kKV * 128, kcol + 64 * a, k0);
-                    for (int kb = 0; kb < 2; ++kb)
-                        for (int a = 0; a < C::ATOMS; ++a)
-                            tma_load_2d(&tmV, &kv_full[st], v + (kb * C::ATOMS + a) * 8192, vcol + 64 * a, k0 + 64 * kb);
+                    if (C::NARROW) {  // K: [128][64] + [128][16]; V: [2][64][64] + [2][64][16]
+                        tma_load_2d(&tmQK, &kv_full[st], k, kcol, k0);
+                        tma_load_2d(&tmQK1, &kv_full[st], k + kKV * 128, kcol + 64, k0);
+                        for (int kb = 0; kb < 2; ++kb) {
+                            tma_load_2d(&tmV, &kv_full[st], v + kb * 8192, vcol, k0 + 64 * kb);
+                            tma_load_2d(&tmV1, &kv_full[st], v + 16384 + kb * 2048, vcol + 64, k0 + 64 * kb);
+                        }
+                    } else {
+                        for (int a = 0; a < C::ATOMS; ++a) tma_load_2d(&tmQK, &kv_full[st], k + a * kKV * 128, kcol + 64 * a, k0);
+                        for (int kb = 0; kb < 2; ++kb)
+                            for (int a = 0; a < C::ATOMS; ++a)
+                                tma_load_2d(&tmV, &kv_full[st], v + (kb * C::ATOMS + a) * 8192, vcol + 64 * a, k0 + 64 * kb);
+                    }
                 }
             }
         }
@@ -545,6 +564,7 @@ __global__ void __launch_bounds__(kThreadsF2, 1)
             // ===== MMA issuer =====
             constexpr uint32_t IDESC_S = make_idesc(kQ, kKV, false, false);
             constexpr uint32_t IDESC_O = make_idesc(kQ, HD, false, true);
+            constexpr uint32_t IDESC_O64 = make_idesc(kQ, 64, false, true), IDESC_O16 = make_idesc(kQ, 16, false, true);
             auto issue_s = [&](int g, uint32_t q_base) {
                 const int st = g % C::ST, sb = g & 1;
                 mbar_wait(&kv_full[st], (g / C::ST) & 1);
@@ -554,8 +574,12 @@ __global__ void __launch_bounds__(kThreadsF2, 1)
 #pragma unroll
                 for (int kk = 0; kk < HD / 16; ++kk) {
                     const int a = kk / 4, w = kk % 4;
-                    const uint64_t ad = make_desc(q_base + a * kQ * 128 + w * 32, 16, 1024);
-                    const uint64_t bd = make_desc(k_base + a * kKV * 128 + w * 32, 16, 1024);
+                    // (NARROW: columns 64..79 are the 32B-swizzled [rows][16] tiles, 8-row groups 256 B apart)
+                    const bool tail = C::NARROW && a == 1;
+                    const uint64_t ad = tail ? make_desc(q_base + kQ * 128, 16, 256, 6)
+                                             : make_desc(q_base + a * kQ * 128 + w * 32, 16, 1024);
+                    const uint64_t bd = tail ? make_desc(k_base + kKV * 128, 16, 256, 6)
+                                             : make_desc(k_base + a * kKV * 128 + w * 32, 16, 1024);
                     umma_if(leader, tmem + sb * 128, ad, bd, IDESC_S, kk > 0 ? 1u : 0u);
                 }
                 umma_commit_if(leader, &s_full[sb]);
@@ -573,8 +597,18 @@ __global__ void __launch_bounds__(kThreadsF2, 1)
                     // P of keys 16 kk .. 16 kk + 15: half kk / 4 wrote its 64 keys as 32 packed
                     // columns at 128 sb + 64 half
                     const uint32_t pcol = static_cast<uint32_t>(sb * 128 + (kk / 4) * 64 + (kk % 4) * 8);
-                    const uint64_t bd = make_desc(v_base + (kk / 4) * C::ATOMS * 8192 + (kk % 4) * 16 * 128, 8192, 1024);
-                    umma_ts_if(leader, tmem + C::T_O + ob * HD, tmem + pcol, bd, IDESC_O, (kk > 0 || (LAZY && j > 0)) ? 1u : 0u);
+                    const uint32_t acc = (kk > 0 || (LAZY && j > 0)) ? 1u : 0u;
+                    if (C::NARROW) {
+                        // O columns 0..63 from V's 128B-swizzled atom, 64..79 from its [64][16]
+                        // 32B-swizzled tail (MN-major, one 16-column atom, 8-key groups 256 B apart)
+                        const uint64_t bd0 = make_desc(v_base + (kk / 4) * 8192 + (kk % 4) * 16 * 128, 8192, 1024);
+                        const uint64_t bd1 = make_desc(v_base + 16384 + (kk / 4) * 2048 + (kk % 4) * 16 * 32, 256, 256, 6);
+                        umma_ts_if(leader, tmem + C::T_O + ob * HD, tmem + pcol, bd0, IDESC_O64, acc);
+                        umma_ts_if(leader, tmem + C::T_O + ob * HD + 64, tmem + pcol, bd1, IDESC_O16, acc);
+                    } else {
+                        const uint64_t bd = make_desc(v_base + (kk / 4) * C::ATOMS * 8192 + (kk % 4) * 16 * 128, 8192, 1024);
+                        umma_ts_if(leader, tmem + C::T_O + ob * HD, tmem + pcol, bd, IDESC_O, acc);
+                    }
                 }
                 if (!LAZY || j + 1 == n_kb) umma_commit_if(leader, &o_full[ob]);
                 umma_commit_if(leader, &pv_done[sb]);
@@ -834,6 +868,12 @@ cudaError_t launch_fwd_tc2(const AttnProblem& a, cudaStream_t st) {
         !make_map(&tv, a.qkv, static_cast<uint64_t>(ld), static_cast<uint64_t>(a.tokens), static_cast<uint64_t>(ld), 64, 64,
                   false, false))
         return cudaErrorInvalidValue;
+    CUtensorMap tqk1 = tqk, tv1 = tv;  // head_dim 80: the 16-column tails (32B swizzle)
+    if (C::NARROW && (!make_map_sw32(&tqk1, a.qkv, static_cast<uint64_t>(ld), static_cast<uint64_t>(a.tokens),
+                                     static_cast<uint64_t>(ld), 16, 128) ||
+                      !make_map_sw32(&tv1, a.qkv, static_cast<uint64_t>(ld), static_cast<uint64_t>(a.tokens),
+                                     static_cast<uint64_t>(ld), 16, 64)))
+        return cudaErrorInvalidValue;
     TcShape sh;
     sh.S = a.seq_len;
     sh.H = a.n_heads;
@@ -846,7 +886,7 @@ cudaError_t launch_fwd_tc2(const AttnProblem& a, cudaStream_t st) {
     const int n_seq = static_cast<int>(a.tokens / a.seq_len);
     const int tiles = ((a.seq_len + kQ - 1) / kQ) * a.n_heads * n_seq;
     const int grid = tiles < num_sms() ? tiles : num_sms();
-    attn_fwd_tc2_kernel<HD, LAZY><<<grid, kThreadsF2, C::SMEM, st>>>(tqk, tv, static_cast<__nv_bfloat16*>(a.o), a.lse, sh,
+    attn_fwd_tc2_kernel<HD, LAZY><<<grid, kThreadsF2, C::SMEM, st>>>(tqk, tv, tqk1, tv1, static_cast<__nv_bfloat16*>(a.o), a.lse, sh,
                                                                 n_seq);
     return cudaGetLastError();
 }

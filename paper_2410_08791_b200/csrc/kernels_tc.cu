@@ -1243,6 +1243,22 @@ bool make_map(CUtensorMap* m, const MapDesc& k) {
 
 // Operand [outer][ld] (inner contiguous; bf16, or fp32 for tf32), 128B-swizzled box
 // {box_inner, box_outer}
+bool make_map_sw32(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint64_t ld,
+                   uint32_t box_inner, uint32_t box_outer) {
+    MapDesc k{};
+    k.dtype = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+    k.rank = 2;
+    k.base = base;
+    k.dims[0] = inner;
+    k.dims[1] = outer;
+    k.dims[2] = 1;
+    k.strides[0] = ld * 2;
+    k.box[0] = box_inner;
+    k.box[1] = box_outer;
+    k.box[2] = 1;
+    k.swizzle = CU_TENSOR_MAP_SWIZZLE_32B;
+    return make_map(m, k);
+}
 bool make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint64_t ld,
               uint32_t box_inner, uint32_t box_outer, bool f32, bool base32) {
     MapDesc k{};

@@ -215,6 +215,9 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
 // {box_inner, box_outer}; cached per (address, shape, box) (kernels_tc.cu)
 bool make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint64_t ld,
               uint32_t box_inner, uint32_t box_outer, bool f32, bool base32);
+// the same over bf16 with the 32-byte swizzle (box_inner <= 16 elements)
+bool make_map_sw32(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint64_t ld,
+                   uint32_t box_inner, uint32_t box_outer);
 
 
 // Attention work order for causal masks (kernels_attn_tc.cu / kernels_attn_bwd.cu): chunks of
