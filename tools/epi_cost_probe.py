@@ -1,7 +1,7 @@
 """Cost of the fused epilogues at the GPT-2 XL block's GEMM shapes (16 x 1024 tokens): the same
 mainloop with each epilogue the block uses, against a plain fp32 / bf16 store and torch.matmul
 (cuBLAS, context only). Back-to-back launches between CUDA events. Prints one JSON line per case.
-Usage: python tools/epi_cost_probe.py"""
+Usage: python tools/epi_cost_probe.py [vit]   (vit: ViT-H/14 at 256 x 257 tokens, exact-erf GELU)"""
 import ctypes as C
 import json
 import os
@@ -14,7 +14,9 @@ from paper_2410_08791_b200 import _capi  # noqa: E402
 
 LIB = _capi.LIB
 BIAS_BF16, GATE_BF16, F32, RESID_F32, GELU_BF16, GELU_GATE_BF16 = 0, 2, 3, 6, 7, 8
-T, D, FF, Q = 16384, 1600, 6400, 4800
+VIT = len(sys.argv) > 1 and sys.argv[1] == "vit"
+T, D, FF, Q = (65792, 1280, 5120, 3840) if VIT else (16384, 1600, 6400, 4800)
+ACT = 1 if VIT else 0  # GELU_ERF / GELU_TANH
 st = torch.cuda.current_stream().cuda_stream
 
 
@@ -67,7 +69,7 @@ def run(name, M, N, K, A, lda, a_mn, B, ldb, b_mn, epi, out, ldo, bias=None, gat
     args = _capi.GemmArgs(M, N, K, A.data_ptr(), lda, a_mn, B.data_ptr(), ldb, b_mn, epi, out.data_ptr(), ldo,
                           bias.data_ptr() if bias is not None else None, 0,
                           gate.data_ptr() if gate is not None else None, ldg, 1, 0, 0,
-                          aux.data_ptr() if aux is not None else None, ldaux, 0, st)
+                          aux.data_ptr() if aux is not None else None, ldaux, ACT, st)
 
     def f():
         rc = LIB.sp_debug_gemm_ex(C.byref(args))
