@@ -94,6 +94,10 @@ __device__ __forceinline__ uint32_t ts_col(int kk) {
 }
 // a descriptor advanced by `bytes` (the 14-bit start field cannot carry: smem < 256 KB)
 __device__ __forceinline__ uint64_t dadd(uint64_t d, uint32_t bytes) { return d + (bytes >> 4); }
+// head_dim 80's 16-column tails: 32B swizzle (layout 6), 8-row groups 256 bytes apart; K-major
+// (the last K step of QK^T-like products) or, as one 16-column MN-major atom, the N = 16 half
+// of the products against the streamed tile
+__device__ __forceinline__ uint64_t tail_desc(uint32_t saddr) { return make_desc(saddr, 256, 256, 6); }
 
 struct BShape {
     int S, H, Hkv, ld, ldo, causal, chunk;  // chunk: causal work order (causal_chunked)
@@ -104,11 +108,16 @@ template <int HD>
 struct BCfg {
     // head_dim 80 (ViT-H/14) takes two 64-column atoms; the MMAs read the first HD columns only
     static constexpr int ATOMS = (HD + 63) / 64;
-    static constexpr int BIG = kRowsB * ATOMS * 128;    // a 128-row tile (ATOMS atoms of 16 KB)
-    static constexpr int SMALL = kStepB * ATOMS * 128;  // a 64-row tile (ATOMS atoms of 8 KB)
-    static constexpr int A_BIG = kRowsB * 128, A_SMALL = kStepB * 128;
-    static constexpr int ST = HD == 64 ? 8 : 3;         // streamed-tile stages
-    static constexpr int OWN = HD == 64 ? 2 : 1;        // own-tile stages (next tile prefetch)
+    // head_dim 80: the 16 columns past the first atom are a 32B-swizzled [rows][16] tile (own
+    // TMA maps), not a second 64-column atom: 160 instead of 256 bytes per row
+    static constexpr bool NARROW = HD % 64 == 16;
+    static constexpr int BIG = NARROW ? kRowsB * (128 + 32) : kRowsB * ATOMS * 128;    // a 128-row tile
+    static constexpr int SMALL = NARROW ? kStepB * (128 + 32) : kStepB * ATOMS * 128;  // a 64-row tile
+    static constexpr int A_BIG = kRowsB * 128, A_SMALL = kStepB * 128;  // the second atom / the tail
+    static constexpr int ST = HD == 64 ? 8 : 3;                 // streamed-tile stages
+    // own-tile stages (next tile prefetch): head_dim 80's narrow tiles make room for the second
+    // (ViT backward 1154 -> 1100 us; six streamed stages instead measured slower, 1156-1190 us)
+    static constexpr int OWN = (HD == 64 || NARROW) ? 2 : 1;
     // dK/dV pass: P / dS written back over S / dP in NB_DKDV buffers. Three buffers at head_dim
     // 64 (dK, dV from column 384) let a warpgroup's next step start without waiting for its
     // previous step's products (the separate-region double-buffered form, SEP, waited there:
@@ -181,7 +190,9 @@ __device__ __forceinline__ void acc_row_out(uint32_t taddr, __nv_bfloat16* dst, 
 template <int HD>
 __global__ void __launch_bounds__(kThreadsB, 1)
     attn_bwd_dq2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmDO,
-                        const __grid_constant__ CUtensorMap tmKV, const __nv_bfloat16* __restrict__ o,
+                        const __grid_constant__ CUtensorMap tmKV, const __grid_constant__ CUtensorMap tmQ1,
+                        const __grid_constant__ CUtensorMap tmDO1, const __grid_constant__ CUtensorMap tmKV1,
+                        const __nv_bfloat16* __restrict__ o,
                         const __nv_bfloat16* __restrict__ dout, const float* __restrict__ lse,
                         float* __restrict__ delta, __nv_bfloat16* __restrict__ dqkv, BShape sh, int n_seq,
                         float* __restrict__ csum) {
@@ -272,8 +283,9 @@ __global__ void __launch_bounds__(kThreadsB, 1)
                 mbar_wait(&q_empty[ob], ((lt / C::OWN) & 1) ^ 1);
                 mbar_expect_tx(&q_full[ob], 2 * C::BIG);
                 for (int a = 0; a < C::ATOMS; ++a) {
-                    tma_load_2d(&tmQ, &q_full[ob], sQ + ob * C::BIG + a * C::A_BIG, h * HD + 64 * a, row0 + qb * kRowsB);
-                    tma_load_2d(&tmDO, &q_full[ob], sDO + ob * C::BIG + a * C::A_BIG, h * HD + 64 * a,
+                    tma_load_2d(C::NARROW && a ? &tmQ1 : &tmQ, &q_full[ob], sQ + ob * C::BIG + a * C::A_BIG, h * HD + 64 * a,
+                                row0 + qb * kRowsB);
+                    tma_load_2d(C::NARROW && a ? &tmDO1 : &tmDO, &q_full[ob], sDO + ob * C::BIG + a * C::A_BIG, h * HD + 64 * a,
                                 row0 + qb * kRowsB);
                 }
                 const int kcol = (sh.H + kvh) * HD, vcol = (sh.H + sh.Hkv + kvh) * HD;
@@ -283,10 +295,10 @@ __global__ void __launch_bounds__(kThreadsB, 1)
                     mbar_wait(&kv_empty[st], ((g / C::ST) & 1) ^ 1);
                     mbar_expect_tx(&kv_full[st], 2 * C::SMALL);
                     for (int a = 0; a < C::ATOMS; ++a) {
-                        tma_load_2d(&tmKV, &kv_full[st], sK + st * C::SMALL + a * C::A_SMALL, kcol + 64 * a,
-                                    row0 + j * kStepB);
-                        tma_load_2d(&tmKV, &kv_full[st], sV + st * C::SMALL + a * C::A_SMALL, vcol + 64 * a,
-                                    row0 + j * kStepB);
+                        tma_load_2d(C::NARROW && a ? &tmKV1 : &tmKV, &kv_full[st], sK + st * C::SMALL + a * C::A_SMALL,
+                                    kcol + 64 * a, row0 + j * kStepB);
+                        tma_load_2d(C::NARROW && a ? &tmKV1 : &tmKV, &kv_full[st], sV + st * C::SMALL + a * C::A_SMALL,
+                                    vcol + 64 * a, row0 + j * kStepB);
                     }
                 }
             }
@@ -296,7 +308,9 @@ __global__ void __launch_bounds__(kThreadsB, 1)
             const uint32_t leader = elect_one();  // ===== MMA issuer =====
             constexpr uint32_t ID_S = make_idesc(128, kStepB, false, false);
             constexpr uint32_t ID_D = make_idesc(128, HD, false, true);
+            constexpr uint32_t ID_D64 = make_idesc(128, 64, false, true), ID_D16 = make_idesc(128, 16, false, true);
             uint64_t dq_, ddo_;  // the tile's Q / dO descriptors (K-major, k step 0)
+            uint32_t q_own = 0, do_own = 0;  // (their shared addresses: the tails)
             // S / dP of step gg into buffer gg & 1, once the softmax warps have loaded step gg - 2's
             auto issue_s = [&](int gg) {
                 const int st = gg % C::ST, bb = gg & 1;
@@ -308,8 +322,15 @@ __global__ void __launch_bounds__(kThreadsB, 1)
 #pragma unroll
                 for (int kk = 0; kk < HD / 16; ++kk) {
                     const uint32_t ob = (kk / 4) * C::A_BIG + (kk % 4) * 32, sb = (kk / 4) * C::A_SMALL + (kk % 4) * 32;
-                    umma_if(leader, tmem + 128 * bb, dadd(dq_, ob), dadd(dk, sb), ID_S, kk > 0);
-                    umma_if(leader, tmem + 128 * bb + 64, dadd(ddo_, ob), dadd(dv, sb), ID_S, kk > 0);
+                    if (C::NARROW && kk == 4) {
+                        umma_if(leader, tmem + 128 * bb, tail_desc(q_own + C::A_BIG),
+                                tail_desc(smem_u32(sK + st * C::SMALL + C::A_SMALL)), ID_S, 1);
+                        umma_if(leader, tmem + 128 * bb + 64, tail_desc(do_own + C::A_BIG),
+                                tail_desc(smem_u32(sV + st * C::SMALL + C::A_SMALL)), ID_S, 1);
+                    } else {
+                        umma_if(leader, tmem + 128 * bb, dadd(dq_, ob), dadd(dk, sb), ID_S, kk > 0);
+                        umma_if(leader, tmem + 128 * bb + 64, dadd(ddo_, ob), dadd(dv, sb), ID_S, kk > 0);
+                    }
                 }
                 umma_commit_if(leader, &s_full[bb]);
             };
@@ -320,9 +341,18 @@ __global__ void __launch_bounds__(kThreadsB, 1)
                 fence_after();
                 const uint64_t dk = make_desc(smem_u32(sK + st * C::SMALL), C::A_SMALL, 1024);
 #pragma unroll
-                for (int kk = 0; kk < kStepB / 16; ++kk)
-                    umma_ts_if(leader, tmem + T_ACC, tmem + T_DS + 32 * bb + ts_col<true>(kk), dadd(dk, kk * 2048), ID_D,
-                            (!first || kk > 0) ? 1u : 0u);
+                for (int kk = 0; kk < kStepB / 16; ++kk) {
+                    const uint32_t acc = (!first || kk > 0) ? 1u : 0u;
+                    if (C::NARROW) {  // dQ columns 0..63 from K's atom, 64..79 from its tail
+                        umma_ts_if(leader, tmem + T_ACC, tmem + T_DS + 32 * bb + ts_col<true>(kk), dadd(dk, kk * 2048),
+                                   ID_D64, acc);
+                        umma_ts_if(leader, tmem + T_ACC + 64, tmem + T_DS + 32 * bb + ts_col<true>(kk),
+                                   tail_desc(smem_u32(sK + st * C::SMALL + C::A_SMALL) + kk * 512), ID_D16, acc);
+                    } else {
+                        umma_ts_if(leader, tmem + T_ACC, tmem + T_DS + 32 * bb + ts_col<true>(kk), dadd(dk, kk * 2048), ID_D,
+                                   acc);
+                    }
+                }
                 umma_commit_if(leader, &ds_free[bb]);
                 umma_commit_if(leader, &kv_empty[st]);
             };
@@ -333,8 +363,10 @@ __global__ void __launch_bounds__(kThreadsB, 1)
                 const int n = steps(qb);
                 const int ob = lt % C::OWN;
                 mbar_wait(&q_full[ob], (lt / C::OWN) & 1);
-                dq_ = make_desc(smem_u32(sQ + ob * C::BIG), 16, 1024);
-                ddo_ = make_desc(smem_u32(sDO + ob * C::BIG), 16, 1024);
+                q_own = smem_u32(sQ + ob * C::BIG);
+                do_own = smem_u32(sDO + ob * C::BIG);
+                dq_ = make_desc(q_own, 16, 1024);
+                ddo_ = make_desc(do_own, 16, 1024);
                 for (int i = 0; i < 2 && i < n; ++i) issue_s(g + i);  // (one step: a sequence <= 64 keys)
                 mbar_wait(acc_empty, (lt & 1) ^ 1);  // the previous tile's dQ is read out
                 fence_after();
@@ -480,7 +512,9 @@ __global__ void __launch_bounds__(kThreadsB, 1)
 template <int HD, bool SEP, int NB, bool TRACE = false>
 __global__ void __launch_bounds__(kThreadsB, 1)
     attn_bwd_dkdv2_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmQ,
-                          const __grid_constant__ CUtensorMap tmDO, const float* __restrict__ lse,
+                          const __grid_constant__ CUtensorMap tmDO, const __grid_constant__ CUtensorMap tmK1,
+                          const __grid_constant__ CUtensorMap tmQ1, const __grid_constant__ CUtensorMap tmDO1,
+                          const float* __restrict__ lse,
                           const float* __restrict__ delta, __nv_bfloat16* __restrict__ dqkv, BShape sh, int n_seq,
                           float* __restrict__ csum) {
     using C = BCfg<HD>;
@@ -584,8 +618,10 @@ __global__ void __launch_bounds__(kThreadsB, 1)
                 mbar_wait(&kv_empty[ob], ((lt / C::OWN) & 1) ^ 1);
                 mbar_expect_tx(&kv_full[ob], 2 * C::BIG);
                 for (int a = 0; a < C::ATOMS; ++a) {
-                    tma_load_2d(&tmK, &kv_full[ob], sK + ob * C::BIG + a * C::A_BIG, kcol + 64 * a, row0 + kb * kRowsB);
-                    tma_load_2d(&tmK, &kv_full[ob], sV + ob * C::BIG + a * C::A_BIG, vcol + 64 * a, row0 + kb * kRowsB);
+                    tma_load_2d(C::NARROW && a ? &tmK1 : &tmK, &kv_full[ob], sK + ob * C::BIG + a * C::A_BIG, kcol + 64 * a,
+                                row0 + kb * kRowsB);
+                    tma_load_2d(C::NARROW && a ? &tmK1 : &tmK, &kv_full[ob], sV + ob * C::BIG + a * C::A_BIG, vcol + 64 * a,
+                                row0 + kb * kRowsB);
                 }
                 const int n = group * per_head(kb);
                 for (int j = 0; j < n; ++j, ++g) {
@@ -602,10 +638,10 @@ __global__ void __launch_bounds__(kThreadsB, 1)
                     const uint32_t lbytes = static_cast<uint32_t>((off + nvalid + 3) / 4 * 16);
                     mbar_expect_tx(&q_full[st], 2 * C::SMALL + 2 * lbytes);
                     for (int a = 0; a < C::ATOMS; ++a) {
-                        tma_load_2d(&tmQ, &q_full[st], sQ + st * C::SMALL + a * C::A_SMALL, hq * HD + 64 * a,
-                                    row0 + qs * kStepB);
-                        tma_load_2d(&tmDO, &q_full[st], sDO + st * C::SMALL + a * C::A_SMALL, hq * HD + 64 * a,
-                                    row0 + qs * kStepB);
+                        tma_load_2d(C::NARROW && a ? &tmQ1 : &tmQ, &q_full[st], sQ + st * C::SMALL + a * C::A_SMALL,
+                                    hq * HD + 64 * a, row0 + qs * kStepB);
+                        tma_load_2d(C::NARROW && a ? &tmDO1 : &tmDO, &q_full[st], sDO + st * C::SMALL + a * C::A_SMALL,
+                                    hq * HD + 64 * a, row0 + qs * kStepB);
                     }
                     bulk_load_b(sL + st * kLStride, lse + (li - off), lbytes, &q_full[st]);
                     bulk_load_b(sD + st * kLStride, delta + (li - off), lbytes, &q_full[st]);
@@ -617,7 +653,9 @@ __global__ void __launch_bounds__(kThreadsB, 1)
             const uint32_t leader = elect_one();  // ===== MMA issuer =====
             constexpr uint32_t ID_S = make_idesc(128, kStepB, false, false);
             constexpr uint32_t ID_D = make_idesc(128, HD, false, true);
+            constexpr uint32_t ID_D64 = make_idesc(128, 64, false, true), ID_D16 = make_idesc(128, 16, false, true);
             uint64_t dk_, dv_;  // the tile's K / V descriptors (K-major, k step 0)
+            uint32_t k_own = 0, v_own = 0;  // (their shared addresses: the tails)
             auto issue_s = [&](int gg) {
                 const int st = gg % C::ST, bb = gg % NB;
                 if (leader) trace_ev<TRACE>(0, gg);
@@ -630,8 +668,15 @@ __global__ void __launch_bounds__(kThreadsB, 1)
 #pragma unroll
                 for (int kk = 0; kk < HD / 16; ++kk) {
                     const uint32_t ob = (kk / 4) * C::A_BIG + (kk % 4) * 32, sb = (kk / 4) * C::A_SMALL + (kk % 4) * 32;
-                    umma_if(leader, tmem + 128 * bb, dadd(dk_, ob), dadd(dq, sb), ID_S, kk > 0);
-                    umma_if(leader, tmem + 128 * bb + 64, dadd(dv_, ob), dadd(ddo, sb), ID_S, kk > 0);
+                    if (C::NARROW && kk == 4) {
+                        umma_if(leader, tmem + 128 * bb, tail_desc(k_own + C::A_BIG),
+                                tail_desc(smem_u32(sQ + st * C::SMALL + C::A_SMALL)), ID_S, 1);
+                        umma_if(leader, tmem + 128 * bb + 64, tail_desc(v_own + C::A_BIG),
+                                tail_desc(smem_u32(sDO + st * C::SMALL + C::A_SMALL)), ID_S, 1);
+                    } else {
+                        umma_if(leader, tmem + 128 * bb, dadd(dk_, ob), dadd(dq, sb), ID_S, kk > 0);
+                        umma_if(leader, tmem + 128 * bb + 64, dadd(dv_, ob), dadd(ddo, sb), ID_S, kk > 0);
+                    }
                 }
                 umma_commit_if(leader, &s_full[bb]);
             };
@@ -646,8 +691,19 @@ __global__ void __launch_bounds__(kThreadsB, 1)
 #pragma unroll
                 for (int kk = 0; kk < kStepB / 16; ++kk) {
                     const uint32_t acc = (!first || kk > 0) ? 1u : 0u;
-                    umma_ts_if(leader, tmem + T_ACC, tmem + ds_col(bb) + ts_col<SEP>(kk), dadd(dq, kk * 2048), ID_D, acc);
-                    umma_ts_if(leader, tmem + T_ACC + HD, tmem + p_col(bb) + ts_col<SEP>(kk), dadd(ddo, kk * 2048), ID_D, acc);
+                    if (C::NARROW) {  // dK / dV columns 0..63 from Q's / dO's atom, 64..79 from the tails
+                        umma_ts_if(leader, tmem + T_ACC, tmem + ds_col(bb) + ts_col<SEP>(kk), dadd(dq, kk * 2048), ID_D64, acc);
+                        umma_ts_if(leader, tmem + T_ACC + 64, tmem + ds_col(bb) + ts_col<SEP>(kk),
+                                   tail_desc(smem_u32(sQ + st * C::SMALL + C::A_SMALL) + kk * 512), ID_D16, acc);
+                        umma_ts_if(leader, tmem + T_ACC + HD, tmem + p_col(bb) + ts_col<SEP>(kk), dadd(ddo, kk * 2048), ID_D64,
+                                   acc);
+                        umma_ts_if(leader, tmem + T_ACC + HD + 64, tmem + p_col(bb) + ts_col<SEP>(kk),
+                                   tail_desc(smem_u32(sDO + st * C::SMALL + C::A_SMALL) + kk * 512), ID_D16, acc);
+                    } else {
+                        umma_ts_if(leader, tmem + T_ACC, tmem + ds_col(bb) + ts_col<SEP>(kk), dadd(dq, kk * 2048), ID_D, acc);
+                        umma_ts_if(leader, tmem + T_ACC + HD, tmem + p_col(bb) + ts_col<SEP>(kk), dadd(ddo, kk * 2048), ID_D,
+                                   acc);
+                    }
                 }
                 if (SEP) umma_commit_if(leader, &ds_free[bb]);
                 umma_commit_if(leader, &q_empty[st]);
@@ -659,8 +715,10 @@ __global__ void __launch_bounds__(kThreadsB, 1)
                 const int n = group * per_head(kb);
                 const int ob = lt % C::OWN;
                 mbar_wait(&kv_full[ob], (lt / C::OWN) & 1);
-                dk_ = make_desc(smem_u32(sK + ob * C::BIG), 16, 1024);
-                dv_ = make_desc(smem_u32(sV + ob * C::BIG), 16, 1024);
+                k_own = smem_u32(sK + ob * C::BIG);
+                v_own = smem_u32(sV + ob * C::BIG);
+                dk_ = make_desc(k_own, 16, 1024);
+                dv_ = make_desc(v_own, 16, 1024);
                 for (int i = 0; i < NB && i < n; ++i) issue_s(g + i);
                 mbar_wait(acc_empty, (lt & 1) ^ 1);  // the previous tile's dK / dV are read out
                 fence_after();
@@ -817,6 +875,11 @@ cudaError_t launch_bwd2(const AttnProblem& a, cudaStream_t st) {
         !make_map(&do128, a.dout, ldo, T, ldo, 64, kRowsB, false, false) ||
         !make_map(&do64, a.dout, ldo, T, ldo, 64, kStepB, false, false))
         return cudaErrorInvalidValue;
+    CUtensorMap n128 = t128, n64 = t64, ndo128 = do128, ndo64 = do64;  // head_dim 80: the 16-column tails
+    if (C::NARROW && (!make_map_sw32(&n128, a.qkv, ld, T, ld, 16, kRowsB) || !make_map_sw32(&n64, a.qkv, ld, T, ld, 16, kStepB) ||
+                      !make_map_sw32(&ndo128, a.dout, ldo, T, ldo, 16, kRowsB) ||
+                      !make_map_sw32(&ndo64, a.dout, ldo, T, ldo, 16, kStepB)))
+        return cudaErrorInvalidValue;
     BShape sh;
     sh.S = a.seq_len;
     sh.H = a.n_heads;
@@ -834,7 +897,7 @@ cudaError_t launch_bwd2(const AttnProblem& a, cudaStream_t st) {
     auto* dq = static_cast<__nv_bfloat16*>(a.dqkv);
     float* cs = attention_colsum_fused(a) ? a.colsum_part : nullptr;
     attn_bwd_dq2_kernel<HD><<<q_tiles < num_sms() ? q_tiles : num_sms(), kThreadsB, C::SMEM_DQ, st>>>(
-        t128, do128, t64, static_cast<const __nv_bfloat16*>(a.o), static_cast<const __nv_bfloat16*>(a.dout), a.lse,
+        t128, do128, t64, n128, ndo128, n64, static_cast<const __nv_bfloat16*>(a.o), static_cast<const __nv_bfloat16*>(a.dout), a.lse,
         a.delta, dq, sh, n_seq, cs);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
@@ -848,11 +911,11 @@ cudaError_t launch_bwd2(const AttnProblem& a, cudaStream_t st) {
         const unsigned int zero = 0;
         cudaMemcpyToSymbolAsync(g_bwd_trace_n, &zero, sizeof(zero), 0, cudaMemcpyHostToDevice, st);
         attn_bwd_dkdv2_kernel<HD, SEP, C::NB_DKDV, true><<<kv_tiles < num_sms() ? kv_tiles : num_sms(), kThreadsB,
-                                                          C::SMEM_DKDV, st>>>(t128, t64, do64, a.lse, a.delta, dq, sh, n_seq, cs);
+                                                          C::SMEM_DKDV, st>>>(t128, t64, do64, n128, n64, ndo64, a.lse, a.delta, dq, sh, n_seq, cs);
         return cudaGetLastError();
     }
     attn_bwd_dkdv2_kernel<HD, SEP, C::NB_DKDV><<<kv_tiles < num_sms() ? kv_tiles : num_sms(), kThreadsB, C::SMEM_DKDV, st>>>(
-        t128, t64, do64, a.lse, a.delta, dq, sh, n_seq, cs);
+        t128, t64, do64, n128, n64, ndo64, a.lse, a.delta, dq, sh, n_seq, cs);
     return cudaGetLastError();
 }
 }  // namespace
