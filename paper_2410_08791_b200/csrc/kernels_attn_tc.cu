@@ -565,12 +565,15 @@ __global__ void __launch_bounds__(kThreadsF2, 1)
             constexpr uint32_t IDESC_S = make_idesc(kQ, kKV, false, false);
             constexpr uint32_t IDESC_O = make_idesc(kQ, HD, false, true);
             constexpr uint32_t IDESC_O64 = make_idesc(kQ, 64, false, true), IDESC_O16 = make_idesc(kQ, 16, false, true);
-            auto issue_s = [&](int g, uint32_t q_base) {
+            // nk: the block's keys inside the sequence; a ragged last block (ViT's 257th key)
+            // multiplies only ceil(nk / 16) * 16 of them (the softmax masks the rest anyway)
+            auto issue_s = [&](int g, uint32_t q_base, int nk) {
                 const int st = g % C::ST, sb = g & 1;
                 mbar_wait(&kv_full[st], (g / C::ST) & 1);
                 if (g >= 2) mbar_wait(&pv_done[sb], ((g - 2) >> 1) & 1);
                 fence_after();
                 const uint32_t k_base = smem_u32(sK + st * C::KV_BYTES);
+                const uint32_t idesc_s = nk >= kKV ? IDESC_S : make_idesc(kQ, (nk + 15) / 16 * 16, false, false);
 #pragma unroll
                 for (int kk = 0; kk < HD / 16; ++kk) {
                     const int a = kk / 4, w = kk % 4;
@@ -580,11 +583,11 @@ __global__ void __launch_bounds__(kThreadsF2, 1)
                                              : make_desc(q_base + a * kQ * 128 + w * 32, 16, 1024);
                     const uint64_t bd = tail ? make_desc(k_base + kKV * 128, 16, 256, 6)
                                              : make_desc(k_base + a * kKV * 128 + w * 32, 16, 1024);
-                    umma_if(leader, tmem + sb * 128, ad, bd, IDESC_S, kk > 0 ? 1u : 0u);
+                    umma_if(leader, tmem + sb * 128, ad, bd, idesc_s, kk > 0 ? 1u : 0u);
                 }
                 umma_commit_if(leader, &s_full[sb]);
             };
-            auto issue_o = [&](int g, int j, int n_kb, int lt) {
+            auto issue_o = [&](int g, int j, int n_kb, int lt, int nk) {
                 const int st = g % C::ST, sb = g & 1;
                 const int ob = LAZY ? (lt & 1) : sb;  // LAZY: one O per tile parity
                 mbar_wait(&p_full[sb], (g >> 1) & 1);
@@ -596,6 +599,7 @@ __global__ void __launch_bounds__(kThreadsF2, 1)
                 for (int kk = 0; kk < kKV / 16; ++kk) {
                     // P of keys 16 kk .. 16 kk + 15: half kk / 4 wrote its 64 keys as 32 packed
                     // columns at 128 sb + 64 half
+                    if (16 * kk >= nk) continue;  // keys past the sequence (P = 0 there)
                     const uint32_t pcol = static_cast<uint32_t>(sb * 128 + (kk / 4) * 64 + (kk % 4) * 8);
                     const uint32_t acc = (kk > 0 || (LAZY && j > 0)) ? 1u : 0u;
                     if (C::NARROW) {
@@ -622,11 +626,12 @@ __global__ void __launch_bounds__(kThreadsF2, 1)
                 mbar_wait(&q_full[qbuf], (lt >> 1) & 1);
                 fence_after();
                 const uint32_t q_base = smem_u32(sQ + qbuf * C::Q_BYTES);
-                issue_s(g, q_base);
+                auto keys = [&](int jj) { return min(kKV, sh.S - jj * kKV); };
+                issue_s(g, q_base, keys(0));
                 for (int j = 0; j < n_kb; ++j) {
-                    if (j + 1 < n_kb) issue_s(g + j + 1, q_base);
+                    if (j + 1 < n_kb) issue_s(g + j + 1, q_base, keys(j + 1));
                     if (j + 1 == n_kb) umma_commit_if(leader, &q_empty[qbuf]);
-                    issue_o(g + j, j, n_kb, lt);
+                    issue_o(g + j, j, n_kb, lt, keys(j));
                 }
                 g += n_kb;
             }
