@@ -1329,6 +1329,7 @@ bool make_epilogue_maps(const GemmProblem& g, int splits, CUtensorMap* to, CUten
 int g_epi_mode = 0;
 int g_narrow = 0;
 int g_raster = 0;  // CTA-pair rasterisation group, 0 = by shape (debug knob "raster")
+int g_dw_split_max = 0;  // cap on choose_dw's split count, 0 = none (debug knob "dw_split_max")
 
 // Epilogue kind: TMA staging for every epilogue but the fused SGD. At short K the epilogue is on
 // the critical path (+8..15% on the d=1280/1600 layer GEMMs, ncu, fixed clocks). At long K the
@@ -1564,6 +1565,7 @@ void set_gemm_debug(const char* key, int value, bool* known) {
     else if (std::strcmp(key, "attn_chunk") == 0) g_attn_chunk = value;
     else if (std::strcmp(key, "narrow") == 0) tc::g_narrow = value;
     else if (std::strcmp(key, "raster") == 0) tc::g_raster = value;
+    else if (std::strcmp(key, "dw_split_max") == 0) tc::g_dw_split_max = value;
     else *known = false;
 }
 
@@ -1625,6 +1627,7 @@ GemmChoice choose_gemm(int M, int N, int K, int splits, int epilogue, bool b_kma
 // 5 splits, 82.6 us); 65792 x 1280 -> pair, 256, 5 splits (161 us, 1337 TFLOP/s).
 // splits = 1 with fused_ok means the SGD is fused into the epilogue (no partials).
 DwChoice choose_dw(int M, int N, int K, int max_splits, bool fused_ok, bool tf32) {
+    if (tc::g_dw_split_max > 0 && max_splits > tc::g_dw_split_max) max_splits = tc::g_dw_split_max;
     const int sms = num_sms();
     const int bke = tf32 ? tc::BK / 2 : tc::BK;  // K elements per k-block
     const int kb = (K + bke - 1) / bke;
