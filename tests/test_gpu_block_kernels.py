@@ -221,6 +221,33 @@ def test_attention_forward_and_backward(B, S, H, Hkv, hd, causal, fwd_kind, bwd_
     LIB.sp_debug_set(None, b"attn_bwd", 0)
 
 
+def test_attention_causal_work_order_changes_nothing():
+    """The causal kernels' chunked (sequence, head) work order (attn_chunk; taken by shape when
+    K / V outgrow L2) only reorders whole tiles: forward and backward outputs are bitwise those
+    of the plain longest-first order, including a last chunk smaller than the others."""
+    B, S, H, Hkv, hd = 5, 256, 4, 2, 128  # 20 (sequence, head) pairs: chunks of 3 leave 2
+    T, W = B * S, (H + 2 * Hkv) * hd
+    qkv = bf(torch.randn(T, W, device="cuda"))
+    dout = bf(torch.randn(T, H * hd, device="cuda"))
+    st = _stream()
+    outs = []
+    for chunk in (1 << 20, 3, 7):
+        assert LIB.sp_debug_set(None, b"attn_chunk", chunk) == 0
+        o = torch.empty(T, H * hd, device="cuda", dtype=torch.bfloat16)
+        lse = torch.empty(B * H * S, device="cuda")
+        delta = torch.empty(B * H * S, device="cuda")
+        dqkv = torch.zeros(T, W, device="cuda", dtype=torch.bfloat16)
+        assert LIB.sp_debug_attention(0, T, S, H, Hkv, hd, 1, qkv.data_ptr(), o.data_ptr(), lse.data_ptr(), None, None,
+                                      None, st) == 0
+        assert LIB.sp_debug_attention(1, T, S, H, Hkv, hd, 1, qkv.data_ptr(), o.data_ptr(), lse.data_ptr(),
+                                      dout.data_ptr(), delta.data_ptr(), dqkv.data_ptr(), st) == 0
+        torch.cuda.synchronize()
+        outs.append((o.clone(), lse.clone(), dqkv.clone()))
+    LIB.sp_debug_set(None, b"attn_chunk", 0)
+    for o, lse, dqkv in outs[1:]:
+        assert torch.equal(o, outs[0][0]) and torch.equal(lse, outs[0][1]) and torch.equal(dqkv, outs[0][2])
+
+
 def test_attention_is_deterministic():
     B, S, H, Hkv, hd = 2, 512, 4, 4, 64
     T, W = B * S, (H + 2 * Hkv) * hd
