@@ -221,6 +221,31 @@ def test_attention_forward_and_backward(B, S, H, Hkv, hd, causal, fwd_kind, bwd_
     LIB.sp_debug_set(None, b"attn_bwd", 0)
 
 
+def test_gemm_tile_order_and_store_kind_change_nothing():
+    """The CTA-pair rasterisation group (by shape: 8, or 16 for weights over 64 MB) and the
+    epilogue's store kind (TMA staging, or direct per-lane stores) reorder tiles and stores only:
+    a residual-epilogue forward and a split-K dW are bitwise the same under every setting."""
+    T, K, N = 4096, 1600, 1600
+    x = bf(torch.randn(T, K, device="cuda"))
+    w = bf(torch.randn(K, N, device="cuda") * 0.02)
+    b = torch.randn(N, device="cuda")
+    res = torch.randn(T, N, device="cuda")
+    dy = bf(torch.randn(T, N, device="cuda") * 1e-2)
+    outs = []
+    for raster, epi_mode in ((0, 0), (1, 0), (16, 0), (0, 1), (0, 2)):
+        assert LIB.sp_debug_set(None, b"raster", raster) == 0
+        assert LIB.sp_debug_set(None, b"epi_mode", epi_mode) == 0
+        y = torch.empty(T, N, device="cuda")
+        gemm(T, N, K, x, K, 0, w, N, 1, EPI_RESID_F32, y, N, bias=b, gate=res, ldg=N)
+        parts = torch.empty(3 * K * N, device="cuda")
+        gemm(K, N, T, x, K, 1, dy, N, 1, EPI_F32, parts, N, splits=3, cta=2, block_n=256)
+        outs.append((y, parts))
+    LIB.sp_debug_set(None, b"raster", 0)
+    LIB.sp_debug_set(None, b"epi_mode", 0)
+    for y, parts in outs[1:]:
+        assert torch.equal(y, outs[0][0]) and torch.equal(parts, outs[0][1])
+
+
 def test_attention_causal_work_order_changes_nothing():
     """The causal kernels' chunked (sequence, head) work order (attn_chunk; taken by shape when
     K / V outgrow L2) only reorders whole tiles: forward and backward outputs are bitwise those
